@@ -1,0 +1,335 @@
+"""Pins of the CPU oracle against what the paper and mathematics fix (no GPU).
+
+Each test names the SURVEY.md §8c pin (P1..P17) and the PAPER.md passage.
+None re-types the oracle's own formula: they check closed forms, invariants,
+brute force, or independent library routines (numpy.linalg.svd / eigvalsh).
+"""
+
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+import workloads as W
+
+GOLDEN = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+def _orth(n, rng):
+    q, r = np.linalg.qr(rng.standard_normal((n, n)))
+    return q * np.sign(np.diag(r))
+
+
+# --- P1: coefficient exactness -----------------------
+
+@pytest.mark.parametrize("K", [2, 3, 8, 20, 41])
+def test_p1_constant_and_linear(K):
+    lam = 7.25
+    c = O.chebyshev_coefficients(lambda x: 1.0, K, lam)
+    assert abs(c[0] - 2.0) < 1e-14 and max(abs(v) for v in c[1:] or [0]) < 1e-14
+    c = O.chebyshev_coefficients(lambda x: 2 * x / lam - 1.0, K, lam)
+    want = [0.0] * K
+    want[1] = 1.0
+    assert max(abs(a - b) for a, b in zip(c, want)) < 1e-14
+
+
+@pytest.mark.parametrize("K,j", [(8, 3), (8, 7), (20, 11), (30, 0)])
+def test_p1_polynomial_reproduced(K, j):
+    # h(x) = cos(j arccos(2x/lam - 1)) is psi_j of the shifted variable;
+    # discrete orthogonality over the K first-kind nodes gives c = 2 e_j (j=0) / e_j.
+    lam = 3.0
+    h = lambda x: math.cos(j * math.acos(max(-1.0, min(1.0, 2 * x / lam - 1.0))))
+    c = O.chebyshev_coefficients(h, K, lam)
+    want = [0.0] * K
+    want[j] = 2.0 if j == 0 else 1.0
+    assert max(abs(a - b) for a, b in zip(c, want)) < 1e-13
+
+
+# --- P2: interpolation at the nodes --------------------------------------------
+
+@pytest.mark.parametrize("kind", ["soft", "hard", "wsoft"])
+def test_p2_interpolates_at_nodes(kind):
+    K, lam = 17, 50.0
+    k = O.Kernel(kind, tau=3.1, w_c=9.0, w_eps=1e-6)
+    c = O.kernel_coefficients(k, K, lam, 1.0)
+    for l in range(1, K + 1):
+        x = lam / 2 * (math.cos(math.pi * (l - 0.5) / K) + 1)
+        assert abs(O.series_eval(c, lam, x) - O.h_response(k, x, 3.1)) < 1e-13
+
+
+# --- P3: recurrence == closed form -----------------------------------------------
+
+def test_p3_psi_recurrence_closed_form():
+    for k in range(65):
+        for th in [0.0, math.pi / 7, math.pi / 3, math.pi / 2, 2.5, math.pi, 0.123]:
+            assert abs(O.chebyshev_psi_recurrence(k, math.cos(th)) - math.cos(k * th)) < 1e-12
+            assert abs(O.chebyshev_psi(k, math.cos(th)) - math.cos(k * th)) < 1e-12
+
+
+# --- golden: kernel values (SPEC examples) ----------------------------------------
+
+def test_golden_kernel_eval():
+    for e in GOLDEN["kernel_eval"]:
+        assert O.h_response(O.Kernel(e["kind"], tau=e["tau"]), e["x"], e["tau"]) == e["h"], e["cite"]
+
+
+def test_golden_power_iteration():
+    for e in GOLDEN["power_iteration"]:
+        G = np.diag(e["diag"])
+        lam, _ = O.power_iteration(lambda v: G @ v, len(e["diag"]), 200)
+        assert abs(lam - e["lambda"]) < 1e-12, e["cite"]
+
+
+def test_golden_exact_shrink():
+    e = GOLDEN["exact_shrink"][0]
+    Y = O.exact_shrink(np.array(e["X"]), O.Kernel(e["kind"], tau=e["tau"]), e["tau"])
+    s = np.linalg.svd(Y, compute_uv=False)
+    assert np.allclose(s, e["singular_values"], atol=1e-14), e["cite"]
+    e = GOLDEN["exact_shrink"][1]
+    Y = O.exact_shrink(np.array(e["X"], float), O.Kernel(e["kind"], tau=e["tau"]), e["tau"])
+    assert np.allclose(Y, e["Y_diag"] * np.eye(4), atol=1e-15), e["cite"]
+
+
+# --- P4: diagonal X -------------------------------------------------------------------
+
+@pytest.mark.parametrize("shape", [(9, 6), (6, 9), (7, 7)])
+def test_p4_diagonal(shape):
+    m, n = shape
+    d = np.array([5.0, 3.0, 2.5, 1.0, 0.5, 0.25, 4.0][:min(m, n)])
+    X = np.zeros(shape)
+    X[np.arange(len(d)), np.arange(len(d))] = d
+    k = O.Kernel("soft", tau=1.1)
+    Y, info = O.cpa_shrink(X, k, 12, T=400, return_info=True)
+    want = np.zeros(shape)
+    for i, di in enumerate(d):
+        want[i, i] = di * O.series_eval(info["coeffs"], info["lambda_max"], di * di)
+    assert np.abs(Y - want).max() <= 1e-13 * np.abs(want).max()
+    off = Y.copy()
+    off[np.arange(len(d)), np.arange(len(d))] = 0
+    assert np.abs(off).max() == 0.0
+
+
+# --- P5: node-exact shrinkage vs the TRUE g ----------------------------------------------
+
+@pytest.mark.parametrize("kind", ["soft", "hard", "wsoft"])
+def test_p5_node_exact(kind):
+    rng = np.random.default_rng(5)
+    K, lam, m, n = 10, 100.0, 14, 10
+    nodes = [lam / 2 * (math.cos(math.pi * (l - 0.5) / K) + 1) for l in range(1, K + 1)]
+    d = np.sqrt(np.array(nodes))
+    U, V = _orth(m, rng)[:, :n], _orth(n, rng)
+    X = (U * d) @ V.T
+    k = O.Kernel(kind, tau=4.0, w_c=20.0, w_eps=1e-6)
+    Y = O.cpa_shrink(X, k, K, lam=lam)
+    want = (U * np.array([O.g_response(k, di, 4.0) for di in d])) @ V.T
+    assert O.rel_fro(Y, want) < 1e-12
+
+
+# --- P6: orthogonal X ---------------------------------------------------------------------
+
+def test_p6_orthogonal():
+    rng = np.random.default_rng(6)
+    a = 3.0
+    Q = _orth(12, rng)
+    Y, info = O.cpa_shrink(a * Q, O.Kernel("soft", tau=1.0), 15, T=30, return_info=True)
+    assert abs(info["lambda_hat"] - a * a) < 1e-13 * a * a
+    f = a * O.series_eval(info["coeffs"], info["lambda_max"], a * a)
+    assert O.rel_fro(Y, f * Q) < 1e-13
+
+
+# --- P7: rank one ---------------------------------------------------------------------------
+
+def test_p7_rank_one():
+    rng = np.random.default_rng(7)
+    u = rng.standard_normal(20); u /= np.linalg.norm(u)
+    v = rng.standard_normal(13); v /= np.linalg.norm(v)
+    sig = 6.5
+    X = sig * np.outer(u, v)
+    Y, info = O.cpa_shrink(X, O.Kernel("soft", tau=2.0), 20, T=50, return_info=True)
+    assert abs(info["lambda_hat"] - sig ** 2) < 1e-12 * sig ** 2
+    f = sig * O.series_eval(info["coeffs"], info["lambda_max"], sig ** 2)
+    assert O.rel_fro(Y, f * np.outer(u, v)) < 1e-13
+
+
+# --- P8: raw coefficients ----------------------------------------------------------------------
+
+@pytest.mark.parametrize("shape", [(11, 7), (7, 11)])
+def test_p8_raw_coefficients(shape):
+    rng = np.random.default_rng(8)
+    X = rng.standard_normal(shape)
+    lam = 2.0 * np.linalg.norm(X, 2) ** 2
+    assert O.rel_fro(O.cpa_shrink(X, None, 4, lam=lam, coeffs=[2.0, 0, 0, 0]), X) < 1e-15
+    G_side = X @ X.T @ X  # (XX^T)X == X(X^T X)
+    assert O.rel_fro(O.cpa_shrink(X, None, 4, lam=lam, coeffs=[lam, lam / 2, 0, 0]), G_side) < 1e-13
+    # e_k -> Psi_k(B_hat) applied to X, compared with a plain GEMM chain of the closed form
+    m, n = shape
+    left = m <= n
+    G = X @ X.T if left else X.T @ X
+    s = G.shape[0]
+    Bh = 2.0 / lam * G - np.eye(s)
+    # Psi_k via the eigen-decomposition closed form: P diag(cos k theta_i) P^T
+    ev, P = np.linalg.eigh(Bh)
+    for kk in [2, 3, 5]:
+        c = [0.0] * 6
+        c[kk] = 1.0
+        Psi = (P * np.cos(kk * np.arccos(np.clip(ev, -1, 1)))) @ P.T
+        want = Psi @ X if left else X @ Psi
+        assert O.rel_fro(O.cpa_shrink(X, None, 6, lam=lam, coeffs=c), want) < 1e-12
+
+
+# --- P9: SVD characterization (+ Jacobi pinned to numpy SVD, P16) ------------------------
+
+@pytest.mark.parametrize("shape,kind", [((64, 48), "soft"), ((30, 40), "hard"), ((25, 25), "wsoft")])
+def test_p9_svd_characterization(shape, kind):
+    X = W.random_dense(*shape, seed=9)
+    k = O.Kernel(kind, tau=3.0, w_c=15.0, w_eps=1e-6)
+    Y, info = O.cpa_shrink(X, k, 20, T=60, return_info=True)
+    Z = O.svd_characterization(X, info["coeffs"], info["lambda_max"])
+    assert O.rel_fro(Y, Z) < 1e-12
+
+
+def test_p16_jacobi_svd():
+    for shape in [(64, 48), (48, 64), (10, 10), (1, 5), (5, 1)]:
+        X = W.random_dense(*shape, seed=16)
+        U, s, V = O.jacobi_svd(X)
+        assert np.linalg.norm(X - (U * s) @ V.T) <= 1e-13 * np.linalg.norm(X)
+        assert np.abs(U.T @ U - np.eye(len(s))).max() < 1e-13
+        assert np.abs(V.T @ V - np.eye(len(s))).max() < 1e-13
+        assert np.allclose(s, np.linalg.svd(X, compute_uv=False), rtol=1e-13, atol=1e-13)
+    # diagonal / rank-1 exact
+    U, s, V = O.jacobi_svd(np.diag([1.0, 4.0, 2.0]))
+    assert list(s) == [4.0, 2.0, 1.0]
+
+
+# --- P10: error vs exact shrinkage decreases with K on config 1 -----------------------------
+
+def test_p10_c1_vs_exact_decreasing():
+    X = W.gen_c1()
+    cfg = W.CONFIGS["c1"]
+    k = O.Kernel(**cfg["kernel"])
+    exact = O.exact_shrink(X, k, 2.0)
+    errs = [O.rel_fro(O.cpa_shrink(X, k, K, T=30), exact) for K in (5, 10, 20, 40)]
+    assert all(a > b for a, b in zip(errs, errs[1:])), errs
+    assert errs[2] <= 2e-2
+
+
+# --- P11: hard with tau = 0 returns X ------------------------------------------------------------
+
+def test_p11_hard_zero_tau_identity():
+    X = W.random_dense(15, 9, seed=11)
+    Y, info = O.cpa_shrink(X, O.Kernel("hard", tau=0.0), 25, T=30, return_info=True)
+    assert info["coeffs"][0] == 2.0 and all(abs(v) < 1e-14 for v in info["coeffs"][1:])
+    assert O.rel_fro(Y, X) < 1e-14
+
+
+# --- P12: singular vectors preserved (YX^T, X^T Y symmetric) -----------------------------------
+
+def test_p12_symmetry():
+    X = W.gen_c1()
+    Y = O.cpa_shrink(X, O.Kernel("soft", tau=2.0), 20, T=30)
+    for M in (Y @ X.T, X.T @ Y):
+        assert np.linalg.norm(M - M.T) <= 1e-12 * np.linalg.norm(M)
+
+
+# --- P13: transpose covariance ---------------------------------------------------------------------
+
+def test_p13_transpose():
+    X = W.random_dense(13, 21, seed=13)
+    k = O.Kernel("soft", tau=1.5)
+    lam = 1.01 * np.linalg.norm(X, 2) ** 2
+    assert O.rel_fro(O.cpa_shrink(X.T, k, 18, lam=lam), O.cpa_shrink(X, k, 18, lam=lam).T) < 1e-13
+
+
+# --- P14: power-of-two scaling is bitwise --------------------------------------------------------------
+
+def test_p14_pow2_bitwise():
+    X = W.random_dense(20, 12, seed=14)
+    a = O.cpa_shrink(X, O.Kernel("soft", tau=1.0), 15, T=30)
+    b = O.cpa_shrink(2 * X, O.Kernel("soft", tau=2.0), 15, T=30)
+    assert np.array_equal(2 * a, b)
+
+
+# --- P15: power iteration ---------------------------------------------------------------------------
+
+def test_p15_power_iteration():
+    rng = np.random.default_rng(15)
+    A = rng.standard_normal((40, 25))
+    G = A.T @ A
+    lam, hist = O.power_iteration(lambda v: G @ v, 25, 2000)
+    assert abs(lam - np.linalg.eigvalsh(G)[-1]) < 1e-12 * lam
+    assert all(b >= a * (1 - 1e-15) for a, b in zip(hist, hist[1:]))  # non-decreasing
+    assert O.power_iteration(lambda v: 0 * v, 5, 10)[0] == 0.0
+
+
+# --- P17: the paper's block-diagonal D, closed form ------------------------------------------------------
+
+@pytest.mark.parametrize("N,nb,copies", [(1000, 10, 1), (200, 4, 1), (120, 6, 4)])
+def test_p17_block_diagonal(N, nb, copies):
+    D = W.block_diag_D(N, nb, copies)
+    p = N // nb
+    s1, s2 = math.sqrt(copies) * (N - p / 2), math.sqrt(copies) * (p / 2)
+    sv = np.linalg.svd(D, compute_uv=False)
+    assert abs(sv[0] - s1) < 1e-9 * s1 and np.allclose(sv[1:nb], s2, rtol=1e-9) and sv[nb] < 1e-9 * s1
+    k = O.Kernel("soft", tau=0.3, tau_relative=True)
+    Y, info = O.cpa_shrink(D, k, 16, T=30, return_info=True)
+    assert abs(info["lambda_hat"] - s1 ** 2) < 1e-12 * s1 ** 2  # exact after one step from 1/sqrt(s)
+    lam, c = info["lambda_max"], info["coeffs"]
+    q = np.ones(N) / math.sqrt(N)
+    Pb = np.zeros((N, N))
+    for b in range(nb):
+        Pb[b * p:(b + 1) * p, b * p:(b + 1) * p] = 1.0 / p
+    f1 = s1 * O.series_eval(c, lam, s1 ** 2)
+    f2 = s2 * O.series_eval(c, lam, s2 ** 2)
+    # D = sqrt(copies) [ (N - p/2) q q^T - (p/2)(P_b - q q^T) ] R with R the row-orthonormal copy map
+    R = np.concatenate([np.eye(N)] * copies, axis=1) / math.sqrt(copies)
+    want = (f1 * np.outer(q, q) - f2 * (Pb - np.outer(q, q))) @ R
+    assert O.rel_fro(Y, want) < 1e-12
+    for e in GOLDEN["block_diag_D"]:
+        sv = np.linalg.svd(W.block_diag_D(e["N"], e["nblocks"]), compute_uv=False)
+        assert abs(sv[0] - e["sigma"][0]) < 1e-9 and np.allclose(sv[1:e["rank"]], e["sigma"][1]), e["cite"]
+
+
+# --- vector / sparse forms agree with Alg. 1 ---------------------------------------------------------------
+
+def test_vector_forms_match_alg1():
+    import scipy.sparse as sp
+    k = O.Kernel("hard", tau=0.5, tau_relative=True)
+    Xw = W.random_dense(12, 30, seed=21)
+    Y = O.cpa_shrink(Xw, k, 14, T=100)
+    Yc, _ = O.cpa_shrink_columns(Xw, [0, 7, 29], k, 14, T=100)
+    assert O.rel_fro(Yc, Y[:, [0, 7, 29]]) < 1e-12
+    Xt = Xw.T.copy()
+    Yr, _ = O.cpa_shrink_rows(Xt, [3, 4], k, 14, T=100)
+    assert O.rel_fro(Yr, Y.T[[3, 4], :]) < 1e-12
+    # sparse: lambda from the m-side (XX^T) power iteration; use a given lambda to compare forms
+    row_ptr, col, val = W.gen_c4(m=40, n=400, nnz=800)
+    Xs = sp.csr_matrix((val, col, row_ptr), shape=(40, 400))
+    lam = 1.01 * np.linalg.norm(Xs.toarray(), 2) ** 2
+    Yd = O.cpa_shrink(Xs.toarray(), k, 14, lam=lam)
+    Ys, _ = O.cpa_shrink_sparse_rows(Xs, [0, 5, 39], k, 14, lam=lam)
+    assert O.rel_fro(Ys, Yd[[0, 5, 39], :]) < 1e-12
+    # sparse power iteration on the m-side equals the dense one on the same side
+    l1, _ = O.sparse_power_iteration(Xs, 50)
+    Xd = Xs.toarray()
+    l2, _ = O.power_iteration(lambda v: Xd @ (Xd.T @ v), 40, 50)
+    assert abs(l1 - l2) < 1e-12 * l2
+
+
+def test_degenerate_zero():
+    Y, info = O.cpa_shrink(np.zeros((5, 3)), O.Kernel("soft", tau=1.0), 10, return_info=True)
+    assert info["degenerate"] and not Y.any()
+
+
+def test_generators_deterministic():
+    assert np.array_equal(W.gen_c1(), W.gen_c1())
+    X = W.gen_c1()
+    assert X.shape == (64, 48)
+    s = np.linalg.svd(X, compute_uv=False)
+    assert s[4] > 10 and s[5] < 2  # rank-5 signal over 0.1 noise
+    r, c, v = W.gen_c4(m=50, n=500, nnz=250)
+    assert r[-1] == 250 and len(set(zip(np.repeat(np.arange(50), np.diff(r)), c))) == 250
+    Xb = W.gen_c3(batch=4)
+    assert Xb.dtype == np.float32 and Xb.shape == (4, 64, 64)
