@@ -1,0 +1,196 @@
+/*
+ * cpa_svt.h -- C ABI of the B200-native CPA singular-value shrinkage library.
+ *
+ * Operation (Algorithm 1 with T = I and epsilon = 0; the
+ * apply-to-X form of PAPER.md:278-307 eq. sing_shrink_from_eig_shrink):
+ *
+ *     Y = G_hat(X) = X H_hat(X^T X)        if m >  n   ("right", Gram n x n)
+ *     Y = G_hat(X) = H_hat(X X^T) X        if m <= n   ("left",  Gram m x m)
+ *
+ * with H_hat(Phi) = c_0/2 Id + sum_{k=1}^{K-1} c_k Psi_k(B_hat),
+ * B_hat = (2/Lambda_max) Phi - Id, the three-term recurrence
+ * Psi_k = 2 B_hat Psi_{k-1} - Psi_{k-2}, and the K
+ * Chebyshev-Gauss coefficients of PAPER.md:233 / 363 for the response h of
+ * PAPER.md:496-519 (hard / soft / weighted soft).  The library never forms
+ * H_hat: it runs the recurrence on W_k = Psi_k(B_hat) X (or X Psi_k(B_hat)),
+ *     W_0 = X,  W_1 = (2/L) G X - X,  W_k = (4/L) G W_{k-1} - 2 W_{k-1} - W_{k-2},
+ *     Y = c_0/2 W_0 + c_1 W_1 + sum_{k>=2} c_k W_k,
+ * each step one fused kernel (GEMM + update + accumulation).
+ *
+ * Conventions (all entry points):
+ *   - Every call returns cpa_svt_status; CPA_SVT_OK == 0.  Arguments are
+ *     validated before any device work; on a non-OK status no output buffer
+ *     has been written unless the status is CPA_SVT_E_CUDA / E_NCCL.
+ *   - Matrices are ROW-MAJOR with a leading dimension in ELEMENTS (ld >= cols).
+ *   - X, Y, CSR arrays and lambda_out are DEVICE pointers on the handle's
+ *     device, owned by the caller, valid until the handle's stream has
+ *     executed the call.  Kernel specs, coefficient arrays, lambda and info
+ *     structs are HOST pointers read (or written) before the call returns.
+ *   - All device work is ordered on the handle's stream and is asynchronous,
+ *     EXCEPT when `info` is non-NULL or `lam` asks for lambda back
+ *     (lam->want_lambda): then the call synchronises the stream before
+ *     returning.  cpa_svt_apply_host is always synchronous.
+ *   - Y must not alias X.  Y may be any caller buffer of the same shape.
+ *   - The handle owns its workspace (Gram, two recurrence buffers, power
+ *     iteration scratch, series parameters), grows it lazily and frees it in
+ *     cpa_svt_free.  A handle is not thread-safe; use one per host thread.
+ *   - Results are deterministic run to run for a fixed shape and world size
+ *     (fixed reduction orders, no floating-point atomics on the dense path).
+ */
+#ifndef CPA_SVT_H
+#define CPA_SVT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CPA_SVT_VERSION_MAJOR 0
+#define CPA_SVT_VERSION_MINOR 1
+/* Largest order K supported (number of coefficients c_0..c_{K-1}). */
+#define CPA_SVT_KMAX 512
+
+typedef struct cpa_svt_handle cpa_svt_handle; /* opaque */
+
+typedef enum {
+  CPA_SVT_OK = 0,
+  CPA_SVT_E_ARG = 1,          /* NULL pointer, K < 2 or K > KMAX, dims < 0, ld < cols, Y aliases X, bad enum */
+  CPA_SVT_E_DOMAIN = 2,       /* lambda_max override < 0 or non-finite, tau < 0, weight parameters invalid */
+  CPA_SVT_E_DIVERGED = 3,     /* reserved: ||Y||_F > 1e3 sum|c_k| ||X||_F */
+  CPA_SVT_E_CUDA = 4,         /* a CUDA runtime call failed (cpa_svt_last_error has the text) */
+  CPA_SVT_E_NCCL = 5,         /* an NCCL call failed or NCCL could not be loaded */
+  CPA_SVT_E_NOMEM = 6,        /* workspace allocation failed */
+  CPA_SVT_E_UNSUPPORTED = 7   /* valid request this build does not implement */
+} cpa_svt_status;
+
+/* Response family h(x; w(x)/rho, tau) of PAPER.md:496-519. */
+typedef enum {
+  CPA_SVT_HARD = 0,  /* h(x; 0, tau):          h = 1            if sqrt(x) > tau, else 0 */
+  CPA_SVT_SOFT = 1,  /* h(x; 1/rho, 1/rho):    h = 1 - tau/sqrt(x) if sqrt(x) > tau, else 0 */
+  CPA_SVT_WSOFT = 2  /* h(x; w(x)/rho, w/rho): h = 1 - w/sqrt(x)   if sqrt(x) > w,   else 0,
+                        w(x) = w_c / (sqrt(max(x - w_shift, 0)) + w_eps)  (reading R10) */
+} cpa_svt_kind;
+
+typedef struct {
+  int32_t kind;          /* cpa_svt_kind */
+  int32_t tau_relative;  /* HARD/SOFT: if nonzero, the threshold is tau * sigma_max_hat, with
+                            sigma_max_hat = sqrt(lambda_hat) (power-iteration estimate, reading R7) */
+  double tau;            /* HARD/SOFT threshold on singular values, >= 0 */
+  double w_c, w_shift, w_eps; /* WSOFT weight parameters, w_c >= 0, w_shift >= 0, w_eps > 0 */
+} cpa_svt_kernel;
+
+typedef enum { CPA_SVT_F64 = 0, CPA_SVT_F32 = 1 } cpa_svt_dtype;
+
+typedef enum {
+  CPA_SVT_MATH_NATIVE = 0, /* f64: DMMA (mma.sync f64) tensor tiles; f32: FFMA */
+  CPA_SVT_MATH_TF32 = 1,   /* f32 data, tcgen05 kind::tf32 with operands rounded to nearest TF32 */
+  CPA_SVT_MATH_3XTF32 = 2  /* f32 data, tcgen05 kind::tf32 hi/lo split (near-fp32 accuracy) */
+} cpa_svt_math;
+
+/* Lambda_max of the Gram (Alg. 1 line 3): power iteration
+ * v_0 = 1/sqrt(s), v_t = G v_{t-1}/||G v_{t-1}||, lambda_hat = ||G v_{T-1}||_2
+ * after T = power_iters products; Lambda_max = safety * lambda_hat (reading R6).
+ * If lambda_max > 0 on input the power iteration is skipped and that value is
+ * used; then lambda_hat := lambda_max / safety.  On return (only if
+ * want_lambda != 0) lambda_hat / lambda_max hold the values used. */
+typedef struct {
+  int32_t power_iters;   /* T >= 1 (ignored when lambda_max > 0 on input) */
+  int32_t want_lambda;   /* nonzero: synchronise and write back lambda_hat / lambda_max */
+  double safety;         /* >= 1; 1.01 in every BASELINE config */
+  double lambda_max;     /* in: > 0 to override; out: value used */
+  double lambda_hat;     /* out */
+} cpa_svt_lambda;
+
+/* Diagnostics (host).  Filled only when passed non-NULL; forces a sync. */
+typedef struct {
+  double lambda_hat, lambda_max, sigma_max_hat, tau_used;
+  int32_t side;          /* 0 = left (G = X X^T), 1 = right (G = X^T X) */
+  int32_t degenerate;    /* 1 if lambda_hat <= 1e-300: Y = 0 */
+  float ms_gram, ms_allreduce, ms_power, ms_recurrence, ms_total;
+  int32_t kernel_launches;  /* device kernels this call launched */
+  int32_t pad;
+} cpa_svt_info;
+
+/* Multi-GPU sharding of the long dimension for cpa_svt_apply (world > 1). */
+typedef enum {
+  CPA_SVT_SHARD_NONE = 0,  /* X is the whole matrix on every rank (replicas) */
+  CPA_SVT_SHARD_COLS = 1,  /* left-apply (global m <= n): X is m x n_local, a column block */
+  CPA_SVT_SHARD_ROWS = 2   /* right-apply (global m > n): X is m_local x n, a row block */
+} cpa_svt_shard;
+
+/* Create a handle bound to `device` and the CUDA stream `cuda_stream`
+ * (a cudaStream_t; NULL = legacy default stream).  For world > 1,
+ * nccl_unique_id points to the 128-byte ncclUniqueId created by
+ * cpa_svt_nccl_unique_id on rank 0 and broadcast by the caller; the library
+ * creates its own NCCL communicator (NCCL is loaded at run time). */
+cpa_svt_status cpa_svt_init(cpa_svt_handle** h, int device, void* cuda_stream,
+                            const void* nccl_unique_id, int rank, int world);
+cpa_svt_status cpa_svt_free(cpa_svt_handle* h);
+
+/* Writes a fresh 128-byte ncclUniqueId into out128 (call on rank 0 only). */
+cpa_svt_status cpa_svt_nccl_unique_id(void* out128);
+
+/* Pure host function, fp64: c_out[k] = (2/K) sum_{l=1}^{K} cos(k theta_l)
+ * h((lambda_max/2)(cos theta_l + 1)), theta_l = pi (l - 1/2)/K, k = 0..K-1
+ * (PAPER.md:233 eq. chebychev_coeff_shifted).  sigma_max_hat resolves a
+ * relative tau.  c_out: host array of K doubles, caller-owned. */
+cpa_svt_status cpa_svt_coeffs(const cpa_svt_kernel* k, int K, double lambda_max,
+                              double sigma_max_hat, double* c_out);
+
+/* Dense shrinkage of one matrix.  m, n: LOCAL shape of X (the shard when
+ * world > 1).  long_global: global extent of the sharded dimension (ignored
+ * for SHARD_NONE).  c: optional host array of K raw coefficients that
+ * replaces line 4 (NULL = computed on the device from `k` and Lambda_max).
+ * lam: required.  info: optional.  dtype/math: F64+NATIVE (DMMA), F32 with
+ * TF32 / 3XTF32 / NATIVE.  X and Y are dtype arrays.  With world > 1 the
+ * partial Grams are summed with one NCCL all-reduce (PAPER.md:278-307:
+ * G = sum over column blocks of X_p X_p^T) and every rank then runs the
+ * recurrence on its own block; Lambda_max is broadcast from rank 0. */
+cpa_svt_status cpa_svt_apply(cpa_svt_handle* h, cpa_svt_dtype dtype, cpa_svt_math math,
+                             int64_t m, int64_t n, cpa_svt_shard shard, int64_t long_global,
+                             const void* X, int64_t ldx, void* Y, int64_t ldy,
+                             const cpa_svt_kernel* k, int K, const double* c,
+                             cpa_svt_lambda* lam, cpa_svt_info* info);
+
+/* Same as cpa_svt_apply (world 1, SHARD_NONE) but X and Y are HOST arrays
+ * (row-major, ld = n).  Copies X to handle-owned device memory, runs the
+ * path, copies Y back, and synchronises.  Pinned host buffers give full
+ * PCIe bandwidth; pageable ones work. */
+cpa_svt_status cpa_svt_apply_host(cpa_svt_handle* h, cpa_svt_dtype dtype, cpa_svt_math math,
+                                  int64_t m, int64_t n, const void* X_host, void* Y_host,
+                                  const cpa_svt_kernel* k, int K, cpa_svt_lambda* lam,
+                                  cpa_svt_info* info);
+
+/* Sparse X (m x n, CSR, fp64): Y = X H_hat(X^T X), the n x n Gram never
+ * formed.  Each step runs Z = W_{k-1} X^T (m x m block rows) then
+ * W_k = (4/L) Z X - 2 W_{k-1} - W_{k-2} fused with Y += c_k W_k.  X is
+ * replicated on every rank (row_ptr int64[m+1], col int32[nnz] sorted per
+ * row, val fp64[nnz], all device); this rank computes rows
+ * [row_begin, row_end) of Y into Y (dense, (row_end-row_begin) x n, ld ldy).
+ * Lambda_max: power iteration on X X^T (m-side), v -> X (X^T v) (reading R4). */
+cpa_svt_status cpa_svt_apply_csr(cpa_svt_handle* h, int64_t m, int64_t n, int64_t nnz,
+                                 const int64_t* row_ptr, const int32_t* col, const double* val,
+                                 int64_t row_begin, int64_t row_end, double* Y, int64_t ldy,
+                                 const cpa_svt_kernel* k, int K, cpa_svt_lambda* lam,
+                                 cpa_svt_info* info);
+
+/* Batched fp32 shrinkage of `batch` independent m x n matrices stored
+ * contiguously ([batch][m][n], row-major): Gram, power iteration, coefficients
+ * and the recurrence per matrix inside one kernel (no host round trip).
+ * lambda_out: optional device array of `batch` floats receiving Lambda_max.
+ * Requires m, n <= 64. */
+cpa_svt_status cpa_svt_apply_batched(cpa_svt_handle* h, int64_t batch, int m, int n,
+                                     const float* X, float* Y, const cpa_svt_kernel* k, int K,
+                                     const cpa_svt_lambda* lam, float* lambda_out);
+
+const char* cpa_svt_status_string(cpa_svt_status s);
+/* Text of the last error recorded on this handle ("" if none). */
+const char* cpa_svt_last_error(const cpa_svt_handle* h);
+/* Number of device kernels launched through this handle since init. */
+int64_t cpa_svt_launch_count(const cpa_svt_handle* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CPA_SVT_H */

@@ -1,0 +1,221 @@
+"""B200-native CPA singular-value shrinkage (arXiv 1705.07112) -- Python binding.
+
+A thin ctypes layer over ``libcpasvt.so`` (C ABI declared in
+``include/cpa_svt.h``).  It only marshals arguments: every step of the method
+runs in the library's sm_100a kernels.  PyTorch is used for device memory and
+streams.  There is no CPU fallback: if the library is missing, importing this
+package raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+__all__ = ["Kernel", "Lambda", "Info", "Handle", "coeffs", "CpaSvtError", "kernel_from_dict",
+           "LIB_PATH", "STATUS", "HARD", "SOFT", "WSOFT", "lib"]
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libcpasvt.so")
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python paper_1705_07112_b200/build.py` "
+                      "(there is no CPU fallback)")
+lib = ctypes.CDLL(LIB_PATH)
+
+HARD, SOFT, WSOFT = 0, 1, 2
+F64, F32 = 0, 1
+MATH = {"native": 0, "tf32": 1, "3xtf32": 2}
+SHARD = {"none": 0, "cols": 1, "rows": 2}
+STATUS = {0: "ok", 1: "E_ARG", 2: "E_DOMAIN", 3: "E_DIVERGED", 4: "E_CUDA", 5: "E_NCCL", 6: "E_NOMEM",
+          7: "E_UNSUPPORTED"}
+
+
+class Kernel(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("tau_relative", ctypes.c_int32), ("tau", ctypes.c_double),
+                ("w_c", ctypes.c_double), ("w_shift", ctypes.c_double), ("w_eps", ctypes.c_double)]
+
+
+class Lambda(ctypes.Structure):
+    _fields_ = [("power_iters", ctypes.c_int32), ("want_lambda", ctypes.c_int32), ("safety", ctypes.c_double),
+                ("lambda_max", ctypes.c_double), ("lambda_hat", ctypes.c_double)]
+
+
+class Info(ctypes.Structure):
+    _fields_ = [("lambda_hat", ctypes.c_double), ("lambda_max", ctypes.c_double),
+                ("sigma_max_hat", ctypes.c_double), ("tau_used", ctypes.c_double),
+                ("side", ctypes.c_int32), ("degenerate", ctypes.c_int32),
+                ("ms_gram", ctypes.c_float), ("ms_allreduce", ctypes.c_float), ("ms_power", ctypes.c_float),
+                ("ms_recurrence", ctypes.c_float), ("ms_total", ctypes.c_float),
+                ("kernel_launches", ctypes.c_int32), ("pad", ctypes.c_int32)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_ if f != "pad"}
+
+
+_p = ctypes.c_void_p
+_i64 = ctypes.c_int64
+lib.cpa_svt_init.argtypes = [ctypes.POINTER(_p), ctypes.c_int, _p, _p, ctypes.c_int, ctypes.c_int]
+lib.cpa_svt_free.argtypes = [_p]
+lib.cpa_svt_nccl_unique_id.argtypes = [_p]
+lib.cpa_svt_coeffs.argtypes = [ctypes.POINTER(Kernel), ctypes.c_int, ctypes.c_double, ctypes.c_double,
+                               ctypes.POINTER(ctypes.c_double)]
+lib.cpa_svt_apply.argtypes = [_p, ctypes.c_int, ctypes.c_int, _i64, _i64, ctypes.c_int, _i64, _p, _i64, _p, _i64,
+                              ctypes.POINTER(Kernel), ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                              ctypes.POINTER(Lambda), ctypes.POINTER(Info)]
+lib.cpa_svt_apply_host.argtypes = [_p, ctypes.c_int, ctypes.c_int, _i64, _i64, _p, _p, ctypes.POINTER(Kernel),
+                                   ctypes.c_int, ctypes.POINTER(Lambda), ctypes.POINTER(Info)]
+lib.cpa_svt_apply_csr.argtypes = [_p, _i64, _i64, _i64, _p, _p, _p, _i64, _i64, _p, _i64, ctypes.POINTER(Kernel),
+                                  ctypes.c_int, ctypes.POINTER(Lambda), ctypes.POINTER(Info)]
+lib.cpa_svt_apply_batched.argtypes = [_p, _i64, ctypes.c_int, ctypes.c_int, _p, _p, ctypes.POINTER(Kernel),
+                                      ctypes.c_int, ctypes.POINTER(Lambda), _p]
+lib.cpa_svt_status_string.restype = ctypes.c_char_p
+lib.cpa_svt_status_string.argtypes = [ctypes.c_int]
+lib.cpa_svt_last_error.restype = ctypes.c_char_p
+lib.cpa_svt_last_error.argtypes = [_p]
+lib.cpa_svt_launch_count.restype = ctypes.c_int64
+lib.cpa_svt_launch_count.argtypes = [_p]
+for _f in ("cpa_svt_init", "cpa_svt_free", "cpa_svt_nccl_unique_id", "cpa_svt_coeffs", "cpa_svt_apply",
+           "cpa_svt_apply_host", "cpa_svt_apply_csr", "cpa_svt_apply_batched"):
+    getattr(lib, _f).restype = ctypes.c_int
+
+
+class CpaSvtError(RuntimeError):
+    def __init__(self, status, detail=""):
+        self.status = status
+        super().__init__(f"cpa_svt status {status} ({STATUS.get(status, '?')}): {detail}")
+
+
+def kernel_from_dict(d) -> Kernel:
+    """{'kind': 'hard'|'soft'|'wsoft', 'tau', 'tau_relative', 'w_c', 'w_shift', 'w_eps'} -> Kernel."""
+    if isinstance(d, Kernel):
+        return d
+    kind = {"hard": HARD, "soft": SOFT, "wsoft": WSOFT}[d["kind"]]
+    return Kernel(kind, int(bool(d.get("tau_relative", False))), float(d.get("tau", 0.0)),
+                  float(d.get("w_c", 0.0)), float(d.get("w_shift", 0.0)), float(d.get("w_eps", 0.0)))
+
+
+def coeffs(kernel, K: int, lambda_max: float, sigma_max_hat: float = 0.0):
+    """cpa_svt_coeffs: the K Chebyshev-Gauss coefficients (host, fp64)."""
+    out = (ctypes.c_double * K)()
+    st = lib.cpa_svt_coeffs(ctypes.byref(kernel_from_dict(kernel)), K, lambda_max, sigma_max_hat, out)
+    if st:
+        raise CpaSvtError(st)
+    return list(out)
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    st = lib.cpa_svt_nccl_unique_id(buf)
+    if st:
+        raise CpaSvtError(st, "ncclGetUniqueId")
+    return buf.raw
+
+
+class Handle:
+    """cpa_svt_init / cpa_svt_free around a device and a CUDA stream."""
+
+    def __init__(self, device: int | None = None, stream=None, nccl_id: bytes | None = None,
+                 rank: int = 0, world: int = 1):
+        import torch
+        self._torch = torch
+        self.device = torch.cuda.current_device() if device is None else device
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        self.stream = stream
+        h = _p()
+        idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id else None
+        st = lib.cpa_svt_init(ctypes.byref(h), self.device, _p(stream.cuda_stream), idbuf, rank, world)
+        if st:
+            raise CpaSvtError(st, "cpa_svt_init")
+        self._h = h
+        self.rank, self.world = rank, world
+
+    def _check(self, st, what):
+        if st:
+            raise CpaSvtError(st, f"{what}: {lib.cpa_svt_last_error(self._h).decode()}")
+
+    @property
+    def launches(self) -> int:
+        return lib.cpa_svt_launch_count(self._h)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.cpa_svt_free(self._h)
+            self._h = None
+
+    __del__ = close
+
+    @staticmethod
+    def _lambda(T, safety, lambda_max, want):
+        return Lambda(int(T), int(bool(want)), float(safety), float(lambda_max or 0.0), 0.0)
+
+    def apply(self, X, kernel, K: int, T: int = 30, safety: float = 1.01, lambda_max: float = 0.0,
+              coeffs=None, Y=None, math: str = "native", shard: str = "none", long_global: int = 0,
+              info: bool = False, want_lambda: bool = False):
+        """cpa_svt_apply on a 2-D CUDA tensor (float64: DMMA path; float32: TF32 paths)."""
+        torch = self._torch
+        assert X.is_cuda and X.dim() == 2 and X.stride(1) == 1
+        if Y is None:
+            Y = torch.empty(X.shape, dtype=X.dtype, device=X.device)
+        assert Y.shape == X.shape and Y.dtype == X.dtype and Y.stride(1) == 1
+        dt = F64 if X.dtype == torch.float64 else F32
+        lam = self._lambda(T, safety, lambda_max, want_lambda)
+        inf = Info() if info else None
+        cbuf = (ctypes.c_double * len(coeffs))(*coeffs) if coeffs is not None else None
+        K = len(coeffs) if coeffs is not None else K
+        st = lib.cpa_svt_apply(self._h, dt, MATH[math], X.shape[0], X.shape[1], SHARD[shard], long_global,
+                               X.data_ptr(), X.stride(0), Y.data_ptr(), Y.stride(0),
+                               ctypes.byref(kernel_from_dict(kernel if kernel is not None else {"kind": "soft"})),
+                               K, cbuf, ctypes.byref(lam), ctypes.byref(inf) if inf is not None else None)
+        self._check(st, "cpa_svt_apply")
+        if info or want_lambda:
+            return Y, (inf.as_dict() if inf is not None else {"lambda_hat": lam.lambda_hat,
+                                                                 "lambda_max": lam.lambda_max})
+        return Y
+
+    def apply_host(self, X, Y, kernel, K: int, T: int = 30, safety: float = 1.01, lambda_max: float = 0.0,
+                   math: str = "native", info: bool = False):
+        """cpa_svt_apply_host: X, Y are contiguous CPU tensors (pinned for full bandwidth)."""
+        torch = self._torch
+        assert not X.is_cuda and X.is_contiguous() and Y.is_contiguous() and X.shape == Y.shape
+        dt = F64 if X.dtype == torch.float64 else F32
+        lam = self._lambda(T, safety, lambda_max, False)
+        inf = Info() if info else None
+        st = lib.cpa_svt_apply_host(self._h, dt, MATH[math], X.shape[0], X.shape[1], X.data_ptr(), Y.data_ptr(),
+                                    ctypes.byref(kernel_from_dict(kernel)), K, ctypes.byref(lam),
+                                    ctypes.byref(inf) if inf is not None else None)
+        self._check(st, "cpa_svt_apply_host")
+        return inf.as_dict() if inf is not None else None
+
+    def apply_batched(self, X, kernel, K: int, T: int = 30, safety: float = 1.01, lambda_max: float = 0.0,
+                      Y=None, lambda_out=None):
+        """cpa_svt_apply_batched on a [batch, m, n] float32 CUDA tensor."""
+        torch = self._torch
+        assert X.is_cuda and X.dim() == 3 and X.dtype == torch.float32 and X.is_contiguous()
+        if Y is None:
+            Y = torch.empty_like(X)
+        lam = self._lambda(T, safety, lambda_max, False)
+        st = lib.cpa_svt_apply_batched(self._h, X.shape[0], X.shape[1], X.shape[2], X.data_ptr(), Y.data_ptr(),
+                                       ctypes.byref(kernel_from_dict(kernel)), K, ctypes.byref(lam),
+                                       lambda_out.data_ptr() if lambda_out is not None else None)
+        self._check(st, "cpa_svt_apply_batched")
+        return Y
+
+    def apply_csr(self, row_ptr, col, val, m: int, n: int, kernel, K: int, T: int = 300, safety: float = 1.01,
+                  lambda_max: float = 0.0, row_begin: int = 0, row_end: int | None = None, Y=None,
+                  info: bool = False, want_lambda: bool = False):
+        """cpa_svt_apply_csr: CSR X (int64 row_ptr, int32 col, float64 val, all CUDA); returns dense rows."""
+        torch = self._torch
+        row_end = m if row_end is None else row_end
+        if Y is None:
+            Y = torch.empty((row_end - row_begin, n), dtype=torch.float64, device=val.device)
+        lam = self._lambda(T, safety, lambda_max, want_lambda)
+        inf = Info() if info else None
+        st = lib.cpa_svt_apply_csr(self._h, m, n, val.numel(), row_ptr.data_ptr(), col.data_ptr(), val.data_ptr(),
+                                   row_begin, row_end, Y.data_ptr(), Y.stride(0),
+                                   ctypes.byref(kernel_from_dict(kernel)), K, ctypes.byref(lam),
+                                   ctypes.byref(inf) if inf is not None else None)
+        self._check(st, "cpa_svt_apply_csr")
+        if info or want_lambda:
+            return Y, (inf.as_dict() if inf is not None else {"lambda_hat": lam.lambda_hat,
+                                                                 "lambda_max": lam.lambda_max})
+        return Y

@@ -1,0 +1,470 @@
+// C ABI of libcpasvt (include/cpa_svt.h): validation, side selection,
+// workspace, launch sequence, NCCL plumbing.  All arithmetic of the method
+// runs in the kernels of dense_f64.cu / power.cu / batched_f32.cu / sparse_f64.cu.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace cpa {
+// dense_f64.cu
+cudaError_t dense_gram_f64(const double* X, int64_t m, int64_t n, int64_t ldx, bool left, double* G,
+                           cudaStream_t st);
+cudaError_t dense_cheb_launch(bool left, bool init, int64_t m, int64_t n, const double* G,
+                              const double* Wsrc, int64_t ldsrc, const double* Wpp, int64_t ldpp,
+                              double* Wout, int64_t ldout, double* Y, int64_t ldy, const SeriesParams* P,
+                              int k, cudaStream_t st);
+// power.cu
+cudaError_t launch_series(SeriesParams* P, const cpa_svt_kernel& k, int K, double safety, double lam_override,
+                          const double* lam_src, const double* c_given, cudaStream_t st);
+size_t power_dense_scratch_doubles(int64_t s);
+cudaError_t launch_power_dense(const double* G, int64_t s, int T, double* scratch, unsigned int* bar,
+                               SeriesParams* P, const cpa_svt_kernel& k, int K, double safety,
+                               const double* c_given, int num_sms, cudaStream_t st);
+// batched_f32.cu
+cudaError_t launch_batched_f32(int64_t batch, int m, int n, const float* X, float* Y, const cpa_svt_kernel& k,
+                               int K, int T, double safety, double lam_override, float* lambda_out,
+                               int num_sms, cudaStream_t st, int* launches);
+// sparse_f64.cu
+struct SparseWork;
+cudaError_t sparse_apply(int64_t m, int64_t n, int64_t nnz, const int64_t* row_ptr, const int32_t* col,
+                         const double* val, int64_t row_begin, int64_t row_end, double* Y, int64_t ldy,
+                         const cpa_svt_kernel& k, int K, int T, double safety, double lam_override,
+                         SeriesParams* P, void* ws, size_t ws_bytes, size_t* ws_needed, int num_sms,
+                         cudaStream_t st, int* launches);
+}  // namespace cpa
+
+using namespace cpa;
+
+// ------------------------------------------------------------------ NCCL (run-time loaded)
+namespace {
+struct NcclApi {
+  void* lib = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool load() {
+    if (lib) return true;
+    lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) return false;
+    GetUniqueId = (decltype(GetUniqueId))dlsym(lib, "ncclGetUniqueId");
+    CommInitRank = (decltype(CommInitRank))dlsym(lib, "ncclCommInitRank");
+    CommDestroy = (decltype(CommDestroy))dlsym(lib, "ncclCommDestroy");
+    AllReduce = (decltype(AllReduce))dlsym(lib, "ncclAllReduce");
+    Broadcast = (decltype(Broadcast))dlsym(lib, "ncclBroadcast");
+    GetErrorString = (decltype(GetErrorString))dlsym(lib, "ncclGetErrorString");
+    return GetUniqueId && CommInitRank && CommDestroy && AllReduce && Broadcast && GetErrorString;
+  }
+};
+NcclApi g_nccl;
+}  // namespace
+
+struct cpa_svt_handle {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int rank = 0, world = 1;
+  ncclComm_t comm = nullptr;
+  int num_sms = 148;
+  SeriesParams* P = nullptr;       // device
+  unsigned int* bar = nullptr;     // device, 2 uints (grid barrier)
+  double* d_c = nullptr;           // device, KMAX (caller coefficients)
+  void* ws = nullptr;              // workspace
+  size_t ws_bytes = 0;
+  void* hx = nullptr;              // apply_host device staging
+  size_t hx_bytes = 0;
+  std::string err;
+  int64_t launches = 0;
+};
+
+#define CU(call)                                                                     \
+  do {                                                                               \
+    cudaError_t e_ = (call);                                                         \
+    if (e_ != cudaSuccess) {                                                         \
+      h->err = std::string(#call) + ": " + cudaGetErrorString(e_);                   \
+      return CPA_SVT_E_CUDA;                                                         \
+    }                                                                                \
+  } while (0)
+
+#define NC(call)                                                                     \
+  do {                                                                               \
+    ncclResult_t r_ = (call);                                                        \
+    if (r_ != ncclSuccess) {                                                         \
+      h->err = std::string(#call) + ": " + g_nccl.GetErrorString(r_);                \
+      return CPA_SVT_E_NCCL;                                                         \
+    }                                                                                \
+  } while (0)
+
+static cpa_svt_status grow(cpa_svt_handle* h, void** p, size_t* have, size_t need) {
+  if (need <= *have) return CPA_SVT_OK;
+  if (*p) {
+    cudaStreamSynchronize(h->stream);
+    cudaFree(*p);
+    *p = nullptr;
+    *have = 0;
+  }
+  cudaError_t e = cudaMalloc(p, need);
+  if (e != cudaSuccess) {
+    h->err = std::string("workspace cudaMalloc: ") + cudaGetErrorString(e);
+    cudaGetLastError();
+    return CPA_SVT_E_NOMEM;
+  }
+  *have = need;
+  return CPA_SVT_OK;
+}
+
+static cpa_svt_status check_kernel(const cpa_svt_kernel* k) {
+  if (!k) return CPA_SVT_E_ARG;
+  if (k->kind < CPA_SVT_HARD || k->kind > CPA_SVT_WSOFT) return CPA_SVT_E_ARG;
+  if (k->kind != CPA_SVT_WSOFT) {
+    if (!(k->tau >= 0.0) || !std::isfinite(k->tau)) return CPA_SVT_E_DOMAIN;
+  } else {
+    if (!(k->w_c >= 0.0) || !(k->w_shift >= 0.0) || !(k->w_eps > 0.0) || !std::isfinite(k->w_c))
+      return CPA_SVT_E_DOMAIN;
+  }
+  return CPA_SVT_OK;
+}
+
+static cpa_svt_status check_lambda(const cpa_svt_lambda* lam) {
+  if (!lam) return CPA_SVT_E_ARG;
+  if (!(lam->safety >= 1.0) || !std::isfinite(lam->safety)) return CPA_SVT_E_DOMAIN;
+  if (!std::isfinite(lam->lambda_max) || lam->lambda_max < 0.0) return CPA_SVT_E_DOMAIN;
+  if (!(lam->lambda_max > 0.0) && lam->power_iters < 1) return CPA_SVT_E_ARG;
+  return CPA_SVT_OK;
+}
+
+extern "C" {
+
+const char* cpa_svt_status_string(cpa_svt_status s) {
+  switch (s) {
+    case CPA_SVT_OK: return "ok";
+    case CPA_SVT_E_ARG: return "invalid argument";
+    case CPA_SVT_E_DOMAIN: return "argument outside the method's domain";
+    case CPA_SVT_E_DIVERGED: return "recurrence diverged";
+    case CPA_SVT_E_CUDA: return "CUDA error";
+    case CPA_SVT_E_NCCL: return "NCCL error";
+    case CPA_SVT_E_NOMEM: return "out of device memory";
+    case CPA_SVT_E_UNSUPPORTED: return "unsupported by this build";
+  }
+  return "unknown status";
+}
+
+const char* cpa_svt_last_error(const cpa_svt_handle* h) { return h ? h->err.c_str() : ""; }
+int64_t cpa_svt_launch_count(const cpa_svt_handle* h) { return h ? h->launches : 0; }
+
+cpa_svt_status cpa_svt_nccl_unique_id(void* out128) {
+  if (!out128) return CPA_SVT_E_ARG;
+  if (!g_nccl.load()) return CPA_SVT_E_NCCL;
+  ncclUniqueId id;
+  if (g_nccl.GetUniqueId(&id) != ncclSuccess) return CPA_SVT_E_NCCL;
+  memcpy(out128, &id, sizeof(id));
+  return CPA_SVT_OK;
+}
+
+cpa_svt_status cpa_svt_init(cpa_svt_handle** out, int device, void* cuda_stream, const void* nccl_unique_id,
+                            int rank, int world) {
+  if (!out || world < 1 || rank < 0 || rank >= world) return CPA_SVT_E_ARG;
+  if (world > 1 && !nccl_unique_id) return CPA_SVT_E_ARG;
+  *out = nullptr;
+  cpa_svt_handle* h = new cpa_svt_handle();
+  h->device = device;
+  h->stream = (cudaStream_t)cuda_stream;
+  h->rank = rank;
+  h->world = world;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (e == cudaSuccess) e = cudaMalloc(&h->P, sizeof(SeriesParams));
+  if (e == cudaSuccess) e = cudaMalloc(&h->bar, 64);
+  if (e == cudaSuccess) e = cudaMemset(h->bar, 0, 64);
+  if (e == cudaSuccess) e = cudaMalloc(&h->d_c, CPA_SVT_KMAX * sizeof(double));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    cpa_svt_free(h);
+    return CPA_SVT_E_CUDA;
+  }
+  if (world > 1) {
+    if (!g_nccl.load()) {
+      cpa_svt_free(h);
+      return CPA_SVT_E_NCCL;
+    }
+    ncclUniqueId id;
+    memcpy(&id, nccl_unique_id, sizeof(id));
+    if (g_nccl.CommInitRank(&h->comm, world, id, rank) != ncclSuccess) {
+      h->comm = nullptr;
+      cpa_svt_free(h);
+      return CPA_SVT_E_NCCL;
+    }
+  }
+  *out = h;
+  return CPA_SVT_OK;
+}
+
+cpa_svt_status cpa_svt_free(cpa_svt_handle* h) {
+  if (!h) return CPA_SVT_OK;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  else cudaDeviceSynchronize();
+  if (h->comm) g_nccl.CommDestroy(h->comm);
+  cudaFree(h->P);
+  cudaFree(h->bar);
+  cudaFree(h->d_c);
+  cudaFree(h->ws);
+  cudaFree(h->hx);
+  delete h;
+  return CPA_SVT_OK;
+}
+
+cpa_svt_status cpa_svt_coeffs(const cpa_svt_kernel* k, int K, double lambda_max, double sigma_max_hat,
+                              double* c_out) {
+  if (!c_out || K < 1 || K > CPA_SVT_KMAX) return CPA_SVT_E_ARG;
+  cpa_svt_status st = check_kernel(k);
+  if (st != CPA_SVT_OK) return st;
+  if (!(lambda_max > 0.0) || !std::isfinite(lambda_max) || !(sigma_max_hat >= 0.0)) return CPA_SVT_E_DOMAIN;
+  const double tau = resolve_tau(*k, sigma_max_hat);
+  std::vector<double> hv(K);
+  for (int l = 0; l < K; ++l) hv[l] = h_response(*k, lambda_max / 2.0 * (cos(cheb_theta(l + 1, K)) + 1.0), tau);
+  for (int kk = 0; kk < K; ++kk) {
+    double acc = 0.0;
+    for (int l = 0; l < K; ++l) acc += cos(kk * cheb_theta(l + 1, K)) * hv[l];
+    c_out[kk] = 2.0 / K * acc;
+  }
+  return CPA_SVT_OK;
+}
+
+static cpa_svt_status fill_info(cpa_svt_handle* h, cpa_svt_info* info, cpa_svt_lambda* lam, int side) {
+  if (!info && !(lam && lam->want_lambda)) return CPA_SVT_OK;
+  SeriesParams hp;
+  CU(cudaMemcpyAsync(&hp, h->P, offsetof(SeriesParams, c), cudaMemcpyDeviceToHost, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  if (info) {
+    info->lambda_hat = hp.lambda_hat;
+    info->lambda_max = hp.lambda_max;
+    info->sigma_max_hat = hp.sigma_hat;
+    info->tau_used = hp.tau;
+    info->side = side;
+    info->degenerate = hp.degenerate;
+  }
+  if (lam && lam->want_lambda) {
+    lam->lambda_hat = hp.lambda_hat;
+    lam->lambda_max = hp.lambda_max;
+  }
+  return CPA_SVT_OK;
+}
+
+struct PhaseTimer {
+  cudaEvent_t ev[6] = {};
+  int n = 0;
+  bool on = false;
+  cudaStream_t st = nullptr;
+  void start(bool enable, cudaStream_t s) {
+    on = enable;
+    st = s;
+    if (!on) return;
+    for (auto& e : ev) cudaEventCreate(&e);
+    cudaEventRecord(ev[n++], st);
+  }
+  void mark() {
+    if (on) cudaEventRecord(ev[n++], st);
+  }
+  float ms(int a, int b) {
+    float t = 0.f;
+    if (on && b < n) cudaEventElapsedTime(&t, ev[a], ev[b]);
+    return t;
+  }
+  ~PhaseTimer() {
+    if (on)
+      for (auto& e : ev) cudaEventDestroy(e);
+  }
+};
+
+static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt_shard shard,
+                                int64_t long_global, const double* X, int64_t ldx, double* Y, int64_t ldy,
+                                const cpa_svt_kernel* k, int K, const double* c, cpa_svt_lambda* lam,
+                                cpa_svt_info* info) {
+  // side selection (reading R3): left iff global m <= global n
+  bool left;
+  if (shard == CPA_SVT_SHARD_COLS) {
+    if (m > long_global || long_global < n) return CPA_SVT_E_ARG;
+    left = true;
+  } else if (shard == CPA_SVT_SHARD_ROWS) {
+    if (long_global <= n || long_global < m) return CPA_SVT_E_ARG;
+    left = false;
+  } else {
+    left = m <= n;
+  }
+  const int64_t s = left ? m : n;
+  const bool sharded = shard != CPA_SVT_SHARD_NONE && h->world > 1;
+  // workspace: G (s*s) | W_a (m*n) | W_b (m*n) | power scratch
+  const size_t nG = (size_t)s * s, nW = (size_t)m * n, nPow = power_dense_scratch_doubles(s);
+  const size_t need = (nG + 2 * nW + nPow) * sizeof(double) + 256;
+  cpa_svt_status st = grow(h, &h->ws, &h->ws_bytes, need);
+  if (st != CPA_SVT_OK) return st;
+  double* G = (double*)h->ws;
+  double* Wa = G + nG;
+  double* Wb = Wa + nW;
+  double* pw = Wb + nW;
+
+  const double* c_dev = nullptr;
+  if (c) {
+    CU(cudaMemcpyAsync(h->d_c, c, K * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+    c_dev = h->d_c;
+  }
+  PhaseTimer tm;
+  tm.start(info != nullptr, h->stream);
+  int launches = 0;
+  // Alg. 1 line 1: partial Gram of this shard
+  CU(dense_gram_f64(X, m, n, ldx, left, G, h->stream));
+  ++launches;
+  tm.mark();
+  // exchange: G = sum_p G_p over NVLink (one all-reduce per shrinkage)
+  if (sharded) NC(g_nccl.AllReduce(G, G, nG, ncclDouble, ncclSum, h->comm, h->stream));
+  tm.mark();
+  // Alg. 1 lines 3-4: Lambda_max and coefficients, on the device
+  if (lam->lambda_max > 0.0) {
+    CU(launch_series(h->P, *k, K, lam->safety, lam->lambda_max, nullptr, c_dev, h->stream));
+  } else {
+    if (s * (int64_t)sizeof(double) > 200 * 1024) return CPA_SVT_E_UNSUPPORTED;
+    CU(launch_power_dense(G, s, lam->power_iters, pw, h->bar, h->P, *k, K, lam->safety, c_dev, h->num_sms,
+                          h->stream));
+  }
+  ++launches;
+  if (sharded) NC(g_nccl.Broadcast(h->P, h->P, sizeof(SeriesParams), ncclChar, 0, h->comm, h->stream));
+  tm.mark();
+  // Alg. 1 lines 5-11 in the apply-to-X form
+  CU(dense_cheb_launch(left, true, m, n, G, X, ldx, nullptr, 0, K > 2 ? Wa : nullptr, n, Y, ldy, h->P, 1,
+                       h->stream));
+  ++launches;
+  for (int kk = 2; kk < K; ++kk) {
+    const double *src, *pp;
+    double* out;
+    int64_t ldsrc, ldpp;
+    if (kk == 2) {
+      src = Wa; ldsrc = n; pp = X; ldpp = ldx; out = Wb;
+    } else {
+      out = (kk & 1) ? Wa : Wb;      // W_k overwrites W_{k-2} in place
+      src = (kk & 1) ? Wb : Wa;
+      ldsrc = n; pp = out; ldpp = n;
+    }
+    if (kk == K - 1) out = nullptr;  // last W_k is never read again
+    CU(dense_cheb_launch(left, false, m, n, G, src, ldsrc, pp, ldpp, out, n, Y, ldy, h->P, kk, h->stream));
+    ++launches;
+  }
+  tm.mark();
+  h->launches += launches;
+  st = fill_info(h, info, lam, left ? 0 : 1);
+  if (st != CPA_SVT_OK) return st;
+  if (info) {
+    info->ms_gram = tm.ms(0, 1);
+    info->ms_allreduce = tm.ms(1, 2);
+    info->ms_power = tm.ms(2, 3);
+    info->ms_recurrence = tm.ms(3, 4);
+    info->ms_total = tm.ms(0, 4);
+    info->kernel_launches = launches;
+  }
+  return CPA_SVT_OK;
+}
+
+cpa_svt_status cpa_svt_apply(cpa_svt_handle* h, cpa_svt_dtype dtype, cpa_svt_math math, int64_t m, int64_t n,
+                             cpa_svt_shard shard, int64_t long_global, const void* X, int64_t ldx, void* Y,
+                             int64_t ldy, const cpa_svt_kernel* k, int K, const double* c, cpa_svt_lambda* lam,
+                             cpa_svt_info* info) {
+  if (!h || !X || !Y || X == Y) return CPA_SVT_E_ARG;
+  if (m < 1 || n < 1 || ldx < n || ldy < n || K < 2 || K > CPA_SVT_KMAX) return CPA_SVT_E_ARG;
+  if (shard < CPA_SVT_SHARD_NONE || shard > CPA_SVT_SHARD_ROWS) return CPA_SVT_E_ARG;
+  if (!c) {
+    cpa_svt_status st = check_kernel(k);
+    if (st != CPA_SVT_OK) return st;
+  }
+  cpa_svt_status st = check_lambda(lam);
+  if (st != CPA_SVT_OK) return st;
+  if (cudaSetDevice(h->device) != cudaSuccess) return CPA_SVT_E_CUDA;
+  cpa_svt_kernel kz{};
+  if (!k) k = &kz;
+  if (dtype == CPA_SVT_F64 && math == CPA_SVT_MATH_NATIVE)
+    return apply_f64(h, m, n, shard, long_global, (const double*)X, ldx, (double*)Y, ldy, k, K, c, lam, info);
+  return CPA_SVT_E_UNSUPPORTED;
+}
+
+cpa_svt_status cpa_svt_apply_host(cpa_svt_handle* h, cpa_svt_dtype dtype, cpa_svt_math math, int64_t m, int64_t n,
+                                  const void* X_host, void* Y_host, const cpa_svt_kernel* k, int K,
+                                  cpa_svt_lambda* lam, cpa_svt_info* info) {
+  if (!h || !X_host || !Y_host || m < 1 || n < 1) return CPA_SVT_E_ARG;
+  const size_t es = dtype == CPA_SVT_F64 ? 8 : 4;
+  const size_t bytes = (size_t)m * n * es;
+  if (cudaSetDevice(h->device) != cudaSuccess) return CPA_SVT_E_CUDA;
+  cpa_svt_status st = grow(h, &h->hx, &h->hx_bytes, 2 * bytes + 256);
+  if (st != CPA_SVT_OK) return st;
+  char* dX = (char*)h->hx;
+  char* dY = dX + ((bytes + 255) / 256) * 256;
+  CU(cudaMemcpyAsync(dX, X_host, bytes, cudaMemcpyHostToDevice, h->stream));
+  st = cpa_svt_apply(h, dtype, math, m, n, CPA_SVT_SHARD_NONE, 0, dX, n, dY, n, k, K, nullptr, lam, info);
+  if (st != CPA_SVT_OK) return st;
+  CU(cudaMemcpyAsync(Y_host, dY, bytes, cudaMemcpyDeviceToHost, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  return CPA_SVT_OK;
+}
+
+cpa_svt_status cpa_svt_apply_batched(cpa_svt_handle* h, int64_t batch, int m, int n, const float* X, float* Y,
+                                     const cpa_svt_kernel* k, int K, const cpa_svt_lambda* lam,
+                                     float* lambda_out) {
+  if (!h || !X || !Y || (const void*)X == (void*)Y || batch < 0 || m < 1 || n < 1 || m > 64 || n > 64)
+    return CPA_SVT_E_ARG;
+  if (K < 2 || K > CPA_SVT_KMAX) return CPA_SVT_E_ARG;
+  cpa_svt_status st = check_kernel(k);
+  if (st != CPA_SVT_OK) return st;
+  st = check_lambda(lam);
+  if (st != CPA_SVT_OK) return st;
+  if (batch == 0) return CPA_SVT_OK;
+  if (cudaSetDevice(h->device) != cudaSuccess) return CPA_SVT_E_CUDA;
+  int launches = 0;
+  CU(launch_batched_f32(batch, m, n, X, Y, *k, K, lam->power_iters, lam->safety, lam->lambda_max, lambda_out,
+                        h->num_sms, h->stream, &launches));
+  h->launches += launches;
+  return CPA_SVT_OK;
+}
+
+cpa_svt_status cpa_svt_apply_csr(cpa_svt_handle* h, int64_t m, int64_t n, int64_t nnz, const int64_t* row_ptr,
+                                 const int32_t* col, const double* val, int64_t row_begin, int64_t row_end,
+                                 double* Y, int64_t ldy, const cpa_svt_kernel* k, int K, cpa_svt_lambda* lam,
+                                 cpa_svt_info* info) {
+  if (!h || !row_ptr || !Y || m < 1 || n < 1 || nnz < 0 || (nnz > 0 && (!col || !val))) return CPA_SVT_E_ARG;
+  if (row_begin < 0 || row_end > m || row_begin > row_end || ldy < n || K < 2 || K > CPA_SVT_KMAX)
+    return CPA_SVT_E_ARG;
+  if (m > 2147483647 || n > 2147483647) return CPA_SVT_E_ARG;
+  cpa_svt_status st = check_kernel(k);
+  if (st != CPA_SVT_OK) return st;
+  st = check_lambda(lam);
+  if (st != CPA_SVT_OK) return st;
+  if (cudaSetDevice(h->device) != cudaSuccess) return CPA_SVT_E_CUDA;
+  size_t need = 0;
+  CU(sparse_apply(m, n, nnz, row_ptr, col, val, row_begin, row_end, Y, ldy, *k, K, lam->power_iters, lam->safety,
+                  lam->lambda_max, h->P, nullptr, 0, &need, h->num_sms, h->stream, nullptr));
+  st = grow(h, &h->ws, &h->ws_bytes, need);
+  if (st != CPA_SVT_OK) return st;
+  PhaseTimer tm;
+  tm.start(info != nullptr, h->stream);
+  int launches = 0;
+  CU(sparse_apply(m, n, nnz, row_ptr, col, val, row_begin, row_end, Y, ldy, *k, K, lam->power_iters, lam->safety,
+                  lam->lambda_max, h->P, h->ws, h->ws_bytes, &need, h->num_sms, h->stream, &launches));
+  tm.mark();
+  h->launches += launches;
+  st = fill_info(h, info, lam, 1);
+  if (st != CPA_SVT_OK) return st;
+  if (info) {
+    info->ms_total = info->ms_recurrence = tm.ms(0, 1);
+    info->kernel_launches = launches;
+  }
+  return CPA_SVT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,104 @@
+// Internal definitions shared by the CUDA translation units of libcpasvt.
+// Product code only: nothing here is shared with oracle/ (which is Python).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <math.h>
+
+#include "cpa_svt.h"
+
+namespace cpa {
+
+constexpr double kDegenerateLambda = 1e-300;  // SPEC.md:287 / reading R17
+
+// Series parameters produced on the device by the power-iteration tail and
+// consumed by every recurrence kernel (no host round trip; reading R6/R7).
+struct SeriesParams {
+  double lambda_hat;   // power-iteration estimate (or override / safety)
+  double lambda_max;   // safety * lambda_hat
+  double sigma_hat;    // sqrt(lambda_hat)
+  double tau;          // resolved absolute threshold
+  double scale2;       // 2 / lambda_max  (0 when degenerate)
+  int32_t degenerate;  // lambda_hat <= 1e-300
+  int32_t K;
+  double c[CPA_SVT_KMAX];
+};
+
+// ---- the response h(x) of PAPER.md:496-519 (host and device) --------------
+__host__ __device__ inline double h_response(const cpa_svt_kernel& k, double x, double tau) {
+  const double r = sqrt(x);
+  switch (k.kind) {
+    case CPA_SVT_HARD:
+      return r > tau ? 1.0 : 0.0;
+    case CPA_SVT_SOFT:
+      return r > tau ? (r - tau) / r : 0.0;
+    default: {  // CPA_SVT_WSOFT
+      const double xs = x - k.w_shift;
+      const double w = k.w_c / (sqrt(xs > 0.0 ? xs : 0.0) + k.w_eps);
+      return r > w ? (r - w) / r : 0.0;
+    }
+  }
+}
+
+__host__ __device__ inline double resolve_tau(const cpa_svt_kernel& k, double sigma_hat) {
+  return k.tau_relative ? k.tau * sigma_hat : k.tau;
+}
+
+// Chebyshev-Gauss node l (1-based) of order K: theta_l = pi (l - 1/2) / K.
+__host__ __device__ inline double cheb_theta(int l, int K) {
+  return 3.141592653589793238462643383279502884 * ((double)l - 0.5) / (double)K;
+}
+
+// ---- small PTX helpers --------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// 8-byte async copy with zero fill when !pred (src-size 0).
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),
+               "r"(pred ? 8 : 0));
+}
+// 16-byte async copy (L2 only) with zero fill when !pred.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),
+               "r"(pred ? 16 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// D = A(8x4, row) * B(4x8, col) + C, fp64 tensor core (SASS DMMA.8x8x4).
+// Lane l holds A[l/4][l%4], B[l%4][l/4], C[l/4][2(l%4)], C[l/4][2(l%4)+1].
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// Sense-free generation barrier for a cooperative (co-resident) grid.
+// count: arrivals this generation (reset by the last arriver); gen: generation.
+__device__ __forceinline__ void grid_barrier(unsigned int* count, volatile unsigned int* gen,
+                                             unsigned int nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int g = *gen;
+    __threadfence();
+    if (atomicAdd(count, 1u) == nblocks - 1) {
+      *count = 0;
+      __threadfence();
+      atomicAdd((unsigned int*)gen, 1u);
+    } else {
+      while (*gen == g) {
+        __nanosleep(32);
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+}  // namespace cpa

@@ -1,0 +1,169 @@
+"""Parity of the fp64 dense CUDA path (DMMA Gram + fused recurrence) with the oracle.
+
+Bar (north_star): relative Frobenius error <= 1e-10 on the fp64 path.  Inputs are
+the seeded workloads; the oracle runs Alg. 1 literally (H_hat formed s x s, then
+one product), the GPU runs the apply-to-X recurrence, so agreement checks the
+arithmetic, not a shared code path.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+TOL64 = 1e-10
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    import paper_1705_07112_b200 as P
+    h = P.Handle(0)
+    yield torch, P, h
+    h.close()
+
+
+def _run(env, X, kernel, K, T=30, **kw):
+    torch, P, h = env
+    Xd = torch.from_numpy(np.ascontiguousarray(X)).cuda()
+    out = h.apply(Xd, kernel, K, T=T, info=True, **kw)
+    Y, info = out
+    torch.cuda.synchronize()
+    return Y.cpu().numpy(), info
+
+
+def test_config1_parity_and_exact(env):
+    cfg = W.CONFIGS["c1"]
+    X = W.gen_c1()
+    Y, info = _run(env, X, cfg["kernel"], cfg["K"], T=cfg["T"])
+    k = O.Kernel(**cfg["kernel"])
+    Yo, io = O.cpa_shrink(X, k, cfg["K"], T=cfg["T"], return_info=True)
+    assert info["side"] == 1 and io["side"] == "right"
+    assert abs(info["lambda_hat"] - io["lambda_hat"]) <= 1e-13 * io["lambda_hat"]
+    assert O.rel_fro(Y, Yo) <= TOL64
+    # and the method's own error vs exact Jacobi-SVD shrinkage (P10 at K = 20)
+    assert O.rel_fro(Y, O.exact_shrink(X, k, 2.0)) <= 2e-2
+
+
+def test_config2_parity(env):
+    cfg = W.CONFIGS["c2"]
+    X = W.gen_c2()
+    Y, info = _run(env, X, cfg["kernel"], cfg["K"], T=cfg["T"])
+    Yo, io = O.cpa_shrink(X, O.Kernel(**cfg["kernel"]), cfg["K"], T=cfg["T"], return_info=True)
+    assert info["side"] == 0
+    assert abs(info["lambda_hat"] - io["lambda_hat"]) <= 1e-12 * io["lambda_hat"]
+    assert abs(info["tau_used"] - io["tau"]) <= 1e-12 * io["tau"]
+    assert O.rel_fro(Y, Yo) <= TOL64
+
+
+SHAPES = [(1, 1), (1, 7), (7, 1), (7, 33), (33, 7), (64, 64), (100, 257), (257, 100), (130, 130), (65, 200)]
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("kind,K", [("soft", 2), ("hard", 3), ("wsoft", 5), ("soft", 20)])
+def test_odd_shapes(env, shape, kind, K):
+    X = W.random_dense(*shape, seed=shape[0] * 1000 + shape[1] + K)
+    kern = {"kind": kind, "tau": 0.3, "tau_relative": True, "w_c": 2.0, "w_shift": 0.0, "w_eps": 1e-6}
+    Y, info = _run(env, X, kern, K, T=40)
+    Yo, io = O.cpa_shrink(X, O.Kernel(**kern), K, T=40, return_info=True)
+    assert info["side"] == (0 if shape[0] <= shape[1] else 1)
+    assert O.rel_fro(Y, Yo) <= TOL64, (shape, kind, K)
+
+
+@pytest.mark.parametrize("shape", [(40, 70), (70, 40)])
+def test_raw_coefficients(env, shape):
+    torch, P, h = env
+    X = W.random_dense(*shape, seed=3)
+    lam = 2.0 * float(np.linalg.norm(X, 2)) ** 2
+    Y, _ = _run(env, X, None, 4, lambda_max=lam, coeffs=[2.0, 0.0, 0.0, 0.0])
+    assert O.rel_fro(Y, X) <= 1e-14
+    Y, _ = _run(env, X, None, 4, lambda_max=lam, coeffs=[lam, lam / 2, 0.0, 0.0])
+    assert O.rel_fro(Y, X @ X.T @ X) <= 1e-13
+    for kk in (2, 3, 5):
+        c = [0.0] * 6
+        c[kk] = 1.0
+        Y, _ = _run(env, X, None, 6, lambda_max=lam, coeffs=c)
+        assert O.rel_fro(Y, O.cpa_shrink(X, None, 6, lam=lam, coeffs=c)) <= 1e-12
+
+
+def test_degenerate_zero(env):
+    Y, info = _run(env, np.zeros((33, 20)), {"kind": "soft", "tau": 1.0}, 10)
+    assert info["degenerate"] == 1 and not Y.any()
+
+
+def test_deterministic_and_pow2(env):
+    X = W.gen_c2(m=300, n=500)
+    k1 = {"kind": "soft", "tau": 1.0}
+    a, _ = _run(env, X, k1, 12)
+    b, _ = _run(env, X, k1, 12)
+    assert np.array_equal(a, b)
+    c, _ = _run(env, 2 * X, {"kind": "soft", "tau": 2.0}, 12)
+    assert np.array_equal(2 * a, c)
+
+
+def test_hard_zero_tau_identity(env):
+    X = W.random_dense(90, 150, seed=11)
+    Y, _ = _run(env, X, {"kind": "hard", "tau": 0.0}, 25)
+    assert O.rel_fro(Y, X) <= 1e-13
+
+
+def test_block_diagonal_closed_form(env):
+    # P17 at a larger, wide shape: the paper's D repeated 4x
+    N, nb, copies = 1024, 16, 4
+    D = W.block_diag_D(N, nb, copies)
+    p = N // nb
+    s1, s2 = math.sqrt(copies) * (N - p / 2), math.sqrt(copies) * (p / 2)
+    kern = {"kind": "soft", "tau": 0.3, "tau_relative": True}
+    Y, info = _run(env, D, kern, 24, T=30)
+    lam, c = info["lambda_max"], O.kernel_coefficients(O.Kernel(**kern), 24, info["lambda_max"],
+                                                        info["sigma_max_hat"])
+    assert abs(info["lambda_hat"] - s1 ** 2) <= 1e-12 * s1 ** 2
+    f1 = s1 * O.series_eval(c, lam, s1 ** 2)
+    f2 = s2 * O.series_eval(c, lam, s2 ** 2)
+    q = np.ones(N) / math.sqrt(N)
+    Pb = np.kron(np.eye(nb), np.ones((p, p)) / p)
+    R = np.concatenate([np.eye(N)] * copies, axis=1) / math.sqrt(copies)
+    want = (f1 * np.outer(q, q) - f2 * (Pb - np.outer(q, q))) @ R
+    assert O.rel_fro(Y, want) <= 1e-12
+
+
+def test_apply_host_matches_device(env):
+    torch, P, h = env
+    X = W.gen_c2(m=256, n=384)
+    kern = {"kind": "soft", "tau": 0.05, "tau_relative": True}
+    Yd, _ = _run(env, X, kern, 15, T=100)
+    Xh = torch.from_numpy(X).pin_memory()
+    Yh = torch.empty_like(Xh).pin_memory()
+    h.apply_host(Xh, Yh, kern, 15, T=100)
+    assert np.array_equal(Yh.numpy(), Yd)
+
+
+def test_strided_inputs(env):
+    torch, P, h = env
+    X = W.random_dense(70, 90, seed=5)
+    big = torch.zeros((70, 101), dtype=torch.float64, device="cuda")
+    big[:, :90] = torch.from_numpy(X).cuda()
+    Xv = big[:, :90]
+    Yv = torch.full((70, 97), 7.0, dtype=torch.float64, device="cuda")[:, :90]
+    kern = {"kind": "soft", "tau": 0.2, "tau_relative": True}
+    h.apply(Xv, kern, 9, T=50, Y=Yv)
+    assert O.rel_fro(Yv.cpu().numpy(), O.cpa_shrink(X, O.Kernel(**kern), 9, T=50)) <= TOL64
+
+
+def test_bad_arguments(env):
+    torch, P, h = env
+    X = torch.zeros((4, 4), dtype=torch.float64, device="cuda")
+    with pytest.raises(P.CpaSvtError) as e:
+        h.apply(X, {"kind": "soft", "tau": 1.0}, 1)
+    assert e.value.status == 1
+    with pytest.raises(P.CpaSvtError) as e:
+        h.apply(X, {"kind": "soft", "tau": -1.0}, 5)
+    assert e.value.status == 2
+    with pytest.raises(P.CpaSvtError) as e:
+        h.apply(X, {"kind": "soft", "tau": 1.0}, 5, Y=X)
+    assert e.value.status == 1
