@@ -179,10 +179,30 @@ cpa_svt_status cpa_svt_apply_csr(cpa_svt_handle* h, int64_t m, int64_t n, int64_
  * contiguously ([batch][m][n], row-major): Gram, power iteration, coefficients
  * and the recurrence per matrix inside one kernel (no host round trip).
  * lambda_out: optional device array of `batch` floats receiving Lambda_max.
- * Requires m, n <= 64. */
+ * Requires m, n <= 64 and K <= 128 (else CPA_SVT_E_UNSUPPORTED). */
 cpa_svt_status cpa_svt_apply_batched(cpa_svt_handle* h, int64_t batch, int m, int n,
                                      const float* X, float* Y, const cpa_svt_kernel* k, int K,
                                      const cpa_svt_lambda* lam, float* lambda_out);
+
+/* Per-phase device timing for measurement: when enabled, the library records a
+ * CUDA event pair on the handle's stream around every launch it makes and
+ * accumulates the elapsed time per phase (no host sync until read). */
+typedef enum {
+  CPA_SVT_PH_GRAM = 0,       /* Gram product (Alg. 1 line 1) */
+  CPA_SVT_PH_ALLREDUCE = 1,  /* NCCL all-reduce of the Gram + Lambda broadcast */
+  CPA_SVT_PH_POWER = 2,      /* power iteration + coefficients (lines 3-4) */
+  CPA_SVT_PH_INIT = 3,       /* W_1 and Y init (lines 5-7) */
+  CPA_SVT_PH_STEP = 4,       /* fused recurrence step (lines 8-11), one per k */
+  CPA_SVT_PH_SPARSE_Z = 5,   /* sparse: Z = W_{k-1} X^T */
+  CPA_SVT_PH_SPARSE_W = 6,   /* sparse: W_k = (4/L) Z X - 2 W_{k-1} - W_{k-2}, Y += c_k W_k */
+  CPA_SVT_PH_BATCHED = 7,    /* batched kernel */
+  CPA_SVT_PH_COUNT = 8
+} cpa_svt_phase;
+/* enable != 0: reset the accumulators and start recording; 0: stop. */
+cpa_svt_status cpa_svt_profile(cpa_svt_handle* h, int enable);
+/* Synchronise the stream, then write per-phase total ms and launch counts
+ * (host arrays of CPA_SVT_PH_COUNT entries; either may be NULL). */
+cpa_svt_status cpa_svt_profile_read(cpa_svt_handle* h, double* ms, int64_t* launches);
 
 const char* cpa_svt_status_string(cpa_svt_status s);
 /* Text of the last error recorded on this handle ("" if none). */

@@ -73,8 +73,12 @@ lib.cpa_svt_last_error.restype = ctypes.c_char_p
 lib.cpa_svt_last_error.argtypes = [_p]
 lib.cpa_svt_launch_count.restype = ctypes.c_int64
 lib.cpa_svt_launch_count.argtypes = [_p]
+lib.cpa_svt_profile.argtypes = [_p, ctypes.c_int]
+lib.cpa_svt_profile_read.argtypes = [_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)]
+PHASES = ["gram", "allreduce", "power", "init", "step", "sparse_z", "sparse_w", "batched"]
 for _f in ("cpa_svt_init", "cpa_svt_free", "cpa_svt_nccl_unique_id", "cpa_svt_coeffs", "cpa_svt_apply",
-           "cpa_svt_apply_host", "cpa_svt_apply_csr", "cpa_svt_apply_batched"):
+           "cpa_svt_apply_host", "cpa_svt_apply_csr", "cpa_svt_apply_batched", "cpa_svt_profile",
+           "cpa_svt_profile_read"):
     getattr(lib, _f).restype = ctypes.c_int
 
 
@@ -136,6 +140,17 @@ class Handle:
     @property
     def launches(self) -> int:
         return lib.cpa_svt_launch_count(self._h)
+
+    def profile(self, enable: bool = True):
+        """cpa_svt_profile: reset and start (or stop) per-phase CUDA-event timing."""
+        self._check(lib.cpa_svt_profile(self._h, int(enable)), "cpa_svt_profile")
+
+    def profile_read(self):
+        """cpa_svt_profile_read -> {phase: (total_ms, launches)} (synchronises)."""
+        ms = (ctypes.c_double * len(PHASES))()
+        n = (ctypes.c_int64 * len(PHASES))()
+        self._check(lib.cpa_svt_profile_read(self._h, ms, n), "cpa_svt_profile_read")
+        return {p: (ms[i], n[i]) for i, p in enumerate(PHASES)}
 
     def close(self):
         if getattr(self, "_h", None):

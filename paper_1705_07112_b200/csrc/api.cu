@@ -6,6 +6,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -15,17 +16,24 @@
 namespace cpa {
 // dense_f64.cu
 cudaError_t dense_gram_f64(const double* X, int64_t m, int64_t n, int64_t ldx, bool left, double* G,
-                           cudaStream_t st);
+                           cudaStream_t st, const double* gscale = nullptr);
 cudaError_t dense_cheb_launch(bool left, bool init, int64_t m, int64_t n, const double* G,
                               const double* Wsrc, int64_t ldsrc, const double* Wpp, int64_t ldpp,
                               double* Wout, int64_t ldout, double* Y, int64_t ldy, const SeriesParams* P,
                               int k, cudaStream_t st);
+size_t dense_flow_sync_ints(int64_t m, int64_t n, int K);
+size_t dense_flow_partial_doubles(int64_t m, int64_t n, int num_sms);
+cudaError_t dense_cheb_flow(bool left, int64_t m, int64_t n, const double* G, const double* X, int64_t ldx,
+                            double* Wa, double* Wb, double* Y, int64_t ldy, const SeriesParams* P, int K, int* sync,
+                            double* partial, int num_sms, cudaStream_t st);
 // power.cu
 cudaError_t launch_series(SeriesParams* P, const cpa_svt_kernel& k, int K, double safety, double lam_override,
                           const double* lam_src, const double* c_given, cudaStream_t st);
 size_t power_dense_scratch_doubles(int64_t s);
-cudaError_t launch_power_dense(const double* G, int64_t s, int T, double* scratch, unsigned int* bar,
-                               SeriesParams* P, const cpa_svt_kernel& k, int K, double safety,
+bool power_use_squaring(int64_t s, int T);
+cudaError_t launch_diag_scale(const double* G, int64_t s, double* scale, cudaStream_t st);
+cudaError_t launch_power_dense(const double* G, const double* G4, int64_t s, int T, double* scratch,
+                               unsigned int* bar, SeriesParams* P, const cpa_svt_kernel& k, int K, double safety,
                                const double* c_given, int num_sms, cudaStream_t st);
 // batched_f32.cu
 cudaError_t launch_batched_f32(int64_t batch, int m, int n, const float* X, float* Y, const cpa_svt_kernel& k,
@@ -85,7 +93,44 @@ struct cpa_svt_handle {
   size_t hx_bytes = 0;
   std::string err;
   int64_t launches = 0;
+  bool use_flow = true;            // persistent dataflow recurrence (CPA_SVT_FLOW=0: one launch per step)
+  // profiling (cpa_svt_profile): event pairs per phase, resolved at read time
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_used;
+  double prof_ms[CPA_SVT_PH_COUNT] = {};
+  int64_t prof_n[CPA_SVT_PH_COUNT] = {};
 };
+
+namespace {
+// RAII: records an event pair around the launches of one phase when profiling.
+struct Phase {
+  cpa_svt_handle* h;
+  int ph;
+  cudaEvent_t e1 = nullptr;
+  Phase(cpa_svt_handle* h_, int ph_, int n = 1) : h(h_), ph(ph_) {
+    if (!h->prof) return;
+    cudaEvent_t e0 = take();
+    e1 = take();
+    cudaEventRecord(e0, h->stream);
+    h->ev_used.push_back({ph, {e0, e1}});
+    h->prof_n[ph] += n;
+  }
+  cudaEvent_t take() {
+    if (h->ev_pool.empty()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      return e;
+    }
+    cudaEvent_t e = h->ev_pool.back();
+    h->ev_pool.pop_back();
+    return e;
+  }
+  ~Phase() {
+    if (e1) cudaEventRecord(e1, h->stream);
+  }
+};
+}  // namespace
 
 #define CU(call)                                                                     \
   do {                                                                               \
@@ -181,6 +226,7 @@ cpa_svt_status cpa_svt_init(cpa_svt_handle** out, int device, void* cuda_stream,
   h->stream = (cudaStream_t)cuda_stream;
   h->rank = rank;
   h->world = world;
+  if (const char* f = getenv("CPA_SVT_FLOW")) h->use_flow = f[0] != '0';
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (e == cudaSuccess) e = cudaMalloc(&h->P, sizeof(SeriesParams));
@@ -220,7 +266,42 @@ cpa_svt_status cpa_svt_free(cpa_svt_handle* h) {
   cudaFree(h->d_c);
   cudaFree(h->ws);
   cudaFree(h->hx);
+  for (auto& u : h->ev_used) {
+    cudaEventDestroy(u.second.first);
+    cudaEventDestroy(u.second.second);
+  }
+  for (auto e : h->ev_pool) cudaEventDestroy(e);
   delete h;
+  return CPA_SVT_OK;
+}
+
+cpa_svt_status cpa_svt_profile(cpa_svt_handle* h, int enable) {
+  if (!h) return CPA_SVT_E_ARG;
+  if (enable) {
+    for (int i = 0; i < CPA_SVT_PH_COUNT; ++i) { h->prof_ms[i] = 0.0; h->prof_n[i] = 0; }
+    for (auto& u : h->ev_used) { h->ev_pool.push_back(u.second.first); h->ev_pool.push_back(u.second.second); }
+    h->ev_used.clear();
+  }
+  h->prof = enable != 0;
+  return CPA_SVT_OK;
+}
+
+cpa_svt_status cpa_svt_profile_read(cpa_svt_handle* h, double* ms, int64_t* launches) {
+  if (!h) return CPA_SVT_E_ARG;
+  CU(cudaSetDevice(h->device));
+  CU(cudaStreamSynchronize(h->stream));
+  for (auto& u : h->ev_used) {
+    float t = 0.f;
+    CU(cudaEventElapsedTime(&t, u.second.first, u.second.second));
+    h->prof_ms[u.first] += t;
+    h->ev_pool.push_back(u.second.first);
+    h->ev_pool.push_back(u.second.second);
+  }
+  h->ev_used.clear();
+  for (int i = 0; i < CPA_SVT_PH_COUNT; ++i) {
+    if (ms) ms[i] = h->prof_ms[i];
+    if (launches) launches[i] = h->prof_n[i];
+  }
   return CPA_SVT_OK;
 }
 
@@ -304,15 +385,20 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
   }
   const int64_t s = left ? m : n;
   const bool sharded = shard != CPA_SVT_SHARD_NONE && h->world > 1;
-  // workspace: G (s*s) | W_a (m*n) | W_b (m*n) | power scratch
+  // workspace: G (s*s) | W_a (m*n) | W_b (m*n) | power scratch | split-K partials | flow sync ints
+  // (G^2 and G^4 for the squared power iteration live in W_a / W_b: free until the recurrence)
   const size_t nG = (size_t)s * s, nW = (size_t)m * n, nPow = power_dense_scratch_doubles(s);
-  const size_t need = (nG + 2 * nW + nPow) * sizeof(double) + 256;
+  const size_t nPart = dense_flow_partial_doubles(m, n, h->num_sms);
+  const size_t nSync = dense_flow_sync_ints(m, n, K);
+  const size_t need = (nG + 2 * nW + nPow + nPart) * sizeof(double) + nSync * sizeof(int) + 256;
   cpa_svt_status st = grow(h, &h->ws, &h->ws_bytes, need);
   if (st != CPA_SVT_OK) return st;
   double* G = (double*)h->ws;
   double* Wa = G + nG;
   double* Wb = Wa + nW;
   double* pw = Wb + nW;
+  double* part = pw + nPow;
+  int* flow_sync = (int*)(part + nPart);
 
   const double* c_dev = nullptr;
   if (c) {
@@ -323,41 +409,74 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
   tm.start(info != nullptr, h->stream);
   int launches = 0;
   // Alg. 1 line 1: partial Gram of this shard
-  CU(dense_gram_f64(X, m, n, ldx, left, G, h->stream));
+  {
+    Phase p(h, CPA_SVT_PH_GRAM);
+    CU(dense_gram_f64(X, m, n, ldx, left, G, h->stream));
+  }
   ++launches;
   tm.mark();
   // exchange: G = sum_p G_p over NVLink (one all-reduce per shrinkage)
-  if (sharded) NC(g_nccl.AllReduce(G, G, nG, ncclDouble, ncclSum, h->comm, h->stream));
+  if (sharded) {
+    Phase p(h, CPA_SVT_PH_ALLREDUCE);
+    NC(g_nccl.AllReduce(G, G, nG, ncclDouble, ncclSum, h->comm, h->stream));
+  }
   tm.mark();
   // Alg. 1 lines 3-4: Lambda_max and coefficients, on the device
   if (lam->lambda_max > 0.0) {
+    Phase p(h, CPA_SVT_PH_POWER);
     CU(launch_series(h->P, *k, K, lam->safety, lam->lambda_max, nullptr, c_dev, h->stream));
   } else {
     if (s * (int64_t)sizeof(double) > 200 * 1024) return CPA_SVT_E_UNSUPPORTED;
-    CU(launch_power_dense(G, s, lam->power_iters, pw, h->bar, h->P, *k, K, lam->safety, c_dev, h->num_sms,
+    Phase p(h, CPA_SVT_PH_POWER);
+    // Repeated squaring: v_{T-1} ~ G^{T-1} v_0 is reached with (T-1)/4 products by
+    // c^4 G^4 (c = 2^-ilogb(max G_ii), exact) plus the remainder by G, then
+    // lambda_hat = ||G v_{T-1}|| -- the same quantity as T plain products (reading R6).
+    const double* G4 = nullptr;
+    if (power_use_squaring(s, lam->power_iters) && nW >= nG) {
+      double* sc = pw + 2 * s + 4096;  // scale slot inside the power scratch
+      CU(launch_diag_scale(G, s, sc, h->stream));
+      CU(dense_gram_f64(G, s, s, s, true, Wa, h->stream, sc));  // c^2 G^2
+      CU(dense_gram_f64(Wa, s, s, s, true, Wb, h->stream));     // c^4 G^4
+      launches += 3;
+      G4 = Wb;
+    }
+    CU(launch_power_dense(G, G4, s, lam->power_iters, pw, h->bar, h->P, *k, K, lam->safety, c_dev, h->num_sms,
                           h->stream));
   }
   ++launches;
-  if (sharded) NC(g_nccl.Broadcast(h->P, h->P, sizeof(SeriesParams), ncclChar, 0, h->comm, h->stream));
+  if (sharded) {
+    Phase p(h, CPA_SVT_PH_ALLREDUCE, 0);
+    NC(g_nccl.Broadcast(h->P, h->P, sizeof(SeriesParams), ncclChar, 0, h->comm, h->stream));
+  }
   tm.mark();
   // Alg. 1 lines 5-11 in the apply-to-X form
-  CU(dense_cheb_launch(left, true, m, n, G, X, ldx, nullptr, 0, K > 2 ? Wa : nullptr, n, Y, ldy, h->P, 1,
-                       h->stream));
-  ++launches;
-  for (int kk = 2; kk < K; ++kk) {
-    const double *src, *pp;
-    double* out;
-    int64_t ldsrc, ldpp;
-    if (kk == 2) {
-      src = Wa; ldsrc = n; pp = X; ldpp = ldx; out = Wb;
-    } else {
-      out = (kk & 1) ? Wa : Wb;      // W_k overwrites W_{k-2} in place
-      src = (kk & 1) ? Wb : Wa;
-      ldsrc = n; pp = out; ldpp = n;
-    }
-    if (kk == K - 1) out = nullptr;  // last W_k is never read again
-    CU(dense_cheb_launch(left, false, m, n, G, src, ldsrc, pp, ldpp, out, n, Y, ldy, h->P, kk, h->stream));
+  if (h->use_flow && K > 2) {
+    Phase p(h, CPA_SVT_PH_STEP);
+    CU(dense_cheb_flow(left, m, n, G, X, ldx, Wa, Wb, Y, ldy, h->P, K, flow_sync, part, h->num_sms, h->stream));
     ++launches;
+  } else {
+    {
+      Phase p(h, CPA_SVT_PH_INIT);
+      CU(dense_cheb_launch(left, true, m, n, G, X, ldx, nullptr, 0, K > 2 ? Wa : nullptr, n, Y, ldy, h->P, 1,
+                           h->stream));
+    }
+    ++launches;
+    for (int kk = 2; kk < K; ++kk) {
+      const double *src, *pp;
+      double* out;
+      int64_t ldsrc, ldpp;
+      if (kk == 2) {
+        src = Wa; ldsrc = n; pp = X; ldpp = ldx; out = Wb;
+      } else {
+        out = (kk & 1) ? Wa : Wb;      // W_k overwrites W_{k-2} in place
+        src = (kk & 1) ? Wb : Wa;
+        ldsrc = n; pp = out; ldpp = n;
+      }
+      if (kk == K - 1) out = nullptr;  // last W_k is never read again
+      Phase p(h, CPA_SVT_PH_STEP);
+      CU(dense_cheb_launch(left, false, m, n, G, src, ldsrc, pp, ldpp, out, n, Y, ldy, h->P, kk, h->stream));
+      ++launches;
+    }
   }
   tm.mark();
   h->launches += launches;
@@ -424,11 +543,15 @@ cpa_svt_status cpa_svt_apply_batched(cpa_svt_handle* h, int64_t batch, int m, in
   if (st != CPA_SVT_OK) return st;
   st = check_lambda(lam);
   if (st != CPA_SVT_OK) return st;
+  if (K > 128) return CPA_SVT_E_UNSUPPORTED;
   if (batch == 0) return CPA_SVT_OK;
   if (cudaSetDevice(h->device) != cudaSuccess) return CPA_SVT_E_CUDA;
   int launches = 0;
-  CU(launch_batched_f32(batch, m, n, X, Y, *k, K, lam->power_iters, lam->safety, lam->lambda_max, lambda_out,
-                        h->num_sms, h->stream, &launches));
+  {
+    Phase p(h, CPA_SVT_PH_BATCHED);
+    CU(launch_batched_f32(batch, m, n, X, Y, *k, K, lam->power_iters, lam->safety, lam->lambda_max, lambda_out,
+                          h->num_sms, h->stream, &launches));
+  }
   h->launches += launches;
   return CPA_SVT_OK;
 }

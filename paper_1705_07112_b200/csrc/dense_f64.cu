@@ -37,6 +37,7 @@ struct GemmArgs {
   const SeriesParams* P;
   int k;                        // coefficient index (STEP)
   int vec_a, vec_b;             // 16-byte loads allowed
+  const double* gscale;         // GRAM: optional device scalar multiplying the output (exact power of 2)
 };
 
 // Elements per stage of an operand whose global slab is OUTER x INNER (INNER contiguous).
@@ -51,7 +52,10 @@ struct OpLayout {
 };
 
 // Copy one OUTER x INNER slab starting at global (o0, i0); elements outside
-// [0, olim) x [0, ilim) are zero-filled.
+// [0, olim) x [0, ilim) are zero-filled.  16-byte chunks go through
+// cp.async.cg (L2 only); ragged or unaligned elements are loaded with ld.global.cg
+// and stored directly -- never through L1, because the recurrence rewrites
+// W in place while a persistent CTA may still hold old lines in its L1.
 template <class L>
 __device__ __forceinline__ void load_slab(double* s, const double* g, int64_t ld, int64_t o0, int64_t i0,
                                           int64_t olim, int64_t ilim, bool vec) {
@@ -67,51 +71,38 @@ __device__ __forceinline__ void load_slab(double* s, const double* g, int64_t ld
     if (vec && orow && gi + 1 < ilim) {
       cp_async16(dst, src, true);
     } else {
-      cp_async8(dst, orow && gi < ilim ? src : g, orow && gi < ilim);
-      cp_async8(dst + 1, orow && gi + 1 < ilim ? src + 1 : g, orow && gi + 1 < ilim);
+      dst[0] = orow && gi < ilim ? __ldcg(src) : 0.0;
+      dst[1] = orow && gi + 1 < ilim ? __ldcg(src + 1) : 0.0;
     }
   }
 }
 
-template <bool A_KC, bool B_KC, int MODE>
-__global__ void __launch_bounds__(NTHREADS) k_dmma_gemm(GemmArgs a) {
+// acc = A[m0:m0+64, :] * B[:, n0:n0+64] over the full Kd, 4-stage cp.async pipeline.
+// Ends with all stages drained and a CTA barrier (smem reusable on return).
+template <bool A_KC, bool B_KC>
+__device__ __forceinline__ void mainloop(const double* Ag, int64_t lda, const double* Bg, int64_t ldb, int64_t M,
+                                         int64_t N, int64_t Kd, int64_t m0, int64_t n0, bool vec_a, bool vec_b,
+                                         double* smem, double (&acc)[4][4][2], int kbeg = 0, int kend = -1) {
   using LA = OpLayout<A_KC, BM>;
   using LB = OpLayout<B_KC, BN>;
-  extern __shared__ __align__(16) double smem[];
   double* sA = smem;
   double* sB = smem + STAGES * LA::SIZE;
-
-  int tm, tn;
-  if (MODE == EPI_GRAM) {
-    // lower-triangular tile (tm >= tn) from the linear block index
-    const int b = blockIdx.x;
-    int r = (int)((sqrt(8.0 * b + 1.0) - 1.0) * 0.5);
-    while ((r + 1) * (r + 2) / 2 <= b) ++r;
-    while (r * (r + 1) / 2 > b) --r;
-    tm = r;
-    tn = b - r * (r + 1) / 2;
-  } else {
-    tm = blockIdx.x;
-    tn = blockIdx.y;
-  }
-  const int64_t m0 = (int64_t)tm * BM, n0 = (int64_t)tn * BN;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
-
-  double acc[4][4][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  const int nk = (int)((a.Kd + BKS - 1) / BKS);
+  if (kend < 0) kend = (int)((Kd + BKS - 1) / BKS);
+  const int nk = kend - kbeg;
   auto load_stage = [&](int kt, int st) {
-    const int64_t k0 = (int64_t)kt * BKS;
-    if (A_KC) load_slab<LA>(sA + st * LA::SIZE, a.A, a.lda, m0, k0, a.M, a.Kd, a.vec_a);
-    else      load_slab<LA>(sA + st * LA::SIZE, a.A, a.lda, k0, m0, a.Kd, a.M, a.vec_a);
-    if (B_KC) load_slab<LB>(sB + st * LB::SIZE, a.B, a.ldb, n0, k0, a.N, a.Kd, a.vec_b);
-    else      load_slab<LB>(sB + st * LB::SIZE, a.B, a.ldb, k0, n0, a.Kd, a.N, a.vec_b);
+    const int64_t k0 = (int64_t)(kbeg + kt) * BKS;
+    if (A_KC) load_slab<LA>(sA + st * LA::SIZE, Ag, lda, m0, k0, M, Kd, vec_a);
+    else      load_slab<LA>(sA + st * LA::SIZE, Ag, lda, k0, m0, Kd, M, vec_a);
+    if (B_KC) load_slab<LB>(sB + st * LB::SIZE, Bg, ldb, n0, k0, N, Kd, vec_b);
+    else      load_slab<LB>(sB + st * LB::SIZE, Bg, ldb, k0, n0, Kd, N, vec_b);
   };
 
 #pragma unroll
@@ -143,28 +134,23 @@ __global__ void __launch_bounds__(NTHREADS) k_dmma_gemm(GemmArgs a) {
     }
   }
   cp_async_wait<0>();
+  __syncthreads();
+}
 
-  // ---------------- epilogue -------------------------------------------------
-  if (MODE == EPI_GRAM) {
-    double* G = a.Wout;
-    const int64_t ld = a.ldwo;
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int64_t r = m0 + wm + i * 8 + g, c = n0 + wn + j * 8 + 2 * t + e;
-          if (r < a.M && c < a.N && r >= c) {
-            G[r * ld + c] = acc[i][j][e];
-            G[c * ld + r] = acc[i][j][e];
-          }
-        }
-    return;
-  }
-  const SeriesParams* P = a.P;
+// Fused recurrence epilogue on one 64x64 accumulator tile (Alg. 1 lines 5-11).
+//   init:  W_1 = (2/L) acc - X,                   Y  = c_0/2 X + c_1 W_1
+//   step:  W_k = (4/L) acc - 2 W_{k-1} - W_{k-2}, Y += c_k W_k
+// Wp = W_{k-1} (init: X), Wpp = W_{k-2}; Wout may alias Wpp (in place).  Loads
+// bypass L1 (ld.global.cg): other CTAs of a persistent launch rewrite W and Y.
+__device__ __forceinline__ void cheb_epilogue(const double (&acc)[4][4][2], int64_t m0, int64_t n0, int64_t M,
+                                              int64_t N, bool init, const double* Wp, int64_t ldwp,
+                                              const double* Wpp, int64_t ldwpp, double* Wout, int64_t ldwo,
+                                              double* Y, int64_t ldy, const SeriesParams* P, int k) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
   const double s2 = P->scale2;
-  if (MODE == EPI_INIT) {
+  if (init) {
     const double h0 = 0.5 * P->c[0], c1 = P->c[1];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
@@ -173,15 +159,15 @@ __global__ void __launch_bounds__(NTHREADS) k_dmma_gemm(GemmArgs a) {
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int64_t r = m0 + wm + i * 8 + g, c = n0 + wn + j * 8 + 2 * t + e;
-          if (r < a.M && c < a.N) {
-            const double x = a.Wp[r * a.ldwp + c];
-            const double w = s2 * acc[i][j][e] - x;          // W_1 = B_hat X
-            if (a.Wout) a.Wout[r * a.ldwo + c] = w;
-            a.Y[r * a.ldy + c] = h0 * x + c1 * w;           // Y = c0/2 W_0 + c1 W_1
+          if (r < M && c < N) {
+            const double x = __ldcg(Wp + r * ldwp + c);
+            const double w = s2 * acc[i][j][e] - x;  // W_1 = B_hat X
+            if (Wout) Wout[r * ldwo + c] = w;
+            Y[r * ldy + c] = h0 * x + c1 * w;       // Y = c0/2 W_0 + c1 W_1
           }
         }
   } else {
-    const double s4 = 2.0 * s2, ck = P->c[a.k];
+    const double s4 = 2.0 * s2, ck = P->c[k];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -189,15 +175,188 @@ __global__ void __launch_bounds__(NTHREADS) k_dmma_gemm(GemmArgs a) {
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int64_t r = m0 + wm + i * 8 + g, c = n0 + wn + j * 8 + 2 * t + e;
-          if (r < a.M && c < a.N) {
-            const double wp = a.Wp[r * a.ldwp + c];
-            const double wpp = a.Wpp[r * a.ldwpp + c];
+          if (r < M && c < N) {
+            const double wp = __ldcg(Wp + r * ldwp + c);
+            const double wpp = __ldcg(Wpp + r * ldwpp + c);
             const double w = s4 * acc[i][j][e] - 2.0 * wp - wpp;  // W_k = 2 B_hat W_{k-1} - W_{k-2}
-            if (a.Wout) a.Wout[r * a.ldwo + c] = w;
-            a.Y[r * a.ldy + c] += ck * w;                      // Y += c_k W_k
+            if (Wout) Wout[r * ldwo + c] = w;
+            Y[r * ldy + c] = __ldcg(Y + r * ldy + c) + ck * w;    // Y += c_k W_k
           }
         }
   }
+}
+
+// ---------------------------------------------------------------------------
+// Persistent dataflow kernel: the init and all K-2 steps in ONE launch.
+// Tiles are claimed in ticket order (step k, panel p, tile q); a tile of step
+// k waits only until its panel of step k-1 is complete (left: column panel of
+// W_{k-1} feeding the B operand; right: row panel feeding A), so SMs that
+// finish a step early start the next one and the 28-launch tail effect and
+// launch gaps disappear.  In-place W_k -> W_{k-2} is safe because every
+// reader of W_{k-2}'s panel belongs to step k-1, which is complete.
+// ---------------------------------------------------------------------------
+struct FlowArgs {
+  int64_t M, N, s;      // output M x N (shape of X); s = Gram side
+  const double* G;
+  const double* X;
+  int64_t ldx;
+  double* Wa;
+  double* Wb;
+  int64_t ldw;
+  double* Y;
+  int64_t ldy;
+  const SeriesParams* P;
+  int K;
+  int tiles_m, tiles_n;
+  int split;            // k-splits per tile (units per tile)
+  int* sync;            // [0] ticket | K * npanels panel counters | ntiles split counters
+  double* partial;      // ntiles * (split - 1) * 64 * 64 (split > 1)
+  int vec_x, vec_w, vec_g;
+};
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Unit = (step k, panel, tile-in-panel, k-split q); claimed in that order.
+// Splits q < split-1 publish partial sums; split split-1 waits for them, adds
+// all partials in the fixed order q = 0..split-1 (deterministic) and runs the
+// fused epilogue.  A unit of step k >= 2 first waits until its panel of
+// step k-1 is complete.
+template <bool LEFT>
+__global__ void __launch_bounds__(NTHREADS) k_cheb_flow(FlowArgs a) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ int s_ticket;
+  const int npanels = LEFT ? a.tiles_n : a.tiles_m;
+  const int ninner = LEFT ? a.tiles_m : a.tiles_n;
+  const int ntiles = a.tiles_m * a.tiles_n;
+  const int S = a.split;
+  const int per_step = ntiles * S;
+  const int total = (a.K - 1) * per_step;
+  int* panel_cnt = a.sync + 1;
+  int* split_cnt = a.sync + 1 + a.K * npanels;
+  const int nk = (int)((a.s + BKS - 1) / BKS);
+  for (;;) {
+    if (threadIdx.x == 0) s_ticket = atomicAdd(a.sync, 1);
+    __syncthreads();
+    const int tk = s_ticket;
+    if (tk >= total) break;
+    const int k = 1 + tk / per_step;
+    const int r = tk % per_step;
+    const int q = r % S;
+    const int tile = r / S;                 // panel-major tile id
+    const int panel = tile / ninner, inner = tile % ninner;
+    const int tm = LEFT ? inner : panel, tn = LEFT ? panel : inner;
+    if (threadIdx.x == 0 && k >= 2) {
+      const int* cnt = panel_cnt + (k - 1) * npanels + panel;
+      while (ld_acquire(cnt) < ninner) __nanosleep(64);
+    }
+    __syncthreads();
+    // W_{k-1}: k=1 -> X; else (k-1 odd ? Wa : Wb).  W_k -> (k odd ? Wa : Wb); W_{k-2} aliases W_k (k >= 3).
+    const double* src = k == 1 ? a.X : (((k - 1) & 1) ? a.Wa : a.Wb);
+    const int64_t ldsrc = k == 1 ? a.ldx : a.ldw;
+    const bool vsrc = k == 1 ? a.vec_x : a.vec_w;
+    const int64_t m0 = (int64_t)tm * BM, n0 = (int64_t)tn * BN;
+    const int kb = (int)((int64_t)nk * q / S), ke = (int)((int64_t)nk * (q + 1) / S);
+    double acc[4][4][2];
+    if (LEFT) mainloop<false, false>(a.G, a.s, src, ldsrc, a.M, a.N, a.s, m0, n0, a.vec_g, vsrc, smem, acc, kb, ke);
+    else      mainloop<true, false>(src, ldsrc, a.G, a.s, a.M, a.N, a.s, m0, n0, vsrc, a.vec_g, smem, acc, kb, ke);
+    if (S > 1) {
+      // splits q < S-1 publish partial sums; split S-1 (the last ticket of the tile,
+      // so it never waits on a later one) adds them in the fixed order q = 0..S-1.
+      double* slot = a.partial + (int64_t)tile * (S - 1) * (BM * BN);
+      if (q < S - 1) {
+        double* mine = slot + (int64_t)q * (BM * BN);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) __stcg(mine + ((i * 4 + j) * 2 + e) * NTHREADS + threadIdx.x, acc[i][j][e]);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          __threadfence();
+          atomicAdd(split_cnt + tile, 1);
+        }
+        continue;
+      }
+      if (threadIdx.x == 0) {
+        while (ld_acquire(split_cnt + tile) < (S - 1) * k) __nanosleep(32);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int off = ((i * 4 + j) * 2 + e) * NTHREADS + threadIdx.x;
+            double sum = __ldcg(slot + off);
+            for (int p = 1; p < S - 1; ++p) sum += __ldcg(slot + (int64_t)p * (BM * BN) + off);
+            acc[i][j][e] = sum + acc[i][j][e];
+          }
+    }
+    double* out = (k & 1) ? a.Wa : a.Wb;
+    const double* pp = k == 2 ? a.X : out;
+    const int64_t ldpp = k == 2 ? a.ldx : a.ldw;
+    if (k == a.K - 1) out = nullptr;
+    cheb_epilogue(acc, m0, n0, a.M, a.N, k == 1, src, ldsrc, pp, ldpp, out, a.ldw, a.Y, a.ldy, a.P, k);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(panel_cnt + k * npanels + panel, 1);
+    }
+  }
+}
+
+template <bool A_KC, bool B_KC, int MODE>
+__global__ void __launch_bounds__(NTHREADS) k_dmma_gemm(GemmArgs a) {
+  extern __shared__ __align__(16) double smem[];
+  int tm, tn;
+  if (MODE == EPI_GRAM) {
+    // lower-triangular tile (tm >= tn) from the linear block index
+    const int b = blockIdx.x;
+    int r = (int)((sqrt(8.0 * b + 1.0) - 1.0) * 0.5);
+    while ((r + 1) * (r + 2) / 2 <= b) ++r;
+    while (r * (r + 1) / 2 > b) --r;
+    tm = r;
+    tn = b - r * (r + 1) / 2;
+  } else {
+    tm = blockIdx.x;
+    tn = blockIdx.y;
+  }
+  const int64_t m0 = (int64_t)tm * BM, n0 = (int64_t)tn * BN;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+
+  double acc[4][4][2];
+  mainloop<A_KC, B_KC>(a.A, a.lda, a.B, a.ldb, a.M, a.N, a.Kd, m0, n0, a.vec_a, a.vec_b, smem, acc);
+
+  // ---------------- epilogue -------------------------------------------------
+  if (MODE == EPI_GRAM) {
+    double* G = a.Wout;
+    const int64_t ld = a.ldwo;
+    const double sc = a.gscale ? *a.gscale : 1.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t r = m0 + wm + i * 8 + g, c = n0 + wn + j * 8 + 2 * t + e;
+          if (r < a.M && c < a.N && r >= c) {
+            const double v = acc[i][j][e] * sc;
+            G[r * ld + c] = v;
+            G[c * ld + r] = v;
+          }
+        }
+    return;
+  }
+  cheb_epilogue(acc, m0, n0, a.M, a.N, MODE == EPI_INIT, a.Wp, a.ldwp, a.Wpp, a.ldwpp, a.Wout, a.ldwo, a.Y, a.ldy,
+                a.P, a.k);
 }
 
 template <bool A_KC, bool B_KC, int MODE>
@@ -222,8 +381,9 @@ static inline bool aligned16(const void* p, int64_t ld) {
 
 // G (s x s, ld s) = X X^T (left, s = m) or X^T X (right, s = n); X m x n row-major.
 cudaError_t dense_gram_f64(const double* X, int64_t m, int64_t n, int64_t ldx, bool left, double* G,
-                           cudaStream_t st) {
+                           cudaStream_t st, const double* gscale) {
   GemmArgs a{};
+  a.gscale = gscale;
   if (left) {  // G(i,j) = sum_l X[i][l] X[j][l]: A(m,k)=X[m][k] (k contig), B(k,n)=X[n][k] (k contig)
     a.M = m; a.N = m; a.Kd = n;
     a.A = X; a.lda = ldx; a.B = X; a.ldb = ldx;
@@ -263,6 +423,61 @@ cudaError_t dense_cheb_launch(bool left, bool init, int64_t m, int64_t n, const 
   if (m == 0 || n == 0) return cudaSuccess;
   if (left) return init ? launch<false, false, EPI_INIT>(a, st) : launch<false, false, EPI_STEP>(a, st);
   return init ? launch<true, false, EPI_INIT>(a, st) : launch<true, false, EPI_STEP>(a, st);
+}
+
+// Whole recurrence (init + K-2 steps) in one persistent launch.
+// k-split per tile: enough units per step to spread over every SM slot
+// (c2: 256 tiles x 4 = 1024 units), at least 4 k-slabs per unit.
+static int flow_split(int64_t m, int64_t n, int64_t s, int num_sms) {
+  const int64_t tiles = ((m + BM - 1) / BM) * ((n + BN - 1) / BN);
+  const int64_t nk = (s + BKS - 1) / BKS;
+  int split = 1;
+  while (split < 8 && tiles * split < 6 * num_sms && nk / (2 * split) >= 4) split *= 2;
+  return split;
+}
+
+size_t dense_flow_sync_ints(int64_t m, int64_t n, int K) {
+  const int64_t tm = (m + BM - 1) / BM, tn = (n + BN - 1) / BN;
+  return (size_t)(1 + (int64_t)K * (tm > tn ? tm : tn) + tm * tn);
+}
+
+size_t dense_flow_partial_doubles(int64_t m, int64_t n, int num_sms) {
+  const int64_t s = m <= n ? m : n;
+  const int split = flow_split(m, n, s, num_sms);
+  const int64_t tiles = ((m + BM - 1) / BM) * ((n + BN - 1) / BN);
+  return split > 1 ? (size_t)(tiles * (split - 1) * BM * BN) : 0;
+}
+
+cudaError_t dense_cheb_flow(bool left, int64_t m, int64_t n, const double* G, const double* X, int64_t ldx,
+                            double* Wa, double* Wb, double* Y, int64_t ldy, const SeriesParams* P, int K, int* sync,
+                            double* partial, int num_sms, cudaStream_t st) {
+  if (m == 0 || n == 0) return cudaSuccess;
+  FlowArgs a{};
+  a.M = m; a.N = n; a.s = left ? m : n;
+  a.G = G; a.X = X; a.ldx = ldx; a.Wa = Wa; a.Wb = Wb; a.ldw = n; a.Y = Y; a.ldy = ldy; a.P = P; a.K = K;
+  a.tiles_m = (int)((m + BM - 1) / BM);
+  a.tiles_n = (int)((n + BN - 1) / BN);
+  a.split = flow_split(m, n, a.s, num_sms);
+  a.sync = sync;
+  a.partial = partial;
+  a.vec_x = aligned16(X, ldx); a.vec_w = aligned16(Wa, n) && aligned16(Wb, n); a.vec_g = aligned16(G, a.s);
+  cudaError_t e = cudaMemsetAsync(sync, 0, dense_flow_sync_ints(m, n, K) * sizeof(int), st);
+  if (e != cudaSuccess) return e;
+  using LA = OpLayout<false, BM>;
+  using LB = OpLayout<false, BN>;
+  using LA2 = OpLayout<true, BM>;
+  const size_t smem = (size_t)STAGES * ((left ? LA::SIZE : LA2::SIZE) + LB::SIZE) * sizeof(double);
+  auto fn = left ? k_cheb_flow<true> : k_cheb_flow<false>;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, NTHREADS, smem);
+  if (e != cudaSuccess) return e;
+  int64_t total = (int64_t)(K - 1) * a.tiles_m * a.tiles_n * a.split;
+  int64_t grid = (int64_t)num_sms * (per_sm > 0 ? per_sm : 1);
+  if (grid > total) grid = total;
+  fn<<<(unsigned)grid, NTHREADS, smem, st>>>(a);
+  return cudaGetLastError();
 }
 
 }  // namespace cpa

@@ -63,11 +63,13 @@ __global__ void k_series(SeriesParams* P, cpa_svt_kernel kern, int K, double saf
 
 struct PowerArgs {
   const double* G;
+  const double* G4;  // c^4 G^4 (nullable): first q products use it
+  int q;             // products by G4
   int64_t s;
   int T;
   double* ubuf;      // 2 * s
   double* part;      // 2 * gridDim.x
-  unsigned int* bar; // [count, gen]
+  unsigned int* bar; // monotonic arrival counter (zeroed before the launch)
   SeriesParams* P;
   cpa_svt_kernel kern;
   int K;
@@ -83,53 +85,85 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+__device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_add(unsigned int* p, unsigned int v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+
 __global__ void __launch_bounds__(256) k_power_dense(PowerArgs a) {
   extern __shared__ __align__(16) double psm[];
   __shared__ double s_warp[8];
   __shared__ double s_norm;
   const int64_t s = a.s;
-  double* sv = psm;               // v (s doubles)
+  double* sv = psm;               // v_{t-1} (s doubles)
   double* sg = psm + s;           // cached rows (rows_per_cta * s) if cache_rows
   const int64_t r0 = (int64_t)blockIdx.x * a.rows_per_cta;
   const int64_t r1 = min(s, r0 + a.rows_per_cta);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  const unsigned int nb = gridDim.x;
+  // products: q by G4 (cached when present), then T - 4q by G; the last one gives lambda_hat
+  const double* Gc = a.q > 0 ? a.G4 : a.G;  // the matrix whose rows are cached
+  const int niter = a.T - 3 * a.q;
   if (a.cache_rows) {
-    for (int64_t e = threadIdx.x; e < (r1 - r0) * s; e += blockDim.x) sg[e] = a.G[r0 * s + e];
+    for (int64_t e = threadIdx.x; e < (r1 - r0) * s; e += blockDim.x) sg[e] = Gc[r0 * s + e];
   }
   const double v0 = 1.0 / sqrt((double)s);
-  double inv = 0.0;
+  for (int64_t j = threadIdx.x; j < s; j += blockDim.x) sv[j] = v0;
+  __syncthreads();
   double lam = 0.0;
-  for (int t = 0; t < a.T; ++t) {
-    // stage v_{t-1} = u_{t-1} / ||u_{t-1}|| (v_0 = 1/sqrt(s))
-    const double* up = a.ubuf + ((t + 1) & 1) * s;
-    for (int64_t j = threadIdx.x; j < s; j += blockDim.x) sv[j] = t == 0 ? v0 : __ldcg(up + j) * inv;
-    __syncthreads();
+  double inv = 1.0;  // 1/||u_{t-1}||, folded into this product (v_{t-1} = u_{t-1} * inv)
+  for (int t = 0; t < niter; ++t) {
+    const bool use4 = t < a.q;
+    const double* Gt = use4 ? a.G4 : a.G;
+    const bool cached = a.cache_rows && (use4 || a.q == 0);
+    // u_t = G v_{t-1}: one warp per row, 4 independent partial sums per lane
     double mysq = 0.0;
     for (int64_t r = r0 + warp; r < r1; r += nwarps) {
-      const double* grow = a.cache_rows ? sg + (r - r0) * s : a.G + r * s;
-      double d = 0.0;
-      for (int64_t j = lane; j < s; j += 32) d += grow[j] * sv[j];
-      d = warp_sum(d);
+      const double* grow = cached ? sg + (r - r0) * s : Gt + r * s;
+      double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+      int64_t j = lane;
+      for (; j + 96 < s; j += 128) {
+        d0 = fma(grow[j], sv[j], d0);
+        d1 = fma(grow[j + 32], sv[j + 32], d1);
+        d2 = fma(grow[j + 64], sv[j + 64], d2);
+        d3 = fma(grow[j + 96], sv[j + 96], d3);
+      }
+      for (; j < s; j += 32) d0 = fma(grow[j], sv[j], d0);
+      const double d = warp_sum((d0 + d1) + (d2 + d3)) * inv;
       if (lane == 0) a.ubuf[(t & 1) * s + r] = d;
-      mysq += d * d;  // identical in all lanes
+      mysq = fma(d, d, mysq);  // identical in all lanes
     }
     if (lane == 0) s_warp[warp] = mysq;
     __syncthreads();
     if (threadIdx.x == 0) {
       double p = 0.0;
       for (int w = 0; w < nwarps; ++w) p += s_warp[w];
-      a.part[(t & 1) * gridDim.x + blockIdx.x] = p;
-    }
-    grid_barrier(a.bar, a.bar + 1, gridDim.x);
-    if (threadIdx.x == 0) {
-      double ss = 0.0;
-      const double* pp = a.part + (t & 1) * gridDim.x;
-      for (unsigned b = 0; b < gridDim.x; ++b) ss += __ldcg(pp + b);
-      s_norm = sqrt(ss);
+      a.part[(t & 1) * nb + blockIdx.x] = p;
+      // arrive (release, cumulative over the bar.sync above): publishes u_t and the partial
+      red_release_add(a.bar, 1u);
+      const unsigned int target = nb * (unsigned)(t + 1);
+      while (ld_acquire_u32(a.bar) < target) {
+      }
     }
     __syncthreads();
+    // ||u_t||: warp 0 re-sums the partials in a fixed order (identical in every CTA)
+    if (warp == 0) {
+      const double* pp = a.part + (t & 1) * nb;
+      double q = 0.0;
+      for (unsigned b = lane; b < nb; b += 32) q += __ldcg(pp + b);
+      q = warp_sum(q);
+      if (lane == 0) s_norm = sqrt(q);
+    }
+    // stage u_t; v_t = u_t / ||u_t|| is applied inside the next product
+    const double* up = a.ubuf + (t & 1) * s;
+    for (int64_t j = threadIdx.x; j < s; j += blockDim.x) sv[j] = __ldcg(up + j);
+    __syncthreads();
     lam = s_norm;
-    if (!(lam > kDegenerateLambda)) { lam = 0.0; break; }
+    if (!(lam > kDegenerateLambda) || !(lam < 1e300)) { lam = lam < 1e300 ? 0.0 : lam; break; }
     inv = 1.0 / lam;
   }
   if (blockIdx.x == 0) compute_series(a.P, a.kern, a.K, a.safety, lam, a.c_given);
@@ -142,30 +176,75 @@ cudaError_t launch_series(SeriesParams* P, const cpa_svt_kernel& k, int K, doubl
 }
 
 // Scratch needed by launch_power_dense (doubles): 2 s + 2 * 148 * 8, plus 2 uints.
-size_t power_dense_scratch_doubles(int64_t s) { return (size_t)(2 * s + 2 * 2048); }
+size_t power_dense_scratch_doubles(int64_t s) { return (size_t)(2 * s + 4096 + 8); }
 
-cudaError_t launch_power_dense(const double* G, int64_t s, int T, double* scratch, unsigned int* bar,
-                               SeriesParams* P, const cpa_svt_kernel& k, int K, double safety,
+// c = 2^-e with e = ilogb(max_i G_ii): G_ii <= lambda_max <= s * max_i G_ii, so
+// c^4 G^4 has its dominant eigenvalue in [1/16, 16 s^4]: no overflow/underflow.
+__global__ void k_diag_scale(const double* G, int64_t s, double* scale) {
+  __shared__ double red[256];
+  double mx = 0.0;
+  for (int64_t i = threadIdx.x; i < s; i += blockDim.x) mx = fmax(mx, G[i * s + i]);
+  red[threadIdx.x] = mx;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double m = red[0];
+    const int e = (m > 0.0 && isfinite(m)) ? ilogb(m) : 0;
+    scale[0] = ldexp(1.0, -2 * e);  // applied to G^2 (one factor c^2)
+  }
+}
+
+cudaError_t launch_diag_scale(const double* G, int64_t s, double* scale, cudaStream_t st) {
+  k_diag_scale<<<1, 256, 0, st>>>(G, s, scale);
+  return cudaGetLastError();
+}
+
+// Squaring pays when two s^3 products cost less than the ~3T/4 products saved,
+// each of which is latency-bound (~2.5 us) for small s.
+bool power_use_squaring(int64_t s, int T) {
+  if (T < 16) return false;
+  const double gemm_us = 2.0 * (double)s * s * s / 25e12 * 1e6;
+  const double iter_us = fmax(2.5, 8.0 * (double)s * s / 5e12 * 1e6);
+  return gemm_us < 0.75 * T * iter_us;
+}
+
+cudaError_t launch_power_dense(const double* G, const double* G4, int64_t s, int T, double* scratch,
+                               unsigned int* bar, SeriesParams* P, const cpa_svt_kernel& k, int K, double safety,
                                const double* c_given, int num_sms, cudaStream_t st) {
   PowerArgs a{};
   a.G = G; a.s = s; a.T = T;
+  a.G4 = G4;
+  a.q = G4 ? (T - 1) / 4 : 0;
   a.ubuf = scratch; a.part = scratch + 2 * s;
   a.bar = bar; a.P = P; a.kern = k; a.K = K; a.safety = safety; a.c_given = c_given;
-  int grid = (int)(s < num_sms ? s : num_sms);
-  if (grid < 1) grid = 1;
-  if (grid > 1024) grid = 1024;
-  a.rows_per_cta = (int)((s + grid - 1) / grid);
-  grid = (int)((s + a.rows_per_cta - 1) / a.rows_per_cta);
+  // Fewest CTAs whose rows of G fit in shared memory (fewer arrivals per
+  // barrier); otherwise one CTA per SM streaming its rows from L2/HBM.
   const size_t budget = 200 * 1024;
   size_t smem = (size_t)s * sizeof(double);
   if (smem > budget) return cudaErrorInvalidValue;  // s > 25600 not supported by this kernel
-  const size_t cached = smem + (size_t)a.rows_per_cta * s * sizeof(double);
-  a.cache_rows = cached <= budget;
-  if (a.cache_rows) smem = cached;
+  int64_t rows_fit = (int64_t)((budget - smem) / ((size_t)s * sizeof(double)));
+  int64_t grid;
+  if (rows_fit >= 1 && (s + rows_fit - 1) / rows_fit <= num_sms) {
+    int64_t g0 = (s + rows_fit - 1) / rows_fit;
+    grid = g0;
+    a.cache_rows = 1;
+  } else {
+    grid = s < num_sms ? s : num_sms;
+    a.cache_rows = 0;
+  }
+  if (grid < 1) grid = 1;
+  a.rows_per_cta = (int)((s + grid - 1) / grid);
+  grid = (s + a.rows_per_cta - 1) / a.rows_per_cta;
+  if (a.cache_rows) smem += (size_t)a.rows_per_cta * s * sizeof(double);
+  cudaError_t e0 = cudaMemsetAsync(bar, 0, sizeof(unsigned int), st);
+  if (e0 != cudaSuccess) return e0;
   cudaError_t e = cudaFuncSetAttribute(k_power_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   void* args[] = {&a};
-  return cudaLaunchCooperativeKernel((void*)k_power_dense, dim3(grid), dim3(256), args, smem, st);
+  return cudaLaunchCooperativeKernel((void*)k_power_dense, dim3((unsigned)grid), dim3(256), args, smem, st);
 }
 
 }  // namespace cpa

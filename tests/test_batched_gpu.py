@@ -1,0 +1,73 @@
+"""Parity of the batched fp32 CUDA path (one CTA per matrix, whole Alg. 1 on chip)
+with the fp64 oracle run per matrix on the fp32-rounded inputs (reading R15).
+
+Bar (north_star): relative Frobenius error <= 1e-4 on the fp32 path, whole batch.
+"""
+
+import numpy as np
+import pytest
+
+import oracle as O
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+TOL32 = 1e-4
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    assert torch.cuda.is_available()
+    import paper_1705_07112_b200 as P
+    h = P.Handle(0)
+    yield torch, P, h
+    h.close()
+
+
+def _run(env, Xb, kern, K, T=30, **kw):
+    torch, P, h = env
+    Xd = torch.from_numpy(np.ascontiguousarray(Xb, dtype=np.float32)).cuda()
+    lam = torch.empty(Xb.shape[0], dtype=torch.float32, device="cuda")
+    Y = h.apply_batched(Xd, kern, K, T=T, lambda_out=lam, **kw)
+    torch.cuda.synchronize()
+    return Y.cpu().numpy().astype(np.float64), lam.cpu().numpy()
+
+
+def test_config3_parity(env):
+    cfg = W.CONFIGS["c3"]
+    Xb = W.gen_c3(batch=512)
+    Y, lam = _run(env, Xb, cfg["kernel"], cfg["K"], T=cfg["T"])
+    Yo, lo = O.cpa_shrink_batched(Xb.astype(np.float64), O.Kernel(**cfg["kernel"]), cfg["K"], T=cfg["T"])
+    err = O.rel_fro(Y, Yo)
+    per = max(O.rel_fro(Y[b], Yo[b]) for b in range(Xb.shape[0]))
+    assert err <= TOL32, (err, per)
+    assert np.max(np.abs(lam - lo) / lo) < 1e-5
+
+
+@pytest.mark.parametrize("shape", [(64, 48), (48, 64), (7, 33), (33, 7), (1, 1), (64, 64), (17, 17), (64, 1)])
+@pytest.mark.parametrize("kind,K", [("soft", 2), ("soft", 20), ("hard", 7), ("wsoft", 12)])
+def test_batched_shapes(env, shape, kind, K):
+    rng = np.random.default_rng(shape[0] * 100 + shape[1] + K)
+    Xb = rng.standard_normal((37,) + shape).astype(np.float32)
+    kern = {"kind": kind, "tau": 0.3, "tau_relative": True, "w_c": 2.0, "w_shift": 0.0, "w_eps": 1e-6}
+    Y, _ = _run(env, Xb, kern, K, T=30)
+    Yo, _ = O.cpa_shrink_batched(Xb.astype(np.float64), O.Kernel(**kern), K, T=30)
+    assert O.rel_fro(Y, Yo) <= TOL32
+
+
+def test_batched_lambda_override_and_zero(env):
+    Xb = np.zeros((5, 20, 30), dtype=np.float32)
+    Xb[1] = np.random.default_rng(1).standard_normal((20, 30))
+    Y, lam = _run(env, Xb, {"kind": "soft", "tau": 0.5}, 10)
+    assert not Y[0].any() and not Y[2:].any() and Y[1].any()
+    Y2, lam2 = _run(env, Xb[1:2], {"kind": "soft", "tau": 0.5}, 10, lambda_max=500.0)
+    Yo = O.cpa_shrink(Xb[1].astype(np.float64), O.Kernel("soft", tau=0.5), 10, lam=500.0)
+    assert O.rel_fro(Y2[0], Yo) <= TOL32 and abs(lam2[0] - 500.0) < 1e-3
+
+
+def test_batched_deterministic(env):
+    Xb = W.gen_c3(batch=300, seed=3)
+    cfg = W.CONFIGS["c3"]
+    a, _ = _run(env, Xb, cfg["kernel"], cfg["K"])
+    b, _ = _run(env, Xb, cfg["kernel"], cfg["K"])
+    assert np.array_equal(a, b)

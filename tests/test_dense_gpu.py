@@ -167,3 +167,26 @@ def test_bad_arguments(env):
     with pytest.raises(P.CpaSvtError) as e:
         h.apply(X, {"kind": "soft", "tau": 1.0}, 5, Y=X)
     assert e.value.status == 1
+
+
+@pytest.mark.parametrize("shape,K", [((1024, 1024), 30), ((300, 70), 9), ((65, 200), 7), ((129, 1000), 5)])
+def test_flow_kernel_matches_per_step(env, shape, K):
+    """The persistent dataflow recurrence (split-K when a step has few tiles) and
+    the one-launch-per-step path differ only in the order of the k-sums."""
+    import os
+    torch, P, _ = env
+    X = W.gen_c2(m=shape[0], n=shape[1], seed=7)
+    kern = {"kind": "soft", "tau": 0.05, "tau_relative": True}
+    Xd = torch.from_numpy(X).cuda()
+    out = {}
+    for flow in ("1", "0"):
+        os.environ["CPA_SVT_FLOW"] = flow
+        try:
+            h2 = P.Handle(0)
+            out[flow] = h2.apply(Xd, kern, K, T=50).cpu().numpy()
+            h2.close()
+        finally:
+            os.environ.pop("CPA_SVT_FLOW", None)
+    assert O.rel_fro(out["1"], out["0"]) <= 1e-13
+    ref = O.cpa_shrink(X, O.Kernel(**kern), K, T=50)
+    assert O.rel_fro(out["1"], ref) <= TOL64 and O.rel_fro(out["0"], ref) <= TOL64
