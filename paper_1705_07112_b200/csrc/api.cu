@@ -40,12 +40,11 @@ cudaError_t launch_batched_f32(int64_t batch, int m, int n, const float* X, floa
                                int K, int T, double safety, double lam_override, float* lambda_out,
                                int num_sms, cudaStream_t st, int* launches);
 // sparse_f64.cu
-struct SparseWork;
 cudaError_t sparse_apply(int64_t m, int64_t n, int64_t nnz, const int64_t* row_ptr, const int32_t* col,
                          const double* val, int64_t row_begin, int64_t row_end, double* Y, int64_t ldy,
                          const cpa_svt_kernel& k, int K, int T, double safety, double lam_override,
                          SeriesParams* P, void* ws, size_t ws_bytes, size_t* ws_needed, int num_sms,
-                         cudaStream_t st, int* launches);
+                         cudaStream_t st, int* launches, SparsePhaseHook hook, void* hook_ctx);
 }  // namespace cpa
 
 using namespace cpa;
@@ -130,6 +129,17 @@ struct Phase {
     if (e1) cudaEventRecord(e1, h->stream);
   }
 };
+// begin/end hook for phases spanning many launches (sparse path)
+void phase_hook(void* ctx, int ph, int begin) {
+  cpa_svt_handle* h = (cpa_svt_handle*)ctx;
+  if (!h->prof) return;
+  if (begin) {
+    Phase p(h, ph);         // records the start event and reserves the pair ...
+    p.e1 = nullptr;         // ... but the end event is recorded by the matching end call
+  } else {
+    cudaEventRecord(h->ev_used.back().second.second, h->stream);
+  }
+}
 }  // namespace
 
 #define CU(call)                                                                     \
@@ -571,14 +581,14 @@ cpa_svt_status cpa_svt_apply_csr(cpa_svt_handle* h, int64_t m, int64_t n, int64_
   if (cudaSetDevice(h->device) != cudaSuccess) return CPA_SVT_E_CUDA;
   size_t need = 0;
   CU(sparse_apply(m, n, nnz, row_ptr, col, val, row_begin, row_end, Y, ldy, *k, K, lam->power_iters, lam->safety,
-                  lam->lambda_max, h->P, nullptr, 0, &need, h->num_sms, h->stream, nullptr));
+                  lam->lambda_max, h->P, nullptr, 0, &need, h->num_sms, h->stream, nullptr, nullptr, nullptr));
   st = grow(h, &h->ws, &h->ws_bytes, need);
   if (st != CPA_SVT_OK) return st;
   PhaseTimer tm;
   tm.start(info != nullptr, h->stream);
   int launches = 0;
   CU(sparse_apply(m, n, nnz, row_ptr, col, val, row_begin, row_end, Y, ldy, *k, K, lam->power_iters, lam->safety,
-                  lam->lambda_max, h->P, h->ws, h->ws_bytes, &need, h->num_sms, h->stream, &launches));
+                  lam->lambda_max, h->P, h->ws, h->ws_bytes, &need, h->num_sms, h->stream, &launches, phase_hook, h));
   tm.mark();
   h->launches += launches;
   st = fill_info(h, info, lam, 1);

@@ -25,6 +25,9 @@ struct SeriesParams {
   double c[CPA_SVT_KMAX];
 };
 
+// Profiling hook for multi-kernel phases: begin = 1 before, 0 after the launches.
+typedef void (*SparsePhaseHook)(void* ctx, int phase, int begin);
+
 // ---- the response h(x) of PAPER.md:496-519 (host and device) --------------
 __host__ __device__ inline double h_response(const cpa_svt_kernel& k, double x, double tau) {
   const double r = sqrt(x);

@@ -1,10 +1,336 @@
-// placeholder: sparse CSR path (next)
+// Sparse path (BASELINE configs[3]): X is m x n CSR fp64; Y = X H_hat(X^T X)
+// with the n x n Gram never formed (PAPER.md:278-307 identity, sparsity
+// motivation PAPER.md:316-334).  Right-apply recurrence, one SpMM pair per step:
+//
+//   Z       = W_{k-1} X^T                                   (rows x m, dense)
+//   W_k     = (4/L) Z X - 2 W_{k-1} - W_{k-2},  Y += c_k W_k   (fused epilogue)
+//   init:   W_1 = (2/L) (X X^T)|rows X - X,  Y = c_0/2 X + c_1 W_1
+//
+// Layout: this rank's rows [row_begin, row_end) are cut into blocks of 32
+// rows; every dense operand (W, Y, Z) is stored block-interleaved --
+// element (i, c) of block b at ((b * C + c) * 32 + i%32) -- so one warp owns a
+// block row and each gathered column c is one coalesced 256-byte load, and
+// rows of a block never interact (the recurrence is row-independent).  Kernels
+// launch block-major, so the gathered W (or Z) block stays L2-resident.
+// Sums run in a fixed order (CSR row order / sorted CSC column order): the
+// result is deterministic.
+//
+// Lambda_max: power iteration on the m-side, v -> X (X^T v) (reading R4), two
+// SpMVs and a deterministic two-level norm per step.
+#include <algorithm>
+
+#include <cub/cub.cuh>
+
 #include "common.cuh"
+
 namespace cpa {
-cudaError_t sparse_apply(int64_t, int64_t, int64_t, const int64_t*, const int32_t*, const double*, int64_t, int64_t,
-                         double*, int64_t, const cpa_svt_kernel&, int, int, double, double, SeriesParams*, void*,
-                         size_t, size_t* need, int, cudaStream_t, int*) {
-  *need = 0;
-  return cudaErrorNotSupported;
+
+constexpr int RB = 32;          // rows per interleaved block (= warp width)
+constexpr int SP_WARPS = 8;     // warps per CTA in the SpMM kernels
+
+__device__ __forceinline__ double warp_sum_sp(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
 }
+
+// ---------------------------------------------------------------- CSC build
+__global__ void k_col_count(const int32_t* col, int64_t nnz, int* cnt) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(cnt + col[e], 1);
+}
+__global__ void k_col_fill(const int64_t* row_ptr, const int32_t* col, const double* val, int64_t m,
+                           const int64_t* cptr, int* cursor, int32_t* crow, double* cval) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+      const int c = col[e];
+      const int64_t p = cptr[c] + atomicAdd(cursor + c, 1);
+      crow[p] = (int32_t)i;
+      cval[p] = val[e];
+    }
+  }
+}
+// sort each column's (row, val) pairs by row (insertion sort, ~nnz/n entries): fixed summation order
+__global__ void k_col_sort(const int64_t* cptr, int64_t n, int32_t* crow, double* cval) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = cptr[c], e = cptr[c + 1];
+    for (int64_t p = b + 1; p < e; ++p) {
+      const int32_t r = crow[p];
+      const double v = cval[p];
+      int64_t q = p - 1;
+      while (q >= b && crow[q] > r) {
+        crow[q + 1] = crow[q];
+        cval[q + 1] = cval[q];
+        --q;
+      }
+      crow[q + 1] = r;
+      cval[q + 1] = v;
+    }
+  }
+}
+__global__ void k_widen(const int* cnt, int64_t n, int64_t* out) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x)
+    out[c] = cnt[c];
+}
+
+// ---------------------------------------------------------------- power iteration
+// u = X^T v (n-vector) via the sorted CSC; one thread per column
+__global__ void k_spmv_t(const int64_t* cptr, const int32_t* crow, const double* cval, int64_t n, const double* v,
+                         const double* scale, double* u) {
+  const double sc = scale ? *scale : 1.0;
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int64_t e = cptr[c]; e < cptr[c + 1]; ++e) s = fma(cval[e], v[crow[e]], s);
+    u[c] = s * sc;
+  }
+}
+// y = X t (m-vector) via CSR; one warp per row; per-block partial sums of y^2
+__global__ void k_spmv(const int64_t* row_ptr, const int32_t* col, const double* val, int64_t m, const double* t,
+                       double* y, double* part) {
+  __shared__ double ws[SP_WARPS];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double sq = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)SP_WARPS + warp; i < m; i += (int64_t)gridDim.x * SP_WARPS) {
+    double s = 0.0;
+    for (int64_t e = row_ptr[i] + lane; e < row_ptr[i + 1]; e += 32) s = fma(val[e], t[col[e]], s);
+    s = warp_sum_sp(s);
+    if (lane == 0) y[i] = s;
+    sq = fma(s, s, sq);
+  }
+  if (lane == 0) ws[warp] = sq;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double p = 0.0;
+    for (int w = 0; w < SP_WARPS; ++w) p += ws[w];
+    part[blockIdx.x] = p;
+  }
+}
+// norm from per-block partials (fixed order); writes lambda_hat and 1/||y||
+__global__ void k_norm(const double* part, int nparts, double* nrm, double* inv) {
+  __shared__ double red[256];
+  double s = 0.0;
+  for (int b = threadIdx.x; b < nparts; b += blockDim.x) s += part[b];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double q = sqrt(red[0]);
+    *nrm = q;
+    *inv = q > kDegenerateLambda ? 1.0 / q : 0.0;
+  }
+}
+__global__ void k_fill(double* v, int64_t n, double x) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    v[i] = x;
+}
+
+// ---------------------------------------------------------------- recurrence
+// W0 (interleaved) <- rows [r0, r0+rows) of X (densify)
+__global__ void k_densify(const int64_t* row_ptr, const int32_t* col, const double* val, int64_t r0, int64_t rows,
+                          int64_t n, double* W) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t i = blockIdx.x * (int64_t)SP_WARPS + warp; i < rows; i += (int64_t)gridDim.x * SP_WARPS) {
+    const int64_t b = i / RB, li = i % RB;
+    for (int64_t e = row_ptr[r0 + i] + lane; e < row_ptr[r0 + i + 1]; e += 32)
+      W[(b * n + col[e]) * RB + li] = val[e];
+  }
+}
+
+// Z[b][j][:] = sum_{l in row j of X} x_jl W[b][l][:]    (one warp per (block b, j))
+__global__ void __launch_bounds__(SP_WARPS * 32) k_spmm_wxt(const int64_t* row_ptr, const int32_t* col,
+                                                            const double* val, int64_t m, int64_t n, int64_t nblk,
+                                                            const double* __restrict__ W, double* __restrict__ Z) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t item = blockIdx.x * (int64_t)SP_WARPS + warp;  // block-major: item = b * m + j
+  if (item >= nblk * m) return;
+  const int64_t b = item / m, j = item % m;
+  const double* Wb = W + b * n * RB + lane;
+  const int64_t e0 = row_ptr[j], e1 = row_ptr[j + 1];
+  double s0 = 0.0, s1 = 0.0;
+  int64_t e = e0;
+  for (; e + 1 < e1; e += 2) {
+    const int32_t c0 = __ldg(col + e), c1 = __ldg(col + e + 1);
+    const double x0 = __ldg(val + e), x1 = __ldg(val + e + 1);
+    s0 = fma(x0, Wb[(int64_t)c0 * RB], s0);
+    s1 = fma(x1, Wb[(int64_t)c1 * RB], s1);
+  }
+  if (e < e1) s0 = fma(__ldg(val + e), Wb[(int64_t)__ldg(col + e) * RB], s0);
+  Z[(b * m + j) * RB + lane] = s0 + s1;
+}
+
+// W_k[b][l][:] = s * sum_{j in col l} x_jl Z[b][j][:] - ... (fused epilogue), one warp per (b, l)
+template <bool INIT>
+__global__ void __launch_bounds__(SP_WARPS * 32) k_spmm_zx(const int64_t* cptr, const int32_t* crow,
+                                                           const double* cval, int64_t m, int64_t n, int64_t nblk,
+                                                           const double* __restrict__ Z, const double* Wp,
+                                                           const double* Wpp, double* Wout, double* Yb,
+                                                           const SeriesParams* P, int k) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t item = blockIdx.x * (int64_t)SP_WARPS + warp;  // item = b * n + l
+  if (item >= nblk * n) return;
+  const int64_t b = item / n, l = item % n;
+  const double* Zb = Z + b * m * RB + lane;
+  const int64_t e0 = cptr[l], e1 = cptr[l + 1];
+  double s0 = 0.0, s1 = 0.0;
+  int64_t e = e0;
+  for (; e + 1 < e1; e += 2) {
+    const int32_t r0 = __ldg(crow + e), r1 = __ldg(crow + e + 1);
+    s0 = fma(__ldg(cval + e), Zb[(int64_t)r0 * RB], s0);
+    s1 = fma(__ldg(cval + e + 1), Zb[(int64_t)r1 * RB], s1);
+  }
+  if (e < e1) s0 = fma(__ldg(cval + e), Zb[(int64_t)__ldg(crow + e) * RB], s0);
+  const double acc = s0 + s1;
+  const int64_t o = item * RB + lane;
+  const double s2 = P->scale2;
+  if (INIT) {
+    const double x = Wp[o];
+    const double w = s2 * acc - x;                 // W_1 = B_hat X
+    if (Wout) Wout[o] = w;
+    Yb[o] = 0.5 * P->c[0] * x + P->c[1] * w;       // Y = c0/2 W_0 + c1 W_1
+  } else {
+    const double w = 2.0 * s2 * acc - 2.0 * Wp[o] - Wpp[o];  // W_k = 2 B_hat W_{k-1} - W_{k-2}
+    if (Wout) Wout[o] = w;
+    Yb[o] += P->c[k] * w;                          // Y += c_k W_k
+  }
+}
+
+// caller Y (row-major, ld) <- interleaved Yb, via a 32 x 32 shared-memory transpose
+__global__ void k_unblock(const double* Yb, int64_t rows, int64_t n, double* Y, int64_t ldy) {
+  __shared__ double t[RB][RB + 1];
+  const int64_t b = blockIdx.y;
+  const int64_t c0 = (int64_t)blockIdx.x * RB;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  for (int r = ty; r < RB; r += 8) {
+    const int64_t c = c0 + r;
+    t[r][tx] = c < n ? Yb[(b * n + c) * RB + tx] : 0.0;
+  }
+  __syncthreads();
+  for (int r = ty; r < RB; r += 8) {
+    const int64_t i = b * RB + r, c = c0 + tx;
+    if (i < rows && c < n) Y[i * ldy + c] = t[tx][r];
+  }
+}
+
+static inline size_t al(size_t b) { return (b + 255) / 256 * 256; }
+
+cudaError_t launch_series(SeriesParams* P, const cpa_svt_kernel& k, int K, double safety, double lam_override,
+                          const double* lam_src, const double* c_given, cudaStream_t st);
+
+cudaError_t sparse_apply(int64_t m, int64_t n, int64_t nnz, const int64_t* row_ptr, const int32_t* col,
+                         const double* val, int64_t row_begin, int64_t row_end, double* Y, int64_t ldy,
+                         const cpa_svt_kernel& kern, int K, int T, double safety, double lam_override,
+                         SeriesParams* P, void* ws, size_t ws_bytes, size_t* ws_needed, int num_sms,
+                         cudaStream_t st, int* launches, SparsePhaseHook hook, void* hook_ctx) {
+  const int64_t rows = row_end - row_begin;
+  const int64_t nblk = (rows + RB - 1) / RB;
+  // workspace layout
+  size_t scan_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (int64_t*)nullptr, (int64_t*)nullptr, (int)(n + 1));
+  const int npart = 4 * num_sms;
+  size_t off = 0;
+  const size_t o_cptr = off; off += al((n + 1) * sizeof(int64_t));
+  const size_t o_cnt = off;  off += al((n + 1) * sizeof(int64_t));  // int counts, then int64 widened
+  const size_t o_crow = off; off += al(nnz * sizeof(int32_t));
+  const size_t o_cval = off; off += al(nnz * sizeof(double));
+  const size_t o_scan = off; off += al(scan_bytes);
+  const size_t o_v = off;    off += al(m * sizeof(double));
+  const size_t o_t = off;    off += al(n * sizeof(double));
+  const size_t o_part = off; off += al(npart * sizeof(double));
+  const size_t o_nrm = off;  off += al(4 * sizeof(double));
+  const size_t blkW = (size_t)nblk * n * RB, blkZ = (size_t)nblk * m * RB;
+  const size_t o_Wa = off;   off += al(blkW * sizeof(double));
+  const size_t o_Wb = off;   off += al(blkW * sizeof(double));
+  const size_t o_Y = off;    off += al(blkW * sizeof(double));
+  const size_t o_Z = off;    off += al(blkZ * sizeof(double));
+  *ws_needed = off;
+  if (!ws || ws_bytes < off) return cudaSuccess;  // size query
+  char* base = (char*)ws;
+  int64_t* cptr = (int64_t*)(base + o_cptr);
+  int* cnt = (int*)(base + o_cnt);
+  int64_t* cnt64 = (int64_t*)(base + o_cnt);
+  int32_t* crow = (int32_t*)(base + o_crow);
+  double* cval = (double*)(base + o_cval);
+  double* v = (double*)(base + o_v);
+  double* tv = (double*)(base + o_t);
+  double* part = (double*)(base + o_part);
+  double* nrm = (double*)(base + o_nrm);
+  double* Wa = (double*)(base + o_Wa);
+  double* Wb = (double*)(base + o_Wb);
+  double* Yb = (double*)(base + o_Y);
+  double* Z = (double*)(base + o_Z);
+  int L = 0;
+  cudaError_t e;
+  const int g = 4 * num_sms;
+#define SPCK(x) do { e = (x); if (e != cudaSuccess) return e; } while (0)
+  // ---- CSC of X (= CSR of X^T), rows sorted within each column
+  if (hook) hook(hook_ctx, CPA_SVT_PH_GRAM, 1);  // structure pass (CSC of X) in the Gram slot
+  SPCK(cudaMemsetAsync(cnt, 0, (n + 1) * sizeof(int), st));
+  k_col_count<<<g, 256, 0, st>>>(col, nnz, cnt); ++L;
+  // widen int counts to int64 in place is unsafe; use cptr as scratch for the widened counts
+  k_widen<<<g, 256, 0, st>>>(cnt, n, cptr); ++L;
+  SPCK(cudaMemsetAsync(cptr + n, 0, sizeof(int64_t), st));
+  SPCK(cub::DeviceScan::ExclusiveSum(base + o_scan, scan_bytes, cptr, cnt64, (int)(n + 1), st)); ++L;
+  SPCK(cudaMemcpyAsync(cptr, cnt64, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+  SPCK(cudaMemsetAsync(cnt, 0, (n + 1) * sizeof(int), st));
+  k_col_fill<<<g, 256, 0, st>>>(row_ptr, col, val, m, cptr, cnt, crow, cval); ++L;
+  k_col_sort<<<g, 256, 0, st>>>(cptr, n, crow, cval); ++L;
+  if (hook) hook(hook_ctx, CPA_SVT_PH_GRAM, 0);
+  // ---- Lambda_max (m-side power iteration) and coefficients
+  if (hook) hook(hook_ctx, CPA_SVT_PH_POWER, 1);
+  if (lam_override > 0.0) {
+    SPCK(launch_series(P, kern, K, safety, lam_override, nullptr, nullptr, st)); ++L;
+  } else {
+    k_fill<<<g, 256, 0, st>>>(v, m, 1.0 / sqrt((double)m)); ++L;
+    const int spg = (int)std::min<int64_t>((m + SP_WARPS - 1) / SP_WARPS, npart);
+    for (int t = 0; t < T; ++t) {
+      // t = X^T v_{t-1} (v_{t-1} = y_{t-1} / ||y_{t-1}||, scale folded in), y_t = X t
+      k_spmv_t<<<g, 256, 0, st>>>(cptr, crow, cval, n, v, t == 0 ? nullptr : nrm + 1, tv); ++L;
+      k_spmv<<<spg, SP_WARPS * 32, 0, st>>>(row_ptr, col, val, m, tv, v, part); ++L;
+      k_norm<<<1, 256, 0, st>>>(part, spg, nrm, nrm + 1); ++L;
+    }
+    SPCK(launch_series(P, kern, K, safety, 0.0, nrm, nullptr, st)); ++L;
+  }
+  if (hook) hook(hook_ctx, CPA_SVT_PH_POWER, 0);
+  // ---- recurrence on this rank's rows
+  if (rows > 0) {
+    SPCK(cudaMemsetAsync(Wa, 0, blkW * sizeof(double), st));  // W_0 = X rows (Wa), densified
+    k_densify<<<g, SP_WARPS * 32, 0, st>>>(row_ptr, col, val, row_begin, rows, n, Wa); ++L;
+    // W_0 = X rows in Wa, W_1 -> Wb, then W_k overwrites W_{k-2} in place
+    // (the epilogue reads W_{k-2}[o] and writes W_k[o] in the same thread).
+    double* W0 = Wa;
+    double* W1 = Wb;
+    const int64_t itemsZ = nblk * m, itemsW = nblk * n;
+    const unsigned gz = (unsigned)((itemsZ + SP_WARPS - 1) / SP_WARPS);
+    const unsigned gw = (unsigned)((itemsW + SP_WARPS - 1) / SP_WARPS);
+    const double* prev = W0;   // W_{k-1}
+    const double* prev2 = nullptr;
+    for (int k = 1; k < K; ++k) {
+      if (hook) hook(hook_ctx, CPA_SVT_PH_SPARSE_Z, 1);
+      k_spmm_wxt<<<gz, SP_WARPS * 32, 0, st>>>(row_ptr, col, val, m, n, nblk, prev, Z); ++L;
+      if (hook) hook(hook_ctx, CPA_SVT_PH_SPARSE_Z, 0);
+      if (hook) hook(hook_ctx, CPA_SVT_PH_SPARSE_W, 1);
+      double* out;
+      if (k == 1) out = W1;                  // W_1 -> Wb
+      else out = (k & 1) ? Wb : Wa;          // W_k overwrites W_{k-2} in place
+      if (k == K - 1) out = nullptr;
+      if (k == 1)
+        k_spmm_zx<true><<<gw, SP_WARPS * 32, 0, st>>>(cptr, crow, cval, m, n, nblk, Z, prev, nullptr, out, Yb, P, k);
+      else
+        k_spmm_zx<false><<<gw, SP_WARPS * 32, 0, st>>>(cptr, crow, cval, m, n, nblk, Z, prev, prev2, out, Yb, P, k);
+      ++L;
+      if (hook) hook(hook_ctx, CPA_SVT_PH_SPARSE_W, 0);
+      prev2 = prev;
+      prev = (k & 1) ? (const double*)Wb : (const double*)Wa;
+    }
+    dim3 ub((unsigned)((n + RB - 1) / RB), (unsigned)nblk);
+    k_unblock<<<ub, dim3(32, 8), 0, st>>>(Yb, rows, n, Y, ldy); ++L;
+  }
+#undef SPCK
+  if (launches) *launches += L;
+  return cudaGetLastError();
+}
+
 }  // namespace cpa
