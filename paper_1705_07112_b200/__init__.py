@@ -153,9 +153,9 @@ class Handle:
         return {p: (ms[i], n[i]) for i, p in enumerate(PHASES)}
 
     def close(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and lib is not None:
             lib.cpa_svt_free(self._h)
-            self._h = None
+        self._h = None
 
     __del__ = close
 

@@ -1,0 +1,127 @@
+"""Measure every BASELINE config on one B200 (device-resident inputs, CUDA events).
+
+Not the driver's bench line (bench.py is): this records the per-config numbers
+kept under profiles/ -- GFLOP/s, ms per SVT, roofline fraction of the dominant
+phase, HBM GB/s where that is the bound.  Usage: python tools/bench_configs.py c1 c3 c4 [--reps N]
+"""
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_1705_07112_b200 as P  # noqa: E402
+import workloads as W  # noqa: E402
+
+PEAKS = json.load(open(os.path.join(ROOT, "profiles", "r01_peaks.json")))
+HBM = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
+    os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+
+
+def timed(fn, reps, h):
+    for _ in range(2):
+        fn()
+    torch.cuda.synchronize()
+    h.profile(True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    for a, b in ev:
+        a.record()
+        fn()
+        b.record()
+    torch.cuda.synchronize()
+    prof = h.profile_read()
+    h.profile(False)
+    ms = sorted(a.elapsed_time(b) for a, b in ev)
+    return ms[len(ms) // 2], {k: (v[0] / reps, v[1] / reps) for k, v in prof.items() if v[1]}
+
+
+def dense(name, h, reps, m=None, n=None, K=None, dtype="f64"):
+    cfg = dict(W.CONFIGS[name])
+    m = m or cfg["m"]
+    n = n or cfg["n"]
+    K = K or cfg["K"]
+    gen = {"c1": lambda: W.gen_c1(), "c2": lambda: W.gen_c2(m=m, n=n), "c5": lambda: W.gen_c5(m=m, n=n)}[name]
+    X = torch.from_numpy(gen()).cuda()
+    Y = torch.empty_like(X)
+    T = cfg["T"]
+    ms, ph = timed(lambda: h.apply(X, cfg["kernel"], K, T=T, Y=Y), reps, h)
+    s, L = min(m, n), max(m, n)
+    F = s * (s + 1) * L + (K - 1) * 2 * s * s * L
+    rec = (K - 1) * 2 * s * s * L
+    step_ms = ph.get("step", (0, 0))[0] + ph.get("init", (0, 0))[0]
+    return {"config": name, "shape": [m, n], "K": K, "T": T, "dtype": dtype, "ms_per_svt": ms,
+            "gflops": F / ms / 1e6, "phases_ms": {k: v[0] for k, v in ph.items()},
+            "recurrence_tflops": rec / step_ms / 1e9 if step_ms else None,
+            "recurrence_frac_of_dmma_peak": rec / step_ms / 1e9 / PEAKS["fp64_dmma_tflops"] if step_ms else None}
+
+
+def batched(h, reps, batch=65536):
+    cfg = W.CONFIGS["c3"]
+    t0 = time.time()
+    Xb = torch.from_numpy(W.gen_c3(batch=batch)).cuda()
+    gen_s = time.time() - t0
+    Y = torch.empty_like(Xb)
+    ms, ph = timed(lambda: h.apply_batched(Xb, cfg["kernel"], cfg["K"], T=cfg["T"], Y=Y), reps, h)
+    s = L = 64
+    per = s * (s + 1) * L + (cfg["K"] - 1) * 2 * s * s * L
+    F = per * batch
+    byt = 2 * batch * 64 * 64 * 4
+    return {"config": "c3", "batch": batch, "ms_per_svt_batch": ms, "gflops": F / ms / 1e6,
+            "fp32_frac": F / ms / 1e9 / PEAKS["fp32_ffma_tflops"], "hbm_gbs": byt / ms / 1e6,
+            "hbm_frac": byt / ms / 1e6 / HBM, "gen_s": gen_s}
+
+
+def sparse(h, reps, m=20000, n=200000, nnz=4_000_000):
+    cfg = W.CONFIGS["c4"]
+    row_ptr, col, val = W.gen_c4(m=m, n=n, nnz=nnz)
+    d = [torch.from_numpy(a).cuda() for a in (row_ptr, col, val)]
+    Y = torch.empty((m, n), dtype=torch.float64, device="cuda")
+    ms, ph = timed(lambda: h.apply_csr(*d, m, n, cfg["kernel"], cfg["K"], T=cfg["T"], Y=Y), reps, h)
+    K = cfg["K"]
+    F = (K - 1) * 4 * m * nnz
+    byt = (K - 1) * (5 * 8 * m * n + 2 * 8 * m * m)
+    zx = ph.get("sparse_w", (0, 0))[0]
+    zw = ph.get("sparse_z", (0, 0))[0]
+    return {"config": "c4", "shape": [m, n, nnz], "ms_per_svt": ms, "gflops": F / ms / 1e6,
+            "algorithmic_GB": byt / 1e9, "hbm_gbs_alg": byt / ms / 1e6, "hbm_frac": byt / ms / 1e6 / HBM,
+            "phases_ms": {k: v[0] for k, v in ph.items()},
+            "spmm_pair_ms_per_step": (zx + zw) / (K - 1)}
+
+
+if __name__ == "__main__":
+    reps = 3
+    args = [a for a in sys.argv[1:]]
+    if "--reps" in args:
+        i = args.index("--reps")
+        reps = int(args[i + 1])
+        del args[i:i + 2]
+    h = P.Handle(0)
+    out = []
+    for a in args:
+        if a == "c1":
+            r = dense("c1", h, reps)
+        elif a == "c2":
+            r = dense("c2", h, reps)
+        elif a.startswith("c5"):          # c5 or c5:KxM scaled, e.g. c5:8192x32768
+            if ":" in a:
+                mm, nn = map(int, a.split(":")[1].split("x"))
+                r = dense("c5", h, reps, m=mm, n=nn)
+            else:
+                r = dense("c5", h, reps)
+        elif a.startswith("c3"):
+            r = batched(h, reps, int(a.split(":")[1]) if ":" in a else 65536)
+        elif a.startswith("c4"):
+            if ":" in a:
+                mm, nn, zz = map(int, a.split(":")[1].split("x"))
+                r = sparse(h, reps, mm, nn, zz)
+            else:
+                r = sparse(h, reps)
+        else:
+            raise SystemExit(f"unknown config {a}")
+        print(json.dumps(r), flush=True)
+        out.append(r)
+        torch.cuda.empty_cache()
