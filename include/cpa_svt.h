@@ -204,6 +204,14 @@ cpa_svt_status cpa_svt_profile(cpa_svt_handle* h, int enable);
  * (host arrays of CPA_SVT_PH_COUNT entries; either may be NULL). */
 cpa_svt_status cpa_svt_profile_read(cpa_svt_handle* h, double* ms, int64_t* launches);
 
+/* Kernel unit test hook (tests only): C (M x N, ld ldc, fp32) = A B on the
+ * tcgen05 TF32 engine, A (M x Kd, K-major, ld lda), B K x N N-contiguous
+ * (b_mn != 0, ld ldb) or N x K K-contiguous (b_mn == 0).  terms = 1 (TF32 of
+ * the rna-rounded operands) or 3 (3xTF32).  All device pointers, ld % 4 == 0.
+ * Synchronous. */
+cpa_svt_status cpa_svt_debug_gemm_tf32(cpa_svt_handle* h, int M, int N, int Kd, const float* A, int64_t lda,
+                                       const float* B, int64_t ldb, int b_mn, float* C, int64_t ldc, int terms);
+
 const char* cpa_svt_status_string(cpa_svt_status s);
 /* Text of the last error recorded on this handle ("" if none). */
 const char* cpa_svt_last_error(const cpa_svt_handle* h);

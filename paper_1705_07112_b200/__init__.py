@@ -73,6 +73,9 @@ lib.cpa_svt_last_error.restype = ctypes.c_char_p
 lib.cpa_svt_last_error.argtypes = [_p]
 lib.cpa_svt_launch_count.restype = ctypes.c_int64
 lib.cpa_svt_launch_count.argtypes = [_p]
+lib.cpa_svt_debug_gemm_tf32.argtypes = [_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, _p, _i64, _p, _i64,
+                                        ctypes.c_int, _p, _i64, ctypes.c_int]
+lib.cpa_svt_debug_gemm_tf32.restype = ctypes.c_int
 lib.cpa_svt_profile.argtypes = [_p, ctypes.c_int]
 lib.cpa_svt_profile_read.argtypes = [_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)]
 PHASES = ["gram", "allreduce", "power", "init", "step", "sparse_z", "sparse_w", "batched"]
@@ -151,6 +154,17 @@ class Handle:
         n = (ctypes.c_int64 * len(PHASES))()
         self._check(lib.cpa_svt_profile_read(self._h, ms, n), "cpa_svt_profile_read")
         return {p: (ms[i], n[i]) for i, p in enumerate(PHASES)}
+
+    def debug_gemm_tf32(self, A, B, b_mn: bool, terms: int = 3):
+        """Kernel unit-test hook: C = A @ B (b_mn) or A @ B.T on the tcgen05 TF32 engine."""
+        torch = self._torch
+        M, Kd = A.shape
+        N = B.shape[1] if b_mn else B.shape[0]
+        C = torch.zeros((M, (N + 3) // 4 * 4), dtype=torch.float32, device=A.device)
+        self._check(lib.cpa_svt_debug_gemm_tf32(self._h, M, N, Kd, A.data_ptr(), A.stride(0), B.data_ptr(),
+                                                B.stride(0), int(b_mn), C.data_ptr(), C.stride(0), terms),
+                    "cpa_svt_debug_gemm_tf32")
+        return C[:, :N]
 
     def close(self):
         if getattr(self, "_h", None) and lib is not None:

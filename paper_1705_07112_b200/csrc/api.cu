@@ -35,6 +35,18 @@ cudaError_t launch_diag_scale(const double* G, int64_t s, double* scale, cudaStr
 cudaError_t launch_power_dense(const double* G, const double* G4, int64_t s, int T, double* scratch,
                                unsigned int* bar, SeriesParams* P, const cpa_svt_kernel& k, int K, double safety,
                                const double* c_given, int num_sms, cudaStream_t st);
+cudaError_t launch_power_dense_f32(const float* G, int64_t s, int64_t ld, int T, double* scratch, unsigned int* bar,
+                                   SeriesParams* P, const cpa_svt_kernel& k, int K, double safety,
+                                   const double* c_given, int num_sms, cudaStream_t st);
+// tc_tf32.cu
+cudaError_t tc_gemm(int mode, int terms, int M, int N, int Kd, const float* Ah, const float* Al, int64_t lda,
+                    const float* Bh, const float* Bl, int64_t ldb, bool b_mn, float* out_f, float* out_h,
+                    float* out_l, int out_split, int64_t ld_out, const float* wp, const float* wpp, int64_t ld_w,
+                    float* y, int64_t ld_y, const SeriesParams* P, int k, int num_sms, cudaStream_t st);
+cudaError_t tf32_prep(const float* X, int64_t m, int64_t n, int64_t ldx, bool transpose, float* Af, float* Ah,
+                      float* Al, int64_t lda, int num_sms, cudaStream_t st);
+cudaError_t tf32_finish(const float* Yi, int64_t ldi, int64_t m, int64_t n, bool transpose, float* Y, int64_t ldy,
+                        int num_sms, cudaStream_t st);
 // batched_f32.cu
 cudaError_t launch_batched_f32(int64_t batch, int m, int n, const float* X, float* Y, const cpa_svt_kernel& k,
                                int K, int T, double safety, double lam_override, float* lambda_out,
@@ -503,6 +515,107 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
   return CPA_SVT_OK;
 }
 
+// fp32 data on the tcgen05 tensor cores: TF32 (rna operands) or 3xTF32 (hi/lo split).
+static cpa_svt_status apply_tf32(cpa_svt_handle* h, int terms, int64_t m, int64_t n, cpa_svt_shard shard,
+                                 int64_t long_global, const float* X, int64_t ldx, float* Y, int64_t ldy,
+                                 const cpa_svt_kernel* k, int K, const double* c, cpa_svt_lambda* lam,
+                                 cpa_svt_info* info) {
+  bool left;
+  if (shard == CPA_SVT_SHARD_COLS) {
+    if (m > long_global || long_global < n) return CPA_SVT_E_ARG;
+    left = true;
+  } else if (shard == CPA_SVT_SHARD_ROWS) {
+    if (long_global <= n || long_global < m) return CPA_SVT_E_ARG;
+    left = false;
+  } else {
+    left = m <= n;
+  }
+  const bool sharded = shard != CPA_SVT_SHARD_NONE && h->world > 1;
+  const int64_t s = left ? m : n, L = left ? n : m;
+  if (s > 2147483647 / 2 || L > 2147483647 / 2) return CPA_SVT_E_UNSUPPORTED;
+  const int64_t sp = (s + 3) / 4 * 4, Lp = (L + 3) / 4 * 4;
+  auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+  const size_t nA = al((size_t)s * Lp * 4), nG = al((size_t)s * sp * 4);
+  const size_t nPow = al(power_dense_scratch_doubles(s) * 8);
+  const size_t need = 7 * nA + 3 * nG + nPow + 256;
+  cpa_svt_status st = grow(h, &h->ws, &h->ws_bytes, need);
+  if (st != CPA_SVT_OK) return st;
+  char* b = (char*)h->ws;
+  float* Xs[3] = {(float*)b, (float*)(b + nA), (float*)(b + 2 * nA)};            // full, hi, lo (set X)
+  float* As[3] = {(float*)(b + 3 * nA), (float*)(b + 4 * nA), (float*)(b + 5 * nA)};  // set A
+  float* Yi = (float*)(b + 6 * nA);
+  float* Gf = (float*)(b + 7 * nA);
+  float* Gh = (float*)(b + 7 * nA + nG);
+  float* Gl = (float*)(b + 7 * nA + 2 * nG);
+  double* pw = (double*)(b + 7 * nA + 3 * nG);
+  const double* c_dev = nullptr;
+  if (c) {
+    CU(cudaMemcpyAsync(h->d_c, c, K * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+    c_dev = h->d_c;
+  }
+  PhaseTimer tm;
+  tm.start(info != nullptr, h->stream);
+  int launches = 0;
+  {
+    Phase p(h, CPA_SVT_PH_GRAM);
+    CU(tf32_prep(X, m, n, ldx, !left, Xs[0], Xs[1], Xs[2], Lp, h->num_sms, h->stream));
+    // Gram always 3xTF32: G(i,j) = sum_l A(i,l) A(j,l), both operands K-major
+    CU(tc_gemm(0, 3, (int)s, (int)s, (int)L, Xs[1], Xs[2], Lp, Xs[1], Xs[2], Lp, false, Gf, Gh, Gl, 3, sp, nullptr,
+               nullptr, 0, nullptr, 0, nullptr, 0, h->num_sms, h->stream));
+    launches += 2;
+  }
+  tm.mark();
+  if (sharded) {
+    Phase p(h, CPA_SVT_PH_ALLREDUCE);
+    // the split copies are rebuilt from the reduced full Gram below
+    NC(g_nccl.AllReduce(Gf, Gf, (size_t)s * sp, ncclFloat, ncclSum, h->comm, h->stream));
+    CU(tf32_prep(Gf, s, sp, sp, false, Gf, Gh, Gl, sp, h->num_sms, h->stream));
+    ++launches;
+  }
+  tm.mark();
+  if (lam->lambda_max > 0.0) {
+    Phase p(h, CPA_SVT_PH_POWER);
+    CU(launch_series(h->P, *k, K, lam->safety, lam->lambda_max, nullptr, c_dev, h->stream));
+  } else {
+    if (s * (int64_t)sizeof(double) > 200 * 1024) return CPA_SVT_E_UNSUPPORTED;
+    Phase p(h, CPA_SVT_PH_POWER);
+    CU(launch_power_dense_f32(Gf, s, sp, lam->power_iters, pw, h->bar, h->P, *k, K, lam->safety, c_dev, h->num_sms,
+                              h->stream));
+  }
+  ++launches;
+  if (sharded) {
+    Phase p(h, CPA_SVT_PH_ALLREDUCE, 0);
+    NC(g_nccl.Broadcast(h->P, h->P, sizeof(SeriesParams), ncclChar, 0, h->comm, h->stream));
+  }
+  tm.mark();
+  float** sets[2] = {Xs, As};
+  for (int kk = 1; kk < K; ++kk) {
+    float** src = sets[(kk - 1) & 1];      // W_{k-1}: k=1 -> X set
+    float** out = sets[kk & 1];            // W_k overwrites W_{k-2} (k >= 2)
+    const bool last = kk == K - 1;
+    Phase p(h, kk == 1 ? CPA_SVT_PH_INIT : CPA_SVT_PH_STEP);
+    CU(tc_gemm(kk == 1 ? 1 : 2, terms, (int)s, (int)L, (int)s, Gh, Gl, sp, src[1], src[2], Lp, true,
+               last ? nullptr : out[0], last ? nullptr : out[1], last ? nullptr : out[2], terms, Lp, src[0],
+               kk == 1 ? nullptr : out[0], Lp, Yi, Lp, h->P, kk, h->num_sms, h->stream));
+    ++launches;
+  }
+  CU(tf32_finish(Yi, Lp, m, n, !left, Y, ldy, h->num_sms, h->stream));
+  ++launches;
+  tm.mark();
+  h->launches += launches;
+  st = fill_info(h, info, lam, left ? 0 : 1);
+  if (st != CPA_SVT_OK) return st;
+  if (info) {
+    info->ms_gram = tm.ms(0, 1);
+    info->ms_allreduce = tm.ms(1, 2);
+    info->ms_power = tm.ms(2, 3);
+    info->ms_recurrence = tm.ms(3, 4);
+    info->ms_total = tm.ms(0, 4);
+    info->kernel_launches = launches;
+  }
+  return CPA_SVT_OK;
+}
+
 cpa_svt_status cpa_svt_apply(cpa_svt_handle* h, cpa_svt_dtype dtype, cpa_svt_math math, int64_t m, int64_t n,
                              cpa_svt_shard shard, int64_t long_global, const void* X, int64_t ldx, void* Y,
                              int64_t ldy, const cpa_svt_kernel* k, int K, const double* c, cpa_svt_lambda* lam,
@@ -521,7 +634,32 @@ cpa_svt_status cpa_svt_apply(cpa_svt_handle* h, cpa_svt_dtype dtype, cpa_svt_mat
   if (!k) k = &kz;
   if (dtype == CPA_SVT_F64 && math == CPA_SVT_MATH_NATIVE)
     return apply_f64(h, m, n, shard, long_global, (const double*)X, ldx, (double*)Y, ldy, k, K, c, lam, info);
+  if (dtype == CPA_SVT_F32 && (math == CPA_SVT_MATH_TF32 || math == CPA_SVT_MATH_3XTF32))
+    return apply_tf32(h, math == CPA_SVT_MATH_TF32 ? 1 : 3, m, n, shard, long_global, (const float*)X, ldx, (float*)Y,
+                      ldy, k, K, c, lam, info);
   return CPA_SVT_E_UNSUPPORTED;
+}
+
+cpa_svt_status cpa_svt_debug_gemm_tf32(cpa_svt_handle* h, int M, int N, int Kd, const float* A, int64_t lda,
+                                       const float* B, int64_t ldb, int b_mn, float* C, int64_t ldc, int terms) {
+  if (!h || !A || !B || !C || M < 1 || N < 1 || Kd < 1 || (terms != 1 && terms != 3)) return CPA_SVT_E_ARG;
+  if (lda % 4 || ldb % 4 || ldc % 4) return CPA_SVT_E_ARG;
+  if (cudaSetDevice(h->device) != cudaSuccess) return CPA_SVT_E_CUDA;
+  const int64_t ra = M, ca = lda, rb = b_mn ? Kd : N, cb = ldb;
+  const size_t na = (size_t)ra * ca, nb = (size_t)rb * cb;
+  cpa_svt_status st = grow(h, &h->ws, &h->ws_bytes, (2 * na + 2 * nb) * 4 + 1024);
+  if (st != CPA_SVT_OK) return st;
+  float* Ah = (float*)h->ws;
+  float* Al = Ah + ((na + 63) / 64) * 64;
+  float* Bh = Al + ((na + 63) / 64) * 64;
+  float* Bl = Bh + ((nb + 63) / 64) * 64;
+  float* dummy = nullptr;
+  CU(tf32_prep(A, ra, ca, lda, false, Ah /*full copy unused*/, Ah, Al, ca, h->num_sms, h->stream));
+  CU(tf32_prep(B, rb, cb, ldb, false, Bh, Bh, Bl, cb, h->num_sms, h->stream));
+  CU(tc_gemm(0, terms, M, N, Kd, Ah, Al, lda, Bh, Bl, ldb, b_mn != 0, C, dummy, dummy, 1, ldc, nullptr, nullptr, 0,
+             nullptr, 0, nullptr, 0, h->num_sms, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  return CPA_SVT_OK;
 }
 
 cpa_svt_status cpa_svt_apply_host(cpa_svt_handle* h, cpa_svt_dtype dtype, cpa_svt_math math, int64_t m, int64_t n,

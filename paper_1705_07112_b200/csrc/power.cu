@@ -61,11 +61,13 @@ __global__ void k_series(SeriesParams* P, cpa_svt_kernel kern, int K, double saf
   compute_series(P, kern, K, safety, lh, c_given);
 }
 
+template <typename E>
 struct PowerArgs {
-  const double* G;
-  const double* G4;  // c^4 G^4 (nullable): first q products use it
+  const E* G;
+  const E* G4;       // c^4 G^4 (nullable): first q products use it
   int q;             // products by G4
   int64_t s;
+  int64_t ld;        // row stride of G / G4 (elements)
   int T;
   double* ubuf;      // 2 * s
   double* part;      // 2 * gridDim.x
@@ -94,22 +96,24 @@ __device__ __forceinline__ void red_release_add(unsigned int* p, unsigned int v)
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
 
-__global__ void __launch_bounds__(256) k_power_dense(PowerArgs a) {
+template <typename E>
+__global__ void __launch_bounds__(256) k_power_dense(PowerArgs<E> a) {
+  using T = E;
   extern __shared__ __align__(16) double psm[];
   __shared__ double s_warp[8];
   __shared__ double s_norm;
   const int64_t s = a.s;
   double* sv = psm;               // v_{t-1} (s doubles)
-  double* sg = psm + s;           // cached rows (rows_per_cta * s) if cache_rows
+  T* sg = reinterpret_cast<T*>(psm + s);  // cached rows (rows_per_cta * s) if cache_rows
   const int64_t r0 = (int64_t)blockIdx.x * a.rows_per_cta;
   const int64_t r1 = min(s, r0 + a.rows_per_cta);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   const unsigned int nb = gridDim.x;
   // products: q by G4 (cached when present), then T - 4q by G; the last one gives lambda_hat
-  const double* Gc = a.q > 0 ? a.G4 : a.G;  // the matrix whose rows are cached
+  const T* Gc = a.q > 0 ? a.G4 : a.G;  // the matrix whose rows are cached
   const int niter = a.T - 3 * a.q;
   if (a.cache_rows) {
-    for (int64_t e = threadIdx.x; e < (r1 - r0) * s; e += blockDim.x) sg[e] = Gc[r0 * s + e];
+    for (int64_t e = threadIdx.x; e < (r1 - r0) * s; e += blockDim.x) sg[e] = Gc[(r0 + e / s) * a.ld + e % s];
   }
   const double v0 = 1.0 / sqrt((double)s);
   for (int64_t j = threadIdx.x; j < s; j += blockDim.x) sv[j] = v0;
@@ -118,21 +122,21 @@ __global__ void __launch_bounds__(256) k_power_dense(PowerArgs a) {
   double inv = 1.0;  // 1/||u_{t-1}||, folded into this product (v_{t-1} = u_{t-1} * inv)
   for (int t = 0; t < niter; ++t) {
     const bool use4 = t < a.q;
-    const double* Gt = use4 ? a.G4 : a.G;
+    const T* Gt = use4 ? a.G4 : a.G;
     const bool cached = a.cache_rows && (use4 || a.q == 0);
     // u_t = G v_{t-1}: one warp per row, 4 independent partial sums per lane
     double mysq = 0.0;
     for (int64_t r = r0 + warp; r < r1; r += nwarps) {
-      const double* grow = cached ? sg + (r - r0) * s : Gt + r * s;
+      const T* grow = cached ? sg + (r - r0) * s : Gt + r * a.ld;
       double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
       int64_t j = lane;
       for (; j + 96 < s; j += 128) {
-        d0 = fma(grow[j], sv[j], d0);
-        d1 = fma(grow[j + 32], sv[j + 32], d1);
-        d2 = fma(grow[j + 64], sv[j + 64], d2);
-        d3 = fma(grow[j + 96], sv[j + 96], d3);
+        d0 = fma((double)grow[j], sv[j], d0);
+        d1 = fma((double)grow[j + 32], sv[j + 32], d1);
+        d2 = fma((double)grow[j + 64], sv[j + 64], d2);
+        d3 = fma((double)grow[j + 96], sv[j + 96], d3);
       }
-      for (; j < s; j += 32) d0 = fma(grow[j], sv[j], d0);
+      for (; j < s; j += 32) d0 = fma((double)grow[j], sv[j], d0);
       const double d = warp_sum((d0 + d1) + (d2 + d3)) * inv;
       if (lane == 0) a.ubuf[(t & 1) * s + r] = d;
       mysq = fma(d, d, mysq);  // identical in all lanes
@@ -211,10 +215,12 @@ bool power_use_squaring(int64_t s, int T) {
   return gemm_us < 0.75 * T * iter_us;
 }
 
-cudaError_t launch_power_dense(const double* G, const double* G4, int64_t s, int T, double* scratch,
-                               unsigned int* bar, SeriesParams* P, const cpa_svt_kernel& k, int K, double safety,
-                               const double* c_given, int num_sms, cudaStream_t st) {
-  PowerArgs a{};
+template <typename E>
+static cudaError_t launch_power_t(const E* G, const E* G4, int64_t s, int64_t ld, int T, double* scratch,
+                                  unsigned int* bar, SeriesParams* P, const cpa_svt_kernel& k, int K, double safety,
+                                  const double* c_given, int num_sms, cudaStream_t st) {
+  PowerArgs<E> a{};
+  a.ld = ld;
   a.G = G; a.s = s; a.T = T;
   a.G4 = G4;
   a.q = G4 ? (T - 1) / 4 : 0;
@@ -225,7 +231,7 @@ cudaError_t launch_power_dense(const double* G, const double* G4, int64_t s, int
   const size_t budget = 200 * 1024;
   size_t smem = (size_t)s * sizeof(double);
   if (smem > budget) return cudaErrorInvalidValue;  // s > 25600 not supported by this kernel
-  int64_t rows_fit = (int64_t)((budget - smem) / ((size_t)s * sizeof(double)));
+  int64_t rows_fit = (int64_t)((budget - smem) / ((size_t)s * sizeof(E)));
   int64_t grid;
   if (rows_fit >= 1 && (s + rows_fit - 1) / rows_fit <= num_sms) {
     int64_t g0 = (s + rows_fit - 1) / rows_fit;
@@ -238,13 +244,25 @@ cudaError_t launch_power_dense(const double* G, const double* G4, int64_t s, int
   if (grid < 1) grid = 1;
   a.rows_per_cta = (int)((s + grid - 1) / grid);
   grid = (s + a.rows_per_cta - 1) / a.rows_per_cta;
-  if (a.cache_rows) smem += (size_t)a.rows_per_cta * s * sizeof(double);
+  if (a.cache_rows) smem += (size_t)a.rows_per_cta * s * sizeof(E);
   cudaError_t e0 = cudaMemsetAsync(bar, 0, sizeof(unsigned int), st);
   if (e0 != cudaSuccess) return e0;
-  cudaError_t e = cudaFuncSetAttribute(k_power_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(k_power_dense<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   void* args[] = {&a};
-  return cudaLaunchCooperativeKernel((void*)k_power_dense, dim3((unsigned)grid), dim3(256), args, smem, st);
+  return cudaLaunchCooperativeKernel((void*)k_power_dense<E>, dim3((unsigned)grid), dim3(256), args, smem, st);
+}
+
+cudaError_t launch_power_dense(const double* G, const double* G4, int64_t s, int T, double* scratch,
+                               unsigned int* bar, SeriesParams* P, const cpa_svt_kernel& k, int K, double safety,
+                               const double* c_given, int num_sms, cudaStream_t st) {
+  return launch_power_t<double>(G, G4, s, s, T, scratch, bar, P, k, K, safety, c_given, num_sms, st);
+}
+// fp32 Gram (TF32 path): the products are accumulated in fp64 all the same
+cudaError_t launch_power_dense_f32(const float* G, int64_t s, int64_t ld, int T, double* scratch, unsigned int* bar,
+                                   SeriesParams* P, const cpa_svt_kernel& k, int K, double safety,
+                                   const double* c_given, int num_sms, cudaStream_t st) {
+  return launch_power_t<float>(G, nullptr, s, ld, T, scratch, bar, P, k, K, safety, c_given, num_sms, st);
 }
 
 }  // namespace cpa

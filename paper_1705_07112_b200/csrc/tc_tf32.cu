@@ -1,0 +1,497 @@
+// fp32 dense path on the 5th-generation tensor cores (tcgen05, kind::tf32):
+// TMA -> shared memory (128-byte swizzle) -> tcgen05.mma (single elected thread,
+// accumulator in TMEM, double-buffered) -> tcgen05.ld -> fused epilogue.
+//
+//   Gram (Alg. 1 l.1):   G = A A^T             (A = X, or X^T when m > n)
+//   Init (l.5-7):    W_1 = (2/L) G A - A,  Y = c_0/2 A + c_1 W_1
+//   Step (l.8-11):   W_k = (4/L) G W_{k-1} - 2 W_{k-1} - W_{k-2},  Y += c_k W_k
+//
+// Operand precision: the tensor core reads only the TF32
+// bits of an fp32 word (truncation), which misses the 1e-4 bar.  Every operand
+// is therefore written by the PRODUCING epilogue as a round-to-nearest TF32
+// "hi" copy (cvt.rna.tf32) and, for 3xTF32, the residual "lo" = rna(x - hi):
+//   TF32:    acc = hi(G) hi(W)
+//   3xTF32:  acc = hi(G) hi(W) + hi(G) lo(W) + lo(G) hi(W)
+// while the recurrence itself (2 W_{k-1} + W_{k-2}, Y) is carried in full fp32.
+// The Gram is always 3xTF32 (its error moves every eigenvalue).
+//
+// Warp roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM allocator +
+// MMA issuer, warps 2..5 = epilogue (TMEM lane quarter = warp % 4).  Persistent
+// grid (one CTA per SM), static tile schedule in grouped-M raster order so the
+// CTAs in flight share A and B panels through L2.
+#include <cuda.h>
+
+#include <cstdlib>
+
+#include "common.cuh"
+
+namespace cpa {
+namespace tc {
+
+constexpr int BM = 128;         // UMMA M (cta_group::1): TMEM lane = tile row
+constexpr int BK = 32;          // fp32 elements per 128-byte swizzled row = one k-slab
+constexpr int UK = 8;           // UMMA K for kind::tf32
+constexpr int NTHR = 192;
+
+enum Mode { GRAM = 0, INIT = 1, STEP = 2 };
+
+struct TcArgs {
+  int M, N, Kd;                  // C (M x N) = A (M x Kd) B (Kd x N)
+  int terms;                     // 1 (TF32) or 3 (3xTF32)
+  int mode;
+  float* out_f;                  // full fp32 result (G or W_k); nullable
+  float* out_h;                  // rna-TF32 hi copy
+  float* out_l;                  // rna-TF32 lo copy (terms_out == 3)
+  int out_split;                 // 1: write hi only; 3: hi and lo
+  int64_t ld_out;
+  const float* wp;               // W_{k-1} (INIT: A = X copy), full fp32
+  const float* wpp;              // W_{k-2} (full)
+  int64_t ld_w;
+  float* y;
+  int64_t ld_y;
+  const SeriesParams* P;
+  int k;
+  int tiles_m, tiles_n;
+  int dbg_lbo, dbg_sbo;          // debugging overrides of the B (MN-major) descriptor strides
+};
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+
+// UMMA shared-memory descriptor (sm_100 "version 1").  layout 2 = SWIZZLE_128B
+// (K-major operands), 1 = SWIZZLE_128B_BASE32B (the only MN-major layout for tf32).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t layout = 2) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;          // version = 1 (Blackwell)
+  d |= (uint64_t)layout << 61;
+  return d;
+}
+// Instruction descriptor, kind::tf32, fp32 accumulate.
+__host__ __device__ constexpr uint32_t instr_desc(int M, int N, bool b_mn_major) {
+  return (1u << 4)                      // c_format = F32
+         | (2u << 7)                    // a_format = TF32
+         | (2u << 10)                   // b_format = TF32
+         | (0u << 15)                   // a K-major
+         | ((b_mn_major ? 1u : 0u) << 16)
+         | ((uint32_t)(N >> 3) << 17)
+         | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_tf32(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(dtmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
+               : "memory");
+}
+// 32 consecutive TMEM columns of this warp's 32 lanes -> 32 registers per thread
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ float rna_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// grouped-M raster: tiles in groups of GROUP row-tiles, columns inside a group
+__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& tm, int& tn) {
+  constexpr int GROUP = 16;
+  const int per_group = GROUP * tiles_n;
+  const int g = t / per_group;
+  const int first = g * GROUP;
+  const int gsize = min(GROUP, tiles_m - first);
+  const int r = t % per_group;
+  tm = first + r % gsize;
+  tn = r / gsize;
+}
+
+template <int BN, int TERMS, bool B_MN>
+struct Smem {
+  static constexpr int A_BYTES = BM * BK * 4;                  // 16 KB per term
+  static constexpr int B_BYTES = BN * BK * 4;                  // BN * 128 B per term
+  static constexpr int STAGE = (TERMS == 3 ? 2 : 1) * (A_BYTES + B_BYTES);
+  static constexpr int STAGES = (200 * 1024) / STAGE > 6 ? 6 : (200 * 1024) / STAGE;
+  static constexpr int BYTES = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+template <int BN, int TERMS, bool B_MN>
+__global__ void __launch_bounds__(NTHR, 1)
+    k_tc_gemm(const __grid_constant__ CUtensorMap tmA_h, const __grid_constant__ CUtensorMap tmA_l,
+              const __grid_constant__ CUtensorMap tmB_h, const __grid_constant__ CUtensorMap tmB_l, TcArgs a) {
+  using S = Smem<BN, TERMS, B_MN>;
+  constexpr int ST = S::STAGES;
+  constexpr int NSPLIT = TERMS == 3 ? 2 : 1;
+  extern __shared__ uint8_t raw_smem[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)raw_smem + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(smem + ST * S::STAGE);
+  uint64_t* empty = full + ST;
+  uint64_t* tfull = empty + ST;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntiles = a.tiles_m * a.tiles_n;
+  const int nk = (a.Kd + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(tfull + b, 1);
+      mbar_init(tempty + b, 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {  // TMEM: 2 accumulators x BN fp32 columns
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                 "r"(2 * BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ============================ TMA producer ============================
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmA_h) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmB_h) : "memory");
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int tm, tn;
+        tile_coords(t, a.tiles_m, a.tiles_n, tm, tn);
+        const int m0 = tm * BM, n0 = tn * BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(empty + stage, phase ^ 1);
+          uint8_t* st = smem + stage * S::STAGE;
+          mbar_expect_tx(full + stage, S::STAGE);
+          const int k0 = kb * BK;
+#pragma unroll
+          for (int h = 0; h < NSPLIT; ++h) {
+            uint8_t* sa = st + h * S::A_BYTES;
+            uint8_t* sb = st + NSPLIT * S::A_BYTES + h * S::B_BYTES;
+            tma_load_2d(sa, h ? &tmA_l : &tmA_h, k0, m0, full + stage);
+            if (B_MN) {
+#pragma unroll
+              for (int c = 0; c < BN / 32; ++c) tma_load_2d(sb + c * 4096, h ? &tmB_l : &tmB_h, n0 + 32 * c, k0, full + stage);
+            } else {
+              tma_load_2d(sb, h ? &tmB_l : &tmB_h, k0, n0, full + stage);
+            }
+          }
+          if (++stage == ST) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ============================ MMA issuer ==============================
+    constexpr uint32_t IDESC = instr_desc(BM, BN, B_MN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      mbar_wait(tempty + acc, aphase ^ 1);
+      tc_fence_after();
+      const uint32_t dtm = tmem_base + (uint32_t)(acc * BN);
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(full + stage, phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t st = smem_u32(smem + stage * S::STAGE);
+          const uint32_t a_h = st, a_l = st + S::A_BYTES;
+          const uint32_t b_h = st + NSPLIT * S::A_BYTES, b_l = b_h + S::B_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < BK / UK; ++kk) {
+            // A K-major: +32 B per UMMA_K inside the swizzled row; B MN-major: +1 KB (one 8-row group)
+            const uint32_t aoff = kk * UK * 4;
+            const uint32_t boff = B_MN ? kk * 1024 : kk * UK * 4;
+            // MN-major B (tf32): SW128 with 32-byte atoms; 32-element MN chunks LBO = 4 KB
+            // apart, 4-row K groups SBO = 512 B apart; one UMMA_K = 8 rows = +1 KB.
+            const uint32_t blbo = B_MN ? (a.dbg_lbo ? a.dbg_lbo : 4096) : 16;
+            const uint32_t bsbo = B_MN ? (a.dbg_sbo ? a.dbg_sbo : 512) : 1024;
+            const uint32_t blay = B_MN ? 1u : 2u;
+            const uint64_t dAh = smem_desc(a_h + aoff, 16, 1024);
+            const uint64_t dBh = smem_desc(b_h + boff, blbo, bsbo, blay);
+            const uint32_t accum = (kb > 0 || kk > 0) ? 1u : 0u;
+            mma_tf32(dtm, dAh, dBh, IDESC, accum);
+            if (TERMS == 3) {
+              const uint64_t dAl = smem_desc(a_l + aoff, 16, 1024);
+              const uint64_t dBl = smem_desc(b_l + boff, blbo, bsbo, blay);
+              mma_tf32(dtm, dAh, dBl, IDESC, 1u);
+              mma_tf32(dtm, dAl, dBh, IDESC, 1u);
+            }
+          }
+          mma_commit(empty + stage);  // frees the smem stage when these MMAs complete
+        }
+        __syncwarp();
+        if (++stage == ST) { stage = 0; phase ^= 1; }
+      }
+      if (lane == 0) mma_commit(tfull + acc);  // accumulator ready for the epilogue
+      __syncwarp();
+      if (++acc == 2) { acc = 0; aphase ^= 1; }
+    }
+  } else {
+    // ============================ epilogue (warps 2..5) ===================
+    const int quarter = warp & 3;  // TMEM lanes [32*quarter, 32*quarter + 32)
+    const int row_in_tile = quarter * 32 + lane;
+    int acc = 0;
+    uint32_t aphase = 0;
+    const SeriesParams* P = a.P;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      int tm, tn;
+      tile_coords(t, a.tiles_m, a.tiles_n, tm, tn);
+      mbar_wait(tfull + acc, aphase);
+      tc_fence_after();
+      const int r = tm * BM + row_in_tile;
+      float s2 = 0.f, h0 = 0.f, c1 = 0.f, ck = 0.f;
+      if (a.mode != GRAM) {
+        s2 = (float)P->scale2;
+        h0 = (float)(0.5 * P->c[0]);
+        c1 = (float)P->c[1];
+        ck = (float)P->c[a.k];
+      }
+#pragma unroll 1
+      for (int cc = 0; cc < BN / 32; ++cc) {
+        float v[32];
+        tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + cc * 32), v);
+        if (r < a.M) {
+          const int c0 = tn * BN + cc * 32;
+#pragma unroll 4
+          for (int j = 0; j < 32; ++j) {
+            const int c = c0 + j;
+            if (c >= a.N) break;
+            float w = v[j];
+            if (a.mode == INIT) {
+              const float x = a.wp[(int64_t)r * a.ld_w + c];
+              w = s2 * v[j] - x;                                   // W_1 = B_hat A
+              a.y[(int64_t)r * a.ld_y + c] = h0 * x + c1 * w;      // Y = c0/2 A + c1 W_1
+            } else if (a.mode == STEP) {
+              const float wp = a.wp[(int64_t)r * a.ld_w + c];
+              const float wpp = a.wpp[(int64_t)r * a.ld_w + c];
+              w = 2.f * s2 * v[j] - 2.f * wp - wpp;                // W_k = 2 B_hat W_{k-1} - W_{k-2}
+              float* yp = a.y + (int64_t)r * a.ld_y + c;
+              *yp = fmaf(ck, w, *yp);                              // Y += c_k W_k
+            }
+            const int64_t o = (int64_t)r * a.ld_out + c;
+            if (a.out_f) a.out_f[o] = w;
+            if (a.out_h) {
+              const float hi = rna_tf32(w);
+              a.out_h[o] = hi;
+              if (a.out_split == 3) a.out_l[o] = rna_tf32(w - hi);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty + acc);
+      if (++acc == 2) { acc = 0; aphase ^= 1; }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(2 * BN));
+  }
+}
+
+// ------------------------------------------------------------------ host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+
+// 2-D fp32 tensor (rows x cols, row stride ld elements), box {32 cols, box_rows}, 128B swizzle
+// (32-byte swizzle atoms for MN-major operands)
+static cudaError_t make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t cols, int64_t ld,
+                            int box_rows, bool atom32 = false) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return cudaErrorNotSupported;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * sizeof(float))};
+  cuuint32_t box[2] = {32u, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1u, 1u};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  atom32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+template <int BN, int TERMS, bool B_MN>
+static cudaError_t launch_t(const CUtensorMap& ah, const CUtensorMap& al, const CUtensorMap& bh,
+                            const CUtensorMap& bl, const TcArgs& a, int num_sms, cudaStream_t st) {
+  using S = Smem<BN, TERMS, B_MN>;
+  auto fn = k_tc_gemm<BN, TERMS, B_MN>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, S::BYTES);
+  if (e != cudaSuccess) return e;
+  const int ntiles = a.tiles_m * a.tiles_n;
+  const int grid = ntiles < num_sms ? ntiles : num_sms;
+  fn<<<grid, NTHR, S::BYTES, st>>>(ah, al, bh, bl, a);
+  return cudaGetLastError();
+}
+
+template <int BN>
+static cudaError_t tc_gemm_bn(int mode, int terms, int M, int N, int Kd, const float* Ah, const float* Al,
+                              int64_t lda, const float* Bh, const float* Bl, int64_t ldb, bool b_mn, float* out_f,
+                              float* out_h, float* out_l, int out_split, int64_t ld_out, const float* wp,
+                              const float* wpp, int64_t ld_w, float* y, int64_t ld_y, const SeriesParams* P, int k,
+                              int num_sms, cudaStream_t st) {
+  using namespace tc;
+  CUtensorMap ah, al, bh, bl;
+  cudaError_t e = make_map(&ah, Ah, M, Kd, lda, BM);
+  if (e == cudaSuccess) e = make_map(&al, terms == 3 ? Al : Ah, M, Kd, lda, BM);
+  if (b_mn) {
+    if (e == cudaSuccess) e = make_map(&bh, Bh, Kd, N, ldb, BK, true);
+    if (e == cudaSuccess) e = make_map(&bl, terms == 3 ? Bl : Bh, Kd, N, ldb, BK, true);
+  } else {
+    if (e == cudaSuccess) e = make_map(&bh, Bh, N, Kd, ldb, BN);
+    if (e == cudaSuccess) e = make_map(&bl, terms == 3 ? Bl : Bh, N, Kd, ldb, BN);
+  }
+  if (e != cudaSuccess) return e;
+  TcArgs a{};
+  a.M = M; a.N = N; a.Kd = Kd; a.terms = terms; a.mode = mode;
+  a.out_f = out_f; a.out_h = out_h; a.out_l = out_l; a.out_split = out_split; a.ld_out = ld_out;
+  a.wp = wp; a.wpp = wpp; a.ld_w = ld_w; a.y = y; a.ld_y = ld_y; a.P = P; a.k = k;
+  a.tiles_m = (M + BM - 1) / BM;
+  a.tiles_n = (N + BN - 1) / BN;
+  if (const char* v = getenv("CPA_SVT_DBG_LBO")) a.dbg_lbo = atoi(v);
+  if (const char* v = getenv("CPA_SVT_DBG_SBO")) a.dbg_sbo = atoi(v);
+  if (terms == 3) {
+    return b_mn ? launch_t<BN, 3, true>(ah, al, bh, bl, a, num_sms, st)
+                : launch_t<BN, 3, false>(ah, al, bh, bl, a, num_sms, st);
+  }
+  return b_mn ? launch_t<BN, 1, true>(ah, al, bh, bl, a, num_sms, st)
+              : launch_t<BN, 1, false>(ah, al, bh, bl, a, num_sms, st);
+}
+
+}  // namespace tc
+
+// One tcgen05 GEMM with the fused epilogue.
+//   A: M x Kd, K-major (row stride lda), given as hi (and lo) fp32 copies
+//   B: b_mn ? Kd x N (N contiguous, row stride ldb) : N x Kd (K contiguous)
+// N tile: 256 columns for single-pass TF32 on wide problems (less TMA traffic
+// per flop), else 128 (3xTF32 needs the shared memory for 3 stages of 4 operands).
+cudaError_t tc_gemm(int mode, int terms, int M, int N, int Kd, const float* Ah, const float* Al, int64_t lda,
+                    const float* Bh, const float* Bl, int64_t ldb, bool b_mn, float* out_f, float* out_h,
+                    float* out_l, int out_split, int64_t ld_out, const float* wp, const float* wpp, int64_t ld_w,
+                    float* y, int64_t ld_y, const SeriesParams* P, int k, int num_sms, cudaStream_t st) {
+  int bn = 128;
+  if (const char* v = getenv("CPA_SVT_TC_BN")) bn = atoi(v) == 256 ? 256 : 128;
+  if (bn == 256)
+    return tc::tc_gemm_bn<256>(mode, terms, M, N, Kd, Ah, Al, lda, Bh, Bl, ldb, b_mn, out_f, out_h, out_l, out_split,
+                               ld_out, wp, wpp, ld_w, y, ld_y, P, k, num_sms, st);
+  return tc::tc_gemm_bn<128>(mode, terms, M, N, Kd, Ah, Al, lda, Bh, Bl, ldb, b_mn, out_f, out_h, out_l, out_split,
+                             ld_out, wp, wpp, ld_w, y, ld_y, P, k, num_sms, st);
+}
+
+// ------------------------------------------------------------------ prep / finish
+// A (s x L, ld lda) <- X or X^T (m x n, ldx); writes full, hi, lo copies
+__global__ void k_tf32_prep(const float* X, int64_t m, int64_t n, int64_t ldx, bool transpose, float* Af, float* Ah,
+                            float* Al, int64_t lda) {
+  const int64_t s = transpose ? n : m, L = transpose ? m : n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < s * L; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i, j;
+    if (transpose) {  // read X coalesced: e -> (X row j, X col i)
+      j = e / s;
+      i = e % s;
+    } else {
+      i = e / L;
+      j = e % L;
+    }
+    const float x = transpose ? X[j * ldx + i] : X[i * ldx + j];
+    const float hi = tc::rna_tf32(x);
+    Af[i * lda + j] = x;
+    Ah[i * lda + j] = hi;
+    if (Al) Al[i * lda + j] = tc::rna_tf32(x - hi);
+  }
+}
+
+// caller Y (m x n, ldy) <- Y_int (s x L) or its transpose
+__global__ void k_tf32_finish(const float* Yi, int64_t ldi, int64_t m, int64_t n, bool transpose, float* Y,
+                              int64_t ldy) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m * n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / n, j = e % n;
+    Y[i * ldy + j] = transpose ? Yi[j * ldi + i] : Yi[i * ldi + j];
+  }
+}
+
+cudaError_t tf32_prep(const float* X, int64_t m, int64_t n, int64_t ldx, bool transpose, float* Af, float* Ah,
+                      float* Al, int64_t lda, int num_sms, cudaStream_t st) {
+  k_tf32_prep<<<num_sms * 8, 256, 0, st>>>(X, m, n, ldx, transpose, Af, Ah, Al, lda);
+  return cudaGetLastError();
+}
+cudaError_t tf32_finish(const float* Yi, int64_t ldi, int64_t m, int64_t n, bool transpose, float* Y, int64_t ldy,
+                        int num_sms, cudaStream_t st) {
+  k_tf32_finish<<<num_sms * 8, 256, 0, st>>>(Yi, ldi, m, n, transpose, Y, ldy);
+  return cudaGetLastError();
+}
+
+}  // namespace cpa

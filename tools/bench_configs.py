@@ -39,24 +39,34 @@ def timed(fn, reps, h):
     return ms[len(ms) // 2], {k: (v[0] / reps, v[1] / reps) for k, v in prof.items() if v[1]}
 
 
-def dense(name, h, reps, m=None, n=None, K=None, dtype="f64"):
+def dense(name, h, reps, m=None, n=None, K=None, dtype="f64", math="native"):
     cfg = dict(W.CONFIGS[name])
     m = m or cfg["m"]
     n = n or cfg["n"]
     K = K or cfg["K"]
     gen = {"c1": lambda: W.gen_c1(), "c2": lambda: W.gen_c2(m=m, n=n), "c5": lambda: W.gen_c5(m=m, n=n)}[name]
     X = torch.from_numpy(gen()).cuda()
+    if dtype == "f32":
+        X = X.float()
     Y = torch.empty_like(X)
     T = cfg["T"]
-    ms, ph = timed(lambda: h.apply(X, cfg["kernel"], K, T=T, Y=Y), reps, h)
+    ms, ph = timed(lambda: h.apply(X, cfg["kernel"], K, T=T, Y=Y, math=math), reps, h)
     s, L = min(m, n), max(m, n)
     F = s * (s + 1) * L + (K - 1) * 2 * s * s * L
     rec = (K - 1) * 2 * s * s * L
     step_ms = ph.get("step", (0, 0))[0] + ph.get("init", (0, 0))[0]
-    return {"config": name, "shape": [m, n], "K": K, "T": T, "dtype": dtype, "ms_per_svt": ms,
-            "gflops": F / ms / 1e6, "phases_ms": {k: v[0] for k, v in ph.items()},
-            "recurrence_tflops": rec / step_ms / 1e9 if step_ms else None,
-            "recurrence_frac_of_dmma_peak": rec / step_ms / 1e9 / PEAKS["fp64_dmma_tflops"] if step_ms else None}
+    r = {"config": name, "shape": [m, n], "K": K, "T": T, "dtype": dtype, "math": math, "ms_per_svt": ms,
+         "gflops": F / ms / 1e6, "phases_ms": {k: v[0] for k, v in ph.items()},
+         "recurrence_tflops": rec / step_ms / 1e9 if step_ms else None}
+    if dtype == "f64":
+        r["recurrence_frac_of_dmma_peak"] = rec / step_ms / 1e9 / PEAKS["fp64_dmma_tflops"] if step_ms else None
+    else:
+        terms = 3 if math == "3xtf32" else 1
+        # tf32 dense peak = measured bf16 burst / 2 (nominal ratio); 3xTF32 issues 3 MMAs per product
+        tf32_peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"] / 2
+        r["tensor_tflops_issued"] = terms * rec / step_ms / 1e9 if step_ms else None
+        r["tensor_frac_of_tf32_peak"] = terms * rec / step_ms / 1e9 / tf32_peak if step_ms else None
+    return r
 
 
 def batched(h, reps, batch=65536):
@@ -106,6 +116,10 @@ if __name__ == "__main__":
             r = dense("c1", h, reps)
         elif a == "c2":
             r = dense("c2", h, reps)
+        elif a.startswith("c5t"):         # fp32 tensor-core variant: c5t:MxN:math
+            parts = a.split(":")
+            mm, nn = map(int, parts[1].split("x")) if len(parts) > 1 else (16384, 65536)
+            r = dense("c5", h, reps, m=mm, n=nn, dtype="f32", math=parts[2] if len(parts) > 2 else "3xtf32")
         elif a.startswith("c5"):          # c5 or c5:KxM scaled, e.g. c5:8192x32768
             if ":" in a:
                 mm, nn = map(int, a.split(":")[1].split("x"))
