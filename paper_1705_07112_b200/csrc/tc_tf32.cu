@@ -162,7 +162,8 @@ struct Smem {
   static constexpr int B_BYTES = BN * BK * 4;                  // BN * 128 B per term
   static constexpr int STAGE = (TERMS == 3 ? 2 : 1) * (A_BYTES + B_BYTES);
   static constexpr int STAGES = (200 * 1024) / STAGE > 6 ? 6 : (200 * 1024) / STAGE;
-  static constexpr int BYTES = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int EPI = 4 * 32 * 33 * 4;                   // per-warp 32x33 transpose buffers
+  static constexpr int BYTES = STAGES * STAGE + EPI + 1024 /*align*/ + 256 /*barriers*/;
 };
 
 template <int BN, int TERMS, bool B_MN>
@@ -174,7 +175,8 @@ __global__ void __launch_bounds__(NTHR, 1)
   constexpr int NSPLIT = TERMS == 3 ? 2 : 1;
   extern __shared__ uint8_t raw_smem[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)raw_smem + 1023) & ~(uintptr_t)1023);
-  uint64_t* full = (uint64_t*)(smem + ST * S::STAGE);
+  float* epi_buf = (float*)(smem + ST * S::STAGE);
+  uint64_t* full = (uint64_t*)(smem + ST * S::STAGE + S::EPI);
   uint64_t* empty = full + ST;
   uint64_t* tfull = empty + ST;
   uint64_t* tempty = tfull + 2;
@@ -287,8 +289,11 @@ __global__ void __launch_bounds__(NTHR, 1)
     }
   } else {
     // ============================ epilogue (warps 2..5) ===================
-    const int quarter = warp & 3;  // TMEM lanes [32*quarter, 32*quarter + 32)
-    const int row_in_tile = quarter * 32 + lane;
+    // Each warp owns TMEM lanes [32q, 32q+32) = 32 tile rows.  Per 32-column chunk:
+    // tcgen05.ld (thread = row), transpose through a private 32x33 smem buffer,
+    // then lane = column: every global load/store is one coalesced 128-byte row segment.
+    const int quarter = warp & 3;  // TMEM lane quarter accessible to this warp
+    float* tb = epi_buf + (warp - 2) * (32 * 33);
     int acc = 0;
     uint32_t aphase = 0;
     const SeriesParams* P = a.P;
@@ -297,7 +302,7 @@ __global__ void __launch_bounds__(NTHR, 1)
       tile_coords(t, a.tiles_m, a.tiles_n, tm, tn);
       mbar_wait(tfull + acc, aphase);
       tc_fence_after();
-      const int r = tm * BM + row_in_tile;
+      const int row0 = tm * BM + quarter * 32;
       float s2 = 0.f, h0 = 0.f, c1 = 0.f, ck = 0.f;
       if (a.mode != GRAM) {
         s2 = (float)P->scale2;
@@ -309,21 +314,25 @@ __global__ void __launch_bounds__(NTHR, 1)
       for (int cc = 0; cc < BN / 32; ++cc) {
         float v[32];
         tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + cc * 32), v);
-        if (r < a.M) {
-          const int c0 = tn * BN + cc * 32;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) tb[lane * 33 + j] = v[j];
+        __syncwarp();
+        const int c = tn * BN + cc * 32 + lane;
+        if (c < a.N) {
 #pragma unroll 4
-          for (int j = 0; j < 32; ++j) {
-            const int c = c0 + j;
-            if (c >= a.N) break;
-            float w = v[j];
+          for (int i = 0; i < 32; ++i) {
+            const int r = row0 + i;
+            if (r >= a.M) break;
+            const float accv = tb[i * 33 + lane];
+            float w = accv;
             if (a.mode == INIT) {
               const float x = a.wp[(int64_t)r * a.ld_w + c];
-              w = s2 * v[j] - x;                                   // W_1 = B_hat A
+              w = s2 * accv - x;                                   // W_1 = B_hat A
               a.y[(int64_t)r * a.ld_y + c] = h0 * x + c1 * w;      // Y = c0/2 A + c1 W_1
             } else if (a.mode == STEP) {
               const float wp = a.wp[(int64_t)r * a.ld_w + c];
               const float wpp = a.wpp[(int64_t)r * a.ld_w + c];
-              w = 2.f * s2 * v[j] - 2.f * wp - wpp;                // W_k = 2 B_hat W_{k-1} - W_{k-2}
+              w = 2.f * s2 * accv - 2.f * wp - wpp;                // W_k = 2 B_hat W_{k-1} - W_{k-2}
               float* yp = a.y + (int64_t)r * a.ld_y + c;
               *yp = fmaf(ck, w, *yp);                              // Y += c_k W_k
             }
@@ -336,6 +345,7 @@ __global__ void __launch_bounds__(NTHR, 1)
             }
           }
         }
+        __syncwarp();
       }
       tc_fence_before();
       __syncwarp();
