@@ -96,6 +96,16 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def max_over_ranks(value: float, device) -> float:
+    """Max of a per-rank number over the torch.distributed world (identity when not initialised)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def oracle_step(cfg, X):
     """One oracle pass over the workload (cpu_baseline / --impl reference legs only)."""
     import oracle as O
@@ -219,11 +229,7 @@ def run_ours(args, cfg):
     prof = h.profile_read()
     h.profile(False)
     gpu_launches = h.launches - launches0
-    ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
+    ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in ev) / args.steps, torch.device("cuda", local))
     value = world * cfg["F"] / (ms * 1e-3) / 1e9
 
     # ---------------- e2e: C-ABI call with HOST buffers ----------------
@@ -241,11 +247,7 @@ def run_ours(args, cfg):
         ee[i][1].record(stream)
     torch.cuda.synchronize()
     barrier()
-    ms_e2e = sum(a.elapsed_time(b) for a, b in ee) / args.steps
-    t = torch.tensor([ms_e2e], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_e2e = float(t.item())
+    ms_e2e = max_over_ranks(sum(a.elapsed_time(b) for a, b in ee) / args.steps, torch.device("cuda", local))
     nbytes = X.size * 8
 
     # ---------------- roofline of the dominant kernel (fused step) ----------------
