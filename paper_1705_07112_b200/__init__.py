@@ -15,7 +15,7 @@ import os
 __all__ = ["Kernel", "Lambda", "Info", "Handle", "coeffs", "CpaSvtError", "kernel_from_dict",
            "LIB_PATH", "STATUS", "HARD", "SOFT", "WSOFT", "lib"]
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libcpasvt.so")
+LIB_PATH = os.environ.get("CPA_SVT_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libcpasvt.so")
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python paper_1705_07112_b200/build.py` "
                       "(there is no CPU fallback)")

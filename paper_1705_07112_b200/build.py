@@ -13,26 +13,34 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
          "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"), "--expt-relaxed-constexpr"]
 
 
-def build(verbose=False, force=False):
+def build(verbose=False, force=False, defines=(), lib=LIB, tag=""):
     objs = []
-    os.makedirs(os.path.join(HERE, "build"), exist_ok=True)
+    bdir = os.path.join(HERE, "build" + tag)
+    os.makedirs(bdir, exist_ok=True)
     for s in SOURCES:
         src = os.path.join(CSRC, s)
-        obj = os.path.join(HERE, "build", s.replace(".cu", ".o"))
+        obj = os.path.join(bdir, s.replace(".cu", ".o"))
         deps = [src, os.path.join(CSRC, "common.cuh"), os.path.join(ROOT, "include", "cpa_svt.h")]
         if force or not os.path.exists(obj) or os.path.getmtime(obj) < max(os.path.getmtime(d) for d in deps):
-            cmd = [NVCC, *FLAGS, "-c", src, "-o", obj]
+            cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
             if verbose:
                 cmd.insert(1, "-Xptxas=-v")
                 print(" ".join(cmd))
             subprocess.run(cmd, check=True)
         objs.append(obj)
-    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
-        subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB, *objs,
+    if force or not os.path.exists(lib) or os.path.getmtime(lib) < max(os.path.getmtime(o) for o in objs):
+        subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", lib, *objs,
                         "-ldl"], check=True)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    build(verbose="-v" in sys.argv, force="-f" in sys.argv)
-    print(LIB)
+    # python build.py [-v] [-f] [--variant TAG DEF1=V DEF2=V ...]  (experiments: lib_TAG.so)
+    if "--variant" in sys.argv:
+        i = sys.argv.index("--variant")
+        tag, defs = sys.argv[i + 1], sys.argv[i + 2:]
+        print(build(verbose="-v" in sys.argv[:i], force=True, defines=defs,
+                    lib=os.path.join(HERE, f"libcpasvt_{tag}.so"), tag="_" + tag))
+    else:
+        build(verbose="-v" in sys.argv, force="-f" in sys.argv)
+        print(LIB)

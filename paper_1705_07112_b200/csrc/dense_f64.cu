@@ -11,11 +11,19 @@
 //
 // CTA tile 64x64, k-slab 16, 4 warps of 32x32 (4x4 DMMA tiles), 4-stage
 // cp.async pipeline (16-byte copies when the leading dimension allows).
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace cpa {
 
-constexpr int BM = 64, BN = 64, BKS = 16, STAGES = 4, NTHREADS = 128;
+#ifndef CPA_DMMA_BK
+#define CPA_DMMA_BK 16
+#endif
+#ifndef CPA_DMMA_STAGES
+#define CPA_DMMA_STAGES 4
+#endif
+constexpr int BM = 64, BN = 64, BKS = CPA_DMMA_BK, STAGES = CPA_DMMA_STAGES, NTHREADS = 128;
 constexpr int PAD = 4;
 
 enum EpiMode { EPI_GRAM = 0, EPI_INIT = 1, EPI_STEP = 2 };
@@ -433,6 +441,7 @@ static int flow_split(int64_t m, int64_t n, int64_t s, int num_sms) {
   const int64_t nk = (s + BKS - 1) / BKS;
   int split = 1;
   while (split < 8 && tiles * split < 6 * num_sms && nk / (2 * split) >= 4) split *= 2;
+  if (const char* v = getenv("CPA_SVT_FLOW_SPLIT")) split = atoi(v) > 0 ? atoi(v) : split;
   return split;
 }
 

@@ -92,6 +92,11 @@ __device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned int ld_relaxed_u32(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void red_release_add(unsigned int* p, unsigned int v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
@@ -113,7 +118,8 @@ __global__ void __launch_bounds__(256) k_power_dense(PowerArgs<E> a) {
   const T* Gc = a.q > 0 ? a.G4 : a.G;  // the matrix whose rows are cached
   const int niter = a.T - 3 * a.q;
   if (a.cache_rows) {
-    for (int64_t e = threadIdx.x; e < (r1 - r0) * s; e += blockDim.x) sg[e] = Gc[(r0 + e / s) * a.ld + e % s];
+    for (int64_t r = r0; r < r1; ++r)
+      for (int64_t j = threadIdx.x; j < s; j += blockDim.x) sg[(r - r0) * s + j] = Gc[r * a.ld + j];
   }
   const double v0 = 1.0 / sqrt((double)s);
   for (int64_t j = threadIdx.x; j < s; j += blockDim.x) sv[j] = v0;
@@ -150,21 +156,43 @@ __global__ void __launch_bounds__(256) k_power_dense(PowerArgs<E> a) {
       // arrive (release, cumulative over the bar.sync above): publishes u_t and the partial
       red_release_add(a.bar, 1u);
       const unsigned int target = nb * (unsigned)(t + 1);
-      while (ld_acquire_u32(a.bar) < target) {
+      while (ld_relaxed_u32(a.bar) < target) {
       }
+      __threadfence();  // acquire: the other CTAs' u_t and partials are visible below
     }
     __syncthreads();
     // ||u_t||: warp 0 re-sums the partials in a fixed order (identical in every CTA)
     if (warp == 0) {
       const double* pp = a.part + (t & 1) * nb;
+      double qv[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const unsigned b = lane + 32 * i;
+        qv[i] = b < nb ? __ldcg(pp + b) : 0.0;
+      }
       double q = 0.0;
-      for (unsigned b = lane; b < nb; b += 32) q += __ldcg(pp + b);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) q += qv[i];
+      for (unsigned b = lane + 256; b < nb; b += 32) q += __ldcg(pp + b);
       q = warp_sum(q);
       if (lane == 0) s_norm = sqrt(q);
     }
-    // stage u_t; v_t = u_t / ||u_t|| is applied inside the next product
+    // stage u_t (all loads in flight before the first store); v_t = u_t / ||u_t||
+    // is applied inside the next product
     const double* up = a.ubuf + (t & 1) * s;
-    for (int64_t j = threadIdx.x; j < s; j += blockDim.x) sv[j] = __ldcg(up + j);
+    for (int64_t j0 = 0; j0 < s; j0 += 8 * blockDim.x) {
+      double uv[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int64_t j = j0 + threadIdx.x + (int64_t)i * blockDim.x;
+        uv[i] = j < s ? __ldcg(up + j) : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int64_t j = j0 + threadIdx.x + (int64_t)i * blockDim.x;
+        if (j < s) sv[j] = uv[i];
+      }
+    }
     __syncthreads();
     lam = s_norm;
     if (!(lam > kDegenerateLambda) || !(lam < 1e300)) { lam = lam < 1e300 ? 0.0 : lam; break; }
@@ -231,16 +259,11 @@ static cudaError_t launch_power_t(const E* G, const E* G4, int64_t s, int64_t ld
   const size_t budget = 200 * 1024;
   size_t smem = (size_t)s * sizeof(double);
   if (smem > budget) return cudaErrorInvalidValue;  // s > 25600 not supported by this kernel
-  int64_t rows_fit = (int64_t)((budget - smem) / ((size_t)s * sizeof(E)));
-  int64_t grid;
-  if (rows_fit >= 1 && (s + rows_fit - 1) / rows_fit <= num_sms) {
-    int64_t g0 = (s + rows_fit - 1) / rows_fit;
-    grid = g0;
-    a.cache_rows = 1;
-  } else {
-    grid = s < num_sms ? s : num_sms;
-    a.cache_rows = 0;
-  }
+  // One CTA per SM (the product is latency-bound: fewer rows per CTA shortens
+  // it); rows cached in shared memory when they fit.
+  int64_t grid = s < num_sms ? s : num_sms;
+  const int64_t rows_per = (s + grid - 1) / grid;
+  a.cache_rows = smem + (size_t)rows_per * s * sizeof(E) <= budget;
   if (grid < 1) grid = 1;
   a.rows_per_cta = (int)((s + grid - 1) / grid);
   grid = (s + a.rows_per_cta - 1) / a.rows_per_cta;

@@ -54,6 +54,27 @@ __global__ void k_dmma(double* out, int iters) {
   if (s == 12345.678) out[0] = s;
 }
 
+// FFMA with all three sources in (distinct, thread-varying) registers: the form a
+// register-tiled outer-product GEMM issues.
+template <int ILP>
+__global__ void k_ffma3(float* out, int iters) {
+  float acc[ILP], a[4], b[4];
+#pragma unroll
+  for (int i = 0; i < ILP; ++i) acc[i] = threadIdx.x * 1e-3f + i;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) { a[i] = 0.999f - threadIdx.x * 1e-6f * i; b[i] = 1e-3f * (i + 1) + threadIdx.x * 1e-7f; }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < ILP; ++i) acc[i] = fmaf(a[i & 3], b[(i >> 2) & 3], acc[i]);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) { a[i] = __shfl_xor_sync(0xffffffffu, a[i], 1) * 1.0000001f; }
+  }
+  float s = 0;
+#pragma unroll
+  for (int i = 0; i < ILP; ++i) s += acc[i];
+  if (s == 12345.678f) out[0] = s;
+}
+
 int main() {
   int dev = 0, nsm = 0, clk = 0, l2 = 0, smem = 0;
   CK(cudaSetDevice(dev));
@@ -83,6 +104,11 @@ int main() {
     CK(cudaEventSynchronize(e1)); cudaEventElapsedTime(&ms, e0, e1);
     fl = 2.0 * 8 * iters * (double)grid * thr;
     printf(", \"ffma_tflops_b%d\": %.3f", blocks_per_sm, fl / ms / 1e9);
+    k_ffma3<16><<<grid, thr>>>((float*)dout, 100);
+    cudaEventRecord(e0); k_ffma3<16><<<grid, thr>>>((float*)dout, iters / 2); cudaEventRecord(e1);
+    CK(cudaEventSynchronize(e1)); cudaEventElapsedTime(&ms, e0, e1);
+    fl = 2.0 * 16 * (iters / 2) * (double)grid * thr;
+    printf(", \"ffma3reg_tflops_b%d\": %.3f", blocks_per_sm, fl / ms / 1e9);
   }
   printf("}\n");
   return 0;
