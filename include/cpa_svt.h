@@ -184,6 +184,15 @@ cpa_svt_status cpa_svt_apply_batched(cpa_svt_handle* h, int64_t batch, int m, in
                                      const float* X, float* Y, const cpa_svt_kernel* k, int K,
                                      const cpa_svt_lambda* lam, float* lambda_out);
 
+/* Handle options (cpa_svt_set_option). */
+typedef enum {
+  CPA_SVT_OPT_FORM = 0      /* dense recurrence form: 0 = auto (fewest flops), 1 = apply-to-X
+                               (W_k = Psi_k(B_hat) X, (K-1) 2 s^2 L flops), 2 = Alg. 1 literal s x s form
+                               (H_hat = sum c_k Psi_k(B_hat) formed on the s x s Gram, then one product
+                               Y = H_hat X: 2(K-2) s^3 + 2 s^2 L flops) */
+} cpa_svt_option;
+cpa_svt_status cpa_svt_set_option(cpa_svt_handle* h, cpa_svt_option opt, int64_t value);
+
 /* Per-phase device timing for measurement: when enabled, the library records a
  * CUDA event pair on the handle's stream around every launch it makes and
  * accumulates the elapsed time per phase (no host sync until read). */
@@ -196,7 +205,8 @@ typedef enum {
   CPA_SVT_PH_SPARSE_Z = 5,   /* sparse: Z = W_{k-1} X^T */
   CPA_SVT_PH_SPARSE_W = 6,   /* sparse: W_k = (4/L) Z X - 2 W_{k-1} - W_{k-2}, Y += c_k W_k */
   CPA_SVT_PH_BATCHED = 7,    /* batched kernel */
-  CPA_SVT_PH_COUNT = 8
+  CPA_SVT_PH_FINAL = 8,      /* s x s form: the final product Y = H_hat X */
+  CPA_SVT_PH_COUNT = 9
 } cpa_svt_phase;
 /* enable != 0: reset the accumulators and start recording; 0: stop. */
 cpa_svt_status cpa_svt_profile(cpa_svt_handle* h, int enable);

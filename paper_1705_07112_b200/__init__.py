@@ -78,7 +78,10 @@ lib.cpa_svt_debug_gemm_tf32.argtypes = [_p, ctypes.c_int, ctypes.c_int, ctypes.c
 lib.cpa_svt_debug_gemm_tf32.restype = ctypes.c_int
 lib.cpa_svt_profile.argtypes = [_p, ctypes.c_int]
 lib.cpa_svt_profile_read.argtypes = [_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)]
-PHASES = ["gram", "allreduce", "power", "init", "step", "sparse_z", "sparse_w", "batched"]
+PHASES = ["gram", "allreduce", "power", "init", "step", "sparse_z", "sparse_w", "batched", "final"]
+lib.cpa_svt_set_option.argtypes = [_p, ctypes.c_int, _i64]
+lib.cpa_svt_set_option.restype = ctypes.c_int
+FORM = {"auto": 0, "apply": 1, "poly": 2}
 for _f in ("cpa_svt_init", "cpa_svt_free", "cpa_svt_nccl_unique_id", "cpa_svt_coeffs", "cpa_svt_apply",
            "cpa_svt_apply_host", "cpa_svt_apply_csr", "cpa_svt_apply_batched", "cpa_svt_profile",
            "cpa_svt_profile_read"):
@@ -143,6 +146,10 @@ class Handle:
     @property
     def launches(self) -> int:
         return lib.cpa_svt_launch_count(self._h)
+
+    def set_form(self, form: str):
+        """cpa_svt_set_option(FORM): 'auto' | 'apply' (W_k = Psi_k X) | 'poly' (Alg. 1 s x s form)."""
+        self._check(lib.cpa_svt_set_option(self._h, 0, FORM[form]), "cpa_svt_set_option")
 
     def profile(self, enable: bool = True):
         """cpa_svt_profile: reset and start (or stop) per-phase CUDA-event timing."""

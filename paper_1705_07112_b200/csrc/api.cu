@@ -23,6 +23,9 @@ cudaError_t dense_cheb_launch(bool left, bool init, int64_t m, int64_t n, const 
                               int k, cudaStream_t st);
 size_t dense_flow_sync_ints(int64_t m, int64_t n, int K);
 size_t dense_flow_partial_doubles(int64_t m, int64_t n, int num_sms);
+cudaError_t dense_gemm_store(int64_t M, int64_t N, int64_t Kd, const double* A, int64_t lda, const double* B,
+                             int64_t ldb, double* C, int64_t ldc, cudaStream_t st);
+cudaError_t dense_eye(double* I, int64_t s, cudaStream_t st);
 cudaError_t dense_cheb_flow(bool left, int64_t m, int64_t n, const double* G, const double* X, int64_t ldx,
                             double* Wa, double* Wb, double* Y, int64_t ldy, const SeriesParams* P, int K, int* sync,
                             double* partial, int num_sms, cudaStream_t st);
@@ -105,6 +108,7 @@ struct cpa_svt_handle {
   std::string err;
   int64_t launches = 0;
   bool use_flow = true;            // persistent dataflow recurrence (CPA_SVT_FLOW=0: one launch per step)
+  int form = 0;                    // CPA_SVT_OPT_FORM
   // profiling (cpa_svt_profile): event pairs per phase, resolved at read time
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -297,6 +301,16 @@ cpa_svt_status cpa_svt_free(cpa_svt_handle* h) {
   return CPA_SVT_OK;
 }
 
+cpa_svt_status cpa_svt_set_option(cpa_svt_handle* h, cpa_svt_option opt, int64_t value) {
+  if (!h) return CPA_SVT_E_ARG;
+  if (opt == CPA_SVT_OPT_FORM) {
+    if (value < 0 || value > 2) return CPA_SVT_E_ARG;
+    h->form = (int)value;
+    return CPA_SVT_OK;
+  }
+  return CPA_SVT_E_ARG;
+}
+
 cpa_svt_status cpa_svt_profile(cpa_svt_handle* h, int enable) {
   if (!h) return CPA_SVT_E_ARG;
   if (enable) {
@@ -390,6 +404,52 @@ struct PhaseTimer {
   }
 };
 
+// Alg. 1 lines 5-11 on (M x N) W_0 = Xsrc: the persistent dataflow kernel, or one
+// launch per step (CPA_SVT_FLOW=0).  Y receives sum_k c_k W_k.
+static cpa_svt_status run_recurrence_f64(cpa_svt_handle* h, bool left, int64_t M, int64_t N, const double* G,
+                                         const double* Xsrc, int64_t ldx, double* Wa, double* Wb, double* Y,
+                                         int64_t ldy, int K, double* part, int* sync, int* launches) {
+  if (h->use_flow && K > 2) {
+    Phase p(h, CPA_SVT_PH_STEP);
+    CU(dense_cheb_flow(left, M, N, G, Xsrc, ldx, Wa, Wb, Y, ldy, h->P, K, sync, part, h->num_sms, h->stream));
+    ++*launches;
+    return CPA_SVT_OK;
+  }
+  {
+    Phase p(h, CPA_SVT_PH_INIT);
+    CU(dense_cheb_launch(left, true, M, N, G, Xsrc, ldx, nullptr, 0, K > 2 ? Wa : nullptr, N, Y, ldy, h->P, 1,
+                         h->stream));
+  }
+  ++*launches;
+  for (int kk = 2; kk < K; ++kk) {
+    const double *src, *pp;
+    double* out;
+    int64_t ldsrc, ldpp;
+    if (kk == 2) {
+      src = Wa; ldsrc = N; pp = Xsrc; ldpp = ldx; out = Wb;
+    } else {
+      out = (kk & 1) ? Wa : Wb;      // W_k overwrites W_{k-2} in place
+      src = (kk & 1) ? Wb : Wa;
+      ldsrc = N; pp = out; ldpp = N;
+    }
+    if (kk == K - 1) out = nullptr;  // last W_k is never read again
+    Phase p(h, CPA_SVT_PH_STEP);
+    CU(dense_cheb_launch(left, false, M, N, G, src, ldsrc, pp, ldpp, out, N, Y, ldy, h->P, kk, h->stream));
+    ++*launches;
+  }
+  return CPA_SVT_OK;
+}
+
+// Which dense form runs (CPA_SVT_OPT_FORM): the s x s polynomial form of Alg. 1
+// costs 2(K-2)s^3 + 2s^2 L against (K-1) 2 s^2 L for apply-to-X -- fewer flops
+// whenever s < L (NEXT-1).
+static bool use_poly_form(const cpa_svt_handle* h, int64_t s, int64_t L, int K) {
+  if (K <= 2) return false;
+  if (h->form == 1) return false;
+  if (h->form == 2) return true;
+  return s < L;
+}
+
 static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt_shard shard,
                                 int64_t long_global, const double* X, int64_t ldx, double* Y, int64_t ldy,
                                 const cpa_svt_kernel* k, int K, const double* c, cpa_svt_lambda* lam,
@@ -405,20 +465,25 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
   } else {
     left = m <= n;
   }
-  const int64_t s = left ? m : n;
+  const int64_t s = left ? m : n, L = left ? n : m;
   const bool sharded = shard != CPA_SVT_SHARD_NONE && h->world > 1;
-  // workspace: G (s*s) | W_a (m*n) | W_b (m*n) | power scratch | split-K partials | flow sync ints
+  const bool poly = use_poly_form(h, s, sharded ? long_global : L, K);
+  // workspace: G (s*s) | W_a | W_b | [I_s | H (s*s) in the poly form] | power scratch | split-K partials | sync
   // (G^2 and G^4 for the squared power iteration live in W_a / W_b: free until the recurrence)
-  const size_t nG = (size_t)s * s, nW = (size_t)m * n, nPow = power_dense_scratch_doubles(s);
-  const size_t nPart = dense_flow_partial_doubles(m, n, h->num_sms);
-  const size_t nSync = dense_flow_sync_ints(m, n, K);
-  const size_t need = (nG + 2 * nW + nPow + nPart) * sizeof(double) + nSync * sizeof(int) + 256;
+  const int64_t RM = poly ? s : m, RN = poly ? s : n;  // shape the recurrence runs on
+  const size_t nG = (size_t)s * s, nW = (size_t)RM * RN, nPow = power_dense_scratch_doubles(s);
+  const size_t nX = poly ? 2 * nG : 0;
+  const size_t nPart = dense_flow_partial_doubles(RM, RN, h->num_sms);
+  const size_t nSync = dense_flow_sync_ints(RM, RN, K);
+  const size_t need = (nG + 2 * nW + nX + nPow + nPart) * sizeof(double) + nSync * sizeof(int) + 256;
   cpa_svt_status st = grow(h, &h->ws, &h->ws_bytes, need);
   if (st != CPA_SVT_OK) return st;
   double* G = (double*)h->ws;
   double* Wa = G + nG;
   double* Wb = Wa + nW;
-  double* pw = Wb + nW;
+  double* Is = Wb + nW;          // poly form: identity (W_0)
+  double* H = Is + nG;           // poly form: H_hat
+  double* pw = Wb + nW + nX;
   double* part = pw + nPow;
   int* flow_sync = (int*)(part + nPart);
 
@@ -471,34 +536,21 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
     NC(g_nccl.Broadcast(h->P, h->P, sizeof(SeriesParams), ncclChar, 0, h->comm, h->stream));
   }
   tm.mark();
-  // Alg. 1 lines 5-11 in the apply-to-X form
-  if (h->use_flow && K > 2) {
-    Phase p(h, CPA_SVT_PH_STEP);
-    CU(dense_cheb_flow(left, m, n, G, X, ldx, Wa, Wb, Y, ldy, h->P, K, flow_sync, part, h->num_sms, h->stream));
-    ++launches;
+  if (!poly) {
+    // Alg. 1 lines 5-11 in the apply-to-X form: W_k = Psi_k(B_hat) X, Y = sum c_k W_k
+    st = run_recurrence_f64(h, left, m, n, G, X, ldx, Wa, Wb, Y, ldy, K, part, flow_sync, &launches);
+    if (st != CPA_SVT_OK) return st;
   } else {
-    {
-      Phase p(h, CPA_SVT_PH_INIT);
-      CU(dense_cheb_launch(left, true, m, n, G, X, ldx, nullptr, 0, K > 2 ? Wa : nullptr, n, Y, ldy, h->P, 1,
-                           h->stream));
-    }
+    // Alg. 1 literally: lines 5-11 on the s x s Gram with Psi_0 = Id (H_hat = sum c_k Psi_k),
+    // then line 12: Y = H_hat X (left) or X H_hat (right) -- one product
+    CU(dense_eye(Is, s, h->stream));
     ++launches;
-    for (int kk = 2; kk < K; ++kk) {
-      const double *src, *pp;
-      double* out;
-      int64_t ldsrc, ldpp;
-      if (kk == 2) {
-        src = Wa; ldsrc = n; pp = X; ldpp = ldx; out = Wb;
-      } else {
-        out = (kk & 1) ? Wa : Wb;      // W_k overwrites W_{k-2} in place
-        src = (kk & 1) ? Wb : Wa;
-        ldsrc = n; pp = out; ldpp = n;
-      }
-      if (kk == K - 1) out = nullptr;  // last W_k is never read again
-      Phase p(h, CPA_SVT_PH_STEP);
-      CU(dense_cheb_launch(left, false, m, n, G, src, ldsrc, pp, ldpp, out, n, Y, ldy, h->P, kk, h->stream));
-      ++launches;
-    }
+    st = run_recurrence_f64(h, true, s, s, G, Is, s, Wa, Wb, H, s, K, part, flow_sync, &launches);
+    if (st != CPA_SVT_OK) return st;
+    Phase p(h, CPA_SVT_PH_FINAL);
+    if (left) CU(dense_gemm_store(s, n, s, H, s, X, ldx, Y, ldy, h->stream));
+    else      CU(dense_gemm_store(m, s, s, X, ldx, H, s, Y, ldy, h->stream));
+    ++launches;
   }
   tm.mark();
   h->launches += launches;

@@ -26,7 +26,7 @@ namespace cpa {
 constexpr int BM = 64, BN = 64, BKS = CPA_DMMA_BK, STAGES = CPA_DMMA_STAGES, NTHREADS = 128;
 constexpr int PAD = 4;
 
-enum EpiMode { EPI_GRAM = 0, EPI_INIT = 1, EPI_STEP = 2 };
+enum EpiMode { EPI_GRAM = 0, EPI_INIT = 1, EPI_STEP = 2, EPI_STORE = 3 };
 
 struct GemmArgs {
   int64_t M, N, Kd;             // C (M x N) = A (M x Kd) * B (Kd x N)
@@ -363,6 +363,18 @@ __global__ void __launch_bounds__(NTHREADS) k_dmma_gemm(GemmArgs a) {
         }
     return;
   }
+  if (MODE == EPI_STORE) {  // plain product (Alg. 1 line 12: Y = H_hat X or X H_hat)
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t r = m0 + wm + i * 8 + g, c = n0 + wn + j * 8 + 2 * t + e;
+          if (r < a.M && c < a.N) a.Y[r * a.ldy + c] = acc[i][j][e];
+        }
+    return;
+  }
   cheb_epilogue(acc, m0, n0, a.M, a.N, MODE == EPI_INIT, a.Wp, a.ldwp, a.Wpp, a.ldwpp, a.Wout, a.ldwo, a.Y, a.ldy,
                 a.P, a.k);
 }
@@ -431,6 +443,28 @@ cudaError_t dense_cheb_launch(bool left, bool init, int64_t m, int64_t n, const 
   if (m == 0 || n == 0) return cudaSuccess;
   if (left) return init ? launch<false, false, EPI_INIT>(a, st) : launch<false, false, EPI_STEP>(a, st);
   return init ? launch<true, false, EPI_INIT>(a, st) : launch<true, false, EPI_STEP>(a, st);
+}
+
+// C (M x N, ldc) = A (M x Kd, row-major, k contiguous) * B (Kd x N, row-major, n contiguous).
+// Used for Alg. 1 line 12 in the s x s polynomial form: Y = H_hat X (left) or X H_hat (right).
+cudaError_t dense_gemm_store(int64_t M, int64_t N, int64_t Kd, const double* A, int64_t lda, const double* B,
+                             int64_t ldb, double* C, int64_t ldc, cudaStream_t st) {
+  GemmArgs a{};
+  a.M = M; a.N = N; a.Kd = Kd;
+  a.A = A; a.lda = lda; a.B = B; a.ldb = ldb;
+  a.vec_a = aligned16(A, lda); a.vec_b = aligned16(B, ldb);
+  a.Y = C; a.ldy = ldc;
+  if (M == 0 || N == 0) return cudaSuccess;
+  return launch<true, false, EPI_STORE>(a, st);
+}
+
+__global__ void k_eye(double* I, int64_t s) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < s * s; e += (int64_t)gridDim.x * blockDim.x)
+    I[e] = (e / s == e % s) ? 1.0 : 0.0;
+}
+cudaError_t dense_eye(double* I, int64_t s, cudaStream_t st) {
+  k_eye<<<1184, 256, 0, st>>>(I, s);
+  return cudaGetLastError();
 }
 
 // Whole recurrence (init + K-2 steps) in one persistent launch.

@@ -190,3 +190,22 @@ def test_flow_kernel_matches_per_step(env, shape, K):
     assert O.rel_fro(out["1"], out["0"]) <= 1e-13
     ref = O.cpa_shrink(X, O.Kernel(**kern), K, T=50)
     assert O.rel_fro(out["1"], ref) <= TOL64 and O.rel_fro(out["0"], ref) <= TOL64
+
+
+@pytest.mark.parametrize("shape,K", [((100, 257), 12), ((257, 100), 9), ((64, 48), 20), ((300, 1000), 30),
+                                     ((129, 129), 5), ((1, 7), 3)])
+def test_both_forms_match_oracle(env, shape, K):
+    """Alg. 1 literal s x s form (H_hat formed, then Y = H_hat X) and the apply-to-X
+    form agree with the oracle and with each other (NEXT-1)."""
+    torch, P, _ = env
+    X = W.gen_c2(m=shape[0], n=shape[1], seed=11)
+    kern = {"kind": "soft", "tau": 0.1, "tau_relative": True}
+    ref = O.cpa_shrink(X, O.Kernel(**kern), K, T=80)
+    out = {}
+    for form in ("poly", "apply"):
+        h2 = P.Handle(0)
+        h2.set_form(form)
+        out[form] = h2.apply(torch.from_numpy(X).cuda(), kern, K, T=80).cpu().numpy()
+        h2.close()
+        assert O.rel_fro(out[form], ref) <= TOL64, form
+    assert O.rel_fro(out["poly"], out["apply"]) <= 1e-12

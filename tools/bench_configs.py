@@ -52,10 +52,12 @@ def dense(name, h, reps, m=None, n=None, K=None, dtype="f64", math="native"):
     T = cfg["T"]
     ms, ph = timed(lambda: h.apply(X, cfg["kernel"], K, T=T, Y=Y, math=math), reps, h)
     s, L = min(m, n), max(m, n)
-    F = s * (s + 1) * L + (K - 1) * 2 * s * s * L
-    rec = (K - 1) * 2 * s * s * L
+    poly = "final" in ph  # Alg. 1 s x s form: 2(K-2)s^3 recurrence + 2 s^2 L final product
+    rec = (K - 2) * 2 * s ** 3 + 2 * s * s * s if poly else (K - 1) * 2 * s * s * L
+    F = s * (s + 1) * L + rec + (2 * s * s * L if poly else 0)
     step_ms = ph.get("step", (0, 0))[0] + ph.get("init", (0, 0))[0]
-    r = {"config": name, "shape": [m, n], "K": K, "T": T, "dtype": dtype, "math": math, "ms_per_svt": ms,
+    r = {"config": name, "shape": [m, n], "K": K, "T": T, "dtype": dtype, "math": math,
+         "form": "poly (Alg. 1 s x s)" if poly else "apply-to-X", "ms_per_svt": ms,
          "gflops": F / ms / 1e6, "phases_ms": {k: v[0] for k, v in ph.items()},
          "recurrence_tflops": rec / step_ms / 1e9 if step_ms else None}
     if dtype == "f64":
