@@ -50,6 +50,7 @@ cudaError_t tf32_prep(const float* X, int64_t m, int64_t n, int64_t ldx, bool tr
                       float* Al, int64_t lda, int num_sms, cudaStream_t st);
 cudaError_t tf32_finish(const float* Yi, int64_t ldi, int64_t m, int64_t n, bool transpose, float* Y, int64_t ldy,
                         int num_sms, cudaStream_t st);
+cudaError_t tf32_eye(float* I, int64_t s, int64_t ld, int num_sms, cudaStream_t st);
 // batched_f32.cu
 cudaError_t launch_batched_f32(int64_t batch, int m, int n, const float* X, float* Y, const cpa_svt_kernel& k,
                                int K, int T, double safety, double lam_override, float* lambda_out,
@@ -586,20 +587,36 @@ static cpa_svt_status apply_tf32(cpa_svt_handle* h, int terms, int64_t m, int64_
   const int64_t s = left ? m : n, L = left ? n : m;
   if (s > 2147483647 / 2 || L > 2147483647 / 2) return CPA_SVT_E_UNSUPPORTED;
   const int64_t sp = (s + 3) / 4 * 4, Lp = (L + 3) / 4 * 4;
+  const bool poly = use_poly_form(h, s, sharded ? long_global : L, K);
   auto al = [](size_t b) { return (b + 255) / 256 * 256; };
   const size_t nA = al((size_t)s * Lp * 4), nG = al((size_t)s * sp * 4);
   const size_t nPow = al(power_dense_scratch_doubles(s) * 8);
-  const size_t need = 7 * nA + 3 * nG + nPow + 256;
+  // X set (full, hi, lo) | Y_int | G (full, hi, lo) | apply: A set (3 x s*Lp)  poly: I set, B set, H (3 x s*sp each)
+  const size_t need = 4 * nA + 3 * nG + (poly ? 9 * nG : 3 * nA) + nPow + 256;
   cpa_svt_status st = grow(h, &h->ws, &h->ws_bytes, need);
   if (st != CPA_SVT_OK) return st;
   char* b = (char*)h->ws;
-  float* Xs[3] = {(float*)b, (float*)(b + nA), (float*)(b + 2 * nA)};            // full, hi, lo (set X)
-  float* As[3] = {(float*)(b + 3 * nA), (float*)(b + 4 * nA), (float*)(b + 5 * nA)};  // set A
-  float* Yi = (float*)(b + 6 * nA);
-  float* Gf = (float*)(b + 7 * nA);
-  float* Gh = (float*)(b + 7 * nA + nG);
-  float* Gl = (float*)(b + 7 * nA + 2 * nG);
-  double* pw = (double*)(b + 7 * nA + 3 * nG);
+  float* Xs[3] = {(float*)b, (float*)(b + nA), (float*)(b + 2 * nA)};
+  float* Yi = (float*)(b + 3 * nA);
+  float* Gf = (float*)(b + 4 * nA);
+  float* Gh = (float*)(b + 4 * nA + nG);
+  float* Gl = (float*)(b + 4 * nA + 2 * nG);
+  char* rest = b + 4 * nA + 3 * nG;
+  float* As[3];
+  float* Is[3];
+  float* Hs[3];
+  double* pw;
+  if (!poly) {
+    for (int i = 0; i < 3; ++i) As[i] = (float*)(rest + i * nA);
+    pw = (double*)(rest + 3 * nA);
+  } else {
+    for (int i = 0; i < 3; ++i) {
+      Is[i] = (float*)(rest + i * nG);
+      As[i] = (float*)(rest + (3 + i) * nG);
+      Hs[i] = (float*)(rest + (6 + i) * nG);
+    }
+    pw = (double*)(rest + 9 * nG);
+  }
   const double* c_dev = nullptr;
   if (c) {
     CU(cudaMemcpyAsync(h->d_c, c, K * sizeof(double), cudaMemcpyHostToDevice, h->stream));
@@ -640,16 +657,33 @@ static cpa_svt_status apply_tf32(cpa_svt_handle* h, int terms, int64_t m, int64_
     NC(g_nccl.Broadcast(h->P, h->P, sizeof(SeriesParams), ncclChar, 0, h->comm, h->stream));
   }
   tm.mark();
-  float** sets[2] = {Xs, As};
+  // W_0 and the shape of the recurrence: apply-to-X (s x L, W_0 = A) or the s x s form (W_0 = Id)
+  float** W0 = poly ? Is : Xs;
+  const int64_t RN = poly ? s : L, ldr = poly ? sp : Lp;
+  float* Yr = poly ? Hs[0] : Yi;
+  if (poly) {
+    CU(tf32_eye(Is[0], s, sp, h->num_sms, h->stream));
+    CU(tf32_prep(Is[0], s, sp, sp, false, Is[0], Is[1], Is[2], sp, h->num_sms, h->stream));
+    launches += 2;
+  }
+  float** sets[2] = {W0, As};
   for (int kk = 1; kk < K; ++kk) {
-    float** src = sets[(kk - 1) & 1];      // W_{k-1}: k=1 -> X set
+    float** src = sets[(kk - 1) & 1];      // W_{k-1}: k=1 -> W_0
     float** out = sets[kk & 1];            // W_k overwrites W_{k-2} (k >= 2)
     const bool last = kk == K - 1;
     Phase p(h, kk == 1 ? CPA_SVT_PH_INIT : CPA_SVT_PH_STEP);
-    CU(tc_gemm(kk == 1 ? 1 : 2, terms, (int)s, (int)L, (int)s, Gh, Gl, sp, src[1], src[2], Lp, true,
-               last ? nullptr : out[0], last ? nullptr : out[1], last ? nullptr : out[2], terms, Lp, src[0],
-               kk == 1 ? nullptr : out[0], Lp, Yi, Lp, h->P, kk, h->num_sms, h->stream));
+    CU(tc_gemm(kk == 1 ? 1 : 2, terms, (int)s, (int)RN, (int)s, Gh, Gl, sp, src[1], src[2], ldr, true,
+               last ? nullptr : out[0], last ? nullptr : out[1], last ? nullptr : out[2], terms, ldr, src[0],
+               kk == 1 ? nullptr : out[0], ldr, Yr, ldr, h->P, kk, h->num_sms, h->stream));
     ++launches;
+  }
+  if (poly) {
+    // Alg. 1 line 12: Y = H_hat A, one tcgen05 product (H_hat split into hi/lo operands)
+    Phase p(h, CPA_SVT_PH_FINAL);
+    CU(tf32_prep(Hs[0], s, sp, sp, false, Hs[0], Hs[1], Hs[2], sp, h->num_sms, h->stream));
+    CU(tc_gemm(0, terms, (int)s, (int)L, (int)s, Hs[1], Hs[2], sp, Xs[1], Xs[2], Lp, true, Yi, nullptr, nullptr, 1,
+               Lp, nullptr, nullptr, 0, nullptr, 0, nullptr, 0, h->num_sms, h->stream));
+    launches += 2;
   }
   CU(tf32_finish(Yi, Lp, m, n, !left, Y, ldy, h->num_sms, h->stream));
   ++launches;

@@ -493,6 +493,15 @@ __global__ void k_tf32_finish(const float* Yi, int64_t ldi, int64_t m, int64_t n
   }
 }
 
+__global__ void k_eye_f32(float* I, int64_t s, int64_t ld) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < s * ld; e += (int64_t)gridDim.x * blockDim.x)
+    I[e] = (e / ld == e % ld) ? 1.f : 0.f;
+}
+cudaError_t tf32_eye(float* I, int64_t s, int64_t ld, int num_sms, cudaStream_t st) {
+  k_eye_f32<<<num_sms * 8, 256, 0, st>>>(I, s, ld);
+  return cudaGetLastError();
+}
+
 cudaError_t tf32_prep(const float* X, int64_t m, int64_t n, int64_t ldx, bool transpose, float* Af, float* Ah,
                       float* Al, int64_t lda, int num_sms, cudaStream_t st) {
   k_tf32_prep<<<num_sms * 8, 256, 0, st>>>(X, m, n, ldx, transpose, Af, Ah, Al, lda);

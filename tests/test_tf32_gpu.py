@@ -83,3 +83,18 @@ def test_tf32_gemm_engine(env):
             for terms, tol in ((3, 2e-5), (1, 3e-3)):
                 C = h.debug_gemm_tf32(A, B, b_mn, terms).double()
                 assert float((C - ref).norm() / ref.norm()) <= tol, (M, N, K, b_mn, terms)
+
+
+@pytest.mark.parametrize("shape,K", [((200, 700), 20), ((700, 200), 12), ((256, 256), 9)])
+def test_tf32_both_forms(env, shape, K):
+    """3xTF32 in the Alg. 1 s x s form and in the apply-to-X form, against the oracle."""
+    torch, P, _ = env
+    X = W.gen_c2(m=shape[0], n=shape[1], seed=2).astype(np.float32).astype(np.float64)
+    kern = {"kind": "soft", "tau": 0.1, "tau_relative": True}
+    ref = O.cpa_shrink(X, O.Kernel(**kern), K, T=100)
+    for form in ("poly", "apply"):
+        h2 = P.Handle(0)
+        h2.set_form(form)
+        Y = h2.apply(torch.from_numpy(X.astype(np.float32)).cuda(), kern, K, T=100, math="3xtf32")
+        h2.close()
+        assert O.rel_fro(Y.cpu().numpy().astype(np.float64), ref) <= TOL32, form
