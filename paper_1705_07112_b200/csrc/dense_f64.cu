@@ -158,39 +158,43 @@ __device__ __forceinline__ void cheb_epilogue(const double (&acc)[4][4][2], int6
   const int g = lane >> 2, t = lane & 3;
   const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
   const double s2 = P->scale2;
-  if (init) {
-    const double h0 = 0.5 * P->c[0], c1 = P->c[1];
+  const double h0 = 0.5 * P->c[0], c1 = P->c[1];
+  const double s4 = 2.0 * s2, ck = init ? 0.0 : P->c[k];
+  // Wout may alias Wpp (W_k overwrites W_{k-2} in place), so the compiler cannot hoist
+  // loads past stores: load one 8-element row group into registers first, then store.
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 4; ++i) {
+    const int64_t r = m0 + wm + i * 8 + g;
+    const bool rok = r < M;
+    double vp[8], vpp[8], vy[8];
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < 4; ++j)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int64_t r = m0 + wm + i * 8 + g, c = n0 + wn + j * 8 + 2 * t + e;
-          if (r < M && c < N) {
-            const double x = __ldcg(Wp + r * ldwp + c);
-            const double w = s2 * acc[i][j][e] - x;  // W_1 = B_hat X
-            if (Wout) Wout[r * ldwo + c] = w;
-            Y[r * ldy + c] = h0 * x + c1 * w;       // Y = c0/2 W_0 + c1 W_1
-          }
+      for (int e = 0; e < 2; ++e) {
+        const int64_t c = n0 + wn + j * 8 + 2 * t + e;
+        const bool ok = rok && c < N;
+        vp[j * 2 + e] = ok ? __ldcg(Wp + r * ldwp + c) : 0.0;
+        vpp[j * 2 + e] = (ok && !init) ? __ldcg(Wpp + r * ldwpp + c) : 0.0;
+        vy[j * 2 + e] = (ok && !init) ? __ldcg(Y + r * ldy + c) : 0.0;
+      }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t c = n0 + wn + j * 8 + 2 * t + e;
+        if (!(rok && c < N)) continue;
+        const int q = j * 2 + e;
+        double w, y;
+        if (init) {
+          w = s2 * acc[i][j][e] - vp[q];                 // W_1 = B_hat X
+          y = h0 * vp[q] + c1 * w;                       // Y = c0/2 W_0 + c1 W_1
+        } else {
+          w = s4 * acc[i][j][e] - 2.0 * vp[q] - vpp[q];  // W_k = 2 B_hat W_{k-1} - W_{k-2}
+          y = vy[q] + ck * w;                            // Y += c_k W_k
         }
-  } else {
-    const double s4 = 2.0 * s2, ck = P->c[k];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int64_t r = m0 + wm + i * 8 + g, c = n0 + wn + j * 8 + 2 * t + e;
-          if (r < M && c < N) {
-            const double wp = __ldcg(Wp + r * ldwp + c);
-            const double wpp = __ldcg(Wpp + r * ldwpp + c);
-            const double w = s4 * acc[i][j][e] - 2.0 * wp - wpp;  // W_k = 2 B_hat W_{k-1} - W_{k-2}
-            if (Wout) Wout[r * ldwo + c] = w;
-            Y[r * ldy + c] = __ldcg(Y + r * ldy + c) + ck * w;    // Y += c_k W_k
-          }
-        }
+        if (Wout) Wout[r * ldwo + c] = w;
+        Y[r * ldy + c] = y;
+      }
   }
 }
 
@@ -222,6 +226,9 @@ struct FlowArgs {
   int vec_x, vec_w, vec_g;
 };
 
+__device__ __forceinline__ void red_release_add_i32(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
@@ -234,7 +241,7 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 // fused epilogue.  A unit of step k >= 2 first waits until its panel of
 // step k-1 is complete.
 template <bool LEFT>
-__global__ void __launch_bounds__(NTHREADS) k_cheb_flow(FlowArgs a) {
+__global__ void __launch_bounds__(NTHREADS, 3) k_cheb_flow(FlowArgs a) {
   extern __shared__ __align__(16) double smem[];
   __shared__ int s_ticket;
   const int npanels = LEFT ? a.tiles_n : a.tiles_m;
@@ -284,10 +291,7 @@ __global__ void __launch_bounds__(NTHREADS) k_cheb_flow(FlowArgs a) {
 #pragma unroll
             for (int e = 0; e < 2; ++e) __stcg(mine + ((i * 4 + j) * 2 + e) * NTHREADS + threadIdx.x, acc[i][j][e]);
         __syncthreads();
-        if (threadIdx.x == 0) {
-          __threadfence();
-          atomicAdd(split_cnt + tile, 1);
-        }
+        if (threadIdx.x == 0) red_release_add_i32(split_cnt + tile, 1);  // release, cumulative over bar.sync
         continue;
       }
       if (threadIdx.x == 0) {
@@ -295,16 +299,27 @@ __global__ void __launch_bounds__(NTHREADS) k_cheb_flow(FlowArgs a) {
       }
       __syncthreads();
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 4; ++i) {
+        // the 8 accumulators of row group i x (S-1) partials in flight, then a fixed-order sum
+        double part[8][3];
+#pragma unroll
+        for (int q8 = 0; q8 < 8; ++q8)
+#pragma unroll
+          for (int p = 0; p < 3; ++p)
+            part[q8][p] = p < S - 1 ? __ldcg(slot + (int64_t)p * (BM * BN) + (i * 8 + q8) * NTHREADS + threadIdx.x)
+                                    : 0.0;
 #pragma unroll
         for (int j = 0; j < 4; ++j)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            const int off = ((i * 4 + j) * 2 + e) * NTHREADS + threadIdx.x;
-            double sum = __ldcg(slot + off);
-            for (int p = 1; p < S - 1; ++p) sum += __ldcg(slot + (int64_t)p * (BM * BN) + off);
+            const int q8 = j * 2 + e;
+            double sum = part[q8][0];
+#pragma unroll
+            for (int p = 1; p < 3; ++p)
+              if (p < S - 1) sum += part[q8][p];
             acc[i][j][e] = sum + acc[i][j][e];
           }
+      }
     }
     double* out = (k & 1) ? a.Wa : a.Wb;
     const double* pp = k == 2 ? a.X : out;
@@ -312,10 +327,7 @@ __global__ void __launch_bounds__(NTHREADS) k_cheb_flow(FlowArgs a) {
     if (k == a.K - 1) out = nullptr;
     cheb_epilogue(acc, m0, n0, a.M, a.N, k == 1, src, ldsrc, pp, ldpp, out, a.ldw, a.Y, a.ldy, a.P, k);
     __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      atomicAdd(panel_cnt + k * npanels + panel, 1);
-    }
+    if (threadIdx.x == 0) red_release_add_i32(panel_cnt + k * npanels + panel, 1);
   }
 }
 
@@ -474,8 +486,8 @@ static int flow_split(int64_t m, int64_t n, int64_t s, int num_sms) {
   const int64_t tiles = ((m + BM - 1) / BM) * ((n + BN - 1) / BN);
   const int64_t nk = (s + BKS - 1) / BKS;
   int split = 1;
-  while (split < 8 && tiles * split < 6 * num_sms && nk / (2 * split) >= 4) split *= 2;
-  if (const char* v = getenv("CPA_SVT_FLOW_SPLIT")) split = atoi(v) > 0 ? atoi(v) : split;
+  while (split < 4 && tiles * split < 6 * num_sms && nk / (2 * split) >= 4) split *= 2;  // <= 4 (reducer registers)
+  if (const char* v = getenv("CPA_SVT_FLOW_SPLIT")) split = (atoi(v) > 0 && atoi(v) <= 4) ? atoi(v) : split;
   return split;
 }
 
