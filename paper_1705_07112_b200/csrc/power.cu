@@ -130,56 +130,34 @@ __global__ void __launch_bounds__(256) k_power_dense(PowerArgs<E> a) {
     const bool use4 = t < a.q;
     const T* Gt = use4 ? a.G4 : a.G;
     const bool cached = a.cache_rows && (use4 || a.q == 0);
-    // u_t = G v_{t-1}: one warp per row, 4 independent partial sums per lane
-    double mysq = 0.0;
+    // u_t = G v_{t-1}: one warp per row, 8 independent partial sums per lane
     for (int64_t r = r0 + warp; r < r1; r += nwarps) {
       const T* grow = cached ? sg + (r - r0) * s : Gt + r * a.ld;
-      double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+      double d[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       int64_t j = lane;
-      for (; j + 96 < s; j += 128) {
-        d0 = fma((double)grow[j], sv[j], d0);
-        d1 = fma((double)grow[j + 32], sv[j + 32], d1);
-        d2 = fma((double)grow[j + 64], sv[j + 64], d2);
-        d3 = fma((double)grow[j + 96], sv[j + 96], d3);
+      for (; j + 224 < s; j += 256) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) d[q] = fma((double)grow[j + 32 * q], sv[j + 32 * q], d[q]);
       }
-      for (; j < s; j += 32) d0 = fma((double)grow[j], sv[j], d0);
-      const double d = warp_sum((d0 + d1) + (d2 + d3)) * inv;
-      if (lane == 0) a.ubuf[(t & 1) * s + r] = d;
-      mysq = fma(d, d, mysq);  // identical in all lanes
+      for (; j < s; j += 32) d[0] = fma((double)grow[j], sv[j], d[0]);
+      const double dd = warp_sum(((d[0] + d[1]) + (d[2] + d[3])) + ((d[4] + d[5]) + (d[6] + d[7]))) * inv;
+      if (lane == 0) a.ubuf[(t & 1) * s + r] = dd;
     }
-    if (lane == 0) s_warp[warp] = mysq;
     __syncthreads();
     if (threadIdx.x == 0) {
-      double p = 0.0;
-      for (int w = 0; w < nwarps; ++w) p += s_warp[w];
-      a.part[(t & 1) * nb + blockIdx.x] = p;
-      // arrive (release, cumulative over the bar.sync above): publishes u_t and the partial
+      // arrive (release, cumulative over the bar.sync above): publishes this CTA's rows of u_t
       red_release_add(a.bar, 1u);
       const unsigned int target = nb * (unsigned)(t + 1);
       while (ld_relaxed_u32(a.bar) < target) {
       }
-      __threadfence();  // acquire: the other CTAs' u_t and partials are visible below
+      __threadfence();  // acquire: the other CTAs' rows of u_t are visible below
     }
     __syncthreads();
-    // ||u_t||: warp 0 re-sums the partials in a fixed order (identical in every CTA)
-    if (warp == 0) {
-      const double* pp = a.part + (t & 1) * nb;
-      double qv[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const unsigned b = lane + 32 * i;
-        qv[i] = b < nb ? __ldcg(pp + b) : 0.0;
-      }
-      double q = 0.0;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) q += qv[i];
-      for (unsigned b = lane + 256; b < nb; b += 32) q += __ldcg(pp + b);
-      q = warp_sum(q);
-      if (lane == 0) s_norm = sqrt(q);
-    }
-    // stage u_t (all loads in flight before the first store); v_t = u_t / ||u_t||
-    // is applied inside the next product
+    // stage u_t (all loads in flight before the first store) and ||u_t||^2 from the staged copy:
+    // every CTA sums the same values in the same fixed order, so all agree bitwise.
+    // v_t = u_t / ||u_t|| is applied inside the next product.
     const double* up = a.ubuf + (t & 1) * s;
+    double sq = 0.0;
     for (int64_t j0 = 0; j0 < s; j0 += 8 * blockDim.x) {
       double uv[8];
 #pragma unroll
@@ -191,7 +169,16 @@ __global__ void __launch_bounds__(256) k_power_dense(PowerArgs<E> a) {
       for (int i = 0; i < 8; ++i) {
         const int64_t j = j0 + threadIdx.x + (int64_t)i * blockDim.x;
         if (j < s) sv[j] = uv[i];
+        sq = fma(uv[i], uv[i], sq);
       }
+    }
+    sq = warp_sum(sq);
+    if (lane == 0) s_warp[warp] = sq;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double q = 0.0;
+      for (int w = 0; w < nwarps; ++w) q += s_warp[w];
+      s_norm = sqrt(q);
     }
     __syncthreads();
     lam = s_norm;
