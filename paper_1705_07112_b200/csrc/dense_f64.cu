@@ -240,8 +240,11 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 // all partials in the fixed order q = 0..split-1 (deterministic) and runs the
 // fused epilogue.  A unit of step k >= 2 first waits until its panel of
 // step k-1 is complete.
+#ifndef CPA_FLOW_MINB
+#define CPA_FLOW_MINB 3
+#endif
 template <bool LEFT>
-__global__ void __launch_bounds__(NTHREADS, 3) k_cheb_flow(FlowArgs a) {
+__global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB) k_cheb_flow(FlowArgs a) {
   extern __shared__ __align__(16) double smem[];
   __shared__ int s_ticket;
   const int npanels = LEFT ? a.tiles_n : a.tiles_m;

@@ -1,4 +1,5 @@
-for v in "" bk32s3 bk16s3 bk16s6 bk32s4; do
+python -m pytest tests/test_dense_gpu.py -q -x 2>&1 | tail -1
+for v in "" f3; do
   if [ -z "$v" ]; then L=""; else L="paper_1705_07112_b200/libcpasvt_$v.so"; fi
-  echo "variant=${v:-default}"; CPA_SVT_LIB=$L python tools/bench_configs.py c2 c5:4096x16384 --reps 3 | python -c "import sys,json; [print(json.loads(l)['config'], round(json.loads(l)['ms_per_svt'],3), json.loads(l)['phases_ms'].get('step'), round(json.loads(l)['recurrence_frac_of_dmma_peak'],3)) for l in sys.stdin]"
+  echo "variant=${v:-default}"; CPA_SVT_LIB=$L python tools/bench_configs.py c2 c5:4096x16384 --reps 3 | python -c "import sys,json; [print(json.loads(l)['config'], round(json.loads(l)['ms_per_svt'],3), json.loads(l)['phases_ms']) for l in sys.stdin]"
 done
