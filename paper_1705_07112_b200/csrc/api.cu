@@ -54,7 +54,7 @@ cudaError_t tf32_eye(float* I, int64_t s, int64_t ld, int num_sms, cudaStream_t 
 // batched_f32.cu
 cudaError_t launch_batched_f32(int64_t batch, int m, int n, const float* X, float* Y, const cpa_svt_kernel& k,
                                int K, int T, double safety, double lam_override, float* lambda_out,
-                               int num_sms, cudaStream_t st, int* launches);
+                               int num_sms, cudaStream_t st, int* launches, double* costab);
 // sparse_f64.cu
 cudaError_t sparse_apply(int64_t m, int64_t n, int64_t nnz, const int64_t* row_ptr, const int32_t* col,
                          const double* val, int64_t row_begin, int64_t row_end, double* Y, int64_t ldy,
@@ -780,11 +780,13 @@ cpa_svt_status cpa_svt_apply_batched(cpa_svt_handle* h, int64_t batch, int m, in
   if (K > 128) return CPA_SVT_E_UNSUPPORTED;
   if (batch == 0) return CPA_SVT_OK;
   if (cudaSetDevice(h->device) != cudaSuccess) return CPA_SVT_E_CUDA;
+  st = grow(h, &h->ws, &h->ws_bytes, 128 * 128 * sizeof(double));  // cos table
+  if (st != CPA_SVT_OK) return st;
   int launches = 0;
   {
     Phase p(h, CPA_SVT_PH_BATCHED);
     CU(launch_batched_f32(batch, m, n, X, Y, *k, K, lam->power_iters, lam->safety, lam->lambda_max, lambda_out,
-                          h->num_sms, h->stream, &launches));
+                          h->num_sms, h->stream, &launches, (double*)h->ws));
   }
   h->launches += launches;
   return CPA_SVT_OK;

@@ -75,6 +75,30 @@ __global__ void k_ffma3(float* out, int iters) {
   if (s == 12345.678f) out[0] = s;
 }
 
+// packed dual FP32 FMA (fma.rn.f32x2 -> SASS FFMA2), register operands varying per thread
+template <int ILP>
+__global__ void k_ffma2(float* out, int iters) {
+  unsigned long long acc[ILP], a[4], b[4];
+#pragma unroll
+  for (int i = 0; i < ILP; ++i) { float2 v = make_float2(threadIdx.x * 1e-3f + i, -i); acc[i] = *(unsigned long long*)&v; }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 va = make_float2(0.999f - threadIdx.x * 1e-6f * i, 0.998f), vb = make_float2(1e-3f * (i + 1), threadIdx.x * 1e-7f);
+    a[i] = *(unsigned long long*)&va; b[i] = *(unsigned long long*)&vb;
+  }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < ILP; ++i)
+      asm volatile("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[i]) : "l"(a[i & 3]), "l"(b[(i >> 2) & 3]));
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] ^= (unsigned long long)(it & 1);
+  }
+  float s = 0;
+#pragma unroll
+  for (int i = 0; i < ILP; ++i) { float2 v = *(float2*)&acc[i]; s += v.x + v.y; }
+  if (s == 12345.678f) out[0] = s;
+}
+
 int main() {
   int dev = 0, nsm = 0, clk = 0, l2 = 0, smem = 0;
   CK(cudaSetDevice(dev));
@@ -109,6 +133,11 @@ int main() {
     CK(cudaEventSynchronize(e1)); cudaEventElapsedTime(&ms, e0, e1);
     fl = 2.0 * 16 * (iters / 2) * (double)grid * thr;
     printf(", \"ffma3reg_tflops_b%d\": %.3f", blocks_per_sm, fl / ms / 1e9);
+    k_ffma2<16><<<grid, thr>>>((float*)dout, 100);
+    cudaEventRecord(e0); k_ffma2<16><<<grid, thr>>>((float*)dout, iters / 2); cudaEventRecord(e1);
+    CK(cudaEventSynchronize(e1)); cudaEventElapsedTime(&ms, e0, e1);
+    fl = 4.0 * 16 * (iters / 2) * (double)grid * thr;
+    printf(", \"ffma2_3reg_tflops_b%d\": %.3f", blocks_per_sm, fl / ms / 1e9);
   }
   printf("}\n");
   return 0;
