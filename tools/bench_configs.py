@@ -22,6 +22,23 @@ HBM = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if o
     os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
 
 
+def oracle_time(kind, budget_s=10.0, **kw):
+    """The CPU oracle timed on this host on a bounded sample of the config (reported, not tuned)."""
+    import oracle as O
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"] or [1])
+    except Exception:
+        cores = os.cpu_count()
+    t0 = time.perf_counter()
+    units, n = 0, 0
+    while time.perf_counter() - t0 < budget_s and n < 20:
+        units += kw["fn"]()
+        n += 1
+    el = time.perf_counter() - t0
+    return {"kind": "oracle", "cores": cores, "seconds": el, "sample": kw["sample"], "units_per_s": units / el}
+
+
 def timed(fn, reps, h):
     for _ in range(2):
         fn()
@@ -104,9 +121,50 @@ def sparse(h, reps, m=20000, n=200000, nnz=4_000_000):
             "spmm_pair_ms_per_step": (zx + zw) / (K - 1)}
 
 
+def oracle_leg(name, r):
+    """Attach the oracle's host timing (bounded sample, extrapolated by algorithmic work)."""
+    import oracle as O
+    import scipy.sparse as sp
+    cfg = W.CONFIGS[name]
+    k = O.Kernel(**cfg["kernel"])
+    if name in ("c1", "c2"):
+        X = W.gen_c1() if name == "c1" else W.gen_c2()
+        o = oracle_time("dense", fn=lambda: (O.cpa_shrink(X, k, cfg["K"], T=cfg["T"]), 1)[1],
+                        sample=f"full {name} SVTs (numpy fp64, Alg. 1 literal)")
+        r["oracle_ms_per_svt"] = 1e3 / o["units_per_s"]
+    elif name == "c3":
+        Xb = W.gen_c3(batch=256)
+        o = oracle_time("batched", fn=lambda: (O.cpa_shrink_batched(Xb[:64], k, cfg["K"], T=cfg["T"]), 64)[1],
+                        sample="64-matrix slices of the c3 recipe, extrapolated to 65536 matrices")
+        r["oracle_ms_per_svt_batch"] = 65536 * 1e3 / o["units_per_s"]
+    elif name == "c4":
+        m, n, nnz = 20000, 200000, 4_000_000
+        rp, col, val = W.gen_c4()
+        Xs = sp.csr_matrix((val, col, rp), shape=(m, n))
+        t0 = time.perf_counter()
+        lam = 1.01 * O.sparse_power_iteration(Xs, 10)[0]
+        t_pow = (time.perf_counter() - t0) / 10 * cfg["T"]
+        rows = list(range(16))
+        o = oracle_time("sparse", fn=lambda: (O.cpa_shrink_sparse_rows(Xs, rows, k, cfg["K"], lam=lam), 16)[1],
+                        sample="16 rows per call (vector form, scipy.sparse), extrapolated to 20000 rows "
+                               "+ T=300 power steps timed on 10")
+        r["oracle_ms_per_svt"] = (t_pow + m / o["units_per_s"]) * 1e3
+    elif name == "c5":
+        X = W.gen_c5(m=1024, n=4096)
+        o = oracle_time("dense", fn=lambda: (O.cpa_shrink(X, k, cfg["K"], T=cfg["T"]), 1)[1],
+                        sample="full SVTs at 1024 x 4096 (c5 recipe), extrapolated to 16384 x 65536 by flops")
+        s0, L0, s1, L1 = 1024, 4096, 16384, 65536
+        f = lambda s_, L_: s_ * s_ * L_ + (cfg["K"] - 2) * 2 * s_ ** 3 + 2 * s_ * s_ * L_
+        r["oracle_ms_per_svt"] = 1e3 / o["units_per_s"] * f(s1, L1) / f(s0, L0)
+    else:
+        return r
+    r["oracle"] = o
+    return r
+
+
 if __name__ == "__main__":
     reps = 3
-    args = [a for a in sys.argv[1:]]
+    args = [a for a in sys.argv[1:] if a != "--oracle"]
     if "--reps" in args:
         i = args.index("--reps")
         reps = int(args[i + 1])
@@ -138,6 +196,8 @@ if __name__ == "__main__":
                 r = sparse(h, reps)
         else:
             raise SystemExit(f"unknown config {a}")
+        if "--oracle" in sys.argv:
+            r = oracle_leg(a.split(":")[0].replace("c5t", "c5"), r)
         print(json.dumps(r), flush=True)
         out.append(r)
         torch.cuda.empty_cache()
