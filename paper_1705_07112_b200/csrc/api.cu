@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -16,7 +17,9 @@
 namespace cpa {
 // dense_f64.cu
 cudaError_t dense_gram_f64(const double* X, int64_t m, int64_t n, int64_t ldx, bool left, double* G,
-                           cudaStream_t st, const double* gscale = nullptr);
+                           cudaStream_t st, const double* gscale = nullptr, double* partial = nullptr,
+                           int* tcount = nullptr);
+size_t dense_gram_partial_doubles(int64_t s);
 cudaError_t dense_cheb_launch(bool left, bool init, int64_t m, int64_t n, const double* G,
                               const double* Wsrc, int64_t ldsrc, const double* Wpp, int64_t ldpp,
                               double* Wout, int64_t ldout, double* Y, int64_t ldy, const SeriesParams* P,
@@ -474,8 +477,8 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
   const int64_t RM = poly ? s : m, RN = poly ? s : n;  // shape the recurrence runs on
   const size_t nG = (size_t)s * s, nW = (size_t)RM * RN, nPow = power_dense_scratch_doubles(s);
   const size_t nX = poly ? 2 * nG : 0;
-  const size_t nPart = dense_flow_partial_doubles(RM, RN, h->num_sms);
-  const size_t nSync = dense_flow_sync_ints(RM, RN, K);
+  const size_t nPart = std::max(dense_flow_partial_doubles(RM, RN, h->num_sms), dense_gram_partial_doubles(s));
+  const size_t nSync = std::max(dense_flow_sync_ints(RM, RN, K), (size_t)((s / 64 + 2) * (s / 64 + 2)));
   const size_t need = (nG + 2 * nW + nX + nPow + nPart) * sizeof(double) + nSync * sizeof(int) + 256;
   cpa_svt_status st = grow(h, &h->ws, &h->ws_bytes, need);
   if (st != CPA_SVT_OK) return st;
@@ -499,7 +502,7 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
   // Alg. 1 line 1: partial Gram of this shard
   {
     Phase p(h, CPA_SVT_PH_GRAM);
-    CU(dense_gram_f64(X, m, n, ldx, left, G, h->stream));
+    CU(dense_gram_f64(X, m, n, ldx, left, G, h->stream, nullptr, part, flow_sync));
   }
   ++launches;
   tm.mark();
@@ -523,8 +526,8 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
     if (power_use_squaring(s, lam->power_iters) && nW >= nG) {
       double* sc = pw + 2 * s + 4096;  // scale slot inside the power scratch
       CU(launch_diag_scale(G, s, sc, h->stream));
-      CU(dense_gram_f64(G, s, s, s, true, Wa, h->stream, sc));  // c^2 G^2
-      CU(dense_gram_f64(Wa, s, s, s, true, Wb, h->stream));     // c^4 G^4
+      CU(dense_gram_f64(G, s, s, s, true, Wa, h->stream, sc, part, flow_sync));       // c^2 G^2
+      CU(dense_gram_f64(Wa, s, s, s, true, Wb, h->stream, nullptr, part, flow_sync));  // c^4 G^4
       launches += 3;
       G4 = Wb;
     }

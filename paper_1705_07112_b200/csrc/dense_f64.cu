@@ -46,6 +46,8 @@ struct GemmArgs {
   int k;                        // coefficient index (STEP)
   int vec_a, vec_b;             // 16-byte loads allowed
   const double* gscale;         // GRAM: optional device scalar multiplying the output (exact power of 2)
+  double* partial;              // GRAM split-K: tiles * split * 64 * 64 partial sums (gridDim.y = split)
+  int* tcount;                  // GRAM split-K: per-tile arrival counters (zeroed before the launch)
 };
 
 // Elements per stage of an operand whose global slab is OUTER x INNER (INNER contiguous).
@@ -356,7 +358,51 @@ __global__ void __launch_bounds__(NTHREADS) k_dmma_gemm(GemmArgs a) {
   const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
 
   double acc[4][4][2];
-  mainloop<A_KC, B_KC>(a.A, a.lda, a.B, a.ldb, a.M, a.N, a.Kd, m0, n0, a.vec_a, a.vec_b, smem, acc);
+  if (MODE == EPI_GRAM && gridDim.y > 1) {
+    // split-K over gridDim.y units per tile (the triangle alone has too few tiles to give
+    // every SMSP more than one warp): every unit publishes its partial; the last to arrive
+    // sums them in the fixed order q = 0..S-1 (deterministic) and stores the tile.
+    __shared__ int s_last;
+    const int S = gridDim.y, q = blockIdx.y;
+    const int nk = (int)((a.Kd + BKS - 1) / BKS);
+    mainloop<A_KC, B_KC>(a.A, a.lda, a.B, a.ldb, a.M, a.N, a.Kd, m0, n0, a.vec_a, a.vec_b, smem, acc,
+                         (int)((int64_t)nk * q / S), (int)((int64_t)nk * (q + 1) / S));
+    double* slot = a.partial + (int64_t)blockIdx.x * S * (BM * BN);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          __stcg(slot + (int64_t)q * (BM * BN) + ((i * 4 + j) * 2 + e) * NTHREADS + threadIdx.x, acc[i][j][e]);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int old;
+      asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;\n" : "=r"(old) : "l"(a.tcount + blockIdx.x) : "memory");
+      s_last = old == S - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      double pv[8][8];  // the 8 accumulators of row group i from up to 8 splits, all loads in flight
+#pragma unroll
+      for (int p = 0; p < 8; ++p)
+#pragma unroll
+        for (int q8 = 0; q8 < 8; ++q8)
+          pv[p][q8] = p < S ? __ldcg(slot + (int64_t)p * (BM * BN) + (i * 8 + q8) * NTHREADS + threadIdx.x) : 0.0;
+#pragma unroll
+      for (int q8 = 0; q8 < 8; ++q8) {
+        double sum = pv[0][q8];
+#pragma unroll
+        for (int p = 1; p < 8; ++p)
+          if (p < S) sum += pv[p][q8];
+        acc[i][q8 >> 1][q8 & 1] = sum;
+      }
+    }
+  } else {
+    mainloop<A_KC, B_KC>(a.A, a.lda, a.B, a.ldb, a.M, a.N, a.Kd, m0, n0, a.vec_a, a.vec_b, smem, acc);
+  }
 
   // ---------------- epilogue -------------------------------------------------
   if (MODE == EPI_GRAM) {
@@ -404,8 +450,23 @@ static cudaError_t launch(const GemmArgs& a, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   const int64_t tm = (a.M + BM - 1) / BM, tn = (a.N + BN - 1) / BN;
   dim3 grid;
-  if (MODE == EPI_GRAM) grid = dim3((unsigned)(tm * (tm + 1) / 2));
-  else grid = dim3((unsigned)tm, (unsigned)tn);
+  if (MODE == EPI_GRAM) {
+    const int64_t tiles = tm * (tm + 1) / 2, nk = (a.Kd + BKS - 1) / BKS;
+    int split = 1;
+    if (a.partial && a.tcount) {  // split-K needs scratch
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      while (split < 8 && tiles * split < 3 * sms && nk / (2 * split) >= 4) split *= 2;
+      if (split > 1) {
+        cudaError_t ez = cudaMemsetAsync(a.tcount, 0, tiles * sizeof(int), st);
+        if (ez != cudaSuccess) return ez;
+      }
+    }
+    grid = dim3((unsigned)tiles, (unsigned)split);
+  } else {
+    grid = dim3((unsigned)tm, (unsigned)tn);
+  }
   fn<<<grid, NTHREADS, smem, st>>>(a);
   return cudaGetLastError();
 }
@@ -415,10 +476,13 @@ static inline bool aligned16(const void* p, int64_t ld) {
 }
 
 // G (s x s, ld s) = X X^T (left, s = m) or X^T X (right, s = n); X m x n row-major.
+// partial / tcount: optional scratch (dense_gram_partial_doubles(s) doubles, tiles ints) enabling split-K
 cudaError_t dense_gram_f64(const double* X, int64_t m, int64_t n, int64_t ldx, bool left, double* G,
-                           cudaStream_t st, const double* gscale) {
+                           cudaStream_t st, const double* gscale, double* partial, int* tcount) {
   GemmArgs a{};
   a.gscale = gscale;
+  a.partial = partial;
+  a.tcount = tcount;
   if (left) {  // G(i,j) = sum_l X[i][l] X[j][l]: A(m,k)=X[m][k] (k contig), B(k,n)=X[n][k] (k contig)
     a.M = m; a.N = m; a.Kd = n;
     a.A = X; a.lda = ldx; a.B = X; a.ldb = ldx;
@@ -497,6 +561,11 @@ static int flow_split(int64_t m, int64_t n, int64_t s, int num_sms) {
 size_t dense_flow_sync_ints(int64_t m, int64_t n, int K) {
   const int64_t tm = (m + BM - 1) / BM, tn = (n + BN - 1) / BN;
   return (size_t)(1 + (int64_t)K * (tm > tn ? tm : tn) + tm * tn);
+}
+
+size_t dense_gram_partial_doubles(int64_t s) {
+  const int64_t t = (s + BM - 1) / BM;
+  return (size_t)(t * (t + 1) / 2) * 8 * BM * BN;
 }
 
 size_t dense_flow_partial_doubles(int64_t m, int64_t n, int num_sms) {
