@@ -109,7 +109,7 @@ typedef struct {
   int32_t degenerate;    /* 1 if lambda_hat <= 1e-300: Y = 0 */
   float ms_gram, ms_allreduce, ms_power, ms_recurrence, ms_total;
   int32_t kernel_launches;  /* device kernels this call launched */
-  int32_t pad;
+  int32_t form;          /* dense form that ran: 1 = apply-to-X, 2 = s x s symmetric, 3 = s x s full tiles */
 } cpa_svt_info;
 
 /* Multi-GPU sharding of the long dimension for cpa_svt_apply (world > 1). */
@@ -189,7 +189,10 @@ typedef enum {
   CPA_SVT_OPT_FORM = 0      /* dense recurrence form: 0 = auto (fewest flops), 1 = apply-to-X
                                (W_k = Psi_k(B_hat) X, (K-1) 2 s^2 L flops), 2 = Alg. 1 literal s x s form
                                (H_hat = sum c_k Psi_k(B_hat) formed on the s x s Gram, then one product
-                               Y = H_hat X: 2(K-2) s^3 + 2 s^2 L flops) */
+                               Y = H_hat X); fp64 computes only the lower-triangle
+                               tiles of each symmetric Psi_k (s^2 (s+1) flops per step), 3 = the s x s
+                               form on full tiles (2 s^3 per step; cross-check).  Auto picks 2 when
+                               K > 2 for fp64; for fp32/TF32 the s x s form (full tiles) when s < L. */
 } cpa_svt_option;
 cpa_svt_status cpa_svt_set_option(cpa_svt_handle* h, cpa_svt_option opt, int64_t value);
 

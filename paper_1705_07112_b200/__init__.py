@@ -45,10 +45,10 @@ class Info(ctypes.Structure):
                 ("side", ctypes.c_int32), ("degenerate", ctypes.c_int32),
                 ("ms_gram", ctypes.c_float), ("ms_allreduce", ctypes.c_float), ("ms_power", ctypes.c_float),
                 ("ms_recurrence", ctypes.c_float), ("ms_total", ctypes.c_float),
-                ("kernel_launches", ctypes.c_int32), ("pad", ctypes.c_int32)]
+                ("kernel_launches", ctypes.c_int32), ("form", ctypes.c_int32)]
 
     def as_dict(self):
-        return {f: getattr(self, f) for f, _ in self._fields_ if f != "pad"}
+        return {f: getattr(self, f) for f, _ in self._fields_}
 
 
 _p = ctypes.c_void_p
@@ -81,7 +81,7 @@ lib.cpa_svt_profile_read.argtypes = [_p, ctypes.POINTER(ctypes.c_double), ctypes
 PHASES = ["gram", "allreduce", "power", "init", "step", "sparse_z", "sparse_w", "batched", "final"]
 lib.cpa_svt_set_option.argtypes = [_p, ctypes.c_int, _i64]
 lib.cpa_svt_set_option.restype = ctypes.c_int
-FORM = {"auto": 0, "apply": 1, "poly": 2}
+FORM = {"auto": 0, "apply": 1, "poly": 2, "poly_full": 3}
 for _f in ("cpa_svt_init", "cpa_svt_free", "cpa_svt_nccl_unique_id", "cpa_svt_coeffs", "cpa_svt_apply",
            "cpa_svt_apply_host", "cpa_svt_apply_csr", "cpa_svt_apply_batched", "cpa_svt_profile",
            "cpa_svt_profile_read"):
@@ -148,7 +148,8 @@ class Handle:
         return lib.cpa_svt_launch_count(self._h)
 
     def set_form(self, form: str):
-        """cpa_svt_set_option(FORM): 'auto' | 'apply' (W_k = Psi_k X) | 'poly' (Alg. 1 s x s form)."""
+        """cpa_svt_set_option(FORM): 'auto' | 'apply' (W_k = Psi_k X) | 'poly' (Alg. 1 s x s form,
+        symmetric lower-triangle tiles) | 'poly_full' (s x s form on full tiles, cross-check)."""
         self._check(lib.cpa_svt_set_option(self._h, 0, FORM[form]), "cpa_svt_set_option")
 
     def profile(self, enable: bool = True):

@@ -29,6 +29,12 @@ size_t dense_flow_partial_doubles(int64_t m, int64_t n, int num_sms);
 cudaError_t dense_gemm_store(int64_t M, int64_t N, int64_t Kd, const double* A, int64_t lda, const double* B,
                              int64_t ldb, double* C, int64_t ldc, cudaStream_t st);
 cudaError_t dense_eye(double* I, int64_t s, cudaStream_t st);
+size_t dense_sym_sync_ints(int64_t s, int K);
+size_t dense_sym_partial_doubles(int64_t s, int num_sms);
+cudaError_t dense_sym_init(int64_t s, const double* G, double* Wa, double* H, const SeriesParams* P, int K,
+                           int num_sms, cudaStream_t st);
+cudaError_t dense_cheb_sym(int64_t s, const double* G, double* Wa, double* Wb, double* H, const SeriesParams* P,
+                           int K, int* sync, double* partial, int num_sms, cudaStream_t st);
 cudaError_t dense_cheb_flow(bool left, int64_t m, int64_t n, const double* G, const double* X, int64_t ldx,
                             double* Wa, double* Wb, double* Y, int64_t ldy, const SeriesParams* P, int K, int* sync,
                             double* partial, int num_sms, cudaStream_t st);
@@ -308,7 +314,7 @@ cpa_svt_status cpa_svt_free(cpa_svt_handle* h) {
 cpa_svt_status cpa_svt_set_option(cpa_svt_handle* h, cpa_svt_option opt, int64_t value) {
   if (!h) return CPA_SVT_E_ARG;
   if (opt == CPA_SVT_OPT_FORM) {
-    if (value < 0 || value > 2) return CPA_SVT_E_ARG;
+    if (value < 0 || value > 3) return CPA_SVT_E_ARG;
     h->form = (int)value;
     return CPA_SVT_OK;
   }
@@ -444,16 +450,15 @@ static cpa_svt_status run_recurrence_f64(cpa_svt_handle* h, bool left, int64_t M
   return CPA_SVT_OK;
 }
 
-// Which dense form runs (CPA_SVT_OPT_FORM): the s x s polynomial form of Alg. 1
-// costs 2(K-2)s^3 + 2s^2 L against (K-1) 2 s^2 L for apply-to-X -- fewer flops
-// whenever s < L (NEXT-1).
-static bool use_poly_form(const cpa_svt_handle* h, int64_t s, int64_t L, int K) {
-  if (K <= 2) return false;
-  if (h->form == 1) return false;
-  if (h->form == 2) return true;
-  return s < L;
+// Which dense form runs (CPA_SVT_OPT_FORM).  The s x s polynomial form of
+// Alg. 1 with symmetric tiles costs (K-2) s^3 + 2 s^2 L_local against
+// (K-1) 2 s^2 L_local for apply-to-X: fewer flops whenever K > 2 (s <= L).
+// Form 3 (the s x s form on full tiles) is kept for cross-checks.
+static int dense_form(const cpa_svt_handle* h, int64_t s, int64_t L_local, int K) {
+  if (K <= 2 || h->form == 1) return 1;
+  if (h->form == 2 || h->form == 3) return h->form;
+  return (double)(K - 2) * s + 2.0 * L_local < 2.0 * (K - 1) * L_local ? 2 : 1;
 }
-
 static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt_shard shard,
                                 int64_t long_global, const double* X, int64_t ldx, double* Y, int64_t ldy,
                                 const cpa_svt_kernel* k, int K, const double* c, cpa_svt_lambda* lam,
@@ -471,14 +476,17 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
   }
   const int64_t s = left ? m : n, L = left ? n : m;
   const bool sharded = shard != CPA_SVT_SHARD_NONE && h->world > 1;
-  const bool poly = use_poly_form(h, s, sharded ? long_global : L, K);
-  // workspace: G (s*s) | W_a | W_b | [I_s | H (s*s) in the poly form] | power scratch | split-K partials | sync
+  const int form = dense_form(h, s, L, K);
+  const bool poly = form != 1;
+  // workspace: G (s*s) | W_a | W_b | [I_s | H (s*s) in the poly forms] | power scratch | split-K partials | sync
   // (G^2 and G^4 for the squared power iteration live in W_a / W_b: free until the recurrence)
   const int64_t RM = poly ? s : m, RN = poly ? s : n;  // shape the recurrence runs on
   const size_t nG = (size_t)s * s, nW = (size_t)RM * RN, nPow = power_dense_scratch_doubles(s);
   const size_t nX = poly ? 2 * nG : 0;
-  const size_t nPart = std::max(dense_flow_partial_doubles(RM, RN, h->num_sms), dense_gram_partial_doubles(s));
-  const size_t nSync = std::max(dense_flow_sync_ints(RM, RN, K), (size_t)((s / 64 + 2) * (s / 64 + 2)));
+  const size_t nPart = std::max({dense_flow_partial_doubles(RM, RN, h->num_sms), dense_gram_partial_doubles(s),
+                                 form == 2 ? dense_sym_partial_doubles(s, h->num_sms) : (size_t)0});
+  const size_t nSync = std::max({dense_flow_sync_ints(RM, RN, K), (size_t)((s / 64 + 2) * (s / 64 + 2)),
+                                 dense_sym_sync_ints(s, K)});
   const size_t need = (nG + 2 * nW + nX + nPow + nPart) * sizeof(double) + nSync * sizeof(int) + 256;
   cpa_svt_status st = grow(h, &h->ws, &h->ws_bytes, need);
   if (st != CPA_SVT_OK) return st;
@@ -547,10 +555,23 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
   } else {
     // Alg. 1 literally: lines 5-11 on the s x s Gram with Psi_0 = Id (H_hat = sum c_k Psi_k),
     // then line 12: Y = H_hat X (left) or X H_hat (right) -- one product
-    CU(dense_eye(Is, s, h->stream));
-    ++launches;
-    st = run_recurrence_f64(h, true, s, s, G, Is, s, Wa, Wb, H, s, K, part, flow_sync, &launches);
-    if (st != CPA_SVT_OK) return st;
+    if (form == 2) {  // symmetric tiles (lower triangle computed, mirrored)
+      {
+        Phase p(h, CPA_SVT_PH_INIT);
+        CU(dense_sym_init(s, G, Wa, H, h->P, K, h->num_sms, h->stream));
+        ++launches;
+      }
+      if (K > 2) {
+        Phase p(h, CPA_SVT_PH_STEP);
+        CU(dense_cheb_sym(s, G, Wa, Wb, H, h->P, K, flow_sync, part, h->num_sms, h->stream));
+        ++launches;
+      }
+    } else {
+      CU(dense_eye(Is, s, h->stream));
+      ++launches;
+      st = run_recurrence_f64(h, true, s, s, G, Is, s, Wa, Wb, H, s, K, part, flow_sync, &launches);
+      if (st != CPA_SVT_OK) return st;
+    }
     Phase p(h, CPA_SVT_PH_FINAL);
     if (left) CU(dense_gemm_store(s, n, s, H, s, X, ldx, Y, ldy, h->stream));
     else      CU(dense_gemm_store(m, s, s, X, ldx, H, s, Y, ldy, h->stream));
@@ -567,6 +588,7 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
     info->ms_recurrence = tm.ms(3, 4);
     info->ms_total = tm.ms(0, 4);
     info->kernel_launches = launches;
+    info->form = form;
   }
   return CPA_SVT_OK;
 }
@@ -590,7 +612,8 @@ static cpa_svt_status apply_tf32(cpa_svt_handle* h, int terms, int64_t m, int64_
   const int64_t s = left ? m : n, L = left ? n : m;
   if (s > 2147483647 / 2 || L > 2147483647 / 2) return CPA_SVT_E_UNSUPPORTED;
   const int64_t sp = (s + 3) / 4 * 4, Lp = (L + 3) / 4 * 4;
-  const bool poly = use_poly_form(h, s, sharded ? long_global : L, K);
+  // s x s form on full tiles (2(K-2) s^3 + 2 s^2 L) when it beats apply-to-X ((K-1) 2 s^2 L)
+  const bool poly = K > 2 && h->form != 1 && (h->form >= 2 || s < L);
   auto al = [](size_t b) { return (b + 255) / 256 * 256; };
   const size_t nA = al((size_t)s * Lp * 4), nG = al((size_t)s * sp * 4);
   const size_t nPow = al(power_dense_scratch_doubles(s) * 8);
@@ -701,6 +724,7 @@ static cpa_svt_status apply_tf32(cpa_svt_handle* h, int terms, int64_t m, int64_
     info->ms_recurrence = tm.ms(3, 4);
     info->ms_total = tm.ms(0, 4);
     info->kernel_launches = launches;
+    info->form = poly ? 3 : 1;
   }
   return CPA_SVT_OK;
 }

@@ -236,6 +236,17 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Spin (relaxed loads: no L1 invalidation per poll) until *p >= target, then one
+// acquire fence: the fence-based form of the release/acquire pattern.
+__device__ __forceinline__ void wait_geq(const int* p, int target) {
+  while (ld_relaxed(p) < target) __nanosleep(32);
+  asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+}
 
 // Unit = (step k, panel, tile-in-panel, k-split q); claimed in that order.
 // Splits q < split-1 publish partial sums; split split-1 waits for them, adds
@@ -333,6 +344,179 @@ __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB) k_cheb_flow(FlowArgs 
     cheb_epilogue(acc, m0, n0, a.M, a.N, k == 1, src, ldsrc, pp, ldpp, out, a.ldw, a.Y, a.ldy, a.P, k);
     __syncthreads();
     if (threadIdx.x == 0) red_release_add_i32(panel_cnt + k * npanels + panel, 1);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Alg. 1 literally on the s x s Gram, symmetric storage.
+// Every Psi_k(B_hat) is a polynomial in the symmetric G, so it is symmetric and
+// G Psi_{k-1} = Psi_{k-1} G: each step computes only the LOWER-triangle tiles
+// (a >= b) -- s^3 instead of 2 s^3 flops -- and mirrors W_k into the upper
+// triangle so the next step reads full column panels.  Only elements r >= c are
+// computed (the diagonal tiles' upper halves are mirror images), so every W_k
+// and H_hat is exactly symmetric.
+//   init (k_sym_init):  W_1 = (2/L) G - I,  H = c_0/2 I + c_1 W_1
+//   step k = 2..K-1:    W_k = (4/L) G W_{k-1} - 2 W_{k-1} - W_{k-2}   (W_0 = I)
+//                       H += c_k W_k   (lower triangle; mirrored at k = K-1)
+// Dependencies: tile (a,b) of step k reads column panel b of W_{k-1} (lower
+// tiles of row b and column b: "cross" b) and overwrites W_{k-2} at (a,b) and
+// (b,a), which step k-1 reads through column panels b and a.  So it waits for
+// crosses a and b of step k-1.  Cross j has exactly T tiles (T tiles per dim):
+// tile (a,b) increments the counters of a and of b (once when a == b).
+// ---------------------------------------------------------------------------
+struct SymArgs {
+  int64_t s;
+  const double* G;
+  double* Wa;           // W_1 (from k_sym_init), then W_k for odd k
+  double* Wb;           // W_k for even k
+  double* H;            // H_hat (s x s, ld s)
+  const SeriesParams* P;
+  int K;
+  int T;                // tiles per dimension
+  int split;
+  int* sync;            // [0] ticket | K * T cross counters | ntri split counters
+  double* partial;      // ntri * (split - 1) * 64 * 64
+  int vec;
+};
+
+__global__ void k_sym_init(const double* __restrict__ G, int64_t s, double* __restrict__ W1, double* __restrict__ H,
+                           const SeriesParams* __restrict__ P) {
+  const double s2 = P->scale2, h0 = 0.5 * P->c[0], c1 = P->c[1];
+  const int64_t n = s * s;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const double id = (e / s == e % s) ? 1.0 : 0.0;
+    const double w = s2 * G[e] - id;                  // W_1 = B_hat = (2/L) G - I   (Alg. 1 line 5-6)
+    if (W1) W1[e] = w;
+    H[e] = h0 * id + c1 * w;                          // H = c_0/2 Psi_0 + c_1 Psi_1 (line 7)
+  }
+}
+
+__device__ __forceinline__ void tri_decode(int b, int& row, int& col) {
+  int r = (int)((sqrt(8.0 * b + 1.0) - 1.0) * 0.5);
+  while ((r + 1) * (r + 2) / 2 <= b) ++r;
+  while (r * (r + 1) / 2 > b) --r;
+  row = r;
+  col = b - r * (r + 1) / 2;
+}
+
+__global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB) k_cheb_sym(SymArgs a) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ int s_ticket;
+  const int T = a.T;
+  const int ntri = T * (T + 1) / 2;
+  const int S = a.split;
+  const int per_step = ntri * S;
+  const int total = (a.K - 2) * per_step;
+  int* cross = a.sync + 1;
+  int* split_cnt = a.sync + 1 + a.K * T;
+  const int64_t s = a.s;
+  const int nk = (int)((s + BKS - 1) / BKS);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  for (;;) {
+    if (threadIdx.x == 0) s_ticket = atomicAdd(a.sync, 1);
+    __syncthreads();
+    const int tk = s_ticket;
+    if (tk >= total) break;
+    const int k = 2 + tk / per_step;
+    const int r = tk % per_step;
+    const int q = r % S;
+    const int tile = r / S;                 // row-major lower-triangle tile id
+    int ta, tb;
+    tri_decode(tile, ta, tb);
+    if (threadIdx.x == 0 && k >= 3) {
+      const int* ca = cross + (k - 1) * T + ta;
+      const int* cb = cross + (k - 1) * T + tb;
+      wait_geq(cb, T);
+      wait_geq(ca, T);
+    }
+    __syncthreads();
+    // W_{k-1}: (k-1 odd ? Wa : Wb); W_k -> (k odd ? Wa : Wb) over W_{k-2} (k >= 3)
+    const double* src = ((k - 1) & 1) ? a.Wa : a.Wb;
+    double* out = (k & 1) ? a.Wa : a.Wb;
+    const int64_t m0 = (int64_t)ta * BM, n0 = (int64_t)tb * BN;
+    const int kb = (int)((int64_t)nk * q / S), ke = (int)((int64_t)nk * (q + 1) / S);
+    double acc[4][4][2];
+    mainloop<false, false>(a.G, s, src, s, s, s, s, m0, n0, a.vec, a.vec, smem, acc, kb, ke);
+    if (S > 1) {
+      double* slot = a.partial + (int64_t)tile * (S - 1) * (BM * BN);
+      if (q < S - 1) {
+        double* mine = slot + (int64_t)q * (BM * BN);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) __stcg(mine + ((i * 4 + j) * 2 + e) * NTHREADS + threadIdx.x, acc[i][j][e]);
+        __syncthreads();
+        if (threadIdx.x == 0) red_release_add_i32(split_cnt + tile, 1);
+        continue;
+      }
+      if (threadIdx.x == 0) wait_geq(split_cnt + tile, (S - 1) * (k - 1));
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        double part[8][3];
+#pragma unroll
+        for (int q8 = 0; q8 < 8; ++q8)
+#pragma unroll
+          for (int p = 0; p < 3; ++p)
+            part[q8][p] = p < S - 1 ? __ldcg(slot + (int64_t)p * (BM * BN) + (i * 8 + q8) * NTHREADS + threadIdx.x)
+                                    : 0.0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int q8 = j * 2 + e;
+            double sum = part[q8][0];
+#pragma unroll
+            for (int p = 1; p < 3; ++p)
+              if (p < S - 1) sum += part[q8][p];
+            acc[i][j][e] = sum + acc[i][j][e];
+          }
+      }
+    }
+    // fused epilogue on the elements r >= c of the tile
+    const double s4 = 2.0 * a.P->scale2, ck = a.P->c[k];
+    const bool last = k == a.K - 1;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t rr = m0 + wm + i * 8 + g;
+      double vp[8], vpp[8], vy[8];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t c = n0 + wn + j * 8 + 2 * t + e;
+          const bool ok = rr < s && c <= rr;
+          const int64_t o = rr * s + c;
+          vp[j * 2 + e] = ok ? __ldcg(src + o) : 0.0;
+          vpp[j * 2 + e] = k == 2 ? (rr == c ? 1.0 : 0.0) : (ok ? __ldcg(out + o) : 0.0);
+          vy[j * 2 + e] = ok ? __ldcg(a.H + o) : 0.0;
+        }
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t c = n0 + wn + j * 8 + 2 * t + e;
+          if (!(rr < s && c <= rr)) continue;
+          const int qq = j * 2 + e;
+          const double w = s4 * acc[i][j][e] - 2.0 * vp[qq] - vpp[qq];   // W_k = 2 B_hat W_{k-1} - W_{k-2}
+          const double y = vy[qq] + ck * w;                                // H += c_k W_k
+          if (!last) {
+            out[rr * s + c] = w;
+            out[c * s + rr] = w;
+          }
+          a.H[rr * s + c] = y;
+          if (last) a.H[c * s + rr] = y;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      red_release_add_i32(cross + k * T + ta, 1);
+      if (ta != tb) red_release_add_i32(cross + k * T + tb, 1);
+    }
   }
 }
 
@@ -604,6 +788,76 @@ cudaError_t dense_cheb_flow(bool left, int64_t m, int64_t n, const double* G, co
   int64_t grid = (int64_t)num_sms * (per_sm > 0 ? per_sm : 1);
   if (grid > total) grid = total;
   fn<<<(unsigned)grid, NTHREADS, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+// ---- symmetric s x s form -------------------------------------------------------
+// k-splits so that the (ntri x split) units of one step fill the resident slots
+// best: each step is close to a barrier (every cross spans the whole triangle),
+// so the quantisation of one step's units onto the slots is what matters.
+static int sym_split(int64_t s, int slots) {
+  const int64_t T = (s + BM - 1) / BM, ntri = T * (T + 1) / 2;
+  const int64_t nk = (s + BKS - 1) / BKS;
+  int best = 1;
+  double best_eff = 0.0;
+  for (int S = 1; S <= 4; ++S) {
+    if (S > 1 && nk / S < 4) break;
+    const int64_t u = ntri * S, waves = (u + slots - 1) / slots;
+    const double eff = (double)u / (double)(waves * slots);
+    if (eff > best_eff + 0.02) { best_eff = eff; best = S; }
+  }
+  if (const char* v = getenv("CPA_SVT_FLOW_SPLIT")) best = (atoi(v) > 0 && atoi(v) <= 4) ? atoi(v) : best;
+  return best;
+}
+
+static int flow_slots(const void* fn, size_t smem, int num_sms) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, NTHREADS, smem) != cudaSuccess) per_sm = 1;
+  return num_sms * (per_sm > 0 ? per_sm : 1);
+}
+
+static size_t sym_smem() { return (size_t)STAGES * (OpLayout<false, BM>::SIZE + OpLayout<false, BN>::SIZE) * sizeof(double); }
+
+size_t dense_sym_sync_ints(int64_t s, int K) {
+  const int64_t T = (s + BM - 1) / BM;
+  return (size_t)(1 + (int64_t)K * T + T * (T + 1) / 2);
+}
+
+size_t dense_sym_partial_doubles(int64_t s, int num_sms) {
+  const int64_t T = (s + BM - 1) / BM;
+  const int S = sym_split(s, flow_slots((const void*)k_cheb_sym, sym_smem(), num_sms));
+  return S > 1 ? (size_t)(T * (T + 1) / 2 * (S - 1) * BM * BN) : 0;
+}
+
+// W_1 = B_hat (into Wa when K > 2) and H = c_0/2 I + c_1 W_1.
+cudaError_t dense_sym_init(int64_t s, const double* G, double* Wa, double* H, const SeriesParams* P, int K,
+                           int num_sms, cudaStream_t st) {
+  if (s == 0) return cudaSuccess;
+  k_sym_init<<<num_sms * 4, 256, 0, st>>>(G, s, K > 2 ? Wa : nullptr, H, P);
+  return cudaGetLastError();
+}
+
+// H_hat += sum_{k=2}^{K-1} c_k Psi_k(B_hat) on the s x s Gram (W_a = W_1, W_b: s x s scratch).
+cudaError_t dense_cheb_sym(int64_t s, const double* G, double* Wa, double* Wb, double* H, const SeriesParams* P,
+                           int K, int* sync, double* partial, int num_sms, cudaStream_t st) {
+  if (s == 0 || K <= 2) return cudaSuccess;
+  cudaError_t e;
+  SymArgs a{};
+  a.s = s; a.G = G; a.Wa = Wa; a.Wb = Wb; a.H = H; a.P = P; a.K = K;
+  a.T = (int)((s + BM - 1) / BM);
+  const size_t smem = sym_smem();
+  e = cudaFuncSetAttribute(k_cheb_sym, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int slots = flow_slots((const void*)k_cheb_sym, smem, num_sms);
+  a.split = sym_split(s, slots);
+  a.sync = sync;
+  a.partial = partial;
+  a.vec = aligned16(G, s) && aligned16(Wa, s) && aligned16(Wb, s);
+  e = cudaMemsetAsync(sync, 0, dense_sym_sync_ints(s, K) * sizeof(int), st);
+  if (e != cudaSuccess) return e;
+  const int64_t total = (int64_t)(K - 2) * a.T * (a.T + 1) / 2 * a.split;
+  const int64_t grid = slots < total ? slots : total;
+  k_cheb_sym<<<(unsigned)grid, NTHREADS, smem, st>>>(a);
   return cudaGetLastError();
 }
 
