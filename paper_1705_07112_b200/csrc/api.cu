@@ -29,12 +29,12 @@ size_t dense_flow_partial_doubles(int64_t m, int64_t n, int num_sms);
 cudaError_t dense_gemm_store(int64_t M, int64_t N, int64_t Kd, const double* A, int64_t lda, const double* B,
                              int64_t ldb, double* C, int64_t ldc, cudaStream_t st);
 cudaError_t dense_eye(double* I, int64_t s, cudaStream_t st);
-size_t dense_sym_sync_ints(int64_t s, int K);
+size_t dense_sym_sync_ints(int64_t s, int K, int num_sms);
 size_t dense_sym_partial_doubles(int64_t s, int num_sms);
 cudaError_t dense_sym_init(int64_t s, const double* G, double* Wa, double* H, const SeriesParams* P, int K,
                            int num_sms, cudaStream_t st);
-cudaError_t dense_cheb_sym(int64_t s, const double* G, double* Wa, double* Wb, double* H, const SeriesParams* P,
-                           int K, int* sync, double* partial, int num_sms, cudaStream_t st);
+cudaError_t dense_cheb_sym(int64_t s, const double* G, double* W0, double* W1, double* W2, double* H,
+                           const SeriesParams* P, int K, int* sync, double* partial, int num_sms, cudaStream_t st);
 cudaError_t dense_cheb_flow(bool left, int64_t m, int64_t n, const double* G, const double* X, int64_t ldx,
                             double* Wa, double* Wb, double* Y, int64_t ldy, const SeriesParams* P, int K, int* sync,
                             double* partial, int num_sms, cudaStream_t st);
@@ -486,7 +486,7 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
   const size_t nPart = std::max({dense_flow_partial_doubles(RM, RN, h->num_sms), dense_gram_partial_doubles(s),
                                  form == 2 ? dense_sym_partial_doubles(s, h->num_sms) : (size_t)0});
   const size_t nSync = std::max({dense_flow_sync_ints(RM, RN, K), (size_t)((s / 64 + 2) * (s / 64 + 2)),
-                                 dense_sym_sync_ints(s, K)});
+                                 dense_sym_sync_ints(s, K, h->num_sms)});
   const size_t need = (nG + 2 * nW + nX + nPow + nPart) * sizeof(double) + nSync * sizeof(int) + 256;
   cpa_svt_status st = grow(h, &h->ws, &h->ws_bytes, need);
   if (st != CPA_SVT_OK) return st;
@@ -563,7 +563,7 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
       }
       if (K > 2) {
         Phase p(h, CPA_SVT_PH_STEP);
-        CU(dense_cheb_sym(s, G, Wa, Wb, H, h->P, K, flow_sync, part, h->num_sms, h->stream));
+        CU(dense_cheb_sym(s, G, Is, Wa, Wb, H, h->P, K, flow_sync, part, h->num_sms, h->stream));  // Is: 3rd W buffer
         ++launches;
       }
     } else {

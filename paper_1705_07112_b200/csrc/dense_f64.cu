@@ -367,13 +367,12 @@ __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB) k_cheb_flow(FlowArgs 
 struct SymArgs {
   int64_t s;
   const double* G;
-  double* Wa;           // W_1 (from k_sym_init), then W_k for odd k
-  double* Wb;           // W_k for even k
+  double* W[3];         // W_k lives in W[k % 3]; W[1] = W_1 from k_sym_init
   double* H;            // H_hat (s x s, ld s)
   const SeriesParams* P;
   int K;
   int T;                // tiles per dimension
-  int split;
+  int split;            // k-splits per tile
   int* sync;            // [0] ticket | K * T cross counters | ntri split counters
   double* partial;      // ntri * (split - 1) * 64 * 64
   int vec;
@@ -399,6 +398,88 @@ __device__ __forceinline__ void tri_decode(int b, int& row, int& col) {
   col = b - r * (r + 1) / 2;
 }
 
+// mainloop for the symmetric kernel: the A slabs (rows of the static G) of the
+// pipeline prologue are issued BEFORE the dependency wait, the B slabs (W_{k-1},
+// produced by the previous step) after it.  cp.async groups: group 0 = {A0..A2, B0},
+// group j = {Bj}: wait_group semantics of the main loop are unchanged.
+template <class Wait>
+__device__ __forceinline__ void mainloop_dep(const double* Ag, const double* Bg, int64_t s, int64_t m0, int64_t n0,
+                                             bool vec, double* smem, double (&acc)[4][4][2], int kbeg, int kend,
+                                             Wait&& wait) {
+  using LA = OpLayout<false, BM>;
+  using LB = OpLayout<false, BN>;
+  double* sA = smem;
+  double* sB = smem + STAGES * LA::SIZE;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const int nk = kend - kbeg;
+#pragma unroll
+  for (int st = 0; st < STAGES - 1; ++st)
+    if (st < nk) load_slab<LA>(sA + st * LA::SIZE, Ag, s, (int64_t)(kbeg + st) * BKS, m0, s, s, vec);
+  wait();
+#pragma unroll
+  for (int st = 0; st < STAGES - 1; ++st) {
+    if (st < nk) load_slab<LB>(sB + st * LB::SIZE, Bg, s, (int64_t)(kbeg + st) * BKS, n0, s, s, vec);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nxt = kt + STAGES - 1;
+      if (nxt < nk) {
+        const int64_t k0 = (int64_t)(kbeg + nxt) * BKS;
+        load_slab<LA>(sA + (nxt % STAGES) * LA::SIZE, Ag, s, k0, m0, s, s, vec);
+        load_slab<LB>(sB + (nxt % STAGES) * LB::SIZE, Bg, s, k0, n0, s, s, vec);
+      }
+      cp_async_commit();
+    }
+    const double* cA = sA + (kt % STAGES) * LA::SIZE;
+    const double* cB = sB + (kt % STAGES) * LB::SIZE;
+#pragma unroll
+    for (int kk = 0; kk < BKS; kk += 4) {
+      double fa[4], fb[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) fa[i] = cA[LA::idx(wm + i * 8 + g, kk + t)];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) fb[j] = cB[LB::idx(wn + j * 8 + g, kk + t)];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], fa[i], fb[j]);
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+}
+
+// Column-major lower-triangle tile index -> (row i, column j), i >= j.
+// Column j holds T - j tiles; C(j) = j (2T - j + 1) / 2 tiles precede it.
+__device__ __forceinline__ void tri_decode_colmajor(int idx, int T, int& row, int& col) {
+  const double b = 2.0 * T + 1.0;
+  int j = (int)((b - sqrt(b * b - 8.0 * idx)) * 0.5);
+  auto C = [&](int jj) { return jj * (2 * T - jj + 1) / 2; };
+  while (j > 0 && C(j) > idx) --j;
+  while (C(j + 1) <= idx) ++j;
+  col = j;
+  row = j + (idx - C(j));
+}
+
+// Dataflow schedule with three W buffers (W_k overwrites W_{k-3}).  Units
+// (step k, tile in column-major lower-triangle order, k-split q) are claimed by
+// ticket.  Tile (i, j) of step k reads column panel j of W_{k-1} = cross j of
+// step k-1 (tiles (l, j), l >= j, and (j, l), l < j) -- in column-major order
+// that cross is complete as soon as column j of step k-1 is, so consecutive
+// steps overlap as a wavefront instead of meeting at a barrier.  Its writes
+// (i, j) and (j, i) land on W_{k-3}, read by step k-2 through column panels j
+// and i (crosses j and i of step k-2; j is implied by cross j of step k-1) and
+// by the step k-1 epilogue of tile (i, j) (in cross j of step k-1): so it also
+// waits for cross i of step k-2.
 __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB) k_cheb_sym(SymArgs a) {
   extern __shared__ __align__(16) double smem[];
   __shared__ int s_ticket;
@@ -422,23 +503,23 @@ __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB) k_cheb_sym(SymArgs a)
     const int k = 2 + tk / per_step;
     const int r = tk % per_step;
     const int q = r % S;
-    const int tile = r / S;                 // row-major lower-triangle tile id
-    int ta, tb;
-    tri_decode(tile, ta, tb);
-    if (threadIdx.x == 0 && k >= 3) {
-      const int* ca = cross + (k - 1) * T + ta;
-      const int* cb = cross + (k - 1) * T + tb;
-      wait_geq(cb, T);
-      wait_geq(ca, T);
-    }
-    __syncthreads();
-    // W_{k-1}: (k-1 odd ? Wa : Wb); W_k -> (k odd ? Wa : Wb) over W_{k-2} (k >= 3)
-    const double* src = ((k - 1) & 1) ? a.Wa : a.Wb;
-    double* out = (k & 1) ? a.Wa : a.Wb;
-    const int64_t m0 = (int64_t)ta * BM, n0 = (int64_t)tb * BN;
+    const int tile = r / S;
+    int ti, tj;
+    tri_decode_colmajor(tile, T, ti, tj);
+    auto buf = [&](int i) { return i == 0 ? a.W[0] : (i == 1 ? a.W[1] : a.W[2]); };
+    const double* src = buf((k - 1) % 3);   // W_{k-1}
+    const double* wpp = buf((k - 2) % 3);   // W_{k-2} (k = 2: identity, implicit)
+    double* out = buf(k % 3);               // W_k over W_{k-3}
+    const int64_t m0 = (int64_t)ti * BM, n0 = (int64_t)tj * BN;
     const int kb = (int)((int64_t)nk * q / S), ke = (int)((int64_t)nk * (q + 1) / S);
     double acc[4][4][2];
-    mainloop<false, false>(a.G, s, src, s, s, s, s, m0, n0, a.vec, a.vec, smem, acc, kb, ke);
+    mainloop_dep(a.G, src, s, m0, n0, a.vec, smem, acc, kb, ke, [&] {
+      if (threadIdx.x == 0) {
+        if (k >= 3) wait_geq(cross + (k - 1) * T + tj, T);
+        if (k >= 4) wait_geq(cross + (k - 2) * T + ti, T);
+      }
+      __syncthreads();
+    });
     if (S > 1) {
       double* slot = a.partial + (int64_t)tile * (S - 1) * (BM * BN);
       if (q < S - 1) {
@@ -455,27 +536,22 @@ __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB) k_cheb_sym(SymArgs a)
       }
       if (threadIdx.x == 0) wait_geq(split_cnt + tile, (S - 1) * (k - 1));
       __syncthreads();
+      double sum[32];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        double part[8][3];
+      for (int rr = 0; rr < 32; ++rr) sum[rr] = __ldcg(slot + rr * NTHREADS + threadIdx.x);
+      for (int p = 1; p < S - 1; ++p) {
+        double v[32];
 #pragma unroll
-        for (int q8 = 0; q8 < 8; ++q8)
+        for (int rr = 0; rr < 32; ++rr) v[rr] = __ldcg(slot + (int64_t)p * (BM * BN) + rr * NTHREADS + threadIdx.x);
 #pragma unroll
-          for (int p = 0; p < 3; ++p)
-            part[q8][p] = p < S - 1 ? __ldcg(slot + (int64_t)p * (BM * BN) + (i * 8 + q8) * NTHREADS + threadIdx.x)
-                                    : 0.0;
+        for (int rr = 0; rr < 32; ++rr) sum[rr] += v[rr];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j)
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int q8 = j * 2 + e;
-            double sum = part[q8][0];
-#pragma unroll
-            for (int p = 1; p < 3; ++p)
-              if (p < S - 1) sum += part[q8][p];
-            acc[i][j][e] = sum + acc[i][j][e];
-          }
-      }
+          for (int e = 0; e < 2; ++e) acc[i][j][e] = sum[(i * 4 + j) * 2 + e] + acc[i][j][e];
     }
     // fused epilogue on the elements r >= c of the tile
     const double s4 = 2.0 * a.P->scale2, ck = a.P->c[k];
@@ -492,7 +568,7 @@ __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB) k_cheb_sym(SymArgs a)
           const bool ok = rr < s && c <= rr;
           const int64_t o = rr * s + c;
           vp[j * 2 + e] = ok ? __ldcg(src + o) : 0.0;
-          vpp[j * 2 + e] = k == 2 ? (rr == c ? 1.0 : 0.0) : (ok ? __ldcg(out + o) : 0.0);
+          vpp[j * 2 + e] = k == 2 ? (rr == c ? 1.0 : 0.0) : (ok ? __ldcg(wpp + o) : 0.0);
           vy[j * 2 + e] = ok ? __ldcg(a.H + o) : 0.0;
         }
 #pragma unroll
@@ -502,11 +578,11 @@ __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB) k_cheb_sym(SymArgs a)
           const int64_t c = n0 + wn + j * 8 + 2 * t + e;
           if (!(rr < s && c <= rr)) continue;
           const int qq = j * 2 + e;
-          const double w = s4 * acc[i][j][e] - 2.0 * vp[qq] - vpp[qq];   // W_k = 2 B_hat W_{k-1} - W_{k-2}
-          const double y = vy[qq] + ck * w;                                // H += c_k W_k
+          const double wv = s4 * acc[i][j][e] - 2.0 * vp[qq] - vpp[qq];  // W_k = 2 B_hat W_{k-1} - W_{k-2}
+          const double y = vy[qq] + ck * wv;                               // H += c_k W_k
           if (!last) {
-            out[rr * s + c] = w;
-            out[c * s + rr] = w;
+            out[rr * s + c] = wv;
+            out[c * s + rr] = wv;
           }
           a.H[rr * s + c] = y;
           if (last) a.H[c * s + rr] = y;
@@ -514,8 +590,8 @@ __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB) k_cheb_sym(SymArgs a)
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      red_release_add_i32(cross + k * T + ta, 1);
-      if (ta != tb) red_release_add_i32(cross + k * T + tb, 1);
+      red_release_add_i32(cross + k * T + ti, 1);
+      if (ti != tj) red_release_add_i32(cross + k * T + tj, 1);
     }
   }
 }
@@ -792,73 +868,68 @@ cudaError_t dense_cheb_flow(bool left, int64_t m, int64_t n, const double* G, co
 }
 
 // ---- symmetric s x s form -------------------------------------------------------
-// k-splits so that the (ntri x split) units of one step fill the resident slots
-// best: each step is close to a barrier (every cross spans the whole triangle),
-// so the quantisation of one step's units onto the slots is what matters.
+static size_t sym_smem() { return (size_t)STAGES * (OpLayout<false, BM>::SIZE + OpLayout<false, BN>::SIZE) * sizeof(double); }
+
+static int sym_slots(int num_sms) {
+  int per_sm = 0;
+  cudaFuncSetAttribute(k_cheb_sym, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sym_smem());
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cheb_sym, NTHREADS, sym_smem()) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  return num_sms * per_sm;
+}
+
+// k-splits per tile: enough units per step to keep about three steps' worth of
+// wavefront in flight on every slot, at least 4 k-slabs per unit, at most 4.
 static int sym_split(int64_t s, int slots) {
   const int64_t T = (s + BM - 1) / BM, ntri = T * (T + 1) / 2;
   const int64_t nk = (s + BKS - 1) / BKS;
-  int best = 1;
-  double best_eff = 0.0;
-  for (int S = 1; S <= 4; ++S) {
-    if (S > 1 && nk / S < 4) break;
-    const int64_t u = ntri * S, waves = (u + slots - 1) / slots;
-    const double eff = (double)u / (double)(waves * slots);
-    if (eff > best_eff + 0.02) { best_eff = eff; best = S; }
-  }
-  if (const char* v = getenv("CPA_SVT_FLOW_SPLIT")) best = (atoi(v) > 0 && atoi(v) <= 4) ? atoi(v) : best;
-  return best;
+  int S = 1;
+  while (S < 4 && ntri * S < 3 * slots && nk / (S + 1) >= 4) ++S;
+  if (const char* v = getenv("CPA_SVT_FLOW_SPLIT")) S = (atoi(v) > 0 && atoi(v) <= 4) ? atoi(v) : S;
+  return S;
 }
 
-static int flow_slots(const void* fn, size_t smem, int num_sms) {
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, NTHREADS, smem) != cudaSuccess) per_sm = 1;
-  return num_sms * (per_sm > 0 ? per_sm : 1);
-}
-
-static size_t sym_smem() { return (size_t)STAGES * (OpLayout<false, BM>::SIZE + OpLayout<false, BN>::SIZE) * sizeof(double); }
-
-size_t dense_sym_sync_ints(int64_t s, int K) {
+size_t dense_sym_sync_ints(int64_t s, int K, int num_sms) {
+  (void)num_sms;
   const int64_t T = (s + BM - 1) / BM;
   return (size_t)(1 + (int64_t)K * T + T * (T + 1) / 2);
 }
 
 size_t dense_sym_partial_doubles(int64_t s, int num_sms) {
   const int64_t T = (s + BM - 1) / BM;
-  const int S = sym_split(s, flow_slots((const void*)k_cheb_sym, sym_smem(), num_sms));
+  const int S = sym_split(s, sym_slots(num_sms));
   return S > 1 ? (size_t)(T * (T + 1) / 2 * (S - 1) * BM * BN) : 0;
 }
 
-// W_1 = B_hat (into Wa when K > 2) and H = c_0/2 I + c_1 W_1.
-cudaError_t dense_sym_init(int64_t s, const double* G, double* Wa, double* H, const SeriesParams* P, int K,
+// W_1 = B_hat (into W1 when K > 2) and H = c_0/2 I + c_1 W_1.
+cudaError_t dense_sym_init(int64_t s, const double* G, double* W1, double* H, const SeriesParams* P, int K,
                            int num_sms, cudaStream_t st) {
   if (s == 0) return cudaSuccess;
-  k_sym_init<<<num_sms * 4, 256, 0, st>>>(G, s, K > 2 ? Wa : nullptr, H, P);
+  k_sym_init<<<num_sms * 4, 256, 0, st>>>(G, s, K > 2 ? W1 : nullptr, H, P);
   return cudaGetLastError();
 }
 
-// H_hat += sum_{k=2}^{K-1} c_k Psi_k(B_hat) on the s x s Gram (W_a = W_1, W_b: s x s scratch).
-cudaError_t dense_cheb_sym(int64_t s, const double* G, double* Wa, double* Wb, double* H, const SeriesParams* P,
-                           int K, int* sync, double* partial, int num_sms, cudaStream_t st) {
+// H_hat += sum_{k=2}^{K-1} c_k Psi_k(B_hat) on the s x s Gram: one persistent launch
+// for all K-2 steps.  W0, W1, W2: s x s buffers, W1 = W_1 from dense_sym_init.
+cudaError_t dense_cheb_sym(int64_t s, const double* G, double* W0, double* W1, double* W2, double* H,
+                           const SeriesParams* P, int K, int* sync, double* partial, int num_sms, cudaStream_t st) {
   if (s == 0 || K <= 2) return cudaSuccess;
-  cudaError_t e;
   SymArgs a{};
-  a.s = s; a.G = G; a.Wa = Wa; a.Wb = Wb; a.H = H; a.P = P; a.K = K;
+  a.s = s; a.G = G; a.W[0] = W0; a.W[1] = W1; a.W[2] = W2; a.H = H; a.P = P; a.K = K;
   a.T = (int)((s + BM - 1) / BM);
   const size_t smem = sym_smem();
-  e = cudaFuncSetAttribute(k_cheb_sym, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  const int slots = flow_slots((const void*)k_cheb_sym, smem, num_sms);
+  const int slots = sym_slots(num_sms);
   a.split = sym_split(s, slots);
   a.sync = sync;
   a.partial = partial;
-  a.vec = aligned16(G, s) && aligned16(Wa, s) && aligned16(Wb, s);
-  e = cudaMemsetAsync(sync, 0, dense_sym_sync_ints(s, K) * sizeof(int), st);
+  a.vec = aligned16(G, s) && aligned16(W0, s) && aligned16(W1, s) && aligned16(W2, s);
+  cudaError_t e = cudaMemsetAsync(sync, 0, dense_sym_sync_ints(s, K, num_sms) * sizeof(int), st);
   if (e != cudaSuccess) return e;
   const int64_t total = (int64_t)(K - 2) * a.T * (a.T + 1) / 2 * a.split;
   const int64_t grid = slots < total ? slots : total;
-  k_cheb_sym<<<(unsigned)grid, NTHREADS, smem, st>>>(a);
-  return cudaGetLastError();
+  void* args[] = {&a};
+  return cudaLaunchCooperativeKernel((void*)k_cheb_sym, dim3((unsigned)grid), dim3(NTHREADS), args, smem, st);
 }
 
 }  // namespace cpa

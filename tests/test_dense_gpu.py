@@ -212,12 +212,14 @@ def test_both_forms_match_oracle(env, shape, K):
     assert O.rel_fro(out["poly"], out["poly_full"]) <= 1e-12
 
 
-@pytest.mark.parametrize("s,K,split", [(1024, 30, 0), (1024, 30, 1), (1024, 30, 2), (1024, 30, 4), (200, 9, 3),
-                                       (1000, 12, 0), (64, 3, 0), (65, 4, 2), (1537, 6, 0)])
+@pytest.mark.parametrize("s,K,split", [(1024, 30, 0), (1024, 30, 1), (1024, 30, 2), (1024, 30, 3), (1024, 30, 4),
+                                       (200, 9, 3), (1000, 12, 0), (64, 3, 0), (65, 4, 2), (1537, 6, 0), (130, 20, 4),
+                                       (300, 5, 0)])
 def test_symmetric_form_splits(env, s, K, split):
-    """Symmetric s x s form (lower-triangle tiles, mirrored W_k) with every k-split
-    count against the oracle; H_hat exactly symmetric shows up as Y = H_hat X for
-    X = I being exactly symmetric."""
+    """Symmetric s x s form (lower-triangle tiles, mirrored W_k, column-major dataflow
+    over three W buffers, `split` k-splits per tile summed in fixed order) against the
+    oracle, deterministic run to run; H_hat exactly symmetric shows up as Y = H_hat X
+    for X = I being exactly symmetric."""
     import os
     torch, P, _ = env
     X = W.gen_c2(m=s, n=s + 37, seed=s + K)
@@ -228,9 +230,11 @@ def test_symmetric_form_splits(env, s, K, split):
         h2 = P.Handle(0)
         h2.set_form("poly")
         Y = h2.apply(torch.from_numpy(X).cuda(), kern, K, T=120).cpu().numpy()
+        Y2 = h2.apply(torch.from_numpy(X).cuda(), kern, K, T=120).cpu().numpy()
         Hx = h2.apply(torch.eye(s, dtype=torch.float64, device="cuda"), kern, K, T=60).cpu().numpy()
         h2.close()
     finally:
         os.environ.pop("CPA_SVT_FLOW_SPLIT", None)
     assert O.rel_fro(Y, O.cpa_shrink(X, O.Kernel(**kern), K, T=120)) <= TOL64
+    assert np.array_equal(Y, Y2)
     assert np.array_equal(Hx, Hx.T)
