@@ -42,6 +42,7 @@ cudaError_t dense_cheb_flow(bool left, int64_t m, int64_t n, const double* G, co
 cudaError_t launch_series(SeriesParams* P, const cpa_svt_kernel& k, int K, double safety, double lam_override,
                           const double* lam_src, const double* c_given, cudaStream_t st);
 size_t power_dense_scratch_doubles(int64_t s);
+size_t power_scale_offset(int64_t s);
 bool power_use_squaring(int64_t s, int T);
 cudaError_t launch_diag_scale(const double* G, int64_t s, double* scale, cudaStream_t st);
 cudaError_t launch_power_dense(const double* G, const double* G4, int64_t s, int T, double* scratch,
@@ -481,10 +482,12 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
   // workspace: G (s*s) | W_a | W_b | [I_s | H (s*s) in the poly forms] | power scratch | split-K partials | sync
   // (G^2 and G^4 for the squared power iteration live in W_a / W_b: free until the recurrence)
   const int64_t RM = poly ? s : m, RN = poly ? s : n;  // shape the recurrence runs on
-  const size_t nG = (size_t)s * s, nW = (size_t)RM * RN, nPow = power_dense_scratch_doubles(s);
+  // every segment starts on a 256-byte boundary (16-byte vector paths, LL words)
+  auto r32 = [](size_t v) { return (v + 31) / 32 * 32; };
+  const size_t nG = r32((size_t)s * s), nW = r32((size_t)RM * RN), nPow = r32(power_dense_scratch_doubles(s));
   const size_t nX = poly ? 2 * nG : 0;
-  const size_t nPart = std::max({dense_flow_partial_doubles(RM, RN, h->num_sms), dense_gram_partial_doubles(s),
-                                 form == 2 ? dense_sym_partial_doubles(s, h->num_sms) : (size_t)0});
+  const size_t nPart = r32(std::max({dense_flow_partial_doubles(RM, RN, h->num_sms), dense_gram_partial_doubles(s),
+                                     form == 2 ? dense_sym_partial_doubles(s, h->num_sms) : (size_t)0}));
   const size_t nSync = std::max({dense_flow_sync_ints(RM, RN, K), (size_t)((s / 64 + 2) * (s / 64 + 2)),
                                  dense_sym_sync_ints(s, K, h->num_sms)});
   const size_t need = (nG + 2 * nW + nX + nPow + nPart) * sizeof(double) + nSync * sizeof(int) + 256;
@@ -532,7 +535,7 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
     // lambda_hat = ||G v_{T-1}|| -- the same quantity as T plain products (reading R6).
     const double* G4 = nullptr;
     if (power_use_squaring(s, lam->power_iters) && nW >= nG) {
-      double* sc = pw + 2 * s + 4096;  // scale slot inside the power scratch
+      double* sc = pw + power_scale_offset(s);  // scale slot inside the power scratch
       CU(launch_diag_scale(G, s, sc, h->stream));
       CU(dense_gram_f64(G, s, s, s, true, Wa, h->stream, sc, part, flow_sync));       // c^2 G^2
       CU(dense_gram_f64(Wa, s, s, s, true, Wb, h->stream, nullptr, part, flow_sync));  // c^4 G^4

@@ -879,14 +879,15 @@ static int sym_slots(int num_sms) {
   return num_sms * per_sm;
 }
 
-// k-splits per tile: enough units per step to keep about three steps' worth of
-// wavefront in flight on every slot, at least 4 k-slabs per unit, at most 4.
+// k-splits per tile: about two units per resident slot per step (shorter units
+// make the wavefront finer; c2 measured: S = 4 / 6 / 8 -> 1.46 / 1.31 / 1.39 ms),
+// at least 4 k-slabs per unit, at most 8.
 static int sym_split(int64_t s, int slots) {
   const int64_t T = (s + BM - 1) / BM, ntri = T * (T + 1) / 2;
   const int64_t nk = (s + BKS - 1) / BKS;
   int S = 1;
-  while (S < 4 && ntri * S < 3 * slots && nk / (S + 1) >= 4) ++S;
-  if (const char* v = getenv("CPA_SVT_FLOW_SPLIT")) S = (atoi(v) > 0 && atoi(v) <= 4) ? atoi(v) : S;
+  while (S < 8 && ntri * S * 10 < 18 * (int64_t)slots && nk / (S + 1) >= 4) ++S;
+  if (const char* v = getenv("CPA_SVT_FLOW_SPLIT")) S = (atoi(v) > 0 && atoi(v) <= 16) ? atoi(v) : S;
   return S;
 }
 

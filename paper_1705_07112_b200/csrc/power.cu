@@ -5,10 +5,17 @@
 // k_power_dense: one cooperative persistent launch for all T products.  Each
 // CTA owns a contiguous block of Gram rows (cached in shared memory when they
 // fit), stages v_{t-1} in shared memory, computes its rows of u_t = G v_{t-1}
-// with one warp per row, publishes u_t and its partial sum of squares, and
-// meets the other CTAs at a grid barrier.  ||u_t|| is re-summed by every CTA
-// in the same fixed order, so all CTAs agree bitwise.  The last barrier is
-// followed by the coefficient computation in CTA 0.
+// with one warp per row and publishes them as flag-carrying LL words; every CTA
+// gathers the whole u_t by spinning on those words (no grid barrier).  ||u_t||
+// is re-summed by every CTA in the same fixed order, so all CTAs agree bitwise.
+// After the last product CTA 0 computes the coefficients.
+#include <cstdio>
+#include <cstdlib>
+
+#ifndef CPA_POLL_WARPS
+#define CPA_POLL_WARPS 4
+#endif
+
 #include "common.cuh"
 
 namespace cpa {
@@ -69,9 +76,7 @@ struct PowerArgs {
   int64_t s;
   int64_t ld;        // row stride of G / G4 (elements)
   int T;
-  double* ubuf;      // 2 * s
-  double* part;      // 2 * gridDim.x
-  unsigned int* bar; // monotonic arrival counter (zeroed before the launch)
+  unsigned long long* ll;  // 2 (parity) * s * 2 LL words, zeroed before the launch
   SeriesParams* P;
   cpa_svt_kernel kern;
   int K;
@@ -87,20 +92,60 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-__device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
-  unsigned int v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-  return v;
+// LL ("low-latency") exchange words: an 8-byte store is single-copy atomic, so a
+// word carrying 32 data bits next to a 32-bit epoch flag is valid exactly when the
+// reader sees the flag of the epoch it waits for.  A double travels as two words.
+__device__ __forceinline__ void st_ll(unsigned long long* p, double v, unsigned flag) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  const unsigned long long w0 = ((unsigned long long)flag << 32) | (b >> 32);
+  const unsigned long long w1 = ((unsigned long long)flag << 32) | (b & 0xffffffffull);
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};\n" ::"l"(p), "l"(w0), "l"(w1) : "memory");
 }
-__device__ __forceinline__ unsigned int ld_relaxed_u32(const unsigned int* p) {
-  unsigned int v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void red_release_add(unsigned int* p, unsigned int v) {
-  asm volatile("red.release.gpu.global.add.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ void ld_ll(const unsigned long long* p, unsigned long long& w0, unsigned long long& w1) {
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];\n" : "=l"(w0), "=l"(w1) : "l"(p) : "memory");
 }
 
+// Gather the s LL-encoded doubles of epoch `flag` into shared memory dst.  Only
+// the first CPA_POLL_WARPS warps poll (every thread of every CTA spinning on the
+// same lines stalls the whole exchange for ~10 us -- measured); each polling lane
+// keeps 8 words in flight and re-issues only the late ones.  Ends with a CTA barrier.
+__device__ __forceinline__ void ll_gather(const unsigned long long* buf, int64_t s, unsigned flag, double* dst) {
+  constexpr int NP = 32 * CPA_POLL_WARPS;
+  if (threadIdx.x < NP) {
+    const int pl = threadIdx.x;
+    for (int64_t j0 = 0; j0 < s; j0 += NP * 8) {
+      unsigned long long w[8][2];
+      unsigned pending = 0;
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (j0 + pl + NP * c < s) pending |= 1u << c;
+      while (pending) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          if (pending & (1u << c)) ld_ll(buf + 2 * (j0 + pl + NP * c), w[c][0], w[c][1]);
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          if ((pending & (1u << c)) && (unsigned)(w[c][0] >> 32) == flag && (unsigned)(w[c][1] >> 32) == flag)
+            pending &= ~(1u << c);
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (j0 + pl + NP * c < s)
+          dst[j0 + pl + NP * c] =
+              __longlong_as_double((long long)(((w[c][0] & 0xffffffffull) << 32) | (w[c][1] & 0xffffffffull)));
+    }
+  }
+  __syncthreads();
+}
+
+// One persistent (cooperative) launch for all T products.  Product t: every CTA
+// computes its rows of u_t = G v_{t-1} (one warp per row) and publishes them as LL
+// words with flag t+1 in buffer t&1; every CTA then reads the whole u_t, spinning
+// per word until its flag arrives -- the data and its readiness travel together,
+// so there is no grid barrier and no separate flag round trip.  Buffer t&1 is
+// rewritten at t+2 only by a CTA that has read all of u_{t+1}, which every CTA
+// publishes after reading all of u_t.  ||u_t|| is re-summed by every CTA in the
+// same fixed order from the staged copy, so all CTAs agree bitwise.
 template <typename E>
 __global__ void __launch_bounds__(256) k_power_dense(PowerArgs<E> a) {
   using T = E;
@@ -113,7 +158,6 @@ __global__ void __launch_bounds__(256) k_power_dense(PowerArgs<E> a) {
   const int64_t r0 = (int64_t)blockIdx.x * a.rows_per_cta;
   const int64_t r1 = min(s, r0 + a.rows_per_cta);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-  const unsigned int nb = gridDim.x;
   // products: q by G4 (cached when present), then T - 4q by G; the last one gives lambda_hat
   const T* Gc = a.q > 0 ? a.G4 : a.G;  // the matrix whose rows are cached
   const int niter = a.T - 3 * a.q;
@@ -126,10 +170,23 @@ __global__ void __launch_bounds__(256) k_power_dense(PowerArgs<E> a) {
   __syncthreads();
   double lam = 0.0;
   double inv = 1.0;  // 1/||u_{t-1}||, folded into this product (v_{t-1} = u_{t-1} * inv)
+#ifdef CPA_POWER_TRACE
+  unsigned long long tr[8][4];
+  auto stamp = [&](int t, int i) {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    if (t < 8) tr[t][i] = v;
+  };
+#else
+  auto stamp = [&](int, int) {};
+#endif
   for (int t = 0; t < niter; ++t) {
+    stamp(t, 0);
     const bool use4 = t < a.q;
     const T* Gt = use4 ? a.G4 : a.G;
     const bool cached = a.cache_rows && (use4 || a.q == 0);
+    const unsigned flag = (unsigned)t + 1u;
+    unsigned long long* buf = a.ll + (int64_t)(t & 1) * s * 2;
     // u_t = G v_{t-1}: one warp per row, 8 independent partial sums per lane
     for (int64_t r = r0 + warp; r < r1; r += nwarps) {
       const T* grow = cached ? sg + (r - r0) * s : Gt + r * a.ld;
@@ -141,37 +198,15 @@ __global__ void __launch_bounds__(256) k_power_dense(PowerArgs<E> a) {
       }
       for (; j < s; j += 32) d[0] = fma((double)grow[j], sv[j], d[0]);
       const double dd = warp_sum(((d[0] + d[1]) + (d[2] + d[3])) + ((d[4] + d[5]) + (d[6] + d[7]))) * inv;
-      if (lane == 0) a.ubuf[(t & 1) * s + r] = dd;
+      if (lane == 0) st_ll(buf + 2 * r, dd, flag);
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      // arrive (release, cumulative over the bar.sync above): publishes this CTA's rows of u_t
-      red_release_add(a.bar, 1u);
-      const unsigned int target = nb * (unsigned)(t + 1);
-      while (ld_relaxed_u32(a.bar) < target) {
-      }
-      __threadfence();  // acquire: the other CTAs' rows of u_t are visible below
-    }
-    __syncthreads();
-    // stage u_t (all loads in flight before the first store) and ||u_t||^2 from the staged copy:
-    // every CTA sums the same values in the same fixed order, so all agree bitwise.
-    // v_t = u_t / ||u_t|| is applied inside the next product.
-    const double* up = a.ubuf + (t & 1) * s;
+    __syncthreads();  // every warp is done reading sv before it is overwritten below
+    stamp(t, 1);
+    // gather u_t into sv, then ||u_t||^2 from the staged copy in a fixed order
+    ll_gather(buf, s, flag, sv);
     double sq = 0.0;
-    for (int64_t j0 = 0; j0 < s; j0 += 8 * blockDim.x) {
-      double uv[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int64_t j = j0 + threadIdx.x + (int64_t)i * blockDim.x;
-        uv[i] = j < s ? __ldcg(up + j) : 0.0;
-      }
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int64_t j = j0 + threadIdx.x + (int64_t)i * blockDim.x;
-        if (j < s) sv[j] = uv[i];
-        sq = fma(uv[i], uv[i], sq);
-      }
-    }
+    for (int64_t j = threadIdx.x; j < s; j += blockDim.x) sq = fma(sv[j], sv[j], sq);
+    stamp(t, 2);
     sq = warp_sum(sq);
     if (lane == 0) s_warp[warp] = sq;
     __syncthreads();
@@ -184,7 +219,126 @@ __global__ void __launch_bounds__(256) k_power_dense(PowerArgs<E> a) {
     lam = s_norm;
     if (!(lam > kDegenerateLambda) || !(lam < 1e300)) { lam = lam < 1e300 ? 0.0 : lam; break; }
     inv = 1.0 / lam;
+    stamp(t, 3);
   }
+#ifdef CPA_POWER_TRACE
+  if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
+    for (int t = 1; t < 8 && t < niter; ++t)
+      printf("blk %d t %d rows %llu gather %llu norm %llu total %llu ns\n", blockIdx.x, t, tr[t][1] - tr[t][0],
+             tr[t][2] - tr[t][1], tr[t][3] - tr[t][2], tr[t][3] - tr[t][0]);
+#endif
+  if (blockIdx.x == 0) compute_series(a.P, a.kern, a.K, a.safety, lam, a.c_given);
+}
+
+// Small s (rows_per_cta x s / 256 <= ROWS x COLS): the CTA's rows of G (or c^4 G^4)
+// live in REGISTERS -- thread x owns columns j = x + 256 c -- and so does its slice of
+// v, gathered straight from the LL words into the same thread.  One block
+// reduction per product carries both the ROWS row partials of u_{t+1} = G u_t and
+// ||u_t||^2, so a product is: FMAs, one reduction, LL publish, LL gather.  The
+// reductions run in a fixed order (warp butterflies, then warps 0..7), so every
+// CTA computes the same ||u_t|| bitwise.
+template <int ROWS, int COLS>
+__global__ void __launch_bounds__(256) k_power_reg(PowerArgs<double> a) {
+  __shared__ double s_part[8][ROWS + 1];
+  __shared__ double s_res[ROWS + 1];
+  __shared__ double s_v[256 * COLS];
+  const int64_t s = a.s;
+  const int64_t r0 = (int64_t)blockIdx.x * a.rows_per_cta;
+  const int nrows = (int)min((int64_t)a.rows_per_cta, s - r0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double g[ROWS][COLS];
+  auto load_rows = [&](const double* M) {
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r)
+#pragma unroll
+      for (int c = 0; c < COLS; ++c) {
+        const int64_t j = threadIdx.x + 256 * c;
+        g[r][c] = (r < nrows && j < s) ? M[(r0 + r) * a.ld + j] : 0.0;
+      }
+  };
+  load_rows(a.q > 0 ? a.G4 : a.G);
+  double v[COLS];
+  const double v0 = 1.0 / sqrt((double)s);
+#pragma unroll
+  for (int c = 0; c < COLS; ++c) v[c] = (threadIdx.x + 256 * c < s) ? v0 : 0.0;
+  const int niter = a.T - 3 * a.q;
+  double lam = 0.0, inv = 1.0;
+  bool degenerate = false;
+  // block reduction of p[0..ROWS] into s_res (fixed order)
+  auto reduce = [&](double (&p)[ROWS + 1]) {
+#pragma unroll
+    for (int r = 0; r <= ROWS; ++r) p[r] = warp_sum(p[r]);
+    if (lane == 0)
+#pragma unroll
+      for (int r = 0; r <= ROWS; ++r) s_part[warp][r] = p[r];
+    __syncthreads();
+    if (threadIdx.x <= ROWS) {
+      double acc = s_part[0][threadIdx.x];
+#pragma unroll
+      for (int w = 1; w < 8; ++w) acc += s_part[w][threadIdx.x];
+      s_res[threadIdx.x] = acc;
+    }
+    __syncthreads();
+  };
+#ifdef CPA_POWER_TRACE
+  unsigned long long tr[8][4];
+  auto stamp = [&](int t, int i) {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    if (t < 8) tr[t][i] = v;
+  };
+#else
+  auto stamp = [&](int, int) {};
+#endif
+  for (int t = 0; t < niter; ++t) {
+    stamp(t, 0);
+    if (a.q > 0 && t == a.q) load_rows(a.G);   // remaining products by G itself
+    double p[ROWS + 1];
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) {
+      double d = 0.0;
+#pragma unroll
+      for (int c = 0; c < COLS; ++c) d = fma(g[r][c], v[c], d);
+      p[r] = d;
+    }
+    double sq = 0.0;
+#pragma unroll
+    for (int c = 0; c < COLS; ++c) sq = fma(v[c], v[c], sq);
+    p[ROWS] = sq;
+    reduce(p);
+    if (t > 0) {  // ||u_{t-1}||: v_{t-1} = u_{t-1} / ||u_{t-1}|| is folded into this product
+      lam = sqrt(s_res[ROWS]);
+      if (!(lam > kDegenerateLambda) || !(lam < 1e300)) { degenerate = true; break; }
+      inv = 1.0 / lam;
+    }
+    stamp(t, 1);
+    const unsigned flag = (unsigned)t + 1u;
+    unsigned long long* buf = a.ll + (int64_t)(t & 1) * s * 2;
+    if (threadIdx.x < nrows) st_ll(buf + 2 * (r0 + threadIdx.x), s_res[threadIdx.x] * inv, flag);
+    ll_gather(buf, s, flag, s_v);
+    stamp(t, 2);
+#pragma unroll
+    for (int c = 0; c < COLS; ++c) v[c] = (threadIdx.x + 256 * c < s) ? s_v[threadIdx.x + 256 * c] : 0.0;
+  }
+  if (!degenerate) {  // lambda_hat = ||u_{niter-1}||
+    double p[ROWS + 1];
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) p[r] = 0.0;
+    double sq = 0.0;
+#pragma unroll
+    for (int c = 0; c < COLS; ++c) sq = fma(v[c], v[c], sq);
+    p[ROWS] = sq;
+    reduce(p);
+    lam = sqrt(s_res[ROWS]);
+    if (!(lam > kDegenerateLambda) || !(lam < 1e300)) degenerate = true;
+  }
+  if (degenerate) lam = lam < 1e300 ? 0.0 : lam;
+#ifdef CPA_POWER_TRACE
+  if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
+    for (int t = 1; t < 8 && t < niter; ++t)
+      printf("reg blk %d t %d reduce %llu gather %llu total %llu ns\n", blockIdx.x, t, tr[t][1] - tr[t][0],
+             tr[t][2] - tr[t][1], tr[t][2] - tr[t][0]);
+#endif
   if (blockIdx.x == 0) compute_series(a.P, a.kern, a.K, a.safety, lam, a.c_given);
 }
 
@@ -194,8 +348,10 @@ cudaError_t launch_series(SeriesParams* P, const cpa_svt_kernel& k, int K, doubl
   return cudaGetLastError();
 }
 
-// Scratch needed by launch_power_dense (doubles): 2 s + 2 * 148 * 8, plus 2 uints.
-size_t power_dense_scratch_doubles(int64_t s) { return (size_t)(2 * s + 4096 + 8); }
+// Scratch needed by launch_power_dense (doubles): the LL exchange (4 s words) and
+// the squaring scale slot at power_scale_offset(s).
+size_t power_dense_scratch_doubles(int64_t s) { return (size_t)(4 * s + 16); }
+size_t power_scale_offset(int64_t s) { return (size_t)(4 * s + 8); }
 
 // c = 2^-e with e = ilogb(max_i G_ii): G_ii <= lambda_max <= s * max_i G_ii, so
 // c^4 G^4 has its dominant eigenvalue in [1/16, 16 s^4]: no overflow/underflow.
@@ -239,8 +395,9 @@ static cudaError_t launch_power_t(const E* G, const E* G4, int64_t s, int64_t ld
   a.G = G; a.s = s; a.T = T;
   a.G4 = G4;
   a.q = G4 ? (T - 1) / 4 : 0;
-  a.ubuf = scratch; a.part = scratch + 2 * s;
-  a.bar = bar; a.P = P; a.kern = k; a.K = K; a.safety = safety; a.c_given = c_given;
+  a.ll = reinterpret_cast<unsigned long long*>(scratch);
+  (void)bar;
+  a.P = P; a.kern = k; a.K = K; a.safety = safety; a.c_given = c_given;
   // Fewest CTAs whose rows of G fit in shared memory (fewer arrivals per
   // barrier); otherwise one CTA per SM streaming its rows from L2/HBM.
   const size_t budget = 200 * 1024;
@@ -255,8 +412,16 @@ static cudaError_t launch_power_t(const E* G, const E* G4, int64_t s, int64_t ld
   a.rows_per_cta = (int)((s + grid - 1) / grid);
   grid = (s + a.rows_per_cta - 1) / a.rows_per_cta;
   if (a.cache_rows) smem += (size_t)a.rows_per_cta * s * sizeof(E);
-  cudaError_t e0 = cudaMemsetAsync(bar, 0, sizeof(unsigned int), st);
+  cudaError_t e0 = cudaMemsetAsync(scratch, 0, (size_t)4 * s * sizeof(double), st);
   if (e0 != cudaSuccess) return e0;
+  if constexpr (sizeof(E) == sizeof(double)) {
+    // register-resident rows for small s (c1, c2): <= 8 rows x 4 columns per thread
+    if (a.rows_per_cta <= 8 && s <= 1024 && !getenv("CPA_SVT_POWER_SMEM")) {
+      void* args[] = {&a};
+      const size_t pad = 0;
+      return cudaLaunchCooperativeKernel((void*)k_power_reg<8, 4>, dim3((unsigned)grid), dim3(256), args, pad, st);
+    }
+  }
   cudaError_t e = cudaFuncSetAttribute(k_power_dense<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   void* args[] = {&a};
