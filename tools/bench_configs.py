@@ -68,14 +68,18 @@ def dense(name, h, reps, m=None, n=None, K=None, dtype="f64", math="native"):
     Y = torch.empty_like(X)
     T = cfg["T"]
     ms, ph = timed(lambda: h.apply(X, cfg["kernel"], K, T=T, Y=Y, math=math), reps, h)
+    form = h.apply(X, cfg["kernel"], K, T=T, Y=Y, math=math, info=True)[1]["form"]
     s, L = min(m, n), max(m, n)
-    poly = "final" in ph  # Alg. 1 s x s form: 2(K-2)s^3 recurrence + 2 s^2 L final product
-    rec = (K - 2) * 2 * s ** 3 + 2 * s * s * s if poly else (K - 1) * 2 * s * s * L
-    F = s * (s + 1) * L + rec + (2 * s * s * L if poly else 0)
-    step_ms = ph.get("step", (0, 0))[0] + ph.get("init", (0, 0))[0]
+    # recurrence flops of the form that ran: 1 apply-to-X (K-1) 2 s^2 L; 2 symmetric s x s (K-2) s^2 (s+1)
+    # (+ final 2 s^2 L); 3 s x s on full tiles (K-2) 2 s^3 (+ final)
+    rec = {1: (K - 1) * 2 * s * s * L, 2: (K - 2) * s * s * (s + 1), 3: (K - 2) * 2 * s ** 3}[form]
+    F_exec = s * (s + 1) * L + rec + (0 if form == 1 else 2 * s * s * L)
+    F_eff = s * (s + 1) * L + (K - 1) * 2 * s * s * L   # bench.py's fixed per-workload count
+    step_ms = ph.get("step", (0, 0))[0] + (ph.get("init", (0, 0))[0] if form == 1 else 0)
     r = {"config": name, "shape": [m, n], "K": K, "T": T, "dtype": dtype, "math": math,
-         "form": "poly (Alg. 1 s x s)" if poly else "apply-to-X", "ms_per_svt": ms,
-         "gflops": F / ms / 1e6, "phases_ms": {k: v[0] for k, v in ph.items()},
+         "form": {1: "apply-to-X", 2: "s x s symmetric", 3: "s x s full tiles"}[form], "ms_per_svt": ms,
+         "gflops_effective": F_eff / ms / 1e6, "gflops_executed": F_exec / ms / 1e6,
+         "phases_ms": {k: v[0] for k, v in ph.items()},
          "recurrence_tflops": rec / step_ms / 1e9 if step_ms else None}
     if dtype == "f64":
         r["recurrence_frac_of_dmma_peak"] = rec / step_ms / 1e9 / PEAKS["fp64_dmma_tflops"] if step_ms else None
