@@ -55,7 +55,11 @@ cudaError_t launch_power_dense_f32(const float* G, int64_t s, int64_t ld, int T,
 cudaError_t tc_gemm(int mode, int terms, int M, int N, int Kd, const float* Ah, const float* Al, int64_t lda,
                     const float* Bh, const float* Bl, int64_t ldb, bool b_mn, float* out_f, float* out_h,
                     float* out_l, int out_split, int64_t ld_out, const float* wp, const float* wpp, int64_t ld_w,
-                    float* y, int64_t ld_y, const SeriesParams* P, int k, int num_sms, cudaStream_t st);
+                    float* y, int64_t ld_y, const SeriesParams* P, int k, int num_sms, cudaStream_t st,
+                    int sym = 0);
+cudaError_t tf32_sym_init(const float* G, int64_t s, int64_t ld, float* Wf, float* Wh, float* Wl, float* H,
+                          const SeriesParams* P, int num_sms, cudaStream_t st);
+cudaError_t tf32_sym_prep(const float* H, int64_t s, int64_t ld, float* Hh, float* Hl, int num_sms, cudaStream_t st);
 cudaError_t tf32_prep(const float* X, int64_t m, int64_t n, int64_t ldx, bool transpose, float* Af, float* Ah,
                       float* Al, int64_t lda, int num_sms, cudaStream_t st);
 cudaError_t tf32_finish(const float* Yi, int64_t ldi, int64_t m, int64_t n, bool transpose, float* Y, int64_t ldy,
@@ -616,7 +620,7 @@ static cpa_svt_status apply_tf32(cpa_svt_handle* h, int terms, int64_t m, int64_
   if (s > 2147483647 / 2 || L > 2147483647 / 2) return CPA_SVT_E_UNSUPPORTED;
   const int64_t sp = (s + 3) / 4 * 4, Lp = (L + 3) / 4 * 4;
   // s x s form on full tiles (2(K-2) s^3 + 2 s^2 L) when it beats apply-to-X ((K-1) 2 s^2 L)
-  const bool poly = K > 2 && h->form != 1 && (h->form >= 2 || s < L);
+  const bool poly = K > 2 && h->form != 1;  // symmetric s x s form: fewer flops for any K > 2
   auto al = [](size_t b) { return (b + 255) / 256 * 256; };
   const size_t nA = al((size_t)s * Lp * 4), nG = al((size_t)s * sp * 4);
   const size_t nPow = al(power_dense_scratch_doubles(s) * 8);
@@ -658,8 +662,9 @@ static cpa_svt_status apply_tf32(cpa_svt_handle* h, int terms, int64_t m, int64_
     Phase p(h, CPA_SVT_PH_GRAM);
     CU(tf32_prep(X, m, n, ldx, !left, Xs[0], Xs[1], Xs[2], Lp, h->num_sms, h->stream));
     // Gram always 3xTF32: G(i,j) = sum_l A(i,l) A(j,l), both operands K-major
+    // lower-triangle tiles only, mirrored (G exactly symmetric)
     CU(tc_gemm(0, 3, (int)s, (int)s, (int)L, Xs[1], Xs[2], Lp, Xs[1], Xs[2], Lp, false, Gf, Gh, Gl, 3, sp, nullptr,
-               nullptr, 0, nullptr, 0, nullptr, 0, h->num_sms, h->stream));
+               nullptr, 0, nullptr, 0, nullptr, 0, h->num_sms, h->stream, 1));
     launches += 2;
   }
   tm.mark();
@@ -690,26 +695,31 @@ static cpa_svt_status apply_tf32(cpa_svt_handle* h, int terms, int64_t m, int64_
   float** W0 = poly ? Is : Xs;
   const int64_t RN = poly ? s : L, ldr = poly ? sp : Lp;
   float* Yr = poly ? Hs[0] : Yi;
+  float** sets[2] = {W0, As};
   if (poly) {
+    // symmetric s x s form: W_1 = B_hat and H elementwise (no product), then lower-triangle
+    // tiles per step with the TF32 operand copies mirrored; W_0 = I is read by step 2 only
     CU(tf32_eye(Is[0], s, sp, h->num_sms, h->stream));
-    CU(tf32_prep(Is[0], s, sp, sp, false, Is[0], Is[1], Is[2], sp, h->num_sms, h->stream));
+    {
+      Phase p(h, CPA_SVT_PH_INIT);
+      CU(tf32_sym_init(Gf, s, sp, As[0], As[1], terms == 3 ? As[2] : nullptr, Hs[0], h->P, h->num_sms, h->stream));
+    }
     launches += 2;
   }
-  float** sets[2] = {W0, As};
-  for (int kk = 1; kk < K; ++kk) {
+  for (int kk = poly ? 2 : 1; kk < K; ++kk) {
     float** src = sets[(kk - 1) & 1];      // W_{k-1}: k=1 -> W_0
     float** out = sets[kk & 1];            // W_k overwrites W_{k-2} (k >= 2)
     const bool last = kk == K - 1;
     Phase p(h, kk == 1 ? CPA_SVT_PH_INIT : CPA_SVT_PH_STEP);
     CU(tc_gemm(kk == 1 ? 1 : 2, terms, (int)s, (int)RN, (int)s, Gh, Gl, sp, src[1], src[2], ldr, true,
                last ? nullptr : out[0], last ? nullptr : out[1], last ? nullptr : out[2], terms, ldr, src[0],
-               kk == 1 ? nullptr : out[0], ldr, Yr, ldr, h->P, kk, h->num_sms, h->stream));
+               kk == 1 ? nullptr : out[0], ldr, Yr, ldr, h->P, kk, h->num_sms, h->stream, poly ? 1 : 0));
     ++launches;
   }
   if (poly) {
     // Alg. 1 line 12: Y = H_hat A, one tcgen05 product (H_hat split into hi/lo operands)
     Phase p(h, CPA_SVT_PH_FINAL);
-    CU(tf32_prep(Hs[0], s, sp, sp, false, Hs[0], Hs[1], Hs[2], sp, h->num_sms, h->stream));
+    CU(tf32_sym_prep(Hs[0], s, sp, Hs[1], Hs[2], h->num_sms, h->stream));  // H lower -> full hi / lo
     CU(tc_gemm(0, terms, (int)s, (int)L, (int)s, Hs[1], Hs[2], sp, Xs[1], Xs[2], Lp, true, Yi, nullptr, nullptr, 1,
                Lp, nullptr, nullptr, 0, nullptr, 0, nullptr, 0, h->num_sms, h->stream));
     launches += 2;
@@ -727,7 +737,7 @@ static cpa_svt_status apply_tf32(cpa_svt_handle* h, int terms, int64_t m, int64_
     info->ms_recurrence = tm.ms(3, 4);
     info->ms_total = tm.ms(0, 4);
     info->kernel_launches = launches;
-    info->form = poly ? 3 : 1;
+    info->form = poly ? 2 : 1;
   }
   return CPA_SVT_OK;
 }

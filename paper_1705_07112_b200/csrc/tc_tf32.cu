@@ -21,7 +21,10 @@
 // CTAs in flight share A and B panels through L2.
 #include <cuda.h>
 
+#include <algorithm>
 #include <cstdlib>
+#include <map>
+#include <vector>
 
 #include "common.cuh"
 
@@ -53,6 +56,13 @@ struct TcArgs {
   int k;
   int tiles_m, tiles_n;
   int dbg_lbo, dbg_sbo;          // debugging overrides of the B (MN-major) descriptor strides
+  // symmetric output (M == N, BN == BM): only tiles meeting the lower triangle run
+  // (from tile_list), only elements r >= c are computed, and the TF32 operand copies
+  // (and out_f when mirror_f) are mirrored to (c, r)
+  int sym;
+  int mirror_f;
+  const int2* tile_list;
+  int ntiles_list;
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -183,8 +193,17 @@ __global__ void __launch_bounds__(NTHR, 1)
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ntiles = a.tiles_m * a.tiles_n;
+  const int ntiles = a.tile_list ? a.ntiles_list : a.tiles_m * a.tiles_n;
   const int nk = (a.Kd + BK - 1) / BK;
+  auto coords = [&](int t, int& tm, int& tn) {
+    if (a.tile_list) {
+      const int2 v = a.tile_list[t];
+      tm = v.x;
+      tn = v.y;
+    } else {
+      tile_coords(t, a.tiles_m, a.tiles_n, tm, tn);
+    }
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < ST; ++s) {
@@ -216,7 +235,7 @@ __global__ void __launch_bounds__(NTHR, 1)
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
         int tm, tn;
-        tile_coords(t, a.tiles_m, a.tiles_n, tm, tn);
+        coords(t, tm, tn);
         const int m0 = tm * BM, n0 = tn * BN;
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(empty + stage, phase ^ 1);
@@ -299,7 +318,7 @@ __global__ void __launch_bounds__(NTHR, 1)
     const SeriesParams* P = a.P;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
       int tm, tn;
-      tile_coords(t, a.tiles_m, a.tiles_n, tm, tn);
+      coords(t, tm, tn);
       mbar_wait(tfull + acc, aphase);
       tc_fence_after();
       const int row0 = tm * BM + quarter * 32;
@@ -317,12 +336,14 @@ __global__ void __launch_bounds__(NTHR, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) tb[lane * 33 + j] = v[j];
         __syncwarp();
-        const int c = tn * BN + cc * 32 + lane;
+        const int cbase = tn * BN + cc * 32;
+        const int c = cbase + lane;
         if (c < a.N) {
 #pragma unroll 4
           for (int i = 0; i < 32; ++i) {
             const int r = row0 + i;
             if (r >= a.M) break;
+            if (a.sym && c > r) continue;                          // upper triangle: mirrored below
             const float accv = tb[i * 33 + lane];
             float w = accv;
             if (a.mode == INIT) {
@@ -343,9 +364,31 @@ __global__ void __launch_bounds__(NTHR, 1)
               a.out_h[o] = hi;
               if (a.out_split == 3) a.out_l[o] = rna_tf32(w - hi);
             }
+            if (a.sym) tb[i * 33 + lane] = w;
           }
         }
         __syncwarp();
+        if (a.sym) {
+          // mirror (r, c) -> (c, r) for r > c from the natural layout (lane = row): for a
+          // fixed column j the warp writes one coalesced 128-byte segment of row c
+          const int r = row0 + lane;
+          if (r < a.M) {
+#pragma unroll 4
+            for (int j = 0; j < 32; ++j) {
+              const int cm = cbase + j;
+              if (cm >= a.N || cm >= r) break;
+              const float w = tb[lane * 33 + j];
+              const int64_t o = (int64_t)cm * a.ld_out + r;
+              if (a.mirror_f && a.out_f) a.out_f[o] = w;
+              if (a.out_h) {
+                const float hi = rna_tf32(w);
+                a.out_h[o] = hi;
+                if (a.out_split == 3) a.out_l[o] = rna_tf32(w - hi);
+              }
+            }
+          }
+          __syncwarp();
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -402,10 +445,35 @@ static cudaError_t launch_t(const CUtensorMap& ah, const CUtensorMap& al, const 
   auto fn = k_tc_gemm<BN, TERMS, B_MN>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, S::BYTES);
   if (e != cudaSuccess) return e;
-  const int ntiles = a.tiles_m * a.tiles_n;
+  const int ntiles = a.tile_list ? a.ntiles_list : a.tiles_m * a.tiles_n;
   const int grid = ntiles < num_sms ? ntiles : num_sms;
   fn<<<grid, NTHR, S::BYTES, st>>>(ah, al, bh, bl, a);
   return cudaGetLastError();
+}
+
+// Lower-triangle tile list (tm >= tn) of a T x T tile grid in the grouped-M raster
+// order of tile_coords; built once per T and kept on the device.
+static const int2* sym_tile_list(int T, int* count) {
+  static std::map<int, std::pair<int2*, int>> cache;
+  auto it = cache.find(T);
+  if (it != cache.end()) {
+    *count = it->second.second;
+    return it->second.first;
+  }
+  std::vector<int2> v;
+  constexpr int GROUP = 16;
+  for (int first = 0; first < T; first += GROUP) {
+    const int gsize = std::min(GROUP, T - first);
+    for (int tn = 0; tn < T; ++tn)
+      for (int r = 0; r < gsize; ++r)
+        if (first + r >= tn) v.push_back(make_int2(first + r, tn));
+  }
+  int2* d = nullptr;
+  if (cudaMalloc(&d, v.size() * sizeof(int2)) != cudaSuccess) return nullptr;
+  if (cudaMemcpy(d, v.data(), v.size() * sizeof(int2), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
+  cache[T] = {d, (int)v.size()};
+  *count = (int)v.size();
+  return d;
 }
 
 template <int BN>
@@ -413,7 +481,7 @@ static cudaError_t tc_gemm_bn(int mode, int terms, int M, int N, int Kd, const f
                               int64_t lda, const float* Bh, const float* Bl, int64_t ldb, bool b_mn, float* out_f,
                               float* out_h, float* out_l, int out_split, int64_t ld_out, const float* wp,
                               const float* wpp, int64_t ld_w, float* y, int64_t ld_y, const SeriesParams* P, int k,
-                              int num_sms, cudaStream_t st) {
+                              int num_sms, cudaStream_t st, int sym) {
   using namespace tc;
   CUtensorMap ah, al, bh, bl;
   cudaError_t e = make_map(&ah, Ah, M, Kd, lda, BM);
@@ -432,6 +500,13 @@ static cudaError_t tc_gemm_bn(int mode, int terms, int M, int N, int Kd, const f
   a.wp = wp; a.wpp = wpp; a.ld_w = ld_w; a.y = y; a.ld_y = ld_y; a.P = P; a.k = k;
   a.tiles_m = (M + BM - 1) / BM;
   a.tiles_n = (N + BN - 1) / BN;
+  if (sym) {
+    if (M != N || BN != BM) return cudaErrorInvalidValue;
+    a.sym = 1;
+    a.mirror_f = mode == GRAM;
+    a.tile_list = sym_tile_list(a.tiles_m, &a.ntiles_list);
+    if (!a.tile_list) return cudaErrorMemoryAllocation;
+  }
   if (const char* v = getenv("CPA_SVT_DBG_LBO")) a.dbg_lbo = atoi(v);
   if (const char* v = getenv("CPA_SVT_DBG_SBO")) a.dbg_sbo = atoi(v);
   if (terms == 3) {
@@ -452,14 +527,15 @@ static cudaError_t tc_gemm_bn(int mode, int terms, int M, int N, int Kd, const f
 cudaError_t tc_gemm(int mode, int terms, int M, int N, int Kd, const float* Ah, const float* Al, int64_t lda,
                     const float* Bh, const float* Bl, int64_t ldb, bool b_mn, float* out_f, float* out_h,
                     float* out_l, int out_split, int64_t ld_out, const float* wp, const float* wpp, int64_t ld_w,
-                    float* y, int64_t ld_y, const SeriesParams* P, int k, int num_sms, cudaStream_t st) {
+                    float* y, int64_t ld_y, const SeriesParams* P, int k, int num_sms, cudaStream_t st, int sym) {
   int bn = 128;
   if (const char* v = getenv("CPA_SVT_TC_BN")) bn = atoi(v) == 256 ? 256 : 128;
+  if (sym) bn = 128;
   if (bn == 256)
     return tc::tc_gemm_bn<256>(mode, terms, M, N, Kd, Ah, Al, lda, Bh, Bl, ldb, b_mn, out_f, out_h, out_l, out_split,
-                               ld_out, wp, wpp, ld_w, y, ld_y, P, k, num_sms, st);
+                               ld_out, wp, wpp, ld_w, y, ld_y, P, k, num_sms, st, sym);
   return tc::tc_gemm_bn<128>(mode, terms, M, N, Kd, Ah, Al, lda, Bh, Bl, ldb, b_mn, out_f, out_h, out_l, out_split,
-                             ld_out, wp, wpp, ld_w, y, ld_y, P, k, num_sms, st);
+                             ld_out, wp, wpp, ld_w, y, ld_y, P, k, num_sms, st, sym);
 }
 
 // ------------------------------------------------------------------ prep / finish
@@ -499,6 +575,66 @@ __global__ void k_eye_f32(float* I, int64_t s, int64_t ld) {
 }
 cudaError_t tf32_eye(float* I, int64_t s, int64_t ld, int num_sms, cudaStream_t st) {
   k_eye_f32<<<num_sms * 8, 256, 0, st>>>(I, s, ld);
+  return cudaGetLastError();
+}
+
+// Symmetric s x s form, k = 1 (Alg. 1 l.5-7): W_1 = (2/L) G - I (full, hi, lo), H = c_0/2 I + c_1 W_1.
+__global__ void k_sym_init_f32(const float* G, int64_t s, int64_t ld, float* Wf, float* Wh, float* Wl, float* H,
+                               const SeriesParams* P) {
+  const float s2 = (float)P->scale2, h0 = (float)(0.5 * P->c[0]), c1 = (float)P->c[1];
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < s * ld; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / ld, j = e % ld;
+    const float id = (i == j) ? 1.f : 0.f;
+    const float w = j < s ? s2 * G[e] - id : 0.f;
+    const float hi = tc::rna_tf32(w);
+    Wf[e] = w;
+    Wh[e] = hi;
+    if (Wl) Wl[e] = tc::rna_tf32(w - hi);
+    H[e] = j < s ? h0 * id + c1 * w : 0.f;
+  }
+}
+cudaError_t tf32_sym_init(const float* G, int64_t s, int64_t ld, float* Wf, float* Wh, float* Wl, float* H,
+                          const SeriesParams* P, int num_sms, cudaStream_t st) {
+  k_sym_init_f32<<<num_sms * 8, 256, 0, st>>>(G, s, ld, Wf, Wh, Wl, H, P);
+  return cudaGetLastError();
+}
+
+// H (lower triangle valid) -> hi / lo TF32 copies of the full symmetric matrix, through
+// 32 x 32 shared-memory tiles (every global access coalesced).
+__global__ void k_sym_prep_f32(const float* H, int64_t s, int64_t ld, float* Hh, float* Hl) {
+  __shared__ float t[32][33];
+  const int T = (int)((s + 31) / 32);
+  for (int64_t b = blockIdx.x; b < (int64_t)T * T; b += gridDim.x) {
+    const int bi = (int)(b / T), bj = (int)(b % T);
+    if (bi < bj) continue;
+    const int64_t r0 = (int64_t)bi * 32, c0 = (int64_t)bj * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+      const int64_t r = r0 + i, c = c0 + threadIdx.x;
+      t[i][threadIdx.x] = (r < s && c < s && (bi != bj || c <= r)) ? H[r * ld + c] : 0.f;
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+      const int64_t r = r0 + i, c = c0 + threadIdx.x;   // lower block (bi, bj)
+      // diagonal block: element (r, c) above its diagonal comes from (c, r)
+      const float v = (bi == bj && threadIdx.x > i) ? t[threadIdx.x][i] : t[i][threadIdx.x];
+      if (r < s && c < s) {
+        const float hi = tc::rna_tf32(v);
+        Hh[r * ld + c] = hi;
+        Hl[r * ld + c] = tc::rna_tf32(v - hi);
+      }
+      const int64_t rm = c0 + i, cm = r0 + threadIdx.x;  // mirror block (bj, bi): element (rm, cm) = H(cm, rm)
+      if (bi != bj && rm < s && cm < s) {
+        const float w = t[threadIdx.x][i];
+        const float hi = tc::rna_tf32(w);
+        Hh[rm * ld + cm] = hi;
+        Hl[rm * ld + cm] = tc::rna_tf32(w - hi);
+      }
+    }
+    __syncthreads();
+  }
+}
+cudaError_t tf32_sym_prep(const float* H, int64_t s, int64_t ld, float* Hh, float* Hl, int num_sms, cudaStream_t st) {
+  k_sym_prep_f32<<<num_sms * 8, dim3(32, 8), 0, st>>>(H, s, ld, Hh, Hl);
   return cudaGetLastError();
 }
 

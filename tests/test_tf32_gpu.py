@@ -85,7 +85,8 @@ def test_tf32_gemm_engine(env):
                 assert float((C - ref).norm() / ref.norm()) <= tol, (M, N, K, b_mn, terms)
 
 
-@pytest.mark.parametrize("shape,K", [((200, 700), 20), ((700, 200), 12), ((256, 256), 9)])
+@pytest.mark.parametrize("shape,K", [((200, 700), 20), ((700, 200), 12), ((256, 256), 9), ((1000, 1300), 7),
+                                     ((129, 400), 4), ((300, 300), 3)])
 def test_tf32_both_forms(env, shape, K):
     """3xTF32 in the Alg. 1 s x s form and in the apply-to-X form, against the oracle."""
     torch, P, _ = env
