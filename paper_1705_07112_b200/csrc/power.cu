@@ -109,8 +109,9 @@ __device__ __forceinline__ void ld_ll(const unsigned long long* p, unsigned long
 // the first CPA_POLL_WARPS warps poll (every thread of every CTA spinning on the
 // same lines stalls the whole exchange for ~10 us -- measured); each polling lane
 // keeps 8 words in flight and re-issues only the late ones.  Ends with a CTA barrier.
-__device__ __forceinline__ void ll_gather(const unsigned long long* buf, int64_t s, unsigned flag, double* dst) {
-  constexpr int NP = 32 * CPA_POLL_WARPS;
+__device__ __forceinline__ void ll_gather(const unsigned long long* buf, int64_t s, unsigned flag, double* dst,
+                                          int np = 32 * CPA_POLL_WARPS) {
+  const int NP = np;
   if (threadIdx.x < NP) {
     const int pl = threadIdx.x;
     for (int64_t j0 = 0; j0 < s; j0 += NP * 8) {
@@ -342,6 +343,87 @@ __global__ void __launch_bounds__(256) k_power_reg(PowerArgs<double> a) {
   if (blockIdx.x == 0) compute_series(a.P, a.kern, a.K, a.safety, lam, a.c_given);
 }
 
+// Large s: the Gram does not fit on chip, so every product streams G from HBM
+// once.  One CTA (512 threads) per SM owns a contiguous block of rows; a warp
+// reads a row with 16-byte vector loads, 8 in flight per lane (4 KB per warp,
+// 64 KB per SM: enough memory-level parallelism for the HBM roofline); v_{t-1}
+// (fp64) lives in shared memory.  Exchange and norm as in k_power_dense, with
+// enough polling lanes that a gather takes a few rounds.
+template <typename E>
+__global__ void __launch_bounds__(512) k_power_stream(PowerArgs<E> a) {
+  extern __shared__ __align__(16) double psm[];
+  __shared__ double s_warp[16];
+  __shared__ double s_norm;
+  constexpr int VEC = 16 / sizeof(E);  // elements per 16-byte load
+  const int64_t s = a.s;
+  double* sv = psm;
+  const int64_t r0 = (int64_t)blockIdx.x * a.rows_per_cta;
+  const int64_t r1 = min(s, r0 + a.rows_per_cta);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  const bool vec = (a.ld % VEC) == 0 && ((reinterpret_cast<uintptr_t>(a.G) & 15) == 0) &&
+                   (a.G4 == nullptr || (reinterpret_cast<uintptr_t>(a.G4) & 15) == 0);
+  const double v0 = 1.0 / sqrt((double)s);
+  for (int64_t j = threadIdx.x; j < s; j += blockDim.x) sv[j] = v0;
+  __syncthreads();
+  const int np = (int)min((int64_t)blockDim.x, max((int64_t)128, (s + 7) / 8 / 32 * 32));
+  double lam = 0.0, inv = 1.0;
+  const int niter = a.T - 3 * a.q;   // q products by c^4 G^4, then the rest by G
+  for (int t = 0; t < niter; ++t) {
+    const unsigned flag = (unsigned)t + 1u;
+    unsigned long long* buf = a.ll + (int64_t)(t & 1) * s * 2;
+    const E* Gt = t < a.q ? a.G4 : a.G;
+    for (int64_t r = r0 + warp; r < r1; r += nwarps) {
+      const E* row = Gt + r * a.ld;
+      double d[4] = {0, 0, 0, 0};
+      int64_t j = 0;
+      if (vec) {
+        constexpr int STEP = 32 * VEC * 8;   // elements per warp iteration (8 loads per lane)
+        for (; j + STEP <= s; j += STEP) {
+          E x[8][VEC];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const E* p = row + j + (int64_t)(u * 32 + lane) * VEC;
+            if constexpr (VEC == 4) {
+              const float4 q = __ldcs(reinterpret_cast<const float4*>(p));
+              x[u][0] = q.x; x[u][1] = q.y; x[u][2] = q.z; x[u][3] = q.w;
+            } else {
+              const double2 q = __ldcs(reinterpret_cast<const double2*>(p));
+              x[u][0] = q.x; x[u][1] = q.y;
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) {
+              const int64_t jj = j + (int64_t)(u * 32 + lane) * VEC + e;
+              d[(u * VEC + e) & 3] = fma((double)x[u][e], sv[jj], d[(u * VEC + e) & 3]);
+            }
+        }
+      }
+      for (int64_t jj = j + lane; jj < s; jj += 32) d[0] = fma((double)row[jj], sv[jj], d[0]);
+      const double dd = warp_sum((d[0] + d[1]) + (d[2] + d[3])) * inv;
+      if (lane == 0) st_ll(buf + 2 * r, dd, flag);
+    }
+    __syncthreads();  // every warp is done reading sv
+    ll_gather(buf, s, flag, sv, np);
+    double sq = 0.0;
+    for (int64_t j = threadIdx.x; j < s; j += blockDim.x) sq = fma(sv[j], sv[j], sq);
+    sq = warp_sum(sq);
+    if (lane == 0) s_warp[warp] = sq;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double q = 0.0;
+      for (int w = 0; w < nwarps; ++w) q += s_warp[w];
+      s_norm = sqrt(q);
+    }
+    __syncthreads();
+    lam = s_norm;
+    if (!(lam > kDegenerateLambda) || !(lam < 1e300)) { lam = lam < 1e300 ? 0.0 : lam; break; }
+    inv = 1.0 / lam;
+  }
+  if (blockIdx.x == 0) compute_series(a.P, a.kern, a.K, a.safety, lam, a.c_given);
+}
+
 cudaError_t launch_series(SeriesParams* P, const cpa_svt_kernel& k, int K, double safety, double lam_override,
                           const double* lam_src, const double* c_given, cudaStream_t st) {
   k_series<<<1, 256, 0, st>>>(P, k, K, safety, lam_override, lam_src, c_given);
@@ -381,8 +463,8 @@ cudaError_t launch_diag_scale(const double* G, int64_t s, double* scale, cudaStr
 // each of which is latency-bound (~2.5 us) for small s.
 bool power_use_squaring(int64_t s, int T) {
   if (T < 16) return false;
-  const double gemm_us = 2.0 * (double)s * s * s / 25e12 * 1e6;
-  const double iter_us = fmax(2.5, 8.0 * (double)s * s / 5e12 * 1e6);
+  const double gemm_us = 2.0 * (double)s * s * s / 30e12 * 1e6;         // two symmetric squarings
+  const double iter_us = fmax(2.2, 8.0 * (double)s * s / 6e12 * 1e6 + 5.0);  // LL product: latency or HBM
   return gemm_us < 0.75 * T * iter_us;
 }
 
@@ -414,6 +496,16 @@ static cudaError_t launch_power_t(const E* G, const E* G4, int64_t s, int64_t ld
   if (a.cache_rows) smem += (size_t)a.rows_per_cta * s * sizeof(E);
   cudaError_t e0 = cudaMemsetAsync(scratch, 0, (size_t)4 * s * sizeof(double), st);
   if (e0 != cudaSuccess) return e0;
+  if (!a.cache_rows) {
+    // rows do not fit on chip: stream G (or c^4 G^4) from HBM / L2 every product
+    a.rows_per_cta = (int)((s + num_sms - 1) / num_sms);
+    const int64_t g2 = (s + a.rows_per_cta - 1) / a.rows_per_cta;
+    const size_t sm2 = (size_t)s * sizeof(double);
+    cudaError_t e2 = cudaFuncSetAttribute(k_power_stream<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+    if (e2 != cudaSuccess) return e2;
+    void* args[] = {&a};
+    return cudaLaunchCooperativeKernel((void*)k_power_stream<E>, dim3((unsigned)g2), dim3(512), args, sm2, st);
+  }
   if constexpr (sizeof(E) == sizeof(double)) {
     // register-resident rows for small s (c1, c2): <= 8 rows x 4 columns per thread
     if (a.rows_per_cta <= 8 && s <= 1024 && !getenv("CPA_SVT_POWER_SMEM")) {
