@@ -514,10 +514,12 @@ __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB) k_cheb_sym(SymArgs a)
     const int kb = (int)((int64_t)nk * q / S), ke = (int)((int64_t)nk * (q + 1) / S);
     double acc[4][4][2];
     mainloop_dep(a.G, src, s, m0, n0, a.vec, smem, acc, kb, ke, [&] {
+#ifndef CPA_SYM_NOWAIT  // (timing experiment only: wrong results without the waits)
       if (threadIdx.x == 0) {
         if (k >= 3) wait_geq(cross + (k - 1) * T + tj, T);
         if (k >= 4) wait_geq(cross + (k - 2) * T + ti, T);
       }
+#endif
       __syncthreads();
     });
     if (S > 1) {
