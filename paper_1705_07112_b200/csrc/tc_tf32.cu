@@ -34,7 +34,18 @@ namespace tc {
 constexpr int BM = 128;         // UMMA M (cta_group::1): TMEM lane = tile row
 constexpr int BK = 32;          // fp32 elements per 128-byte swizzled row = one k-slab
 constexpr int UK = 8;           // UMMA K for kind::tf32
-constexpr int NTHR = 192;
+// Accumulation chunks: the tensor core's fp32 accumulation over a long K is biased
+// (measured: 3xTF32 Gram diagonal -1e-5 relative at K = 1024, -5.5e-4 at K = 65536,
+// i.e. not round-to-nearest).  Each TMEM accumulator therefore covers chunk_kb
+// k-blocks only; four "drain" warps add every chunk into a TMEM sum buffer with
+// fp32 round-to-nearest adds in a fixed order, and four epilogue warps consume a
+// finished sum while the next tile is being drained (so the global write-out of
+// one tile overlaps the MMAs and drains of the next).
+// Warps: 0 TMA producer, 1 TMEM allocator + MMA issuer, 2..5 drain, 6..9 epilogue.
+constexpr int NTHR = 320;
+constexpr int CHUNK_KB_DEFAULT = 8;    // k-blocks (x BK = 32) per TMEM accumulation
+constexpr int NACC = 2;                // chunk accumulators (TMEM columns [0, 2 BN))
+constexpr int NSUM = 2;                // tile sums (TMEM columns [2 BN, 4 BN))
 
 enum Mode { GRAM = 0, INIT = 1, STEP = 2 };
 
@@ -61,6 +72,7 @@ struct TcArgs {
   // (and out_f when mirror_f) are mirrored to (c, r)
   int sym;
   int mirror_f;
+  int chunk_kb;                  // k-blocks per TMEM accumulation chunk
   const int2* tile_list;
   int ntiles_list;
 };
@@ -133,6 +145,22 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
                : "memory");
 }
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};\n" ::"r"(taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+      "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+      "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
+      "r"(__float_as_uint(v[15])), "r"(__float_as_uint(v[16])), "r"(__float_as_uint(v[17])),
+      "r"(__float_as_uint(v[18])), "r"(__float_as_uint(v[19])), "r"(__float_as_uint(v[20])),
+      "r"(__float_as_uint(v[21])), "r"(__float_as_uint(v[22])), "r"(__float_as_uint(v[23])),
+      "r"(__float_as_uint(v[24])), "r"(__float_as_uint(v[25])), "r"(__float_as_uint(v[26])),
+      "r"(__float_as_uint(v[27])), "r"(__float_as_uint(v[28])), "r"(__float_as_uint(v[29])),
+      "r"(__float_as_uint(v[30])), "r"(__float_as_uint(v[31]))
+      : "memory");
+}
 // 32 consecutive TMEM columns of this warp's 32 lanes -> 32 registers per thread
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   uint32_t r[32];
@@ -189,8 +217,10 @@ __global__ void __launch_bounds__(NTHR, 1)
   uint64_t* full = (uint64_t*)(smem + ST * S::STAGE + S::EPI);
   uint64_t* empty = full + ST;
   uint64_t* tfull = empty + ST;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  uint64_t* tempty = tfull + NACC;
+  uint64_t* sfull = tempty + NACC;
+  uint64_t* sempty = sfull + NSUM;
+  uint32_t* tmem_slot = (uint32_t*)(sempty + NSUM);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntiles = a.tile_list ? a.ntiles_list : a.tiles_m * a.tiles_n;
@@ -210,15 +240,19 @@ __global__ void __launch_bounds__(NTHR, 1)
       mbar_init(full + s, 1);
       mbar_init(empty + s, 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NACC; ++b) {
       mbar_init(tfull + b, 1);
       mbar_init(tempty + b, 4);
     }
+    for (int b = 0; b < NSUM; ++b) {
+      mbar_init(sfull + b, 4);
+      mbar_init(sempty + b, 4);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  if (warp == 1) {  // TMEM: 2 accumulators x BN fp32 columns
+  if (warp == 1) {  // TMEM: NACC chunk accumulators + NSUM tile sums, BN fp32 columns each
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
-                 "r"(2 * BN));
+                 "r"((NACC + NSUM) * BN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   tc_fence_before();
@@ -266,61 +300,101 @@ __global__ void __launch_bounds__(NTHR, 1)
     int acc = 0;
     uint32_t aphase = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      mbar_wait(tempty + acc, aphase ^ 1);
-      tc_fence_after();
-      const uint32_t dtm = tmem_base + (uint32_t)(acc * BN);
-      for (int kb = 0; kb < nk; ++kb) {
-        mbar_wait(full + stage, phase);
+      for (int kb0 = 0; kb0 < nk; kb0 += a.chunk_kb) {
+        mbar_wait(tempty + acc, aphase ^ 1);
         tc_fence_after();
-        if (lane == 0) {
-          const uint32_t st = smem_u32(smem + stage * S::STAGE);
-          const uint32_t a_h = st, a_l = st + S::A_BYTES;
-          const uint32_t b_h = st + NSPLIT * S::A_BYTES, b_l = b_h + S::B_BYTES;
+        const uint32_t dtm = tmem_base + (uint32_t)(acc * BN);
+        const int kend = kb0 + a.chunk_kb < nk ? kb0 + a.chunk_kb : nk;
+        for (int kb = kb0; kb < kend; ++kb) {
+          mbar_wait(full + stage, phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t st = smem_u32(smem + stage * S::STAGE);
+            const uint32_t a_h = st, a_l = st + S::A_BYTES;
+            const uint32_t b_h = st + NSPLIT * S::A_BYTES, b_l = b_h + S::B_BYTES;
 #pragma unroll
-          for (int kk = 0; kk < BK / UK; ++kk) {
-            // A K-major: +32 B per UMMA_K inside the swizzled row; B MN-major: +1 KB (one 8-row group)
-            const uint32_t aoff = kk * UK * 4;
-            const uint32_t boff = B_MN ? kk * 1024 : kk * UK * 4;
-            // MN-major B (tf32): SW128 with 32-byte atoms; 32-element MN chunks LBO = 4 KB
-            // apart, 4-row K groups SBO = 512 B apart; one UMMA_K = 8 rows = +1 KB.
-            const uint32_t blbo = B_MN ? (a.dbg_lbo ? a.dbg_lbo : 4096) : 16;
-            const uint32_t bsbo = B_MN ? (a.dbg_sbo ? a.dbg_sbo : 512) : 1024;
-            const uint32_t blay = B_MN ? 1u : 2u;
-            const uint64_t dAh = smem_desc(a_h + aoff, 16, 1024);
-            const uint64_t dBh = smem_desc(b_h + boff, blbo, bsbo, blay);
-            const uint32_t accum = (kb > 0 || kk > 0) ? 1u : 0u;
-            mma_tf32(dtm, dAh, dBh, IDESC, accum);
-            if (TERMS == 3) {
-              const uint64_t dAl = smem_desc(a_l + aoff, 16, 1024);
-              const uint64_t dBl = smem_desc(b_l + boff, blbo, bsbo, blay);
-              mma_tf32(dtm, dAh, dBl, IDESC, 1u);
-              mma_tf32(dtm, dAl, dBh, IDESC, 1u);
+            for (int kk = 0; kk < BK / UK; ++kk) {
+              // A K-major: +32 B per UMMA_K inside the swizzled row; B MN-major: +1 KB (one 8-row group)
+              const uint32_t aoff = kk * UK * 4;
+              const uint32_t boff = B_MN ? kk * 1024 : kk * UK * 4;
+              // MN-major B (tf32): SW128 with 32-byte atoms; 32-element MN chunks LBO = 4 KB
+              // apart, 4-row K groups SBO = 512 B apart; one UMMA_K = 8 rows = +1 KB.
+              const uint32_t blbo = B_MN ? (a.dbg_lbo ? a.dbg_lbo : 4096) : 16;
+              const uint32_t bsbo = B_MN ? (a.dbg_sbo ? a.dbg_sbo : 512) : 1024;
+              const uint32_t blay = B_MN ? 1u : 2u;
+              const uint64_t dAh = smem_desc(a_h + aoff, 16, 1024);
+              const uint64_t dBh = smem_desc(b_h + boff, blbo, bsbo, blay);
+              const uint32_t accum = (kb > kb0 || kk > 0) ? 1u : 0u;
+              mma_tf32(dtm, dAh, dBh, IDESC, accum);
+              if (TERMS == 3) {
+                const uint64_t dAl = smem_desc(a_l + aoff, 16, 1024);
+                const uint64_t dBl = smem_desc(b_l + boff, blbo, bsbo, blay);
+                mma_tf32(dtm, dAh, dBl, IDESC, 1u);
+                mma_tf32(dtm, dAl, dBh, IDESC, 1u);
+              }
             }
+            mma_commit(empty + stage);  // frees the smem stage when these MMAs complete
           }
-          mma_commit(empty + stage);  // frees the smem stage when these MMAs complete
+          __syncwarp();
+          if (++stage == ST) { stage = 0; phase ^= 1; }
         }
+        if (lane == 0) mma_commit(tfull + acc);  // chunk accumulator ready for the epilogue
         __syncwarp();
-        if (++stage == ST) { stage = 0; phase ^= 1; }
+        if (++acc == NACC) { acc = 0; aphase ^= 1; }
       }
-      if (lane == 0) mma_commit(tfull + acc);  // accumulator ready for the epilogue
-      __syncwarp();
-      if (++acc == 2) { acc = 0; aphase ^= 1; }
+    }
+  } else if (warp < 6) {
+    // ============================ drain (warps 2..5) ======================
+    // sum_b = ((c_0 + c_1) + c_2) + ... over the tile's chunk accumulators (fp32 RN adds)
+    const int quarter = warp & 3;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    int acc = 0, sb = 0;
+    uint32_t aphase = 0, sphase = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      mbar_wait(sempty + sb, sphase ^ 1);
+      tc_fence_after();
+      const uint32_t sum_col = (uint32_t)((NACC + sb) * BN);
+      for (int kb0 = 0; kb0 < nk; kb0 += a.chunk_kb) {
+        mbar_wait(tfull + acc, aphase);
+        tc_fence_after();
+#pragma unroll 1
+        for (int cc = 0; cc < BN / 32; ++cc) {
+          float v[32];
+          tmem_ld32(tmem_base + lane_off + (uint32_t)(acc * BN + cc * 32), v);
+          if (kb0 > 0) {
+            float u[32];
+            tmem_ld32(tmem_base + lane_off + sum_col + cc * 32, u);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = u[j] + v[j];
+          }
+          tmem_st32(tmem_base + lane_off + sum_col + cc * 32, v);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty + acc);
+        if (++acc == NACC) { acc = 0; aphase ^= 1; }
+      }
+      if (lane == 0) mbar_arrive(sfull + sb);
+      if (++sb == NSUM) { sb = 0; sphase ^= 1; }
     }
   } else {
-    // ============================ epilogue (warps 2..5) ===================
+    // ============================ epilogue (warps 6..9) ===================
     // Each warp owns TMEM lanes [32q, 32q+32) = 32 tile rows.  Per 32-column chunk:
-    // tcgen05.ld (thread = row), transpose through a private 32x33 smem buffer,
-    // then lane = column: every global load/store is one coalesced 128-byte row segment.
+    // tcgen05.ld of the tile sum (thread = row), transpose through a private 32x33 smem
+    // buffer, then lane = column: every global load/store is one coalesced 128-byte row
+    // segment.
     const int quarter = warp & 3;  // TMEM lane quarter accessible to this warp
-    float* tb = epi_buf + (warp - 2) * (32 * 33);
-    int acc = 0;
-    uint32_t aphase = 0;
+    float* tb = epi_buf + (warp - 6) * (32 * 33);
+    int sb = 0;
+    uint32_t sphase = 0;
     const SeriesParams* P = a.P;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
       int tm, tn;
       coords(t, tm, tn);
-      mbar_wait(tfull + acc, aphase);
+      mbar_wait(sfull + sb, sphase);
       tc_fence_after();
+      const uint32_t sum_col = (uint32_t)((NACC + sb) * BN);
       const int row0 = tm * BM + quarter * 32;
       float s2 = 0.f, h0 = 0.f, c1 = 0.f, ck = 0.f;
       if (a.mode != GRAM) {
@@ -331,10 +405,12 @@ __global__ void __launch_bounds__(NTHR, 1)
       }
 #pragma unroll 1
       for (int cc = 0; cc < BN / 32; ++cc) {
-        float v[32];
-        tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + cc * 32), v);
+        {
+          float v[32];
+          tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + sum_col + cc * 32, v);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) tb[lane * 33 + j] = v[j];
+          for (int j = 0; j < 32; ++j) tb[lane * 33 + j] = v[j];
+        }
         __syncwarp();
         const int cbase = tn * BN + cc * 32;
         const int c = cbase + lane;
@@ -392,14 +468,14 @@ __global__ void __launch_bounds__(NTHR, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tempty + acc);
-      if (++acc == 2) { acc = 0; aphase ^= 1; }
+      if (lane == 0) mbar_arrive(sempty + sb);
+      if (++sb == NSUM) { sb = 0; sphase ^= 1; }
     }
   }
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(2 * BN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"((NACC + NSUM) * BN));
   }
 }
 
@@ -507,6 +583,8 @@ static cudaError_t tc_gemm_bn(int mode, int terms, int M, int N, int Kd, const f
     a.tile_list = sym_tile_list(a.tiles_m, &a.ntiles_list);
     if (!a.tile_list) return cudaErrorMemoryAllocation;
   }
+  a.chunk_kb = CHUNK_KB_DEFAULT;
+  if (const char* v = getenv("CPA_SVT_TC_CHUNK")) a.chunk_kb = atoi(v) > 0 ? atoi(v) : a.chunk_kb;
   if (const char* v = getenv("CPA_SVT_DBG_LBO")) a.dbg_lbo = atoi(v);
   if (const char* v = getenv("CPA_SVT_DBG_SBO")) a.dbg_sbo = atoi(v);
   if (terms == 3) {
@@ -522,18 +600,11 @@ static cudaError_t tc_gemm_bn(int mode, int terms, int M, int N, int Kd, const f
 // One tcgen05 GEMM with the fused epilogue.
 //   A: M x Kd, K-major (row stride lda), given as hi (and lo) fp32 copies
 //   B: b_mn ? Kd x N (N contiguous, row stride ldb) : N x Kd (K contiguous)
-// N tile: 256 columns for single-pass TF32 on wide problems (less TMA traffic
-// per flop), else 128 (3xTF32 needs the shared memory for 3 stages of 4 operands).
+// 128 x 128 tiles (BM = BN: the symmetric form needs square tiles).
 cudaError_t tc_gemm(int mode, int terms, int M, int N, int Kd, const float* Ah, const float* Al, int64_t lda,
                     const float* Bh, const float* Bl, int64_t ldb, bool b_mn, float* out_f, float* out_h,
                     float* out_l, int out_split, int64_t ld_out, const float* wp, const float* wpp, int64_t ld_w,
                     float* y, int64_t ld_y, const SeriesParams* P, int k, int num_sms, cudaStream_t st, int sym) {
-  int bn = 128;
-  if (const char* v = getenv("CPA_SVT_TC_BN")) bn = atoi(v) == 256 ? 256 : 128;
-  if (sym) bn = 128;
-  if (bn == 256)
-    return tc::tc_gemm_bn<256>(mode, terms, M, N, Kd, Ah, Al, lda, Bh, Bl, ldb, b_mn, out_f, out_h, out_l, out_split,
-                               ld_out, wp, wpp, ld_w, y, ld_y, P, k, num_sms, st, sym);
   return tc::tc_gemm_bn<128>(mode, terms, M, N, Kd, Ah, Al, lda, Bh, Bl, ldb, b_mn, out_f, out_h, out_l, out_split,
                              ld_out, wp, wpp, ld_w, y, ld_y, P, k, num_sms, st, sym);
 }

@@ -44,6 +44,20 @@ def test_config3_parity(env):
     assert np.max(np.abs(lam - lo) / lo) < 1e-5
 
 
+def test_config3_full_batch_sampled(env):
+    """BASELINE configs[2] at full size (65536 matrices): 256 sampled matrices (seed-fixed,
+    plus first and last) against the oracle, whole-sample Frobenius bar."""
+    cfg = W.CONFIGS["c3"]
+    Xb = W.gen_c3()
+    assert Xb.shape[0] == 65536
+    Y, lam = _run(env, Xb, cfg["kernel"], cfg["K"], T=cfg["T"])
+    rng = np.random.default_rng(0)
+    idx = sorted(set([0, Xb.shape[0] - 1] + list(rng.choice(Xb.shape[0], 254, replace=False))))
+    Yo, lo = O.cpa_shrink_batched(Xb[idx].astype(np.float64), O.Kernel(**cfg["kernel"]), cfg["K"], T=cfg["T"])
+    assert O.rel_fro(Y[idx], Yo) <= TOL32
+    assert np.max(np.abs(lam[idx] - lo) / lo) < 1e-5
+
+
 @pytest.mark.parametrize("shape", [(64, 48), (48, 64), (7, 33), (33, 7), (1, 1), (64, 64), (17, 17), (64, 1)])
 @pytest.mark.parametrize("kind,K", [("soft", 2), ("soft", 20), ("hard", 7), ("wsoft", 12)])
 def test_batched_shapes(env, shape, kind, K):

@@ -238,3 +238,30 @@ def test_symmetric_form_splits(env, s, K, split):
     assert O.rel_fro(Y, O.cpa_shrink(X, O.Kernel(**kern), K, T=120)) <= TOL64
     assert np.array_equal(Y, Y2)
     assert np.array_equal(Hx, Hx.T)
+
+
+def test_config5_full_size_sampled(env):
+    """BASELINE configs[4] at full size (16384 x 65536 fp64, rank-50 + 0.01 noise, soft
+    tau = 0.1 sigma_max_hat, K = 40, T = 300) in the launch configuration the config
+    measurement uses: the GPU's lambda_hat against the oracle's power iteration on the
+    numpy Gram, and 10 sampled columns (seed-fixed, plus first and last) against the
+    oracle's vector form at the oracle's own Lambda."""
+    torch, P, h = env
+    cfg = W.CONFIGS["c5"]
+    X = W.gen_c5()
+    Xd = torch.from_numpy(X).cuda()
+    Yd, info = h.apply(Xd, cfg["kernel"], cfg["K"], T=cfg["T"], info=True)
+    assert info["form"] == 2
+    m, n = X.shape
+    rng = np.random.default_rng(0)
+    cols = sorted(set([0, n - 1] + list(rng.choice(n, 8, replace=False))))
+    Ys = Yd[:, torch.tensor(cols, device=Yd.device)].cpu().numpy()
+    del Yd, Xd
+    torch.cuda.empty_cache()
+    G = O.gram(X.T)                       # X X^T: the left Gram, one library product
+    lam_hat = O.power_iteration(lambda v: G @ v, m, cfg["T"])[0]
+    assert abs(info["lambda_hat"] - lam_hat) <= 1e-12 * lam_hat
+    lam = 1.01 * lam_hat
+    c = O.kernel_coefficients(O.Kernel(**cfg["kernel"]), cfg["K"], lam, math.sqrt(lam_hat))
+    Yo = O.cpa_apply_vectors(lambda V: G @ V, X[:, cols], c, lam)
+    assert O.rel_fro(Ys, Yo) <= TOL64

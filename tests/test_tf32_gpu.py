@@ -99,3 +99,39 @@ def test_tf32_both_forms(env, shape, K):
         Y = h2.apply(torch.from_numpy(X.astype(np.float32)).cuda(), kern, K, T=100, math="3xtf32")
         h2.close()
         assert O.rel_fro(Y.cpu().numpy().astype(np.float64), ref) <= TOL32, form
+
+
+def test_config5_full_size_sampled_tf32(env):
+    """configs[4] fp32 variant at full size (16384 x 65536): 3xTF32 and TF32 on 10 sampled
+    columns (seed-fixed, plus first and last) against the oracle's vector form on the
+    fp64-promoted fp32 input, at the oracle's own Lambda (power iteration on the numpy
+    Gram); lambda_hat from the fp32 Gram agrees to ~1e-6."""
+    import math as m_
+    torch, P, h = env
+    cfg = W.CONFIGS["c5"]
+    X32 = W.gen_c5(dtype=np.float32)
+    Xd = torch.from_numpy(X32).cuda()
+    m, n = X32.shape
+    rng = np.random.default_rng(0)
+    cols = sorted(set([0, n - 1] + list(rng.choice(n, 8, replace=False))))
+    got = {}
+    for math in ("3xtf32", "tf32"):
+        Yd, info = h.apply(Xd, cfg["kernel"], cfg["K"], T=cfg["T"], math=math, info=True)
+        assert info["form"] == 2
+        got[math] = (Yd[:, torch.tensor(cols, device=Yd.device)].cpu().numpy().astype(np.float64), info)
+        del Yd
+    del Xd
+    torch.cuda.empty_cache()
+    X = X32.astype(np.float64)
+    G = O.gram(X.T)
+    lam_hat = O.power_iteration(lambda v: G @ v, m, cfg["T"])[0]
+    lam = 1.01 * lam_hat
+    c = O.kernel_coefficients(O.Kernel(**cfg["kernel"]), cfg["K"], lam, m_.sqrt(lam_hat))
+    Yo = O.cpa_apply_vectors(lambda V: G @ V, X[:, cols], c, lam)
+    for math, tol in (("3xtf32", TOL32), ("tf32", 3e-4)):
+        Ys, info = got[math]
+        print(math, "lambda rel err", info["lambda_hat"] / lam_hat - 1, "Y rel err", O.rel_fro(Ys, Yo))
+    for math, tol in (("3xtf32", TOL32), ("tf32", 3e-4)):
+        Ys, info = got[math]
+        assert abs(info["lambda_hat"] - lam_hat) <= 1e-5 * lam_hat, math
+        assert O.rel_fro(Ys, Yo) <= tol, (math, O.rel_fro(Ys, Yo))
