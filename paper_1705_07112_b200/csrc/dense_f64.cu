@@ -610,6 +610,10 @@ __global__ void __launch_bounds__(NTHREADS) k_dmma_gemm(GemmArgs a) {
     while (r * (r + 1) / 2 > b) --r;
     tm = r;
     tn = b - r * (r + 1) / 2;
+  } else if (MODE == EPI_STORE) {
+    const int tiles_n = (int)((a.N + BN - 1) / BN);
+    tm = blockIdx.x / tiles_n;
+    tn = blockIdx.x % tiles_n;
   } else {
     tm = blockIdx.x;
     tn = blockIdx.y;
@@ -620,7 +624,7 @@ __global__ void __launch_bounds__(NTHREADS) k_dmma_gemm(GemmArgs a) {
   const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
 
   double acc[4][4][2];
-  if (MODE == EPI_GRAM && gridDim.y > 1) {
+  if ((MODE == EPI_GRAM || MODE == EPI_STORE) && gridDim.y > 1) {
     // split-K over gridDim.y units per tile (the triangle alone has too few tiles to give
     // every SMSP more than one warp): every unit publishes its partial; the last to arrive
     // sums them in the fixed order q = 0..S-1 (deterministic) and stores the tile.
@@ -702,6 +706,22 @@ __global__ void __launch_bounds__(NTHREADS) k_dmma_gemm(GemmArgs a) {
                 a.P, a.k);
 }
 
+// k-splits (1..8, >= 4 k-slabs each) whose units fill whole waves of the resident
+// slots best; ties (within 3%) go to fewer splits.  Only when the tiles alone
+// leave slots idle (fewer than 3 waves).
+static int best_split(int64_t tiles, int64_t nk, int64_t slots) {
+  if (tiles >= 3 * slots) return 1;
+  int best = 1;
+  double best_eff = 0.0;
+  for (int S = 1; S <= 8; ++S) {
+    if (S > 1 && nk / S < 4) break;
+    const int64_t u = tiles * S, waves = (u + slots - 1) / slots;
+    const double eff = (double)u / (double)(waves * slots);
+    if (eff > best_eff + 0.03) { best_eff = eff; best = S; }
+  }
+  return best;
+}
+
 template <bool A_KC, bool B_KC, int MODE>
 static cudaError_t launch(const GemmArgs& a, cudaStream_t st) {
   using LA = OpLayout<A_KC, BM>;
@@ -712,14 +732,16 @@ static cudaError_t launch(const GemmArgs& a, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   const int64_t tm = (a.M + BM - 1) / BM, tn = (a.N + BN - 1) / BN;
   dim3 grid;
-  if (MODE == EPI_GRAM) {
-    const int64_t tiles = tm * (tm + 1) / 2, nk = (a.Kd + BKS - 1) / BKS;
+  if (MODE == EPI_GRAM || MODE == EPI_STORE) {
+    const int64_t tiles = MODE == EPI_GRAM ? tm * (tm + 1) / 2 : tm * tn, nk = (a.Kd + BKS - 1) / BKS;
     int split = 1;
-    if (a.partial && a.tcount) {  // split-K needs scratch
-      int dev = 0, sms = 148;
+    if (a.partial && a.tcount) {  // split-K needs scratch (sized by dense_split_partial_doubles)
+      int dev = 0, sms = 148, per_sm = 1;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      while (split < 8 && tiles * split < 3 * sms && nk / (2 * split) >= 4) split *= 2;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, NTHREADS, smem) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+      split = best_split(tiles, nk, (int64_t)sms * per_sm);
       if (split > 1) {
         cudaError_t ez = cudaMemsetAsync(a.tcount, 0, tiles * sizeof(int), st);
         if (ez != cudaSuccess) return ez;
@@ -786,11 +808,15 @@ cudaError_t dense_cheb_launch(bool left, bool init, int64_t m, int64_t n, const 
   return init ? launch<true, false, EPI_INIT>(a, st) : launch<true, false, EPI_STEP>(a, st);
 }
 
+size_t dense_store_partial_doubles(int64_t M, int64_t N);
+
 // C (M x N, ldc) = A (M x Kd, row-major, k contiguous) * B (Kd x N, row-major, n contiguous).
 // Used for Alg. 1 line 12 in the s x s polynomial form: Y = H_hat X (left) or X H_hat (right).
 cudaError_t dense_gemm_store(int64_t M, int64_t N, int64_t Kd, const double* A, int64_t lda, const double* B,
-                             int64_t ldb, double* C, int64_t ldc, cudaStream_t st) {
+                             int64_t ldb, double* C, int64_t ldc, cudaStream_t st, double* partial, int* tcount) {
   GemmArgs a{};
+  a.partial = dense_store_partial_doubles(M, N) ? partial : nullptr;
+  a.tcount = tcount;
   a.M = M; a.N = N; a.Kd = Kd;
   a.A = A; a.lda = lda; a.B = B; a.ldb = ldb;
   a.vec_a = aligned16(A, lda); a.vec_b = aligned16(B, ldb);
@@ -828,6 +854,13 @@ size_t dense_flow_sync_ints(int64_t m, int64_t n, int K) {
 size_t dense_gram_partial_doubles(int64_t s) {
   const int64_t t = (s + BM - 1) / BM;
   return (size_t)(t * (t + 1) / 2) * 8 * BM * BN;
+}
+
+// split-K scratch of dense_gemm_store (M x N output): used only when the tiles
+// leave slots idle (< 3 waves of 3 x 148), so bounded by 1332 tiles x 8 splits.
+size_t dense_store_partial_doubles(int64_t M, int64_t N) {
+  const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  return tiles < 1332 ? (size_t)tiles * 8 * BM * BN : 0;
 }
 
 size_t dense_flow_partial_doubles(int64_t m, int64_t n, int num_sms) {
