@@ -27,7 +27,7 @@ __all__ = [
     "series_eval", "gram", "power_iteration", "cpa_shrink", "cpa_apply_vectors",
     "cpa_shrink_columns", "cpa_shrink_rows", "cpa_shrink_batched",
     "sparse_power_iteration", "cpa_shrink_sparse_rows", "jacobi_svd",
-    "exact_shrink", "svd_characterization", "rel_fro",
+    "exact_shrink", "svd_characterization", "rel_fro", "haar1_matrix", "cpa_shrink_transform",
     "DEFAULT_SAFETY", "DEGENERATE_LAMBDA",
 ]
 
@@ -258,6 +258,79 @@ def _alg1(B, kernel, K, T, safety, lam_override, coeffs):
         Psi_km2, Psi_km1 = Psi_km1, Psi_k
     # line 12: G_hat(B) <- B T^T H T with T = I
     return B @ H, info
+
+
+# ---------------------------------------------------------------------------
+# Alg. 1 with a sparsifying transform T (NEXT-2 / reading R22)
+# ---------------------------------------------------------------------------
+
+def haar1_matrix(n: int) -> np.ndarray:
+    """One-level Haar DWT as an n x n orthogonal matrix T (forward transform y -> T y,
+    PAPER.md:321-322, 628-630).  Rows 0..ceil(n/2)-1 are the low-pass (scaling)
+    coefficients (y_{2i} + y_{2i+1})/sqrt 2 -- for odd n the last sample is its own
+    low-pass coefficient -- and the remaining floor(n/2) rows the high-pass (wavelet)
+    coefficients (y_{2i} - y_{2i+1})/sqrt 2."""
+    nh = n // 2
+    nl = n - nh
+    T = np.zeros((n, n))
+    r = 1.0 / math.sqrt(2.0)
+    for i in range(nh):
+        T[i, 2 * i] = r
+        T[i, 2 * i + 1] = r
+        T[nl + i, 2 * i] = r
+        T[nl + i, 2 * i + 1] = -r
+    if nl > nh:
+        T[nl - 1, n - 1] = 1.0
+    return T
+
+
+def cpa_shrink_transform(X, kernel: Kernel, K: int, T: int = 30, safety: float = DEFAULT_SAFETY,
+                         lam: float | None = None, return_info: bool = False):
+    """Algorithm 1 with T = the one-level Haar DWT of the Gram index
+    and the high-frequency components of Phi set to 0 (reading R22):
+
+      line 1  Phi  <- T B^T B T^T
+      line 2  Phi_ <- Phi with its high-frequency rows and columns zeroed
+      lines 3-11 as in cpa_shrink, on Phi_ (s x s; Psi_0 = Id over the whole index space)
+      line 12 G_hat(B) <- B T^T H_hat(Phi_) T
+
+    Orientation as cpa_shrink: a wide X (m <= n) runs on B = X^T (Gram X X^T)."""
+    X = np.asarray(X, dtype=np.float64)
+    m, n = X.shape
+    B = X.T if m <= n else X
+    s = B.shape[1]
+    Tm = haar1_matrix(s)
+    nl = s - s // 2
+    # line 1
+    Phi = Tm @ gram(B) @ Tm.T
+    # line 2: high-frequency components set to 0
+    Phi_ = Phi.copy()
+    Phi_[nl:, :] = 0.0
+    Phi_[:, nl:] = 0.0
+    # line 3
+    lam_, lam_hat, sig_hat = _lambda_and_sigma(
+        lambda: power_iteration(lambda v: Phi_ @ v, s, T)[0], lam, safety)
+    info = {"lambda_hat": lam_hat, "lambda_max": lam_, "sigma_max_hat": sig_hat, "degenerate": False}
+    if lam_hat <= DEGENERATE_LAMBDA:
+        info["degenerate"] = True
+        return (np.zeros_like(X), info) if return_info else np.zeros_like(X)
+    # line 4
+    c = kernel_coefficients(kernel, K, lam_, sig_hat)
+    info["tau"] = resolve_tau(kernel, sig_hat)
+    info["coeffs"] = c
+    # lines 5-11
+    Id = np.eye(s)
+    Bh = (2.0 / lam_) * Phi_ - Id
+    Psi_km2, Psi_km1 = Id, Bh
+    H = 0.5 * c[0] * Psi_km2 + c[1] * Psi_km1
+    for k in range(2, K):
+        Psi_k = 2.0 * (Bh @ Psi_km1) - Psi_km2
+        H = H + c[k] * Psi_k
+        Psi_km2, Psi_km1 = Psi_km1, Psi_k
+    # line 12
+    Y = B @ Tm.T @ H @ Tm
+    Y = Y.T if m <= n else Y
+    return (Y, info) if return_info else Y
 
 
 def cpa_apply_vectors(apply_phi, V, c, lam: float):

@@ -333,3 +333,69 @@ def test_generators_deterministic():
     assert r[-1] == 250 and len(set(zip(np.repeat(np.arange(50), np.diff(r)), c))) == 250
     Xb = W.gen_c3(batch=4)
     assert Xb.dtype == np.float32 and Xb.shape == (4, 64, 64)
+
+
+# ---- NEXT-2: Alg. 1 with the one-level Haar DWT (reading R22)
+
+@pytest.mark.parametrize("n", [1, 2, 7, 8, 33])
+def test_haar1_orthogonal(n):
+    T = O.haar1_matrix(n)
+    assert np.allclose(T @ T.T, np.eye(n), atol=1e-15) and np.allclose(T.T @ T, np.eye(n), atol=1e-15)
+    # low-pass rows average adjacent pairs, high-pass rows difference them
+    y = np.arange(n, dtype=float)
+    t = T @ y
+    nh = n // 2
+    assert np.allclose(t[:nh], (y[0:2 * nh:2] + y[1:2 * nh:2]) / np.sqrt(2))
+    assert np.allclose(t[n - nh:], (y[0:2 * nh:2] - y[1:2 * nh:2]) / np.sqrt(2))
+
+
+@pytest.mark.parametrize("shape", [(20, 40), (40, 26), (31, 60)])
+def test_transform_lowpass_signal_equals_identity_transform(shape):
+    """A signal with no high-frequency content along the Gram index (pairwise equal rows /
+    columns) has Phi_ = Phi = T G T^T exactly, and T^T H(T G T^T) T = H(G) for orthogonal T:
+    the transform variant reduces to plain Alg. 1 (T = I)."""
+    m, n = shape
+    rng = np.random.default_rng(m * n)
+    left = m <= n
+    s = m if left else n
+    base = rng.standard_normal(((s + 1) // 2, n if left else m))
+    full = np.repeat(base, 2, axis=0)[:s]
+    X = full if left else full.T
+    kern = O.Kernel(kind="soft", tau=0.2, tau_relative=True)
+    # the power iterations start from 1/sqrt(s) in different bases (T^T 1 != 1), so fix
+    # Lambda to compare the series itself; lambda_hat then agrees to its convergence
+    lam = 1.01 * float(np.linalg.eigvalsh(X @ X.T if left else X.T @ X)[-1])
+    Yt = O.cpa_shrink_transform(X, kern, 12, lam=lam)
+    Yi = O.cpa_shrink(X, kern, 12, lam=lam)
+    assert O.rel_fro(Yt, Yi) <= 1e-12
+    _, it = O.cpa_shrink_transform(X, kern, 12, T=300, return_info=True)
+    assert abs(it["lambda_hat"] * 1.01 / lam - 1) <= 1e-9
+
+
+@pytest.mark.parametrize("shape", [(16, 30), (30, 17), (9, 9)])
+def test_transform_block_structure(shape):
+    """In the transform basis Phi_ = blockdiag(G_L, 0) with G_L the Gram of the low-pass
+    half A_L = T_L A, so H_hat(Phi_) = blockdiag(H_hat(G_L), h_hat(0) I): the result equals
+    T_L^T H_hat(G_L) A_L + h_hat(0) T_H^T A_H, with h_hat(0) = c_0/2 + sum_k c_k (-1)^k
+    (psi_k(-1) = (-1)^k, PAPER.md:158)."""
+    X = np.random.default_rng(5).standard_normal(shape)
+    m, n = shape
+    left = m <= n
+    A = X if left else X.T
+    s = A.shape[0]
+    Tm = O.haar1_matrix(s)
+    nl = s - s // 2
+    AL, AH = Tm[:nl] @ A, Tm[nl:] @ A
+    kern = O.Kernel(kind="soft", tau=0.3, tau_relative=True)
+    K = 9
+    Y, info = O.cpa_shrink_transform(X, kern, K, T=80, return_info=True)
+    c = info["coeffs"]
+    lam = info["lambda_max"]
+    # H_hat(G_L) A_L by the vector form at the same Lambda and coefficients
+    GL = AL @ AL.T
+    YL = O.cpa_apply_vectors(lambda V: GL @ V, AL, c, lam)
+    h0 = 0.5 * c[0] + sum(c[k] * (-1) ** k for k in range(1, K))
+    want = Tm[:nl].T @ YL + h0 * (Tm[nl:].T @ AH)
+    want = want if left else want.T
+    assert O.rel_fro(Y, want) <= 1e-12
+    assert abs(O.series_eval(c, lam, 0.0) - h0) <= 1e-12 * max(1.0, abs(h0))
