@@ -191,8 +191,13 @@ typedef enum {
                                (H_hat = sum c_k Psi_k(B_hat) formed on the s x s Gram, then one product
                                Y = H_hat X); fp64 computes only the lower-triangle
                                tiles of each symmetric Psi_k (s^2 (s+1) flops per step), 3 = the s x s
-                               form on full tiles (2 s^3 per step; cross-check).  Auto picks 2 when
-                               K > 2 for fp64; for fp32/TF32 the s x s form (full tiles) when s < L. */
+                               form on full tiles (2 s^3 per step; cross-check).  Auto picks 2 whenever
+                               K > 2 (fp64 and fp32/TF32; the TF32 s x s form is symmetric too). */,
+  CPA_SVT_OPT_TRANSFORM = 1 /* NEXT-2, Alg. 1 line 1-2 with a sparsifying transform (PAPER.md:320-352,
+                               628-630): 0 = T = I (default); 1 = one-level Haar DWT of the Gram index
+                               with the high-frequency components of Phi set to 0 -- Alg. 1 then runs
+                               on the low-pass half and line 12 applies B T^T H_hat(Phi_) T.  fp64
+                               dense, unsharded only (else CPA_SVT_E_UNSUPPORTED). */
 } cpa_svt_option;
 cpa_svt_status cpa_svt_set_option(cpa_svt_handle* h, cpa_svt_option opt, int64_t value);
 

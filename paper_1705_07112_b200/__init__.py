@@ -152,6 +152,11 @@ class Handle:
         symmetric lower-triangle tiles) | 'poly_full' (s x s form on full tiles, cross-check)."""
         self._check(lib.cpa_svt_set_option(self._h, 0, FORM[form]), "cpa_svt_set_option")
 
+    def set_transform(self, transform: str):
+        """cpa_svt_set_option(TRANSFORM): 'none' (T = I) | 'haar1' (one-level Haar DWT of the Gram
+        index, high-frequency components of Phi set to 0; NEXT-2)."""
+        self._check(lib.cpa_svt_set_option(self._h, 1, {"none": 0, "haar1": 1}[transform]), "cpa_svt_set_option")
+
     def profile(self, enable: bool = True):
         """cpa_svt_profile: reset and start (or stop) per-phase CUDA-event timing."""
         self._check(lib.cpa_svt_profile(self._h, int(enable)), "cpa_svt_profile")

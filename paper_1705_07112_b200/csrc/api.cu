@@ -30,6 +30,10 @@ cudaError_t dense_gemm_store(int64_t M, int64_t N, int64_t Kd, const double* A, 
                              int64_t ldb, double* C, int64_t ldc, cudaStream_t st, double* partial = nullptr,
                              int* tcount = nullptr);
 size_t dense_store_partial_doubles(int64_t M, int64_t N);
+cudaError_t dense_haar_split(const double* X, int64_t m, int64_t n, int64_t ldx, bool left, double* AL, double* AH,
+                             int num_sms, cudaStream_t st);
+cudaError_t dense_haar_combine(const double* YL, const double* AH, const SeriesParams* P, int64_t m, int64_t n,
+                               bool left, double* Y, int64_t ldy, int num_sms, cudaStream_t st);
 cudaError_t dense_eye(double* I, int64_t s, cudaStream_t st);
 size_t dense_sym_sync_ints(int64_t s, int K, int num_sms);
 size_t dense_sym_partial_doubles(int64_t s, int num_sms);
@@ -121,6 +125,9 @@ struct cpa_svt_handle {
   void* ws = nullptr;              // workspace
   size_t ws_bytes = 0;
   void* hx = nullptr;              // apply_host device staging
+  void* tws = nullptr;             // transform workspace (A_L, A_H, Y_L)
+  size_t tws_bytes = 0;
+  int transform = 0;               // CPA_SVT_OPT_TRANSFORM
   size_t hx_bytes = 0;
   std::string err;
   int64_t launches = 0;
@@ -309,6 +316,7 @@ cpa_svt_status cpa_svt_free(cpa_svt_handle* h) {
   cudaFree(h->d_c);
   cudaFree(h->ws);
   cudaFree(h->hx);
+  cudaFree(h->tws);
   for (auto& u : h->ev_used) {
     cudaEventDestroy(u.second.first);
     cudaEventDestroy(u.second.second);
@@ -320,6 +328,11 @@ cpa_svt_status cpa_svt_free(cpa_svt_handle* h) {
 
 cpa_svt_status cpa_svt_set_option(cpa_svt_handle* h, cpa_svt_option opt, int64_t value) {
   if (!h) return CPA_SVT_E_ARG;
+  if (opt == CPA_SVT_OPT_TRANSFORM) {
+    if (value < 0 || value > 1) return CPA_SVT_E_ARG;
+    h->transform = (int)value;
+    return CPA_SVT_OK;
+  }
   if (opt == CPA_SVT_OPT_FORM) {
     if (value < 0 || value > 3) return CPA_SVT_E_ARG;
     h->form = (int)value;
@@ -469,7 +482,52 @@ static int dense_form(const cpa_svt_handle* h, int64_t s, int64_t L_local, int K
 static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt_shard shard,
                                 int64_t long_global, const double* X, int64_t ldx, double* Y, int64_t ldy,
                                 const cpa_svt_kernel* k, int K, const double* c, cpa_svt_lambda* lam,
+                                cpa_svt_info* info);
+
+// NEXT-2 (reading R22): Alg. 1 with T = one-level Haar DWT of the Gram index and the
+// high-frequency components of Phi zeroed.  In the transform basis Phi_ = blockdiag(G_L, 0)
+// with G_L the Gram of the low-pass half A_L, so Alg. 1 runs on A_L unchanged and line 12
+// recombines Y = T_L^T (H_hat(G_L) A_L) + h_hat(0) T_H^T A_H.
+static cpa_svt_status apply_f64_haar(cpa_svt_handle* h, int64_t m, int64_t n, const double* X, int64_t ldx,
+                                     double* Y, int64_t ldy, const cpa_svt_kernel* k, int K, const double* c,
+                                     cpa_svt_lambda* lam, cpa_svt_info* info) {
+  const bool left = m <= n;
+  const int64_t s = left ? m : n, L = left ? n : m, nh = s / 2, nl = s - nh;
+  const size_t nL = ((size_t)nl * L + 31) / 32 * 32, nH = ((size_t)nh * L + 31) / 32 * 32;
+  cpa_svt_status st = grow(h, &h->tws, &h->tws_bytes, (2 * nL + nH) * sizeof(double) + 256);
+  if (st != CPA_SVT_OK) return st;
+  double* AL = (double*)h->tws;
+  double* YL = AL + nL;
+  double* AH = YL + nL;
+  {
+    Phase p(h, CPA_SVT_PH_GRAM);
+    CU(dense_haar_split(X, m, n, ldx, left, AL, AH, h->num_sms, h->stream));
+  }
+  const int64_t ml = left ? nl : m, nn = left ? n : nl;   // A_L in X's orientation
+  h->transform = 0;
+  st = apply_f64(h, ml, nn, CPA_SVT_SHARD_NONE, 0, AL, nn, YL, nn, k, K, c, lam, info);
+  h->transform = 1;
+  if (st != CPA_SVT_OK) return st;
+  {
+    Phase p(h, CPA_SVT_PH_FINAL);
+    CU(dense_haar_combine(YL, AH, h->P, m, n, left, Y, ldy, h->num_sms, h->stream));
+  }
+  h->launches += 2;
+  if (info) {
+    info->kernel_launches += 2;
+    info->side = left ? 0 : 1;
+  }
+  return CPA_SVT_OK;
+}
+
+static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt_shard shard,
+                                int64_t long_global, const double* X, int64_t ldx, double* Y, int64_t ldy,
+                                const cpa_svt_kernel* k, int K, const double* c, cpa_svt_lambda* lam,
                                 cpa_svt_info* info) {
+  if (h->transform == 1) {
+    if (shard != CPA_SVT_SHARD_NONE && h->world > 1) return CPA_SVT_E_UNSUPPORTED;
+    return apply_f64_haar(h, m, n, X, ldx, Y, ldy, k, K, c, lam, info);
+  }
   // side selection (reading R3): left iff global m <= global n
   bool left;
   if (shard == CPA_SVT_SHARD_COLS) {
@@ -763,6 +821,7 @@ cpa_svt_status cpa_svt_apply(cpa_svt_handle* h, cpa_svt_dtype dtype, cpa_svt_mat
   if (!k) k = &kz;
   if (dtype == CPA_SVT_F64 && math == CPA_SVT_MATH_NATIVE)
     return apply_f64(h, m, n, shard, long_global, (const double*)X, ldx, (double*)Y, ldy, k, K, c, lam, info);
+  if (h->transform) return CPA_SVT_E_UNSUPPORTED;  // the transform variant is fp64-only
   if (dtype == CPA_SVT_F32 && (math == CPA_SVT_MATH_TF32 || math == CPA_SVT_MATH_3XTF32))
     return apply_tf32(h, math == CPA_SVT_MATH_TF32 ? 1 : 3, m, n, shard, long_global, (const float*)X, ldx, (float*)Y,
                       ldy, k, K, c, lam, info);

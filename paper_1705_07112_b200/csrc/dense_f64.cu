@@ -968,4 +968,77 @@ cudaError_t dense_cheb_sym(int64_t s, const double* G, double* W0, double* W1, d
   return cudaLaunchCooperativeKernel((void*)k_cheb_sym, dim3((unsigned)grid), dim3(NTHREADS), args, smem, st);
 }
 
+// ---- NEXT-2: one-level Haar DWT of the Gram index (reading R22)
+// A = X (left, Gram index = rows) or X^T (right, Gram index = columns); s = Gram side,
+// nh = s / 2 pairs, nl = s - nh low-pass coefficients (odd s: the last sample is its own).
+//   split:   A_L[i] = (A[2i] + A[2i+1]) / sqrt 2,  A_H[i] = (A[2i] - A[2i+1]) / sqrt 2
+//   combine: Y[2i] = (Y_L[i] + h0 A_H[i]) / sqrt 2,  Y[2i+1] = (Y_L[i] - h0 A_H[i]) / sqrt 2,
+//            h0 = h_hat(0) = c_0/2 + sum_k c_k (-1)^k  (the series on the zeroed high band)
+// Layout: left: A_L nl x n, A_H nh x n (ld n); right: A_L m x nl (ld nl), A_H m x nh (ld nh).
+constexpr double kRsqrt2 = 0.70710678118654752440;
+
+__global__ void k_haar_split(const double* __restrict__ X, int64_t m, int64_t n, int64_t ldx, int left,
+                             double* __restrict__ AL, double* __restrict__ AH) {
+  const int64_t s = left ? m : n, nh = s / 2, nl = s - nh, L = left ? n : m;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nl * L; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i, l;  // i: low-pass index, l: position along the long side
+    if (left) { i = e / L; l = e % L; } else { l = e / nl; i = e % nl; }
+    auto x = [&](int64_t g) { return left ? X[g * ldx + l] : X[l * ldx + g]; };
+    double lo, hi = 0.0;
+    if (i < nh) {
+      const double a = x(2 * i), b = x(2 * i + 1);
+      lo = (a + b) * kRsqrt2;
+      hi = (a - b) * kRsqrt2;
+    } else {
+      lo = x(s - 1);
+    }
+    if (left) {
+      AL[i * L + l] = lo;
+      if (i < nh) AH[i * L + l] = hi;
+    } else {
+      AL[l * nl + i] = lo;
+      if (i < nh) AH[l * nh + i] = hi;
+    }
+  }
+}
+
+__global__ void k_haar_combine(const double* __restrict__ YL, const double* __restrict__ AH,
+                               const SeriesParams* __restrict__ P, int64_t m, int64_t n, int left,
+                               double* __restrict__ Y, int64_t ldy) {
+  __shared__ double s_h0;
+  if (threadIdx.x == 0) {
+    double h0 = 0.5 * P->c[0];
+    for (int k = 1; k < P->K; ++k) h0 += (k & 1) ? -P->c[k] : P->c[k];
+    s_h0 = h0;
+  }
+  __syncthreads();
+  const double h0 = s_h0;
+  const int64_t s = left ? m : n, nh = s / 2, nl = s - nh, L = left ? n : m;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < s * L; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t g, l;  // g: Gram index, l: long-side position
+    if (left) { g = e / L; l = e % L; } else { l = e / s; g = e % s; }
+    const int64_t i = g / 2;
+    double v;
+    if (i >= nh) {
+      v = left ? YL[(nl - 1) * L + l] : YL[l * nl + (nl - 1)];
+    } else {
+      const double lo = left ? YL[i * L + l] : YL[l * nl + i];
+      const double hi = h0 * (left ? AH[i * L + l] : AH[l * nh + i]);
+      v = ((g & 1) ? lo - hi : lo + hi) * kRsqrt2;
+    }
+    if (left) Y[g * ldy + l] = v; else Y[l * ldy + g] = v;
+  }
+}
+
+cudaError_t dense_haar_split(const double* X, int64_t m, int64_t n, int64_t ldx, bool left, double* AL, double* AH,
+                             int num_sms, cudaStream_t st) {
+  k_haar_split<<<num_sms * 8, 256, 0, st>>>(X, m, n, ldx, left ? 1 : 0, AL, AH);
+  return cudaGetLastError();
+}
+cudaError_t dense_haar_combine(const double* YL, const double* AH, const SeriesParams* P, int64_t m, int64_t n,
+                               bool left, double* Y, int64_t ldy, int num_sms, cudaStream_t st) {
+  k_haar_combine<<<num_sms * 8, 256, 0, st>>>(YL, AH, P, m, n, left ? 1 : 0, Y, ldy);
+  return cudaGetLastError();
+}
+
 }  // namespace cpa

@@ -142,3 +142,20 @@ def block_diag_D(N: int, nblocks: int, ncopies: int = 1) -> np.ndarray:
 def random_dense(m: int, n: int, seed: int = 0, dtype=np.float64) -> np.ndarray:
     """Plain N(0,1) matrix (odd-shape parity cases)."""
     return np.random.default_rng(seed).standard_normal((m, n)).astype(dtype)
+
+
+def gen_pinpaint(seed: int = 0, m: int = 2560, n: int = 1920) -> np.ndarray:
+    """Context shape (not a BASELINE config, SURVEY 8d 'p-inpaint'): a stand-in for one
+    2560 x 1920 colour channel of the paper's texture images, values in
+    [0, 1]: three separable 2-D cosines with random frequencies and phases (DCT-sparse and
+    low rank), min-max scaled, plus N(0, 0.02^2).  Seeded; no arithmetic of the method."""
+    rng = np.random.default_rng(seed)
+    i = np.arange(m)[:, None]
+    j = np.arange(n)[None, :]
+    X = np.zeros((m, n))
+    for _ in range(3):
+        fi, fj = rng.uniform(0.002, 0.05, 2)
+        pi, pj = rng.uniform(0, 2 * np.pi, 2)
+        X += rng.uniform(0.5, 1.0) * np.cos(2 * np.pi * fi * i + pi) * np.cos(2 * np.pi * fj * j + pj)
+    X = (X - X.min()) / (X.max() - X.min())
+    return X + 0.02 * rng.standard_normal((m, n))
