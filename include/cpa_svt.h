@@ -197,7 +197,10 @@ typedef enum {
                                628-630): 0 = T = I (default); 1 = one-level Haar DWT of the Gram index
                                with the high-frequency components of Phi set to 0 -- Alg. 1 then runs
                                on the low-pass half and line 12 applies B T^T H_hat(Phi_) T.  fp64
-                               dense, unsharded only (else CPA_SVT_E_UNSUPPORTED). */
+                               dense, unsharded only (else CPA_SVT_E_UNSUPPORTED). */,
+  CPA_SVT_OPT_BATCHED = 2   /* engine of cpa_svt_apply_batched: 0 = auto (tcgen05), 1 = fp32 FFMA (exact
+                               fp32 products, apply-to-X form), 2 = tcgen05 3xTF32 (s x s form,
+                               M = N = 64 MMAs, TMEM accumulators). */
 } cpa_svt_option;
 cpa_svt_status cpa_svt_set_option(cpa_svt_handle* h, cpa_svt_option opt, int64_t value);
 

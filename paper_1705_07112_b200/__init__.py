@@ -152,6 +152,10 @@ class Handle:
         symmetric lower-triangle tiles) | 'poly_full' (s x s form on full tiles, cross-check)."""
         self._check(lib.cpa_svt_set_option(self._h, 0, FORM[form]), "cpa_svt_set_option")
 
+    def set_batched_engine(self, engine: str):
+        """cpa_svt_set_option(BATCHED): 'auto' | 'ffma' (fp32 FFMA) | 'tc' (tcgen05 3xTF32)."""
+        self._check(lib.cpa_svt_set_option(self._h, 2, {"auto": 0, "ffma": 1, "tc": 2}[engine]), "cpa_svt_set_option")
+
     def set_transform(self, transform: str):
         """cpa_svt_set_option(TRANSFORM): 'none' (T = I) | 'haar1' (one-level Haar DWT of the Gram
         index, high-frequency components of Phi set to 0; NEXT-2)."""

@@ -75,6 +75,9 @@ cudaError_t tf32_eye(float* I, int64_t s, int64_t ld, int num_sms, cudaStream_t 
 cudaError_t launch_batched_f32(int64_t batch, int m, int n, const float* X, float* Y, const cpa_svt_kernel& k,
                                int K, int T, double safety, double lam_override, float* lambda_out,
                                int num_sms, cudaStream_t st, int* launches, double* costab);
+cudaError_t launch_batched_tc(int64_t batch, int m, int n, const float* X, float* Y, const cpa_svt_kernel& k,
+                               int K, int T, double safety, double lam_override, float* lambda_out,
+                               int num_sms, cudaStream_t st, int* launches, double* costab);
 // sparse_f64.cu
 cudaError_t sparse_apply(int64_t m, int64_t n, int64_t nnz, const int64_t* row_ptr, const int32_t* col,
                          const double* val, int64_t row_begin, int64_t row_end, double* Y, int64_t ldy,
@@ -128,6 +131,7 @@ struct cpa_svt_handle {
   void* tws = nullptr;             // transform workspace (A_L, A_H, Y_L)
   size_t tws_bytes = 0;
   int transform = 0;               // CPA_SVT_OPT_TRANSFORM
+  int batched_engine = 0;          // CPA_SVT_OPT_BATCHED: 0 auto (tensor cores), 1 FFMA, 2 tcgen05
   size_t hx_bytes = 0;
   std::string err;
   int64_t launches = 0;
@@ -328,6 +332,11 @@ cpa_svt_status cpa_svt_free(cpa_svt_handle* h) {
 
 cpa_svt_status cpa_svt_set_option(cpa_svt_handle* h, cpa_svt_option opt, int64_t value) {
   if (!h) return CPA_SVT_E_ARG;
+  if (opt == CPA_SVT_OPT_BATCHED) {
+    if (value < 0 || value > 2) return CPA_SVT_E_ARG;
+    h->batched_engine = (int)value;
+    return CPA_SVT_OK;
+  }
   if (opt == CPA_SVT_OPT_TRANSFORM) {
     if (value < 0 || value > 1) return CPA_SVT_E_ARG;
     h->transform = (int)value;
@@ -887,8 +896,12 @@ cpa_svt_status cpa_svt_apply_batched(cpa_svt_handle* h, int64_t batch, int m, in
   int launches = 0;
   {
     Phase p(h, CPA_SVT_PH_BATCHED);
-    CU(launch_batched_f32(batch, m, n, X, Y, *k, K, lam->power_iters, lam->safety, lam->lambda_max, lambda_out,
-                          h->num_sms, h->stream, &launches, (double*)h->ws));
+    if (h->batched_engine == 1)
+      CU(launch_batched_f32(batch, m, n, X, Y, *k, K, lam->power_iters, lam->safety, lam->lambda_max, lambda_out,
+                            h->num_sms, h->stream, &launches, (double*)h->ws));
+    else
+      CU(launch_batched_tc(batch, m, n, X, Y, *k, K, lam->power_iters, lam->safety, lam->lambda_max, lambda_out,
+                           h->num_sms, h->stream, &launches, (double*)h->ws));
   }
   h->launches += launches;
   return CPA_SVT_OK;

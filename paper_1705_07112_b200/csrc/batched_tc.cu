@@ -1,0 +1,485 @@
+// Batched fp32 path on the 5th-generation tensor cores (BASELINE configs[2]: 65536
+// independent patch-group matrices, m, n <= 64): the whole of Alg. 1 (PAPER.md:354-373,
+// T = I, eps = 0) per matrix inside one persistent CTA, every matrix product a
+// tcgen05.mma (cta_group::1, kind::tf32, M = N = 64) in 3xTF32 (hi/lo operand split,
+// round-to-nearest: acc = hi hi + hi lo + lo hi), accumulator in TMEM.
+//
+//   A = X (m <= n) or X^T, zero-padded to 64 x 64;  s = Gram side
+//   line 1:    G = A A^T                          (tcgen05; both operands = rows of A)
+//   line 3:    lambda_hat: T power steps on G      (fp32 CUDA cores, G rows in registers)
+//   line 4:    c_k (fp64, K-node rule)
+//   line 5-7:  Psi_1 = (2/L) G - I,  H = c_0/2 I + c_1 Psi_1
+//   line 8-11: Psi_k = (4/L) G Psi_{k-1} - 2 Psi_{k-1} - Psi_{k-2},  H += c_k Psi_k   (tcgen05)
+//   line 12:   Y = H A                             (tcgen05; B operand = rows of A^T)
+//
+// A step multiplies from the right, D = Psi_{k-1} G^T (A operand = rows of Psi_{k-1}, exactly
+// as the epilogue thread that owns the row writes them; B operand = rows of the fixed G):
+// G^T = G up to the Gram's rounding, a constant perturbation, and Psi_{k-1} G = G Psi_{k-1}
+// (polynomials in G commute).  The other association, D = G Psi_{k-1}^T with the rows of
+// Psi as B operand, assumes Psi symmetric: its antisymmetric rounding error then follows a
+// recurrence with multiplier -2 - (4/L) sqrt(l_a l_b), outside [-2, 2] -- measured 1e-7 at
+// K = 8 growing to 1e-4 at K = 20.
+//
+// Operands live in shared memory in the canonical K-major SWIZZLE_128B layout (128-byte
+// rows of 32 fp32, 8-row atoms, 16-byte chunk c of row r at c ^ (r & 7)), two 8 KB
+// k-blocks per 64 x 64 operand; descriptors as in tc_tf32.cu.  TMEM layout for M = 64
+// (probed, tools/probes/tc_m64_probe.cu): row r of D lives in lane 32 (r / 16) + r % 16,
+// column j in column j -- so lanes 0..15 of each warp own the 64 rows (16 per warp).
+// TMEM columns [0, 64): D.  The epilogue reads D with tcgen05.ld.16x256b (all 32 threads of a
+// warp: 2 rows x 16 columns each); Psi_{k-1}, Psi_{k-2} and H stay in registers in that layout.
+#include <cstdio>
+#include <cstdlib>
+
+#include "common.cuh"
+
+namespace cpa {
+namespace btc {
+
+constexpr int NT = 128;                 // threads per CTA (4 warps, 16 D rows each)
+constexpr int OPB = 64 * 64 * 4;        // bytes of one 64 x 64 fp32 operand (two 8 KB k-blocks)
+
+__device__ __forceinline__ uint32_t sw(int r, int k) {  // byte offset of (r, k) in a K-major SW128 operand
+  return (uint32_t)((k >> 5) * 8192 + r * 128 + ((((k & 31) >> 2) ^ (r & 7)) << 4) + (k & 3) * 4);
+}
+__device__ __forceinline__ uint64_t desc(uint32_t addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)(16 >> 4) << 16;        // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;      // SBO: 8 rows x 128 B
+  d |= (uint64_t)1 << 46;                // version 1
+  d |= (uint64_t)2 << 61;                // SWIZZLE_128B
+  return d;
+}
+constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(64 >> 3) << 17) | ((uint32_t)(64 >> 4) << 24);
+
+__device__ __forceinline__ float rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+// write fp32 x as TF32 hi / lo at (r, k) of the operand pair at (hi, hi + OPB)
+__device__ __forceinline__ void put(uint8_t* hi, int r, int k, float x) {
+  const float h = rna(x);
+  const uint32_t o = sw(r, k);
+  *reinterpret_cast<float*>(hi + o) = h;
+  *reinterpret_cast<float*>(hi + OPB + o) = rna(x - h);
+}
+// 4 consecutive k (one 16-byte chunk) of row r
+__device__ __forceinline__ void put4(uint8_t* hi, int r, int k, float x0, float x1, float x2, float x3) {
+  const uint32_t o = sw(r, k);
+  const float h0 = rna(x0), h1 = rna(x1), h2 = rna(x2), h3 = rna(x3);
+  *reinterpret_cast<float4*>(hi + o) = make_float4(h0, h1, h2, h3);
+  *reinterpret_cast<float4*>(hi + OPB + o) = make_float4(rna(x0 - h0), rna(x1 - h1), rna(x2 - h2), rna(x3 - h3));
+}
+
+// D = Aop * Bop^T over K = 64 in 3xTF32 (24 MMAs), issued by one thread; completion on bar.
+__device__ __forceinline__ void mma64(uint32_t tmem_d, const uint8_t* a_hi, const uint8_t* b_hi, uint64_t* bar) {
+  const uint32_t ah = smem_u32(a_hi), al = ah + OPB, bh = smem_u32(b_hi), bl = bh + OPB;
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) {
+    const uint32_t off = (kk >> 2) * 8192 + (kk & 3) * 32;
+    const uint64_t dah = desc(ah + off), dal = desc(al + off), dbh = desc(bh + off), dbl = desc(bl + off);
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %5, %3, 1;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %6, %2, %3, 1;\n}\n" ::"r"(tmem_d),
+        "l"(dah), "l"(dbh), "r"(IDESC), "r"(kk > 0 ? 1u : 0u), "l"(dbl), "l"(dal)
+        : "memory");
+  }
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra WAIT_%=;\n}\n" ::"r"(
+          smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void st32(uint32_t taddr, const float (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};\n" ::"r"(taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+      "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+      "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
+      "r"(__float_as_uint(v[15])), "r"(__float_as_uint(v[16])), "r"(__float_as_uint(v[17])),
+      "r"(__float_as_uint(v[18])), "r"(__float_as_uint(v[19])), "r"(__float_as_uint(v[20])),
+      "r"(__float_as_uint(v[21])), "r"(__float_as_uint(v[22])), "r"(__float_as_uint(v[23])),
+      "r"(__float_as_uint(v[24])), "r"(__float_as_uint(v[25])), "r"(__float_as_uint(v[26])),
+      "r"(__float_as_uint(v[27])), "r"(__float_as_uint(v[28])), "r"(__float_as_uint(v[29])),
+      "r"(__float_as_uint(v[30])), "r"(__float_as_uint(v[31]))
+      : "memory");
+}
+// all generic-proxy smem writes and TMEM accesses of the CTA done before the next MMA issue
+__device__ __forceinline__ void sync_for_mma() {
+  asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+}
+
+struct Args {
+  int64_t batch;
+  int m, n;
+  const float* X;
+  float* Y;
+  cpa_svt_kernel kern;
+  int K, T;
+  double safety, lam_override;
+  float* lambda_out;
+  const double* costab;   // cos(k theta_l), K x K
+};
+
+// smem: [A (hi, lo) -> Psi / H operand] [G (hi, lo)] [A^T (hi, lo)]  (3 x 32 KB, 1 KB aligned)
+constexpr int SMEM = 3 * 2 * OPB + 1024;
+
+// tcgen05.ld.16x256b.x8: the 16 rows x 64 columns of D in this warp's lane quarter, spread
+// over all 32 threads (probed, tools/probes/tc_m64_probe.cu): thread t holds rows
+// r0 = t/4 and r1 = t/4 + 8 (warp-local), columns 8c + 2(t%4) + {0, 1}, c = 0..7, as
+// v[4c + 0] = (r0, 8c+2q), v[4c + 1] = (r0, 8c+2q+1), v[4c + 2] = (r1, 8c+2q), v[4c + 3] = (r1, 8c+2q+1).
+__device__ __forceinline__ void ld_frag(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x256b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+// write a fragment (layout of ld_frag) as TF32 hi / lo operand rows: element (row, col) at sw(row, col)
+__device__ __forceinline__ void put_frag(uint8_t* hi, int row0, int q, const float (&v)[32]) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = row0 + 8 * h, k = 8 * c + 2 * q;
+      const float x0 = v[4 * c + 2 * h], x1 = v[4 * c + 2 * h + 1];
+      const float h0 = rna(x0), h1 = rna(x1);
+      const uint32_t o = sw(r, k);
+      *reinterpret_cast<float2*>(hi + o) = make_float2(h0, h1);
+      *reinterpret_cast<float2*>(hi + OPB + o) = make_float2(rna(x0 - h0), rna(x1 - h1));
+    }
+}
+
+__global__ void __launch_bounds__(NT, 1) k_batched_tc(Args a) {
+  extern __shared__ uint8_t raw[];
+  uint8_t* base = (uint8_t*)(((uintptr_t)raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sP = base;                 // A, then Psi_{k-1}, then H (A operand)
+  uint8_t* sG = base + 2 * OPB;       // G (B operand of the steps)
+  uint8_t* sAT = base + 4 * OPB;      // A^T (B operand of line 12)
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  __shared__ float sV[64];
+  __shared__ float sRed[4];
+  __shared__ double sHn[CPA_SVT_KMAX];
+  __shared__ float sC[CPA_SVT_KMAX];
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int q = lane & 3;
+  const int row0 = warp * 16 + (lane >> 2), row1 = row0 + 8;    // this thread's two D rows
+  const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+  const bool left = a.m <= a.n;
+  const int s = left ? a.m : a.n, L = left ? a.n : a.m;
+  const int K = a.K;
+  const int64_t mn = (int64_t)a.m * a.n;
+  auto colof = [&](int e) { return 8 * (e >> 2) + 2 * q + (e & 1); };
+  // 64 x 64 matrices at 16-byte aligned addresses take the vector load path (A = X)
+  const bool full64 = a.m == 64 && a.n == 64 && ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0);
+  auto rowof = [&](int e) { return (e & 2) ? row1 : row0; };
+
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;\n" ::"r"(smem_u32(&tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tD = tslot;
+  uint32_t phase = 0;
+
+#ifdef CPA_BTC_TRACE
+  long long tr[8] = {};
+#define BTC_STAMP(i) tr[i] = clock64()
+#else
+#define BTC_STAMP(i)
+#endif
+  for (int64_t b = blockIdx.x; b < a.batch; b += gridDim.x) {
+    const float* X = a.X + b * mn;
+    BTC_STAMP(0);
+    // ---- load A (s x L, zero-padded to 64 x 64) as operand rows (sP) and A^T rows (sAT);
+    //      all of the thread's global loads in flight before the first conversion
+    {
+      float4 v[8];
+      if (full64) {
+#pragma unroll
+        for (int it = 0; it < 8; ++it) v[it] = __ldg(reinterpret_cast<const float4*>(X) + it * NT + tid);
+      } else {
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          const int e = it * NT + tid, i = e >> 4, j = (e & 15) * 4;   // A(i, j..j+3)
+          float t4[4];
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq) {
+            const int jj = j + qq;
+            t4[qq] = (i < s && jj < L) ? __ldg(left ? X + (int64_t)i * a.n + jj : X + (int64_t)jj * a.n + i) : 0.f;
+          }
+          v[it] = make_float4(t4[0], t4[1], t4[2], t4[3]);
+        }
+      }
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        const int e = it * NT + tid, i = e >> 4, j = (e & 15) * 4;
+        put4(sP, i, j, v[it].x, v[it].y, v[it].z, v[it].w);
+        put(sAT, j, i, v[it].x);
+        put(sAT, j + 1, i, v[it].y);
+        put(sAT, j + 2, i, v[it].z);
+        put(sAT, j + 3, i, v[it].w);
+      }
+    }
+    sync_for_mma();
+    BTC_STAMP(1);
+    // ---- line 1: G = A A^T
+    if (tid == 0) btc::mma64(tD, sP, sP, &bar);
+    mbar_wait(&bar, phase);
+    phase ^= 1;
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    float g[32];
+    ld_frag(tD + lane_off, g);
+    // ---- line 3: Lambda_max by T power steps (fp32, fixed order).  Repeated squaring (as the
+    //      dense path, reading R6): v_{T-1} ~ G^{T-1} v_0 through q = (T-1)/4 products by
+    //      c^4 G^4 (c = 2^-ilogb(max G_ii), exact) then T - 4q by G; two extra tcgen05 products
+    //      instead of 3q power steps.
+    double lam_hat;
+    if (a.lam_override > 0.0) {
+      lam_hat = a.lam_override / a.safety;
+    } else {
+      const int qsq = a.T >= 8 ? (a.T - 1) / 4 : 0;
+      float g4[32];
+      if (qsq > 0) {
+        float dmax = 0.f;
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+          if (rowof(e) == colof(e)) dmax = fmaxf(dmax, g[e]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+        if (lane == 0) sRed[warp] = dmax;
+        __syncthreads();
+        dmax = fmaxf(fmaxf(sRed[0], sRed[1]), fmaxf(sRed[2], sRed[3]));
+        const float cs = (dmax > 0.f && isfinite(dmax)) ? ldexpf(1.f, -ilogbf(dmax)) : 1.f;
+#pragma unroll
+        for (int e = 0; e < 32; ++e) g4[e] = cs * g[e];
+        for (int sq = 0; sq < 2; ++sq) {               // (cG)^2, then (c^2 G^2)^2
+          put_frag(sP, row0, q, g4);
+          put_frag(sG, row0, q, g4);
+          sync_for_mma();
+          if (tid == 0) btc::mma64(tD, sP, sG, &bar);
+          mbar_wait(&bar, phase);
+          phase ^= 1;
+          asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+          ld_frag(tD + lane_off, g4);
+          asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+          __syncthreads();                             // everyone has read D and the operands
+        }
+      }
+      if (tid < 64) sV[tid] = tid < s ? rsqrtf((float)s) : 0.f;
+      __syncthreads();
+      float nrm = 0.f;
+      const int niter = a.T - 3 * qsq;
+      for (int t = 0; t < niter; ++t) {
+        const bool use4 = t < qsq;
+        float u0a = 0.f, u0b = 0.f, u1a = 0.f, u1b = 0.f;   // row0 / row1 partial sums (2 chains each)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float v0 = sV[8 * c + 2 * q], v1 = sV[8 * c + 2 * q + 1];
+          u0a = fmaf(use4 ? g4[4 * c + 0] : g[4 * c + 0], v0, u0a);
+          u0b = fmaf(use4 ? g4[4 * c + 1] : g[4 * c + 1], v1, u0b);
+          u1a = fmaf(use4 ? g4[4 * c + 2] : g[4 * c + 2], v0, u1a);
+          u1b = fmaf(use4 ? g4[4 * c + 3] : g[4 * c + 3], v1, u1b);
+        }
+        float u0 = u0a + u0b, u1 = u1a + u1b;
+        u0 += __shfl_xor_sync(0xffffffffu, u0, 1);
+        u1 += __shfl_xor_sync(0xffffffffu, u1, 1);
+        u0 += __shfl_xor_sync(0xffffffffu, u0, 2);
+        u1 += __shfl_xor_sync(0xffffffffu, u1, 2);
+        float sq = q == 0 ? u0 * u0 + u1 * u1 : 0.f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+        if (lane == 0) sRed[warp] = sq;
+        __syncthreads();
+        nrm = sqrtf((sRed[0] + sRed[1]) + (sRed[2] + sRed[3]));
+        if (!(nrm > 0.f)) break;
+        if (q == 0) {
+          sV[row0] = u0 / nrm;
+          sV[row1] = u1 / nrm;
+        }
+        __syncthreads();
+      }
+      lam_hat = nrm > 0.f ? (double)nrm : 0.0;
+    }
+    BTC_STAMP(2);
+    // ---- line 4: coefficients (fp64) for this matrix's Lambda_max
+    const bool degen = !(lam_hat > kDegenerateLambda);
+    const double lam = a.safety * lam_hat;
+    const double tau = resolve_tau(a.kern, sqrt(lam_hat));
+    for (int l = tid; l < K; l += NT) sHn[l] = h_response(a.kern, lam / 2.0 * (cos(cheb_theta(l + 1, K)) + 1.0), tau);
+    __syncthreads();
+    for (int k = tid; k < K; k += NT) {
+      double acc_c = 0.0;
+      const double* ct = a.costab + k * K;
+      for (int l = 0; l < K; ++l) acc_c += __ldg(ct + l) * sHn[l];
+      sC[k] = degen ? 0.f : (float)(2.0 / K * acc_c);
+    }
+    __syncthreads();
+    if (tid == 0 && a.lambda_out) a.lambda_out[b] = (float)lam;
+    const float s2 = degen ? 0.f : (float)(2.0 / lam);
+    const float s4 = 2.f * s2;
+
+    BTC_STAMP(3);
+    // ---- lines 5-7: Psi_1 = s2 G - I, H = c0/2 I + c1 Psi_1 (all in this thread's fragment)
+    float wp[32], wpp[32], hh[32];
+    {
+      const float h0 = 0.5f * sC[0], c1 = sC[1];
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {
+        const float id = (rowof(e) == colof(e)) ? 1.f : 0.f;
+        const float w = s2 * g[e] - id;
+        wp[e] = w;
+        wpp[e] = id;                                 // Psi_0 = I
+        hh[e] = h0 * id + c1 * w;
+      }
+      put_frag(sG, row0, q, g);                      // B operand of the steps: rows of G
+      put_frag(sP, row0, q, wp);                     // A operand: rows of Psi_1
+    }
+    sync_for_mma();
+    BTC_STAMP(4);
+    // ---- lines 8-11: D = Psi_{k-1} G^T, Psi_k = s4 D - 2 Psi_{k-1} - Psi_{k-2}, H += c_k Psi_k
+#ifdef CPA_BTC_TRACE
+    long long ss[5] = {};
+#endif
+    for (int k = 2; k < K; ++k) {
+#ifdef CPA_BTC_TRACE
+      if (k == 6) ss[0] = clock64();
+#endif
+      if (tid == 0) btc::mma64(tD, sP, sG, &bar);
+#ifdef CPA_BTC_TRACE
+      if (k == 6) ss[1] = clock64();
+#endif
+      mbar_wait(&bar, phase);
+      phase ^= 1;
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+#ifdef CPA_BTC_TRACE
+      if (k == 6) ss[2] = clock64();
+#endif
+      float d[32];
+      ld_frag(tD + lane_off, d);
+      const float ck = sC[k];
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {
+        const float w = s4 * d[e] - 2.f * wp[e] - wpp[e];   // Psi_k = 2 B_hat Psi_{k-1} - Psi_{k-2}
+        hh[e] = fmaf(ck, w, hh[e]);                          // H += c_k Psi_k
+        wpp[e] = wp[e];
+        wp[e] = w;
+      }
+      if (k + 1 < K) put_frag(sP, row0, q, wp);
+#ifdef CPA_BTC_TRACE
+      if (k == 6) ss[3] = clock64();
+#endif
+      sync_for_mma();
+#ifdef CPA_BTC_TRACE
+      if (k == 6) ss[4] = clock64();
+#endif
+    }
+#ifdef CPA_BTC_TRACE
+    if (tid == 0 && blockIdx.x == 0 && b < 3 * gridDim.x)
+      printf("btc step: issue %lld wait %lld epilogue %lld sync %lld\n", ss[1] - ss[0], ss[2] - ss[1], ss[3] - ss[2],
+             ss[4] - ss[3]);
+#endif
+    BTC_STAMP(5);
+    // ---- line 12: Y = H A  (A operand = rows of H, B operand = rows of A^T)
+    put_frag(sP, row0, q, hh);
+    sync_for_mma();
+    if (tid == 0) btc::mma64(tD, sP, sAT, &bar);
+    mbar_wait(&bar, phase);
+    phase ^= 1;
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    {
+      float d[32];
+      ld_frag(tD + lane_off, d);
+      float* Yb = a.Y + b * mn;
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {
+        const int r = rowof(e), c = colof(e);
+        if (r < s && c < L) {
+          if (left) Yb[(int64_t)r * a.n + c] = d[e];
+          else Yb[(int64_t)c * a.n + r] = d[e];
+        }
+      }
+    }
+    BTC_STAMP(6);
+#ifdef CPA_BTC_TRACE
+    if (tid == 0 && blockIdx.x == 0 && b < 3 * gridDim.x)
+      printf("btc b=%lld load %lld gram+power %lld coef %lld init %lld steps %lld final %lld\n", (long long)b,
+             tr[1] - tr[0], tr[2] - tr[1], tr[3] - tr[2], tr[4] - tr[3], tr[5] - tr[4], tr[6] - tr[5]);
+#endif
+    // TMEM D and the operands are rewritten by the next matrix only after this barrier
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;\n" ::"r"(tslot));
+}
+
+}  // namespace btc
+
+__global__ void k_costab(double* tab, int K);
+
+cudaError_t launch_batched_tc(int64_t batch, int m, int n, const float* X, float* Y, const cpa_svt_kernel& k, int K,
+                              int T, double safety, double lam_override, float* lambda_out, int num_sms,
+                              cudaStream_t st, int* launches, double* costab) {
+  if (K > CPA_SVT_KMAX) return cudaErrorNotSupported;
+  k_costab<<<(K * K + 255) / 256, 256, 0, st>>>(costab, K);
+  if (launches) ++*launches;
+  btc::Args a{batch, m, n, X, Y, k, K, T, safety, lam_override, lambda_out, costab};
+  cudaError_t e = cudaFuncSetAttribute(btc::k_batched_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, btc::SMEM);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, btc::k_batched_tc, btc::NT, btc::SMEM);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 2) per_sm = 2;   // 2 x (97 KB smem, 128 thr x <= 255 regs, 64 TMEM columns) fit one SM
+  if (const char* v = getenv("CPA_SVT_BTC_PER_SM")) per_sm = atoi(v);
+  int64_t grid = (int64_t)num_sms * (per_sm > 0 ? per_sm : 1);
+  if (grid > batch) grid = batch;
+  btc::k_batched_tc<<<(unsigned)grid, btc::NT, btc::SMEM, st>>>(a);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+}  // namespace cpa
