@@ -90,6 +90,28 @@ __device__ __forceinline__ void mma64(uint32_t tmem_d, const uint8_t* a_hi, cons
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
                : "memory");
 }
+// Same product with the A operand in TMEM ("ts" form, probed: A row r in the M = 64 D lane of
+// row r, element k in column k; one UMMA_K = 8 columns): hi / lo at tmem_a_hi / tmem_a_lo.
+// At M = 64 the smem-A form is limited by its shared-memory A reads (measured 61 cycles per
+// M64 N64 K8 MMA against the 32-cycle floor).
+__device__ __forceinline__ void mma64_ts(uint32_t tmem_d, uint32_t ta_hi, uint32_t ta_lo, const uint8_t* b_hi,
+                                         uint64_t* bar) {
+  const uint32_t bh = smem_u32(b_hi), bl = bh + OPB;
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) {
+    const uint32_t off = (kk >> 2) * 8192 + (kk & 3) * 32;
+    const uint64_t dbh = desc(bh + off), dbl = desc(bl + off);
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %5, %3, 1;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%6], %2, %3, 1;\n}\n" ::"r"(tmem_d),
+        "r"(ta_hi + kk * 8), "l"(dbh), "r"(IDESC), "r"(kk > 0 ? 1u : 0u), "l"(dbl), "r"(ta_lo + kk * 8)
+        : "memory");
+  }
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
+               : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n.reg .pred p;\nWAIT_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra WAIT_%=;\n}\n" ::"r"(
@@ -169,6 +191,34 @@ __device__ __forceinline__ void ld_frag(uint32_t taddr, float (&v)[32]) {
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
+// store a fragment (layout of ld_frag) as TF32 hi / lo A operands in TMEM (same layout)
+__device__ __forceinline__ void st_frag_hl(uint32_t t_hi, uint32_t t_lo, const float (&v)[32]) {
+  uint32_t h[32], l[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const float x = v[i], hx = rna(x);
+    h[i] = __float_as_uint(hx);
+    l[i] = __float_as_uint(rna(x - hx));
+  }
+#define BTC_ST16(addr, r)                                                                                          \
+  asm volatile("tcgen05.st.sync.aligned.16x256b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16," \
+               "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};\n" ::"r"(addr),                    \
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),     \
+               "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),         \
+               "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),        \
+               "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])                     \
+               : "memory")
+  BTC_ST16(t_hi, h);
+  BTC_ST16(t_lo, l);
+#undef BTC_ST16
+}
+// TMEM stores done and visible to the next MMA issue (no shared-memory writes involved)
+__device__ __forceinline__ void sync_tmem_for_mma() {
+  asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+}
 // write a fragment (layout of ld_frag) as TF32 hi / lo operand rows: element (row, col) at sw(row, col)
 __device__ __forceinline__ void put_frag(uint8_t* hi, int row0, int q, const float (&v)[32]) {
 #pragma unroll
@@ -215,13 +265,13 @@ __global__ void __launch_bounds__(NT, 1) k_batched_tc(Args a) {
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;\n" ::"r"(smem_u32(&tslot)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;\n" ::"r"(smem_u32(&tslot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  const uint32_t tD = tslot;
+  const uint32_t tD = tslot, tAh = tslot + 64, tAl = tslot + 128;   // D, A operand (hi, lo)
   uint32_t phase = 0;
 
 #ifdef CPA_BTC_TRACE
@@ -296,10 +346,10 @@ __global__ void __launch_bounds__(NT, 1) k_batched_tc(Args a) {
 #pragma unroll
         for (int e = 0; e < 32; ++e) g4[e] = cs * g[e];
         for (int sq = 0; sq < 2; ++sq) {               // (cG)^2, then (c^2 G^2)^2
-          put_frag(sP, row0, q, g4);
+          st_frag_hl(tAh + lane_off, tAl + lane_off, g4);
           put_frag(sG, row0, q, g4);
           sync_for_mma();
-          if (tid == 0) btc::mma64(tD, sP, sG, &bar);
+          if (tid == 0) btc::mma64_ts(tD, tAh, tAl, sG, &bar);
           mbar_wait(&bar, phase);
           phase ^= 1;
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
@@ -375,7 +425,7 @@ __global__ void __launch_bounds__(NT, 1) k_batched_tc(Args a) {
         hh[e] = h0 * id + c1 * w;
       }
       put_frag(sG, row0, q, g);                      // B operand of the steps: rows of G
-      put_frag(sP, row0, q, wp);                     // A operand: rows of Psi_1
+      st_frag_hl(tAh + lane_off, tAl + lane_off, wp); // A operand (TMEM): rows of Psi_1
     }
     sync_for_mma();
     BTC_STAMP(4);
@@ -387,7 +437,7 @@ __global__ void __launch_bounds__(NT, 1) k_batched_tc(Args a) {
 #ifdef CPA_BTC_TRACE
       if (k == 6) ss[0] = clock64();
 #endif
-      if (tid == 0) btc::mma64(tD, sP, sG, &bar);
+      if (tid == 0) btc::mma64_ts(tD, tAh, tAl, sG, &bar);
 #ifdef CPA_BTC_TRACE
       if (k == 6) ss[1] = clock64();
 #endif
@@ -407,11 +457,11 @@ __global__ void __launch_bounds__(NT, 1) k_batched_tc(Args a) {
         wpp[e] = wp[e];
         wp[e] = w;
       }
-      if (k + 1 < K) put_frag(sP, row0, q, wp);
+      if (k + 1 < K) st_frag_hl(tAh + lane_off, tAl + lane_off, wp);
 #ifdef CPA_BTC_TRACE
       if (k == 6) ss[3] = clock64();
 #endif
-      sync_for_mma();
+      sync_tmem_for_mma();
 #ifdef CPA_BTC_TRACE
       if (k == 6) ss[4] = clock64();
 #endif
@@ -423,9 +473,9 @@ __global__ void __launch_bounds__(NT, 1) k_batched_tc(Args a) {
 #endif
     BTC_STAMP(5);
     // ---- line 12: Y = H A  (A operand = rows of H, B operand = rows of A^T)
-    put_frag(sP, row0, q, hh);
-    sync_for_mma();
-    if (tid == 0) btc::mma64(tD, sP, sAT, &bar);
+    st_frag_hl(tAh + lane_off, tAl + lane_off, hh);
+    sync_tmem_for_mma();
+    if (tid == 0) btc::mma64_ts(tD, tAh, tAl, sAT, &bar);
     mbar_wait(&bar, phase);
     phase ^= 1;
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
@@ -454,7 +504,7 @@ __global__ void __launch_bounds__(NT, 1) k_batched_tc(Args a) {
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   }
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;\n" ::"r"(tslot));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;\n" ::"r"(tslot));
 }
 
 }  // namespace btc
