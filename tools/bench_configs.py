@@ -100,10 +100,20 @@ def batched(h, reps, batch=65536):
     Y = torch.empty_like(Xb)
     ms, ph = timed(lambda: h.apply_batched(Xb, cfg["kernel"], cfg["K"], T=cfg["T"], Y=Y), reps, h)
     s = L = 64
-    per = s * (s + 1) * L + (cfg["K"] - 1) * 2 * s * s * L
+    K, T = cfg["K"], cfg["T"]
+    per = s * (s + 1) * L + (K - 1) * 2 * s * s * L
     F = per * batch
     byt = 2 * batch * 64 * 64 * 4
-    return {"config": "c3", "batch": batch, "ms_per_svt_batch": ms, "gflops": F / ms / 1e6,
+    # tcgen05 engine (default): Gram, 2 squarings, K-2 steps, line 12 = K + 1 products of 64^3,
+    # each 3 TF32 MMAs (3xTF32); TF32 dense peak = MEASURED_PEAKS bf16 / 2, halved at M = 64
+    # (one MMA of M64 N64 K8 per 64 cycles per SM)
+    products = (2 if T >= 8 else 0) + 1 + (K - 2) + 1
+    tensor_flops = batch * products * 3 * 2 * s * s * L
+    tf32_peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"] / 2
+    return {"config": "c3", "batch": batch, "engine": "tcgen05 3xTF32 (M=N=64, A in TMEM)", "ms_per_svt_batch": ms,
+            "gflops": F / ms / 1e6, "tensor_tflops_issued": tensor_flops / ms / 1e9,
+            "tensor_frac_of_tf32_peak": tensor_flops / ms / 1e9 / tf32_peak,
+            "tensor_frac_of_m64_ceiling": tensor_flops / ms / 1e9 / (tf32_peak / 2),
             "fp32_frac": F / ms / 1e9 / PEAKS["fp32_ffma_tflops"], "hbm_gbs": byt / ms / 1e6,
             "hbm_frac": byt / ms / 1e6 / HBM, "gen_s": gen_s}
 
