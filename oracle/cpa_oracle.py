@@ -28,6 +28,7 @@ __all__ = [
     "cpa_shrink_columns", "cpa_shrink_rows", "cpa_shrink_batched",
     "sparse_power_iteration", "cpa_shrink_sparse_rows", "jacobi_svd",
     "exact_shrink", "svd_characterization", "rel_fro", "haar1_matrix", "cpa_shrink_transform",
+    "dct2_matrix", "synthetic_D", "admm_recover",
     "DEFAULT_SAFETY", "DEGENERATE_LAMBDA",
 ]
 
@@ -331,6 +332,76 @@ def cpa_shrink_transform(X, kernel: Kernel, K: int, T: int = 30, safety: float =
     Y = B @ Tm.T @ H @ Tm
     Y = Y.T if m <= n else Y
     return (Y, info) if return_info else Y
+
+
+# ---------------------------------------------------------------------------
+# NEXT-3: ADMM recovery with CPA shrinkage as the nuclear-norm prox
+# (PAPER.md:657-692 ADMM, 1193-1214 eq. admm_algorithm_inp, 1095-1100 synthetic data)
+# ---------------------------------------------------------------------------
+
+def dct2_matrix(n: int) -> np.ndarray:
+    """Orthonormal DCT-II matrix C (C y = DCT of y; PAPER.md:1185 uses DCT matrices T1, T2):
+    C[k, j] = a_k cos(pi (2j + 1) k / (2n)), a_0 = sqrt(1/n), a_k = sqrt(2/n)."""
+    k = np.arange(n)[:, None]
+    j = np.arange(n)[None, :]
+    C = np.cos(np.pi * (2 * j + 1) * k / (2 * n)) * math.sqrt(2.0 / n)
+    C[0, :] = math.sqrt(1.0 / n)
+    return C
+
+
+def synthetic_D(N: int, rank: int) -> np.ndarray:
+    """The paper's synthetic matrix: D = J - blkdiag(0.5 1 1^T, rank), N x N."""
+    p = N // rank
+    D = np.ones((N, N))
+    for b in range(rank):
+        D[b * p:(b + 1) * p, b * p:(b + 1) * p] -= 0.5
+    return D
+
+
+def admm_recover(D_obs, mask, kernel: Kernel, K: int, T: int, rho: float, eta: float,
+                 max_iter: int = 300, tol: float = 1e-4, shrink=None, return_history: bool = False):
+    """ADMM of PAPER.md:1193-1214 (eq. admm_algorithm_inp) for the synthetic experiment
+    (PAPER.md:1095-1100): the average-term constraint z^(5) is dropped, so
+    K l = [l; Psi l; Omega l; l] with Psi = 2-D orthonormal DCT (C_m L C_n^T) and Omega the
+    observed-entry selector (mask = 1 on observed entries).  K^T K = (3 + mask) I elementwise.
+
+      l   <- (K^T K)^-1 K^T (z - u)
+      z1  <- prox_{1/rho ||.||_*}(l + u1)      -- CPA shrinkage (or `shrink`)
+      z2  <- soft(Psi l + u2, eta / rho)
+      z3  <- D_obs on the observed entries     (Pi_I keeps the assigned values)
+      z4  <- clip(l + u4, 0, 1)                (Pi_D)
+      u   <- u + K l - z
+    stopping: ||l_{t+1} - l_t|| / ||l_{t+1}|| < tol (PAPER.md:694 footnote).  z, u start at 0."""
+    D_obs = np.asarray(D_obs, dtype=np.float64)
+    w = np.asarray(mask, dtype=np.float64)
+    m, n = D_obs.shape
+    Cm, Cn = dct2_matrix(m), dct2_matrix(n)
+    psi = lambda X: Cm @ X @ Cn.T
+    psit = lambda S: Cm.T @ S @ Cn
+    if shrink is None:
+        shrink = lambda X: cpa_shrink(X, kernel, K, T=T)
+    z1 = np.zeros((m, n)); z2 = np.zeros((m, n)); z4 = np.zeros((m, n))
+    z3 = w * D_obs
+    u1 = np.zeros((m, n)); u2 = np.zeros((m, n)); u3 = np.zeros((m, n)); u4 = np.zeros((m, n))
+    l = np.zeros((m, n))
+    hist = []
+    for it in range(max_iter):
+        l_prev = l
+        l = ((z1 - u1) + psit(z2 - u2) + w * (z3 - u3) + (z4 - u4)) / (3.0 + w)
+        pl = psi(l)
+        z1 = shrink(l + u1)
+        v2 = pl + u2
+        z2 = np.sign(v2) * np.maximum(np.abs(v2) - eta / rho, 0.0)
+        z4 = np.clip(l + u4, 0.0, 1.0)
+        u1 = u1 + l - z1
+        u2 = u2 + pl - z2
+        u3 = u3 + w * l - z3
+        u4 = u4 + l - z4
+        rel = float(np.linalg.norm(l - l_prev) / max(np.linalg.norm(l), 1e-300))
+        hist.append(rel)
+        if rel < tol:
+            break
+    return (l, hist) if return_history else l
 
 
 def cpa_apply_vectors(apply_phi, V, c, lam: float):

@@ -399,3 +399,53 @@ def test_transform_block_structure(shape):
     want = want if left else want.T
     assert O.rel_fro(Y, want) <= 1e-12
     assert abs(O.series_eval(c, lam, 0.0) - h0) <= 1e-12 * max(1.0, abs(h0))
+
+
+# ---- NEXT-3: ADMM recovery (synthetic D of PAPER.md:1095-1100)
+
+@pytest.mark.parametrize("n", [1, 2, 5, 16])
+def test_dct2_orthonormal(n):
+    C = O.dct2_matrix(n)
+    assert np.allclose(C @ C.T, np.eye(n), atol=1e-14)
+    # DCT of a constant vector is concentrated in the DC coefficient
+    y = np.full(n, 3.0)
+    assert np.allclose((C @ y)[1:], 0.0, atol=1e-13) and abs((C @ y)[0] - 3.0 * np.sqrt(n)) < 1e-12
+
+
+def test_synthetic_D_spectrum():
+    # sigma_1 = N - p/2, sigma_2..rank = p/2, rank exactly `rank`
+    N, r = 120, 6
+    p = N // r
+    s = np.linalg.svd(O.synthetic_D(N, r), compute_uv=False)
+    assert abs(s[0] - (N - p / 2)) < 1e-9 and np.allclose(s[1:r], p / 2, atol=1e-9) and s[r] < 1e-9
+
+
+def _svd_soft(X, tau):
+    U, sv, Vt = np.linalg.svd(X, full_matrices=False)
+    return (U * np.maximum(sv - tau, 0.0)) @ Vt
+
+
+def test_admm_exact_shrink_recovers_full_observation():
+    """With every entry observed and tiny weights, the ADMM fixed point is the data itself:
+    z3 pins l to D on all entries."""
+    D = O.synthetic_D(60, 5)
+    mask = np.ones_like(D)
+    kern = O.Kernel(kind="soft", tau=0.05, tau_relative=False)
+    L = O.admm_recover(D, mask, kern, 10, 30, rho=20.0, eta=0.0, max_iter=400, tol=1e-9,
+                       shrink=lambda X: _svd_soft(X, 0.05))
+    assert O.rel_fro(L, D) <= 1e-3
+
+
+def test_admm_cpa_tracks_exact_on_corrupted_D():
+    """10% of D zeroed: the CPA-ADMM recovery is close to the exact-shrinkage
+    ADMM recovery and much closer to D than the corrupted input (the paper's Fig. 9 claim)."""
+    rng = np.random.default_rng(0)
+    D = O.synthetic_D(80, 4)
+    mask = (rng.random(D.shape) >= 0.10).astype(float)
+    Dobs = D * mask
+    kern = O.Kernel(kind="soft", tau=1.0, tau_relative=False)
+    Lc = O.admm_recover(Dobs, mask, kern, 20, 30, rho=1.0, eta=0.01, max_iter=300, tol=1e-4)
+    Le = O.admm_recover(Dobs, mask, kern, 20, 30, rho=1.0, eta=0.01, max_iter=300, tol=1e-4,
+                        shrink=lambda X: _svd_soft(X, 1.0))
+    assert O.rel_fro(Lc, D) < 0.5 * O.rel_fro(Dobs, D)
+    assert O.rel_fro(Lc, Le) < 0.05
