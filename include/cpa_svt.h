@@ -184,6 +184,30 @@ cpa_svt_status cpa_svt_apply_batched(cpa_svt_handle* h, int64_t batch, int m, in
                                      const float* X, float* Y, const cpa_svt_kernel* k, int K,
                                      const cpa_svt_lambda* lam, float* lambda_out);
 
+/* NEXT-3: the paper's ADMM recovery with CPA shrinkage as the nuclear-norm prox
+ * (eq. admm_algorithm_inp; synthetic experiment
+ * PAPER.md:1095-1100 without the average-term constraint):
+ *   min ||L||_* + eta ||Psi(L)||_1  s.t. L = D on the observed entries, L in [0, 1],
+ * Psi = orthonormal 2-D DCT-II.  ADMM iterations (z, u start at 0):
+ *   l = (K^T K)^-1 K^T (z - u);  z1 = CPA-shrink_soft(1/rho)(l + u1);  z2 = soft(Psi l + u2, eta/rho);
+ *   z3 = observed D;  z4 = clip(l + u4, 0, 1);  u += K l - z;  stop: ||dl|| / ||l|| < tol.
+ * D (m x n, row-major, ld n) and mask (m x n bytes, nonzero = observed) are device pointers;
+ * L (m x n) receives the last l.  The shrinkage uses this handle's fp64 dense path (its form and
+ * transform options apply), K terms and lam (power iterations / override) per call.  One host
+ * sync per iteration.  Errors: E_ARG (null / sizes / K), E_DOMAIN (rho <= 0, eta < 0, tol < 0,
+ * max_iter < 1), E_CUDA. */
+typedef struct {
+  double rho, eta, tol;   /* in */
+  int32_t max_iter;       /* in, >= 1 */
+  int32_t iters;          /* out: iterations run */
+  double last_rel;        /* out: last ||l_{t+1} - l_t|| / ||l_{t+1}|| */
+  double ms_shrink;       /* out: CUDA-event time inside the CPA shrinkage calls */
+  double ms_total;        /* out: CUDA-event time of the whole loop */
+} cpa_svt_admm;
+cpa_svt_status cpa_svt_admm_recover(cpa_svt_handle* h, int64_t m, int64_t n, const double* D,
+                                    const unsigned char* mask, int K, const cpa_svt_lambda* lam,
+                                    cpa_svt_admm* opt, double* L);
+
 /* Handle options (cpa_svt_set_option). */
 typedef enum {
   CPA_SVT_OPT_FORM = 0      /* dense recurrence form: 0 = auto (fewest flops), 1 = apply-to-X

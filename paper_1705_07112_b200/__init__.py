@@ -34,6 +34,12 @@ class Kernel(ctypes.Structure):
                 ("w_c", ctypes.c_double), ("w_shift", ctypes.c_double), ("w_eps", ctypes.c_double)]
 
 
+class Admm(ctypes.Structure):
+    _fields_ = [("rho", ctypes.c_double), ("eta", ctypes.c_double), ("tol", ctypes.c_double),
+                ("max_iter", ctypes.c_int32), ("iters", ctypes.c_int32), ("last_rel", ctypes.c_double),
+                ("ms_shrink", ctypes.c_double), ("ms_total", ctypes.c_double)]
+
+
 class Lambda(ctypes.Structure):
     _fields_ = [("power_iters", ctypes.c_int32), ("want_lambda", ctypes.c_int32), ("safety", ctypes.c_double),
                 ("lambda_max", ctypes.c_double), ("lambda_hat", ctypes.c_double)]
@@ -80,6 +86,8 @@ lib.cpa_svt_profile.argtypes = [_p, ctypes.c_int]
 lib.cpa_svt_profile_read.argtypes = [_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)]
 PHASES = ["gram", "allreduce", "power", "init", "step", "sparse_z", "sparse_w", "batched", "final"]
 lib.cpa_svt_set_option.argtypes = [_p, ctypes.c_int, _i64]
+lib.cpa_svt_admm_recover.argtypes = [_p, _i64, _i64, _p, _p, ctypes.c_int, ctypes.POINTER(Lambda), ctypes.POINTER(Admm), _p]
+lib.cpa_svt_admm_recover.restype = ctypes.c_int
 lib.cpa_svt_set_option.restype = ctypes.c_int
 FORM = {"auto": 0, "apply": 1, "poly": 2, "poly_full": 3}
 for _f in ("cpa_svt_init", "cpa_svt_free", "cpa_svt_nccl_unique_id", "cpa_svt_coeffs", "cpa_svt_apply",
@@ -245,6 +253,22 @@ class Handle:
                                        lambda_out.data_ptr() if lambda_out is not None else None)
         self._check(st, "cpa_svt_apply_batched")
         return Y
+
+    def admm_recover(self, D, mask, K: int, rho: float, eta: float, T: int = 30, tol: float = 1e-4,
+                     max_iter: int = 300, safety: float = 1.01, L=None):
+        """cpa_svt_admm_recover (NEXT-3): ADMM recovery of the observed entries of D (float64 CUDA
+        m x n) under a uint8 CUDA mask (nonzero = observed); returns (L, info)."""
+        torch = self._torch
+        assert D.is_cuda and D.dtype == torch.float64 and D.is_contiguous() and D.dim() == 2
+        assert mask.is_cuda and mask.dtype == torch.uint8 and mask.shape == D.shape and mask.is_contiguous()
+        if L is None:
+            L = torch.empty_like(D)
+        lam = self._lambda(T, safety, 0.0, False)
+        opt = Admm(float(rho), float(eta), float(tol), int(max_iter), 0, 0.0, 0.0, 0.0)
+        st = lib.cpa_svt_admm_recover(self._h, D.shape[0], D.shape[1], D.data_ptr(), mask.data_ptr(), K,
+                                      ctypes.byref(lam), ctypes.byref(opt), L.data_ptr())
+        self._check(st, "cpa_svt_admm_recover")
+        return L, {"iters": opt.iters, "last_rel": opt.last_rel, "ms_shrink": opt.ms_shrink, "ms_total": opt.ms_total}
 
     def apply_csr(self, row_ptr, col, val, m: int, n: int, kernel, K: int, T: int = 300, safety: float = 1.01,
                   lambda_max: float = 0.0, row_begin: int = 0, row_end: int | None = None, Y=None,

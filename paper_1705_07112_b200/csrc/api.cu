@@ -30,6 +30,16 @@ cudaError_t dense_gemm_store(int64_t M, int64_t N, int64_t Kd, const double* A, 
                              int64_t ldb, double* C, int64_t ldc, cudaStream_t st, double* partial = nullptr,
                              int* tcount = nullptr);
 size_t dense_store_partial_doubles(int64_t M, int64_t N);
+// admm.cu
+cudaError_t admm_dct(double* C, double* CT, int64_t n, int num_sms, cudaStream_t st);
+cudaError_t admm_sub(const double* a, const double* b, double* out, int64_t N, cudaStream_t st);
+cudaError_t admm_l(const double* z1, const double* u1, const double* pt, const uint8_t* mask, const double* D,
+                   const double* u3, const double* z4, const double* u4, double* l, double* t, int64_t N,
+                   cudaStream_t st);
+int admm_tail_blocks();
+cudaError_t admm_tail(const double* l, const double* lprev, const double* pl, const double* z1, const uint8_t* mask,
+                      const double* D, double* z2, double* z4, double* u1, double* u2, double* u3, double* u4,
+                      double thr, int64_t N, double* part, cudaStream_t st);
 cudaError_t dense_haar_split(const double* X, int64_t m, int64_t n, int64_t ldx, bool left, double* AL, double* AH,
                              int num_sms, cudaStream_t st);
 cudaError_t dense_haar_combine(const double* YL, const double* AH, const SeriesParams* P, int64_t m, int64_t n,
@@ -129,6 +139,8 @@ struct cpa_svt_handle {
   size_t ws_bytes = 0;
   void* hx = nullptr;              // apply_host device staging
   void* tws = nullptr;             // transform workspace (A_L, A_H, Y_L)
+  void* aws = nullptr;             // ADMM workspace
+  size_t aws_bytes = 0;
   size_t tws_bytes = 0;
   int transform = 0;               // CPA_SVT_OPT_TRANSFORM
   int batched_engine = 0;          // CPA_SVT_OPT_BATCHED: 0 auto (tensor cores), 1 FFMA, 2 tcgen05
@@ -321,6 +333,7 @@ cpa_svt_status cpa_svt_free(cpa_svt_handle* h) {
   cudaFree(h->ws);
   cudaFree(h->hx);
   cudaFree(h->tws);
+  cudaFree(h->aws);
   for (auto& u : h->ev_used) {
     cudaEventDestroy(u.second.first);
     cudaEventDestroy(u.second.second);
@@ -875,6 +888,94 @@ cpa_svt_status cpa_svt_apply_host(cpa_svt_handle* h, cpa_svt_dtype dtype, cpa_sv
   if (st != CPA_SVT_OK) return st;
   CU(cudaMemcpyAsync(Y_host, dY, bytes, cudaMemcpyDeviceToHost, h->stream));
   CU(cudaStreamSynchronize(h->stream));
+  return CPA_SVT_OK;
+}
+
+// NEXT-3 (synthetic experiment PAPER.md:1095-1100): ADMM recovery of L from
+// the observed entries of D.  K l = [l; Psi l; Omega l; l], Psi = C_m . C_n^T (orthonormal 2-D
+// DCT), K^T K = (3 + mask) I; the nuclear prox is the CPA shrinkage (soft, tau = 1/rho) of this
+// handle.  One host sync per iteration (the stopping test).
+cpa_svt_status cpa_svt_admm_recover(cpa_svt_handle* h, int64_t m, int64_t n, const double* D, const uint8_t* mask,
+                                    int K, const cpa_svt_lambda* lam, cpa_svt_admm* opt, double* L) {
+  if (!h || !D || !mask || !L || !opt || !lam || m < 1 || n < 1 || K < 2 || K > CPA_SVT_KMAX) return CPA_SVT_E_ARG;
+  if (!(opt->rho > 0.0) || !(opt->eta >= 0.0) || !(opt->tol >= 0.0) || opt->max_iter < 1) return CPA_SVT_E_DOMAIN;
+  cpa_svt_status st = check_lambda(lam);
+  if (st != CPA_SVT_OK) return st;
+  if (cudaSetDevice(h->device) != cudaSuccess) return CPA_SVT_E_CUDA;
+  const int64_t N = m * n;
+  auto r32 = [](size_t v) { return (v + 31) / 32 * 32; };
+  const size_t nb = r32((size_t)N), nm = r32((size_t)(m * m)), nn = r32((size_t)(n * n));
+  const int nparts = admm_tail_blocks();
+  st = grow(h, &h->aws, &h->aws_bytes, (14 * nb + 2 * nm + 2 * nn + 2 * (size_t)nparts) * sizeof(double) + 256);
+  if (st != CPA_SVT_OK) return st;
+  double* p = (double*)h->aws;
+  auto take = [&](size_t cnt) { double* q = p; p += cnt; return q; };
+  double *Cm = take(nm), *CmT = take(nm), *Cn = take(nn), *CnT = take(nn);
+  double *z1 = take(nb), *z2 = take(nb), *z4 = take(nb), *u1 = take(nb), *u2 = take(nb), *u3 = take(nb),
+         *u4 = take(nb), *la = take(nb), *lb = take(nb), *pl = take(nb), *t = take(nb), *tmp = take(nb),
+         *A1 = take(nb), *pt = take(nb);
+  double* part = take(2 * (size_t)nparts);
+  CU(admm_dct(Cm, CmT, m, h->num_sms, h->stream));
+  CU(admm_dct(Cn, CnT, n, h->num_sms, h->stream));
+  for (double* b : {z1, z2, z4, u1, u2, u3, u4, la})
+    CU(cudaMemsetAsync(b, 0, (size_t)N * sizeof(double), h->stream));
+  cpa_svt_kernel kern{};
+  kern.kind = CPA_SVT_SOFT;
+  kern.tau = 1.0 / opt->rho;
+  kern.tau_relative = 0;
+  cpa_svt_lambda lm = *lam;
+  lm.want_lambda = 0;
+  cudaEvent_t e0, e1, ea, eb;
+  cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventCreate(&ea); cudaEventCreate(&eb);
+  cudaEventRecord(ea, h->stream);
+  std::vector<double> hp(2 * (size_t)nparts);
+  double ms_shrink = 0.0, rel = 0.0;
+  double* l = la;
+  double* lprev = lb;
+  int it = 0;
+  for (; it < opt->max_iter; ++it) {
+    std::swap(l, lprev);   // lprev = l_t; l receives l_{t+1}
+    // Psi^T (z2 - u2) = C_m^T (z2 - u2) C_n
+    CU(admm_sub(z2, u2, tmp, N, h->stream));
+    CU(dense_gemm_store(m, n, m, CmT, m, tmp, n, A1, n, h->stream));
+    CU(dense_gemm_store(m, n, n, A1, n, Cn, n, pt, n, h->stream));
+    CU(admm_l(z1, u1, pt, mask, D, u3, z4, u4, l, t, N, h->stream));
+    // Psi l = C_m l C_n^T
+    CU(dense_gemm_store(m, n, m, Cm, m, l, n, A1, n, h->stream));
+    CU(dense_gemm_store(m, n, n, A1, n, CnT, n, pl, n, h->stream));
+    // z1 = prox_{1/rho ||.||_*}(l + u1): the CPA shrinkage
+    cudaEventRecord(e0, h->stream);
+    st = apply_f64(h, m, n, CPA_SVT_SHARD_NONE, 0, t, n, z1, n, &kern, K, nullptr, &lm, nullptr);
+    if (st != CPA_SVT_OK) return st;
+    cudaEventRecord(e1, h->stream);
+    CU(admm_tail(l, lprev, pl, z1, mask, D, z2, z4, u1, u2, u3, u4, opt->eta / opt->rho, N, part, h->stream));
+    CU(cudaMemcpyAsync(hp.data(), part, hp.size() * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    ms_shrink += ms;
+    double a = 0.0, b = 0.0;
+    for (int i = 0; i < nparts; ++i) {
+      a += hp[2 * i];
+      b += hp[2 * i + 1];
+    }
+    rel = sqrt(a) / fmax(sqrt(b), 1e-300);
+    h->launches += 9;
+    if (rel < opt->tol) {
+      ++it;
+      break;
+    }
+  }
+  cudaEventRecord(eb, h->stream);
+  CU(cudaMemcpyAsync(L, l, (size_t)N * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  float mt = 0.f;
+  cudaEventElapsedTime(&mt, ea, eb);
+  cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(ea); cudaEventDestroy(eb);
+  opt->iters = it;
+  opt->last_rel = rel;
+  opt->ms_shrink = ms_shrink;
+  opt->ms_total = mt;
   return CPA_SVT_OK;
 }
 

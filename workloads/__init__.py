@@ -159,3 +159,13 @@ def gen_pinpaint(seed: int = 0, m: int = 2560, n: int = 1920) -> np.ndarray:
         X += rng.uniform(0.5, 1.0) * np.cos(2 * np.pi * fi * i + pi) * np.cos(2 * np.pi * fj * j + pj)
     X = (X - X.min()) / (X.max() - X.min())
     return X + 0.02 * rng.standard_normal((m, n))
+
+
+def synthetic_D(N: int, rank: int) -> np.ndarray:
+    """The paper's synthetic data: D = J - blkdiag(0.5 1 1^T) with `rank`
+    diagonal blocks of size N / rank.  Deterministic; no arithmetic of the method."""
+    p = N // rank
+    D = np.ones((N, N))
+    for b in range(rank):
+        D[b * p:(b + 1) * p, b * p:(b + 1) * p] -= 0.5
+    return D
