@@ -27,7 +27,6 @@
 // column j in column j -- so lanes 0..15 of each warp own the 64 rows (16 per warp).
 // TMEM columns [0, 64): D.  The epilogue reads D with tcgen05.ld.16x256b (all 32 threads of a
 // warp: 2 rows x 16 columns each); Psi_{k-1}, Psi_{k-2} and H stay in registers in that layout.
-#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -274,15 +273,8 @@ __global__ void __launch_bounds__(NT, 1) k_batched_tc(Args a) {
   const uint32_t tD = tslot, tAh = tslot + 64, tAl = tslot + 128;   // D, A operand (hi, lo)
   uint32_t phase = 0;
 
-#ifdef CPA_BTC_TRACE
-  long long tr[8] = {};
-#define BTC_STAMP(i) tr[i] = clock64()
-#else
-#define BTC_STAMP(i)
-#endif
   for (int64_t b = blockIdx.x; b < a.batch; b += gridDim.x) {
     const float* X = a.X + b * mn;
-    BTC_STAMP(0);
     // ---- load A (s x L, zero-padded to 64 x 64) as operand rows (sP) and A^T rows (sAT);
     //      all of the thread's global loads in flight before the first conversion
     {
@@ -314,7 +306,6 @@ __global__ void __launch_bounds__(NT, 1) k_batched_tc(Args a) {
       }
     }
     sync_for_mma();
-    BTC_STAMP(1);
     // ---- line 1: G = A A^T
     if (tid == 0) btc::mma64(tD, sP, sP, &bar);
     mbar_wait(&bar, phase);
@@ -393,7 +384,6 @@ __global__ void __launch_bounds__(NT, 1) k_batched_tc(Args a) {
       }
       lam_hat = nrm > 0.f ? (double)nrm : 0.0;
     }
-    BTC_STAMP(2);
     // ---- line 4: coefficients (fp64) for this matrix's Lambda_max
     const bool degen = !(lam_hat > kDegenerateLambda);
     const double lam = a.safety * lam_hat;
@@ -411,7 +401,6 @@ __global__ void __launch_bounds__(NT, 1) k_batched_tc(Args a) {
     const float s2 = degen ? 0.f : (float)(2.0 / lam);
     const float s4 = 2.f * s2;
 
-    BTC_STAMP(3);
     // ---- lines 5-7: Psi_1 = s2 G - I, H = c0/2 I + c1 Psi_1 (all in this thread's fragment)
     float wp[32], wpp[32], hh[32];
     {
@@ -428,25 +417,12 @@ __global__ void __launch_bounds__(NT, 1) k_batched_tc(Args a) {
       st_frag_hl(tAh + lane_off, tAl + lane_off, wp); // A operand (TMEM): rows of Psi_1
     }
     sync_for_mma();
-    BTC_STAMP(4);
     // ---- lines 8-11: D = Psi_{k-1} G^T, Psi_k = s4 D - 2 Psi_{k-1} - Psi_{k-2}, H += c_k Psi_k
-#ifdef CPA_BTC_TRACE
-    long long ss[5] = {};
-#endif
     for (int k = 2; k < K; ++k) {
-#ifdef CPA_BTC_TRACE
-      if (k == 6) ss[0] = clock64();
-#endif
       if (tid == 0) btc::mma64_ts(tD, tAh, tAl, sG, &bar);
-#ifdef CPA_BTC_TRACE
-      if (k == 6) ss[1] = clock64();
-#endif
       mbar_wait(&bar, phase);
       phase ^= 1;
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-#ifdef CPA_BTC_TRACE
-      if (k == 6) ss[2] = clock64();
-#endif
       float d[32];
       ld_frag(tD + lane_off, d);
       const float ck = sC[k];
@@ -458,20 +434,8 @@ __global__ void __launch_bounds__(NT, 1) k_batched_tc(Args a) {
         wp[e] = w;
       }
       if (k + 1 < K) st_frag_hl(tAh + lane_off, tAl + lane_off, wp);
-#ifdef CPA_BTC_TRACE
-      if (k == 6) ss[3] = clock64();
-#endif
       sync_tmem_for_mma();
-#ifdef CPA_BTC_TRACE
-      if (k == 6) ss[4] = clock64();
-#endif
     }
-#ifdef CPA_BTC_TRACE
-    if (tid == 0 && blockIdx.x == 0 && b < 3 * gridDim.x)
-      printf("btc step: issue %lld wait %lld epilogue %lld sync %lld\n", ss[1] - ss[0], ss[2] - ss[1], ss[3] - ss[2],
-             ss[4] - ss[3]);
-#endif
-    BTC_STAMP(5);
     // ---- line 12: Y = H A  (A operand = rows of H, B operand = rows of A^T)
     st_frag_hl(tAh + lane_off, tAl + lane_off, hh);
     sync_tmem_for_mma();
@@ -492,12 +456,6 @@ __global__ void __launch_bounds__(NT, 1) k_batched_tc(Args a) {
         }
       }
     }
-    BTC_STAMP(6);
-#ifdef CPA_BTC_TRACE
-    if (tid == 0 && blockIdx.x == 0 && b < 3 * gridDim.x)
-      printf("btc b=%lld load %lld gram+power %lld coef %lld init %lld steps %lld final %lld\n", (long long)b,
-             tr[1] - tr[0], tr[2] - tr[1], tr[3] - tr[2], tr[4] - tr[3], tr[5] - tr[4], tr[6] - tr[5]);
-#endif
     // TMEM D and the operands are rewritten by the next matrix only after this barrier
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();

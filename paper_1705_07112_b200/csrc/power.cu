@@ -9,7 +9,6 @@
 // gathers the whole u_t by spinning on those words (no grid barrier).  ||u_t||
 // is re-summed by every CTA in the same fixed order, so all CTAs agree bitwise.
 // After the last product CTA 0 computes the coefficients.
-#include <cstdio>
 #include <cstdlib>
 
 #ifndef CPA_POLL_WARPS
@@ -171,18 +170,7 @@ __global__ void __launch_bounds__(256) k_power_dense(PowerArgs<E> a) {
   __syncthreads();
   double lam = 0.0;
   double inv = 1.0;  // 1/||u_{t-1}||, folded into this product (v_{t-1} = u_{t-1} * inv)
-#ifdef CPA_POWER_TRACE
-  unsigned long long tr[8][4];
-  auto stamp = [&](int t, int i) {
-    unsigned long long v;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
-    if (t < 8) tr[t][i] = v;
-  };
-#else
-  auto stamp = [&](int, int) {};
-#endif
   for (int t = 0; t < niter; ++t) {
-    stamp(t, 0);
     const bool use4 = t < a.q;
     const T* Gt = use4 ? a.G4 : a.G;
     const bool cached = a.cache_rows && (use4 || a.q == 0);
@@ -202,12 +190,10 @@ __global__ void __launch_bounds__(256) k_power_dense(PowerArgs<E> a) {
       if (lane == 0) st_ll(buf + 2 * r, dd, flag);
     }
     __syncthreads();  // every warp is done reading sv before it is overwritten below
-    stamp(t, 1);
     // gather u_t into sv, then ||u_t||^2 from the staged copy in a fixed order
     ll_gather(buf, s, flag, sv);
     double sq = 0.0;
     for (int64_t j = threadIdx.x; j < s; j += blockDim.x) sq = fma(sv[j], sv[j], sq);
-    stamp(t, 2);
     sq = warp_sum(sq);
     if (lane == 0) s_warp[warp] = sq;
     __syncthreads();
@@ -220,14 +206,7 @@ __global__ void __launch_bounds__(256) k_power_dense(PowerArgs<E> a) {
     lam = s_norm;
     if (!(lam > kDegenerateLambda) || !(lam < 1e300)) { lam = lam < 1e300 ? 0.0 : lam; break; }
     inv = 1.0 / lam;
-    stamp(t, 3);
   }
-#ifdef CPA_POWER_TRACE
-  if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
-    for (int t = 1; t < 8 && t < niter; ++t)
-      printf("blk %d t %d rows %llu gather %llu norm %llu total %llu ns\n", blockIdx.x, t, tr[t][1] - tr[t][0],
-             tr[t][2] - tr[t][1], tr[t][3] - tr[t][2], tr[t][3] - tr[t][0]);
-#endif
   if (blockIdx.x == 0) compute_series(a.P, a.kern, a.K, a.safety, lam, a.c_given);
 }
 
@@ -281,18 +260,7 @@ __global__ void __launch_bounds__(256) k_power_reg(PowerArgs<double> a) {
     }
     __syncthreads();
   };
-#ifdef CPA_POWER_TRACE
-  unsigned long long tr[8][4];
-  auto stamp = [&](int t, int i) {
-    unsigned long long v;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
-    if (t < 8) tr[t][i] = v;
-  };
-#else
-  auto stamp = [&](int, int) {};
-#endif
   for (int t = 0; t < niter; ++t) {
-    stamp(t, 0);
     if (a.q > 0 && t == a.q) load_rows(a.G);   // remaining products by G itself
     double p[ROWS + 1];
 #pragma unroll
@@ -312,12 +280,10 @@ __global__ void __launch_bounds__(256) k_power_reg(PowerArgs<double> a) {
       if (!(lam > kDegenerateLambda) || !(lam < 1e300)) { degenerate = true; break; }
       inv = 1.0 / lam;
     }
-    stamp(t, 1);
     const unsigned flag = (unsigned)t + 1u;
     unsigned long long* buf = a.ll + (int64_t)(t & 1) * s * 2;
     if (threadIdx.x < nrows) st_ll(buf + 2 * (r0 + threadIdx.x), s_res[threadIdx.x] * inv, flag);
     ll_gather(buf, s, flag, s_v);
-    stamp(t, 2);
 #pragma unroll
     for (int c = 0; c < COLS; ++c) v[c] = (threadIdx.x + 256 * c < s) ? s_v[threadIdx.x + 256 * c] : 0.0;
   }
@@ -334,12 +300,6 @@ __global__ void __launch_bounds__(256) k_power_reg(PowerArgs<double> a) {
     if (!(lam > kDegenerateLambda) || !(lam < 1e300)) degenerate = true;
   }
   if (degenerate) lam = lam < 1e300 ? 0.0 : lam;
-#ifdef CPA_POWER_TRACE
-  if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
-    for (int t = 1; t < 8 && t < niter; ++t)
-      printf("reg blk %d t %d reduce %llu gather %llu total %llu ns\n", blockIdx.x, t, tr[t][1] - tr[t][0],
-             tr[t][2] - tr[t][1], tr[t][2] - tr[t][0]);
-#endif
   if (blockIdx.x == 0) compute_series(a.P, a.kern, a.K, a.safety, lam, a.c_given);
 }
 
