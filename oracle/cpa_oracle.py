@@ -28,7 +28,7 @@ __all__ = [
     "cpa_shrink_columns", "cpa_shrink_rows", "cpa_shrink_batched",
     "sparse_power_iteration", "cpa_shrink_sparse_rows", "jacobi_svd",
     "exact_shrink", "svd_characterization", "rel_fro", "haar1_matrix", "cpa_shrink_transform",
-    "dct2_matrix", "synthetic_D", "admm_recover",
+    "dct2_matrix", "synthetic_D", "admm_recover", "threshold_components",
     "DEFAULT_SAFETY", "DEGENERATE_LAMBDA",
 ]
 
@@ -285,33 +285,59 @@ def haar1_matrix(n: int) -> np.ndarray:
     return T
 
 
+def threshold_components(Phi, eps_mode=None, eps=0.0):
+    """Line 2 of Alg. 1, eq. threshold_components: keep Phi_ij with
+    |Phi_ij| >= epsilon, zero the rest.  eps_mode None keeps all; "abs": epsilon = eps;
+    "topk": epsilon = K(|Phi|, k), the k-th largest |Phi_ij|, k = int(eps)
+    (every entry tied with the k-th largest is kept).  Returns (Phi_, epsilon)."""
+    if eps_mode is None:
+        return Phi, 0.0
+    A = np.abs(Phi)
+    if eps_mode == "abs":
+        thr = float(eps)
+    elif eps_mode == "topk":
+        k = int(eps)
+        flat = np.sort(A.ravel())[::-1]
+        thr = float(flat[min(max(k, 1), flat.size) - 1])
+    else:
+        raise ValueError(eps_mode)
+    return np.where(A >= thr, Phi, 0.0), thr
+
+
 def cpa_shrink_transform(X, kernel: Kernel, K: int, T: int = 30, safety: float = DEFAULT_SAFETY,
-                         lam: float | None = None, return_info: bool = False):
-    """Algorithm 1 with T = the one-level Haar DWT of the Gram index
-    and the high-frequency components of Phi set to 0 (reading R22):
+                         lam: float | None = None, return_info: bool = False, transform: str = "haar1",
+                         eps_mode=None, eps: float = 0.0):
+    """Algorithm 1 with a sparsifying orthogonal transform T of the Gram
+    index (PAPER.md:320-352):
 
       line 1  Phi  <- T B^T B T^T
-      line 2  Phi_ <- Phi with its high-frequency rows and columns zeroed
+      line 2  Phi_ <- Phi thresholded (eq. threshold_components); for the
+              one-level Haar DWT the high-frequency rows and columns are zeroed first
+              (reading R22)
       lines 3-11 as in cpa_shrink, on Phi_ (s x s; Psi_0 = Id over the whole index space)
       line 12 G_hat(B) <- B T^T H_hat(Phi_) T
 
+    transform: "haar1" (haar1_matrix) or "dct" (dct2_matrix, orthonormal DCT-II).
     Orientation as cpa_shrink: a wide X (m <= n) runs on B = X^T (Gram X X^T)."""
     X = np.asarray(X, dtype=np.float64)
     m, n = X.shape
     B = X.T if m <= n else X
     s = B.shape[1]
-    Tm = haar1_matrix(s)
-    nl = s - s // 2
+    Tm = haar1_matrix(s) if transform == "haar1" else dct2_matrix(s)
     # line 1
     Phi = Tm @ gram(B) @ Tm.T
-    # line 2: high-frequency components set to 0
+    # line 2
     Phi_ = Phi.copy()
-    Phi_[nl:, :] = 0.0
-    Phi_[:, nl:] = 0.0
+    if transform == "haar1":
+        nl = s - s // 2
+        Phi_[nl:, :] = 0.0
+        Phi_[:, nl:] = 0.0
+    Phi_, thr = threshold_components(Phi_, eps_mode, eps)
     # line 3
     lam_, lam_hat, sig_hat = _lambda_and_sigma(
         lambda: power_iteration(lambda v: Phi_ @ v, s, T)[0], lam, safety)
-    info = {"lambda_hat": lam_hat, "lambda_max": lam_, "sigma_max_hat": sig_hat, "degenerate": False}
+    info = {"lambda_hat": lam_hat, "lambda_max": lam_, "sigma_max_hat": sig_hat, "degenerate": False,
+            "epsilon": thr, "nnz": int(np.count_nonzero(Phi_))}
     if lam_hat <= DEGENERATE_LAMBDA:
         info["degenerate"] = True
         return (np.zeros_like(X), info) if return_info else np.zeros_like(X)

@@ -449,3 +449,46 @@ def test_admm_cpa_tracks_exact_on_corrupted_D():
                         shrink=lambda X: _svd_soft(X, 1.0))
     assert O.rel_fro(Lc, D) < 0.5 * O.rel_fro(Dobs, D)
     assert O.rel_fro(Lc, Le) < 0.05
+
+
+# ---- NEXT-2 DCT + epsilon thresholding
+
+def test_threshold_components_topk_and_abs():
+    Phi = np.array([[4.0, -3.0, 0.5], [-3.0, 2.0, -1.0], [0.5, -1.0, 1.5]])
+    P1, t1 = O.threshold_components(Phi, "topk", 4)      # |.| sorted: 4, 3, 3, 2, 1.5, 1, 1, .5, .5
+    assert t1 == 2.0 and np.count_nonzero(P1) == 4 and np.array_equal(P1, P1.T)
+    P2, t2 = O.threshold_components(Phi, "abs", 1.0)
+    assert t2 == 1.0 and np.count_nonzero(P2) == 7 and P2[0, 2] == 0.0
+    P3, _ = O.threshold_components(Phi, None)
+    assert P3 is Phi
+
+
+@pytest.mark.parametrize("shape", [(24, 40), (40, 24)])
+def test_dct_keep_all_equals_identity_transform(shape):
+    """T orthogonal and nothing thresholded: T^T H(T G T^T) T = H(G), so the DCT variant
+    reduces to plain Alg. 1 at a fixed Lambda."""
+    X = np.random.default_rng(9).standard_normal(shape)
+    m, n = shape
+    kern = O.Kernel(kind="soft", tau=0.3, tau_relative=True)
+    lam = 1.01 * float(np.linalg.eigvalsh(X @ X.T if m <= n else X.T @ X)[-1])
+    Yd = O.cpa_shrink_transform(X, kern, 10, lam=lam, transform="dct")
+    Yi = O.cpa_shrink(X, kern, 10, lam=lam)
+    assert O.rel_fro(Yd, Yi) <= 1e-12
+
+
+def test_dct_thresholded_is_exact_shrink_of_the_thresholded_gram():
+    """With components thresholded the method is Alg. 1 on Phi_ exactly: its result equals
+    T^T H_hat(Phi_) T applied to B, where H_hat(Phi_) is evaluated spectrally (eigh of Phi_,
+    the series at each eigenvalue) -- an independent route to the same quantity."""
+    X = np.random.default_rng(4).standard_normal((30, 50))
+    kern = O.Kernel(kind="hard", tau=0.4, tau_relative=True)
+    K = 11
+    Y, info = O.cpa_shrink_transform(X, kern, K, T=200, return_info=True, transform="dct",
+                                      eps_mode="topk", eps=120)
+    Tm = O.dct2_matrix(30)
+    Phi_, _ = O.threshold_components(Tm @ (X @ X.T) @ Tm.T, "topk", 120)
+    w, V = np.linalg.eigh(Phi_)
+    hh = np.array([O.series_eval(info["coeffs"], info["lambda_max"], x) for x in w])
+    H = (V * hh) @ V.T
+    assert O.rel_fro(Y, Tm.T @ H @ Tm @ X) <= 1e-11
+    assert info["nnz"] >= 120
