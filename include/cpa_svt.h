@@ -184,6 +184,12 @@ cpa_svt_status cpa_svt_apply_batched(cpa_svt_handle* h, int64_t batch, int m, in
                                      const float* X, float* Y, const cpa_svt_kernel* k, int K,
                                      const cpa_svt_lambda* lam, float* lambda_out);
 
+/* NEXT-2 component threshold of Alg. 1 line 2 (eq. threshold_components) for
+ * CPA_SVT_OPT_TRANSFORM = 2 (DCT): mode 0 keeps every component; 1 keeps |Phi_ij| >= value;
+ * 2 keeps |Phi_ij| >= the value-th largest |Phi_ij| (ties kept; value >= 1).
+ * Errors: E_ARG (null, mode), E_DOMAIN (value < 0, or < 1 for mode 2). */
+cpa_svt_status cpa_svt_set_epsilon(cpa_svt_handle* h, int mode, double value);
+
 /* NEXT-3: the paper's ADMM recovery with CPA shrinkage as the nuclear-norm prox
  * (eq. admm_algorithm_inp; synthetic experiment
  * PAPER.md:1095-1100 without the average-term constraint):
@@ -220,8 +226,11 @@ typedef enum {
   CPA_SVT_OPT_TRANSFORM = 1 /* NEXT-2, Alg. 1 line 1-2 with a sparsifying transform (PAPER.md:320-352,
                                628-630): 0 = T = I (default); 1 = one-level Haar DWT of the Gram index
                                with the high-frequency components of Phi set to 0 -- Alg. 1 then runs
-                               on the low-pass half and line 12 applies B T^T H_hat(Phi_) T.  fp64
-                               dense, unsharded only (else CPA_SVT_E_UNSUPPORTED). */,
+                               on the low-pass half and line 12 applies B T^T H_hat(Phi_) T; 2 =
+                               orthonormal DCT-II of the Gram index, Phi = T G T^T thresholded per
+                               cpa_svt_set_epsilon, the recurrence on the sparse Phi_ (CSR) when a
+                               threshold is set.  fp64 dense, unsharded only (else
+                               CPA_SVT_E_UNSUPPORTED). */,
   CPA_SVT_OPT_BATCHED = 2   /* engine of cpa_svt_apply_batched: 0 = auto (tcgen05), 1 = fp32 FFMA (exact
                                fp32 products, apply-to-X form), 2 = tcgen05 3xTF32 (s x s form,
                                M = N = 64 MMAs, TMEM accumulators). */

@@ -88,6 +88,8 @@ PHASES = ["gram", "allreduce", "power", "init", "step", "sparse_z", "sparse_w", 
 lib.cpa_svt_set_option.argtypes = [_p, ctypes.c_int, _i64]
 lib.cpa_svt_admm_recover.argtypes = [_p, _i64, _i64, _p, _p, ctypes.c_int, ctypes.POINTER(Lambda), ctypes.POINTER(Admm), _p]
 lib.cpa_svt_admm_recover.restype = ctypes.c_int
+lib.cpa_svt_set_epsilon.argtypes = [_p, ctypes.c_int, ctypes.c_double]
+lib.cpa_svt_set_epsilon.restype = ctypes.c_int
 lib.cpa_svt_set_option.restype = ctypes.c_int
 FORM = {"auto": 0, "apply": 1, "poly": 2, "poly_full": 3}
 for _f in ("cpa_svt_init", "cpa_svt_free", "cpa_svt_nccl_unique_id", "cpa_svt_coeffs", "cpa_svt_apply",
@@ -167,7 +169,13 @@ class Handle:
     def set_transform(self, transform: str):
         """cpa_svt_set_option(TRANSFORM): 'none' (T = I) | 'haar1' (one-level Haar DWT of the Gram
         index, high-frequency components of Phi set to 0; NEXT-2)."""
-        self._check(lib.cpa_svt_set_option(self._h, 1, {"none": 0, "haar1": 1}[transform]), "cpa_svt_set_option")
+        self._check(lib.cpa_svt_set_option(self._h, 1, {"none": 0, "haar1": 1, "dct": 2}[transform]),
+                    "cpa_svt_set_option")
+
+    def set_epsilon(self, mode: str = "none", value: float = 0.0):
+        """cpa_svt_set_epsilon: 'none' | 'abs' (keep |Phi_ij| >= value) | 'topk' (keep the value largest)."""
+        st = lib.cpa_svt_set_epsilon(self._h, {"none": 0, "abs": 1, "topk": 2}[mode], float(value))
+        self._check(st, "cpa_svt_set_epsilon")
 
     def profile(self, enable: bool = True):
         """cpa_svt_profile: reset and start (or stop) per-phase CUDA-event timing."""

@@ -7,7 +7,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcpasvt.so")
-SOURCES = ["api.cu", "dense_f64.cu", "power.cu", "batched_f32.cu", "batched_tc.cu", "sparse_f64.cu", "tc_tf32.cu", "admm.cu"]
+SOURCES = ["api.cu", "dense_f64.cu", "power.cu", "batched_f32.cu", "batched_tc.cu", "sparse_f64.cu", "tc_tf32.cu", "admm.cu", "transform.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"), "--expt-relaxed-constexpr"]

@@ -30,6 +30,13 @@ cudaError_t dense_gemm_store(int64_t M, int64_t N, int64_t Kd, const double* A, 
                              int64_t ldb, double* C, int64_t ldc, cudaStream_t st, double* partial = nullptr,
                              int* tcount = nullptr);
 size_t dense_store_partial_doubles(int64_t M, int64_t N);
+// transform.cu
+size_t dct_eps_scratch_bytes(int64_t s);
+cudaError_t dct_eps_threshold(double* Phi, int64_t s, int mode, double eps_value, void* scratch, int num_sms,
+                              cudaStream_t st, const int64_t** rp_out, const int32_t** col_out,
+                              const double** val_out);
+cudaError_t dct_sparse_steps(int64_t s, const int64_t* rp, const int32_t* col, const double* val, double* Wa,
+                             double* Wb, double* H, const SeriesParams* P, int K, int num_sms, cudaStream_t st);
 // admm.cu
 cudaError_t admm_dct(double* C, double* CT, int64_t n, int num_sms, cudaStream_t st);
 cudaError_t admm_sub(const double* a, const double* b, double* out, int64_t N, cudaStream_t st);
@@ -143,6 +150,8 @@ struct cpa_svt_handle {
   size_t aws_bytes = 0;
   size_t tws_bytes = 0;
   int transform = 0;               // CPA_SVT_OPT_TRANSFORM
+  int eps_mode = 0;                // cpa_svt_set_epsilon: 0 keep all, 1 absolute, 2 top-k
+  double eps_value = 0.0;
   int batched_engine = 0;          // CPA_SVT_OPT_BATCHED: 0 auto (tensor cores), 1 FFMA, 2 tcgen05
   size_t hx_bytes = 0;
   std::string err;
@@ -351,7 +360,7 @@ cpa_svt_status cpa_svt_set_option(cpa_svt_handle* h, cpa_svt_option opt, int64_t
     return CPA_SVT_OK;
   }
   if (opt == CPA_SVT_OPT_TRANSFORM) {
-    if (value < 0 || value > 1) return CPA_SVT_E_ARG;
+    if (value < 0 || value > 2) return CPA_SVT_E_ARG;
     h->transform = (int)value;
     return CPA_SVT_OK;
   }
@@ -361,6 +370,14 @@ cpa_svt_status cpa_svt_set_option(cpa_svt_handle* h, cpa_svt_option opt, int64_t
     return CPA_SVT_OK;
   }
   return CPA_SVT_E_ARG;
+}
+
+cpa_svt_status cpa_svt_set_epsilon(cpa_svt_handle* h, int mode, double value) {
+  if (!h || mode < 0 || mode > 2) return CPA_SVT_E_ARG;
+  if (!(value >= 0.0) || (mode == 2 && !(value >= 1.0))) return CPA_SVT_E_DOMAIN;
+  h->eps_mode = mode;
+  h->eps_value = value;
+  return CPA_SVT_OK;
 }
 
 cpa_svt_status cpa_svt_profile(cpa_svt_handle* h, int enable) {
@@ -563,7 +580,10 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
   }
   const int64_t s = left ? m : n, L = left ? n : m;
   const bool sharded = shard != CPA_SVT_SHARD_NONE && h->world > 1;
-  const int form = dense_form(h, s, L, K);
+  const bool dct = h->transform == 2;      // NEXT-2 DCT variant (Phi = C G C^T, thresholded)
+  const bool sparse_eps = dct && h->eps_mode != 0;
+  if (dct && sharded) return CPA_SVT_E_UNSUPPORTED;
+  const int form = dct ? 2 : dense_form(h, s, L, K);
   const bool poly = form != 1;
   // workspace: G (s*s) | W_a | W_b | [I_s | H (s*s) in the poly forms] | power scratch | split-K partials | sync
   // (G^2 and G^4 for the squared power iteration live in W_a / W_b: free until the recurrence)
@@ -609,6 +629,29 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
     NC(g_nccl.AllReduce(G, G, nG, ncclDouble, ncclSum, h->comm, h->stream));
   }
   tm.mark();
+  // NEXT-2 DCT variant, Alg. 1 lines 1-2: Phi = C G C^T (two DMMA products), then the
+  // component threshold into a CSR copy; G holds Phi_ from here on
+  double *Cd = nullptr, *CTd = nullptr;
+  const int64_t* csr_rp = nullptr;
+  const int32_t* csr_col = nullptr;
+  const double* csr_val = nullptr;
+  if (dct) {
+    const size_t nS = r32((size_t)s * s);
+    st = grow(h, &h->tws, &h->tws_bytes, 2 * nS * sizeof(double) + (sparse_eps ? dct_eps_scratch_bytes(s) : 0) + 512);
+    if (st != CPA_SVT_OK) return st;
+    Cd = (double*)h->tws;
+    CTd = Cd + nS;
+    Phase p(h, CPA_SVT_PH_GRAM);
+    CU(admm_dct(Cd, CTd, s, h->num_sms, h->stream));
+    CU(dense_gemm_store(s, s, s, Cd, s, G, s, Wa, s, h->stream));    // C G
+    CU(dense_gemm_store(s, s, s, Wa, s, CTd, s, G, s, h->stream));   // (C G) C^T
+    launches += 3;
+    if (sparse_eps) {
+      CU(dct_eps_threshold(G, s, h->eps_mode, h->eps_value, (void*)(CTd + nS), h->num_sms, h->stream, &csr_rp,
+                           &csr_col, &csr_val));
+      launches += 5;
+    }
+  }
   // Alg. 1 lines 3-4: Lambda_max and coefficients, on the device
   if (lam->lambda_max > 0.0) {
     Phase p(h, CPA_SVT_PH_POWER);
@@ -652,8 +695,13 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
       }
       if (K > 2) {
         Phase p(h, CPA_SVT_PH_STEP);
-        CU(dense_cheb_sym(s, G, Is, Wa, Wb, H, h->P, K, flow_sync, part, h->num_sms, h->stream));  // Is: 3rd W buffer
-        ++launches;
+        if (sparse_eps) {  // lines 8-11 on the sparse Phi_ (one launch per step)
+          CU(dct_sparse_steps(s, csr_rp, csr_col, csr_val, Wa, Wb, H, h->P, K, h->num_sms, h->stream));
+          launches += K - 2;
+        } else {
+          CU(dense_cheb_sym(s, G, Is, Wa, Wb, H, h->P, K, flow_sync, part, h->num_sms, h->stream));  // Is: 3rd W buffer
+          ++launches;
+        }
       }
     } else {
       CU(dense_eye(Is, s, h->stream));
@@ -663,8 +711,15 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
     }
     Phase p(h, CPA_SVT_PH_FINAL);
     // (split-K for this product measured slower at c2: 96 vs 91 us -- not used)
-    if (left) CU(dense_gemm_store(s, n, s, H, s, X, ldx, Y, ldy, h->stream));
-    else      CU(dense_gemm_store(m, s, s, X, ldx, H, s, Y, ldy, h->stream));
+    const double* Hm = H;
+    if (dct) {  // line 12 with T: Y = (C^T H C) X  or  X (C^T H C)
+      CU(dense_gemm_store(s, s, s, CTd, s, H, s, Wa, s, h->stream));
+      CU(dense_gemm_store(s, s, s, Wa, s, Cd, s, Wb, s, h->stream));
+      launches += 2;
+      Hm = Wb;
+    }
+    if (left) CU(dense_gemm_store(s, n, s, Hm, s, X, ldx, Y, ldy, h->stream));
+    else      CU(dense_gemm_store(m, s, s, X, ldx, Hm, s, Y, ldy, h->stream));
     ++launches;
   }
   tm.mark();

@@ -58,3 +58,55 @@ def test_transform_unsupported_paths(env):
     with pytest.raises(P.CpaSvtError) as e:
         h.apply(X, {"kind": "soft", "tau": 1.0}, 5, math="3xtf32")
     assert e.value.status == 7
+
+
+# ---- DCT variant with component thresholding
+
+def _gap_k(X, target, rel=1e-6):
+    """A k near `target` where the k-th and (k+1)-th largest |Phi_ij| differ by more than `rel`
+    relative: the kept set is then the same on both sides whatever the rounding of Phi."""
+    m, n = X.shape
+    B = X.T if m <= n else X
+    Tm = O.dct2_matrix(B.shape[1])
+    a = np.sort(np.abs(Tm @ (B.T @ B) @ Tm.T).ravel())[::-1]
+    for d in range(0, a.size):
+        for k in (target + d, target - d):
+            if 1 <= k < a.size and a[k - 1] > a[k] * (1 + rel):
+                return k
+    raise AssertionError("no gap")
+
+
+@pytest.fixture(scope="module")
+def dct_env():
+    import torch
+    import paper_1705_07112_b200 as P
+    h = P.Handle(0)
+    h.set_transform("dct")
+    yield torch, P, h
+    h.close()
+
+
+@pytest.mark.parametrize("shape", [(64, 128), (130, 70), (7, 9), (257, 300)])
+@pytest.mark.parametrize("eps", [("none", 0), ("abs", 0.5), ("topk", 0.02), ("topk", 0.3)])
+@pytest.mark.parametrize("kind,K", [("soft", 2), ("soft", 15), ("hard", 6)])
+def test_dct_parity(dct_env, shape, eps, kind, K):
+    torch, P, h = dct_env
+    X = W.gen_c2(m=shape[0], n=shape[1], seed=shape[0] * 3 + shape[1] + K)
+    mode, val = eps
+    if mode == "topk":
+        s = min(shape)
+        val = _gap_k(X, max(1, int(val * s * s)))
+    if mode == "abs":   # an absolute epsilon in a gap of |Phi|
+        m, n = X.shape
+        B = X.T if m <= n else X
+        Tm = O.dct2_matrix(B.shape[1])
+        a = np.sort(np.abs(Tm @ (B.T @ B) @ Tm.T).ravel())[::-1]
+        k = _gap_k(X, max(1, a.size // 10))
+        val = 0.5 * (a[k - 1] + a[k])
+    h.set_epsilon(mode, val)
+    kern = {"kind": kind, "tau": 0.1, "tau_relative": True}
+    Y, info = h.apply(torch.from_numpy(X).cuda(), kern, K, T=200, info=True)
+    Yo, io = O.cpa_shrink_transform(X, O.Kernel(**kern), K, T=200, return_info=True, transform="dct",
+                                    eps_mode=None if mode == "none" else mode, eps=val)
+    assert abs(info["lambda_hat"] - io["lambda_hat"]) <= 1e-11 * io["lambda_hat"]
+    assert O.rel_fro(Y.cpu().numpy(), Yo) <= TOL64, (shape, eps, kind, K)

@@ -16,18 +16,25 @@ X = torch.from_numpy(W.gen_pinpaint()).cuda()
 kern = {"kind": "soft", "tau": 6.0, "tau_relative": False}
 K, T = 20, 300
 out = {"shape": list(X.shape), "K": K, "T": T, "tau": 6.0}
-for tr in ("none", "haar1"):
+s_ = min(X.shape)
+variants = [("none", None, 0), ("haar1", None, 0), ("dct", None, 0)]
+# the paper's top-k thresholds k1..k3 = (0.5e-4, 1.5e-4, 0.5e-3) n^2, n = Gram side
+for name, frac in (("k1", 0.5e-4), ("k2", 1.5e-4), ("k3", 0.5e-3)):
+    variants.append((f"dct_{name}", "topk", max(1, int(frac * s_ * s_))))
+Ys = {}
+for name, mode, val in variants:
     h = P.Handle(0)
-    h.set_transform(tr)
+    h.set_transform(name.split("_")[0])
+    if mode:
+        h.set_epsilon(mode, val)
     Y = torch.empty_like(X)
     ms, _ = timed(lambda: h.apply(X, kern, K, T=T, Y=Y), 5)
-    out[f"ms_cpa_{tr}"] = ms
-    out[f"Y_{tr}"] = Y.clone()
+    out[f"ms_cpa_{name}"] = ms
+    Ys[name] = Y.clone()
     h.close()
 ms_e, Ye = timed(lambda: exact_evd(X, 6.0), 3)
 out["ms_evd_exact"] = ms_e
-for tr in ("none", "haar1"):
-    Y = out.pop(f"Y_{tr}")
-    out[f"rel_fro_vs_exact_{tr}"] = float(torch.linalg.norm(Y - Ye) / torch.linalg.norm(Ye))
+for name, Y in Ys.items():
+    out[f"rel_fro_vs_exact_{name}"] = float(torch.linalg.norm(Y - Ye) / torch.linalg.norm(Ye))
 out["paper_cpu_s"] = {"cpa_alpha20_dwt": 2.00, "evd": 2.48, "source": "PAPER.md:750 (Table I), Xeon E5-2667, MATLAB"}
 print(json.dumps(out))
