@@ -241,10 +241,12 @@ __global__ void __launch_bounds__(NT, 1) k_batched_tc(Args a) {
   uint8_t* sAT = base + 4 * OPB;      // A^T (B operand of line 12)
   __shared__ uint64_t bar;
   __shared__ uint32_t tslot;
-  __shared__ float sV[64];
+  __shared__ float sV2[2][64];
+  __shared__ float sRed2[2][4];
   __shared__ float sRed[4];
-  __shared__ double sHn[CPA_SVT_KMAX];
-  __shared__ float sC[CPA_SVT_KMAX];
+  __shared__ double sNode[128];   // K <= 128 on the batched path (cpa_svt_apply_batched)
+  __shared__ double sHn[128];
+  __shared__ float sC[128];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int q = lane & 3;
@@ -272,6 +274,8 @@ __global__ void __launch_bounds__(NT, 1) k_batched_tc(Args a) {
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tD = tslot, tAh = tslot + 64, tAl = tslot + 128;   // D, A operand (hi, lo)
   uint32_t phase = 0;
+  // Chebyshev-Gauss nodes x_l / Lambda = (cos theta_l + 1) / 2, once per CTA
+  for (int l = tid; l < K; l += NT) sNode[l] = 0.5 * (cos(cheb_theta(l + 1, K)) + 1.0);
 
   for (int64_t b = blockIdx.x; b < a.batch; b += gridDim.x) {
     const float* X = a.X + b * mn;
@@ -349,16 +353,19 @@ __global__ void __launch_bounds__(NT, 1) k_batched_tc(Args a) {
           __syncthreads();                             // everyone has read D and the operands
         }
       }
-      if (tid < 64) sV[tid] = tid < s ? rsqrtf((float)s) : 0.f;
+      // one CTA barrier per product: u_t = G v_{t-1} with v_{t-1} = u_{t-1} / ||u_{t-1}|| folded
+      // in as a scale of the product; u_t and the partial ||u_t||^2 go to ping-pong buffers
+      if (tid < 64) sV2[0][tid] = tid < s ? rsqrtf((float)s) : 0.f;
       __syncthreads();
-      float nrm = 0.f;
+      float nrm = 0.f, inv = 1.f;
       const int niter = a.T - 3 * qsq;
       for (int t = 0; t < niter; ++t) {
         const bool use4 = t < qsq;
+        const float* vin = sV2[t & 1];
         float u0a = 0.f, u0b = 0.f, u1a = 0.f, u1b = 0.f;   // row0 / row1 partial sums (2 chains each)
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-          const float v0 = sV[8 * c + 2 * q], v1 = sV[8 * c + 2 * q + 1];
+          const float v0 = vin[8 * c + 2 * q], v1 = vin[8 * c + 2 * q + 1];
           u0a = fmaf(use4 ? g4[4 * c + 0] : g[4 * c + 0], v0, u0a);
           u0b = fmaf(use4 ? g4[4 * c + 1] : g[4 * c + 1], v1, u0b);
           u1a = fmaf(use4 ? g4[4 * c + 2] : g[4 * c + 2], v0, u1a);
@@ -369,18 +376,21 @@ __global__ void __launch_bounds__(NT, 1) k_batched_tc(Args a) {
         u1 += __shfl_xor_sync(0xffffffffu, u1, 1);
         u0 += __shfl_xor_sync(0xffffffffu, u0, 2);
         u1 += __shfl_xor_sync(0xffffffffu, u1, 2);
+        u0 *= inv;
+        u1 *= inv;
         float sq = q == 0 ? u0 * u0 + u1 * u1 : 0.f;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-        if (lane == 0) sRed[warp] = sq;
-        __syncthreads();
-        nrm = sqrtf((sRed[0] + sRed[1]) + (sRed[2] + sRed[3]));
-        if (!(nrm > 0.f)) break;
+        if (lane == 0) sRed2[t & 1][warp] = sq;
         if (q == 0) {
-          sV[row0] = u0 / nrm;
-          sV[row1] = u1 / nrm;
+          sV2[(t + 1) & 1][row0] = u0;
+          sV2[(t + 1) & 1][row1] = u1;
         }
         __syncthreads();
+        const float* rd = sRed2[t & 1];
+        nrm = sqrtf((rd[0] + rd[1]) + (rd[2] + rd[3]));
+        if (!(nrm > 0.f)) break;
+        inv = 1.f / nrm;
       }
       lam_hat = nrm > 0.f ? (double)nrm : 0.0;
     }
@@ -388,13 +398,19 @@ __global__ void __launch_bounds__(NT, 1) k_batched_tc(Args a) {
     const bool degen = !(lam_hat > kDegenerateLambda);
     const double lam = a.safety * lam_hat;
     const double tau = resolve_tau(a.kern, sqrt(lam_hat));
-    for (int l = tid; l < K; l += NT) sHn[l] = h_response(a.kern, lam / 2.0 * (cos(cheb_theta(l + 1, K)) + 1.0), tau);
+    for (int l = tid; l < K; l += NT) sHn[l] = h_response(a.kern, lam * sNode[l], tau);
     __syncthreads();
-    for (int k = tid; k < K; k += NT) {
+    // c_k = (2/K) sum_l cos(k theta_l) h_l: 4 threads per k (residues of l mod 4), fixed-order reduction
+    for (int k0 = 0; k0 < K; k0 += NT / 4) {
+      const int k = k0 + (tid >> 2), r = tid & 3;
       double acc_c = 0.0;
-      const double* ct = a.costab + k * K;
-      for (int l = 0; l < K; ++l) acc_c += __ldg(ct + l) * sHn[l];
-      sC[k] = degen ? 0.f : (float)(2.0 / K * acc_c);
+      if (k < K) {
+        const double* ct = a.costab + (int64_t)k * K;
+        for (int l = r; l < K; l += 4) acc_c = fma(__ldg(ct + l), sHn[l], acc_c);
+      }
+      acc_c += __shfl_xor_sync(0xffffffffu, acc_c, 1);
+      acc_c += __shfl_xor_sync(0xffffffffu, acc_c, 2);
+      if (k < K && r == 0) sC[k] = degen ? 0.f : (float)(2.0 / K * acc_c);
     }
     __syncthreads();
     if (tid == 0 && a.lambda_out) a.lambda_out[b] = (float)lam;
@@ -472,7 +488,7 @@ __global__ void k_costab(double* tab, int K);
 cudaError_t launch_batched_tc(int64_t batch, int m, int n, const float* X, float* Y, const cpa_svt_kernel& k, int K,
                               int T, double safety, double lam_override, float* lambda_out, int num_sms,
                               cudaStream_t st, int* launches, double* costab) {
-  if (K > CPA_SVT_KMAX) return cudaErrorNotSupported;
+  if (K > 128) return cudaErrorNotSupported;
   k_costab<<<(K * K + 255) / 256, 256, 0, st>>>(costab, K);
   if (launches) ++*launches;
   btc::Args a{batch, m, n, X, Y, k, K, T, safety, lam_override, lambda_out, costab};
