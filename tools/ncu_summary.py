@@ -34,7 +34,10 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active", "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
         "smsp__issue_active.avg.pct_of_peak_sustained_active", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
-        "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"]
+        "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+        "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+        "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+        "sm__inst_executed_pipe_tmem.avg.pct_of_peak_sustained_active", "lts__t_bytes.sum"]
 
 
 def report(path):
@@ -46,8 +49,9 @@ def report(path):
         name = d[h.index("Kernel Name")] if "Kernel Name" in h else "?"
         out.append(f"== {name[:100]}")
         for k in KEYS:
-            if k in h:
-                i = h.index(k)
+            hk = [x for x in h if x == k or x.endswith("." + k)]
+            if hk:
+                i = h.index(hk[0])
                 out.append(f"   {k:80s} {d[i]:>14s} {units[i]}")
         st = []
         for i, k in enumerate(h):
