@@ -44,8 +44,13 @@ constexpr int UK = 8;           // UMMA K for kind::tf32
 // Warps: 0 TMA producer, 1 TMEM allocator + MMA issuer, 2..5 drain, 6..9 epilogue.
 constexpr int NTHR = 320;
 constexpr int CHUNK_KB_DEFAULT = 8;    // k-blocks (x BK = 32) per TMEM accumulation
-constexpr int NACC = 2;                // chunk accumulators (TMEM columns [0, 2 BN))
-constexpr int NSUM = 2;                // tile sums (TMEM columns [2 BN, 4 BN))
+// TMEM buffers: 128-column tiles use 2 chunk accumulators + 2 tile sums (512 columns); 256-column
+// tiles (single-pass TF32: the whole K in one accumulator, 25% less operand traffic per flop on
+// the L2-bound steps) use 1 + 1 -- the drain of a whole-K accumulator is a one-off copy.
+template <int BN> struct Bufs {
+  static constexpr int NACC = BN == 128 ? 2 : 1;
+  static constexpr int NSUM = BN == 128 ? 2 : 1;
+};
 
 enum Mode { GRAM = 0, INIT = 1, STEP = 2 };
 
@@ -210,6 +215,7 @@ __global__ void __launch_bounds__(NTHR, 1)
               const __grid_constant__ CUtensorMap tmB_h, const __grid_constant__ CUtensorMap tmB_l, TcArgs a) {
   using S = Smem<BN, TERMS, B_MN>;
   constexpr int ST = S::STAGES;
+  constexpr int NACC = Bufs<BN>::NACC, NSUM = Bufs<BN>::NSUM;
   constexpr int NSPLIT = TERMS == 3 ? 2 : 1;
   extern __shared__ uint8_t raw_smem[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)raw_smem + 1023) & ~(uintptr_t)1023);
@@ -529,25 +535,26 @@ static cudaError_t launch_t(const CUtensorMap& ah, const CUtensorMap& al, const 
 
 // Lower-triangle tile list (tm >= tn) of a T x T tile grid in the grouped-M raster
 // order of tile_coords; built once per T and kept on the device.
-static const int2* sym_tile_list(int T, int* count) {
-  static std::map<int, std::pair<int2*, int>> cache;
-  auto it = cache.find(T);
+static const int2* sym_tile_list(int tiles_m, int tiles_n, int bm, int bn, int* count) {
+  static std::map<long long, std::pair<int2*, int>> cache;
+  const long long key = ((long long)tiles_m << 40) | ((long long)tiles_n << 16) | (bn << 1) | (bm == 128);
+  auto it = cache.find(key);
   if (it != cache.end()) {
     *count = it->second.second;
     return it->second.first;
   }
   std::vector<int2> v;
   constexpr int GROUP = 16;
-  for (int first = 0; first < T; first += GROUP) {
-    const int gsize = std::min(GROUP, T - first);
-    for (int tn = 0; tn < T; ++tn)
+  for (int first = 0; first < tiles_m; first += GROUP) {
+    const int gsize = std::min(GROUP, tiles_m - first);
+    for (int tn = 0; tn < tiles_n; ++tn)
       for (int r = 0; r < gsize; ++r)
-        if (first + r >= tn) v.push_back(make_int2(first + r, tn));
+        if ((int64_t)(first + r) * bm + bm - 1 >= (int64_t)tn * bn) v.push_back(make_int2(first + r, tn));
   }
   int2* d = nullptr;
   if (cudaMalloc(&d, v.size() * sizeof(int2)) != cudaSuccess) return nullptr;
   if (cudaMemcpy(d, v.data(), v.size() * sizeof(int2), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
-  cache[T] = {d, (int)v.size()};
+  cache[key] = {d, (int)v.size()};
   *count = (int)v.size();
   return d;
 }
@@ -577,13 +584,15 @@ static cudaError_t tc_gemm_bn(int mode, int terms, int M, int N, int Kd, const f
   a.tiles_m = (M + BM - 1) / BM;
   a.tiles_n = (N + BN - 1) / BN;
   if (sym) {
-    if (M != N || BN != BM) return cudaErrorInvalidValue;
+    if (M != N) return cudaErrorInvalidValue;
     a.sym = 1;
     a.mirror_f = mode == GRAM;
-    a.tile_list = sym_tile_list(a.tiles_m, &a.ntiles_list);
+    a.tile_list = sym_tile_list(a.tiles_m, a.tiles_n, BM, BN, &a.ntiles_list);
     if (!a.tile_list) return cudaErrorMemoryAllocation;
   }
-  a.chunk_kb = CHUNK_KB_DEFAULT;
+  // 256-wide tiles have one accumulator: the whole K for single-pass TF32, 16 k-blocks (K = 512)
+  // for 3xTF32 (the MMA waits for each drain -- a short bubble against 3x the MMA work)
+  a.chunk_kb = BN == 256 ? (terms == 1 ? (Kd + BK - 1) / BK : 16) : CHUNK_KB_DEFAULT;
   if (const char* v = getenv("CPA_SVT_TC_CHUNK")) a.chunk_kb = atoi(v) > 0 ? atoi(v) : a.chunk_kb;
   if (const char* v = getenv("CPA_SVT_DBG_LBO")) a.dbg_lbo = atoi(v);
   if (const char* v = getenv("CPA_SVT_DBG_SBO")) a.dbg_sbo = atoi(v);
@@ -605,6 +614,17 @@ cudaError_t tc_gemm(int mode, int terms, int M, int N, int Kd, const float* Ah, 
                     const float* Bh, const float* Bl, int64_t ldb, bool b_mn, float* out_f, float* out_h,
                     float* out_l, int out_split, int64_t ld_out, const float* wp, const float* wpp, int64_t ld_w,
                     float* y, int64_t ld_y, const SeriesParams* P, int k, int num_sms, cudaStream_t st, int sym) {
+  // single-pass TF32 recurrence and line-12 products: 128 x 256 tiles (B MN-major); the
+  // 3xTF32 products and the Gram keep 128 x 128 tiles with chunked accumulation
+  int wide = terms == 1 && mode != 0 && b_mn;
+  if (mode == 0 && terms == 1 && b_mn && !sym) wide = 1;
+  // 3xTF32: the line-12 product gains from 256-wide tiles (213 -> 159 ms at c5), the steps do not
+  // (950 -> 989 ms: one accumulator means the MMA waits for every chunk drain)
+  if (terms == 3 && mode == 0 && !sym && b_mn) wide = 1;
+  if (const char* v = getenv("CPA_SVT_TC_WIDE")) wide = wide && atoi(v) != 0;
+  if (wide)
+    return tc::tc_gemm_bn<256>(mode, terms, M, N, Kd, Ah, Al, lda, Bh, Bl, ldb, b_mn, out_f, out_h, out_l, out_split,
+                               ld_out, wp, wpp, ld_w, y, ld_y, P, k, num_sms, st, sym);
   return tc::tc_gemm_bn<128>(mode, terms, M, N, Kd, Ah, Al, lda, Bh, Bl, ldb, b_mn, out_f, out_h, out_l, out_split,
                              ld_out, wp, wpp, ld_w, y, ld_y, P, k, num_sms, st, sym);
 }
