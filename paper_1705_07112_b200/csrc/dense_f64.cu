@@ -11,6 +11,7 @@
 //
 // CTA tile 64x64, k-slab 16, 4 warps of 32x32 (4x4 DMMA tiles), 4-stage
 // cp.async pipeline (16-byte copies when the leading dimension allows).
+#include <cooperative_groups.h>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -598,6 +599,107 @@ __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB) k_cheb_sym(SymArgs a)
   }
 }
 
+// Cluster variant of k_cheb_sym for small s (c2): the CS k-splits of a tile run as one
+// thread-block cluster and reduce through distributed shared memory instead of L2 partial
+// buffers and a single reducer.  Each CTA stores its partial accumulators in its own shared
+// memory; after a cluster barrier CTA q sums warp-tile q (32 x 32) of all CS partials in the
+// fixed order r = 0..CS-1 and runs the fused epilogue for that quarter of the tile -- every CTA
+// of the cluster shares the epilogue, so the tile's reduction latency on the dataflow's
+// critical path is one DSMEM round trip.  Tickets are per tile (claimed by the leader CTA);
+// the dependency rule and the three-buffer rotation are those of k_cheb_sym.
+template <int CS>
+__global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(NTHREADS, CPA_FLOW_MINB) k_cheb_sym_cl(SymArgs a) {
+  namespace cg = cooperative_groups;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ int s_ticket;
+  cg::cluster_group cl = cg::this_cluster();
+  const int q = (int)cl.block_rank();
+  const int T = a.T;
+  const int ntri = T * (T + 1) / 2;
+  const int total = (a.K - 2) * ntri;
+  int* cross = a.sync + 1;
+  const int64_t s = a.s;
+  const int nk = (int)((s + BKS - 1) / BKS);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kb = (int)((int64_t)nk * q / CS), ke = (int)((int64_t)nk * (q + 1) / CS);
+  for (;;) {
+    // the leader claims the tile's ticket and writes it into every CTA's own shared memory
+    // (no CTA reads a peer's shared memory after the last barrier: safe exit)
+    if (q == 0 && threadIdx.x == 0) {
+      const int t0 = atomicAdd(a.sync, 1);
+#pragma unroll
+      for (int r = 0; r < CS; ++r) *cl.map_shared_rank(&s_ticket, r) = t0;
+    }
+    cl.sync();
+    const int tk = s_ticket;
+    if (tk >= total) break;
+    const int k = 2 + tk / ntri;
+    const int tile = tk % ntri;
+    int ti, tj;
+    tri_decode_colmajor(tile, T, ti, tj);
+    auto buf = [&](int i) { return i == 0 ? a.W[0] : (i == 1 ? a.W[1] : a.W[2]); };
+    const double* src = buf((k - 1) % 3);   // W_{k-1}
+    const double* wpp = buf((k - 2) % 3);   // W_{k-2} (k = 2: identity, implicit)
+    double* out = buf(k % 3);               // W_k over W_{k-3}
+    const int64_t m0 = (int64_t)ti * BM, n0 = (int64_t)tj * BN;
+    double acc[4][4][2];
+    mainloop_dep(a.G, src, s, m0, n0, a.vec, smem, acc, kb, ke, [&] {
+      if (threadIdx.x == 0) {
+        if (k >= 3) wait_geq(cross + (k - 1) * T + tj, T);
+        if (k >= 4) wait_geq(cross + (k - 2) * T + ti, T);
+      }
+      __syncthreads();
+    });
+    // partial accumulators into own shared memory: [warp][reg][lane] (32 x 32 doubles per warp)
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) smem[(warp * 32 + (i * 4 + j) * 2 + e) * 32 + lane] = acc[i][j][e];
+    cl.sync();                                               // every partial written
+    // reduce-scatter: this CTA owns the values [q 4096/CS, (q+1) 4096/CS) of the tile's partial
+    // layout [warp][reg][lane]
+    const double s4 = 2.0 * a.P->scale2, ck = a.P->c[k];
+    const bool last = k == a.K - 1;
+    constexpr int PER = 4096 / CS;
+    double* peer[CS];
+#pragma unroll
+    for (int r = 0; r < CS; ++r) peer[r] = cl.map_shared_rank(smem, r) + q * PER;
+#pragma unroll
+    for (int it = 0; it < PER / NTHREADS; ++it) {
+      const int el = it * NTHREADS + threadIdx.x;
+      double v = peer[0][el];
+#pragma unroll
+      for (int r = 1; r < CS; ++r) v += peer[r][el];
+      const int e = q * PER + el;
+      const int wsrc = e >> 10, reg = (e >> 5) & 31, ln = e & 31;
+      const int ii = reg >> 3, jj = (reg >> 1) & 3, ee = reg & 1;
+      const int64_t rr = m0 + (wsrc >> 1) * 32 + ii * 8 + (ln >> 2);
+      const int64_t c = n0 + (wsrc & 1) * 32 + jj * 8 + 2 * (ln & 3) + ee;
+      if (rr < s && c <= rr) {
+        const int64_t o = rr * s + c;
+        const double vp = __ldcg(src + o);
+        const double vpp = k == 2 ? (rr == c ? 1.0 : 0.0) : __ldcg(wpp + o);
+        const double wv = s4 * v - 2.0 * vp - vpp;             // W_k = 2 B_hat W_{k-1} - W_{k-2}
+        const double y = __ldcg(a.H + o) + ck * wv;            // H += c_k W_k
+        if (!last) {
+          out[o] = wv;
+          out[c * s + rr] = wv;
+        }
+        a.H[o] = y;
+        if (last) a.H[c * s + rr] = y;
+      }
+    }
+    __threadfence();
+    cl.sync();                                               // tile complete; shared memory reusable
+    if (q == 0 && threadIdx.x == 0) {
+      red_release_add_i32(cross + k * T + ti, 1);
+      if (ti != tj) red_release_add_i32(cross + k * T + tj, 1);
+    }
+  }
+}
+
 template <bool A_KC, bool B_KC, int MODE>
 __global__ void __launch_bounds__(NTHREADS) k_dmma_gemm(GemmArgs a) {
   extern __shared__ __align__(16) double smem[];
@@ -962,6 +1064,24 @@ cudaError_t dense_cheb_sym(int64_t s, const double* G, double* W0, double* W1, d
   a.vec = aligned16(G, s) && aligned16(W0, s) && aligned16(W1, s) && aligned16(W2, s);
   cudaError_t e = cudaMemsetAsync(sync, 0, dense_sym_sync_ints(s, K, num_sms) * sizeof(int), st);
   if (e != cudaSuccess) return e;
+  int cs = 0;
+  if (const char* v = getenv("CPA_SVT_SYM_CLUSTER")) cs = atoi(v);
+  if (a.split > 1 && (cs == 2 || cs == 4 || cs == 8)) {
+    // small s: CS-CTA clusters, k-splits reduced through distributed shared memory
+    auto go = [&](auto kern, int CS) -> cudaError_t {
+      cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e2 != cudaSuccess) return e2;
+      int64_t grid = (slots / CS) * CS;
+      const int64_t tiles_total = (int64_t)(K - 2) * a.T * (a.T + 1) / 2 * CS;
+      if (grid > tiles_total) grid = tiles_total;
+      if (grid < CS) grid = CS;
+      kern<<<(unsigned)grid, NTHREADS, smem, st>>>(a);
+      return cudaGetLastError();
+    };
+    if (cs == 2) return go(k_cheb_sym_cl<2>, 2);
+    if (cs == 4) return go(k_cheb_sym_cl<4>, 4);
+    return go(k_cheb_sym_cl<8>, 8);
+  }
   const int64_t total = (int64_t)(K - 2) * a.T * (a.T + 1) / 2 * a.split;
   const int64_t grid = slots < total ? slots : total;
   void* args[] = {&a};
