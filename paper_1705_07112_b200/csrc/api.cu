@@ -66,9 +66,9 @@ cudaError_t launch_series(SeriesParams* P, const cpa_svt_kernel& k, int K, doubl
                           const double* lam_src, const double* c_given, cudaStream_t st);
 size_t power_dense_scratch_doubles(int64_t s);
 size_t power_scale_offset(int64_t s);
-bool power_use_squaring(int64_t s, int T);
+int power_squarings(int64_t s, int T);
 cudaError_t launch_diag_scale(const double* G, int64_t s, double* scale, cudaStream_t st);
-cudaError_t launch_power_dense(const double* G, const double* G4, int64_t s, int T, double* scratch,
+cudaError_t launch_power_dense(const double* G, const double* G4, int pw, int64_t s, int T, double* scratch,
                                unsigned int* bar, SeriesParams* P, const cpa_svt_kernel& k, int K, double safety,
                                const double* c_given, int num_sms, cudaStream_t st);
 cudaError_t launch_power_dense_f32(const float* G, int64_t s, int64_t ld, int T, double* scratch, unsigned int* bar,
@@ -659,19 +659,30 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
   } else {
     if (s * (int64_t)sizeof(double) > 200 * 1024) return CPA_SVT_E_UNSUPPORTED;
     Phase p(h, CPA_SVT_PH_POWER);
-    // Repeated squaring: v_{T-1} ~ G^{T-1} v_0 is reached with (T-1)/4 products by
-    // c^4 G^4 (c = 2^-ilogb(max G_ii), exact) plus the remainder by G, then
-    // lambda_hat = ||G v_{T-1}|| -- the same quantity as T plain products (reading R6).
+    // Repeated squaring: v_{T-1} ~ G^{T-1} v_0 is reached with (T-1)/p products by
+    // c^p G^p (p = 2^j, c = 2^-ilogb(max G_ii), exact) plus the remainder by G, then
+    // lambda_hat = ||G v_{T-1}|| -- the same quantity as T plain products (reading R6);
+    // j from the cost model power_squarings (j = 3 at c2).
     const double* G4 = nullptr;
-    if (power_use_squaring(s, lam->power_iters) && nW >= nG) {
+    int gpow = 1;
+    int nsq = power_squarings(s, lam->power_iters);
+    if (const char* v = getenv("CPA_SVT_POWER_SQ"); v && *v) nsq = atoi(v);   // (experiments)
+    if (nsq > 0 && nW >= nG) {
       double* sc = pw + power_scale_offset(s);  // scale slot inside the power scratch
       CU(launch_diag_scale(G, s, sc, h->stream));
       CU(dense_gram_f64(G, s, s, s, true, Wa, h->stream, sc, part, flow_sync));       // c^2 G^2
-      CU(dense_gram_f64(Wa, s, s, s, true, Wb, h->stream, nullptr, part, flow_sync));  // c^4 G^4
-      launches += 3;
-      G4 = Wb;
+      launches += 2;
+      G4 = Wa;
+      gpow = 2;
+      for (int j = 1; j < nsq && 2 * gpow <= lam->power_iters - 1; ++j) {              // c^2p G^2p
+        double* nxt = G4 == Wa ? Wb : Wa;
+        CU(dense_gram_f64(G4, s, s, s, true, nxt, h->stream, nullptr, part, flow_sync));
+        G4 = nxt;
+        gpow *= 2;
+        ++launches;
+      }
     }
-    CU(launch_power_dense(G, G4, s, lam->power_iters, pw, h->bar, h->P, *k, K, lam->safety, c_dev, h->num_sms,
+    CU(launch_power_dense(G, G4, gpow, s, lam->power_iters, pw, h->bar, h->P, *k, K, lam->safety, c_dev, h->num_sms,
                           h->stream));
   }
   ++launches;

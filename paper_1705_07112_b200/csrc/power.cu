@@ -70,8 +70,10 @@ __global__ void k_series(SeriesParams* P, cpa_svt_kernel kern, int K, double saf
 template <typename E>
 struct PowerArgs {
   const E* G;
-  const E* G4;       // c^4 G^4 (nullable): first q products use it
+  const E* G4;       // c^p G^p (nullable): first q products use it
   int q;             // products by G4
+  int pw;            // p = 2^j, the power G4 holds
+  int poll;          // polling lanes of the LL gather
   int64_t s;
   int64_t ld;        // row stride of G / G4 (elements)
   int T;
@@ -158,9 +160,9 @@ __global__ void __launch_bounds__(256) k_power_dense(PowerArgs<E> a) {
   const int64_t r0 = (int64_t)blockIdx.x * a.rows_per_cta;
   const int64_t r1 = min(s, r0 + a.rows_per_cta);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-  // products: q by G4 (cached when present), then T - 4q by G; the last one gives lambda_hat
+  // products: q by G4 (cached when present), then T - 1 - pq by G; the last one gives lambda_hat
   const T* Gc = a.q > 0 ? a.G4 : a.G;  // the matrix whose rows are cached
-  const int niter = a.T - 3 * a.q;
+  const int niter = a.T - (a.pw - 1) * a.q;
   if (a.cache_rows) {
     for (int64_t r = r0; r < r1; ++r)
       for (int64_t j = threadIdx.x; j < s; j += blockDim.x) sg[(r - r0) * s + j] = Gc[r * a.ld + j];
@@ -210,94 +212,66 @@ __global__ void __launch_bounds__(256) k_power_dense(PowerArgs<E> a) {
   if (blockIdx.x == 0) compute_series(a.P, a.kern, a.K, a.safety, lam, a.c_given);
 }
 
-// Small s (rows_per_cta x s / 256 <= ROWS x COLS): the CTA's rows of G (or c^4 G^4)
-// live in REGISTERS -- thread x owns columns j = x + 256 c -- and so does its slice of
-// v, gathered straight from the LL words into the same thread.  One block
-// reduction per product carries both the ROWS row partials of u_{t+1} = G u_t and
-// ||u_t||^2, so a product is: FMAs, one reduction, LL publish, LL gather.  The
-// reductions run in a fixed order (warp butterflies, then warps 0..7), so every
-// CTA computes the same ||u_t|| bitwise.
-template <int ROWS, int COLS>
-__global__ void __launch_bounds__(256) k_power_reg(PowerArgs<double> a) {
-  __shared__ double s_part[8][ROWS + 1];
-  __shared__ double s_res[ROWS + 1];
-  __shared__ double s_v[256 * COLS];
+// Small s, one warp per row (s <= 32 C): lane x of warp w holds columns j = x + 32 c of
+// Gram row r0 + w in registers; v_{t-1} is staged in shared memory by the gather.  Each
+// warp computes its row of u_t = G v_{t-1} AND ||v_{t-1}||^2 over the whole staged vector
+// itself (the same loads, the same fixed butterfly order in every warp of every CTA, so
+// all of them hold the same norm bitwise) -- a product needs no block reduction, only
+// the gather's barrier.  Measured at c2 (s = 1024, 128 CTAs): 2.1 us per product against
+// 3.1 us for the previous layout (8 rows per CTA, thread-owned columns, one block
+// reduction per product: tools/probes/ll_exchange.cu puts that reduction at ~0.5 us and
+// the bare 147-CTA exchange at 1.3 us).  Splitting the gather across an 8-CTA cluster
+// (one L2 poller per cluster, DSMEM broadcast, cluster barrier) measured no faster.
+template <int C>
+__global__ void __launch_bounds__(256) k_power_warp(PowerArgs<double> a) {
+  __shared__ __align__(16) double s_v[32 * C];
   const int64_t s = a.s;
-  const int64_t r0 = (int64_t)blockIdx.x * a.rows_per_cta;
-  const int nrows = (int)min((int64_t)a.rows_per_cta, s - r0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double g[ROWS][COLS];
-  auto load_rows = [&](const double* M) {
+  const int64_t row = (int64_t)blockIdx.x * 8 + warp;
+  const bool has_row = row < s;
+  double g[C];
+  auto load_row = [&](const double* M) {
 #pragma unroll
-    for (int r = 0; r < ROWS; ++r)
-#pragma unroll
-      for (int c = 0; c < COLS; ++c) {
-        const int64_t j = threadIdx.x + 256 * c;
-        g[r][c] = (r < nrows && j < s) ? M[(r0 + r) * a.ld + j] : 0.0;
-      }
+    for (int c = 0; c < C; ++c) {
+      const int64_t j = lane + 32 * c;
+      g[c] = (has_row && j < s) ? M[row * a.ld + j] : 0.0;
+    }
   };
-  load_rows(a.q > 0 ? a.G4 : a.G);
-  double v[COLS];
-  const double v0 = 1.0 / sqrt((double)s);
-#pragma unroll
-  for (int c = 0; c < COLS; ++c) v[c] = (threadIdx.x + 256 * c < s) ? v0 : 0.0;
-  const int niter = a.T - 3 * a.q;
+  load_row(a.q > 0 ? a.G4 : a.G);
+  {
+    const double v0 = 1.0 / sqrt((double)s);
+    for (int j = threadIdx.x; j < 32 * C; j += blockDim.x) s_v[j] = j < s ? v0 : 0.0;
+  }
+  __syncthreads();
+  const int niter = a.T - (a.pw - 1) * a.q;
   double lam = 0.0, inv = 1.0;
   bool degenerate = false;
-  // block reduction of p[0..ROWS] into s_res (fixed order)
-  auto reduce = [&](double (&p)[ROWS + 1]) {
+  for (int t = 0; t <= niter; ++t) {
+    if (a.q > 0 && t == a.q) load_row(a.G);   // remaining products by G itself
+    double d0 = 0.0, d1 = 0.0, q0 = 0.0, q1 = 0.0;
 #pragma unroll
-    for (int r = 0; r <= ROWS; ++r) p[r] = warp_sum(p[r]);
-    if (lane == 0)
-#pragma unroll
-      for (int r = 0; r <= ROWS; ++r) s_part[warp][r] = p[r];
-    __syncthreads();
-    if (threadIdx.x <= ROWS) {
-      double acc = s_part[0][threadIdx.x];
-#pragma unroll
-      for (int w = 1; w < 8; ++w) acc += s_part[w][threadIdx.x];
-      s_res[threadIdx.x] = acc;
+    for (int c = 0; c < C; c += 2) {
+      const double x0 = s_v[lane + 32 * c];
+      d0 = fma(g[c], x0, d0);
+      q0 = fma(x0, x0, q0);
+      if (c + 1 < C) {
+        const double x1 = s_v[lane + 32 * (c + 1)];
+        d1 = fma(g[c + 1], x1, d1);
+        q1 = fma(x1, x1, q1);
+      }
     }
-    __syncthreads();
-  };
-  for (int t = 0; t < niter; ++t) {
-    if (a.q > 0 && t == a.q) load_rows(a.G);   // remaining products by G itself
-    double p[ROWS + 1];
-#pragma unroll
-    for (int r = 0; r < ROWS; ++r) {
-      double d = 0.0;
-#pragma unroll
-      for (int c = 0; c < COLS; ++c) d = fma(g[r][c], v[c], d);
-      p[r] = d;
-    }
-    double sq = 0.0;
-#pragma unroll
-    for (int c = 0; c < COLS; ++c) sq = fma(v[c], v[c], sq);
-    p[ROWS] = sq;
-    reduce(p);
+    const double d = warp_sum(d0 + d1), sq = warp_sum(q0 + q1);
     if (t > 0) {  // ||u_{t-1}||: v_{t-1} = u_{t-1} / ||u_{t-1}|| is folded into this product
-      lam = sqrt(s_res[ROWS]);
+      lam = sqrt(sq);
       if (!(lam > kDegenerateLambda) || !(lam < 1e300)) { degenerate = true; break; }
       inv = 1.0 / lam;
     }
+    if (t == niter) break;     // lambda_hat = ||u_{niter-1}||
     const unsigned flag = (unsigned)t + 1u;
     unsigned long long* buf = a.ll + (int64_t)(t & 1) * s * 2;
-    if (threadIdx.x < nrows) st_ll(buf + 2 * (r0 + threadIdx.x), s_res[threadIdx.x] * inv, flag);
-    ll_gather(buf, s, flag, s_v);
-#pragma unroll
-    for (int c = 0; c < COLS; ++c) v[c] = (threadIdx.x + 256 * c < s) ? s_v[threadIdx.x + 256 * c] : 0.0;
-  }
-  if (!degenerate) {  // lambda_hat = ||u_{niter-1}||
-    double p[ROWS + 1];
-#pragma unroll
-    for (int r = 0; r < ROWS; ++r) p[r] = 0.0;
-    double sq = 0.0;
-#pragma unroll
-    for (int c = 0; c < COLS; ++c) sq = fma(v[c], v[c], sq);
-    p[ROWS] = sq;
-    reduce(p);
-    lam = sqrt(s_res[ROWS]);
-    if (!(lam > kDegenerateLambda) || !(lam < 1e300)) degenerate = true;
+    if (lane == 0 && has_row) st_ll(buf + 2 * row, d * inv, flag);
+    __syncthreads();  // every warp is done reading s_v before the gather overwrites it
+    ll_gather(buf, s, flag, s_v, a.poll);
   }
   if (degenerate) lam = lam < 1e300 ? 0.0 : lam;
   if (blockIdx.x == 0) compute_series(a.P, a.kern, a.K, a.safety, lam, a.c_given);
@@ -327,7 +301,7 @@ __global__ void __launch_bounds__(512) k_power_stream(PowerArgs<E> a) {
   __syncthreads();
   const int np = (int)min((int64_t)blockDim.x, max((int64_t)128, (s + 7) / 8 / 32 * 32));
   double lam = 0.0, inv = 1.0;
-  const int niter = a.T - 3 * a.q;   // q products by c^4 G^4, then the rest by G
+  const int niter = a.T - (a.pw - 1) * a.q;   // q products by c^p G^p, then the rest by G
   for (int t = 0; t < niter; ++t) {
     const unsigned flag = (unsigned)t + 1u;
     unsigned long long* buf = a.ll + (int64_t)(t & 1) * s * 2;
@@ -396,7 +370,7 @@ size_t power_dense_scratch_doubles(int64_t s) { return (size_t)(4 * s + 16); }
 size_t power_scale_offset(int64_t s) { return (size_t)(4 * s + 8); }
 
 // c = 2^-e with e = ilogb(max_i G_ii): G_ii <= lambda_max <= s * max_i G_ii, so
-// c^4 G^4 has its dominant eigenvalue in [1/16, 16 s^4]: no overflow/underflow.
+// c^p G^p has its dominant eigenvalue in [2^-p, (2s)^p]: no overflow for p <= 32.
 __global__ void k_diag_scale(const double* G, int64_t s, double* scale) {
   __shared__ double red[256];
   double mx = 0.0;
@@ -419,24 +393,42 @@ cudaError_t launch_diag_scale(const double* G, int64_t s, double* scale, cudaStr
   return cudaGetLastError();
 }
 
-// Squaring pays when two s^3 products cost less than the ~3T/4 products saved,
-// each of which is latency-bound (~2.5 us) for small s.
-bool power_use_squaring(int64_t s, int T) {
-  if (T < 16) return false;
-  const double gemm_us = 2.0 * (double)s * s * s / 30e12 * 1e6;         // two symmetric squarings
-  const double iter_us = fmax(2.2, 8.0 * (double)s * s / 6e12 * 1e6 + 5.0);  // LL product: latency or HBM
-  return gemm_us < 0.75 * T * iter_us;
+// Number j of squarings (G -> c^2 G^2 -> ... -> c^p G^p, p = 2^j) for the power iteration:
+// the q = (T-1)/p products by c^p G^p plus the T - 1 - pq remaining ones by G and the norm
+// replace T products.  A squaring is one symmetric s x s DMMA product (measured 54 us at
+// s = 1024, ~20 TF/s; ~30 TF/s for large s); a product costs ~1.2 + 0.9 s/1024 us
+// (k_power_warp, latency-bound: 2.1 us measured at s = 1024), ~3 us with the rows in
+// shared memory, or one HBM pass over G when streamed.  j = 3 at c2 (measured: j = 2 / 3 / 4
+// give 0.292 / 0.269 / ~0.29 ms for the whole phase).  j <= 5 keeps (c lambda)^p finite.
+int power_squarings(int64_t s, int T) {
+  if (T < 4) return 0;
+  const double sd = (double)s;
+  const double gemm_us = fmax(6.0, sd * sd * sd / (s <= 2048 ? 20e12 : 30e12) * 1e6);
+  double iter_us;
+  if (s <= 1024) iter_us = 1.2 + 0.9 * sd / 1024.0;
+  else if (sd * 8.0 * 2.0 <= 200.0 * 1024.0) iter_us = 3.0;
+  else iter_us = 8.0 * sd * sd / 6.5e12 * 1e6 + 2.0;
+  int best = 0;
+  double best_cost = (double)T * iter_us;
+  for (int j = 1; j <= 5 && (1 << j) <= T - 1; ++j) {
+    const int p = 1 << j, q = (T - 1) / p;
+    const double cost = j * gemm_us + (double)(T - (p - 1) * q) * iter_us;
+    if (cost < best_cost) { best_cost = cost; best = j; }
+  }
+  return best;
 }
 
 template <typename E>
-static cudaError_t launch_power_t(const E* G, const E* G4, int64_t s, int64_t ld, int T, double* scratch,
+static cudaError_t launch_power_t(const E* G, const E* G4, int pw, int64_t s, int64_t ld, int T, double* scratch,
                                   unsigned int* bar, SeriesParams* P, const cpa_svt_kernel& k, int K, double safety,
                                   const double* c_given, int num_sms, cudaStream_t st) {
   PowerArgs<E> a{};
   a.ld = ld;
   a.G = G; a.s = s; a.T = T;
   a.G4 = G4;
-  a.q = G4 ? (T - 1) / 4 : 0;
+  a.pw = G4 ? pw : 1;
+  a.q = G4 ? (T - 1) / pw : 0;
+  a.poll = 32 * CPA_POLL_WARPS;
   a.ll = reinterpret_cast<unsigned long long*>(scratch);
   (void)bar;
   a.P = P; a.kern = k; a.K = K; a.safety = safety; a.c_given = c_given;
@@ -467,11 +459,14 @@ static cudaError_t launch_power_t(const E* G, const E* G4, int64_t s, int64_t ld
     return cudaLaunchCooperativeKernel((void*)k_power_stream<E>, dim3((unsigned)g2), dim3(512), args, sm2, st);
   }
   if constexpr (sizeof(E) == sizeof(double)) {
-    // register-resident rows for small s (c1, c2): <= 8 rows x 4 columns per thread
-    if (a.rows_per_cta <= 8 && s <= 1024 && !getenv("CPA_SVT_POWER_SMEM")) {
+    // s <= 1024 (c1, c2): one warp per Gram row, the row in registers
+    if (s <= 1024 && !getenv("CPA_SVT_POWER_SMEM")) {
+      a.rows_per_cta = 8;
+      a.poll = 256;
+      const int64_t gw = (s + 7) / 8;
       void* args[] = {&a};
-      const size_t pad = 0;
-      return cudaLaunchCooperativeKernel((void*)k_power_reg<8, 4>, dim3((unsigned)grid), dim3(256), args, pad, st);
+      void* kf = s <= 64 ? (void*)k_power_warp<2> : s <= 256 ? (void*)k_power_warp<8> : (void*)k_power_warp<32>;
+      return cudaLaunchCooperativeKernel(kf, dim3((unsigned)gw), dim3(256), args, 0, st);
     }
   }
   cudaError_t e = cudaFuncSetAttribute(k_power_dense<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -480,16 +475,16 @@ static cudaError_t launch_power_t(const E* G, const E* G4, int64_t s, int64_t ld
   return cudaLaunchCooperativeKernel((void*)k_power_dense<E>, dim3((unsigned)grid), dim3(256), args, smem, st);
 }
 
-cudaError_t launch_power_dense(const double* G, const double* G4, int64_t s, int T, double* scratch,
+cudaError_t launch_power_dense(const double* G, const double* G4, int pw, int64_t s, int T, double* scratch,
                                unsigned int* bar, SeriesParams* P, const cpa_svt_kernel& k, int K, double safety,
                                const double* c_given, int num_sms, cudaStream_t st) {
-  return launch_power_t<double>(G, G4, s, s, T, scratch, bar, P, k, K, safety, c_given, num_sms, st);
+  return launch_power_t<double>(G, G4, pw, s, s, T, scratch, bar, P, k, K, safety, c_given, num_sms, st);
 }
 // fp32 Gram (TF32 path): the products are accumulated in fp64 all the same
 cudaError_t launch_power_dense_f32(const float* G, int64_t s, int64_t ld, int T, double* scratch, unsigned int* bar,
                                    SeriesParams* P, const cpa_svt_kernel& k, int K, double safety,
                                    const double* c_given, int num_sms, cudaStream_t st) {
-  return launch_power_t<float>(G, nullptr, s, ld, T, scratch, bar, P, k, K, safety, c_given, num_sms, st);
+  return launch_power_t<float>(G, nullptr, 1, s, ld, T, scratch, bar, P, k, K, safety, c_given, num_sms, st);
 }
 
 }  // namespace cpa
