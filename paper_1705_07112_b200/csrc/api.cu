@@ -592,8 +592,10 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
   auto r32 = [](size_t v) { return (v + 31) / 32 * 32; };
   const size_t nG = r32((size_t)s * s), nW = r32((size_t)RM * RN), nPow = r32(power_dense_scratch_doubles(s));
   const size_t nX = poly ? 2 * nG : 0;
+  const bool final_split = getenv("CPA_SVT_FINAL_NOSPLIT") == nullptr;  // line-12 product split-K (default on)
   const size_t nPart = r32(std::max({dense_flow_partial_doubles(RM, RN, h->num_sms), dense_gram_partial_doubles(s),
-                                     form == 2 ? dense_sym_partial_doubles(s, h->num_sms) : (size_t)0}));
+                                     form == 2 ? dense_sym_partial_doubles(s, h->num_sms) : (size_t)0,
+                                     final_split && poly ? dense_store_partial_doubles(m, n) : (size_t)0}));
   const size_t nSync = std::max({dense_flow_sync_ints(RM, RN, K), (size_t)((s / 64 + 2) * (s / 64 + 2)),
                                  dense_sym_sync_ints(s, K, h->num_sms), (size_t)1332});
   const size_t need = (nG + 2 * nW + nX + nPow + nPart) * sizeof(double) + nSync * sizeof(int) + 256;
@@ -721,7 +723,7 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
       if (st != CPA_SVT_OK) return st;
     }
     Phase p(h, CPA_SVT_PH_FINAL);
-    // (split-K for this product measured slower at c2: 96 vs 91 us -- not used)
+    // (split-K over the k = s dimension when the tiles alone leave slots idle: c2 111 -> 96 us)
     const double* Hm = H;
     if (dct) {  // line 12 with T: Y = (C^T H C) X  or  X (C^T H C)
       CU(dense_gemm_store(s, s, s, CTd, s, H, s, Wa, s, h->stream));
@@ -729,8 +731,10 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
       launches += 2;
       Hm = Wb;
     }
-    if (left) CU(dense_gemm_store(s, n, s, Hm, s, X, ldx, Y, ldy, h->stream));
-    else      CU(dense_gemm_store(m, s, s, X, ldx, Hm, s, Y, ldy, h->stream));
+    double* fp = final_split ? part : nullptr;
+    int* fs = final_split ? flow_sync : nullptr;
+    if (left) CU(dense_gemm_store(s, n, s, Hm, s, X, ldx, Y, ldy, h->stream, fp, fs));
+    else      CU(dense_gemm_store(m, s, s, X, ldx, Hm, s, Y, ldy, h->stream, fp, fs));
     ++launches;
   }
   tm.mark();

@@ -844,6 +844,9 @@ static cudaError_t launch(const GemmArgs& a, cudaStream_t st) {
       if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, NTHREADS, smem) != cudaSuccess || per_sm < 1)
         per_sm = 1;
       split = best_split(tiles, nk, (int64_t)sms * per_sm);
+      if (const char* v = getenv(MODE == EPI_STORE ? "CPA_SVT_STORE_SPLIT" : "CPA_SVT_GRAM_SPLIT");
+          v && atoi(v) >= 1 && atoi(v) <= 8)
+        split = atoi(v);   // (experiments)
       if (split > 1) {
         cudaError_t ez = cudaMemsetAsync(a.tcount, 0, tiles * sizeof(int), st);
         if (ez != cudaSuccess) return ez;
