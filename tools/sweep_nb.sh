@@ -1,0 +1,4 @@
+timeout 600 python -m pytest tests/test_dense_gpu.py tests/test_transform_gpu.py -q -x 2>&1 | tail -1
+for v in "" "CPA_SVT_SYM_3BUF=1"; do
+  echo "[$v]"; env $v timeout 300 python tools/bench_configs.py c1 c2 c5:8192x32768 --reps 5 | python -c "import sys,json; [print(json.loads(l)['config'], round(json.loads(l)['ms_per_svt'],3), {k: round(v,3) for k,v in json.loads(l)['phases_ms'].items()}) for l in sys.stdin]"
+done
