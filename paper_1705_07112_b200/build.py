@@ -20,7 +20,8 @@ def build(verbose=False, force=False, defines=(), lib=LIB, tag=""):
     for s in SOURCES:
         src = os.path.join(CSRC, s)
         obj = os.path.join(bdir, s.replace(".cu", ".o"))
-        deps = [src, os.path.join(CSRC, "common.cuh"), os.path.join(ROOT, "include", "cpa_svt.h")]
+        deps = [src, os.path.join(CSRC, "common.cuh"), os.path.join(CSRC, "tma.cuh"),
+                os.path.join(ROOT, "include", "cpa_svt.h")]
         if force or not os.path.exists(obj) or os.path.getmtime(obj) < max(os.path.getmtime(d) for d in deps):
             cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
             if verbose:

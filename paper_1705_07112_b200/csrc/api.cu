@@ -592,7 +592,7 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
   auto r32 = [](size_t v) { return (v + 31) / 32 * 32; };
   const size_t nG = r32((size_t)s * s), nW = r32((size_t)RM * RN), nPow = r32(power_dense_scratch_doubles(s));
   const size_t nX = poly ? 2 * nG : 0;
-  const bool final_split = getenv("CPA_SVT_FINAL_NOSPLIT") == nullptr;  // line-12 product split-K (default on)
+  const bool final_split = !env_on("CPA_SVT_FINAL_NOSPLIT");  // line-12 product split-K (default on)
   const size_t nPart = r32(std::max({dense_flow_partial_doubles(RM, RN, h->num_sms), dense_gram_partial_doubles(s),
                                      form == 2 ? dense_sym_partial_doubles(s, h->num_sms) : (size_t)0,
                                      final_split && poly ? dense_store_partial_doubles(m, n) : (size_t)0}));

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include "cpa_svt.h"
 
@@ -54,6 +55,12 @@ __host__ __device__ inline double cheb_theta(int l, int K) {
 }
 
 // ---- small PTX helpers --------------------------------------------------------
+// Experiment switches: true iff the environment variable is set to a non-empty value other than "0".
+inline bool env_on(const char* name) {
+  const char* v = getenv(name);
+  return v != nullptr && v[0] != '\0' && !(v[0] == '0' && v[1] == '\0');
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

@@ -15,6 +15,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "tma.cuh"
 
 namespace cpa {
 
@@ -481,6 +482,101 @@ __device__ __forceinline__ void tri_decode_colmajor(int idx, int T, int& row, in
 // and i (crosses j and i of step k-2; j is implied by cross j of step k-1) and
 // by the step k-1 epilogue of tile (i, j) (in cross j of step k-1): so it also
 // waits for cross i of step k-2.
+// After the mainloop of unit (step k, tile (ti, tj), k-split q): split-K publish (q < S-1)
+// or reduce (q = S-1, all partials summed in the fixed order q = 0..S-1), then the fused
+// epilogue on the tile's r >= c elements and the release of its crosses.
+template <bool tma>
+__device__ __forceinline__ void sym_finish(const SymArgs& a, int k, int tile, int q, int ti, int tj,
+                                           double (&acc)[4][4][2]) {
+  const int T = a.T;
+  const int S = a.split;
+  int* cross = a.sync + 1;
+  int* split_cnt = a.sync + 1 + a.K * T;
+  const int64_t s = a.s;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  auto buf = [&](int i) { return i == 0 ? a.W[0] : (i == 1 ? a.W[1] : a.W[2]); };
+  const double* src = buf((k - 1) % 3);   // W_{k-1}
+  const double* wpp = buf((k - 2) % 3);   // W_{k-2} (k = 2: identity, implicit)
+  double* out = buf(k % 3);               // W_k over W_{k-3}
+  const int64_t m0 = (int64_t)ti * BM, n0 = (int64_t)tj * BN;
+  if (S > 1) {
+    double* slot = a.partial + (int64_t)tile * (S - 1) * (BM * BN);
+    if (q < S - 1) {
+      double* mine = slot + (int64_t)q * (BM * BN);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) __stcg(mine + ((i * 4 + j) * 2 + e) * NTHREADS + threadIdx.x, acc[i][j][e]);
+      __syncthreads();
+      if (threadIdx.x == 0) red_release_add_i32(split_cnt + tile, 1);
+      return;
+    }
+    if (threadIdx.x == 0) wait_geq(split_cnt + tile, (S - 1) * (k - 1));
+    __syncthreads();
+    double sum[32];
+#pragma unroll
+    for (int rr = 0; rr < 32; ++rr) sum[rr] = __ldcg(slot + rr * NTHREADS + threadIdx.x);
+    for (int p = 1; p < S - 1; ++p) {
+      double v[32];
+#pragma unroll
+      for (int rr = 0; rr < 32; ++rr) v[rr] = __ldcg(slot + (int64_t)p * (BM * BN) + rr * NTHREADS + threadIdx.x);
+#pragma unroll
+      for (int rr = 0; rr < 32; ++rr) sum[rr] += v[rr];
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) acc[i][j][e] = sum[(i * 4 + j) * 2 + e] + acc[i][j][e];
+  }
+  // fused epilogue on the elements r >= c of the tile
+  const double s4 = 2.0 * a.P->scale2, ck = a.P->c[k];
+  const bool last = k == a.K - 1;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t rr = m0 + wm + i * 8 + g;
+    double vp[8], vpp[8], vy[8];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t c = n0 + wn + j * 8 + 2 * t + e;
+        const bool ok = rr < s && c <= rr;
+        const int64_t o = rr * s + c;
+        vp[j * 2 + e] = ok ? __ldcg(src + o) : 0.0;
+        vpp[j * 2 + e] = k == 2 ? (rr == c ? 1.0 : 0.0) : (ok ? __ldcg(wpp + o) : 0.0);
+        vy[j * 2 + e] = ok ? __ldcg(a.H + o) : 0.0;
+      }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t c = n0 + wn + j * 8 + 2 * t + e;
+        if (!(rr < s && c <= rr)) continue;
+        const int qq = j * 2 + e;
+        const double wv = s4 * acc[i][j][e] - 2.0 * vp[qq] - vpp[qq];  // W_k = 2 B_hat W_{k-1} - W_{k-2}
+        const double y = vy[qq] + ck * wv;                               // H += c_k W_k
+        if (!last) {
+          out[rr * s + c] = wv;
+          out[c * s + rr] = wv;
+        }
+        a.H[rr * s + c] = y;
+        if (last) a.H[c * s + rr] = y;
+      }
+  }
+  if (tma) fence_proxy_async_global();   // W_k / H stores -> later TMA (async-proxy) reads
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    red_release_add_i32(cross + k * T + ti, 1);
+    if (ti != tj) red_release_add_i32(cross + k * T + tj, 1);
+  }
+}
+
 __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB) k_cheb_sym(SymArgs a) {
   extern __shared__ __align__(16) double smem[];
   __shared__ int s_ticket;
@@ -490,12 +586,8 @@ __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB) k_cheb_sym(SymArgs a)
   const int per_step = ntri * S;
   const int total = (a.K - 2) * per_step;
   int* cross = a.sync + 1;
-  int* split_cnt = a.sync + 1 + a.K * T;
   const int64_t s = a.s;
   const int nk = (int)((s + BKS - 1) / BKS);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = lane >> 2, t = lane & 3;
-  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
   for (;;) {
     if (threadIdx.x == 0) s_ticket = atomicAdd(a.sync, 1);
     __syncthreads();
@@ -509,8 +601,6 @@ __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB) k_cheb_sym(SymArgs a)
     tri_decode_colmajor(tile, T, ti, tj);
     auto buf = [&](int i) { return i == 0 ? a.W[0] : (i == 1 ? a.W[1] : a.W[2]); };
     const double* src = buf((k - 1) % 3);   // W_{k-1}
-    const double* wpp = buf((k - 2) % 3);   // W_{k-2} (k = 2: identity, implicit)
-    double* out = buf(k % 3);               // W_k over W_{k-3}
     const int64_t m0 = (int64_t)ti * BM, n0 = (int64_t)tj * BN;
     const int kb = (int)((int64_t)nk * q / S), ke = (int)((int64_t)nk * (q + 1) / S);
     double acc[4][4][2];
@@ -523,79 +613,147 @@ __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB) k_cheb_sym(SymArgs a)
 #endif
       __syncthreads();
     });
-    if (S > 1) {
-      double* slot = a.partial + (int64_t)tile * (S - 1) * (BM * BN);
-      if (q < S - 1) {
-        double* mine = slot + (int64_t)q * (BM * BN);
+    sym_finish<false>(a, k, tile, q, ti, tj, acc);
+  }
+}
+
+// TMA-fed variant of k_cheb_sym (same units, dependencies and epilogue).  The k-slabs of
+// G and W_{k-1} arrive by cp.async.bulk.tensor (16-column x 16-row boxes, 128-byte swizzle)
+// into a 4-stage ring guarded by mbarriers: thread 0 is the producer (it refills the stage
+// of slab kt-1 at the top of slab kt, after the empty barrier says all four warps are done
+// with it); the warps wait only on the full barrier of the slab they consume -- no CTA
+// barrier per slab and no per-thread copy instructions.  Fragment loads: DMMA step kk
+// consumes the k rows {8(kk/2) + 2t + kk%2 : t = 0..3} (a fixed permutation of the slab's
+// 16 rows, the same for A and B), so the four rows a half-warp reads carry the XOR
+// patterns {0,2,4,6} or {1,3,5,7} of the swizzle and hit 32 distinct banks.
+constexpr int TBK = 16, TSTAGES = 4;
+constexpr int BOX_BYTES = 16 * TBK * 8;          // 16 doubles x TBK rows
+constexpr int TSTAGE_BYTES = 8 * BOX_BYTES;      // A: 4 boxes (64 m), B: 4 boxes (64 n)
+struct SymMaps {
+  CUtensorMap g;
+  CUtensorMap w[3];
+};
+__global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB)
+    k_cheb_sym_tma(const __grid_constant__ SymMaps mp, SymArgs a) {
+  extern __shared__ unsigned char tsm_raw[];
+  __shared__ __align__(8) uint64_t full[TSTAGES], empty[TSTAGES];
+  __shared__ int s_ticket;
+  // 1024-byte aligned ring (the 128-byte swizzle pattern repeats every 1024 bytes); pointer
+  // arithmetic on the __shared__ array keeps the fragment loads in the shared window (LDS)
+  unsigned char* base = tsm_raw + ((1024u - (smem_u32(tsm_raw) & 1023u)) & 1023u);
+  const int T = a.T;
+  const int ntri = T * (T + 1) / 2;
+  const int S = a.split;
+  const int per_step = ntri * S;
+  const int total = (a.K - 2) * per_step;
+  int* cross = a.sync + 1;
+  const int nk = (int)((a.s + TBK - 1) / TBK);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < TSTAGES; ++st) {
+      mbar_init(full + st, 1);
+      mbar_init(empty + st, 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  // byte offset of element (row r, column c) of a box: r*128 + (((c/2) ^ (r%8)) * 16) + (c%2)*8
+  uint32_t coff[2][2];
+#pragma unroll
+  for (int par = 0; par < 2; ++par)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) coff[par][h] = ((((h * 8 + g) >> 1) ^ (2 * t + par)) << 4) | ((g & 1) * 8);
+  const uint32_t roff = 256 * t;
+  const uint32_t boxa = (wm >> 4) * BOX_BYTES, boxb = (4 + (wn >> 4)) * BOX_BYTES;
+  uint32_t it = 0;  // slabs consumed by this CTA so far (stage = it % TSTAGES, phase = it / TSTAGES)
+  for (;;) {
+    if (threadIdx.x == 0) s_ticket = atomicAdd(a.sync, 1);
+    __syncthreads();
+    const int tk = s_ticket;
+    if (tk >= total) break;
+    const int k = 2 + tk / per_step;
+    const int r = tk % per_step;
+    const int q = r % S;
+    const int tile = r / S;
+    int ti, tj;
+    tri_decode_colmajor(tile, T, ti, tj);
+    const CUtensorMap* wmap = &mp.w[(k - 1) % 3];   // W_{k-1}
+    const int m0 = ti * BM, n0 = tj * BN;
+    const int kb = (int)((int64_t)nk * q / S), ke = (int)((int64_t)nk * (q + 1) / S);
+    const int nku = ke - kb;
+    if (threadIdx.x == 0) {
+      // prologue: the static G slabs before the dependency wait, the W_{k-1} slabs after it
+      const int P = nku < TSTAGES - 1 ? nku : TSTAGES - 1;
+      for (int p = 0; p < P; ++p) {
+        const uint32_t sl = it + p, st = sl % TSTAGES;
+        mbar_wait(empty + st, ((sl / TSTAGES) & 1) ^ 1);
+        mbar_expect_tx(full + st, TSTAGE_BYTES);
+        for (int b = 0; b < 4; ++b)
+          tma_load_2d(base + st * TSTAGE_BYTES + b * BOX_BYTES, &mp.g, m0 + 16 * b, (kb + p) * TBK, full + st);
+      }
+      if (k >= 3) wait_geq(cross + (k - 1) * T + tj, T);
+      if (k >= 4) wait_geq(cross + (k - 2) * T + ti, T);
+      fence_proxy_async_global();   // generic-proxy W_{k-1} stores of other CTAs -> TMA reads
+      for (int p = 0; p < P; ++p) {
+        const uint32_t st = (it + p) % TSTAGES;
+        for (int b = 0; b < 4; ++b)
+          tma_load_2d(base + st * TSTAGE_BYTES + (4 + b) * BOX_BYTES, wmap, n0 + 16 * b, (kb + p) * TBK, full + st);
+      }
+    }
+    // The epilogue's generic loads of W_{k-1}, W_{k-2} and H must be ordered after thread 0's
+    // acquire of the dependency: every warp waits on the full barrier of a refilled slab, whose
+    // expect_tx arrive thread 0 made after that acquire (release -> acquire at CTA scope); a
+    // unit too short to refill (nku < TSTAGES) takes a CTA barrier instead.
+    if (nku < TSTAGES) __syncthreads();
+    else __syncwarp();
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int kt = 0; kt < nku; ++kt) {
+      if (threadIdx.x == 0 && kt + TSTAGES - 1 < nku) {   // refill the stage of slab kt-1
+        const int kn = kt + TSTAGES - 1;
+        const uint32_t sl = it + kn, st = sl % TSTAGES;
+        mbar_wait(empty + st, ((sl / TSTAGES) & 1) ^ 1);
+        mbar_expect_tx(full + st, TSTAGE_BYTES);
+        unsigned char* d = base + st * TSTAGE_BYTES;
+        for (int b = 0; b < 4; ++b) tma_load_2d(d + b * BOX_BYTES, &mp.g, m0 + 16 * b, (kb + kn) * TBK, full + st);
+        for (int b = 0; b < 4; ++b)
+          tma_load_2d(d + (4 + b) * BOX_BYTES, wmap, n0 + 16 * b, (kb + kn) * TBK, full + st);
+      }
+      __syncwarp();
+      const uint32_t sl = it + kt, st = sl % TSTAGES;
+      mbar_wait(full + st, (sl / TSTAGES) & 1);
+      const unsigned char* sa = base + st * TSTAGE_BYTES + boxa;
+      const unsigned char* sb = base + st * TSTAGE_BYTES + boxb;
+#pragma unroll
+      for (int kk = 0; kk < TBK / 4; ++kk) {
+        const int par = kk & 1;
+        const uint32_t ro = 1024 * (kk >> 1) + 128 * par + roff;
+        double fa[4], fb[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          fa[i] = *reinterpret_cast<const double*>(sa + (i >> 1) * BOX_BYTES + ro + coff[par][i & 1]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          fb[j] = *reinterpret_cast<const double*>(sb + (j >> 1) * BOX_BYTES + ro + coff[par][j & 1]);
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) __stcg(mine + ((i * 4 + j) * 2 + e) * NTHREADS + threadIdx.x, acc[i][j][e]);
-        __syncthreads();
-        if (threadIdx.x == 0) red_release_add_i32(split_cnt + tile, 1);
-        continue;
+          for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], fa[i], fb[j]);
       }
-      if (threadIdx.x == 0) wait_geq(split_cnt + tile, (S - 1) * (k - 1));
-      __syncthreads();
-      double sum[32];
-#pragma unroll
-      for (int rr = 0; rr < 32; ++rr) sum[rr] = __ldcg(slot + rr * NTHREADS + threadIdx.x);
-      for (int p = 1; p < S - 1; ++p) {
-        double v[32];
-#pragma unroll
-        for (int rr = 0; rr < 32; ++rr) v[rr] = __ldcg(slot + (int64_t)p * (BM * BN) + rr * NTHREADS + threadIdx.x);
-#pragma unroll
-        for (int rr = 0; rr < 32; ++rr) sum[rr] += v[rr];
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) acc[i][j][e] = sum[(i * 4 + j) * 2 + e] + acc[i][j][e];
+      // the stage is rewritten by the async proxy (TMA) once all four warps have arrived:
+      // order this warp's generic-proxy fragment loads before that (without the fence ptxas
+      // may issue the arrive before the loads have completed -- a measured data race)
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + st);
     }
-    // fused epilogue on the elements r >= c of the tile
-    const double s4 = 2.0 * a.P->scale2, ck = a.P->c[k];
-    const bool last = k == a.K - 1;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int64_t rr = m0 + wm + i * 8 + g;
-      double vp[8], vpp[8], vy[8];
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int64_t c = n0 + wn + j * 8 + 2 * t + e;
-          const bool ok = rr < s && c <= rr;
-          const int64_t o = rr * s + c;
-          vp[j * 2 + e] = ok ? __ldcg(src + o) : 0.0;
-          vpp[j * 2 + e] = k == 2 ? (rr == c ? 1.0 : 0.0) : (ok ? __ldcg(wpp + o) : 0.0);
-          vy[j * 2 + e] = ok ? __ldcg(a.H + o) : 0.0;
-        }
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int64_t c = n0 + wn + j * 8 + 2 * t + e;
-          if (!(rr < s && c <= rr)) continue;
-          const int qq = j * 2 + e;
-          const double wv = s4 * acc[i][j][e] - 2.0 * vp[qq] - vpp[qq];  // W_k = 2 B_hat W_{k-1} - W_{k-2}
-          const double y = vy[qq] + ck * wv;                               // H += c_k W_k
-          if (!last) {
-            out[rr * s + c] = wv;
-            out[c * s + rr] = wv;
-          }
-          a.H[rr * s + c] = y;
-          if (last) a.H[c * s + rr] = y;
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      red_release_add_i32(cross + k * T + ti, 1);
-      if (ti != tj) red_release_add_i32(cross + k * T + tj, 1);
-    }
+    it += nku;
+    sym_finish<true>(a, k, tile, q, ti, tj, acc);
   }
 }
 
@@ -1087,6 +1245,38 @@ cudaError_t dense_cheb_sym(int64_t s, const double* G, double* W0, double* W1, d
   }
   const int64_t total = (int64_t)(K - 2) * a.T * (a.T + 1) / 2 * a.split;
   const int64_t grid = slots < total ? slots : total;
+  if (!env_on("CPA_SVT_SYM_NOTMA") && s % 2 == 0 && s <= INT32_MAX / 2) {
+    // TMA-fed kernel (default; the cp.async kernel for odd s, whose rows are not 16-byte
+    // aligned): one fp64 tensor map per operand (16 x 16 boxes, 128-byte swizzle)
+    EncodeTiledFn fn = encode_fn();
+    SymMaps mp;
+    bool ok = fn != nullptr;
+    const double* ops[4] = {G, W0, W1, W2};
+    CUtensorMap* maps[4] = {&mp.g, &mp.w[0], &mp.w[1], &mp.w[2]};
+    for (int i = 0; i < 4 && ok; ++i) {
+      cuuint64_t dims[2] = {(cuuint64_t)s, (cuuint64_t)s};
+      cuuint64_t strides[1] = {(cuuint64_t)(s * sizeof(double))};
+      cuuint32_t box[2] = {16u, (cuuint32_t)TBK};
+      cuuint32_t estr[2] = {1u, 1u};
+      ok = fn(maps[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)ops[i], dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
+    if (ok) {
+      const size_t tsmem = (size_t)TSTAGES * TSTAGE_BYTES + 1024;
+      e = cudaFuncSetAttribute(k_cheb_sym_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
+      if (e != cudaSuccess) return e;
+      int per_sm = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cheb_sym_tma, NTHREADS, tsmem) != cudaSuccess ||
+          per_sm < 1)
+        return cudaErrorLaunchOutOfResources;
+      int64_t tgrid = (int64_t)num_sms * per_sm;
+      if (tgrid > total) tgrid = total;
+      void* targs[] = {&mp, &a};
+      return cudaLaunchCooperativeKernel((void*)k_cheb_sym_tma, dim3((unsigned)tgrid), dim3(NTHREADS), targs, tsmem,
+                                         st);
+    }
+  }
   void* args[] = {&a};
   return cudaLaunchCooperativeKernel((void*)k_cheb_sym, dim3((unsigned)grid), dim3(NTHREADS), args, smem, st);
 }

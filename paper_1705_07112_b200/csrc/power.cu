@@ -460,7 +460,7 @@ static cudaError_t launch_power_t(const E* G, const E* G4, int pw, int64_t s, in
   }
   if constexpr (sizeof(E) == sizeof(double)) {
     // s <= 1024 (c1, c2): one warp per Gram row, the row in registers
-    if (s <= 1024 && !getenv("CPA_SVT_POWER_SMEM")) {
+    if (s <= 1024 && !env_on("CPA_SVT_POWER_SMEM")) {
       a.rows_per_cta = 8;
       a.poll = 256;
       const int64_t gw = (s + 7) / 8;
