@@ -264,4 +264,6 @@ def test_config5_full_size_sampled(env):
     lam = 1.01 * lam_hat
     c = O.kernel_coefficients(O.Kernel(**cfg["kernel"]), cfg["K"], lam, math.sqrt(lam_hat))
     Yo = O.cpa_apply_vectors(lambda V: G @ V, X[:, cols], c, lam)
-    assert O.rel_fro(Ys, Yo) <= TOL64
+    err = O.rel_fro(Ys, Yo)
+    print(f"c5 full size: lambda_hat rel diff {abs(info['lambda_hat'] - lam_hat) / lam_hat:.3e}, Y rel err {err:.3e}")
+    assert err <= TOL64
