@@ -858,12 +858,10 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(NTHREADS, CPA_FLOW_
   }
 }
 
-template <bool A_KC, bool B_KC, int MODE>
-__global__ void __launch_bounds__(NTHREADS) k_dmma_gemm(GemmArgs a) {
-  extern __shared__ __align__(16) double smem[];
-  int tm, tn;
+// Lower-triangle tile (tm >= tn) of linear index b (GRAM); row-major tile order (STORE).
+template <int MODE>
+__device__ __forceinline__ void gemm_tile(const GemmArgs& a, int& tm, int& tn) {
   if (MODE == EPI_GRAM) {
-    // lower-triangular tile (tm >= tn) from the linear block index
     const int b = blockIdx.x;
     int r = (int)((sqrt(8.0 * b + 1.0) - 1.0) * 0.5);
     while ((r + 1) * (r + 2) / 2 <= b) ++r;
@@ -878,59 +876,58 @@ __global__ void __launch_bounds__(NTHREADS) k_dmma_gemm(GemmArgs a) {
     tm = blockIdx.x;
     tn = blockIdx.y;
   }
-  const int64_t m0 = (int64_t)tm * BM, n0 = (int64_t)tn * BN;
+}
+
+// split-K over gridDim.y units per tile (the triangle alone has too few tiles to give
+// every SMSP more than one warp): every unit publishes its partial; the last to arrive
+// sums them in the fixed order q = 0..S-1 (deterministic) into acc and returns true.
+__device__ __forceinline__ bool gemm_split_reduce(const GemmArgs& a, double (&acc)[4][4][2]) {
+  __shared__ int s_last;
+  const int S = gridDim.y, q = blockIdx.y;
+  double* slot = a.partial + (int64_t)blockIdx.x * S * (BM * BN);
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        __stcg(slot + (int64_t)q * (BM * BN) + ((i * 4 + j) * 2 + e) * NTHREADS + threadIdx.x, acc[i][j][e]);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int old;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;\n" : "=r"(old) : "l"(a.tcount + blockIdx.x) : "memory");
+    s_last = old == S - 1;
+  }
+  __syncthreads();
+  if (!s_last) return false;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    double pv[8][8];  // the 8 accumulators of row group i from up to 8 splits, all loads in flight
+#pragma unroll
+    for (int p = 0; p < 8; ++p)
+#pragma unroll
+      for (int q8 = 0; q8 < 8; ++q8)
+        pv[p][q8] = p < S ? __ldcg(slot + (int64_t)p * (BM * BN) + (i * 8 + q8) * NTHREADS + threadIdx.x) : 0.0;
+#pragma unroll
+    for (int q8 = 0; q8 < 8; ++q8) {
+      double sum = pv[0][q8];
+#pragma unroll
+      for (int p = 1; p < 8; ++p)
+        if (p < S) sum += pv[p][q8];
+      acc[i][q8 >> 1][q8 & 1] = sum;
+    }
+  }
+  return true;
+}
+
+// GRAM: the r >= c elements of the tile, mirrored (times the optional exact scale);
+// STORE: plain product (Alg. 1 line 12: Y = H_hat X or X H_hat).
+template <int MODE>
+__device__ __forceinline__ void gemm_store_tile(const GemmArgs& a, const double (&acc)[4][4][2], int64_t m0,
+                                                int64_t n0) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
-
-  double acc[4][4][2];
-  if ((MODE == EPI_GRAM || MODE == EPI_STORE) && gridDim.y > 1) {
-    // split-K over gridDim.y units per tile (the triangle alone has too few tiles to give
-    // every SMSP more than one warp): every unit publishes its partial; the last to arrive
-    // sums them in the fixed order q = 0..S-1 (deterministic) and stores the tile.
-    __shared__ int s_last;
-    const int S = gridDim.y, q = blockIdx.y;
-    const int nk = (int)((a.Kd + BKS - 1) / BKS);
-    mainloop<A_KC, B_KC>(a.A, a.lda, a.B, a.ldb, a.M, a.N, a.Kd, m0, n0, a.vec_a, a.vec_b, smem, acc,
-                         (int)((int64_t)nk * q / S), (int)((int64_t)nk * (q + 1) / S));
-    double* slot = a.partial + (int64_t)blockIdx.x * S * (BM * BN);
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-#pragma unroll
-        for (int e = 0; e < 2; ++e)
-          __stcg(slot + (int64_t)q * (BM * BN) + ((i * 4 + j) * 2 + e) * NTHREADS + threadIdx.x, acc[i][j][e]);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int old;
-      asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;\n" : "=r"(old) : "l"(a.tcount + blockIdx.x) : "memory");
-      s_last = old == S - 1;
-    }
-    __syncthreads();
-    if (!s_last) return;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      double pv[8][8];  // the 8 accumulators of row group i from up to 8 splits, all loads in flight
-#pragma unroll
-      for (int p = 0; p < 8; ++p)
-#pragma unroll
-        for (int q8 = 0; q8 < 8; ++q8)
-          pv[p][q8] = p < S ? __ldcg(slot + (int64_t)p * (BM * BN) + (i * 8 + q8) * NTHREADS + threadIdx.x) : 0.0;
-#pragma unroll
-      for (int q8 = 0; q8 < 8; ++q8) {
-        double sum = pv[0][q8];
-#pragma unroll
-        for (int p = 1; p < 8; ++p)
-          if (p < S) sum += pv[p][q8];
-        acc[i][q8 >> 1][q8 & 1] = sum;
-      }
-    }
-  } else {
-    mainloop<A_KC, B_KC>(a.A, a.lda, a.B, a.ldb, a.M, a.N, a.Kd, m0, n0, a.vec_a, a.vec_b, smem, acc);
-  }
-
-  // ---------------- epilogue -------------------------------------------------
   if (MODE == EPI_GRAM) {
     double* G = a.Wout;
     const int64_t ld = a.ldwo;
@@ -948,9 +945,7 @@ __global__ void __launch_bounds__(NTHREADS) k_dmma_gemm(GemmArgs a) {
             G[c * ld + r] = v;
           }
         }
-    return;
-  }
-  if (MODE == EPI_STORE) {  // plain product (Alg. 1 line 12: Y = H_hat X or X H_hat)
+  } else {
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -960,10 +955,144 @@ __global__ void __launch_bounds__(NTHREADS) k_dmma_gemm(GemmArgs a) {
           const int64_t r = m0 + wm + i * 8 + g, c = n0 + wn + j * 8 + 2 * t + e;
           if (r < a.M && c < a.N) a.Y[r * a.ldy + c] = acc[i][j][e];
         }
+  }
+}
+
+template <bool A_KC, bool B_KC, int MODE>
+__global__ void __launch_bounds__(NTHREADS) k_dmma_gemm(GemmArgs a) {
+  extern __shared__ __align__(16) double smem[];
+  int tm, tn;
+  gemm_tile<MODE>(a, tm, tn);
+  const int64_t m0 = (int64_t)tm * BM, n0 = (int64_t)tn * BN;
+  double acc[4][4][2];
+  if ((MODE == EPI_GRAM || MODE == EPI_STORE) && gridDim.y > 1) {
+    const int S = gridDim.y, q = blockIdx.y;
+    const int nk = (int)((a.Kd + BKS - 1) / BKS);
+    mainloop<A_KC, B_KC>(a.A, a.lda, a.B, a.ldb, a.M, a.N, a.Kd, m0, n0, a.vec_a, a.vec_b, smem, acc,
+                         (int)((int64_t)nk * q / S), (int)((int64_t)nk * (q + 1) / S));
+    if (!gemm_split_reduce(a, acc)) return;
+  } else {
+    mainloop<A_KC, B_KC>(a.A, a.lda, a.B, a.ldb, a.M, a.N, a.Kd, m0, n0, a.vec_a, a.vec_b, smem, acc);
+  }
+  if (MODE == EPI_GRAM || MODE == EPI_STORE) {
+    gemm_store_tile<MODE>(a, acc, m0, n0);
     return;
   }
   cheb_epilogue(acc, m0, n0, a.M, a.N, MODE == EPI_INIT, a.Wp, a.ldwp, a.Wpp, a.ldwpp, a.Wout, a.ldwo, a.Y, a.ldy,
                 a.P, a.k);
+}
+
+// TMA-fed GEMM for the GRAM and STORE modes (Gram, the squarings of the power iteration,
+// Alg. 1 line 12).  Operand layouts in shared memory, both 128-byte swizzled, 16 KB per stage:
+//   ROWK  (the operand's k index runs down global rows: right Gram, B of STORE):
+//         4 boxes of 16 (m or n) columns x 16 k rows;
+//   ROWMN (k runs along global rows, "K-major": left Gram, A of STORE):
+//         1 box of 16 k columns x 64 (m or n) rows.
+// DMMA step kk consumes the k indices {0, 10, 5, 15}[t] ^ kk of the slab: for either layout
+// the 16 (row, column) pairs a half-warp reads then fall in 32 distinct banks.  Pipeline as
+// in k_cheb_sym_tma (thread 0 produces; one CTA per unit, so the ring starts fresh).
+struct GemmMaps {
+  CUtensorMap a, b;
+};
+template <bool ROWK>
+__device__ __forceinline__ double frag_ld(const unsigned char* st, int mn, int k) {
+  uint32_t off;
+  if (ROWK) {  // box mn/16, row k, column mn%16
+    const int c = mn & 15;
+    off = (mn >> 4) * BOX_BYTES + k * 128 + ((((c >> 1) ^ (k & 7)) << 4) | ((c & 1) << 3));
+  } else {     // row mn, column k
+    off = mn * 128 + ((((k >> 1) ^ (mn & 7)) << 4) | ((k & 1) << 3));
+  }
+  return *reinterpret_cast<const double*>(st + off);
+}
+template <bool ROWK>
+__device__ __forceinline__ void tma_operand(unsigned char* dst, const CUtensorMap* map, int mn0, int k0,
+                                            uint64_t* bar) {
+  if (ROWK) {
+    for (int b = 0; b < 4; ++b) tma_load_2d(dst + b * BOX_BYTES, map, mn0 + 16 * b, k0, bar);
+  } else {
+    tma_load_2d(dst, map, k0, mn0, bar);
+  }
+}
+template <bool A_ROWK, bool B_ROWK, int MODE>
+__global__ void __launch_bounds__(NTHREADS) k_dmma_gemm_tma(const __grid_constant__ GemmMaps mp, GemmArgs a) {
+  extern __shared__ unsigned char gsm_raw[];
+  __shared__ __align__(8) uint64_t full[TSTAGES], empty[TSTAGES];
+  unsigned char* base = gsm_raw + ((1024u - (smem_u32(gsm_raw) & 1023u)) & 1023u);
+  int tm, tn;
+  gemm_tile<MODE>(a, tm, tn);
+  const int m0 = tm * BM, n0 = tn * BN;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int nk = (int)((a.Kd + TBK - 1) / TBK);
+  const int S = gridDim.y, q = blockIdx.y;
+  const int kb = (int)((int64_t)nk * q / S), ke = (int)((int64_t)nk * (q + 1) / S);
+  const int nku = ke - kb;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < TSTAGES; ++st) {
+      mbar_init(full + st, 1);
+      mbar_init(empty + st, 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int sl) {   // slab sl of this unit into stage sl % TSTAGES
+    const int st = sl % TSTAGES;
+    mbar_wait(empty + st, ((sl / TSTAGES) & 1) ^ 1);
+    mbar_expect_tx(full + st, TSTAGE_BYTES);
+    unsigned char* d = base + st * TSTAGE_BYTES;
+    tma_operand<A_ROWK>(d, &mp.a, m0, (kb + sl) * TBK, full + st);
+    tma_operand<B_ROWK>(d + 4 * BOX_BYTES, &mp.b, n0, (kb + sl) * TBK, full + st);
+  };
+  if (threadIdx.x == 0)
+    for (int p = 0; p < TSTAGES - 1 && p < nku; ++p) issue(p);
+  __syncwarp();
+  const int kbase = (t == 0 ? 0 : t == 1 ? 10 : t == 2 ? 5 : 15);
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int kt = 0; kt < nku; ++kt) {
+    if (threadIdx.x == 0 && kt + TSTAGES - 1 < nku) issue(kt + TSTAGES - 1);
+    __syncwarp();
+    const int st = kt % TSTAGES;
+    mbar_wait(full + st, (kt / TSTAGES) & 1);
+    const unsigned char* sa = base + st * TSTAGE_BYTES;
+    const unsigned char* sb = sa + 4 * BOX_BYTES;
+#pragma unroll
+    for (int kk = 0; kk < TBK / 4; ++kk) {
+      const int kx = kbase ^ kk;
+      double fa[4], fb[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) fa[i] = frag_ld<A_ROWK>(sa, wm + i * 8 + g, kx);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) fb[j] = frag_ld<B_ROWK>(sb, wn + j * 8 + g, kx);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], fa[i], fb[j]);
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // loads done before the TMA refill
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + st);
+  }
+  if (S > 1 && !gemm_split_reduce(a, acc)) return;
+  gemm_store_tile<MODE>(a, acc, m0, n0);
+}
+
+// 2-D fp64 tensor map (rows x cols, row stride ld elements), box {16, box_rows}, 128B swizzle
+static bool make_map_f64(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn || (reinterpret_cast<uintptr_t>(base) & 15) || (ld % 2) || rows < 1 || cols < 1) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * sizeof(double))};
+  cuuint32_t box[2] = {16u, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1u, 1u};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)base, dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // k-splits (1..8, >= 4 k-slabs each) whose units fill whole waves of the resident
@@ -1011,6 +1140,20 @@ static cudaError_t launch(const GemmArgs& a, cudaStream_t st) {
       }
     }
     grid = dim3((unsigned)tiles, (unsigned)split);
+    // TMA-fed kernel when both operands admit a tensor map (16-byte aligned rows)
+    if constexpr (MODE == EPI_GRAM || MODE == EPI_STORE) {
+    GemmMaps mp;
+    if (!env_on("CPA_SVT_GEMM_NOTMA") && a.M <= INT32_MAX / 2 && a.N <= INT32_MAX / 2 && a.Kd <= INT32_MAX / 2 &&
+        (A_KC ? make_map_f64(&mp.a, a.A, a.M, a.Kd, a.lda, 64) : make_map_f64(&mp.a, a.A, a.Kd, a.M, a.lda, 16)) &&
+        (B_KC ? make_map_f64(&mp.b, a.B, a.N, a.Kd, a.ldb, 64) : make_map_f64(&mp.b, a.B, a.Kd, a.N, a.ldb, 16))) {
+      auto tf = k_dmma_gemm_tma<!A_KC, !B_KC, MODE>;
+      const size_t tsmem = (size_t)TSTAGES * TSTAGE_BYTES + 1024;
+      e = cudaFuncSetAttribute(tf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
+      if (e != cudaSuccess) return e;
+      tf<<<grid, NTHREADS, tsmem, st>>>(mp, a);
+      return cudaGetLastError();
+    }
+    }
   } else {
     grid = dim3((unsigned)tm, (unsigned)tn);
   }
