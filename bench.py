@@ -269,14 +269,16 @@ def run_ours(args, cfg):
     nbytes = X.size * 8
 
     # ---------------- roofline of the dominant kernel (fused step) ----------------
-    # form 2 (auto for K > 2): k_cheb_sym -- all K-2 steps of the symmetric s x s form in ONE
+    # form 2 (auto for K > 2): k_cheb_sym_tma (k_cheb_sym for odd s) -- all K-2 steps of the symmetric s x s form in ONE
     # persistent launch, algorithmic work s^2 (s+1) flops per step (lower-triangle elements,
     # 2s flops each).  form 1: k_cheb_flow -- init + K-2 steps of apply-to-X, 2 s^2 L per product.
     s_, L_ = min(cfg["m"], cfg["n"]), max(cfg["m"], cfg["n"])
     step_ms, step_n = prof["step"]
     avg = step_ms / max(step_n, 1)
     if form == 2:
-        kname = "k_cheb_sym (symmetric s x s recurrence: K-2 fused steps in one persistent launch, DMMA)"
+        kname = ("k_cheb_sym_tma (symmetric s x s recurrence: K-2 fused steps in one persistent launch, "
+                 "TMA-fed DMMA)" if s_ % 2 == 0 else
+                 "k_cheb_sym (symmetric s x s recurrence: K-2 fused steps in one persistent launch, cp.async-fed DMMA)")
         flops_per_launch = (K - 2) * s_ * s_ * (s_ + 1) * args.steps / max(step_n, 1)
     else:
         products = (K - 1) if prof["init"][1] == 0 else (K - 2)
