@@ -267,3 +267,27 @@ def test_config5_full_size_sampled(env):
     err = O.rel_fro(Ys, Yo)
     print(f"c5 full size: lambda_hat rel diff {abs(info['lambda_hat'] - lam_hat) / lam_hat:.3e}, Y rel err {err:.3e}")
     assert err <= TOL64
+
+
+@pytest.mark.parametrize("shape,K", [((100, 257), 12), ((258, 130), 9), ((1024, 1100), 30), ((66, 66), 5)])
+def test_tma_kernels_against_cp_async_and_oracle(env, shape, K):
+    """The TMA-fed kernels (k_cheb_sym_tma, k_dmma_gemm_tma: default for 16-byte aligned
+    rows) against the cp.async kernels they replace (CPA_SVT_SYM_NOTMA / CPA_SVT_GEMM_NOTMA)
+    on even, ragged s (TMA zero-fills the out-of-range box elements) and against the
+    oracle.  The two kernels sum the 16 k of a slab in different orders, so they agree to
+    rounding, not bitwise."""
+    import os
+    X = W.gen_c2(seed=11, m=shape[0], n=shape[1])
+    kern = {"kind": "soft", "tau": 0.1, "tau_relative": True}
+    Y_tma, i_tma = _run(env, X, kern, K, T=60)
+    os.environ["CPA_SVT_SYM_NOTMA"] = "1"
+    os.environ["CPA_SVT_GEMM_NOTMA"] = "1"
+    try:
+        Y_cpa, i_cpa = _run(env, X, kern, K, T=60)
+    finally:
+        del os.environ["CPA_SVT_SYM_NOTMA"], os.environ["CPA_SVT_GEMM_NOTMA"]
+    assert i_tma["form"] == 2 and i_cpa["form"] == 2
+    assert abs(i_tma["lambda_hat"] - i_cpa["lambda_hat"]) <= 1e-13 * i_cpa["lambda_hat"]
+    assert O.rel_fro(Y_tma, Y_cpa) <= 1e-13
+    Yo = O.cpa_shrink(X, O.Kernel(**kern), K, T=60)
+    assert O.rel_fro(Y_tma, Yo) <= TOL64
