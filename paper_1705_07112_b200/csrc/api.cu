@@ -26,6 +26,9 @@ cudaError_t dense_cheb_launch(bool left, bool init, int64_t m, int64_t n, const 
                               int k, cudaStream_t st);
 size_t dense_flow_sync_ints(int64_t m, int64_t n, int K);
 size_t dense_flow_partial_doubles(int64_t m, int64_t n, int num_sms);
+void dense_gram_chunk_range(int64_t kd, int q, int S, int64_t* k0, int64_t* k1);
+cudaError_t dense_gram_f64_chunk(const double* X, int64_t m, int64_t n, int64_t ldx, bool left, double* G,
+                                 cudaStream_t st, double* partial, int* tcount, int q, int S);
 cudaError_t dense_gemm_store(int64_t M, int64_t N, int64_t Kd, const double* A, int64_t lda, const double* B,
                              int64_t ldb, double* C, int64_t ldc, cudaStream_t st, double* partial = nullptr,
                              int* tcount = nullptr);
@@ -159,6 +162,13 @@ struct cpa_svt_handle {
   bool use_flow = true;            // persistent dataflow recurrence (CPA_SVT_FLOW=0: one launch per step)
   int form = 0;                    // CPA_SVT_OPT_FORM
   // profiling (cpa_svt_profile): event pairs per phase, resolved at read time
+  // cpa_svt_apply_host pipeline: X arrives in kPipe k-chunks on copy_stream, each chunk's
+  // split-K Gram unit starts when it lands; Y leaves in kPipe chunks as line 12 produces them
+  static constexpr int kPipe = 4;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t pev[2 * kPipe] = {};
+  const double* hp_X = nullptr;    // host X / Y of the call in flight (nullptr: no pipeline)
+  double* hp_Y = nullptr;
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_used;
@@ -348,6 +358,9 @@ cpa_svt_status cpa_svt_free(cpa_svt_handle* h) {
     cudaEventDestroy(u.second.second);
   }
   for (auto e : h->ev_pool) cudaEventDestroy(e);
+  for (auto e : h->pev)
+    if (e) cudaEventDestroy(e);
+  if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   delete h;
   return CPA_SVT_OK;
 }
@@ -585,6 +598,10 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
   if (dct && sharded) return CPA_SVT_E_UNSUPPORTED;
   const int form = dct ? 2 : dense_form(h, s, L, K);
   const bool poly = form != 1;
+  if (h->hp_X && (sharded || dct || !poly)) {   // (the host pipeline covers the plain s x s form only)
+    CU(cudaMemcpyAsync((double*)X, h->hp_X, (size_t)m * n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+    h->hp_X = nullptr;
+  }
   // workspace: G (s*s) | W_a | W_b | [I_s | H (s*s) in the poly forms] | power scratch | split-K partials | sync
   // (G^2 and G^4 for the squared power iteration live in W_a / W_b: free until the recurrence)
   const int64_t RM = poly ? s : m, RN = poly ? s : n;  // shape the recurrence runs on
@@ -621,7 +638,30 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
   // Alg. 1 line 1: partial Gram of this shard
   {
     Phase p(h, CPA_SVT_PH_GRAM);
-    CU(dense_gram_f64(X, m, n, ldx, left, G, h->stream, nullptr, part, flow_sync));
+    if (h->hp_X && !sharded && !dct) {
+      // host pipeline: unit q of the split-K Gram waits only for the q-th k-range of X
+      // (columns for the left Gram, rows for the right one) to land
+      const int S = cpa_svt_handle::kPipe;
+      for (int q = 0; q < S; ++q) {
+        int64_t k0, k1;
+        dense_gram_chunk_range(left ? n : m, q, S, &k0, &k1);
+        if (k1 > k0) {
+          if (left)
+            CU(cudaMemcpy2DAsync((double*)X + k0, ldx * sizeof(double), h->hp_X + k0, n * sizeof(double),
+                                 (k1 - k0) * sizeof(double), m, cudaMemcpyHostToDevice, h->copy_stream));
+          else
+            CU(cudaMemcpyAsync((double*)X + k0 * ldx, h->hp_X + k0 * n, (k1 - k0) * n * sizeof(double),
+                               cudaMemcpyHostToDevice, h->copy_stream));
+        }
+        CU(cudaEventRecord(h->pev[q], h->copy_stream));
+        CU(cudaStreamWaitEvent(h->stream, h->pev[q], 0));
+        CU(dense_gram_f64_chunk(X, m, n, ldx, left, G, h->stream, part, flow_sync, q, S));
+        ++launches;
+      }
+      --launches;
+    } else {
+      CU(dense_gram_f64(X, m, n, ldx, left, G, h->stream, nullptr, part, flow_sync));
+    }
   }
   ++launches;
   tm.mark();
@@ -733,8 +773,35 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
     }
     double* fp = final_split ? part : nullptr;
     int* fs = final_split ? flow_sync : nullptr;
-    if (left) CU(dense_gemm_store(s, n, s, Hm, s, X, ldx, Y, ldy, h->stream, fp, fs));
-    else      CU(dense_gemm_store(m, s, s, X, ldx, Hm, s, Y, ldy, h->stream, fp, fs));
+    if (h->hp_Y && !dct) {
+      // host pipeline: Y leaves in chunks (column blocks for the left product, row blocks
+      // for the right one) while the next chunk is computed
+      const int S = cpa_svt_handle::kPipe;
+      const int64_t Lc = left ? n : m;
+      for (int q = 0; q < S; ++q) {
+        const int64_t c0 = Lc * q / S / 64 * 64, c1 = q == S - 1 ? Lc : Lc * (q + 1) / S / 64 * 64;
+        if (c1 <= c0) continue;
+        if (left) {
+          CU(dense_gemm_store(s, c1 - c0, s, Hm, s, X + c0, ldx, Y + c0, ldy, h->stream, fp, fs));
+          CU(cudaEventRecord(h->pev[S + q], h->stream));
+          CU(cudaStreamWaitEvent(h->copy_stream, h->pev[S + q], 0));
+          CU(cudaMemcpy2DAsync(h->hp_Y + c0, n * sizeof(double), Y + c0, ldy * sizeof(double),
+                               (c1 - c0) * sizeof(double), m, cudaMemcpyDeviceToHost, h->copy_stream));
+        } else {
+          CU(dense_gemm_store(c1 - c0, s, s, X + c0 * ldx, ldx, Hm, s, Y + c0 * ldy, ldy, h->stream, fp, fs));
+          CU(cudaEventRecord(h->pev[S + q], h->stream));
+          CU(cudaStreamWaitEvent(h->copy_stream, h->pev[S + q], 0));
+          CU(cudaMemcpyAsync(h->hp_Y + c0 * n, Y + c0 * ldy, (c1 - c0) * n * sizeof(double),
+                             cudaMemcpyDeviceToHost, h->copy_stream));
+        }
+        ++launches;
+      }
+      --launches;
+      h->hp_Y = nullptr;   // delivered
+    } else {
+      if (left) CU(dense_gemm_store(s, n, s, Hm, s, X, ldx, Y, ldy, h->stream, fp, fs));
+      else      CU(dense_gemm_store(m, s, s, X, ldx, Hm, s, Y, ldy, h->stream, fp, fs));
+    }
     ++launches;
   }
   tm.mark();
@@ -953,6 +1020,35 @@ cpa_svt_status cpa_svt_apply_host(cpa_svt_handle* h, cpa_svt_dtype dtype, cpa_sv
   if (st != CPA_SVT_OK) return st;
   char* dX = (char*)h->hx;
   char* dY = dX + ((bytes + 255) / 256) * 256;
+  // fp64 s x s polynomial form (no transform): copies overlapped with the split-K Gram and
+  // with line 12 (apply_f64); otherwise one copy each way around the call
+  const int64_t s = std::min(m, n), L = std::max(m, n);
+  const int64_t tri = ((s + 63) / 64) * ((s + 63) / 64 + 1) / 2;
+  const bool pipe = dtype == CPA_SVT_F64 && math == CPA_SVT_MATH_NATIVE && h->transform == 0 && K > 2 &&
+                    dense_form(h, s, L, K) != 1 && s >= 256 && tri < 1332 && !env_on("CPA_SVT_HOST_NOPIPE");
+  if (pipe) {
+    if (!h->copy_stream && cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking) != cudaSuccess)
+      return CPA_SVT_E_CUDA;
+    for (auto& e : h->pev)
+      if (!e && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return CPA_SVT_E_CUDA;
+    // the previous call's work on dX / dY is ordered before this call's copies
+    CU(cudaEventRecord(h->pev[0], h->stream));
+    CU(cudaStreamWaitEvent(h->copy_stream, h->pev[0], 0));
+    h->hp_X = (const double*)X_host;
+    h->hp_Y = (double*)Y_host;
+    st = cpa_svt_apply(h, dtype, math, m, n, CPA_SVT_SHARD_NONE, 0, dX, n, dY, n, k, K, nullptr, lam, info);
+    const bool delivered = h->hp_Y == nullptr;
+    h->hp_X = nullptr;
+    h->hp_Y = nullptr;
+    if (st != CPA_SVT_OK) {
+      cudaStreamSynchronize(h->copy_stream);
+      return st;
+    }
+    if (!delivered) CU(cudaMemcpyAsync(Y_host, dY, bytes, cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    CU(cudaStreamSynchronize(h->copy_stream));
+    return CPA_SVT_OK;
+  }
   CU(cudaMemcpyAsync(dX, X_host, bytes, cudaMemcpyHostToDevice, h->stream));
   st = cpa_svt_apply(h, dtype, math, m, n, CPA_SVT_SHARD_NONE, 0, dX, n, dY, n, k, K, nullptr, lam, info);
   if (st != CPA_SVT_OK) return st;

@@ -50,6 +50,8 @@ struct GemmArgs {
   const double* gscale;         // GRAM: optional device scalar multiplying the output (exact power of 2)
   double* partial;              // GRAM split-K: tiles * split * 64 * 64 partial sums (gridDim.y = split)
   int* tcount;                  // GRAM split-K: per-tile arrival counters (zeroed before the launch)
+  int sS, sq0;                  // split-K across launches: S units per tile, this launch is unit sq0
+                                // (sS = 0: one launch, gridDim.y units)
 };
 
 // Elements per stage of an operand whose global slab is OUTER x INNER (INNER contiguous).
@@ -626,7 +628,10 @@ __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB) k_cheb_sym(SymArgs a)
 // consumes the k rows {8(kk/2) + 2t + kk%2 : t = 0..3} (a fixed permutation of the slab's
 // 16 rows, the same for A and B), so the four rows a half-warp reads carry the XOR
 // patterns {0,2,4,6} or {1,3,5,7} of the swizzle and hit 32 distinct banks.
-constexpr int TBK = 16, TSTAGES = 4;
+#ifndef CPA_TMA_STAGES
+#define CPA_TMA_STAGES 4
+#endif
+constexpr int TBK = 16, TSTAGES = CPA_TMA_STAGES;
 constexpr int BOX_BYTES = 16 * TBK * 8;          // 16 doubles x TBK rows
 constexpr int TSTAGE_BYTES = 8 * BOX_BYTES;      // A: 4 boxes (64 m), B: 4 boxes (64 n)
 struct SymMaps {
@@ -883,7 +888,7 @@ __device__ __forceinline__ void gemm_tile(const GemmArgs& a, int& tm, int& tn) {
 // sums them in the fixed order q = 0..S-1 (deterministic) into acc and returns true.
 __device__ __forceinline__ bool gemm_split_reduce(const GemmArgs& a, double (&acc)[4][4][2]) {
   __shared__ int s_last;
-  const int S = gridDim.y, q = blockIdx.y;
+  const int S = a.sS ? a.sS : gridDim.y, q = a.sq0 + blockIdx.y;
   double* slot = a.partial + (int64_t)blockIdx.x * S * (BM * BN);
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -965,8 +970,8 @@ __global__ void __launch_bounds__(NTHREADS) k_dmma_gemm(GemmArgs a) {
   gemm_tile<MODE>(a, tm, tn);
   const int64_t m0 = (int64_t)tm * BM, n0 = (int64_t)tn * BN;
   double acc[4][4][2];
-  if ((MODE == EPI_GRAM || MODE == EPI_STORE) && gridDim.y > 1) {
-    const int S = gridDim.y, q = blockIdx.y;
+  if ((MODE == EPI_GRAM || MODE == EPI_STORE) && (a.sS ? a.sS : (int)gridDim.y) > 1) {
+    const int S = a.sS ? a.sS : gridDim.y, q = a.sq0 + blockIdx.y;
     const int nk = (int)((a.Kd + BKS - 1) / BKS);
     mainloop<A_KC, B_KC>(a.A, a.lda, a.B, a.ldb, a.M, a.N, a.Kd, m0, n0, a.vec_a, a.vec_b, smem, acc,
                          (int)((int64_t)nk * q / S), (int)((int64_t)nk * (q + 1) / S));
@@ -1026,7 +1031,7 @@ __global__ void __launch_bounds__(NTHREADS) k_dmma_gemm_tma(const __grid_constan
   const int g = lane >> 2, t = lane & 3;
   const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
   const int nk = (int)((a.Kd + TBK - 1) / TBK);
-  const int S = gridDim.y, q = blockIdx.y;
+  const int S = a.sS ? a.sS : gridDim.y, q = a.sq0 + blockIdx.y;
   const int kb = (int)((int64_t)nk * q / S), ke = (int)((int64_t)nk * (q + 1) / S);
   const int nku = ke - kb;
   if (threadIdx.x == 0) {
@@ -1124,7 +1129,12 @@ static cudaError_t launch(const GemmArgs& a, cudaStream_t st) {
   if (MODE == EPI_GRAM || MODE == EPI_STORE) {
     const int64_t tiles = MODE == EPI_GRAM ? tm * (tm + 1) / 2 : tm * tn, nk = (a.Kd + BKS - 1) / BKS;
     int split = 1;
-    if (a.partial && a.tcount) {  // split-K needs scratch (sized by dense_split_partial_doubles)
+    if (a.sS > 0) {               // one unit of an across-launch split (dense_gram_f64_chunk)
+      if (a.sq0 == 0) {
+        cudaError_t ez = cudaMemsetAsync(a.tcount, 0, tiles * sizeof(int), st);
+        if (ez != cudaSuccess) return ez;
+      }
+    } else if (a.partial && a.tcount) {  // split-K needs scratch (sized by dense_split_partial_doubles)
       int dev = 0, sms = 148, per_sm = 1;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1183,6 +1193,28 @@ cudaError_t dense_gram_f64(const double* X, int64_t m, int64_t n, int64_t ldx, b
   a.Wout = G; a.ldwo = a.M;
   a.vec_a = a.vec_b = aligned16(X, ldx);
   if (a.M == 0) return cudaSuccess;
+  return left ? launch<true, true, EPI_GRAM>(a, st) : launch<false, false, EPI_GRAM>(a, st);
+}
+
+// Unit q of an S-way split-K Gram as its own launch (see dense_gram_chunk_range); the launch
+// of the last-arriving unit stores G.  S <= 8, dense_gram_partial_doubles(s) > 0.
+cudaError_t dense_gram_f64_chunk(const double* X, int64_t m, int64_t n, int64_t ldx, bool left, double* G,
+                                 cudaStream_t st, double* partial, int* tcount, int q, int S) {
+  GemmArgs a{};
+  a.partial = partial;
+  a.tcount = tcount;
+  a.sS = S;
+  a.sq0 = q;
+  if (left) {
+    a.M = m; a.N = m; a.Kd = n;
+    a.A = X; a.lda = ldx; a.B = X; a.ldb = ldx;
+  } else {
+    a.M = n; a.N = n; a.Kd = m;
+    a.A = X; a.lda = ldx; a.B = X; a.ldb = ldx;
+  }
+  a.Wout = G; a.ldwo = a.M;
+  a.vec_a = a.vec_b = aligned16(X, ldx);
+  if (a.M == 0 || S < 1 || S > 8 || !partial || !tcount) return cudaErrorInvalidValue;
   return left ? launch<true, true, EPI_GRAM>(a, st) : launch<false, false, EPI_GRAM>(a, st);
 }
 
@@ -1258,8 +1290,17 @@ size_t dense_flow_sync_ints(int64_t m, int64_t n, int K) {
 }
 
 size_t dense_gram_partial_doubles(int64_t s) {
-  const int64_t t = (s + BM - 1) / BM;
-  return (size_t)(t * (t + 1) / 2) * 8 * BM * BN;
+  const int64_t t = (s + BM - 1) / BM, tiles = t * (t + 1) / 2;
+  return tiles < 1332 ? (size_t)tiles * 8 * BM * BN : 0;   // (no split-K beyond 3 waves of 3 x 148)
+}
+
+// Unit q of S of the split-K Gram in its own launch (the host pipeline of cpa_svt_apply_host
+// launches unit q as soon as the q-th k-range of X has arrived): k-range of unit q in
+// elements, and the launch.  partial / tcount as for dense_gram_f64 (S <= 8, tiles < 1332).
+void dense_gram_chunk_range(int64_t kd, int q, int S, int64_t* k0, int64_t* k1) {
+  const int64_t nk = (kd + BKS - 1) / BKS;
+  *k0 = std::min(kd, nk * q / S * BKS);
+  *k1 = std::min(kd, nk * (q + 1) / S * BKS);
 }
 
 // split-K scratch of dense_gemm_store (M x N output): used only when the tiles

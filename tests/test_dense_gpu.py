@@ -132,14 +132,28 @@ def test_block_diagonal_closed_form(env):
     assert O.rel_fro(Y, want) <= 1e-12
 
 
-def test_apply_host_matches_device(env):
+@pytest.mark.parametrize("shape", [(256, 384), (300, 1000), (1100, 300), (1024, 1024)])
+def test_apply_host_matches_device(env, shape):
+    """cpa_svt_apply_host: with the host pipeline (X copied in four k-chunks, each starting
+    its unit of the split-K Gram; Y copied out in four chunks of line 12) it matches the
+    device-resident call to rounding (different split-K order) and the oracle; without it
+    (CPA_SVT_HOST_NOPIPE) bitwise."""
+    import os
     torch, P, h = env
-    X = W.gen_c2(m=256, n=384)
+    X = W.gen_c2(m=shape[0], n=shape[1])
     kern = {"kind": "soft", "tau": 0.05, "tau_relative": True}
     Yd, _ = _run(env, X, kern, 15, T=100)
     Xh = torch.from_numpy(X).pin_memory()
-    Yh = torch.empty_like(Xh).pin_memory()
+    Yh = torch.full_like(Xh, float("nan")).pin_memory()
     h.apply_host(Xh, Yh, kern, 15, T=100)
+    assert O.rel_fro(Yh.numpy(), Yd) <= 1e-12
+    assert O.rel_fro(Yh.numpy(), O.cpa_shrink(X, O.Kernel(**kern), 15, T=100)) <= TOL64
+    os.environ["CPA_SVT_HOST_NOPIPE"] = "1"
+    try:
+        Yh.fill_(float("nan"))
+        h.apply_host(Xh, Yh, kern, 15, T=100)
+    finally:
+        del os.environ["CPA_SVT_HOST_NOPIPE"]
     assert np.array_equal(Yh.numpy(), Yd)
 
 
