@@ -275,7 +275,10 @@ def run_ours(args, cfg):
     s_, L_ = min(cfg["m"], cfg["n"]), max(cfg["m"], cfg["n"])
     step_ms, step_n = prof["step"]
     avg = step_ms / max(step_n, 1)
-    if form == 2:
+    if form == 4:   # (c1-sized problems: the whole SVT in one thread block)
+        kname = "k_small_f64 (all of Alg. 1 in one thread block, shared memory, DFMA)"
+        flops_per_launch = dense_executed_flops(cfg["m"], cfg["n"], K, 3) * args.steps / max(step_n, 1)
+    elif form == 2:
         kname = ("k_cheb_sym_tma (symmetric s x s recurrence: K-2 fused steps in one persistent launch, "
                  "TMA-fed DMMA)" if s_ % 2 == 0 else
                  "k_cheb_sym (symmetric s x s recurrence: K-2 fused steps in one persistent launch, cp.async-fed DMMA)")
@@ -306,7 +309,8 @@ def run_ours(args, cfg):
                      "peak_source": "measured FP64 DMMA loop, profiles/r01_peaks.json (MEASURED_PEAKS.json has no fp64)",
                      "launch_ms": avg, "phase_share": phase_share,
                      "phase_ms_per_step": {k: v[0] / args.steps for k, v in prof.items() if v[1]}},
-        "form": {1: "apply-to-X", 2: "Alg. 1 s x s form, symmetric tiles", 3: "s x s form, full tiles"}[form],
+        "form": {1: "apply-to-X", 2: "Alg. 1 s x s form, symmetric tiles", 3: "s x s form, full tiles",
+                 4: "Alg. 1 s x s form in one thread block"}[form],
         "algorithmic_gflop_executed": executed / 1e9,
         "gflops_executed": world * executed / (ms * 1e-3) / 1e9,
         "e2e": {"value": world * cfg["F"] / (ms_e2e * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": ms_e2e,

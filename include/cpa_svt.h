@@ -109,7 +109,8 @@ typedef struct {
   int32_t degenerate;    /* 1 if lambda_hat <= 1e-300: Y = 0 */
   float ms_gram, ms_allreduce, ms_power, ms_recurrence, ms_total;
   int32_t kernel_launches;  /* device kernels this call launched */
-  int32_t form;          /* dense form that ran: 1 = apply-to-X, 2 = s x s symmetric, 3 = s x s full tiles */
+  int32_t form;          /* dense form that ran: 1 = apply-to-X, 2 = s x s symmetric, 3 = s x s full tiles,
+                            4 = s x s in one thread block (fp64, s <= 64 and L <= 128, FORM auto) */
 } cpa_svt_info;
 
 /* Multi-GPU sharding of the long dimension for cpa_svt_apply (world > 1). */

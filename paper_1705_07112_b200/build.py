@@ -7,7 +7,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcpasvt.so")
-SOURCES = ["api.cu", "dense_f64.cu", "power.cu", "batched_f32.cu", "batched_tc.cu", "sparse_f64.cu", "tc_tf32.cu", "admm.cu", "transform.cu"]
+SOURCES = ["api.cu", "dense_f64.cu", "power.cu", "batched_f32.cu", "batched_tc.cu", "sparse_f64.cu", "tc_tf32.cu", "admm.cu",
+           "transform.cu", "small_f64.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"), "--expt-relaxed-constexpr"]
@@ -20,7 +21,7 @@ def build(verbose=False, force=False, defines=(), lib=LIB, tag=""):
     for s in SOURCES:
         src = os.path.join(CSRC, s)
         obj = os.path.join(bdir, s.replace(".cu", ".o"))
-        deps = [src, os.path.join(CSRC, "common.cuh"), os.path.join(CSRC, "tma.cuh"),
+        deps = [src, os.path.join(CSRC, "common.cuh"), os.path.join(CSRC, "tma.cuh"), os.path.join(CSRC, "series.cuh"),
                 os.path.join(ROOT, "include", "cpa_svt.h")]
         if force or not os.path.exists(obj) or os.path.getmtime(obj) < max(os.path.getmtime(d) for d in deps):
             cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-c", src, "-o", obj]

@@ -27,6 +27,10 @@ cudaError_t dense_cheb_launch(bool left, bool init, int64_t m, int64_t n, const 
 size_t dense_flow_sync_ints(int64_t m, int64_t n, int K);
 size_t dense_flow_partial_doubles(int64_t m, int64_t n, int num_sms);
 void dense_gram_chunk_range(int64_t kd, int q, int S, int64_t* k0, int64_t* k1);
+bool small_f64_fits(int64_t m, int64_t n);
+cudaError_t launch_small_f64(const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t m, int64_t n,
+                             SeriesParams* P, const cpa_svt_kernel& k, int K, int T, double safety,
+                             double lam_override, const double* c_given, int nsq, cudaStream_t st);
 cudaError_t dense_gram_f64_chunk(const double* X, int64_t m, int64_t n, int64_t ldx, bool left, double* G,
                                  cudaStream_t st, double* partial, int* tcount, int q, int S);
 cudaError_t dense_gemm_store(int64_t M, int64_t N, int64_t Kd, const double* A, int64_t lda, const double* B,
@@ -596,6 +600,39 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
   const bool dct = h->transform == 2;      // NEXT-2 DCT variant (Phi = C G C^T, thresholded)
   const bool sparse_eps = dct && h->eps_mode != 0;
   if (dct && sharded) return CPA_SVT_E_UNSUPPORTED;
+  // small problems (s <= 64, L <= 128, e.g. BASELINE configs[0]): all of Alg. 1 in one
+  // thread block (small_f64.cu) -- the s x s form, automatic form selection only
+  if (!sharded && !dct && h->form == 0 && small_f64_fits(m, n) && !env_on("CPA_SVT_NO_SMALL")) {
+    if (h->hp_X) {
+      CU(cudaMemcpyAsync((double*)X, h->hp_X, (size_t)m * n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+      h->hp_X = nullptr;
+    }
+    const double* c_small = nullptr;
+    if (c) {
+      CU(cudaMemcpyAsync(h->d_c, c, K * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+      c_small = h->d_c;
+    }
+    PhaseTimer tm;
+    tm.start(info != nullptr, h->stream);
+    {
+      Phase p(h, CPA_SVT_PH_STEP);
+      const int nsq = lam->lambda_max > 0.0 ? 0 : power_squarings(s, lam->power_iters);
+      CU(launch_small_f64(X, ldx, Y, ldy, m, n, h->P, *k, K, lam->power_iters, lam->safety, lam->lambda_max,
+                          c_small, nsq, h->stream));
+    }
+    tm.mark();
+    h->launches += 1;
+    cpa_svt_status st = fill_info(h, info, lam, left ? 0 : 1);
+    if (st != CPA_SVT_OK) return st;
+    if (info) {
+      info->ms_gram = info->ms_allreduce = info->ms_power = 0.0f;
+      info->ms_recurrence = tm.ms(0, 1);
+      info->ms_total = tm.ms(0, 1);
+      info->kernel_launches = 1;
+      info->form = 4;
+    }
+    return CPA_SVT_OK;
+  }
   const int form = dct ? 2 : dense_form(h, s, L, K);
   const bool poly = form != 1;
   if (h->hp_X && (sharded || dct || !poly)) {   // (the host pipeline covers the plain s x s form only)

@@ -1,0 +1,267 @@
+// Small fp64 problems (s <= 64, L <= 128; BASELINE configs[0] is 64 x 48): the whole of
+// Algorithm 1 in ONE thread block of 4 warps, every operand in shared
+// memory (64 x 64 padded, leading dimension 68: conflict-free DMMA fragments).  The grid
+// path spends ~10 us per recurrence step on one 64 x 64 tile (ticket, dependency wait, TMA
+// prologue and epilogue of a grid-wide dataflow); here a step is one DMMA.8x8x4 product of
+// the block (each warp a 32 x 32 quarter) and a barrier.
+//
+//   line 1   G = A A^T from At = A^T (left: A = X, right: A = X^T)
+//   line 3   power iteration, T products (reading R6), squared as on the grid path:
+//            q products by c^p G^p (p = 2^j, c = 2^-ilogb(max G_ii)), the rest by G;
+//            lambda_hat = ||G v_{T-1}||
+//   line 4   compute_series (series.cuh)
+//   5 - 11   W_1 = (2/L) G - I, H = c_0/2 I + c_1 W_1;  W_k = 2 (2/L) G W_{k-1} - 2 W_{k-1} - W_{k-2},
+//            H += c_k W_k  (the s x s form, reading R19)
+//   line 12  P = H A: left Y = P, right Y = P^T
+// Sums run in fixed orders (deterministic).
+#include <algorithm>
+
+#include "common.cuh"
+#include "series.cuh"
+
+namespace cpa {
+
+struct SmallArgs {
+  const double* X;
+  int64_t ldx;
+  double* Y;
+  int64_t ldy;
+  int m, n;
+  SeriesParams* P;
+  cpa_svt_kernel kern;
+  int K, T;
+  double safety;
+  double lam_override;   // > 0: Lambda given, no power iteration
+  const double* c_given; // device, nullable
+  int nsq;               // squarings before the power iteration
+};
+
+constexpr int SM_THREADS = 128;   // 4 warps: one 32 x 32 quarter of a 64 x 64 DMMA tile each
+constexpr int LDP = 68;           // padded leading dimension of the s x s operands (conflict-free fragments)
+
+__device__ __forceinline__ double warp_sum_s(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// acc (this warp's 32 x 32 quarter of the 64 x 64 output tile at column n0) = A * B over k < kd,
+// on DMMA.8x8x4: A stored k-major (element (m, k) at A[k * lda + m]), B stored k-major
+// (element (k, n) at B[k * ldb + n]); every row / column / k beyond the operands' extent is
+// zero in shared memory, so padding contributes nothing.  acc[i][j][e] holds
+// C(wm + 8i + g, n0 + wn + 8j + 2t + e).
+__device__ __forceinline__ void dmma_tile(const double* A, int lda, const double* B, int ldb, int kd, int n0,
+                                          double (&acc)[4][4][2]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int kk = 0; kk < kd; kk += 4) {
+    double fa[4], fb[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) fa[i] = A[(kk + t) * lda + wm + i * 8 + g];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) fb[j] = B[(kk + t) * ldb + n0 + wn + j * 8 + g];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], fa[i], fb[j]);
+  }
+}
+
+// C (64 x 64 padded, ld LDP) = scale * A B for symmetric s x s operands (stored row-major,
+// which is the k-major form of a symmetric matrix).  C aliases neither A nor B.
+__device__ __forceinline__ void sq_product(const double* A, const double* B, double* C, int s, double scale) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  double acc[4][4][2];
+  dmma_tile(A, LDP, B, LDP, (s + 3) & ~3, 0, acc);
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) C[(wm + i * 8 + g) * LDP + wn + j * 8 + 2 * t + e] = acc[i][j][e] * scale;
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(SM_THREADS, 1) k_small_f64(SmallArgs a) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double s_red[SM_THREADS / 32];
+  __shared__ double s_v[64], s_u[64];
+  __shared__ double s_scal[2];
+  const bool left = a.m <= a.n;
+  const int s = left ? a.m : a.n, L = left ? a.n : a.m;
+  const int kL = (L + 3) & ~3, ldt = LDP, lda = ((L + 3) & ~3) + 4;
+  double* G = sm;                  // 64 x LDP each, zero outside s x s
+  double* Gp = G + 64 * LDP;       // c^p G^p, then H
+  double* Wa = Gp + 64 * LDP;
+  double* Wb = Wa + 64 * LDP;
+  double* Op = Wb + 64 * LDP;      // At (kL x LDP: k-major A^T) for line 1, A (64 x lda) for line 12
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3, wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  for (int e = tid; e < 4 * 64 * LDP; e += SM_THREADS) sm[e] = 0.0;
+  // ---- At(l, i) = A(i, l): right A = X^T so At = X (L = m rows); left A = X so At = X^T
+  for (int e = tid; e < kL * ldt; e += SM_THREADS) {
+    const int r = e / ldt, c = e % ldt;
+    double v = 0.0;
+    if (r < L && c < s) v = left ? a.X[(int64_t)c * a.ldx + r] : a.X[(int64_t)r * a.ldx + c];
+    Op[e] = v;
+  }
+  __syncthreads();
+  // ---- line 1: G = A A^T: G(i, j) = sum_l At(l, i) At(l, j)
+  {
+    double acc[4][4][2];
+    dmma_tile(Op, ldt, Op, ldt, kL, 0, acc);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) G[(wm + i * 8 + g) * LDP + wn + j * 8 + 2 * t + e] = acc[i][j][e];
+  }
+  __syncthreads();
+  // ---- line 3: power iteration
+  double lam = 0.0;
+  if (a.lam_override > 0.0) {
+    lam = a.lam_override / a.safety;
+  } else {
+    int p = 1, q = 0;
+    if (a.nsq > 0) {
+      if (tid == 0) {
+        double mx = 0.0;
+        for (int i = 0; i < s; ++i) mx = fmax(mx, G[i * LDP + i]);
+        const int e = (mx > 0.0 && isfinite(mx)) ? ilogb(mx) : 0;
+        s_scal[0] = ldexp(1.0, -2 * e);   // c^2, exact
+      }
+      __syncthreads();
+      sq_product(G, G, Gp, s, s_scal[0]);          // c^2 G^2
+      p = 2;
+      for (int j = 1; j < a.nsq && 2 * p <= a.T - 1; ++j) {
+        sq_product(Gp, Gp, Wa, s, 1.0);            // c^{2p} G^{2p}
+        for (int e = tid; e < 64 * LDP; e += SM_THREADS) Gp[e] = Wa[e];
+        __syncthreads();
+        p *= 2;
+      }
+      q = (a.T - 1) / p;
+    }
+    const int niter = a.T - (p - 1) * q;
+    for (int i = tid; i < 64; i += SM_THREADS) s_v[i] = i < s ? 1.0 / sqrt((double)s) : 0.0;
+    __syncthreads();
+    bool degenerate = false;
+    for (int it = 0; it < niter; ++it) {
+      const double* M = it < q ? Gp : G;
+      double u = 0.0;
+      if (tid < s)
+        for (int l = 0; l < s; ++l) u = fma(M[tid * LDP + l], s_v[l], u);
+      if (tid < 64) s_u[tid] = u;
+      const double sq = warp_sum_s(u * u);
+      if (lane == 0) s_red[warp] = sq;
+      __syncthreads();
+      if (tid == 0) {
+        double tot = 0.0;
+        for (int w = 0; w < SM_THREADS / 32; ++w) tot += s_red[w];
+        s_scal[1] = sqrt(tot);
+      }
+      __syncthreads();
+      lam = s_scal[1];
+      if (!(lam > kDegenerateLambda) || !(lam < 1e300)) { degenerate = true; break; }
+      if (tid < s) s_v[tid] = s_u[tid] / lam;
+      __syncthreads();
+    }
+    if (degenerate) lam = lam < 1e300 ? 0.0 : lam;
+  }
+  // ---- line 4
+  compute_series(a.P, a.kern, a.K, a.safety, lam, a.c_given);
+  __syncthreads();
+  const double s2 = a.P->scale2, s4 = 2.0 * s2;
+  // ---- lines 5-7: W_1 (Wa), H (Gp), zero outside s x s
+  double* H = Gp;
+  for (int e = tid; e < 64 * LDP; e += SM_THREADS) {
+    const int r = e / LDP, c = e % LDP;
+    const double id = (r == c && r < s) ? 1.0 : 0.0;
+    const double w = (r < s && c < s) ? s2 * G[e] - id : 0.0;
+    Wa[e] = w;
+    H[e] = 0.5 * a.P->c[0] * id + a.P->c[1] * w;
+  }
+  __syncthreads();
+  // ---- lines 8-11: W_k = s4 G W_{k-1} - 2 W_{k-1} - W_{k-2} over W_{k-2}, H += c_k W_k
+  double* Wp = Wa;   // W_{k-1}
+  double* Wq = Wb;   // W_{k-2} (k = 2: the identity, implicit)
+  const int ks = (s + 3) & ~3;
+  for (int k = 2; k < a.K; ++k) {
+    double acc[4][4][2];
+    dmma_tile(G, LDP, Wp, LDP, ks, 0, acc);
+    const double ck = a.P->c[k];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = wm + i * 8 + g, c = wn + j * 8 + 2 * t + e, o = r * LDP + c;
+          const double wpp = k == 2 ? ((r == c && r < s) ? 1.0 : 0.0) : Wq[o];
+          const double w = s4 * acc[i][j][e] - 2.0 * Wp[o] - wpp;   // W_k = 2 B_hat W_{k-1} - W_{k-2}
+          Wq[o] = w;                                                   // (read only by this thread)
+          H[o] += ck * w;                                              // H += c_k W_k
+        }
+    __syncthreads();
+    double* tmp = Wp;
+    Wp = Wq;
+    Wq = tmp;
+  }
+  // ---- line 12: P = H A (s x L; A(k, n) k-major = row-major A), right Y = P^T, left Y = P
+  for (int e = tid; e < 64 * lda; e += SM_THREADS) {
+    const int r = e / lda, c = e % lda;
+    double v = 0.0;
+    if (r < s && c < L) v = left ? a.X[(int64_t)r * a.ldx + c] : a.X[(int64_t)c * a.ldx + r];
+    Op[e] = v;
+  }
+  __syncthreads();
+  for (int n0 = 0; n0 < L; n0 += 64) {
+    double acc[4][4][2];
+    dmma_tile(H, LDP, Op, lda, ks, n0, acc);   // H symmetric: k-major H = row-major H
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = wm + i * 8 + g, c = n0 + wn + j * 8 + 2 * t + e;
+          if (r < s && c < L) {
+            if (left) a.Y[(int64_t)r * a.ldy + c] = acc[i][j][e];
+            else      a.Y[(int64_t)c * a.ldy + r] = acc[i][j][e];
+          }
+        }
+  }
+}
+
+size_t small_f64_smem(int64_t m, int64_t n) {
+  const int64_t s = m < n ? m : n, L = m < n ? n : m;
+  const int64_t kL = (L + 3) / 4 * 4, ncol = (L + 63) / 64 * 64;
+  const int64_t op = std::max(kL * LDP, 64 * (ncol + 4));   // At for line 1 / A for line 12
+  (void)s;
+  return (size_t)(4 * 64 * LDP + op) * sizeof(double);
+}
+bool small_f64_fits(int64_t m, int64_t n) {
+  const int64_t s = m < n ? m : n, L = m < n ? n : m;
+  return s >= 1 && s <= 64 && L <= 128 && small_f64_smem(m, n) <= 220 * 1024;
+}
+
+cudaError_t launch_small_f64(const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t m, int64_t n,
+                             SeriesParams* P, const cpa_svt_kernel& k, int K, int T, double safety,
+                             double lam_override, const double* c_given, int nsq, cudaStream_t st) {
+  SmallArgs a{};
+  a.X = X; a.ldx = ldx; a.Y = Y; a.ldy = ldy; a.m = (int)m; a.n = (int)n;
+  a.P = P; a.kern = k; a.K = K; a.T = T; a.safety = safety; a.lam_override = lam_override;
+  a.c_given = c_given; a.nsq = nsq;
+  const size_t smem = small_f64_smem(m, n);
+  cudaError_t e = cudaFuncSetAttribute(k_small_f64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_small_f64<<<1, SM_THREADS, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace cpa

@@ -306,3 +306,24 @@ def test_tma_kernels_against_cp_async_and_oracle(env, shape, K):
     assert O.rel_fro(Y_tma, Y_cpa) <= 1e-11
     Yo = O.cpa_shrink(X, O.Kernel(**kern), K, T=60)
     assert O.rel_fro(Y_tma, Yo) <= TOL64
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (7, 33), (33, 7), (64, 48), (48, 64), (64, 64), (40, 128), (128, 40)])
+def test_small_kernel_against_grid_path_and_oracle(env, shape):
+    """Small problems (s <= 64, L <= 128) run all of Alg. 1 in one thread block (form 4);
+    the grid path (CPA_SVT_NO_SMALL) and the oracle must agree with it."""
+    import os
+    X = W.random_dense(*shape, seed=3)
+    kern = {"kind": "soft", "tau": 0.2, "tau_relative": True}
+    Y1, i1 = _run(env, X, kern, 12, T=30)
+    os.environ["CPA_SVT_NO_SMALL"] = "1"
+    try:
+        Y2, i2 = _run(env, X, kern, 12, T=30)
+    finally:
+        del os.environ["CPA_SVT_NO_SMALL"]
+    assert i1["form"] == 4 and i2["form"] != 4
+    assert abs(i1["lambda_hat"] - i2["lambda_hat"]) <= 1e-12 * i2["lambda_hat"]
+    assert O.rel_fro(Y1, Y2) <= 1e-12
+    Yo, io = O.cpa_shrink(X, O.Kernel(**kern), 12, T=30, return_info=True)
+    assert abs(i1["lambda_hat"] - io["lambda_hat"]) <= 1e-12 * io["lambda_hat"]
+    assert O.rel_fro(Y1, Yo) <= TOL64

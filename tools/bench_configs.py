@@ -72,12 +72,16 @@ def dense(name, h, reps, m=None, n=None, K=None, dtype="f64", math="native"):
     s, L = min(m, n), max(m, n)
     # recurrence flops of the form that ran: 1 apply-to-X (K-1) 2 s^2 L; 2 symmetric s x s (K-2) s^2 (s+1)
     # (+ final 2 s^2 L); 3 s x s on full tiles (K-2) 2 s^3 (+ final)
-    rec = {1: (K - 1) * 2 * s * s * L, 2: (K - 2) * s * s * (s + 1), 3: (K - 2) * 2 * s ** 3}[form]
+    # 4: the whole SVT in one thread block (s <= 64, L <= 128): full s x s products, the step
+    #    phase is the whole kernel
+    rec = {1: (K - 1) * 2 * s * s * L, 2: (K - 2) * s * s * (s + 1), 3: (K - 2) * 2 * s ** 3,
+           4: (K - 2) * 2 * s ** 3}[form]
     F_exec = s * (s + 1) * L + rec + (0 if form == 1 else 2 * s * s * L)
     F_eff = s * (s + 1) * L + (K - 1) * 2 * s * s * L   # bench.py's fixed per-workload count
     step_ms = ph.get("step", (0, 0))[0] + (ph.get("init", (0, 0))[0] if form == 1 else 0)
     r = {"config": name, "shape": [m, n], "K": K, "T": T, "dtype": dtype, "math": math,
-         "form": {1: "apply-to-X", 2: "s x s symmetric", 3: "s x s full tiles"}[form], "ms_per_svt": ms,
+         "form": {1: "apply-to-X", 2: "s x s symmetric", 3: "s x s full tiles", 4: "s x s, one thread block"}[form],
+         "ms_per_svt": ms,
          "gflops_effective": F_eff / ms / 1e6, "gflops_executed": F_exec / ms / 1e6,
          "phases_ms": {k: v[0] for k, v in ph.items()},
          "recurrence_tflops": rec / step_ms / 1e9 if step_ms else None}
