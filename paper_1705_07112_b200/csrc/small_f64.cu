@@ -102,6 +102,14 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_f64(SmallArgs a) {
   double* Op = Wb + 64 * LDP;      // At (kL x LDP: k-major A^T) for line 1, A (64 x lda) for line 12
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3, wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+#ifdef CPA_SMALL_TRACE
+  long long stamp[8];
+  int ns = 0;
+  stamp[ns++] = clock64();
+#define STAMP() stamp[ns++] = clock64()
+#else
+#define STAMP()
+#endif
   for (int e = tid; e < 4 * 64 * LDP; e += SM_THREADS) sm[e] = 0.0;
   // ---- At(l, i) = A(i, l): right A = X^T so At = X (L = m rows); left A = X so At = X^T
   for (int e = tid; e < kL * ldt; e += SM_THREADS) {
@@ -123,6 +131,7 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_f64(SmallArgs a) {
         for (int e = 0; e < 2; ++e) G[(wm + i * 8 + g) * LDP + wn + j * 8 + 2 * t + e] = acc[i][j][e];
   }
   __syncthreads();
+  STAMP();
   // ---- line 3: power iteration
   double lam = 0.0;
   if (a.lam_override > 0.0) {
@@ -173,9 +182,11 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_f64(SmallArgs a) {
     }
     if (degenerate) lam = lam < 1e300 ? 0.0 : lam;
   }
+  STAMP();
   // ---- line 4
   compute_series(a.P, a.kern, a.K, a.safety, lam, a.c_given);
   __syncthreads();
+  STAMP();
   const double s2 = a.P->scale2, s4 = 2.0 * s2;
   // ---- lines 5-7: W_1 (Wa), H (Gp), zero outside s x s
   double* H = Gp;
@@ -212,6 +223,7 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_f64(SmallArgs a) {
     Wp = Wq;
     Wq = tmp;
   }
+  STAMP();
   // ---- line 12: P = H A (s x L; A(k, n) k-major = row-major A), right Y = P^T, left Y = P
   for (int e = tid; e < 64 * lda; e += SM_THREADS) {
     const int r = e / lda, c = e % lda;
@@ -236,6 +248,13 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_f64(SmallArgs a) {
           }
         }
   }
+#ifdef CPA_SMALL_TRACE
+  __syncthreads();
+  STAMP();
+  if (tid == 0)
+    for (int i = 0; i < ns; ++i) a.Y[i] = (double)(stamp[i] - stamp[0]);
+#endif
+#undef STAMP
 }
 
 size_t small_f64_smem(int64_t m, int64_t n) {
