@@ -45,45 +45,50 @@ __device__ __forceinline__ double warp_sum_s(double v) {
   return v;
 }
 
-// acc (this warp's 32 x 32 quarter of the 64 x 64 output tile at column n0) = A * B over k < kd,
-// on DMMA.8x8x4: A stored k-major (element (m, k) at A[k * lda + m]), B stored k-major
-// (element (k, n) at B[k * ldb + n]); every row / column / k beyond the operands' extent is
-// zero in shared memory, so padding contributes nothing.  acc[i][j][e] holds
+// The block's output tile is (16h x 16h) for h = ceil(ceil(s / 8) / 2) <= 4 8 x 8 DMMA tiles per
+// warp and dimension: warp w covers rows wm = 8h (w / 2) and columns wn = 8h (w % 2) of it, so
+// the four warps split the s x s products evenly (s = 48: 3 x 3 tiles each, no padding work).
+// acc = A * B over k < kd on DMMA.8x8x4: A stored k-major (element (m, k) at A[k * lda + m]),
+// B stored k-major (element (k, n) at B[k * ldb + n]); rows / columns / k beyond the operands'
+// extent are zero in shared memory.  acc[i][j][e] (i, j < h) holds
 // C(wm + 8i + g, n0 + wn + 8j + 2t + e).
-__device__ __forceinline__ void dmma_tile(const double* A, int lda, const double* B, int ldb, int kd, int n0,
+__device__ __forceinline__ void dmma_tile(const double* A, int lda, const double* B, int ldb, int kd, int n0, int h,
                                           double (&acc)[4][4][2]) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int wm = (warp >> 1) * 8 * h, wn = (warp & 1) * 8 * h;
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll 4
   for (int kk = 0; kk < kd; kk += 4) {
     double fa[4], fb[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) fa[i] = A[(kk + t) * lda + wm + i * 8 + g];
+    for (int i = 0; i < 4; ++i) fa[i] = i < h ? A[(kk + t) * lda + wm + i * 8 + g] : 0.0;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) fb[j] = B[(kk + t) * ldb + n0 + wn + j * 8 + g];
+    for (int j = 0; j < 4; ++j) fb[j] = j < h ? B[(kk + t) * ldb + n0 + wn + j * 8 + g] : 0.0;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], fa[i], fb[j]);
+      for (int j = 0; j < 4; ++j)
+        if (i < h && j < h) dmma_8x8x4(acc[i][j][0], acc[i][j][1], fa[i], fb[j]);
   }
 }
 
-// C (64 x 64 padded, ld LDP) = scale * A B for symmetric s x s operands (stored row-major,
-// which is the k-major form of a symmetric matrix).  C aliases neither A nor B.
-__device__ __forceinline__ void sq_product(const double* A, const double* B, double* C, int s, double scale) {
+// C (padded, ld LDP) = scale * A B for symmetric s x s operands (stored row-major, which is the
+// k-major form of a symmetric matrix).  C aliases neither A nor B.
+__device__ __forceinline__ void sq_product(const double* A, const double* B, double* C, int s, int h, double scale) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int wm = (warp >> 1) * 8 * h, wn = (warp & 1) * 8 * h;
   double acc[4][4][2];
-  dmma_tile(A, LDP, B, LDP, (s + 3) & ~3, 0, acc);
+  dmma_tile(A, LDP, B, LDP, (s + 3) & ~3, 0, h, acc);
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j)
+      if (i < h && j < h)
 #pragma unroll
-      for (int e = 0; e < 2; ++e) C[(wm + i * 8 + g) * LDP + wn + j * 8 + 2 * t + e] = acc[i][j][e] * scale;
+        for (int e = 0; e < 2; ++e) C[(wm + i * 8 + g) * LDP + wn + j * 8 + 2 * t + e] = acc[i][j][e] * scale;
   __syncthreads();
 }
 
@@ -101,7 +106,8 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_f64(SmallArgs a) {
   double* Wb = Wa + 64 * LDP;
   double* Op = Wb + 64 * LDP;      // At (kL x LDP: k-major A^T) for line 1, A (64 x lda) for line 12
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, t = lane & 3, wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int h = ((s + 7) / 8 + 1) / 2;   // 8 x 8 DMMA tiles per warp and dimension
+  const int g = lane >> 2, t = lane & 3, wm = (warp >> 1) * 8 * h, wn = (warp & 1) * 8 * h;
 #ifdef CPA_SMALL_TRACE
   long long stamp[8];
   int ns = 0;
@@ -122,13 +128,14 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_f64(SmallArgs a) {
   // ---- line 1: G = A A^T: G(i, j) = sum_l At(l, i) At(l, j)
   {
     double acc[4][4][2];
-    dmma_tile(Op, ldt, Op, ldt, kL, 0, acc);
+    dmma_tile(Op, ldt, Op, ldt, kL, 0, h, acc);
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j)
+        if (i < h && j < h)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) G[(wm + i * 8 + g) * LDP + wn + j * 8 + 2 * t + e] = acc[i][j][e];
+          for (int e = 0; e < 2; ++e) G[(wm + i * 8 + g) * LDP + wn + j * 8 + 2 * t + e] = acc[i][j][e];
   }
   __syncthreads();
   STAMP();
@@ -146,10 +153,10 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_f64(SmallArgs a) {
         s_scal[0] = ldexp(1.0, -2 * e);   // c^2, exact
       }
       __syncthreads();
-      sq_product(G, G, Gp, s, s_scal[0]);          // c^2 G^2
+      sq_product(G, G, Gp, s, h, s_scal[0]);          // c^2 G^2
       p = 2;
       for (int j = 1; j < a.nsq && 2 * p <= a.T - 1; ++j) {
-        sq_product(Gp, Gp, Wa, s, 1.0);            // c^{2p} G^{2p}
+        sq_product(Gp, Gp, Wa, s, h, 1.0);            // c^{2p} G^{2p}
         for (int e = tid; e < 64 * LDP; e += SM_THREADS) Gp[e] = Wa[e];
         __syncthreads();
         p *= 2;
@@ -204,12 +211,13 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_f64(SmallArgs a) {
   const int ks = (s + 3) & ~3;
   for (int k = 2; k < a.K; ++k) {
     double acc[4][4][2];
-    dmma_tile(G, LDP, Wp, LDP, ks, 0, acc);
+    dmma_tile(G, LDP, Wp, LDP, ks, 0, h, acc);
     const double ck = a.P->c[k];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j)
+        if (i < h && j < h)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int r = wm + i * 8 + g, c = wn + j * 8 + 2 * t + e, o = r * LDP + c;
@@ -232,13 +240,14 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_f64(SmallArgs a) {
     Op[e] = v;
   }
   __syncthreads();
-  for (int n0 = 0; n0 < L; n0 += 64) {
+  for (int n0 = 0; n0 < L; n0 += 16 * h) {
     double acc[4][4][2];
-    dmma_tile(H, LDP, Op, lda, ks, n0, acc);   // H symmetric: k-major H = row-major H
+    dmma_tile(H, LDP, Op, lda, ks, n0, h, acc);   // H symmetric: k-major H = row-major H
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j)
+        if (i < h && j < h)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int r = wm + i * 8 + g, c = n0 + wn + j * 8 + 2 * t + e;
@@ -262,7 +271,7 @@ size_t small_f64_smem(int64_t m, int64_t n) {
   const int64_t kL = (L + 3) / 4 * 4, ncol = (L + 63) / 64 * 64;
   const int64_t op = std::max(kL * LDP, 64 * (ncol + 4));   // At for line 1 / A for line 12
   (void)s;
-  return (size_t)(4 * 64 * LDP + op) * sizeof(double);
+  return (size_t)(4 * 64 * LDP + op + 64) * sizeof(double);   // (+64: line-12 fragment reads past the last row)
 }
 bool small_f64_fits(int64_t m, int64_t n) {
   const int64_t s = m < n ? m : n, L = m < n ? n : m;
