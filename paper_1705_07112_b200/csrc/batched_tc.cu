@@ -235,7 +235,7 @@ __device__ __forceinline__ void put_frag(uint8_t* hi, int row0, int q, const flo
 
 __global__ void __launch_bounds__(NT, 1) k_batched_tc(Args a) {
   extern __shared__ uint8_t raw[];
-  uint8_t* base = (uint8_t*)(((uintptr_t)raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* base = raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);   // (stays in the shared window: STS, not ST)
   uint8_t* sP = base;                 // A, then Psi_{k-1}, then H (A operand)
   uint8_t* sG = base + 2 * OPB;       // G (B operand of the steps)
   uint8_t* sAT = base + 4 * OPB;      // A^T (B operand of line 12)

@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(NTHR, 1)
   constexpr int NACC = Bufs<BN>::NACC, NSUM = Bufs<BN>::NSUM;
   constexpr int NSPLIT = TERMS == 3 ? 2 : 1;
   extern __shared__ uint8_t raw_smem[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)raw_smem + 1023) & ~(uintptr_t)1023);
+  uint8_t* smem = raw_smem + ((1024u - (smem_u32(raw_smem) & 1023u)) & 1023u);   // (stays in the shared window)
   float* epi_buf = (float*)(smem + ST * S::STAGE);
   uint64_t* full = (uint64_t*)(smem + ST * S::STAGE + S::EPI);
   uint64_t* empty = full + ST;
