@@ -905,22 +905,32 @@ __device__ __forceinline__ bool gemm_split_reduce(const GemmArgs& a, double (&ac
   }
   __syncthreads();
   if (!s_last) return false;
+  // the 8 accumulators of row group i, summed over the splits in the fixed order p = 0..S-1,
+  // four splits' loads in flight at a time (the register budget of three CTAs per SM)
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    double pv[8][8];  // the 8 accumulators of row group i from up to 8 splits, all loads in flight
+    double sum[8];
 #pragma unroll
-    for (int p = 0; p < 8; ++p)
+    for (int p0 = 0; p0 < 8; p0 += 4) {
+      if (p0 >= S) break;
+      double pv[4][8];
 #pragma unroll
-      for (int q8 = 0; q8 < 8; ++q8)
-        pv[p][q8] = p < S ? __ldcg(slot + (int64_t)p * (BM * BN) + (i * 8 + q8) * NTHREADS + threadIdx.x) : 0.0;
+      for (int p = 0; p < 4; ++p)
 #pragma unroll
-    for (int q8 = 0; q8 < 8; ++q8) {
-      double sum = pv[0][q8];
+        for (int q8 = 0; q8 < 8; ++q8)
+          pv[p][q8] = p0 + p < S ? __ldcg(slot + (int64_t)(p0 + p) * (BM * BN) + (i * 8 + q8) * NTHREADS + threadIdx.x)
+                                 : 0.0;
 #pragma unroll
-      for (int p = 1; p < 8; ++p)
-        if (p < S) sum += pv[p][q8];
-      acc[i][q8 >> 1][q8 & 1] = sum;
+      for (int q8 = 0; q8 < 8; ++q8) {
+        double v = p0 == 0 ? pv[0][q8] : sum[q8] + pv[0][q8];
+#pragma unroll
+        for (int p = 1; p < 4; ++p)
+          if (p0 + p < S) v += pv[p][q8];
+        sum[q8] = v;
+      }
     }
+#pragma unroll
+    for (int q8 = 0; q8 < 8; ++q8) acc[i][q8 >> 1][q8 & 1] = sum[q8];
   }
   return true;
 }
@@ -1020,7 +1030,7 @@ __device__ __forceinline__ void tma_operand(unsigned char* dst, const CUtensorMa
   }
 }
 template <bool A_ROWK, bool B_ROWK, int MODE>
-__global__ void __launch_bounds__(NTHREADS) k_dmma_gemm_tma(const __grid_constant__ GemmMaps mp, GemmArgs a) {
+__global__ void __launch_bounds__(NTHREADS, 3) k_dmma_gemm_tma(const __grid_constant__ GemmMaps mp, GemmArgs a) {
   extern __shared__ unsigned char gsm_raw[];
   __shared__ __align__(8) uint64_t full[TSTAGES], empty[TSTAGES];
   unsigned char* base = gsm_raw + ((1024u - (smem_u32(gsm_raw) & 1023u)) & 1023u);
