@@ -28,7 +28,7 @@ __all__ = [
     "cpa_shrink_columns", "cpa_shrink_rows", "cpa_shrink_batched",
     "sparse_power_iteration", "cpa_shrink_sparse_rows", "jacobi_svd",
     "exact_shrink", "svd_characterization", "rel_fro", "haar1_matrix", "cpa_shrink_transform",
-    "dct2_matrix", "synthetic_D", "admm_recover", "threshold_components",
+    "dct2_matrix", "dct2_block_matrix", "synthetic_D", "admm_recover", "threshold_components",
     "DEFAULT_SAFETY", "DEGENERATE_LAMBDA",
 ]
 
@@ -317,13 +317,14 @@ def cpa_shrink_transform(X, kernel: Kernel, K: int, T: int = 30, safety: float =
       lines 3-11 as in cpa_shrink, on Phi_ (s x s; Psi_0 = Id over the whole index space)
       line 12 G_hat(B) <- B T^T H_hat(Phi_) T
 
-    transform: "haar1" (haar1_matrix) or "dct" (dct2_matrix, orthonormal DCT-II).
+    transform: "haar1" (haar1_matrix), "dct" (dct2_matrix, orthonormal DCT-II) or "dct8"
+    (dct2_block_matrix: the 8 x 8 block DCT of PAPER.md:947).
     Orientation as cpa_shrink: a wide X (m <= n) runs on B = X^T (Gram X X^T)."""
     X = np.asarray(X, dtype=np.float64)
     m, n = X.shape
     B = X.T if m <= n else X
     s = B.shape[1]
-    Tm = haar1_matrix(s) if transform == "haar1" else dct2_matrix(s)
+    Tm = {"haar1": haar1_matrix, "dct": dct2_matrix, "dct8": dct2_block_matrix}[transform](s)
     # line 1
     Phi = Tm @ gram(B) @ Tm.T
     # line 2
@@ -373,6 +374,17 @@ def dct2_matrix(n: int) -> np.ndarray:
     C = np.cos(np.pi * (2 * j + 1) * k / (2 * n)) * math.sqrt(2.0 / n)
     C[0, :] = math.sqrt(1.0 / n)
     return C
+
+
+def dct2_block_matrix(n: int, b: int = 8) -> np.ndarray:
+    """Block DCT ("the block diagonal forms of the DCT (block DCT) whose block
+    size was 8x8"): T = blockdiag(C_b, ..., C_b, C_r) with C_b = dct2_matrix(b) and, when b does
+    not divide n, a last block C_r = dct2_matrix(n mod b) (reading R24)."""
+    T = np.zeros((n, n))
+    for i0 in range(0, n, b):
+        w = min(b, n - i0)
+        T[i0:i0 + w, i0:i0 + w] = dct2_matrix(w)
+    return T
 
 
 def synthetic_D(N: int, rank: int) -> np.ndarray:

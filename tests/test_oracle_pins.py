@@ -492,3 +492,44 @@ def test_dct_thresholded_is_exact_shrink_of_the_thresholded_gram():
     H = (V * hh) @ V.T
     assert O.rel_fro(Y, Tm.T @ H @ Tm @ X) <= 1e-11
     assert info["nnz"] >= 120
+
+
+# ---- NEXT-2 block DCT (block diagonal DCT with 8 x 8 blocks; reading R24)
+
+@pytest.mark.parametrize("n", [1, 5, 8, 16, 21])
+def test_block_dct_structure(n):
+    T = O.dct2_block_matrix(n)
+    assert np.allclose(T @ T.T, np.eye(n), atol=1e-14)
+    for i0 in range(0, n, 8):            # each diagonal block is the DCT-II of its size...
+        w = min(8, n - i0)
+        assert np.array_equal(T[i0:i0 + w, i0:i0 + w], O.dct2_matrix(w))
+        T[i0:i0 + w, i0:i0 + w] = 0.0
+    assert not T.any()                   # ...and nothing couples two blocks
+    # an 8-periodic signal constant on every block has only DC coefficients per block
+    y = np.repeat(np.arange(1.0, 4.0), 8)
+    c = O.dct2_block_matrix(24) @ y
+    assert np.allclose(np.delete(c, [0, 8, 16]), 0.0, atol=1e-13)
+
+
+@pytest.mark.parametrize("shape", [(20, 44), (44, 20)])
+def test_block_dct_keep_all_equals_identity_transform(shape):
+    X = np.random.default_rng(2).standard_normal(shape)
+    m, n = shape
+    kern = O.Kernel(kind="soft", tau=0.3, tau_relative=True)
+    lam = 1.01 * float(np.linalg.eigvalsh(X @ X.T if m <= n else X.T @ X)[-1])
+    Yb = O.cpa_shrink_transform(X, kern, 10, lam=lam, transform="dct8")
+    assert O.rel_fro(Yb, O.cpa_shrink(X, kern, 10, lam=lam)) <= 1e-12
+
+
+def test_block_dct_thresholded_is_exact_shrink_of_the_thresholded_gram():
+    X = np.random.default_rng(6).standard_normal((28, 45))
+    kern = O.Kernel(kind="soft", tau=0.2, tau_relative=True)
+    K = 9
+    Y, info = O.cpa_shrink_transform(X, kern, K, T=200, return_info=True, transform="dct8",
+                                      eps_mode="abs", eps=1.5)
+    Tm = O.dct2_block_matrix(28)
+    Phi_, _ = O.threshold_components(Tm @ (X @ X.T) @ Tm.T, "abs", 1.5)
+    w, V = np.linalg.eigh(Phi_)
+    hh = np.array([O.series_eval(info["coeffs"], info["lambda_max"], x) for x in w])
+    assert O.rel_fro(Y, Tm.T @ ((V * hh) @ V.T) @ Tm @ X) <= 1e-11
+    assert 0 < info["nnz"] < 28 * 28
