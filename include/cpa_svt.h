@@ -186,7 +186,7 @@ cpa_svt_status cpa_svt_apply_batched(cpa_svt_handle* h, int64_t batch, int m, in
                                      const cpa_svt_lambda* lam, float* lambda_out);
 
 /* NEXT-2 component threshold of Alg. 1 line 2 (eq. threshold_components) for
- * CPA_SVT_OPT_TRANSFORM = 2 (DCT): mode 0 keeps every component; 1 keeps |Phi_ij| >= value;
+ * CPA_SVT_OPT_TRANSFORM = 2 or 3 (DCT, block DCT): mode 0 keeps every component; 1 keeps |Phi_ij| >= value;
  * 2 keeps |Phi_ij| >= the value-th largest |Phi_ij| (ties kept; value >= 1).
  * Errors: E_ARG (null, mode), E_DOMAIN (value < 0, or < 1 for mode 2). */
 cpa_svt_status cpa_svt_set_epsilon(cpa_svt_handle* h, int mode, double value);
@@ -230,7 +230,9 @@ typedef enum {
                                on the low-pass half and line 12 applies B T^T H_hat(Phi_) T; 2 =
                                orthonormal DCT-II of the Gram index, Phi = T G T^T thresholded per
                                cpa_svt_set_epsilon, the recurrence on the sparse Phi_ (CSR) when a
-                               threshold is set.  fp64 dense, unsharded only (else
+                               threshold is set; 3 = the 8 x 8 block DCT (T =
+                               blockdiag of 8 x 8 DCT-II blocks, a smaller last block when 8 does not
+                               divide s), otherwise as 2.  fp64 dense, unsharded only (else
                                CPA_SVT_E_UNSUPPORTED). */,
   CPA_SVT_OPT_BATCHED = 2   /* engine of cpa_svt_apply_batched: 0 = auto (tcgen05), 1 = fp32 FFMA (exact
                                fp32 products, apply-to-X form), 2 = tcgen05 3xTF32 (s x s form,

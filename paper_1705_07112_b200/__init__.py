@@ -168,8 +168,9 @@ class Handle:
 
     def set_transform(self, transform: str):
         """cpa_svt_set_option(TRANSFORM): 'none' (T = I) | 'haar1' (one-level Haar DWT of the Gram
-        index, high-frequency components of Phi set to 0; NEXT-2)."""
-        self._check(lib.cpa_svt_set_option(self._h, 1, {"none": 0, "haar1": 1, "dct": 2}[transform]),
+        index, high-frequency components of Phi set to 0; NEXT-2) | 'dct'
+        (orthonormal DCT-II) | 'dct8' (8 x 8 block DCT)."""
+        self._check(lib.cpa_svt_set_option(self._h, 1, {"none": 0, "haar1": 1, "dct": 2, "dct8": 3}[transform]),
                     "cpa_svt_set_option")
 
     def set_epsilon(self, mode: str = "none", value: float = 0.0):

@@ -46,6 +46,7 @@ cudaError_t dct_sparse_steps(int64_t s, const int64_t* rp, const int32_t* col, c
                              double* Wb, double* H, const SeriesParams* P, int K, int num_sms, cudaStream_t st);
 // admm.cu
 cudaError_t admm_dct(double* C, double* CT, int64_t n, int num_sms, cudaStream_t st);
+cudaError_t block_dct_sandwich(const double* A, double* out, int64_t s, int inverse, cudaStream_t st);
 cudaError_t admm_sub(const double* a, const double* b, double* out, int64_t N, cudaStream_t st);
 cudaError_t admm_l(const double* z1, const double* u1, const double* pt, const uint8_t* mask, const double* D,
                    const double* u3, const double* z4, const double* u4, double* l, double* t, int64_t N,
@@ -377,7 +378,7 @@ cpa_svt_status cpa_svt_set_option(cpa_svt_handle* h, cpa_svt_option opt, int64_t
     return CPA_SVT_OK;
   }
   if (opt == CPA_SVT_OPT_TRANSFORM) {
-    if (value < 0 || value > 2) return CPA_SVT_E_ARG;
+    if (value < 0 || value > 3) return CPA_SVT_E_ARG;
     h->transform = (int)value;
     return CPA_SVT_OK;
   }
@@ -597,7 +598,8 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
   }
   const int64_t s = left ? m : n, L = left ? n : m;
   const bool sharded = shard != CPA_SVT_SHARD_NONE && h->world > 1;
-  const bool dct = h->transform == 2;      // NEXT-2 DCT variant (Phi = C G C^T, thresholded)
+  const bool dct = h->transform == 2 || h->transform == 3;   // NEXT-2 DCT variants (Phi = C G C^T, thresholded)
+  const bool bdct = h->transform == 3;     // 8 x 8 block DCT
   const bool sparse_eps = dct && h->eps_mode != 0;
   if (dct && sharded) return CPA_SVT_E_UNSUPPORTED;
   // small problems (s <= 64, L <= 128, e.g. BASELINE configs[0]): all of Alg. 1 in one
@@ -721,10 +723,16 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
     Cd = (double*)h->tws;
     CTd = Cd + nS;
     Phase p(h, CPA_SVT_PH_GRAM);
-    CU(admm_dct(Cd, CTd, s, h->num_sms, h->stream));
-    CU(dense_gemm_store(s, s, s, Cd, s, G, s, Wa, s, h->stream));    // C G
-    CU(dense_gemm_store(s, s, s, Wa, s, CTd, s, G, s, h->stream));   // (C G) C^T
-    launches += 3;
+    if (bdct) {   // block-diagonal C: Phi = C G C^T block pair by block pair
+      CU(block_dct_sandwich(G, Wa, s, 0, h->stream));
+      CU(cudaMemcpyAsync(G, Wa, (size_t)s * s * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+      launches += 1;
+    } else {
+      CU(admm_dct(Cd, CTd, s, h->num_sms, h->stream));
+      CU(dense_gemm_store(s, s, s, Cd, s, G, s, Wa, s, h->stream));    // C G
+      CU(dense_gemm_store(s, s, s, Wa, s, CTd, s, G, s, h->stream));   // (C G) C^T
+      launches += 3;
+    }
     if (sparse_eps) {
       CU(dct_eps_threshold(G, s, h->eps_mode, h->eps_value, (void*)(CTd + nS), h->num_sms, h->stream, &csr_rp,
                            &csr_col, &csr_val));
@@ -802,7 +810,11 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
     Phase p(h, CPA_SVT_PH_FINAL);
     // (split-K over the k = s dimension when the tiles alone leave slots idle: c2 111 -> 96 us)
     const double* Hm = H;
-    if (dct) {  // line 12 with T: Y = (C^T H C) X  or  X (C^T H C)
+    if (bdct) {  // line 12 with T: Y = (C^T H C) X  or  X (C^T H C), C block diagonal
+      CU(block_dct_sandwich(H, Wb, s, 1, h->stream));
+      launches += 1;
+      Hm = Wb;
+    } else if (dct) {
       CU(dense_gemm_store(s, s, s, CTd, s, H, s, Wa, s, h->stream));
       CU(dense_gemm_store(s, s, s, Wa, s, Cd, s, Wb, s, h->stream));
       launches += 2;

@@ -117,6 +117,47 @@ __global__ void __launch_bounds__(256) k_sparse_sym_step(int64_t s, const int64_
   }
 }
 
+// NEXT-2 block DCT (reading R24): C = blockdiag(C_8, ..., C_8, C_r), C_w the
+// orthonormal DCT-II of size w (C_w[k][j] = a_k cos(pi (2j + 1) k / (2w)), a_0 = sqrt(1/w),
+// a_k = sqrt(2/w)), r = s mod 8 for a ragged last block.  out = C A C^T (inverse = 0) or
+// C^T A C (inverse = 1) for an s x s A: one 64-thread CTA per 8 x 8 block pair,
+// out_IJ = C_wI A_IJ C_wJ^T (or the transposed factors) -- 16 FMAs per element instead of
+// two dense s^3 products.  Fixed summation order.
+__global__ void __launch_bounds__(64) k_block_dct_sandwich(const double* __restrict__ A, double* __restrict__ out,
+                                                           int64_t s, int inverse) {
+  __shared__ double sA[8][8], sT[8][8], sCi[8][8], sCj[8][8];
+  const int64_t nb = (s + 7) / 8;
+  const int64_t bi = blockIdx.x / nb, bj = blockIdx.x % nb;
+  const int64_t i0 = bi * 8, j0 = bj * 8;
+  const int wi = (int)min((int64_t)8, s - i0), wj = (int)min((int64_t)8, s - j0);
+  const int r = threadIdx.x >> 3, c = threadIdx.x & 7;
+  auto dctc = [](int w, int k, int j) {   // C_w[k][j]
+    if (k >= w || j >= w) return 0.0;
+    const double a = k == 0 ? sqrt(1.0 / w) : sqrt(2.0 / w);
+    return a * cos(3.141592653589793238462643383279502884 * (double)((2 * j + 1) * k) / (double)(2 * w));
+  };
+  sCi[r][c] = dctc(wi, r, c);
+  sCj[r][c] = dctc(wj, r, c);
+  sA[r][c] = (r < wi && c < wj) ? A[(i0 + r) * s + j0 + c] : 0.0;
+  __syncthreads();
+  // T = F_I A_IJ, F_I = C_wI (forward) or C_wI^T (inverse)
+  double t = 0.0;
+  for (int p = 0; p < 8; ++p) t = fma(inverse ? sCi[p][r] : sCi[r][p], sA[p][c], t);
+  sT[r][c] = t;
+  __syncthreads();
+  // out_IJ = T F_J^T
+  double o = 0.0;
+  for (int q = 0; q < 8; ++q) o = fma(sT[r][q], inverse ? sCj[q][c] : sCj[c][q], o);
+  if (r < wi && c < wj) out[(i0 + r) * s + j0 + c] = o;
+}
+
+cudaError_t block_dct_sandwich(const double* A, double* out, int64_t s, int inverse, cudaStream_t st) {
+  const int64_t nb = (s + 7) / 8;
+  if (nb * nb > INT32_MAX) return cudaErrorInvalidValue;
+  k_block_dct_sandwich<<<(unsigned)(nb * nb), 64, 0, st>>>(A, out, s, inverse);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------------------------- host
 size_t dct_eps_scratch_bytes(int64_t s) {
   const size_t N = (size_t)s * s;

@@ -62,12 +62,12 @@ def test_transform_unsupported_paths(env):
 
 # ---- DCT variant with component thresholding
 
-def _gap_k(X, target, rel=1e-6):
+def _gap_k(X, target, rel=1e-6, tmat=None):
     """A k near `target` where the k-th and (k+1)-th largest |Phi_ij| differ by more than `rel`
     relative: the kept set is then the same on both sides whatever the rounding of Phi."""
     m, n = X.shape
     B = X.T if m <= n else X
-    Tm = O.dct2_matrix(B.shape[1])
+    Tm = (tmat or O.dct2_matrix)(B.shape[1])
     a = np.sort(np.abs(Tm @ (B.T @ B) @ Tm.T).ravel())[::-1]
     for d in range(0, a.size):
         for k in (target + d, target - d):
@@ -107,6 +107,44 @@ def test_dct_parity(dct_env, shape, eps, kind, K):
     kern = {"kind": kind, "tau": 0.1, "tau_relative": True}
     Y, info = h.apply(torch.from_numpy(X).cuda(), kern, K, T=200, info=True)
     Yo, io = O.cpa_shrink_transform(X, O.Kernel(**kern), K, T=200, return_info=True, transform="dct",
+                                    eps_mode=None if mode == "none" else mode, eps=val)
+    assert abs(info["lambda_hat"] - io["lambda_hat"]) <= 1e-11 * io["lambda_hat"]
+    assert O.rel_fro(Y.cpu().numpy(), Yo) <= TOL64, (shape, eps, kind, K)
+
+
+# ---- 8 x 8 block DCT (reading R24): ragged last blocks included
+
+@pytest.fixture(scope="module")
+def bdct_env():
+    import torch
+    import paper_1705_07112_b200 as P
+    h = P.Handle(0)
+    h.set_transform("dct8")
+    yield torch, P, h
+    h.close()
+
+
+@pytest.mark.parametrize("shape", [(64, 128), (130, 70), (7, 9), (257, 300)])
+@pytest.mark.parametrize("eps", [("none", 0), ("abs", 0.1), ("topk", 0.05)])
+@pytest.mark.parametrize("kind,K", [("soft", 15), ("hard", 6)])
+def test_block_dct_parity(bdct_env, shape, eps, kind, K):
+    torch, P, h = bdct_env
+    X = W.gen_c2(m=shape[0], n=shape[1], seed=shape[0] * 5 + shape[1] + K)
+    mode, val = eps
+    s = min(shape)
+    if mode == "topk":
+        val = _gap_k(X, max(1, int(val * s * s)), tmat=O.dct2_block_matrix)
+    if mode == "abs":   # an absolute epsilon in a gap of |Phi|
+        m, n = X.shape
+        B = X.T if m <= n else X
+        Tm = O.dct2_block_matrix(B.shape[1])
+        a = np.sort(np.abs(Tm @ (B.T @ B) @ Tm.T).ravel())[::-1]
+        k = _gap_k(X, max(1, int(val * a.size)), tmat=O.dct2_block_matrix)
+        val = 0.5 * (a[k - 1] + a[k])
+    h.set_epsilon(mode, val)
+    kern = {"kind": kind, "tau": 0.1, "tau_relative": True}
+    Y, info = h.apply(torch.from_numpy(X).cuda(), kern, K, T=200, info=True)
+    Yo, io = O.cpa_shrink_transform(X, O.Kernel(**kern), K, T=200, return_info=True, transform="dct8",
                                     eps_mode=None if mode == "none" else mode, eps=val)
     assert abs(info["lambda_hat"] - io["lambda_hat"]) <= 1e-11 * io["lambda_hat"]
     assert O.rel_fro(Y.cpu().numpy(), Yo) <= TOL64, (shape, eps, kind, K)
