@@ -1,7 +1,8 @@
 """NEXT-2 measurement on the paper's own inpainting shape (context, not a BASELINE config):
 2560 x 1920 fp64 stand-in (workloads.gen_pinpaint), soft threshold 1/rho = 6,
 K = 20: plain CPA (T = I), CPA with the one-level Haar DWT (high band of Phi zeroed,
-PAPER.md:628-630), and the exact EVD-based shrinkage, on one B200.  The paper's CPU times
+PAPER.md:628-630), with the DCT and the 8 x 8 block DCT (keep-all and top-k thresholds), and the
+exact EVD-based shrinkage, on one B200.  The paper's CPU times
 (Table I): 2.00 s (alpha = 20, DWT) and 2.48 s (EVD)."""
 import json, os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -21,6 +22,10 @@ variants = [("none", None, 0), ("haar1", None, 0), ("dct", None, 0)]
 # the paper's top-k thresholds k1..k3 = (0.5e-4, 1.5e-4, 0.5e-3) n^2, n = Gram side
 for name, frac in (("k1", 0.5e-4), ("k2", 1.5e-4), ("k3", 0.5e-3)):
     variants.append((f"dct_{name}", "topk", max(1, int(frac * s_ * s_))))
+# the 8 x 8 block DCT, keep-all and the same top-k thresholds
+variants.append(("dct8", None, 0))
+for name, frac in (("k1", 0.5e-4), ("k2", 1.5e-4), ("k3", 0.5e-3)):
+    variants.append((f"dct8_{name}", "topk", max(1, int(frac * s_ * s_))))
 Ys = {}
 for name, mode, val in variants:
     h = P.Handle(0)
