@@ -29,6 +29,7 @@ __all__ = [
     "sparse_power_iteration", "cpa_shrink_sparse_rows", "jacobi_svd",
     "exact_shrink", "svd_characterization", "rel_fro", "haar1_matrix", "cpa_shrink_transform",
     "dct2_matrix", "dct2_block_matrix", "synthetic_D", "admm_recover", "threshold_components",
+    "epsilon_schedule_k",
     "DEFAULT_SAFETY", "DEGENERATE_LAMBDA",
 ]
 
@@ -396,8 +397,18 @@ def synthetic_D(N: int, rank: int) -> np.ndarray:
     return D
 
 
+def epsilon_schedule_k(E: float, n: int) -> int:
+    """The recommended threshold of eq. recommendation_epsilon: epsilon(E_t)
+    = the k-th largest |Phi_|, k = (0.5e-4) n^2 if E_t > E_l, (1.5e-4) n^2 if E_l >= E_t > E_m,
+    (0.5e-3) n^2 otherwise, E_l = 0.3e-1, E_m = 6e-4, n x n the size of Phi_.
+    k = max(1, floor(.)) (reading R25)."""
+    frac = 0.5e-4 if E > 0.3e-1 else (1.5e-4 if E > 6e-4 else 0.5e-3)
+    return max(1, int(frac * n * n))
+
+
 def admm_recover(D_obs, mask, kernel: Kernel, K: int, T: int, rho: float, eta: float,
-                 max_iter: int = 300, tol: float = 1e-4, shrink=None, return_history: bool = False):
+                 max_iter: int = 300, tol: float = 1e-4, shrink=None, return_history: bool = False,
+                 transform: str | None = None, adaptive_eps: bool = False):
     """ADMM of PAPER.md:1193-1214 (eq. admm_algorithm_inp) for the synthetic experiment
     (PAPER.md:1095-1100): the average-term constraint z^(5) is dropped, so
     K l = [l; Psi l; Omega l; l] with Psi = 2-D orthonormal DCT (C_m L C_n^T) and Omega the
@@ -409,13 +420,24 @@ def admm_recover(D_obs, mask, kernel: Kernel, K: int, T: int, rho: float, eta: f
       z3  <- D_obs on the observed entries     (Pi_I keeps the assigned values)
       z4  <- clip(l + u4, 0, 1)                (Pi_D)
       u   <- u + K l - z
-    stopping: ||l_{t+1} - l_t|| / ||l_{t+1}|| < tol (PAPER.md:694 footnote).  z, u start at 0."""
+    stopping: ||l_{t+1} - l_t|| / ||l_{t+1}|| < tol (PAPER.md:694 footnote).  z, u start at 0.
+    transform: the shrinkage runs cpa_shrink_transform with this T ("dct" / "dct8" / "haar1");
+    adaptive_eps: its components are thresholded at epsilon(E) of epsilon_schedule_k with E the
+    previous iteration's ||dl|| / ||l|| (the first iteration: E = inf; reading R25)."""
     D_obs = np.asarray(D_obs, dtype=np.float64)
     w = np.asarray(mask, dtype=np.float64)
     m, n = D_obs.shape
     Cm, Cn = dct2_matrix(m), dct2_matrix(n)
     psi = lambda X: Cm @ X @ Cn.T
     psit = lambda S: Cm.T @ S @ Cn
+    E_prev = [math.inf]
+    if shrink is None and transform is not None:
+        def shrink(X):
+            s_ = min(X.shape)
+            if adaptive_eps:
+                return cpa_shrink_transform(X, kernel, K, T=T, transform=transform, eps_mode="topk",
+                                            eps=epsilon_schedule_k(E_prev[0], s_))
+            return cpa_shrink_transform(X, kernel, K, T=T, transform=transform)
     if shrink is None:
         shrink = lambda X: cpa_shrink(X, kernel, K, T=T)
     z1 = np.zeros((m, n)); z2 = np.zeros((m, n)); z4 = np.zeros((m, n))
@@ -437,6 +459,7 @@ def admm_recover(D_obs, mask, kernel: Kernel, K: int, T: int, rho: float, eta: f
         u4 = u4 + l - z4
         rel = float(np.linalg.norm(l - l_prev) / max(np.linalg.norm(l), 1e-300))
         hist.append(rel)
+        E_prev[0] = rel
         if rel < tol:
             break
     return (l, hist) if return_history else l

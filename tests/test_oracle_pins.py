@@ -533,3 +533,40 @@ def test_block_dct_thresholded_is_exact_shrink_of_the_thresholded_gram():
     hh = np.array([O.series_eval(info["coeffs"], info["lambda_max"], x) for x in w])
     assert O.rel_fro(Y, Tm.T @ ((V * hh) @ V.T) @ Tm @ X) <= 1e-11
     assert 0 < info["nnz"] < 28 * 28
+
+
+# ---- NEXT-2 adaptive epsilon of the ADMM (eq. recommendation_epsilon)
+
+def test_epsilon_schedule_k_breakpoints():
+    n = 1000                                     # k1..k3 of PAPER.md:1074-1076 at n = 1000
+    assert O.epsilon_schedule_k(float("inf"), n) == 50
+    assert O.epsilon_schedule_k(0.031, n) == 50
+    assert O.epsilon_schedule_k(0.03, n) == 150   # E_l >= E > E_m
+    assert O.epsilon_schedule_k(6.01e-4, n) == 150
+    assert O.epsilon_schedule_k(6e-4, n) == 500   # otherwise
+    assert O.epsilon_schedule_k(0.0, n) == 500
+    assert O.epsilon_schedule_k(1.0, 10) == 1     # never below one component
+
+
+def test_admm_adaptive_eps_uses_the_schedule(monkeypatch):
+    """The adaptive ADMM thresholds iteration t's shrinkage at the schedule's k for the error of
+    iteration t - 1 (E = inf first): the k passed to every shrink call is recorded and checked
+    against the returned error history."""
+    from oracle import cpa_oracle as CO
+    rng = np.random.default_rng(3)
+    D = O.synthetic_D(200, 4)
+    mask = (rng.random(D.shape) >= 0.1).astype(float)
+    kern = O.Kernel(kind="soft", tau=1.0, tau_relative=False)
+    seen = []
+    real = CO.cpa_shrink_transform
+    def spy(X, *a, **kw):
+        seen.append((kw.get("eps_mode"), kw.get("eps"), kw.get("transform")))
+        return real(X, *a, **kw)
+    monkeypatch.setattr(CO, "cpa_shrink_transform", spy)
+    L, hist = O.admm_recover(D * mask, mask, kern, 8, 30, rho=1.0, eta=0.01, max_iter=5, tol=0.0,
+                             transform="dct", adaptive_eps=True, return_history=True)
+    assert len(seen) == len(hist) == 5
+    want = [O.epsilon_schedule_k(E, 200) for E in [float("inf")] + hist[:-1]]
+    assert [k for _, k, _ in seen] == want
+    assert all(mode == "topk" and tr == "dct" for mode, _, tr in seen)
+    assert want[0] == 2 and np.isfinite(L).all()
