@@ -210,6 +210,13 @@ typedef struct {
   double last_rel;        /* out: last ||l_{t+1} - l_t|| / ||l_{t+1}|| */
   double ms_shrink;       /* out: CUDA-event time inside the CPA shrinkage calls */
   double ms_total;        /* out: CUDA-event time of the whole loop */
+  int32_t adaptive_eps;   /* in: 1 = threshold the transform-domain Gram of every shrinkage at the
+                             recommended epsilon(E_t) (eq. recommendation_epsilon):
+                             the k-th largest |Phi_ij|, k = (0.5e-4 | 1.5e-4 | 0.5e-3) s^2 for the
+                             previous iteration's E > 0.03 | > 6e-4 | otherwise (first: 0.5e-4 s^2);
+                             needs CPA_SVT_OPT_TRANSFORM 2 or 3 (else E_ARG); 0 = the handle's own
+                             cpa_svt_set_epsilon setting */
+  int32_t reserved;
 } cpa_svt_admm;
 cpa_svt_status cpa_svt_admm_recover(cpa_svt_handle* h, int64_t m, int64_t n, const double* D,
                                     const unsigned char* mask, int K, const cpa_svt_lambda* lam,

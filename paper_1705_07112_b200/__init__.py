@@ -37,7 +37,8 @@ class Kernel(ctypes.Structure):
 class Admm(ctypes.Structure):
     _fields_ = [("rho", ctypes.c_double), ("eta", ctypes.c_double), ("tol", ctypes.c_double),
                 ("max_iter", ctypes.c_int32), ("iters", ctypes.c_int32), ("last_rel", ctypes.c_double),
-                ("ms_shrink", ctypes.c_double), ("ms_total", ctypes.c_double)]
+                ("ms_shrink", ctypes.c_double), ("ms_total", ctypes.c_double),
+                ("adaptive_eps", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 class Lambda(ctypes.Structure):
@@ -264,16 +265,17 @@ class Handle:
         return Y
 
     def admm_recover(self, D, mask, K: int, rho: float, eta: float, T: int = 30, tol: float = 1e-4,
-                     max_iter: int = 300, safety: float = 1.01, L=None):
+                     max_iter: int = 300, safety: float = 1.01, L=None, adaptive_eps: bool = False):
         """cpa_svt_admm_recover (NEXT-3): ADMM recovery of the observed entries of D (float64 CUDA
-        m x n) under a uint8 CUDA mask (nonzero = observed); returns (L, info)."""
+        m x n) under a uint8 CUDA mask (nonzero = observed); returns (L, info).  adaptive_eps: the
+        recommended epsilon(E_t) schedule of PAPER.md:968-975 (needs set_transform('dct'|'dct8'))."""
         torch = self._torch
         assert D.is_cuda and D.dtype == torch.float64 and D.is_contiguous() and D.dim() == 2
         assert mask.is_cuda and mask.dtype == torch.uint8 and mask.shape == D.shape and mask.is_contiguous()
         if L is None:
             L = torch.empty_like(D)
         lam = self._lambda(T, safety, 0.0, False)
-        opt = Admm(float(rho), float(eta), float(tol), int(max_iter), 0, 0.0, 0.0, 0.0)
+        opt = Admm(float(rho), float(eta), float(tol), int(max_iter), 0, 0.0, 0.0, 0.0, int(bool(adaptive_eps)), 0)
         st = lib.cpa_svt_admm_recover(self._h, D.shape[0], D.shape[1], D.data_ptr(), mask.data_ptr(), K,
                                       ctypes.byref(lam), ctypes.byref(opt), L.data_ptr())
         self._check(st, "cpa_svt_admm_recover")

@@ -1140,6 +1140,17 @@ cpa_svt_status cpa_svt_admm_recover(cpa_svt_handle* h, int64_t m, int64_t n, con
   kern.tau_relative = 0;
   cpa_svt_lambda lm = *lam;
   lm.want_lambda = 0;
+  // adaptive epsilon (eq. recommendation_epsilon; reading R25): the k-th
+  // largest |Phi_ij| with k from the previous iteration's error, the handle's setting restored after
+  if (opt->adaptive_eps && h->transform != 2 && h->transform != 3) return CPA_SVT_E_ARG;
+  const int saved_mode = h->eps_mode;
+  const double saved_value = h->eps_value;
+  const int64_t s_adm = std::min(m, n);
+  auto eps_k = [&](double E) {
+    const double frac = E > 0.3e-1 ? 0.5e-4 : (E > 6e-4 ? 1.5e-4 : 0.5e-3);
+    return std::max(1.0, std::floor(frac * (double)s_adm * (double)s_adm));
+  };
+  double E_prev = INFINITY;
   cudaEvent_t e0, e1, ea, eb;
   cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventCreate(&ea); cudaEventCreate(&eb);
   cudaEventRecord(ea, h->stream);
@@ -1160,7 +1171,15 @@ cpa_svt_status cpa_svt_admm_recover(cpa_svt_handle* h, int64_t m, int64_t n, con
     CU(dense_gemm_store(m, n, n, A1, n, CnT, n, pl, n, h->stream));
     // z1 = prox_{1/rho ||.||_*}(l + u1): the CPA shrinkage
     cudaEventRecord(e0, h->stream);
+    if (opt->adaptive_eps) {
+      h->eps_mode = 2;
+      h->eps_value = eps_k(E_prev);
+    }
     st = apply_f64(h, m, n, CPA_SVT_SHARD_NONE, 0, t, n, z1, n, &kern, K, nullptr, &lm, nullptr);
+    if (opt->adaptive_eps) {
+      h->eps_mode = saved_mode;
+      h->eps_value = saved_value;
+    }
     if (st != CPA_SVT_OK) return st;
     cudaEventRecord(e1, h->stream);
     CU(admm_tail(l, lprev, pl, z1, mask, D, z2, z4, u1, u2, u3, u4, opt->eta / opt->rho, N, part, h->stream));
@@ -1175,6 +1194,7 @@ cpa_svt_status cpa_svt_admm_recover(cpa_svt_handle* h, int64_t m, int64_t n, con
       b += hp[2 * i + 1];
     }
     rel = sqrt(a) / fmax(sqrt(b), 1e-300);
+    E_prev = rel;
     h->launches += 9;
     if (rel < opt->tol) {
       ++it;
