@@ -634,14 +634,21 @@ __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB) k_cheb_sym(SymArgs a)
 constexpr int TBK = 16, TSTAGES = CPA_TMA_STAGES;
 constexpr int BOX_BYTES = 16 * TBK * 8;          // 16 doubles x TBK rows
 constexpr int TSTAGE_BYTES = 8 * BOX_BYTES;      // A: 4 boxes (64 m), B: 4 boxes (64 n)
+
 struct SymMaps {
   CUtensorMap g;
   CUtensorMap w[3];
 };
+// SBK-deep slabs in an SSTAGES ring: <16, 4> (64 KB) for short units (c2: ~11 slabs each),
+// <32, 2> (64 KB, half the mbarrier round trips) for long ones (s >= 4096: c5 shape 608 ->
+// 586 ms; at c2 it costs 1.27 -> 1.39 ms).
+template <int SBK, int SSTAGES>
 __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB)
     k_cheb_sym_tma(const __grid_constant__ SymMaps mp, SymArgs a) {
+  constexpr int SBOX_BYTES = 16 * SBK * 8;
+  constexpr int SSTAGE_BYTES = 8 * SBOX_BYTES;
   extern __shared__ unsigned char tsm_raw[];
-  __shared__ __align__(8) uint64_t full[TSTAGES], empty[TSTAGES];
+  __shared__ __align__(8) uint64_t full[SSTAGES], empty[SSTAGES];
   __shared__ int s_ticket;
   // 1024-byte aligned ring (the 128-byte swizzle pattern repeats every 1024 bytes); pointer
   // arithmetic on the __shared__ array keeps the fragment loads in the shared window (LDS)
@@ -652,12 +659,12 @@ __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB)
   const int per_step = ntri * S;
   const int total = (a.K - 2) * per_step;
   int* cross = a.sync + 1;
-  const int nk = (int)((a.s + TBK - 1) / TBK);
+  const int nk = (int)((a.s + SBK - 1) / SBK);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
   if (threadIdx.x == 0) {
-    for (int st = 0; st < TSTAGES; ++st) {
+    for (int st = 0; st < SSTAGES; ++st) {
       mbar_init(full + st, 1);
       mbar_init(empty + st, 4);
     }
@@ -671,8 +678,8 @@ __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB)
 #pragma unroll
     for (int h = 0; h < 2; ++h) coff[par][h] = ((((h * 8 + g) >> 1) ^ (2 * t + par)) << 4) | ((g & 1) * 8);
   const uint32_t roff = 256 * t;
-  const uint32_t boxa = (wm >> 4) * BOX_BYTES, boxb = (4 + (wn >> 4)) * BOX_BYTES;
-  uint32_t it = 0;  // slabs consumed by this CTA so far (stage = it % TSTAGES, phase = it / TSTAGES)
+  const uint32_t boxa = (wm >> 4) * SBOX_BYTES, boxb = (4 + (wn >> 4)) * SBOX_BYTES;
+  uint32_t it = 0;  // slabs consumed by this CTA so far (stage = it % SSTAGES, phase = it / SSTAGES)
   for (;;) {
     if (threadIdx.x == 0) s_ticket = atomicAdd(a.sync, 1);
     __syncthreads();
@@ -690,28 +697,28 @@ __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB)
     const int nku = ke - kb;
     if (threadIdx.x == 0) {
       // prologue: the static G slabs before the dependency wait, the W_{k-1} slabs after it
-      const int P = nku < TSTAGES - 1 ? nku : TSTAGES - 1;
+      const int P = nku < SSTAGES - 1 ? nku : SSTAGES - 1;
       for (int p = 0; p < P; ++p) {
-        const uint32_t sl = it + p, st = sl % TSTAGES;
-        mbar_wait(empty + st, ((sl / TSTAGES) & 1) ^ 1);
-        mbar_expect_tx(full + st, TSTAGE_BYTES);
+        const uint32_t sl = it + p, st = sl % SSTAGES;
+        mbar_wait(empty + st, ((sl / SSTAGES) & 1) ^ 1);
+        mbar_expect_tx(full + st, SSTAGE_BYTES);
         for (int b = 0; b < 4; ++b)
-          tma_load_2d(base + st * TSTAGE_BYTES + b * BOX_BYTES, &mp.g, m0 + 16 * b, (kb + p) * TBK, full + st);
+          tma_load_2d(base + st * SSTAGE_BYTES + b * SBOX_BYTES, &mp.g, m0 + 16 * b, (kb + p) * SBK, full + st);
       }
       if (k >= 3) wait_geq(cross + (k - 1) * T + tj, T);
       if (k >= 4) wait_geq(cross + (k - 2) * T + ti, T);
       fence_proxy_async_global();   // generic-proxy W_{k-1} stores of other CTAs -> TMA reads
       for (int p = 0; p < P; ++p) {
-        const uint32_t st = (it + p) % TSTAGES;
+        const uint32_t st = (it + p) % SSTAGES;
         for (int b = 0; b < 4; ++b)
-          tma_load_2d(base + st * TSTAGE_BYTES + (4 + b) * BOX_BYTES, wmap, n0 + 16 * b, (kb + p) * TBK, full + st);
+          tma_load_2d(base + st * SSTAGE_BYTES + (4 + b) * SBOX_BYTES, wmap, n0 + 16 * b, (kb + p) * SBK, full + st);
       }
     }
     // The epilogue's generic loads of W_{k-1}, W_{k-2} and H must be ordered after thread 0's
     // acquire of the dependency: every warp waits on the full barrier of a refilled slab, whose
     // expect_tx arrive thread 0 made after that acquire (release -> acquire at CTA scope); a
-    // unit too short to refill (nku < TSTAGES) takes a CTA barrier instead.
-    if (nku < TSTAGES) __syncthreads();
+    // unit too short to refill (nku < SSTAGES) takes a CTA barrier instead.
+    if (nku < SSTAGES) __syncthreads();
     else __syncwarp();
     double acc[4][4][2];
 #pragma unroll
@@ -719,32 +726,32 @@ __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB)
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     for (int kt = 0; kt < nku; ++kt) {
-      if (threadIdx.x == 0 && kt + TSTAGES - 1 < nku) {   // refill the stage of slab kt-1
-        const int kn = kt + TSTAGES - 1;
-        const uint32_t sl = it + kn, st = sl % TSTAGES;
-        mbar_wait(empty + st, ((sl / TSTAGES) & 1) ^ 1);
-        mbar_expect_tx(full + st, TSTAGE_BYTES);
-        unsigned char* d = base + st * TSTAGE_BYTES;
-        for (int b = 0; b < 4; ++b) tma_load_2d(d + b * BOX_BYTES, &mp.g, m0 + 16 * b, (kb + kn) * TBK, full + st);
+      if (threadIdx.x == 0 && kt + SSTAGES - 1 < nku) {   // refill the stage of slab kt-1
+        const int kn = kt + SSTAGES - 1;
+        const uint32_t sl = it + kn, st = sl % SSTAGES;
+        mbar_wait(empty + st, ((sl / SSTAGES) & 1) ^ 1);
+        mbar_expect_tx(full + st, SSTAGE_BYTES);
+        unsigned char* d = base + st * SSTAGE_BYTES;
+        for (int b = 0; b < 4; ++b) tma_load_2d(d + b * SBOX_BYTES, &mp.g, m0 + 16 * b, (kb + kn) * SBK, full + st);
         for (int b = 0; b < 4; ++b)
-          tma_load_2d(d + (4 + b) * BOX_BYTES, wmap, n0 + 16 * b, (kb + kn) * TBK, full + st);
+          tma_load_2d(d + (4 + b) * SBOX_BYTES, wmap, n0 + 16 * b, (kb + kn) * SBK, full + st);
       }
       __syncwarp();
-      const uint32_t sl = it + kt, st = sl % TSTAGES;
-      mbar_wait(full + st, (sl / TSTAGES) & 1);
-      const unsigned char* sa = base + st * TSTAGE_BYTES + boxa;
-      const unsigned char* sb = base + st * TSTAGE_BYTES + boxb;
+      const uint32_t sl = it + kt, st = sl % SSTAGES;
+      mbar_wait(full + st, (sl / SSTAGES) & 1);
+      const unsigned char* sa = base + st * SSTAGE_BYTES + boxa;
+      const unsigned char* sb = base + st * SSTAGE_BYTES + boxb;
 #pragma unroll
-      for (int kk = 0; kk < TBK / 4; ++kk) {
+      for (int kk = 0; kk < SBK / 4; ++kk) {
         const int par = kk & 1;
         const uint32_t ro = 1024 * (kk >> 1) + 128 * par + roff;
         double fa[4], fb[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-          fa[i] = *reinterpret_cast<const double*>(sa + (i >> 1) * BOX_BYTES + ro + coff[par][i & 1]);
+          fa[i] = *reinterpret_cast<const double*>(sa + (i >> 1) * SBOX_BYTES + ro + coff[par][i & 1]);
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          fb[j] = *reinterpret_cast<const double*>(sb + (j >> 1) * BOX_BYTES + ro + coff[par][j & 1]);
+          fb[j] = *reinterpret_cast<const double*>(sb + (j >> 1) * SBOX_BYTES + ro + coff[par][j & 1]);
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -1445,30 +1452,31 @@ cudaError_t dense_cheb_sym(int64_t s, const double* G, double* W0, double* W1, d
     EncodeTiledFn fn = encode_fn();
     SymMaps mp;
     bool ok = fn != nullptr;
+    const int sbk = s >= 4096 ? 32 : 16;   // slab depth of the k_cheb_sym_tma instance (see there)
     const double* ops[4] = {G, W0, W1, W2};
     CUtensorMap* maps[4] = {&mp.g, &mp.w[0], &mp.w[1], &mp.w[2]};
     for (int i = 0; i < 4 && ok; ++i) {
       cuuint64_t dims[2] = {(cuuint64_t)s, (cuuint64_t)s};
       cuuint64_t strides[1] = {(cuuint64_t)(s * sizeof(double))};
-      cuuint32_t box[2] = {16u, (cuuint32_t)TBK};
+      cuuint32_t box[2] = {16u, (cuuint32_t)sbk};
       cuuint32_t estr[2] = {1u, 1u};
       ok = fn(maps[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)ops[i], dims, strides, box, estr,
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
     }
     if (ok) {
-      const size_t tsmem = (size_t)TSTAGES * TSTAGE_BYTES + 1024;
-      e = cudaFuncSetAttribute(k_cheb_sym_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
+      // both instances use a 64 KB ring: 4 x 16-deep or 2 x 32-deep stages
+      const size_t tsmem = (size_t)4 * 8 * (16 * 16 * 8) + 1024;
+      auto kf = sbk == 32 ? k_cheb_sym_tma<32, 2> : k_cheb_sym_tma<16, 4>;
+      e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
       if (e != cudaSuccess) return e;
       int per_sm = 0;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cheb_sym_tma, NTHREADS, tsmem) != cudaSuccess ||
-          per_sm < 1)
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kf, NTHREADS, tsmem) != cudaSuccess || per_sm < 1)
         return cudaErrorLaunchOutOfResources;
       int64_t tgrid = (int64_t)num_sms * per_sm;
       if (tgrid > total) tgrid = total;
       void* targs[] = {&mp, &a};
-      return cudaLaunchCooperativeKernel((void*)k_cheb_sym_tma, dim3((unsigned)tgrid), dim3(NTHREADS), targs, tsmem,
-                                         st);
+      return cudaLaunchCooperativeKernel((void*)kf, dim3((unsigned)tgrid), dim3(NTHREADS), targs, tsmem, st);
     }
   }
   void* args[] = {&a};
