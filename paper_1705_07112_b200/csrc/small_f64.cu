@@ -52,7 +52,8 @@ __device__ __forceinline__ double warp_sum_s(double v) {
 // B stored k-major (element (k, n) at B[k * ldb + n]); rows / columns / k beyond the operands'
 // extent are zero in shared memory.  acc[i][j][e] (i, j < h) holds
 // C(wm + 8i + g, n0 + wn + 8j + 2t + e).
-__device__ __forceinline__ void dmma_tile(const double* A, int lda, const double* B, int ldb, int kd, int n0, int h,
+template <int h>
+__device__ __forceinline__ void dmma_tile(const double* A, int lda, const double* B, int ldb, int kd, int n0,
                                           double (&acc)[4][4][2]) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int wm = (warp >> 1) * 8 * h, wn = (warp & 1) * 8 * h;
@@ -77,11 +78,12 @@ __device__ __forceinline__ void dmma_tile(const double* A, int lda, const double
 
 // C (padded, ld LDP) = scale * A B for symmetric s x s operands (stored row-major, which is the
 // k-major form of a symmetric matrix).  C aliases neither A nor B.
-__device__ __forceinline__ void sq_product(const double* A, const double* B, double* C, int s, int h, double scale) {
+template <int h>
+__device__ __forceinline__ void sq_product(const double* A, const double* B, double* C, int s, double scale) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int wm = (warp >> 1) * 8 * h, wn = (warp & 1) * 8 * h;
   double acc[4][4][2];
-  dmma_tile(A, LDP, B, LDP, (s + 3) & ~3, 0, h, acc);
+  dmma_tile<h>(A, LDP, B, LDP, (s + 3) & ~3, 0, acc);
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -92,6 +94,7 @@ __device__ __forceinline__ void sq_product(const double* A, const double* B, dou
   __syncthreads();
 }
 
+template <int h>   // 8 x 8 DMMA tiles per warp and dimension: ceil(ceil(s / 8) / 2)
 __global__ void __launch_bounds__(SM_THREADS, 1) k_small_f64(SmallArgs a) {
   extern __shared__ __align__(16) double sm[];
   __shared__ double s_red[SM_THREADS / 32];
@@ -106,7 +109,6 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_f64(SmallArgs a) {
   double* Wb = Wa + 64 * LDP;
   double* Op = Wb + 64 * LDP;      // At (kL x LDP: k-major A^T) for line 1, A (64 x lda) for line 12
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int h = ((s + 7) / 8 + 1) / 2;   // 8 x 8 DMMA tiles per warp and dimension
   const int g = lane >> 2, t = lane & 3, wm = (warp >> 1) * 8 * h, wn = (warp & 1) * 8 * h;
 #ifdef CPA_SMALL_TRACE
   long long stamp[8];
@@ -128,7 +130,7 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_f64(SmallArgs a) {
   // ---- line 1: G = A A^T: G(i, j) = sum_l At(l, i) At(l, j)
   {
     double acc[4][4][2];
-    dmma_tile(Op, ldt, Op, ldt, kL, 0, h, acc);
+    dmma_tile<h>(Op, ldt, Op, ldt, kL, 0, acc);
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -153,10 +155,10 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_f64(SmallArgs a) {
         s_scal[0] = ldexp(1.0, -2 * e);   // c^2, exact
       }
       __syncthreads();
-      sq_product(G, G, Gp, s, h, s_scal[0]);          // c^2 G^2
+      sq_product<h>(G, G, Gp, s, s_scal[0]);          // c^2 G^2
       p = 2;
       for (int j = 1; j < a.nsq && 2 * p <= a.T - 1; ++j) {
-        sq_product(Gp, Gp, Wa, s, h, 1.0);            // c^{2p} G^{2p}
+        sq_product<h>(Gp, Gp, Wa, s, 1.0);            // c^{2p} G^{2p}
         for (int e = tid; e < 64 * LDP; e += SM_THREADS) Gp[e] = Wa[e];
         __syncthreads();
         p *= 2;
@@ -211,7 +213,7 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_f64(SmallArgs a) {
   const int ks = (s + 3) & ~3;
   for (int k = 2; k < a.K; ++k) {
     double acc[4][4][2];
-    dmma_tile(G, LDP, Wp, LDP, ks, 0, h, acc);
+    dmma_tile<h>(G, LDP, Wp, LDP, ks, 0, acc);
     const double ck = a.P->c[k];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
@@ -242,7 +244,7 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_f64(SmallArgs a) {
   __syncthreads();
   for (int n0 = 0; n0 < L; n0 += 16 * h) {
     double acc[4][4][2];
-    dmma_tile(H, LDP, Op, lda, ks, n0, h, acc);   // H symmetric: k-major H = row-major H
+    dmma_tile<h>(H, LDP, Op, lda, ks, n0, acc);   // H symmetric: k-major H = row-major H
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -286,9 +288,12 @@ cudaError_t launch_small_f64(const double* X, int64_t ldx, double* Y, int64_t ld
   a.P = P; a.kern = k; a.K = K; a.T = T; a.safety = safety; a.lam_override = lam_override;
   a.c_given = c_given; a.nsq = nsq;
   const size_t smem = small_f64_smem(m, n);
-  cudaError_t e = cudaFuncSetAttribute(k_small_f64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int64_t s = m < n ? m : n;
+  const int h = (int)(((s + 7) / 8 + 1) / 2);
+  auto kf = h == 1 ? k_small_f64<1> : h == 2 ? k_small_f64<2> : h == 3 ? k_small_f64<3> : k_small_f64<4>;
+  cudaError_t e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_small_f64<<<1, SM_THREADS, smem, st>>>(a);
+  kf<<<1, SM_THREADS, smem, st>>>(a);
   return cudaGetLastError();
 }
 
