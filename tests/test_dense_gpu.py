@@ -327,3 +327,15 @@ def test_small_kernel_against_grid_path_and_oracle(env, shape):
     Yo, io = O.cpa_shrink(X, O.Kernel(**kern), 12, T=30, return_info=True)
     assert abs(i1["lambda_hat"] - io["lambda_hat"]) <= 1e-12 * io["lambda_hat"]
     assert O.rel_fro(Y1, Yo) <= TOL64
+
+
+@pytest.mark.parametrize("shape", [(40, 56), (150, 90)])
+def test_max_order(env, shape):
+    """K = CPA_SVT_KMAX (512) on the single-block path (40 x 56) and the grid path (150 x 90):
+    the coefficients of the 512-point rule and 510 recurrence steps against the oracle."""
+    X = W.random_dense(*shape, seed=21)
+    kern = {"kind": "soft", "tau": 0.25, "tau_relative": True}
+    Y, info = _run(env, X, kern, 512, T=60)
+    Yo, io = O.cpa_shrink(X, O.Kernel(**kern), 512, T=60, return_info=True)
+    assert abs(info["lambda_hat"] - io["lambda_hat"]) <= 1e-12 * io["lambda_hat"]
+    assert O.rel_fro(Y, Yo) <= TOL64
