@@ -161,6 +161,31 @@ def gen_pinpaint(seed: int = 0, m: int = 2560, n: int = 1920) -> np.ndarray:
     return X + 0.02 * rng.standard_normal((m, n))
 
 
+def gen_pvideo(seed: int = 0, h: int = 360, w: int = 240, frames: int = 5000, blocks: int = 173) -> np.ndarray:
+    """Context shape (not a BASELINE config, SURVEY 8d 'p-video'): a stand-in for the paper's
+    86400 x 5000 background-modeling matrix (pixels x frames, values in
+    [0, 1]): a rank-1 static background (a smooth [0, 1] frame repeated in every column) plus
+    `blocks` 5 x 5 foreground blocks per frame (~5% of the pixels) moving at constant
+    velocities, set to random [0, 1] values.  Seeded; no arithmetic of the method."""
+    rng = np.random.default_rng(seed)
+    yy, xx = np.meshgrid(np.arange(h), np.arange(w), indexing="ij")
+    bg = np.zeros((h, w))
+    for _ in range(4):
+        fy, fx = rng.uniform(0.002, 0.02, 2)
+        bg += rng.uniform(0.5, 1.0) * np.cos(2 * np.pi * fy * yy + rng.uniform(0, 6.3)) * np.cos(
+            2 * np.pi * fx * xx + rng.uniform(0, 6.3))
+    bg = (bg - bg.min()) / (bg.max() - bg.min())
+    X = np.repeat(bg.reshape(-1, 1), frames, axis=1)             # (h w) x frames, Fortran-free copy
+    y0, x0 = rng.uniform(0, h, blocks), rng.uniform(0, w, blocks)
+    vy, vx = rng.uniform(-0.5, 0.5, blocks), rng.uniform(-0.5, 0.5, blocks)
+    dy, dx = np.meshgrid(np.arange(5), np.arange(5), indexing="ij")
+    for t in range(frames):
+        py = (np.floor(y0 + vy * t).astype(np.int64) % (h - 5))[:, None] + dy.reshape(1, -1)
+        px = (np.floor(x0 + vx * t).astype(np.int64) % (w - 5))[:, None] + dx.reshape(1, -1)
+        X[(py * w + px).ravel(), t] = rng.random(blocks * 25)
+    return X
+
+
 def synthetic_D(N: int, rank: int) -> np.ndarray:
     """The paper's synthetic data: D = J - blkdiag(0.5 1 1^T) with `rank`
     diagonal blocks of size N / rank.  Deterministic; no arithmetic of the method."""
