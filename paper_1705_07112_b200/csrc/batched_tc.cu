@@ -24,9 +24,12 @@
 // rows of 32 fp32, 8-row atoms, 16-byte chunk c of row r at c ^ (r & 7)), two 8 KB
 // k-blocks per 64 x 64 operand; descriptors as in tc_tf32.cu.  TMEM layout for M = 64
 // (probed, tools/probes/tc_m64_probe.cu): row r of D lives in lane 32 (r / 16) + r % 16,
-// column j in column j -- so lanes 0..15 of each warp own the 64 rows (16 per warp).
-// TMEM columns [0, 64): D.  The epilogue reads D with tcgen05.ld.16x256b (all 32 threads of a
-// warp: 2 rows x 16 columns each); Psi_{k-1}, Psi_{k-2} and H stay in registers in that layout.
+// column j in column j -- so lanes 0..15 of each lane quarter own the 64 rows (16 per quarter).
+// TMEM columns [0, 64): D.  Eight warps: warp w reads rows 16 (w % 4) .. +15 (its quarter) and
+// columns 32 (w / 4) .. +31 with tcgen05.ld.16x256b.x4 (all 32 threads: 2 rows x 8 columns
+// each); Psi_{k-1}, Psi_{k-2} and H stay in registers in that layout.  Eight warps instead of
+// four halve the epilogue between two MMAs, which is exposed (tensor pipe idle) whenever
+// the other CTA on the SM is in its own epilogue.
 #include <cstdlib>
 
 #include "common.cuh"
@@ -34,7 +37,9 @@
 namespace cpa {
 namespace btc {
 
-constexpr int NT = 128;                 // threads per CTA (4 warps, 16 D rows each)
+constexpr int NT = 256;                 // threads per CTA (8 warps: warp w owns D rows 16 (w % 4) .. +15,
+                                        // columns 32 (w / 4) .. +31 -- a TMEM lane quarter is warp w % 4's)
+constexpr int NW = NT / 32;
 constexpr int OPB = 64 * 64 * 4;        // bytes of one 64 x 64 fp32 operand (two 8 KB k-blocks)
 
 __device__ __forceinline__ uint32_t sw(int r, int k) {  // byte offset of (r, k) in a K-major SW128 operand
@@ -172,40 +177,35 @@ struct Args {
 // smem: [A (hi, lo) -> Psi / H operand] [G (hi, lo)] [A^T (hi, lo)]  (3 x 32 KB, 1 KB aligned)
 constexpr int SMEM = 3 * 2 * OPB + 1024;
 
-// tcgen05.ld.16x256b.x8: the 16 rows x 64 columns of D in this warp's lane quarter, spread
-// over all 32 threads (probed, tools/probes/tc_m64_probe.cu): thread t holds rows
-// r0 = t/4 and r1 = t/4 + 8 (warp-local), columns 8c + 2(t%4) + {0, 1}, c = 0..7, as
+// tcgen05.ld.16x256b.x4: 16 rows x 32 columns of D in this warp's lane quarter, spread over
+// all 32 threads (probed, tools/probes/tc_m64_probe.cu): thread t holds rows r0 = t/4 and
+// r1 = t/4 + 8 (warp-local), columns 8c + 2(t%4) + {0, 1}, c = 0..3 (relative to the address), as
 // v[4c + 0] = (r0, 8c+2q), v[4c + 1] = (r0, 8c+2q+1), v[4c + 2] = (r1, 8c+2q), v[4c + 3] = (r1, 8c+2q+1).
-__device__ __forceinline__ void ld_frag(uint32_t taddr, float (&v)[32]) {
-  uint32_t r[32];
+constexpr int FR = 16;   // fragment elements per thread
+__device__ __forceinline__ void ld_frag(uint32_t taddr, float (&v)[FR]) {
+  uint32_t r[FR];
   asm volatile(
-      "tcgen05.ld.sync.aligned.16x256b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      "tcgen05.ld.sync.aligned.16x256b.x4.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+  for (int i = 0; i < FR; ++i) v[i] = __uint_as_float(r[i]);
 }
 // store a fragment (layout of ld_frag) as TF32 hi / lo A operands in TMEM (same layout)
-__device__ __forceinline__ void st_frag_hl(uint32_t t_hi, uint32_t t_lo, const float (&v)[32]) {
-  uint32_t h[32], l[32];
+__device__ __forceinline__ void st_frag_hl(uint32_t t_hi, uint32_t t_lo, const float (&v)[FR]) {
+  uint32_t h[FR], l[FR];
 #pragma unroll
-  for (int i = 0; i < 32; ++i) {
+  for (int i = 0; i < FR; ++i) {
     const float x = v[i], hx = rna(x);
     h[i] = __float_as_uint(hx);
     l[i] = __float_as_uint(rna(x - hx));
   }
 #define BTC_ST16(addr, r)                                                                                          \
-  asm volatile("tcgen05.st.sync.aligned.16x256b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16," \
-               "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};\n" ::"r"(addr),                    \
-               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),     \
-               "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),         \
-               "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),        \
-               "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])                     \
+  asm volatile("tcgen05.st.sync.aligned.16x256b.x4.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n" \
+               ::"r"(addr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),  \
+               "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])          \
                : "memory")
   BTC_ST16(t_hi, h);
   BTC_ST16(t_lo, l);
@@ -219,12 +219,12 @@ __device__ __forceinline__ void sync_tmem_for_mma() {
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
 }
 // write a fragment (layout of ld_frag) as TF32 hi / lo operand rows: element (row, col) at sw(row, col)
-__device__ __forceinline__ void put_frag(uint8_t* hi, int row0, int q, const float (&v)[32]) {
+__device__ __forceinline__ void put_frag(uint8_t* hi, int row0, int col0, const float (&v)[FR]) {
 #pragma unroll
-  for (int c = 0; c < 8; ++c)
+  for (int c = 0; c < FR / 4; ++c)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int r = row0 + 8 * h, k = 8 * c + 2 * q;
+      const int r = row0 + 8 * h, k = col0 + 8 * c;
       const float x0 = v[4 * c + 2 * h], x1 = v[4 * c + 2 * h + 1];
       const float h0 = rna(x0), h1 = rna(x1);
       const uint32_t o = sw(r, k);
@@ -233,7 +233,7 @@ __device__ __forceinline__ void put_frag(uint8_t* hi, int row0, int q, const flo
     }
 }
 
-__global__ void __launch_bounds__(NT, 1) k_batched_tc(Args a) {
+__global__ void __launch_bounds__(NT, 2) k_batched_tc(Args a) {
   extern __shared__ uint8_t raw[];
   uint8_t* base = raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);   // (stays in the shared window: STS, not ST)
   uint8_t* sP = base;                 // A, then Psi_{k-1}, then H (A operand)
@@ -242,21 +242,24 @@ __global__ void __launch_bounds__(NT, 1) k_batched_tc(Args a) {
   __shared__ uint64_t bar;
   __shared__ uint32_t tslot;
   __shared__ float sV2[2][64];
-  __shared__ float sRed2[2][4];
-  __shared__ float sRed[4];
+  __shared__ float sU2[2][2][64];   // per column half: partial row sums of a power product
+  __shared__ float sRed2[2][NW / 2];
+  __shared__ float sRed[NW];
   __shared__ double sNode[128];   // K <= 128 on the batched path (cpa_svt_apply_batched)
   __shared__ double sHn[128];
   __shared__ float sC[128];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int q = lane & 3;
-  const int row0 = warp * 16 + (lane >> 2), row1 = row0 + 8;    // this thread's two D rows
-  const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+  const int q = lane & 3, wq = warp & 3, ch = warp >> 2;
+  const int row0 = wq * 16 + (lane >> 2), row1 = row0 + 8;      // this thread's two D rows
+  const int col0 = 32 * ch + 2 * q;                              // and its first column
+  // TMEM address of this warp's fragment: lane quarter wq, column half ch
+  const uint32_t lane_off = ((uint32_t)(wq * 32) << 16) + 32u * ch;
   const bool left = a.m <= a.n;
   const int s = left ? a.m : a.n, L = left ? a.n : a.m;
   const int K = a.K;
   const int64_t mn = (int64_t)a.m * a.n;
-  auto colof = [&](int e) { return 8 * (e >> 2) + 2 * q + (e & 1); };
+  auto colof = [&](int e) { return col0 + 8 * (e >> 2) + (e & 1); };
   // 64 x 64 matrices at 16-byte aligned addresses take the vector load path (A = X)
   const bool full64 = a.m == 64 && a.n == 64 && ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0);
   auto rowof = [&](int e) { return (e & 2) ? row1 : row0; };
@@ -282,13 +285,14 @@ __global__ void __launch_bounds__(NT, 1) k_batched_tc(Args a) {
     // ---- load A (s x L, zero-padded to 64 x 64) as operand rows (sP) and A^T rows (sAT);
     //      all of the thread's global loads in flight before the first conversion
     {
-      float4 v[8];
+      constexpr int NIT = 1024 / NT;
+      float4 v[NIT];
       if (full64) {
 #pragma unroll
-        for (int it = 0; it < 8; ++it) v[it] = __ldg(reinterpret_cast<const float4*>(X) + it * NT + tid);
+        for (int it = 0; it < NIT; ++it) v[it] = __ldg(reinterpret_cast<const float4*>(X) + it * NT + tid);
       } else {
 #pragma unroll
-        for (int it = 0; it < 8; ++it) {
+        for (int it = 0; it < NIT; ++it) {
           const int e = it * NT + tid, i = e >> 4, j = (e & 15) * 4;   // A(i, j..j+3)
           float t4[4];
 #pragma unroll
@@ -300,7 +304,7 @@ __global__ void __launch_bounds__(NT, 1) k_batched_tc(Args a) {
         }
       }
 #pragma unroll
-      for (int it = 0; it < 8; ++it) {
+      for (int it = 0; it < NIT; ++it) {
         const int e = it * NT + tid, i = e >> 4, j = (e & 15) * 4;
         put4(sP, i, j, v[it].x, v[it].y, v[it].z, v[it].w);
         put(sAT, j, i, v[it].x);
@@ -315,7 +319,7 @@ __global__ void __launch_bounds__(NT, 1) k_batched_tc(Args a) {
     mbar_wait(&bar, phase);
     phase ^= 1;
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    float g[32];
+    float g[FR];
     ld_frag(tD + lane_off, g);
     // ---- line 3: Lambda_max by T power steps (fp32, fixed order).  Repeated squaring (as the
     //      dense path, reading R6): v_{T-1} ~ G^{T-1} v_0 through q = (T-1)/4 products by
@@ -326,23 +330,25 @@ __global__ void __launch_bounds__(NT, 1) k_batched_tc(Args a) {
       lam_hat = a.lam_override / a.safety;
     } else {
       const int qsq = a.T >= 8 ? (a.T - 1) / 4 : 0;
-      float g4[32];
+      float g4[FR];
       if (qsq > 0) {
         float dmax = 0.f;
 #pragma unroll
-        for (int e = 0; e < 32; ++e)
+        for (int e = 0; e < FR; ++e)
           if (rowof(e) == colof(e)) dmax = fmaxf(dmax, g[e]);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
         if (lane == 0) sRed[warp] = dmax;
         __syncthreads();
-        dmax = fmaxf(fmaxf(sRed[0], sRed[1]), fmaxf(sRed[2], sRed[3]));
+        dmax = sRed[0];
+#pragma unroll
+        for (int w = 1; w < NW; ++w) dmax = fmaxf(dmax, sRed[w]);
         const float cs = (dmax > 0.f && isfinite(dmax)) ? ldexpf(1.f, -ilogbf(dmax)) : 1.f;
 #pragma unroll
-        for (int e = 0; e < 32; ++e) g4[e] = cs * g[e];
+        for (int e = 0; e < FR; ++e) g4[e] = cs * g[e];
         for (int sq = 0; sq < 2; ++sq) {               // (cG)^2, then (c^2 G^2)^2
           st_frag_hl(tAh + lane_off, tAl + lane_off, g4);
-          put_frag(sG, row0, q, g4);
+          put_frag(sG, row0, col0, g4);
           sync_for_mma();
           if (tid == 0) btc::mma64_ts(tD, tAh, tAl, sG, &bar);
           mbar_wait(&bar, phase);
@@ -353,8 +359,9 @@ __global__ void __launch_bounds__(NT, 1) k_batched_tc(Args a) {
           __syncthreads();                             // everyone has read D and the operands
         }
       }
-      // one CTA barrier per product: u_t = G v_{t-1} with v_{t-1} = u_{t-1} / ||u_{t-1}|| folded
-      // in as a scale of the product; u_t and the partial ||u_t||^2 go to ping-pong buffers
+      // u_t = G v_{t-1} with v_{t-1} = u_{t-1} / ||u_{t-1}|| folded in as a scale of the product:
+      // each column half's partial row sums go to sU2, warps 0-1 add the halves (fixed order),
+      // store u_t and reduce ||u_t||^2; ping-pong buffers, two CTA barriers per product
       if (tid < 64) sV2[0][tid] = tid < s ? rsqrtf((float)s) : 0.f;
       __syncthreads();
       float nrm = 0.f, inv = 1.f;
@@ -364,8 +371,8 @@ __global__ void __launch_bounds__(NT, 1) k_batched_tc(Args a) {
         const float* vin = sV2[t & 1];
         float u0a = 0.f, u0b = 0.f, u1a = 0.f, u1b = 0.f;   // row0 / row1 partial sums (2 chains each)
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const float v0 = vin[8 * c + 2 * q], v1 = vin[8 * c + 2 * q + 1];
+        for (int c = 0; c < FR / 4; ++c) {
+          const float v0 = vin[col0 + 8 * c], v1 = vin[col0 + 8 * c + 1];
           u0a = fmaf(use4 ? g4[4 * c + 0] : g[4 * c + 0], v0, u0a);
           u0b = fmaf(use4 ? g4[4 * c + 1] : g[4 * c + 1], v1, u0b);
           u1a = fmaf(use4 ? g4[4 * c + 2] : g[4 * c + 2], v0, u1a);
@@ -376,19 +383,21 @@ __global__ void __launch_bounds__(NT, 1) k_batched_tc(Args a) {
         u1 += __shfl_xor_sync(0xffffffffu, u1, 1);
         u0 += __shfl_xor_sync(0xffffffffu, u0, 2);
         u1 += __shfl_xor_sync(0xffffffffu, u1, 2);
-        u0 *= inv;
-        u1 *= inv;
-        float sq = q == 0 ? u0 * u0 + u1 * u1 : 0.f;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-        if (lane == 0) sRed2[t & 1][warp] = sq;
         if (q == 0) {
-          sV2[(t + 1) & 1][row0] = u0;
-          sV2[(t + 1) & 1][row1] = u1;
+          sU2[t & 1][ch][row0] = u0;
+          sU2[t & 1][ch][row1] = u1;
         }
         __syncthreads();
-        const float* rd = sRed2[t & 1];
-        nrm = sqrtf((rd[0] + rd[1]) + (rd[2] + rd[3]));
+        if (tid < 64) {
+          const float u = (sU2[t & 1][0][tid] + sU2[t & 1][1][tid]) * inv;
+          sV2[(t + 1) & 1][tid] = u;
+          float sq = u * u;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+          if (lane == 0) sRed2[t & 1][warp] = sq;
+        }
+        __syncthreads();
+        nrm = sqrtf(sRed2[t & 1][0] + sRed2[t & 1][1]);
         if (!(nrm > 0.f)) break;
         inv = 1.f / nrm;
       }
@@ -418,18 +427,18 @@ __global__ void __launch_bounds__(NT, 1) k_batched_tc(Args a) {
     const float s4 = 2.f * s2;
 
     // ---- lines 5-7: Psi_1 = s2 G - I, H = c0/2 I + c1 Psi_1 (all in this thread's fragment)
-    float wp[32], wpp[32], hh[32];
+    float wp[FR], wpp[FR], hh[FR];
     {
       const float h0 = 0.5f * sC[0], c1 = sC[1];
 #pragma unroll
-      for (int e = 0; e < 32; ++e) {
+      for (int e = 0; e < FR; ++e) {
         const float id = (rowof(e) == colof(e)) ? 1.f : 0.f;
         const float w = s2 * g[e] - id;
         wp[e] = w;
         wpp[e] = id;                                 // Psi_0 = I
         hh[e] = h0 * id + c1 * w;
       }
-      put_frag(sG, row0, q, g);                      // B operand of the steps: rows of G
+      put_frag(sG, row0, col0, g);                      // B operand of the steps: rows of G
       st_frag_hl(tAh + lane_off, tAl + lane_off, wp); // A operand (TMEM): rows of Psi_1
     }
     sync_for_mma();
@@ -439,11 +448,11 @@ __global__ void __launch_bounds__(NT, 1) k_batched_tc(Args a) {
       mbar_wait(&bar, phase);
       phase ^= 1;
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      float d[32];
+      float d[FR];
       ld_frag(tD + lane_off, d);
       const float ck = sC[k];
 #pragma unroll
-      for (int e = 0; e < 32; ++e) {
+      for (int e = 0; e < FR; ++e) {
         const float w = s4 * d[e] - 2.f * wp[e] - wpp[e];   // Psi_k = 2 B_hat Psi_{k-1} - Psi_{k-2}
         hh[e] = fmaf(ck, w, hh[e]);                          // H += c_k Psi_k
         wpp[e] = wp[e];
@@ -460,11 +469,11 @@ __global__ void __launch_bounds__(NT, 1) k_batched_tc(Args a) {
     phase ^= 1;
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     {
-      float d[32];
+      float d[FR];
       ld_frag(tD + lane_off, d);
       float* Yb = a.Y + b * mn;
 #pragma unroll
-      for (int e = 0; e < 32; ++e) {
+      for (int e = 0; e < FR; ++e) {
         const int r = rowof(e), c = colof(e);
         if (r < s && c < L) {
           if (left) Yb[(int64_t)r * a.n + c] = d[e];
@@ -497,7 +506,7 @@ cudaError_t launch_batched_tc(int64_t batch, int m, int n, const float* X, float
   int per_sm = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, btc::k_batched_tc, btc::NT, btc::SMEM);
   if (e != cudaSuccess) return e;
-  if (per_sm < 2) per_sm = 2;   // 2 x (97 KB smem, 128 thr x <= 255 regs, 64 TMEM columns) fit one SM
+  if (per_sm < 2) per_sm = 2;   // 2 x (97 KB smem, 256 thr x <= 128 regs, 256 TMEM columns) fit one SM
   if (const char* v = getenv("CPA_SVT_BTC_PER_SM")) per_sm = atoi(v);
   int64_t grid = (int64_t)num_sms * (per_sm > 0 ? per_sm : 1);
   if (grid > batch) grid = batch;
