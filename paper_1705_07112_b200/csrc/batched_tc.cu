@@ -76,31 +76,22 @@ __device__ __forceinline__ void put4(uint8_t* hi, int r, int k, float x0, float 
   *reinterpret_cast<float4*>(hi + OPB + o) = make_float4(rna(x0 - h0), rna(x1 - h1), rna(x2 - h2), rna(x3 - h3));
 }
 
-// D = Aop * Bop^T over K = 64 in 3xTF32 (24 MMAs), issued by one thread; completion on bar.
-__device__ __forceinline__ void mma64(uint32_t tmem_d, const uint8_t* a_hi, const uint8_t* b_hi, uint64_t* bar) {
-  const uint32_t ah = smem_u32(a_hi), al = ah + OPB, bh = smem_u32(b_hi), bl = bh + OPB;
-#pragma unroll
-  for (int kk = 0; kk < 8; ++kk) {
-    const uint32_t off = (kk >> 2) * 8192 + (kk & 3) * 32;
-    const uint64_t dah = desc(ah + off), dal = desc(al + off), dbh = desc(bh + off), dbl = desc(bl + off);
-    asm volatile(
-        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %5, %3, 1;\n"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %6, %2, %3, 1;\n}\n" ::"r"(tmem_d),
-        "l"(dah), "l"(dbh), "r"(IDESC), "r"(kk > 0 ? 1u : 0u), "l"(dbl), "l"(dal)
-        : "memory");
-  }
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
-               : "memory");
-}
-// Same product with the A operand in TMEM ("ts" form, probed: A row r in the M = 64 D lane of
-// row r, element k in column k; one UMMA_K = 8 columns): hi / lo at tmem_a_hi / tmem_a_lo.
+// D0 + D1 = Aop * Bop^T over K = 64 in 3xTF32 (24 MMAs), A operand in TMEM ("ts" form, probed:
+// A row r in the M = 64 D lane of row r, element k in column k; one UMMA_K = 8 columns), issued
+// by one thread; completion on bar.  D0 (lane offset 0) accumulates hi*hi + hi*lo with A_hi at
+// lane offset 0, D1 (lane offset 16) lo*hi with A_lo at lane offset 16: an M = 64 MMA runs on
+// one 16-lane half of each lane quarter, A and D in the same half (probed,
+// tools/probes/tc_m64_lane16_probe.cu), so D, A_hi and A_lo fit 128 TMEM columns instead of
+// 192 (three CTAs per SM instead of two).  The epilogue adds D0 + D1.
 // At M = 64 the smem-A form is limited by its shared-memory A reads (measured 61 cycles per
-// M64 N64 K8 MMA against the 32-cycle floor).
-__device__ __forceinline__ void mma64_ts(uint32_t tmem_d, uint32_t ta_hi, uint32_t ta_lo, const uint8_t* b_hi,
-                                         uint64_t* bar) {
-  const uint32_t bh = smem_u32(b_hi), bl = bh + OPB;
+// M64 N64 K8 MMA against the 32-cycle floor), hence A in TMEM.
+__device__ __forceinline__ void mma64_ts(uint32_t tmem_d0, uint32_t tmem_d1, uint32_t ta_hi, uint32_t ta_lo,
+                                         const uint8_t* b_hi, uint64_t* bar) {
+  // opaque to the optimiser: the 16 descriptors are rebuilt per call by the issuing thread
+  // instead of being hoisted out of the step loop into 32 registers of every thread
+  uint32_t bh;
+  asm volatile("mov.b32 %0, %1;\n" : "=r"(bh) : "r"(smem_u32(b_hi)));
+  const uint32_t bl = bh + OPB;
 #pragma unroll
   for (int kk = 0; kk < 8; ++kk) {
     const uint32_t off = (kk >> 2) * 8192 + (kk & 3) * 32;
@@ -108,9 +99,10 @@ __device__ __forceinline__ void mma64_ts(uint32_t tmem_d, uint32_t ta_hi, uint32
     asm volatile(
         "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %5, %3, 1;\n"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%6], %2, %3, 1;\n}\n" ::"r"(tmem_d),
-        "r"(ta_hi + kk * 8), "l"(dbh), "r"(IDESC), "r"(kk > 0 ? 1u : 0u), "l"(dbl), "r"(ta_lo + kk * 8)
+        "tcgen05.mma.cta_group::1.kind::tf32 [%7], [%6], %2, %3, p;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %5, %3, 1;\n}\n" ::"r"(tmem_d0),
+        "r"(ta_hi + kk * 8), "l"(dbh), "r"(IDESC), "r"(kk > 0 ? 1u : 0u), "l"(dbl), "r"(ta_lo + kk * 8),
+        "r"(tmem_d1)
         : "memory");
   }
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
@@ -174,8 +166,11 @@ struct Args {
   const double* costab;   // cos(k theta_l), K x K
 };
 
-// smem: [A (hi, lo) -> Psi / H operand] [G (hi, lo)] [A^T (hi, lo)]  (3 x 32 KB, 1 KB aligned)
-constexpr int SMEM = 3 * 2 * OPB + 1024;
+// smem: one B operand (hi, lo; 32 KB, 1 KB aligned): rows of A (line 1), of c^p G^p (squarings),
+// of G (lines 8-11), of A^T (line 12); then H in the threads' fragment layout (16 KB, float4
+// [FR / 4][NT]: conflict-free), which keeps the step's register state (Psi_{k-1}, Psi_{k-2}, D)
+// within the 80 registers of three 256-thread CTAs per SM
+constexpr int SMEM = 2 * OPB + 64 * 64 * 4 + 1024;
 
 // tcgen05.ld.16x256b.x4: 16 rows x 32 columns of D in this warp's lane quarter, spread over
 // all 32 threads (probed, tools/probes/tc_m64_probe.cu): thread t holds rows r0 = t/4 and
@@ -192,6 +187,23 @@ __device__ __forceinline__ void ld_frag(uint32_t taddr, float (&v)[FR]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
   for (int i = 0; i < FR; ++i) v[i] = __uint_as_float(r[i]);
+}
+// D = D0 + D1 (fragment layout of ld_frag), in two 8-column halves of 8 registers each so
+// that at most 16 loaded registers are live beside the recurrence state
+__device__ __forceinline__ void ld_frag2(uint32_t taddr0, uint32_t taddr1, float (&v)[FR]) {
+#pragma unroll
+  for (int hf = 0; hf < 2; ++hf) {
+    uint32_t r[8], u[8];
+    asm volatile("tcgen05.ld.sync.aligned.16x256b.x2.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr0 + 16 * hf));
+    asm volatile("tcgen05.ld.sync.aligned.16x256b.x2.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                 : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7])
+                 : "r"(taddr1 + 16 * hf));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[8 * hf + i] = __uint_as_float(r[i]) + __uint_as_float(u[i]);
+  }
 }
 // store a fragment (layout of ld_frag) as TF32 hi / lo A operands in TMEM (same layout)
 __device__ __forceinline__ void st_frag_hl(uint32_t t_hi, uint32_t t_lo, const float (&v)[FR]) {
@@ -233,12 +245,11 @@ __device__ __forceinline__ void put_frag(uint8_t* hi, int row0, int col0, const 
     }
 }
 
-__global__ void __launch_bounds__(NT, 2) k_batched_tc(Args a) {
+__global__ void __launch_bounds__(NT, 3) k_batched_tc(Args a) {
   extern __shared__ uint8_t raw[];
   uint8_t* base = raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);   // (stays in the shared window: STS, not ST)
-  uint8_t* sP = base;                 // A, then Psi_{k-1}, then H (A operand)
-  uint8_t* sG = base + 2 * OPB;       // G (B operand of the steps)
-  uint8_t* sAT = base + 4 * OPB;      // A^T (B operand of line 12)
+  uint8_t* sB = base;                 // B operand
+  float4* sH4 = reinterpret_cast<float4*>(base + 2 * OPB);   // H fragments
   __shared__ uint64_t bar;
   __shared__ uint32_t tslot;
   __shared__ float sV2[2][64];
@@ -260,67 +271,60 @@ __global__ void __launch_bounds__(NT, 2) k_batched_tc(Args a) {
   const int K = a.K;
   const int64_t mn = (int64_t)a.m * a.n;
   auto colof = [&](int e) { return col0 + 8 * (e >> 2) + (e & 1); };
-  // 64 x 64 matrices at 16-byte aligned addresses take the vector load path (A = X)
-  const bool full64 = a.m == 64 && a.n == 64 && ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0);
+  // 64 x 64 matrices at 8-byte aligned addresses take the float2 load path (A = X)
+  const bool full64 = a.m == 64 && a.n == 64 && ((reinterpret_cast<uintptr_t>(a.X) & 7) == 0);
   auto rowof = [&](int e) { return (e & 2) ? row1 : row0; };
+  // A (s x L, zero-padded to 64 x 64) in this thread's fragment layout: v[e] = A(rowof(e), colof(e))
+  auto load_frag = [&](const float* X, float (&v)[FR]) {
+    if (full64) {
+#pragma unroll
+      for (int e = 0; e < FR; e += 2) {
+        const float2 x2 = __ldg(reinterpret_cast<const float2*>(X + rowof(e) * 64 + colof(e)));
+        v[e] = x2.x;
+        v[e + 1] = x2.y;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < FR; ++e) {
+        const int i = rowof(e), j = colof(e);
+        v[e] = (i < s && j < L) ? __ldg(left ? X + (int64_t)i * a.n + j : X + (int64_t)j * a.n + i) : 0.f;
+      }
+    }
+  };
 
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&bar)));
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;\n" ::"r"(smem_u32(&tslot)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;\n" ::"r"(smem_u32(&tslot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  const uint32_t tD = tslot, tAh = tslot + 64, tAl = tslot + 128;   // D, A operand (hi, lo)
+  // lanes +0: D0 (columns 0-63), A_hi (64-127); lanes +16: D1, A_lo
+  const uint32_t tD = tslot, tAh = tslot + 64, tD1 = tD + (16u << 16), tAl = tAh + (16u << 16);
   uint32_t phase = 0;
   // Chebyshev-Gauss nodes x_l / Lambda = (cos theta_l + 1) / 2, once per CTA
   for (int l = tid; l < K; l += NT) sNode[l] = 0.5 * (cos(cheb_theta(l + 1, K)) + 1.0);
 
   for (int64_t b = blockIdx.x; b < a.batch; b += gridDim.x) {
     const float* X = a.X + b * mn;
-    // ---- load A (s x L, zero-padded to 64 x 64) as operand rows (sP) and A^T rows (sAT);
-    //      all of the thread's global loads in flight before the first conversion
+    // ---- line 1: G = A A^T (A operand: A in TMEM; B operand: rows of A)
     {
-      constexpr int NIT = 1024 / NT;
-      float4 v[NIT];
-      if (full64) {
-#pragma unroll
-        for (int it = 0; it < NIT; ++it) v[it] = __ldg(reinterpret_cast<const float4*>(X) + it * NT + tid);
-      } else {
-#pragma unroll
-        for (int it = 0; it < NIT; ++it) {
-          const int e = it * NT + tid, i = e >> 4, j = (e & 15) * 4;   // A(i, j..j+3)
-          float t4[4];
-#pragma unroll
-          for (int qq = 0; qq < 4; ++qq) {
-            const int jj = j + qq;
-            t4[qq] = (i < s && jj < L) ? __ldg(left ? X + (int64_t)i * a.n + jj : X + (int64_t)jj * a.n + i) : 0.f;
-          }
-          v[it] = make_float4(t4[0], t4[1], t4[2], t4[3]);
-        }
-      }
-#pragma unroll
-      for (int it = 0; it < NIT; ++it) {
-        const int e = it * NT + tid, i = e >> 4, j = (e & 15) * 4;
-        put4(sP, i, j, v[it].x, v[it].y, v[it].z, v[it].w);
-        put(sAT, j, i, v[it].x);
-        put(sAT, j + 1, i, v[it].y);
-        put(sAT, j + 2, i, v[it].z);
-        put(sAT, j + 3, i, v[it].w);
-      }
+      float av[FR];
+      load_frag(X, av);
+      put_frag(sB, row0, col0, av);
+      st_frag_hl(tAh + lane_off, tAl + lane_off, av);
     }
     sync_for_mma();
-    // ---- line 1: G = A A^T
-    if (tid == 0) btc::mma64(tD, sP, sP, &bar);
+    if (tid == 0) btc::mma64_ts(tD, tD1, tAh, tAl, sB, &bar);
     mbar_wait(&bar, phase);
     phase ^= 1;
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     float g[FR];
-    ld_frag(tD + lane_off, g);
+    ld_frag2(tD + lane_off, tD1 + lane_off, g);
     // ---- line 3: Lambda_max by T power steps (fp32, fixed order).  Repeated squaring (as the
     //      dense path, reading R6): v_{T-1} ~ G^{T-1} v_0 through q = (T-1)/4 products by
     //      c^4 G^4 (c = 2^-ilogb(max G_ii), exact) then T - 4q by G; two extra tcgen05 products
@@ -348,13 +352,13 @@ __global__ void __launch_bounds__(NT, 2) k_batched_tc(Args a) {
         for (int e = 0; e < FR; ++e) g4[e] = cs * g[e];
         for (int sq = 0; sq < 2; ++sq) {               // (cG)^2, then (c^2 G^2)^2
           st_frag_hl(tAh + lane_off, tAl + lane_off, g4);
-          put_frag(sG, row0, col0, g4);
+          put_frag(sB, row0, col0, g4);
           sync_for_mma();
-          if (tid == 0) btc::mma64_ts(tD, tAh, tAl, sG, &bar);
+          if (tid == 0) btc::mma64_ts(tD, tD1, tAh, tAl, sB, &bar);
           mbar_wait(&bar, phase);
           phase ^= 1;
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-          ld_frag(tD + lane_off, g4);
+          ld_frag2(tD + lane_off, tD1 + lane_off, g4);
           asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
           __syncthreads();                             // everyone has read D and the operands
         }
@@ -427,9 +431,10 @@ __global__ void __launch_bounds__(NT, 2) k_batched_tc(Args a) {
     const float s4 = 2.f * s2;
 
     // ---- lines 5-7: Psi_1 = s2 G - I, H = c0/2 I + c1 Psi_1 (all in this thread's fragment)
-    float wp[FR], wpp[FR], hh[FR];
+    float wp[FR], wpp[FR];
     {
       const float h0 = 0.5f * sC[0], c1 = sC[1];
+      float hh[FR];
 #pragma unroll
       for (int e = 0; e < FR; ++e) {
         const float id = (rowof(e) == colof(e)) ? 1.f : 0.f;
@@ -438,39 +443,65 @@ __global__ void __launch_bounds__(NT, 2) k_batched_tc(Args a) {
         wpp[e] = id;                                 // Psi_0 = I
         hh[e] = h0 * id + c1 * w;
       }
-      put_frag(sG, row0, col0, g);                      // B operand of the steps: rows of G
+#pragma unroll
+      for (int c = 0; c < FR / 4; ++c) sH4[c * NT + tid] = make_float4(hh[4 * c], hh[4 * c + 1], hh[4 * c + 2], hh[4 * c + 3]);
+      put_frag(sB, row0, col0, g);                      // B operand of the steps: rows of G
       st_frag_hl(tAh + lane_off, tAl + lane_off, wp); // A operand (TMEM): rows of Psi_1
     }
     sync_for_mma();
     // ---- lines 8-11: D = Psi_{k-1} G^T, Psi_k = s4 D - 2 Psi_{k-1} - Psi_{k-2}, H += c_k Psi_k
     for (int k = 2; k < K; ++k) {
-      if (tid == 0) btc::mma64_ts(tD, tAh, tAl, sG, &bar);
+      if (tid == 0) btc::mma64_ts(tD, tD1, tAh, tAl, sB, &bar);
       mbar_wait(&bar, phase);
       phase ^= 1;
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       float d[FR];
-      ld_frag(tD + lane_off, d);
+      ld_frag2(tD + lane_off, tD1 + lane_off, d);
       const float ck = sC[k];
 #pragma unroll
-      for (int e = 0; e < FR; ++e) {
-        const float w = s4 * d[e] - 2.f * wp[e] - wpp[e];   // Psi_k = 2 B_hat Psi_{k-1} - Psi_{k-2}
-        hh[e] = fmaf(ck, w, hh[e]);                          // H += c_k Psi_k
-        wpp[e] = wp[e];
-        wp[e] = w;
+      for (int c = 0; c < FR / 4; ++c) {
+        float4 h4 = sH4[c * NT + tid];
+        float* hp = &h4.x;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int e = 4 * c + i;
+          const float w = s4 * d[e] - 2.f * wp[e] - wpp[e];   // Psi_k = 2 B_hat Psi_{k-1} - Psi_{k-2}
+          hp[i] = fmaf(ck, w, hp[i]);                          // H += c_k Psi_k
+          wpp[e] = wp[e];
+          wp[e] = w;
+        }
+        sH4[c * NT + tid] = h4;
       }
       if (k + 1 < K) st_frag_hl(tAh + lane_off, tAl + lane_off, wp);
       sync_tmem_for_mma();
     }
-    // ---- line 12: Y = H A  (A operand = rows of H, B operand = rows of A^T)
-    st_frag_hl(tAh + lane_off, tAl + lane_off, hh);
-    sync_tmem_for_mma();
-    if (tid == 0) btc::mma64_ts(tD, tAh, tAl, sAT, &bar);
+    // ---- line 12: Y = H A  (A operand = rows of H, B operand = rows of A^T: A re-read, from L2)
+    {
+      float hh[FR];
+#pragma unroll
+      for (int c = 0; c < FR / 4; ++c) {
+        const float4 h4 = sH4[c * NT + tid];
+        hh[4 * c] = h4.x;
+        hh[4 * c + 1] = h4.y;
+        hh[4 * c + 2] = h4.z;
+        hh[4 * c + 3] = h4.w;
+      }
+      st_frag_hl(tAh + lane_off, tAl + lane_off, hh);
+    }
+    {
+      float av[FR];
+      load_frag(X, av);
+#pragma unroll
+      for (int e = 0; e < FR; ++e) put(sB, colof(e), rowof(e), av[e]);
+    }
+    sync_for_mma();
+    if (tid == 0) btc::mma64_ts(tD, tD1, tAh, tAl, sB, &bar);
     mbar_wait(&bar, phase);
     phase ^= 1;
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     {
       float d[FR];
-      ld_frag(tD + lane_off, d);
+      ld_frag2(tD + lane_off, tD1 + lane_off, d);
       float* Yb = a.Y + b * mn;
 #pragma unroll
       for (int e = 0; e < FR; ++e) {
@@ -487,7 +518,7 @@ __global__ void __launch_bounds__(NT, 2) k_batched_tc(Args a) {
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   }
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;\n" ::"r"(tslot));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;\n" ::"r"(tslot));
 }
 
 }  // namespace btc
@@ -506,7 +537,7 @@ cudaError_t launch_batched_tc(int64_t batch, int m, int n, const float* X, float
   int per_sm = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, btc::k_batched_tc, btc::NT, btc::SMEM);
   if (e != cudaSuccess) return e;
-  if (per_sm < 2) per_sm = 2;   // 2 x (97 KB smem, 256 thr x <= 128 regs, 256 TMEM columns) fit one SM
+  if (per_sm < 3) per_sm = 3;   // 3 x (49 KB smem, 256 thr x <= 80 regs, 128 TMEM columns) fit one SM
   if (const char* v = getenv("CPA_SVT_BTC_PER_SM")) per_sm = atoi(v);
   int64_t grid = (int64_t)num_sms * (per_sm > 0 ? per_sm : 1);
   if (grid > batch) grid = batch;
