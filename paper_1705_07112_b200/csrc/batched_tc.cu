@@ -91,11 +91,13 @@ __device__ __forceinline__ void mma64_ts(uint32_t tmem_d0, uint32_t tmem_d1, uin
   // instead of being hoisted out of the step loop into 32 registers of every thread
   uint32_t bh;
   asm volatile("mov.b32 %0, %1;\n" : "=r"(bh) : "r"(smem_u32(b_hi)));
-  const uint32_t bl = bh + OPB;
+  // the descriptor's start-address field is addr >> 4 in 14 bits (no carry below 256 KB), so a
+  // k-block's descriptor is the base descriptor plus off >> 4
+  const uint64_t dbh0 = desc(bh), dbl0 = desc(bh + OPB);
 #pragma unroll
   for (int kk = 0; kk < 8; ++kk) {
     const uint32_t off = (kk >> 2) * 8192 + (kk & 3) * 32;
-    const uint64_t dbh = desc(bh + off), dbl = desc(bl + off);
+    const uint64_t dbh = dbh0 + (off >> 4), dbl = dbl0 + (off >> 4);
     asm volatile(
         "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n"
