@@ -37,9 +37,11 @@
 namespace cpa {
 namespace btc {
 
-constexpr int NT = 256;                 // threads per CTA (8 warps: warp w owns D rows 16 (w % 4) .. +15,
-                                        // columns 32 (w / 4) .. +31 -- a TMEM lane quarter is warp w % 4's)
-constexpr int NW = NT / 32;
+// Threads per CTA NT = 128 (default: 4 warps, warp w owns D rows 16 w .. +15, all 64 columns;
+// 4 CTAs per SM) or 256 (CPA_SVT_BTC_NT=256: 8 warps, warp w owns rows 16 (w % 4) .. +15 and
+// columns 32 (w / 4) .. +31 -- a TMEM lane quarter is warp w % 4's; 3 CTAs per SM, registers);
+// FR = 4096 / NT fragment elements per thread.  More matrices in flight per SM beat a shorter
+// epilogue per matrix: c3 8.05 ms (128) against 8.62 ms (256).
 constexpr int OPB = 64 * 64 * 4;        // bytes of one 64 x 64 fp32 operand (two 8 KB k-blocks)
 
 __device__ __forceinline__ uint32_t sw(int r, int k) {  // byte offset of (r, k) in a K-major SW128 operand
@@ -178,23 +180,12 @@ constexpr int SMEM = 2 * OPB + 64 * 64 * 4 + 1024;
 // all 32 threads (probed, tools/probes/tc_m64_probe.cu): thread t holds rows r0 = t/4 and
 // r1 = t/4 + 8 (warp-local), columns 8c + 2(t%4) + {0, 1}, c = 0..3 (relative to the address), as
 // v[4c + 0] = (r0, 8c+2q), v[4c + 1] = (r0, 8c+2q+1), v[4c + 2] = (r1, 8c+2q), v[4c + 3] = (r1, 8c+2q+1).
-constexpr int FR = 16;   // fragment elements per thread
-__device__ __forceinline__ void ld_frag(uint32_t taddr, float (&v)[FR]) {
-  uint32_t r[FR];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.16x256b.x4.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < FR; ++i) v[i] = __uint_as_float(r[i]);
-}
-// D = D0 + D1 (fragment layout of ld_frag), in two 8-column halves of 8 registers each so
-// that at most 16 loaded registers are live beside the recurrence state
+// D = D0 + D1 in the fragment layout above, in 16-column pieces of 8 registers each so that
+// at most 16 loaded registers are live beside the recurrence state
+template <int FR>
 __device__ __forceinline__ void ld_frag2(uint32_t taddr0, uint32_t taddr1, float (&v)[FR]) {
 #pragma unroll
-  for (int hf = 0; hf < 2; ++hf) {
+  for (int hf = 0; hf < FR / 8; ++hf) {
     uint32_t r[8], u[8];
     asm volatile("tcgen05.ld.sync.aligned.16x256b.x2.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
@@ -207,7 +198,8 @@ __device__ __forceinline__ void ld_frag2(uint32_t taddr0, uint32_t taddr1, float
     for (int i = 0; i < 8; ++i) v[8 * hf + i] = __uint_as_float(r[i]) + __uint_as_float(u[i]);
   }
 }
-// store a fragment (layout of ld_frag) as TF32 hi / lo A operands in TMEM (same layout)
+// store a fragment (layout of ld_frag2) as TF32 hi / lo A operands in TMEM (same layout)
+template <int FR>
 __device__ __forceinline__ void st_frag_hl(uint32_t t_hi, uint32_t t_lo, const float (&v)[FR]) {
   uint32_t h[FR], l[FR];
 #pragma unroll
@@ -221,8 +213,11 @@ __device__ __forceinline__ void st_frag_hl(uint32_t t_hi, uint32_t t_lo, const f
                ::"r"(addr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),  \
                "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])          \
                : "memory")
-  BTC_ST16(t_hi, h);
-  BTC_ST16(t_lo, l);
+#pragma unroll
+  for (int c = 0; c < FR / 16; ++c) {   // 32 columns per x4 store
+    BTC_ST16(t_hi + 32 * c, (h + 16 * c));
+    BTC_ST16(t_lo + 32 * c, (l + 16 * c));
+  }
 #undef BTC_ST16
 }
 // TMEM stores done and visible to the next MMA issue (no shared-memory writes involved)
@@ -232,7 +227,8 @@ __device__ __forceinline__ void sync_tmem_for_mma() {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
 }
-// write a fragment (layout of ld_frag) as TF32 hi / lo operand rows: element (row, col) at sw(row, col)
+// write a fragment (layout of ld_frag2) as TF32 hi / lo operand rows: element (row, col) at sw(row, col)
+template <int FR>
 __device__ __forceinline__ void put_frag(uint8_t* hi, int row0, int col0, const float (&v)[FR]) {
 #pragma unroll
   for (int c = 0; c < FR / 4; ++c)
@@ -247,7 +243,9 @@ __device__ __forceinline__ void put_frag(uint8_t* hi, int row0, int col0, const 
     }
 }
 
-__global__ void __launch_bounds__(NT, 3) k_batched_tc(Args a) {
+template <int NT>
+__global__ void __launch_bounds__(NT, NT == 256 ? 3 : 4) k_batched_tc(Args a) {
+  constexpr int NW = NT / 32, FR = 4096 / NT, NCH = NW / 4;   // NCH column groups
   extern __shared__ uint8_t raw[];
   uint8_t* base = raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);   // (stays in the shared window: STS, not ST)
   uint8_t* sB = base;                 // B operand
@@ -255,8 +253,8 @@ __global__ void __launch_bounds__(NT, 3) k_batched_tc(Args a) {
   __shared__ uint64_t bar;
   __shared__ uint32_t tslot;
   __shared__ float sV2[2][64];
-  __shared__ float sU2[2][2][64];   // per column half: partial row sums of a power product
-  __shared__ float sRed2[2][NW / 2];
+  __shared__ float sU2[2][NCH][64];   // per column group: partial row sums of a power product
+  __shared__ float sRed2[2][2];
   __shared__ float sRed[NW];
   __shared__ double sNode[128];   // K <= 128 on the batched path (cpa_svt_apply_batched)
   __shared__ double sHn[128];
@@ -395,7 +393,9 @@ __global__ void __launch_bounds__(NT, 3) k_batched_tc(Args a) {
         }
         __syncthreads();
         if (tid < 64) {
-          const float u = (sU2[t & 1][0][tid] + sU2[t & 1][1][tid]) * inv;
+          float u = sU2[t & 1][0][tid];
+          if (NCH == 2) u += sU2[t & 1][NCH - 1][tid];
+          u *= inv;
           sV2[(t + 1) & 1][tid] = u;
           float sq = u * u;
 #pragma unroll
@@ -534,16 +534,21 @@ cudaError_t launch_batched_tc(int64_t batch, int m, int n, const float* X, float
   k_costab<<<(K * K + 255) / 256, 256, 0, st>>>(costab, K);
   if (launches) ++*launches;
   btc::Args a{batch, m, n, X, Y, k, K, T, safety, lam_override, lambda_out, costab};
-  cudaError_t e = cudaFuncSetAttribute(btc::k_batched_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, btc::SMEM);
+  const char* ntv = getenv("CPA_SVT_BTC_NT");
+  const int nt = (ntv && atoi(ntv) == 256) ? 256 : 128;   // 128: measured c3 8.05 ms against 8.62 ms
+  auto kern = nt == 128 ? btc::k_batched_tc<128> : btc::k_batched_tc<256>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, btc::SMEM);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, btc::k_batched_tc, btc::NT, btc::SMEM);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nt, btc::SMEM);
   if (e != cudaSuccess) return e;
-  if (per_sm < 3) per_sm = 3;   // 3 x (49 KB smem, 256 thr x <= 80 regs, 128 TMEM columns) fit one SM
+  // 3 x (49 KB smem, 256 thr x <= 80 regs, 128 TMEM columns) or 4 x (128 thr x <= 128 regs) fit one SM
+  const int want = nt == 128 ? 4 : 3;
+  if (per_sm < want) per_sm = want;
   if (const char* v = getenv("CPA_SVT_BTC_PER_SM")) per_sm = atoi(v);
   int64_t grid = (int64_t)num_sms * (per_sm > 0 ? per_sm : 1);
   if (grid > batch) grid = batch;
-  btc::k_batched_tc<<<(unsigned)grid, btc::NT, btc::SMEM, st>>>(a);
+  kern<<<(unsigned)grid, nt, btc::SMEM, st>>>(a);
   if (launches) ++*launches;
   return cudaGetLastError();
 }
