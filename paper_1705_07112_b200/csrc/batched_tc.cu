@@ -87,6 +87,9 @@ __device__ __forceinline__ void put4(uint8_t* hi, int r, int k, float x0, float 
 // 192 (three CTAs per SM instead of two).  The epilogue adds D0 + D1.
 // At M = 64 the smem-A form is limited by its shared-memory A reads (measured 61 cycles per
 // M64 N64 K8 MMA against the 32-cycle floor), hence A in TMEM.
+// ACC0: D0 accumulates onto its current contents from the first k-block (the step's
+// -2 Psi_{k-1} - Psi_{k-2}, stored by the epilogue), D1 always starts from zero.
+template <bool ACC0 = false>
 __device__ __forceinline__ void mma64_ts(uint32_t tmem_d0, uint32_t tmem_d1, uint32_t ta_hi, uint32_t ta_lo,
                                          const uint8_t* b_hi, uint64_t* bar) {
   // opaque to the optimiser: the 16 descriptors are rebuilt per call by the issuing thread
@@ -101,12 +104,12 @@ __device__ __forceinline__ void mma64_ts(uint32_t tmem_d0, uint32_t tmem_d1, uin
     const uint32_t off = (kk >> 2) * 8192 + (kk & 3) * 32;
     const uint64_t dbh = dbh0 + (off >> 4), dbl = dbl0 + (off >> 4);
     asm volatile(
-        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n"
+        "{\n.reg .pred p, p0;\nsetp.ne.b32 p, %4, 0;\nsetp.ne.b32 p0, %8, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p0;\n"
         "tcgen05.mma.cta_group::1.kind::tf32 [%7], [%6], %2, %3, p;\n"
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %5, %3, 1;\n}\n" ::"r"(tmem_d0),
         "r"(ta_hi + kk * 8), "l"(dbh), "r"(IDESC), "r"(kk > 0 ? 1u : 0u), "l"(dbl), "r"(ta_lo + kk * 8),
-        "r"(tmem_d1)
+        "r"(tmem_d1), "r"((ACC0 || kk > 0) ? 1u : 0u)
         : "memory");
   }
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
@@ -199,27 +202,38 @@ __device__ __forceinline__ void ld_frag2(uint32_t taddr0, uint32_t taddr1, float
   }
 }
 // store a fragment (layout of ld_frag2) as TF32 hi / lo A operands in TMEM (same layout)
-template <int FR>
-__device__ __forceinline__ void st_frag_hl(uint32_t t_hi, uint32_t t_lo, const float (&v)[FR]) {
-  uint32_t h[FR], l[FR];
-#pragma unroll
-  for (int i = 0; i < FR; ++i) {
-    const float x = v[i], hx = rna(x);
-    h[i] = __float_as_uint(hx);
-    l[i] = __float_as_uint(rna(x - hx));
-  }
 #define BTC_ST16(addr, r)                                                                                          \
   asm volatile("tcgen05.st.sync.aligned.16x256b.x4.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n" \
                ::"r"(addr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),  \
                "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])          \
                : "memory")
+template <int FR>
+__device__ __forceinline__ void st_frag_hl(uint32_t t_hi, uint32_t t_lo, const float (&v)[FR]) {
 #pragma unroll
-  for (int c = 0; c < FR / 16; ++c) {   // 32 columns per x4 store
-    BTC_ST16(t_hi + 32 * c, (h + 16 * c));
-    BTC_ST16(t_lo + 32 * c, (l + 16 * c));
+  for (int c = 0; c < FR / 16; ++c) {   // 32 columns per x4 store; one piece's hi / lo live at a time
+    uint32_t h[16], l[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const float x = v[16 * c + i], hx = rna(x);
+      h[i] = __float_as_uint(hx);
+      l[i] = __float_as_uint(rna(x - hx));
+    }
+    BTC_ST16(t_hi + 32 * c, h);
+    BTC_ST16(t_lo + 32 * c, l);
   }
-#undef BTC_ST16
 }
+// store a fragment (layout of ld_frag2) as fp32 into TMEM (the D0 accumulator)
+template <int FR>
+__device__ __forceinline__ void st_frag(uint32_t taddr, const float (&v)[FR]) {
+#pragma unroll
+  for (int c = 0; c < FR / 16; ++c) {
+    uint32_t h[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) h[i] = __float_as_uint(v[16 * c + i]);
+    BTC_ST16(taddr + 32 * c, h);
+  }
+}
+#undef BTC_ST16
 // TMEM stores done and visible to the next MMA issue (no shared-memory writes involved)
 __device__ __forceinline__ void sync_tmem_for_mma() {
   asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
@@ -433,7 +447,10 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : 4) k_batched_tc(Args a) {
     const float s4 = 2.f * s2;
 
     // ---- lines 5-7: Psi_1 = s2 G - I, H = c0/2 I + c1 Psi_1 (all in this thread's fragment)
-    float wp[FR], wpp[FR];
+    // The steps run on the tensor core whole: B operand = rows of s4 G, and D0 is preloaded
+    // with -2 Psi_{k-1} - Psi_{k-2}, so D0 + D1 = Psi_{k-1} (s4 G)^T - 2 Psi_{k-1} - Psi_{k-2}
+    // = Psi_k (lines 8-9) and only Psi_{k-1} stays in registers.
+    float wp[FR];
     {
       const float h0 = 0.5f * sC[0], c1 = sC[1];
       float hh[FR];
@@ -442,18 +459,21 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : 4) k_batched_tc(Args a) {
         const float id = (rowof(e) == colof(e)) ? 1.f : 0.f;
         const float w = s2 * g[e] - id;
         wp[e] = w;
-        wpp[e] = id;                                 // Psi_0 = I
         hh[e] = h0 * id + c1 * w;
+        g[e] *= s4;
       }
 #pragma unroll
       for (int c = 0; c < FR / 4; ++c) sH4[c * NT + tid] = make_float4(hh[4 * c], hh[4 * c + 1], hh[4 * c + 2], hh[4 * c + 3]);
-      put_frag(sB, row0, col0, g);                      // B operand of the steps: rows of G
+      put_frag(sB, row0, col0, g);                      // B operand of the steps: rows of s4 G
       st_frag_hl(tAh + lane_off, tAl + lane_off, wp); // A operand (TMEM): rows of Psi_1
+#pragma unroll
+      for (int e = 0; e < FR; ++e) hh[e] = -2.f * wp[e] - ((rowof(e) == colof(e)) ? 1.f : 0.f);   // Psi_0 = I
+      st_frag(tD + lane_off, hh);
     }
     sync_for_mma();
-    // ---- lines 8-11: D = Psi_{k-1} G^T, Psi_k = s4 D - 2 Psi_{k-1} - Psi_{k-2}, H += c_k Psi_k
+    // ---- lines 8-11: Psi_k = D0 + D1, H += c_k Psi_k; next A = Psi_k, next D0 = -2 Psi_k - Psi_{k-1}
     for (int k = 2; k < K; ++k) {
-      if (tid == 0) btc::mma64_ts(tD, tD1, tAh, tAl, sB, &bar);
+      if (tid == 0) btc::mma64_ts<true>(tD, tD1, tAh, tAl, sB, &bar);
       mbar_wait(&bar, phase);
       phase ^= 1;
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
@@ -463,18 +483,22 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : 4) k_batched_tc(Args a) {
 #pragma unroll
       for (int c = 0; c < FR / 4; ++c) {
         float4 h4 = sH4[c * NT + tid];
-        float* hp = &h4.x;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int e = 4 * c + i;
-          const float w = s4 * d[e] - 2.f * wp[e] - wpp[e];   // Psi_k = 2 B_hat Psi_{k-1} - Psi_{k-2}
-          hp[i] = fmaf(ck, w, hp[i]);                          // H += c_k Psi_k
-          wpp[e] = wp[e];
-          wp[e] = w;
-        }
+        h4.x = fmaf(ck, d[4 * c], h4.x);                       // H += c_k Psi_k
+        h4.y = fmaf(ck, d[4 * c + 1], h4.y);
+        h4.z = fmaf(ck, d[4 * c + 2], h4.z);
+        h4.w = fmaf(ck, d[4 * c + 3], h4.w);
         sH4[c * NT + tid] = h4;
       }
-      if (k + 1 < K) st_frag_hl(tAh + lane_off, tAl + lane_off, wp);
+      if (k + 1 < K) {
+        st_frag_hl(tAh + lane_off, tAl + lane_off, d);
+#pragma unroll
+        for (int e = 0; e < FR; ++e) {
+          const float nx = -2.f * d[e] - wp[e];
+          wp[e] = d[e];
+          d[e] = nx;
+        }
+        st_frag(tD + lane_off, d);
+      }
       sync_tmem_for_mma();
     }
     // ---- line 12: Y = H A  (A operand = rows of H, B operand = rows of A^T: A re-read, from L2)
