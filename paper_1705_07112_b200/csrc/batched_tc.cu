@@ -325,6 +325,14 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : 4) k_batched_tc(Args a) {
 
   for (int64_t b = blockIdx.x; b < a.batch; b += gridDim.x) {
     const float* X = a.X + b * mn;
+    // the CTA's next matrix into L2 while this one is processed (one bulk prefetch; 16-byte
+    // granules only)
+    if (tid == 0 && b + gridDim.x < a.batch) {
+      const float* Xn = a.X + (b + gridDim.x) * mn;
+      const uint32_t bytes = (uint32_t)(mn * 4);
+      if (((reinterpret_cast<uintptr_t>(Xn) | bytes) & 15) == 0)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(Xn), "r"(bytes) : "memory");
+    }
     // ---- line 1: G = A A^T (A operand: A in TMEM; B operand: rows of A)
     {
       float av[FR];
