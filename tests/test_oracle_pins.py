@@ -570,3 +570,73 @@ def test_admm_adaptive_eps_uses_the_schedule(monkeypatch):
     assert [k for _, k, _ in seen] == want
     assert all(mode == "topk" and tr == "dct" for mode, _, tr in seen)
     assert want[0] == 2 and np.isfinite(L).all()
+
+
+# --- weighted soft (BASELINE configs[2]) and relative tau: pins independent of h_response -----
+
+def test_golden_wsoft_eval():
+    # hand-computed values of eq. filter_response_ours, weighted-soft member
+    for e in GOLDEN["wsoft_eval"]:
+        k = O.Kernel("wsoft", w_c=e["w_c"], w_shift=e["w_shift"], w_eps=e["w_eps"])
+        assert abs(O.h_response(k, e["x"], 0.0) - e["h"]) <= 1e-15, e["cite"]
+        assert abs(O.g_response(k, math.sqrt(e["x"]), 0.0) - e["g"]) <= 1e-14 * max(1.0, e["g"]), e["cite"]
+
+
+def test_wsoft_constant_weight_is_soft():
+    # With w_shift >= every Gram eigenvalue the weight is the constant w_c / w_eps (the paper's
+    # constant-weight case, Fig. 3(b)/(d) captions), so weighted soft must be soft
+    # shrinkage with tau = w_c / w_eps -- bitwise, every coefficient and output.
+    X = W.random_dense(23, 17, seed=31)
+    soft = O.Kernel("soft", tau=3.0)
+    wsoft = O.Kernel("wsoft", w_c=3.0, w_shift=1e12, w_eps=1.0)
+    Ys, i1 = O.cpa_shrink(X, soft, 18, T=60, return_info=True)
+    Yw, i2 = O.cpa_shrink(X, wsoft, 18, T=60, return_info=True)
+    assert i1["coeffs"] == i2["coeffs"]
+    assert np.array_equal(Ys, Yw)
+    # and the batched loop (c3's engine in the oracle) agrees with it
+    Xb = np.stack([X[:16, :16], 2 * X[:16, :16]])
+    Yb, _ = O.cpa_shrink_batched(Xb, wsoft, 18, T=60)
+    for b in range(2):
+        assert np.array_equal(Yb[b], O.cpa_shrink(Xb[b], soft, 18, T=60))
+
+
+def test_p5_node_exact_wsoft_closed_form():
+    # Singular values at the Chebyshev nodes: the K-point rule interpolates h exactly there
+    # (PAPER.md:233), so Y = U g(Sigma) V^T with the closed form of the weighted-soft singular-value
+    # response g(sigma) = max(sigma - w_c/(sigma + w_eps), 0) (w_shift = 0; PAPER.md:510-512, 520:
+    # g(sqrt x) = sqrt(x) h(x)) -- built here without h_response.
+    rng = np.random.default_rng(55)
+    K, lam, m, n = 12, 144.0, 17, 12
+    nodes = [lam / 2 * (math.cos(math.pi * (l - 0.5) / K) + 1) for l in range(1, K + 1)]
+    d = np.sqrt(np.array(nodes))
+    U, V = _orth(m, rng)[:, :n], _orth(n, rng)
+    X = (U * d) @ V.T
+    w_c, w_eps = 22.4, 1e-6
+    g = np.array([max(s - w_c / (s + w_eps), 0.0) for s in d])
+    assert (g == 0).sum() >= 3 and (g > 0).sum() >= 3      # both branches exercised
+    want = (U * g) @ V.T
+    Y = O.cpa_shrink(X, O.Kernel("wsoft", w_c=w_c, w_eps=w_eps), K, lam=lam)
+    assert O.rel_fro(Y, want) < 1e-12
+
+
+def test_relative_tau_is_tau_times_sigma_max():
+    # Reading R7: a relative threshold is tau * sigma_max_hat with sigma_max_hat = sqrt(lambda_hat)
+    # (before the 1.01 safety factor).  At a converged power iteration lambda_hat = sigma_1(X)^2,
+    # so the threshold must equal tau * sigma_1 from an independent SVD (numpy LAPACK).
+    rng = np.random.default_rng(71)
+    U, V = _orth(30, rng)[:, :20], _orth(20, rng)
+    sv = np.linspace(10.0, 1.0, 20)
+    X = (U * sv) @ V.T
+    for kind in ("soft", "hard"):
+        k = O.Kernel(kind, tau=0.37, tau_relative=True)
+        Y, info = O.cpa_shrink(X, k, 16, T=400, return_info=True)
+        s1 = np.linalg.svd(X, compute_uv=False)[0]
+        assert abs(info["tau"] - 0.37 * s1) <= 1e-12 * s1
+        assert abs(info["sigma_max_hat"] - s1) <= 1e-12 * s1
+        assert abs(info["lambda_max"] - 1.01 * s1 * s1) <= 1e-12 * s1 * s1
+        # the output equals the absolute-tau shrinkage at that threshold and Lambda_max
+        Ya = O.cpa_shrink(X, O.Kernel(kind, tau=0.37 * s1), 16, lam=1.01 * s1 * s1)
+        assert O.rel_fro(Y, Ya) < 1e-12
+    # scale invariance of a relative threshold: shrink(a X) = a shrink(X)
+    k = O.Kernel("soft", tau=0.37, tau_relative=True)
+    assert O.rel_fro(O.cpa_shrink(3.0 * X, k, 16, T=400), 3.0 * O.cpa_shrink(X, k, 16, T=400)) < 1e-12
