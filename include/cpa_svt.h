@@ -11,16 +11,21 @@
  * B_hat = (2/Lambda_max) Phi - Id, the three-term recurrence
  * Psi_k = 2 B_hat Psi_{k-1} - Psi_{k-2}, and the K
  * Chebyshev-Gauss coefficients of PAPER.md:233 / 363 for the response h of
- * PAPER.md:496-519 (hard / soft / weighted soft).  The library never forms
- * H_hat: it runs the recurrence on W_k = Psi_k(B_hat) X (or X Psi_k(B_hat)),
+ * PAPER.md:496-519 (hard / soft / weighted soft).  Two evaluation orders of the
+ * same polynomial are built (CPA_SVT_OPT_FORM):
+ *   - the Alg. 1 s x s form (default for K > 2): the three-term recurrence on the
+ *     s x s Gram, Psi_0 = Id, Psi_1 = B_hat, Psi_k = 2 B_hat Psi_{k-1} - Psi_{k-2}
+ *     (PAPER.md:364-370), H_hat = c_0/2 Id + sum_k c_k Psi_k formed on the device,
+ *     then ONE product Y = H_hat X (or X H_hat), Alg. 1 line 12;
+ *   - the apply-to-X form (line 12 distributed over the sum):
  *     W_0 = X,  W_1 = (2/L) G X - X,  W_k = (4/L) G W_{k-1} - 2 W_{k-1} - W_{k-2},
- *     Y = c_0/2 W_0 + c_1 W_1 + sum_{k>=2} c_k W_k,
- * each step one fused kernel (GEMM + update + accumulation).
+ *     Y = c_0/2 W_0 + c_1 W_1 + sum_{k>=2} c_k W_k.
+ * Every recurrence step is one fused kernel (product + update + accumulation).
  *
  * Conventions (all entry points):
  *   - Every call returns cpa_svt_status; CPA_SVT_OK == 0.  Arguments are
  *     validated before any device work; on a non-OK status no output buffer
- *     has been written unless the status is CPA_SVT_E_CUDA / E_NCCL.
+ *     has been written unless the status is CPA_SVT_E_CUDA / E_NCCL / E_DIVERGED.
  *   - Matrices are ROW-MAJOR with a leading dimension in ELEMENTS (ld >= cols).
  *   - X, Y, CSR arrays and lambda_out are DEVICE pointers on the handle's
  *     device, owned by the caller, valid until the handle's stream has
@@ -28,8 +33,9 @@
  *     structs are HOST pointers read (or written) before the call returns.
  *   - All device work is ordered on the handle's stream and is asynchronous,
  *     EXCEPT when `info` is non-NULL or `lam` asks for lambda back
- *     (lam->want_lambda): then the call synchronises the stream before
- *     returning.  cpa_svt_apply_host is always synchronous.
+ *     (lam->want_lambda) or CPA_SVT_OPT_DIVERGENCE is 2: then the call
+ *     synchronises the stream before returning.  cpa_svt_apply_host is always
+ *     synchronous.
  *   - Y must not alias X.  Y may be any caller buffer of the same shape.
  *   - The handle owns its workspace (Gram, two recurrence buffers, power
  *     iteration scratch, series parameters), grows it lazily and frees it in
@@ -57,7 +63,10 @@ typedef enum {
   CPA_SVT_OK = 0,
   CPA_SVT_E_ARG = 1,          /* NULL pointer, K < 2 or K > KMAX, dims < 0, ld < cols, Y aliases X, bad enum */
   CPA_SVT_E_DOMAIN = 2,       /* lambda_max override < 0 or non-finite, tau < 0, weight parameters invalid */
-  CPA_SVT_E_DIVERGED = 3,     /* reserved: ||Y||_F > 1e3 sum|c_k| ||X||_F */
+  CPA_SVT_E_DIVERGED = 3,     /* ||Y||_F > 1e3 sum|c_k| ||X||_F, or Y not finite (the series is
+                                 bounded only for a Gram spectrum inside [0, Lambda_max]):
+                                 Y HAS been written (and is meaningless).  Reported by calls that synchronise
+                                 (info / want_lambda / apply_host, or CPA_SVT_OPT_DIVERGENCE = 2). */
   CPA_SVT_E_CUDA = 4,         /* a CUDA runtime call failed (cpa_svt_last_error has the text) */
   CPA_SVT_E_NCCL = 5,         /* an NCCL call failed or NCCL could not be loaded */
   CPA_SVT_E_NOMEM = 6,        /* workspace allocation failed */
@@ -83,9 +92,12 @@ typedef struct {
 typedef enum { CPA_SVT_F64 = 0, CPA_SVT_F32 = 1 } cpa_svt_dtype;
 
 typedef enum {
-  CPA_SVT_MATH_NATIVE = 0, /* f64: DMMA (mma.sync f64) tensor tiles; f32: FFMA */
-  CPA_SVT_MATH_TF32 = 1,   /* f32 data, tcgen05 kind::tf32 with operands rounded to nearest TF32 */
-  CPA_SVT_MATH_3XTF32 = 2  /* f32 data, tcgen05 kind::tf32 hi/lo split (near-fp32 accuracy) */
+  CPA_SVT_MATH_NATIVE = 0, /* f64 only: DMMA (mma.sync f64) tensor tiles.  f32 + NATIVE is not built
+                              (CPA_SVT_E_UNSUPPORTED): fp32 data runs on the tensor cores (below) */
+  CPA_SVT_MATH_TF32 = 1,   /* f32 data, single-pass tcgen05 kind::tf32, operands rounded to nearest TF32
+                              (Gram in 3xTF32).  Reduced accuracy: ~0.5-2e-4 relative Frobenius error
+                              measured -- NOT the <= 1e-4 fp32 bar of the north star; use 3XTF32 for that */
+  CPA_SVT_MATH_3XTF32 = 2  /* f32 data, tcgen05 kind::tf32 hi/lo split (near-fp32 accuracy, <= 1e-4) */
 } cpa_svt_math;
 
 /* Lambda_max of the Gram (Alg. 1 line 3): power iteration
@@ -113,7 +125,7 @@ typedef struct {
                             4 = s x s in one thread block (fp64, s <= 64 and L <= 128, FORM auto) */
 } cpa_svt_info;
 
-/* Multi-GPU sharding of the long dimension for cpa_svt_apply (world > 1). */
+/* Multi-GPU sharding of the long dimension for cpa_svt_apply (handles with a communicator). */
 typedef enum {
   CPA_SVT_SHARD_NONE = 0,  /* X is the whole matrix on every rank (replicas) */
   CPA_SVT_SHARD_COLS = 1,  /* left-apply (global m <= n): X is m x n_local, a column block */
@@ -121,13 +133,20 @@ typedef enum {
 } cpa_svt_shard;
 
 /* Create a handle bound to `device` and the CUDA stream `cuda_stream`
- * (a cudaStream_t; NULL = legacy default stream).  For world > 1,
- * nccl_unique_id points to the 128-byte ncclUniqueId created by
- * cpa_svt_nccl_unique_id on rank 0 and broadcast by the caller; the library
- * creates its own NCCL communicator (NCCL is loaded at run time). */
+ * (a cudaStream_t; NULL = legacy default stream).  nccl_unique_id points to
+ * the 128-byte ncclUniqueId created by cpa_svt_nccl_unique_id on rank 0 and
+ * broadcast by the caller (required for world > 1; optional for world == 1,
+ * where it creates a one-rank communicator so the sharded path with its
+ * collectives runs on one GPU); the library creates its own NCCL communicator
+ * (NCCL is loaded at run time).  The sharded calls below run their
+ * collectives whenever the handle has a communicator. */
 cpa_svt_status cpa_svt_init(cpa_svt_handle** h, int device, void* cuda_stream,
                             const void* nccl_unique_id, int rank, int world);
 cpa_svt_status cpa_svt_free(cpa_svt_handle* h);
+
+/* The handle's NCCL communicator as NCCL reports it (ncclCommCount / ncclCommUserRank):
+ * *nranks = 0, *rank = -1 when the handle has none.  Host pointers.  E_ARG on NULL. */
+cpa_svt_status cpa_svt_comm_info(const cpa_svt_handle* h, int* nranks, int* rank);
 
 /* Writes a fresh 128-byte ncclUniqueId into out128 (call on rank 0 only). */
 cpa_svt_status cpa_svt_nccl_unique_id(void* out128);
@@ -144,10 +163,12 @@ cpa_svt_status cpa_svt_coeffs(const cpa_svt_kernel* k, int K, double lambda_max,
  * for SHARD_NONE).  c: optional host array of K raw coefficients that
  * replaces line 4 (NULL = computed on the device from `k` and Lambda_max).
  * lam: required.  info: optional.  dtype/math: F64+NATIVE (DMMA), F32 with
- * TF32 / 3XTF32 / NATIVE.  X and Y are dtype arrays.  With world > 1 the
- * partial Grams are summed with one NCCL all-reduce (PAPER.md:278-307:
- * G = sum over column blocks of X_p X_p^T) and every rank then runs the
- * recurrence on its own block; Lambda_max is broadcast from rank 0. */
+ * TF32 / 3XTF32.  X and Y are dtype arrays.  With a communicator and a shard
+ * mode the partial Grams are summed with one NCCL all-reduce (PAPER.md:278-307:
+ * G = sum over column blocks of X_p X_p^T), Lambda_max and the coefficients are
+ * broadcast from rank 0, and every rank applies the series to its own block.
+ * All ranks must make the same call (same global shape, K, kernel, options);
+ * argument errors are detected on every rank before the first collective. */
 cpa_svt_status cpa_svt_apply(cpa_svt_handle* h, cpa_svt_dtype dtype, cpa_svt_math math,
                              int64_t m, int64_t n, cpa_svt_shard shard, int64_t long_global,
                              const void* X, int64_t ldx, void* Y, int64_t ldy,
@@ -241,9 +262,14 @@ typedef enum {
                                blockdiag of 8 x 8 DCT-II blocks, a smaller last block when 8 does not
                                divide s), otherwise as 2.  fp64 dense, unsharded only (else
                                CPA_SVT_E_UNSUPPORTED). */,
-  CPA_SVT_OPT_BATCHED = 2   /* engine of cpa_svt_apply_batched: 0 = auto (tcgen05), 1 = fp32 FFMA (exact
+  CPA_SVT_OPT_BATCHED = 2,  /* engine of cpa_svt_apply_batched: 0 = auto (tcgen05), 1 = fp32 FFMA (exact
                                fp32 products, apply-to-X form), 2 = tcgen05 3xTF32 (s x s form,
                                M = N = 64 MMAs, TMEM accumulators). */
+  CPA_SVT_OPT_DIVERGENCE = 3 /* SPEC.md:215 check of apply / apply_host / apply_csr outputs (one extra pass
+                               over X and Y): 0 = off, 1 = on, the verdict (CPA_SVT_E_DIVERGED) returned by
+                               calls that synchronise anyway (default), 2 = on, every call synchronises and
+                               returns it.  Sharded calls compare this rank's block of Y with its block of X.
+                               cpa_svt_apply_batched is not checked. */
 } cpa_svt_option;
 cpa_svt_status cpa_svt_set_option(cpa_svt_handle* h, cpa_svt_option opt, int64_t value);
 

@@ -87,6 +87,8 @@ lib.cpa_svt_profile.argtypes = [_p, ctypes.c_int]
 lib.cpa_svt_profile_read.argtypes = [_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)]
 PHASES = ["gram", "allreduce", "power", "init", "step", "sparse_z", "sparse_w", "batched", "final"]
 lib.cpa_svt_set_option.argtypes = [_p, ctypes.c_int, _i64]
+lib.cpa_svt_comm_info.argtypes = [_p, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
+lib.cpa_svt_comm_info.restype = ctypes.c_int
 lib.cpa_svt_admm_recover.argtypes = [_p, _i64, _i64, _p, _p, ctypes.c_int, ctypes.POINTER(Lambda), ctypes.POINTER(Admm), _p]
 lib.cpa_svt_admm_recover.restype = ctypes.c_int
 lib.cpa_svt_set_epsilon.argtypes = [_p, ctypes.c_int, ctypes.c_double]
@@ -149,10 +151,17 @@ class Handle:
             raise CpaSvtError(st, "cpa_svt_init")
         self._h = h
         self.rank, self.world = rank, world
+        self.has_comm = nccl_id is not None   # the library created an NCCL communicator (any world size)
 
     def _check(self, st, what):
         if st:
             raise CpaSvtError(st, f"{what}: {lib.cpa_svt_last_error(self._h).decode()}")
+
+    def comm_info(self):
+        """cpa_svt_comm_info -> (nranks, rank) of the library's NCCL communicator ((0, -1): none)."""
+        nr, rk = ctypes.c_int(0), ctypes.c_int(0)
+        self._check(lib.cpa_svt_comm_info(self._h, ctypes.byref(nr), ctypes.byref(rk)), "cpa_svt_comm_info")
+        return nr.value, rk.value
 
     @property
     def launches(self) -> int:
@@ -162,6 +171,11 @@ class Handle:
         """cpa_svt_set_option(FORM): 'auto' | 'apply' (W_k = Psi_k X) | 'poly' (Alg. 1 s x s form,
         symmetric lower-triangle tiles) | 'poly_full' (s x s form on full tiles, cross-check)."""
         self._check(lib.cpa_svt_set_option(self._h, 0, FORM[form]), "cpa_svt_set_option")
+
+    def set_divergence(self, mode: str):
+        """cpa_svt_set_option(DIVERGENCE): 'off' | 'on' (E_DIVERGED reported by syncing calls) |
+        'sync' (every call synchronises and reports it).  SPEC.md:215."""
+        self._check(lib.cpa_svt_set_option(self._h, 3, {"off": 0, "on": 1, "sync": 2}[mode]), "cpa_svt_set_option")
 
     def set_batched_engine(self, engine: str):
         """cpa_svt_set_option(BATCHED): 'auto' | 'ffma' (fp32 FFMA) | 'tc' (tcgen05 3xTF32)."""
@@ -213,14 +227,17 @@ class Handle:
         return Lambda(int(T), int(bool(want)), float(safety), float(lambda_max or 0.0), 0.0)
 
     def apply(self, X, kernel, K: int, T: int = 30, safety: float = 1.01, lambda_max: float = 0.0,
-              coeffs=None, Y=None, math: str = "native", shard: str = "none", long_global: int = 0,
+              coeffs=None, Y=None, math: str | None = None, shard: str = "none", long_global: int = 0,
               info: bool = False, want_lambda: bool = False):
-        """cpa_svt_apply on a 2-D CUDA tensor (float64: DMMA path; float32: TF32 paths)."""
+        """cpa_svt_apply on a 2-D CUDA tensor (float64: DMMA path; float32: tcgen05 3xTF32 by
+        default, math='tf32' for the single-pass reduced-accuracy mode)."""
         torch = self._torch
-        assert X.is_cuda and X.dim() == 2 and X.stride(1) == 1
+        assert X.is_cuda and X.dim() == 2 and X.stride(1) == 1 and X.dtype in (torch.float64, torch.float32)
+        if math is None:
+            math = "native" if X.dtype == torch.float64 else "3xtf32"
         if Y is None:
             Y = torch.empty(X.shape, dtype=X.dtype, device=X.device)
-        assert Y.shape == X.shape and Y.dtype == X.dtype and Y.stride(1) == 1
+        assert Y.shape == X.shape and Y.dtype == X.dtype and Y.stride(1) == 1 and Y.device == X.device
         dt = F64 if X.dtype == torch.float64 else F32
         lam = self._lambda(T, safety, lambda_max, want_lambda)
         inf = Info() if info else None
@@ -257,6 +274,13 @@ class Handle:
         assert X.is_cuda and X.dim() == 3 and X.dtype == torch.float32 and X.is_contiguous()
         if Y is None:
             Y = torch.empty_like(X)
+        # the kernel writes batch*m*n floats at Y and one float per matrix at lambda_out
+        assert (Y.is_cuda and Y.device == X.device and Y.dtype == torch.float32 and Y.is_contiguous()
+                and Y.shape == X.shape), "Y must be a contiguous float32 CUDA tensor shaped like X"
+        if lambda_out is not None:
+            assert (lambda_out.is_cuda and lambda_out.device == X.device and lambda_out.dtype == torch.float32
+                    and lambda_out.is_contiguous() and lambda_out.numel() >= X.shape[0]), \
+                "lambda_out must be a contiguous float32 CUDA tensor with >= batch elements"
         lam = self._lambda(T, safety, lambda_max, False)
         st = lib.cpa_svt_apply_batched(self._h, X.shape[0], X.shape[1], X.shape[2], X.data_ptr(), Y.data_ptr(),
                                        ctypes.byref(kernel_from_dict(kernel)), K, ctypes.byref(lam),
@@ -287,8 +311,15 @@ class Handle:
         """cpa_svt_apply_csr: CSR X (int64 row_ptr, int32 col, float64 val, all CUDA); returns dense rows."""
         torch = self._torch
         row_end = m if row_end is None else row_end
+        assert row_ptr.is_cuda and row_ptr.dtype == torch.int64 and row_ptr.is_contiguous() and row_ptr.numel() == m + 1
+        assert col.is_cuda and col.dtype == torch.int32 and col.is_contiguous()
+        assert val.is_cuda and val.dtype == torch.float64 and val.is_contiguous() and col.numel() == val.numel()
+        assert 0 <= row_begin <= row_end <= m
         if Y is None:
             Y = torch.empty((row_end - row_begin, n), dtype=torch.float64, device=val.device)
+        assert (Y.is_cuda and Y.device == val.device and Y.dtype == torch.float64 and Y.dim() == 2
+                and Y.stride(1) == 1 and Y.shape[0] >= row_end - row_begin and Y.shape[1] == n), \
+            "Y must be a float64 CUDA tensor with >= row_end - row_begin rows of n columns"
         lam = self._lambda(T, safety, lambda_max, want_lambda)
         inf = Info() if info else None
         st = lib.cpa_svt_apply_csr(self._h, m, n, val.numel(), row_ptr.data_ptr(), col.data_ptr(), val.data_ptr(),

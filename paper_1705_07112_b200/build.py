@@ -8,14 +8,14 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcpasvt.so")
 SOURCES = ["api.cu", "dense_f64.cu", "power.cu", "batched_f32.cu", "batched_tc.cu", "sparse_f64.cu", "tc_tf32.cu", "admm.cu",
-           "transform.cu", "small_f64.cu"]
+           "transform.cu", "small_f64.cu", "check.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"), "--expt-relaxed-constexpr"]
 
 
 def build(verbose=False, force=False, defines=(), lib=LIB, tag=""):
-    objs = []
+    objs, cmds = [], []
     bdir = os.path.join(HERE, "build" + tag)
     os.makedirs(bdir, exist_ok=True)
     for s in SOURCES:
@@ -28,8 +28,14 @@ def build(verbose=False, force=False, defines=(), lib=LIB, tag=""):
             if verbose:
                 cmd.insert(1, "-Xptxas=-v")
                 print(" ".join(cmd))
-            subprocess.run(cmd, check=True)
+            cmds.append(cmd)
         objs.append(obj)
+    # translation units compile in parallel (nvcc is single-threaded per file)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 1) or 1) as ex:
+        for r in list(ex.map(lambda c: subprocess.run(c), cmds)):
+            if r.returncode:
+                raise subprocess.CalledProcessError(r.returncode, r.args)
     if force or not os.path.exists(lib) or os.path.getmtime(lib) < max(os.path.getmtime(o) for o in objs):
         subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", lib, *objs,
                         "-ldl"], check=True)

@@ -103,6 +103,12 @@ cudaError_t launch_batched_f32(int64_t batch, int m, int n, const float* X, floa
 cudaError_t launch_batched_tc(int64_t batch, int m, int n, const float* X, float* Y, const cpa_svt_kernel& k,
                                int K, int T, double safety, double lam_override, float* lambda_out,
                                int num_sms, cudaStream_t st, int* launches, double* costab);
+// check.cu
+size_t divergence_scratch_doubles();
+cudaError_t divergence_check_f64(const double* X, int64_t xr, int64_t xc, int64_t ldx, const double* Y, int64_t yr,
+                                 int64_t yc, int64_t ldy, double* scratch, SeriesParams* P, cudaStream_t st);
+cudaError_t divergence_check_f32(const float* X, int64_t xr, int64_t xc, int64_t ldx, const float* Y, int64_t yr,
+                                 int64_t yc, int64_t ldy, double* scratch, SeriesParams* P, cudaStream_t st);
 // sparse_f64.cu
 cudaError_t sparse_apply(int64_t m, int64_t n, int64_t nnz, const int64_t* row_ptr, const int32_t* col,
                          const double* val, int64_t row_begin, int64_t row_end, double* Y, int64_t ldy,
@@ -124,6 +130,8 @@ struct NcclApi {
                             cudaStream_t) = nullptr;
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*CommCount)(const ncclComm_t, int*) = nullptr;
+  ncclResult_t (*CommUserRank)(const ncclComm_t, int*) = nullptr;
   bool load() {
     if (lib) return true;
     lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
@@ -135,7 +143,10 @@ struct NcclApi {
     AllReduce = (decltype(AllReduce))dlsym(lib, "ncclAllReduce");
     Broadcast = (decltype(Broadcast))dlsym(lib, "ncclBroadcast");
     GetErrorString = (decltype(GetErrorString))dlsym(lib, "ncclGetErrorString");
-    return GetUniqueId && CommInitRank && CommDestroy && AllReduce && Broadcast && GetErrorString;
+    CommCount = (decltype(CommCount))dlsym(lib, "ncclCommCount");
+    CommUserRank = (decltype(CommUserRank))dlsym(lib, "ncclCommUserRank");
+    return GetUniqueId && CommInitRank && CommDestroy && AllReduce && Broadcast && GetErrorString && CommCount &&
+           CommUserRank;
   }
 };
 NcclApi g_nccl;
@@ -150,6 +161,8 @@ struct cpa_svt_handle {
   SeriesParams* P = nullptr;       // device
   unsigned int* bar = nullptr;     // device, 2 uints (grid barrier)
   double* d_c = nullptr;           // device, KMAX (caller coefficients)
+  double* dchk = nullptr;          // device, divergence-check partial sums
+  int div_mode = 1;                // CPA_SVT_OPT_DIVERGENCE: 0 off, 1 check (status on syncing calls), 2 check + sync
   void* ws = nullptr;              // workspace
   size_t ws_bytes = 0;
   void* hx = nullptr;              // apply_host device staging
@@ -297,6 +310,16 @@ const char* cpa_svt_status_string(cpa_svt_status s) {
 const char* cpa_svt_last_error(const cpa_svt_handle* h) { return h ? h->err.c_str() : ""; }
 int64_t cpa_svt_launch_count(const cpa_svt_handle* h) { return h ? h->launches : 0; }
 
+cpa_svt_status cpa_svt_comm_info(const cpa_svt_handle* h, int* nranks, int* rank) {
+  if (!h || !nranks || !rank) return CPA_SVT_E_ARG;
+  *nranks = 0;
+  *rank = -1;
+  if (!h->comm) return CPA_SVT_OK;
+  if (g_nccl.CommCount(h->comm, nranks) != ncclSuccess || g_nccl.CommUserRank(h->comm, rank) != ncclSuccess)
+    return CPA_SVT_E_NCCL;
+  return CPA_SVT_OK;
+}
+
 cpa_svt_status cpa_svt_nccl_unique_id(void* out128) {
   if (!out128) return CPA_SVT_E_ARG;
   if (!g_nccl.load()) return CPA_SVT_E_NCCL;
@@ -323,12 +346,16 @@ cpa_svt_status cpa_svt_init(cpa_svt_handle** out, int device, void* cuda_stream,
   if (e == cudaSuccess) e = cudaMalloc(&h->bar, 64);
   if (e == cudaSuccess) e = cudaMemset(h->bar, 0, 64);
   if (e == cudaSuccess) e = cudaMalloc(&h->d_c, CPA_SVT_KMAX * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&h->dchk, divergence_scratch_doubles() * sizeof(double));
+  if (e == cudaSuccess) e = cudaMemset(h->dchk, 0, divergence_scratch_doubles() * sizeof(double));
   if (e != cudaSuccess) {
     cudaGetLastError();
     cpa_svt_free(h);
     return CPA_SVT_E_CUDA;
   }
-  if (world > 1) {
+  // a communicator whenever an id is given -- also for world == 1, so the shipped exchange
+  // (all-reduce of the Gram, broadcast of the series parameters) runs on a single GPU too
+  if (nccl_unique_id) {
     if (!g_nccl.load()) {
       cpa_svt_free(h);
       return CPA_SVT_E_NCCL;
@@ -354,6 +381,7 @@ cpa_svt_status cpa_svt_free(cpa_svt_handle* h) {
   cudaFree(h->P);
   cudaFree(h->bar);
   cudaFree(h->d_c);
+  cudaFree(h->dchk);
   cudaFree(h->ws);
   cudaFree(h->hx);
   cudaFree(h->tws);
@@ -380,6 +408,11 @@ cpa_svt_status cpa_svt_set_option(cpa_svt_handle* h, cpa_svt_option opt, int64_t
   if (opt == CPA_SVT_OPT_TRANSFORM) {
     if (value < 0 || value > 3) return CPA_SVT_E_ARG;
     h->transform = (int)value;
+    return CPA_SVT_OK;
+  }
+  if (opt == CPA_SVT_OPT_DIVERGENCE) {
+    if (value < 0 || value > 2) return CPA_SVT_E_ARG;
+    h->div_mode = (int)value;
     return CPA_SVT_OK;
   }
   if (opt == CPA_SVT_OPT_FORM) {
@@ -445,8 +478,10 @@ cpa_svt_status cpa_svt_coeffs(const cpa_svt_kernel* k, int K, double lambda_max,
   return CPA_SVT_OK;
 }
 
+// Synchronises and reports Lambda / info when the caller asked for them (or when
+// CPA_SVT_OPT_DIVERGENCE = 2); returns CPA_SVT_E_DIVERGED if the device check flagged the output.
 static cpa_svt_status fill_info(cpa_svt_handle* h, cpa_svt_info* info, cpa_svt_lambda* lam, int side) {
-  if (!info && !(lam && lam->want_lambda)) return CPA_SVT_OK;
+  if (!info && !(lam && lam->want_lambda) && h->div_mode != 2) return CPA_SVT_OK;
   SeriesParams hp;
   CU(cudaMemcpyAsync(&hp, h->P, offsetof(SeriesParams, c), cudaMemcpyDeviceToHost, h->stream));
   CU(cudaStreamSynchronize(h->stream));
@@ -462,6 +497,33 @@ static cpa_svt_status fill_info(cpa_svt_handle* h, cpa_svt_info* info, cpa_svt_l
     lam->lambda_hat = hp.lambda_hat;
     lam->lambda_max = hp.lambda_max;
   }
+  if (h->div_mode && hp.diverged) {
+    h->err = "||Y||_F > 1e3 sum|c_k| ||X||_F (or non-finite Y): Lambda_max below the Gram's top eigenvalue?";
+    return CPA_SVT_E_DIVERGED;
+  }
+  return CPA_SVT_OK;
+}
+
+// The divergence verdict of the last call (the stream must have been synchronised).
+static cpa_svt_status read_verdict(cpa_svt_handle* h) {
+  if (!h->div_mode) return CPA_SVT_OK;
+  int32_t d = 0;
+  CU(cudaMemcpy(&d, (const char*)h->P + offsetof(SeriesParams, diverged), sizeof(d), cudaMemcpyDeviceToHost));
+  if (d) {
+    h->err = "||Y||_F > 1e3 sum|c_k| ||X||_F (or non-finite Y): Lambda_max below the Gram's top eigenvalue?";
+    return CPA_SVT_E_DIVERGED;
+  }
+  return CPA_SVT_OK;
+}
+
+// SPEC.md:215 divergence check of the output against the input (check.cu); the verdict is read
+// by fill_info / read_verdict.  Off with CPA_SVT_OPT_DIVERGENCE = 0.
+static cpa_svt_status check_f64(cpa_svt_handle* h, const double* X, int64_t xr, int64_t xc, int64_t ldx,
+                                const double* Y, int64_t yr, int64_t yc, int64_t ldy, int* launches) {
+  if (!h->div_mode) return CPA_SVT_OK;
+  Phase p(h, CPA_SVT_PH_FINAL, 0);
+  CU(divergence_check_f64(X, xr, xc, ldx, Y, yr, yc, ldy, h->dchk, h->P, h->stream));
+  *launches += 1;
   return CPA_SVT_OK;
 }
 
@@ -562,19 +624,25 @@ static cpa_svt_status apply_f64_haar(cpa_svt_handle* h, int64_t m, int64_t n, co
   }
   const int64_t ml = left ? nl : m, nn = left ? n : nl;   // A_L in X's orientation
   h->transform = 0;
+  const int div_mode = h->div_mode;
+  h->div_mode = 0;   // the check below covers the recombined output
   st = apply_f64(h, ml, nn, CPA_SVT_SHARD_NONE, 0, AL, nn, YL, nn, k, K, c, lam, info);
   h->transform = 1;
+  h->div_mode = div_mode;
   if (st != CPA_SVT_OK) return st;
+  int nlh = 2;
   {
     Phase p(h, CPA_SVT_PH_FINAL);
     CU(dense_haar_combine(YL, AH, h->P, m, n, left, Y, ldy, h->num_sms, h->stream));
   }
-  h->launches += 2;
+  st = check_f64(h, X, m, n, ldx, Y, m, n, ldy, &nlh);
+  if (st != CPA_SVT_OK) return st;
+  h->launches += nlh;
   if (info) {
-    info->kernel_launches += 2;
+    info->kernel_launches += nlh;
     info->side = left ? 0 : 1;
   }
-  return CPA_SVT_OK;
+  return fill_info(h, info, lam, left ? 0 : 1);
 }
 
 static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt_shard shard,
@@ -582,7 +650,7 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
                                 const cpa_svt_kernel* k, int K, const double* c, cpa_svt_lambda* lam,
                                 cpa_svt_info* info) {
   if (h->transform == 1) {
-    if (shard != CPA_SVT_SHARD_NONE && h->world > 1) return CPA_SVT_E_UNSUPPORTED;
+    if (shard != CPA_SVT_SHARD_NONE && h->comm != nullptr) return CPA_SVT_E_UNSUPPORTED;
     return apply_f64_haar(h, m, n, X, ldx, Y, ldy, k, K, c, lam, info);
   }
   // side selection (reading R3): left iff global m <= global n
@@ -597,11 +665,13 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
     left = m <= n;
   }
   const int64_t s = left ? m : n, L = left ? n : m;
-  const bool sharded = shard != CPA_SVT_SHARD_NONE && h->world > 1;
+  const bool sharded = shard != CPA_SVT_SHARD_NONE && h->comm != nullptr;
   const bool dct = h->transform == 2 || h->transform == 3;   // NEXT-2 DCT variants (Phi = C G C^T, thresholded)
   const bool bdct = h->transform == 3;     // 8 x 8 block DCT
   const bool sparse_eps = dct && h->eps_mode != 0;
   if (dct && sharded) return CPA_SVT_E_UNSUPPORTED;
+  // validated before any device work or collective (see apply_tf32)
+  if (!(lam->lambda_max > 0.0) && s * (int64_t)sizeof(double) > 200 * 1024) return CPA_SVT_E_UNSUPPORTED;
   // small problems (s <= 64, L <= 128, e.g. BASELINE configs[0]): all of Alg. 1 in one
   // thread block (small_f64.cu) -- the s x s form, automatic form selection only
   if (!sharded && !dct && h->form == 0 && small_f64_fits(m, n) && !env_on("CPA_SVT_NO_SMALL")) {
@@ -623,17 +693,19 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
                           c_small, nsq, h->stream));
     }
     tm.mark();
-    h->launches += 1;
-    cpa_svt_status st = fill_info(h, info, lam, left ? 0 : 1);
+    int nl = 1;
+    cpa_svt_status st = check_f64(h, X, m, n, ldx, Y, m, n, ldy, &nl);
     if (st != CPA_SVT_OK) return st;
+    h->launches += nl;
+    st = fill_info(h, info, lam, left ? 0 : 1);
     if (info) {
       info->ms_gram = info->ms_allreduce = info->ms_power = 0.0f;
       info->ms_recurrence = tm.ms(0, 1);
       info->ms_total = tm.ms(0, 1);
-      info->kernel_launches = 1;
+      info->kernel_launches = nl;
       info->form = 4;
     }
-    return CPA_SVT_OK;
+    return st;
   }
   const int form = dct ? 2 : dense_form(h, s, L, K);
   const bool poly = form != 1;
@@ -744,7 +816,6 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
     Phase p(h, CPA_SVT_PH_POWER);
     CU(launch_series(h->P, *k, K, lam->safety, lam->lambda_max, nullptr, c_dev, h->stream));
   } else {
-    if (s * (int64_t)sizeof(double) > 200 * 1024) return CPA_SVT_E_UNSUPPORTED;
     Phase p(h, CPA_SVT_PH_POWER);
     // Repeated squaring: v_{T-1} ~ G^{T-1} v_0 is reached with (T-1)/p products by
     // c^p G^p (p = 2^j, c = 2^-ilogb(max G_ii), exact) plus the remainder by G, then
@@ -854,9 +925,10 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
     ++launches;
   }
   tm.mark();
+  st = check_f64(h, X, m, n, ldx, Y, m, n, ldy, &launches);
+  if (st != CPA_SVT_OK) return st;
   h->launches += launches;
   st = fill_info(h, info, lam, left ? 0 : 1);
-  if (st != CPA_SVT_OK) return st;
   if (info) {
     info->ms_gram = tm.ms(0, 1);
     info->ms_allreduce = tm.ms(1, 2);
@@ -866,7 +938,7 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
     info->kernel_launches = launches;
     info->form = form;
   }
-  return CPA_SVT_OK;
+  return st;
 }
 
 // fp32 data on the tcgen05 tensor cores: TF32 (rna operands) or 3xTF32 (hi/lo split).
@@ -884,9 +956,12 @@ static cpa_svt_status apply_tf32(cpa_svt_handle* h, int terms, int64_t m, int64_
   } else {
     left = m <= n;
   }
-  const bool sharded = shard != CPA_SVT_SHARD_NONE && h->world > 1;
+  const bool sharded = shard != CPA_SVT_SHARD_NONE && h->comm != nullptr;
   const int64_t s = left ? m : n, L = left ? n : m;
   if (s > 2147483647 / 2 || L > 2147483647 / 2) return CPA_SVT_E_UNSUPPORTED;
+  // every rank validates before the first collective is enqueued (a rank that returned
+  // early would leave its peers waiting inside NCCL)
+  if (!(lam->lambda_max > 0.0) && s * (int64_t)sizeof(double) > 200 * 1024) return CPA_SVT_E_UNSUPPORTED;
   const int64_t sp = (s + 3) / 4 * 4, Lp = (L + 3) / 4 * 4;
   // s x s form on full tiles (2(K-2) s^3 + 2 s^2 L) when it beats apply-to-X ((K-1) 2 s^2 L)
   const bool poly = K > 2 && h->form != 1;  // symmetric s x s form: fewer flops for any K > 2
@@ -949,7 +1024,6 @@ static cpa_svt_status apply_tf32(cpa_svt_handle* h, int terms, int64_t m, int64_
     Phase p(h, CPA_SVT_PH_POWER);
     CU(launch_series(h->P, *k, K, lam->safety, lam->lambda_max, nullptr, c_dev, h->stream));
   } else {
-    if (s * (int64_t)sizeof(double) > 200 * 1024) return CPA_SVT_E_UNSUPPORTED;
     Phase p(h, CPA_SVT_PH_POWER);
     CU(launch_power_dense_f32(Gf, s, sp, lam->power_iters, pw, h->bar, h->P, *k, K, lam->safety, c_dev, h->num_sms,
                               h->stream));
@@ -996,9 +1070,13 @@ static cpa_svt_status apply_tf32(cpa_svt_handle* h, int terms, int64_t m, int64_
   CU(tf32_finish(Yi, Lp, m, n, !left, Y, ldy, h->num_sms, h->stream));
   ++launches;
   tm.mark();
+  if (h->div_mode) {
+    Phase p(h, CPA_SVT_PH_FINAL, 0);
+    CU(divergence_check_f32(X, m, n, ldx, Y, m, n, ldy, h->dchk, h->P, h->stream));
+    launches += 1;
+  }
   h->launches += launches;
   st = fill_info(h, info, lam, left ? 0 : 1);
-  if (st != CPA_SVT_OK) return st;
   if (info) {
     info->ms_gram = tm.ms(0, 1);
     info->ms_allreduce = tm.ms(1, 2);
@@ -1008,7 +1086,7 @@ static cpa_svt_status apply_tf32(cpa_svt_handle* h, int terms, int64_t m, int64_
     info->kernel_launches = launches;
     info->form = poly ? 2 : 1;
   }
-  return CPA_SVT_OK;
+  return st;
 }
 
 cpa_svt_status cpa_svt_apply(cpa_svt_handle* h, cpa_svt_dtype dtype, cpa_svt_math math, int64_t m, int64_t n,
@@ -1089,21 +1167,21 @@ cpa_svt_status cpa_svt_apply_host(cpa_svt_handle* h, cpa_svt_dtype dtype, cpa_sv
     const bool delivered = h->hp_Y == nullptr;
     h->hp_X = nullptr;
     h->hp_Y = nullptr;
-    if (st != CPA_SVT_OK) {
+    if (st != CPA_SVT_OK && st != CPA_SVT_E_DIVERGED) {
       cudaStreamSynchronize(h->copy_stream);
       return st;
     }
     if (!delivered) CU(cudaMemcpyAsync(Y_host, dY, bytes, cudaMemcpyDeviceToHost, h->stream));
     CU(cudaStreamSynchronize(h->stream));
     CU(cudaStreamSynchronize(h->copy_stream));
-    return CPA_SVT_OK;
+    return read_verdict(h);
   }
   CU(cudaMemcpyAsync(dX, X_host, bytes, cudaMemcpyHostToDevice, h->stream));
   st = cpa_svt_apply(h, dtype, math, m, n, CPA_SVT_SHARD_NONE, 0, dX, n, dY, n, k, K, nullptr, lam, info);
-  if (st != CPA_SVT_OK) return st;
+  if (st != CPA_SVT_OK && st != CPA_SVT_E_DIVERGED) return st;
   CU(cudaMemcpyAsync(Y_host, dY, bytes, cudaMemcpyDeviceToHost, h->stream));
   CU(cudaStreamSynchronize(h->stream));
-  return CPA_SVT_OK;
+  return read_verdict(h);
 }
 
 // NEXT-3 (synthetic experiment PAPER.md:1095-1100): ADMM recovery of L from
@@ -1267,14 +1345,17 @@ cpa_svt_status cpa_svt_apply_csr(cpa_svt_handle* h, int64_t m, int64_t n, int64_
   CU(sparse_apply(m, n, nnz, row_ptr, col, val, row_begin, row_end, Y, ldy, *k, K, lam->power_iters, lam->safety,
                   lam->lambda_max, h->P, h->ws, h->ws_bytes, &need, h->num_sms, h->stream, &launches, phase_hook, h));
   tm.mark();
+  if (h->div_mode && nnz > 0) {   // ||X||_F from the stored values; this rank's rows of Y
+    CU(divergence_check_f64(val, 1, nnz, nnz, Y, row_end - row_begin, n, ldy, h->dchk, h->P, h->stream));
+    launches += 1;
+  }
   h->launches += launches;
   st = fill_info(h, info, lam, 1);
-  if (st != CPA_SVT_OK) return st;
   if (info) {
     info->ms_total = info->ms_recurrence = tm.ms(0, 1);
     info->kernel_launches = launches;
   }
-  return CPA_SVT_OK;
+  return st;
 }
 
 }  // extern "C"

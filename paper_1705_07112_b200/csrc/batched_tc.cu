@@ -32,6 +32,8 @@
 // the other CTA on the SM is in its own epilogue.
 #include <cstdlib>
 
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace cpa {
@@ -357,6 +359,8 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : 4) k_batched_tc(Args a) {
     } else {
       const int qsq = a.T >= 8 ? (a.T - 1) / 4 : 0;
       float g4[FR];
+#pragma unroll
+      for (int e = 0; e < FR; ++e) g4[e] = g[e];   // (only read when qsq > 0, then overwritten below)
       if (qsq > 0) {
         float dmax = 0.f;
 #pragma unroll
@@ -575,9 +579,12 @@ cudaError_t launch_batched_tc(int64_t batch, int m, int n, const float* X, float
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nt, btc::SMEM);
   if (e != cudaSuccess) return e;
   // 3 x (49 KB smem, 256 thr x <= 80 regs, 128 TMEM columns) or 4 x (128 thr x <= 128 regs) fit one SM
+  // (never more than `want`: each CTA holds its 128 TMEM columns for the whole persistent loop, so a
+  // fifth CTA on an SM would block in tcgen05.alloc forever; fewer if registers / shared memory
+  // limit residency -- the grid then stays one wave of what is actually resident)
   const int want = nt == 128 ? 4 : 3;
-  if (per_sm < want) per_sm = want;
-  if (const char* v = getenv("CPA_SVT_BTC_PER_SM")) per_sm = atoi(v);
+  if (per_sm > want) per_sm = want;
+  if (const char* v = getenv("CPA_SVT_BTC_PER_SM")) per_sm = std::min(atoi(v), per_sm);
   int64_t grid = (int64_t)num_sms * (per_sm > 0 ? per_sm : 1);
   if (grid > batch) grid = batch;
   kern<<<(unsigned)grid, nt, btc::SMEM, st>>>(a);

@@ -23,6 +23,8 @@ struct SeriesParams {
   double scale2;       // 2 / lambda_max  (0 when degenerate)
   int32_t degenerate;  // lambda_hat <= 1e-300
   int32_t K;
+  int32_t diverged;    // set by the divergence check (check.cu) after the recurrence, reset by compute_series
+  int32_t pad_;
   double c[CPA_SVT_KMAX];
 };
 

@@ -23,6 +23,7 @@ __device__ __forceinline__ void compute_series(SeriesParams* P, const cpa_svt_ke
     P->scale2 = degen ? 0.0 : 2.0 / lam;
     P->degenerate = degen;
     P->K = K;
+    P->diverged = 0;
     s_hdr[0] = lam;
     s_hdr[1] = tau;
     s_hdr[2] = degen;

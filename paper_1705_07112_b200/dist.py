@@ -49,20 +49,34 @@ def local_block(X, world: int, rank: int):
     return X[b:e, :]
 
 
-def make_handle(device: int, group=None):
-    """A Handle whose library-side NCCL communicator spans the torch.distributed world."""
+def make_handle(device: int, group=None, comm: bool = True):
+    """A Handle whose library-side NCCL communicator spans the torch.distributed world.
+
+    comm=True creates the communicator at any world size -- also a one-rank one, so the
+    sharded path with its NCCL all-reduce / broadcast runs on a single GPU.  Without
+    torch.distributed the id is made locally (world 1)."""
     import torch.distributed as dist
-    from . import Handle
+    from . import Handle, nccl_unique_id
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
-    nid = broadcast_nccl_id(group=group) if world > 1 else None
+    if world > 1:
+        nid = broadcast_nccl_id(group=group)
+    else:
+        nid = nccl_unique_id() if comm else None
     return Handle(device, nccl_id=nid, rank=rank, world=world)
 
 
-def apply_sharded(h, X_local, m_global: int, n_global: int, kernel, K: int, **kw):
-    """cpa_svt_apply on this rank's block; returns this rank's block of Y."""
+def shard_args(m_global: int, n_global: int, has_comm: bool) -> dict:
+    """shard / long_global arguments of cpa_svt_apply for a block of the (m_global x n_global) X."""
+    if not has_comm:
+        return {"shard": "none", "long_global": 0}
     shard = sharded_side(m_global, n_global)
-    long_global = n_global if shard == "cols" else m_global
-    if h.world == 1:
-        shard = "none"
-    return h.apply(X_local, kernel, K, shard=shard, long_global=long_global, **kw)
+    return {"shard": shard, "long_global": n_global if shard == "cols" else m_global}
+
+
+def apply_sharded(h, X_local, m_global: int, n_global: int, kernel, K: int, **kw):
+    """cpa_svt_apply on this rank's block; returns this rank's block of Y.  With a communicator
+    (any world size) the library runs the exchange: all-reduce of the partial Grams, broadcast
+    of the series parameters."""
+    return h.apply(X_local, kernel, K, **shard_args(m_global, n_global, getattr(h, "has_comm", h.world > 1)),
+                   **kw)

@@ -85,3 +85,46 @@ def test_batched_deterministic(env):
     a, _ = _run(env, Xb, cfg["kernel"], cfg["K"])
     b, _ = _run(env, Xb, cfg["kernel"], cfg["K"])
     assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("T", [1, 2, 5, 7, 8, 9])
+def test_batched_short_power_iterations(env, T):
+    """T < 8 runs the power iteration without the squared Gram (qsq = 0); T = 8, 9 the first
+    squared cases.  The oracle runs the same T plain products (reading R6)."""
+    cfg = W.CONFIGS["c3"]
+    Xb = W.gen_c3(batch=64, seed=T)
+    Y, lam = _run(env, Xb, cfg["kernel"], cfg["K"], T=T)
+    Yo, lo = O.cpa_shrink_batched(Xb.astype(np.float64), O.Kernel(**cfg["kernel"]), cfg["K"], T=T)
+    assert O.rel_fro(Y, Yo) <= TOL32
+    assert np.max(np.abs(lam - lo) / lo) < 1e-5
+
+
+def test_batched_256_thread_instance(env):
+    """The 8-warp CTA instance (CPA_SVT_BTC_NT=256, 3 CTAs per SM) against the oracle and
+    against the default 128-thread instance."""
+    import os
+    cfg = W.CONFIGS["c3"]
+    Xb = W.gen_c3(batch=1000, seed=9)
+    Y128, _ = _run(env, Xb, cfg["kernel"], cfg["K"], T=cfg["T"])
+    os.environ["CPA_SVT_BTC_NT"] = "256"
+    try:
+        Y256, lam = _run(env, Xb, cfg["kernel"], cfg["K"], T=cfg["T"])
+    finally:
+        del os.environ["CPA_SVT_BTC_NT"]
+    Yo, lo = O.cpa_shrink_batched(Xb.astype(np.float64), O.Kernel(**cfg["kernel"]), cfg["K"], T=cfg["T"])
+    assert O.rel_fro(Y256, Yo) <= TOL32 and O.rel_fro(Y128, Yo) <= TOL32
+    assert O.rel_fro(Y256, Y128) <= 1e-5
+
+
+def test_batched_argument_checks(env):
+    torch, P, h = env
+    X = torch.zeros((4, 8, 8), dtype=torch.float32, device="cuda")
+    kern = {"kind": "soft", "tau": 0.5}
+    with pytest.raises(AssertionError):
+        h.apply_batched(X, kern, 5, Y=torch.zeros((3, 8, 8), dtype=torch.float32, device="cuda"))
+    with pytest.raises(AssertionError):
+        h.apply_batched(X, kern, 5, Y=torch.zeros((4, 8, 8), dtype=torch.float64, device="cuda"))
+    with pytest.raises(AssertionError):
+        h.apply_batched(X, kern, 5, lambda_out=torch.zeros(3, dtype=torch.float32, device="cuda"))
+    with pytest.raises(AssertionError):
+        h.apply_batched(X, kern, 5, lambda_out=torch.zeros(4, dtype=torch.float64, device="cuda"))

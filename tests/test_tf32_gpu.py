@@ -2,10 +2,12 @@
 and 3xTF32) with the fp64 oracle on the fp32-rounded inputs (reading R15).
 
 Bar (north_star): relative Frobenius error <= 1e-4 on the fp32/TF32 path.  The
-3xTF32 mode (the fp32 default) meets it with ~50x margin (measured 1-3e-6);
-single-pass TF32 with round-to-nearest operands lands at 0.6-1.5e-4, i.e. it
-does NOT meet the bar on every input: it is tested against
-3e-4 and reported, not claimed.
+3xTF32 mode (the fp32 default, CPA_SVT_MATH_3XTF32) meets it with ~50x margin
+(measured 1-3e-6) and is the fp32 path the north-star numbers are claimed on.
+Single-pass TF32 (CPA_SVT_MATH_TF32, declared in include/cpa_svt.h as a
+reduced-accuracy mode) lands at 0.5-1.5e-4 on the small shapes below: there it is
+gated at TF32_REDUCED = 3e-4 and NOT claimed; the c5 full-size single-pass run
+(the only single-pass number reported) is gated at the 1e-4 bar.
 """
 
 import numpy as np
@@ -16,6 +18,7 @@ import workloads as W
 
 pytestmark = pytest.mark.gpu
 TOL32 = 1e-4
+TF32_REDUCED = 3e-4   # single-pass TF32 on small shapes: reported, not claimed (see above)
 
 
 @pytest.fixture(scope="module")
@@ -56,7 +59,7 @@ def test_tf32_parity(env, math, shape, K):
     Yo, io = O.cpa_shrink(X, O.Kernel(**kern), K, T=300, return_info=True)
     # lambda_hat of an fp32 Gram: unconverged power iterations move by ~T * eps_G
     assert abs(info["lambda_hat"] - io["lambda_hat"]) <= 1e-4 * io["lambda_hat"]
-    assert O.rel_fro(Y, Yo) <= (TOL32 if math == "3xtf32" else 3e-4), O.rel_fro(Y, Yo)
+    assert O.rel_fro(Y, Yo) <= (TOL32 if math == "3xtf32" else TF32_REDUCED), O.rel_fro(Y, Yo)
 
 
 def test_tf32_config5_proxy(env):
@@ -66,7 +69,7 @@ def test_tf32_config5_proxy(env):
     Yo = O.cpa_shrink(X, O.Kernel(**cfg["kernel"]), cfg["K"], T=cfg["T"])
     for math in ("tf32", "3xtf32"):
         Y, _ = _run(env, X, cfg["kernel"], cfg["K"], math, T=cfg["T"])
-        assert O.rel_fro(Y, Yo) <= (TOL32 if math == "3xtf32" else 3e-4), (math, O.rel_fro(Y, Yo))
+        assert O.rel_fro(Y, Yo) <= (TOL32 if math == "3xtf32" else TF32_REDUCED), (math, O.rel_fro(Y, Yo))
 
 
 def test_tf32_gemm_engine(env):
@@ -128,10 +131,10 @@ def test_config5_full_size_sampled_tf32(env):
     lam = 1.01 * lam_hat
     c = O.kernel_coefficients(O.Kernel(**cfg["kernel"]), cfg["K"], lam, m_.sqrt(lam_hat))
     Yo = O.cpa_apply_vectors(lambda V: G @ V, X[:, cols], c, lam)
-    for math, tol in (("3xtf32", TOL32), ("tf32", 3e-4)):
+    for math, tol in (("3xtf32", TOL32), ("tf32", TOL32)):
         Ys, info = got[math]
         print(math, "lambda rel err", info["lambda_hat"] / lam_hat - 1, "Y rel err", O.rel_fro(Ys, Yo))
-    for math, tol in (("3xtf32", TOL32), ("tf32", 3e-4)):
+    for math, tol in (("3xtf32", TOL32), ("tf32", TOL32)):
         Ys, info = got[math]
         assert abs(info["lambda_hat"] - lam_hat) <= 1e-5 * lam_hat, math
         assert O.rel_fro(Ys, Yo) <= tol, (math, O.rel_fro(Ys, Yo))

@@ -194,3 +194,29 @@ def synthetic_D(N: int, rank: int) -> np.ndarray:
     for b in range(rank):
         D[b * p:(b + 1) * p, b * p:(b + 1) * p] -= 0.5
     return D
+
+
+def gen_c3_closed_form(batch: int = 65536, seed: int = 0, n: int = 64, n_scales: int = 256):
+    """Closed-form stand-ins for the c3 batch (full-scale checks without the oracle per matrix):
+    matrix b has scale a = scales[b % n_scales] (uniform in [0.5, 20]);
+      even b: X_b = a Q_b, Q_b a random orthogonal n x n matrix (QR of a Gaussian draw, signs fixed);
+      odd b:  X_b = a diag(ratios) with the fixed ratios (1, then uniform in [0.05, 0.5]) -- a
+              dominant first entry so the power iteration converges in a few steps.
+    Returns (X float32 [batch, n, n], scales float64 [n_scales], ratios float64 [n]).  No arithmetic
+    of the method; the expected outputs come from the oracle's series (tests)."""
+    rng = np.random.default_rng(seed)
+    scales = rng.uniform(0.5, 20.0, n_scales)
+    ratios = np.concatenate([[1.0], rng.uniform(0.05, 0.5, n - 1)])
+    X = np.zeros((batch, n, n), dtype=np.float32)
+    ne = (batch + 1) // 2
+    blk = 4096
+    for i in range(0, ne, blk):
+        j = min(ne, i + blk)
+        q, r = np.linalg.qr(rng.standard_normal((j - i, n, n)))
+        q = q * np.sign(np.diagonal(r, axis1=1, axis2=2))[:, None, :]
+        b = 2 * np.arange(i, j)
+        X[b] = (scales[b % n_scales][:, None, None] * q).astype(np.float32)
+    b = np.arange(1, batch, 2)
+    idx = np.arange(n)
+    X[b[:, None], idx[None, :], idx[None, :]] = (scales[b % n_scales][:, None] * ratios[None, :]).astype(np.float32)
+    return X, scales, ratios
