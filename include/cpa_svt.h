@@ -285,8 +285,9 @@ typedef enum {
   CPA_SVT_PH_SPARSE_Z = 5,   /* sparse: Z = W_{k-1} X^T */
   CPA_SVT_PH_SPARSE_W = 6,   /* sparse: W_k = (4/L) Z X - 2 W_{k-1} - W_{k-2}, Y += c_k W_k */
   CPA_SVT_PH_BATCHED = 7,    /* batched kernel */
-  CPA_SVT_PH_FINAL = 8,      /* s x s form: the final product Y = H_hat X */
-  CPA_SVT_PH_COUNT = 9
+  CPA_SVT_PH_FINAL = 8,      /* s x s form: the final product Y = H_hat X (+ the divergence check) */
+  CPA_SVT_PH_EXCHANGE = 9,   /* multi-GPU s x s form: per-step all-gather of the tile panels + unpack */
+  CPA_SVT_PH_COUNT = 10
 } cpa_svt_phase;
 /* enable != 0: reset the accumulators and start recording; 0: stop. */
 cpa_svt_status cpa_svt_profile(cpa_svt_handle* h, int enable);

@@ -85,7 +85,7 @@ lib.cpa_svt_debug_gemm_tf32.argtypes = [_p, ctypes.c_int, ctypes.c_int, ctypes.c
 lib.cpa_svt_debug_gemm_tf32.restype = ctypes.c_int
 lib.cpa_svt_profile.argtypes = [_p, ctypes.c_int]
 lib.cpa_svt_profile_read.argtypes = [_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)]
-PHASES = ["gram", "allreduce", "power", "init", "step", "sparse_z", "sparse_w", "batched", "final"]
+PHASES = ["gram", "allreduce", "power", "init", "step", "sparse_z", "sparse_w", "batched", "final", "exchange"]
 lib.cpa_svt_set_option.argtypes = [_p, ctypes.c_int, _i64]
 lib.cpa_svt_comm_info.argtypes = [_p, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
 lib.cpa_svt_comm_info.restype = ctypes.c_int

@@ -61,6 +61,14 @@ cudaError_t dense_haar_combine(const double* YL, const double* AH, const SeriesP
                                bool left, double* Y, int64_t ldy, int num_sms, cudaStream_t st);
 cudaError_t dense_eye(double* I, int64_t s, cudaStream_t st);
 size_t dense_sym_sync_ints(int64_t s, int K, int num_sms);
+int64_t dense_sym_ntri(int64_t s);
+int64_t dense_sym_panel_tile0(int64_t s, int p, int P);
+int64_t dense_sym_panel_slot(int64_t s, int P);
+size_t dense_sym_panel_partial_doubles(int64_t s, int P, int num_sms);
+cudaError_t dense_cheb_sym_panel(int64_t s, const double* G, double* W0, double* W1, double* W2, double* H,
+                                 const SeriesParams* P, int K, int kstep, int64_t tile0, int64_t ntile,
+                                 double* gout, int* sync, double* partial, int num_sms, cudaStream_t st);
+cudaError_t dense_sym_unpack(const double* gbuf, int64_t s, int P, double* out, cudaStream_t st);
 size_t dense_sym_partial_doubles(int64_t s, int num_sms);
 cudaError_t dense_sym_init(int64_t s, const double* G, double* Wa, double* H, const SeriesParams* P, int K,
                            int num_sms, cudaStream_t st);
@@ -129,6 +137,7 @@ struct NcclApi {
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
   ncclResult_t (*CommCount)(const ncclComm_t, int*) = nullptr;
   ncclResult_t (*CommUserRank)(const ncclComm_t, int*) = nullptr;
@@ -142,11 +151,12 @@ struct NcclApi {
     CommDestroy = (decltype(CommDestroy))dlsym(lib, "ncclCommDestroy");
     AllReduce = (decltype(AllReduce))dlsym(lib, "ncclAllReduce");
     Broadcast = (decltype(Broadcast))dlsym(lib, "ncclBroadcast");
+    AllGather = (decltype(AllGather))dlsym(lib, "ncclAllGather");
     GetErrorString = (decltype(GetErrorString))dlsym(lib, "ncclGetErrorString");
     CommCount = (decltype(CommCount))dlsym(lib, "ncclCommCount");
     CommUserRank = (decltype(CommUserRank))dlsym(lib, "ncclCommUserRank");
-    return GetUniqueId && CommInitRank && CommDestroy && AllReduce && Broadcast && GetErrorString && CommCount &&
-           CommUserRank;
+    return GetUniqueId && CommInitRank && CommDestroy && AllReduce && Broadcast && AllGather && GetErrorString &&
+           CommCount && CommUserRank;
   }
 };
 NcclApi g_nccl;
@@ -709,6 +719,18 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
   }
   const int form = dct ? 2 : dense_form(h, s, L, K);
   const bool poly = form != 1;
+  // Multi-GPU s x s recurrence (form 2, sharded): each rank computes a contiguous 1/P of the
+  // lower tiles of every step and the steps' tiles are all-gathered (ncclAllGather, in place)
+  // and unpacked into the full Psi_k on every rank -- instead of every rank evaluating the whole
+  // s x s recurrence.  CPA_SVT_PANELS=1 forces it at world 1 (real NCCL all-gather of one rank);
+  // CPA_SVT_PANEL_SIM=P runs P virtual ranks' panels one after the other on one GPU (tests of the
+  // partition / pack / unpack; the slots are already in place, so no collective).
+  int panel_sim = 0;
+  if (const char* v = getenv("CPA_SVT_PANEL_SIM")) panel_sim = atoi(v);
+  const bool panels = form == 2 && K > 2 && !sparse_eps &&
+                      ((sharded && (h->world > 1 || env_on("CPA_SVT_PANELS"))) || (panel_sim > 1 && h->world == 1));
+  const int panel_P = panels ? (panel_sim > 1 && h->world == 1 ? panel_sim : h->world) : 1;
+  const size_t nGb = panels ? (size_t)panel_P * (size_t)dense_sym_panel_slot(s, panel_P) * 4096 : 0;
   if (h->hp_X && (sharded || dct || !poly)) {   // (the host pipeline covers the plain s x s form only)
     CU(cudaMemcpyAsync((double*)X, h->hp_X, (size_t)m * n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
     h->hp_X = nullptr;
@@ -723,10 +745,11 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
   const bool final_split = !env_on("CPA_SVT_FINAL_NOSPLIT");  // line-12 product split-K (default on)
   const size_t nPart = r32(std::max({dense_flow_partial_doubles(RM, RN, h->num_sms), dense_gram_partial_doubles(s),
                                      form == 2 ? dense_sym_partial_doubles(s, h->num_sms) : (size_t)0,
+                                     panels ? dense_sym_panel_partial_doubles(s, panel_P, h->num_sms) : (size_t)0,
                                      final_split && poly ? dense_store_partial_doubles(m, n) : (size_t)0}));
   const size_t nSync = std::max({dense_flow_sync_ints(RM, RN, K), (size_t)((s / 64 + 2) * (s / 64 + 2)),
                                  dense_sym_sync_ints(s, K, h->num_sms), (size_t)1332});
-  const size_t need = (nG + 2 * nW + nX + nPow + nPart) * sizeof(double) + nSync * sizeof(int) + 256;
+  const size_t need = (nG + 2 * nW + nX + nPow + nPart + nGb) * sizeof(double) + nSync * sizeof(int) + 256;
   cpa_svt_status st = grow(h, &h->ws, &h->ws_bytes, need);
   if (st != CPA_SVT_OK) return st;
   double* G = (double*)h->ws;
@@ -736,7 +759,8 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
   double* H = Is + nG;           // poly form: H_hat
   double* pw = Wb + nW + nX;
   double* part = pw + nPow;
-  int* flow_sync = (int*)(part + nPart);
+  double* gbuf = part + nPart;    // panel mode: P all-gather slots of packed 64 x 64 tiles
+  int* flow_sync = (int*)(gbuf + nGb);
 
   const double* c_dev = nullptr;
   if (c) {
@@ -863,11 +887,32 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
         ++launches;
       }
       if (K > 2) {
-        Phase p(h, CPA_SVT_PH_STEP);
         if (sparse_eps) {  // lines 8-11 on the sparse Phi_ (one launch per step)
+          Phase p(h, CPA_SVT_PH_STEP);
           CU(dct_sparse_steps(s, csr_rp, csr_col, csr_val, Wa, Wb, H, h->P, K, h->num_sms, h->stream));
           launches += K - 2;
+        } else if (panels) {
+          double* Wr[3] = {Is, Wa, Wb};   // Psi_k lives in Wr[k % 3]; Wr[1] = Psi_1 from the init
+          const int64_t slot = dense_sym_panel_slot(s, panel_P);
+          for (int kk = 2; kk < K; ++kk) {
+            const int v0 = panel_sim > 1 ? 0 : h->rank, v1 = panel_sim > 1 ? panel_P : h->rank + 1;
+            for (int v = v0; v < v1; ++v) {
+              const int64_t t0 = dense_sym_panel_tile0(s, v, panel_P), t1 = dense_sym_panel_tile0(s, v + 1, panel_P);
+              Phase ps(h, CPA_SVT_PH_STEP);
+              CU(dense_cheb_sym_panel(s, G, Wr[0], Wr[1], Wr[2], H, h->P, K, kk, t0, t1 - t0,
+                                      gbuf + (size_t)v * slot * 4096, flow_sync, part, h->num_sms, h->stream));
+              ++launches;
+            }
+            Phase px(h, CPA_SVT_PH_EXCHANGE);
+            if (panel_sim <= 1)
+              NC(g_nccl.AllGather(gbuf + (size_t)h->rank * slot * 4096, gbuf, (size_t)slot * 4096, ncclDouble,
+                                  h->comm, h->stream));
+            // Psi_k into its rotation buffer (over Psi_{k-3}); the last step's slots hold H_hat
+            CU(dense_sym_unpack(gbuf, s, panel_P, kk == K - 1 ? H : Wr[kk % 3], h->stream));
+            ++launches;
+          }
         } else {
+          Phase p(h, CPA_SVT_PH_STEP);
           CU(dense_cheb_sym(s, G, Is, Wa, Wb, H, h->P, K, flow_sync, part, h->num_sms, h->stream));  // Is: 3rd W buffer
           ++launches;
         }

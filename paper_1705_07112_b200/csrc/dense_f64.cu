@@ -380,6 +380,13 @@ struct SymArgs {
   int* sync;            // [0] ticket | K * T cross counters | ntri split counters
   double* partial;      // ntri * (split - 1) * 64 * 64
   int vec;
+  // panel mode (multi-GPU row panels of the lower triangle): this launch computes ONE step
+  // (kstep) on the ntile tiles [tile0, tile0 + ntile) of the column-major lower-triangle order,
+  // with W_{k-1} / W_{k-2} complete on entry (no dependency waits), and writes W_k (or, at the
+  // last step, H) of those tiles PACKED to gout: tile t at gout + (t - tile0) * 4096, row-major
+  // 64 x 64 -- the slot the all-gather exchanges.  H accumulates in place on the own tiles.
+  int panel, kstep, tile0, ntile;
+  double* gout;
 };
 
 __global__ void k_sym_init(const double* __restrict__ G, int64_t s, double* __restrict__ W1, double* __restrict__ H,
@@ -503,8 +510,9 @@ __device__ __forceinline__ void sym_finish(const SymArgs& a, int k, int tile, in
   const double* wpp = buf((k - 2) % 3);   // W_{k-2} (k = 2: identity, implicit)
   double* out = buf(k % 3);               // W_k over W_{k-3}
   const int64_t m0 = (int64_t)ti * BM, n0 = (int64_t)tj * BN;
+  const int kc = a.panel ? 2 : k;         // split counters: per launch in panel mode (zeroed before it)
   if (S > 1) {
-    double* slot = a.partial + (int64_t)tile * (S - 1) * (BM * BN);
+    double* slot = a.partial + (int64_t)(tile - (a.panel ? a.tile0 : 0)) * (S - 1) * (BM * BN);
     if (q < S - 1) {
       double* mine = slot + (int64_t)q * (BM * BN);
 #pragma unroll
@@ -517,7 +525,7 @@ __device__ __forceinline__ void sym_finish(const SymArgs& a, int k, int tile, in
       if (threadIdx.x == 0) red_release_add_i32(split_cnt + tile, 1);
       return;
     }
-    if (threadIdx.x == 0) wait_geq(split_cnt + tile, (S - 1) * (k - 1));
+    if (threadIdx.x == 0) wait_geq(split_cnt + tile, (S - 1) * (kc - 1));
     __syncthreads();
     double sum[32];
 #pragma unroll
@@ -563,6 +571,11 @@ __device__ __forceinline__ void sym_finish(const SymArgs& a, int k, int tile, in
         const int qq = j * 2 + e;
         const double wv = s4 * acc[i][j][e] - 2.0 * vp[qq] - vpp[qq];  // W_k = 2 B_hat W_{k-1} - W_{k-2}
         const double y = vy[qq] + ck * wv;                               // H += c_k W_k
+        if (a.panel) {   // packed slot of the all-gather: W_k, or H at the last step
+          a.gout[(int64_t)(tile - a.tile0) * (BM * BN) + (rr - m0) * BN + (c - n0)] = last ? y : wv;
+          if (!last) a.H[rr * s + c] = y;
+          continue;
+        }
         if (!last) {
           out[rr * s + c] = wv;
           out[c * s + rr] = wv;
@@ -570,6 +583,10 @@ __device__ __forceinline__ void sym_finish(const SymArgs& a, int k, int tile, in
         a.H[rr * s + c] = y;
         if (last) a.H[c * s + rr] = y;
       }
+  }
+  if (a.panel) {   // (the launch boundary orders the stores; no crosses to release)
+    __syncthreads();
+    return;
   }
   if (tma) fence_proxy_async_global();   // W_k / H stores -> later TMA (async-proxy) reads
   __syncthreads();
@@ -585,8 +602,8 @@ __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB) k_cheb_sym(SymArgs a)
   const int T = a.T;
   const int ntri = T * (T + 1) / 2;
   const int S = a.split;
-  const int per_step = ntri * S;
-  const int total = (a.K - 2) * per_step;
+  const int per_step = (a.panel ? a.ntile : ntri) * S;
+  const int total = a.panel ? per_step : (a.K - 2) * per_step;
   int* cross = a.sync + 1;
   const int64_t s = a.s;
   const int nk = (int)((s + BKS - 1) / BKS);
@@ -595,10 +612,10 @@ __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB) k_cheb_sym(SymArgs a)
     __syncthreads();
     const int tk = s_ticket;
     if (tk >= total) break;
-    const int k = 2 + tk / per_step;
+    const int k = a.panel ? a.kstep : 2 + tk / per_step;
     const int r = tk % per_step;
     const int q = r % S;
-    const int tile = r / S;
+    const int tile = r / S + (a.panel ? a.tile0 : 0);
     int ti, tj;
     tri_decode_colmajor(tile, T, ti, tj);
     auto buf = [&](int i) { return i == 0 ? a.W[0] : (i == 1 ? a.W[1] : a.W[2]); };
@@ -608,7 +625,7 @@ __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB) k_cheb_sym(SymArgs a)
     double acc[4][4][2];
     mainloop_dep(a.G, src, s, m0, n0, a.vec, smem, acc, kb, ke, [&] {
 #ifndef CPA_SYM_NOWAIT  // (timing experiment only: wrong results without the waits)
-      if (threadIdx.x == 0) {
+      if (threadIdx.x == 0 && !a.panel) {
         if (k >= 3) wait_geq(cross + (k - 1) * T + tj, T);
         if (k >= 4) wait_geq(cross + (k - 2) * T + ti, T);
       }
@@ -656,8 +673,8 @@ __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB)
   const int T = a.T;
   const int ntri = T * (T + 1) / 2;
   const int S = a.split;
-  const int per_step = ntri * S;
-  const int total = (a.K - 2) * per_step;
+  const int per_step = (a.panel ? a.ntile : ntri) * S;
+  const int total = a.panel ? per_step : (a.K - 2) * per_step;
   int* cross = a.sync + 1;
   const int nk = (int)((a.s + SBK - 1) / SBK);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -685,10 +702,10 @@ __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB)
     __syncthreads();
     const int tk = s_ticket;
     if (tk >= total) break;
-    const int k = 2 + tk / per_step;
+    const int k = a.panel ? a.kstep : 2 + tk / per_step;
     const int r = tk % per_step;
     const int q = r % S;
-    const int tile = r / S;
+    const int tile = r / S + (a.panel ? a.tile0 : 0);
     int ti, tj;
     tri_decode_colmajor(tile, T, ti, tj);
     const CUtensorMap* wmap = &mp.w[(k - 1) % 3];   // W_{k-1}
@@ -705,8 +722,10 @@ __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB)
         for (int b = 0; b < 4; ++b)
           tma_load_2d(base + st * SSTAGE_BYTES + b * SBOX_BYTES, &mp.g, m0 + 16 * b, (kb + p) * SBK, full + st);
       }
-      if (k >= 3) wait_geq(cross + (k - 1) * T + tj, T);
-      if (k >= 4) wait_geq(cross + (k - 2) * T + ti, T);
+      if (!a.panel) {
+        if (k >= 3) wait_geq(cross + (k - 1) * T + tj, T);
+        if (k >= 4) wait_geq(cross + (k - 2) * T + ti, T);
+      }
       fence_proxy_async_global();   // generic-proxy W_{k-1} stores of other CTAs -> TMA reads
       for (int p = 0; p < P; ++p) {
         const uint32_t st = (it + p) % SSTAGES;
@@ -1381,8 +1400,8 @@ static int sym_slots(int num_sms) {
 // k-splits per tile: about two units per resident slot per step (shorter units
 // make the wavefront finer; c2 measured: S = 4 / 6 / 8 -> 1.46 / 1.31 / 1.39 ms),
 // at least 4 k-slabs per unit, at most 8.
-static int sym_split(int64_t s, int slots) {
-  const int64_t T = (s + BM - 1) / BM, ntri = T * (T + 1) / 2;
+static int sym_split(int64_t s, int slots, int64_t ntiles = -1) {
+  const int64_t T = (s + BM - 1) / BM, ntri = ntiles >= 0 ? ntiles : T * (T + 1) / 2;
   const int64_t nk = (s + BKS - 1) / BKS;
   int S = 1;
   while (S < 8 && ntri * S * 10 < 18 * (int64_t)slots && nk / (S + 1) >= 4) ++S;
@@ -1409,6 +1428,8 @@ cudaError_t dense_sym_init(int64_t s, const double* G, double* W1, double* H, co
   k_sym_init<<<num_sms * 4, 256, 0, st>>>(G, s, K > 2 ? W1 : nullptr, H, P);
   return cudaGetLastError();
 }
+
+static cudaError_t sym_launch(SymArgs& a, int64_t total, int slots, int num_sms, cudaStream_t st);
 
 // H_hat += sum_{k=2}^{K-1} c_k Psi_k(B_hat) on the s x s Gram: one persistent launch
 // for all K-2 steps.  W0, W1, W2: s x s buffers, W1 = W_1 from dense_sym_init.
@@ -1445,15 +1466,23 @@ cudaError_t dense_cheb_sym(int64_t s, const double* G, double* W0, double* W1, d
     return go(k_cheb_sym_cl<8>, 8);
   }
   const int64_t total = (int64_t)(K - 2) * a.T * (a.T + 1) / 2 * a.split;
+  return sym_launch(a, total, slots, num_sms, st);
+}
+
+// The persistent symmetric-step kernel over `total` units: TMA-fed for even s (the cp.async
+// kernel for odd s, whose rows are not 16-byte aligned).
+static cudaError_t sym_launch(SymArgs& a, int64_t total, int slots, int num_sms, cudaStream_t st) {
+  const int64_t s = a.s;
+  const size_t smem = sym_smem();
   const int64_t grid = slots < total ? slots : total;
+  cudaError_t e;
   if (!env_on("CPA_SVT_SYM_NOTMA") && s % 2 == 0 && s <= INT32_MAX / 2) {
-    // TMA-fed kernel (default; the cp.async kernel for odd s, whose rows are not 16-byte
-    // aligned): one fp64 tensor map per operand (16 x 16 boxes, 128-byte swizzle)
+    // one fp64 tensor map per operand (16 x 16 boxes, 128-byte swizzle)
     EncodeTiledFn fn = encode_fn();
     SymMaps mp;
     bool ok = fn != nullptr;
     const int sbk = s >= 4096 ? 32 : 16;   // slab depth of the k_cheb_sym_tma instance (see there)
-    const double* ops[4] = {G, W0, W1, W2};
+    const double* ops[4] = {a.G, a.W[0], a.W[1], a.W[2]};
     CUtensorMap* maps[4] = {&mp.g, &mp.w[0], &mp.w[1], &mp.w[2]};
     for (int i = 0; i < 4 && ok; ++i) {
       cuuint64_t dims[2] = {(cuuint64_t)s, (cuuint64_t)s};
@@ -1481,6 +1510,88 @@ cudaError_t dense_cheb_sym(int64_t s, const double* G, double* W0, double* W1, d
   }
   void* args[] = {&a};
   return cudaLaunchCooperativeKernel((void*)k_cheb_sym, dim3((unsigned)grid), dim3(NTHREADS), args, smem, st);
+}
+
+// ---- panel mode (multi-GPU): one step on a contiguous range of lower tiles ------------
+// Tiles of the column-major lower-triangle order are split in P contiguous, balanced ranges;
+// rank p owns [panel_tile0(p), panel_tile0(p + 1)).
+int64_t dense_sym_ntri(int64_t s) {
+  const int64_t T = (s + BM - 1) / BM;
+  return T * (T + 1) / 2;
+}
+int64_t dense_sym_panel_tile0(int64_t s, int p, int P) { return dense_sym_ntri(s) * p / P; }
+int64_t dense_sym_panel_slot(int64_t s, int P) {   // tiles per all-gather slot (the largest range)
+  const int64_t n = dense_sym_ntri(s);
+  return (n + P - 1) / P;
+}
+size_t dense_sym_panel_partial_doubles(int64_t s, int P, int num_sms) {
+  const int64_t nt = dense_sym_panel_slot(s, P);
+  const int S = sym_split(s, sym_slots(num_sms), nt);
+  return S > 1 ? (size_t)(nt * (S - 1) * BM * BN) : 0;
+}
+
+// Step kstep of the symmetric recurrence on tiles [tile0, tile0 + ntile): W_k (or, at the last
+// step, H) of those tiles packed into gout (ntile x 64 x 64, row-major tiles).  W0..W2 / H as in
+// dense_cheb_sym, with W_{kstep-1} and W_{kstep-2} complete (unpacked) on entry.
+cudaError_t dense_cheb_sym_panel(int64_t s, const double* G, double* W0, double* W1, double* W2, double* H,
+                                 const SeriesParams* P, int K, int kstep, int64_t tile0, int64_t ntile,
+                                 double* gout, int* sync, double* partial, int num_sms, cudaStream_t st) {
+  if (s == 0 || K <= 2 || ntile <= 0) return cudaSuccess;
+  SymArgs a{};
+  a.s = s; a.G = G; a.W[0] = W0; a.W[1] = W1; a.W[2] = W2; a.H = H; a.P = P; a.K = K;
+  a.T = (int)((s + BM - 1) / BM);
+  const int slots = sym_slots(num_sms);
+  a.split = sym_split(s, slots, ntile);
+  a.sync = sync;
+  a.partial = partial;
+  a.vec = aligned16(G, s) && aligned16(W0, s) && aligned16(W1, s) && aligned16(W2, s);
+  a.panel = 1;
+  a.kstep = kstep;
+  a.tile0 = (int)tile0;
+  a.ntile = (int)ntile;
+  a.gout = gout;
+  cudaError_t e = cudaMemsetAsync(sync, 0, dense_sym_sync_ints(s, K, num_sms) * sizeof(int), st);
+  if (e != cudaSuccess) return e;
+  return sym_launch(a, ntile * a.split, slots, num_sms, st);
+}
+
+// Gathered slots -> full symmetric matrix: tile t (global column-major lower order) of owner p
+// sits at g + (p * slot + t - tile0(p)) * 4096; element (r, c), r >= c, lands at (r, c) and
+// (c, r).  One CTA per tile, the mirror written through a shared-memory transpose (coalesced).
+__global__ void __launch_bounds__(256) k_sym_unpack(const double* __restrict__ g, int64_t s, int T, int P,
+                                                    int64_t ntri, int64_t slot, double* __restrict__ out) {
+  __shared__ double tile_s[BM][BN + 1];
+  const int64_t t = blockIdx.x;
+  int p = (int)(t * P / ntri);
+  while (p + 1 < P && (ntri * (p + 1)) / P <= t) ++p;
+  while (p > 0 && (ntri * p) / P > t) --p;
+  const int64_t lt = t - (ntri * p) / P;
+  const double* src = g + ((int64_t)p * slot + lt) * (BM * BN);
+  int ti, tj;
+  tri_decode_colmajor((int)t, T, ti, tj);
+  const int64_t m0 = (int64_t)ti * BM, n0 = (int64_t)tj * BN;
+  for (int e = threadIdx.x; e < BM * BN; e += blockDim.x) {
+    const int r = e / BN, c = e % BN;
+    const double v = __ldcs(src + e);
+    tile_s[r][c] = v;
+    const int64_t rr = m0 + r, cc = n0 + c;
+    if (rr < s && cc < s && (ti != tj || r >= c)) out[rr * s + cc] = v;
+  }
+  __syncthreads();
+  // mirror: out[(n0 + c) * s + m0 + r] = tile(r, c), rows of the transposed tile contiguous
+  for (int e = threadIdx.x; e < BM * BN; e += blockDim.x) {
+    const int c = e / BM, r = e % BM;
+    const int64_t rr = m0 + r, cc = n0 + c;
+    if (rr < s && cc < s && (ti != tj || r > c)) out[cc * s + rr] = tile_s[r][c];
+  }
+}
+
+cudaError_t dense_sym_unpack(const double* gbuf, int64_t s, int P, double* out, cudaStream_t st) {
+  const int64_t ntri = dense_sym_ntri(s);
+  if (ntri == 0) return cudaSuccess;
+  k_sym_unpack<<<(unsigned)ntri, 256, 0, st>>>(gbuf, s, (int)((s + BM - 1) / BM), P, ntri,
+                                              dense_sym_panel_slot(s, P), out);
+  return cudaGetLastError();
 }
 
 // ---- NEXT-2: one-level Haar DWT of the Gram index (reading R22)

@@ -80,3 +80,12 @@ def apply_sharded(h, X_local, m_global: int, n_global: int, kernel, K: int, **kw
     of the series parameters."""
     return h.apply(X_local, kernel, K, **shard_args(m_global, n_global, getattr(h, "has_comm", h.world > 1)),
                    **kw)
+
+
+def panel_ranges(s: int, world: int) -> list[tuple[int, int]]:
+    """Tile ranges of the multi-GPU s x s recurrence (the library's partition, dense_f64.cu
+    dense_sym_panel_tile0): the T(T+1)/2 lower 64 x 64 tiles of an s x s matrix in column-major
+    order, T = ceil(s / 64), split in `world` contiguous ranges [ntri p / P, ntri (p+1) / P)."""
+    T = (s + 63) // 64
+    ntri = T * (T + 1) // 2
+    return [(ntri * p // world, ntri * (p + 1) // world) for p in range(world)]

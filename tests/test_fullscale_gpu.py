@@ -68,7 +68,9 @@ def test_c5_shape_block_diagonal_every_element(env, math_):
     for r0 in range(0, N, 2048):
         rows = torch.arange(r0, r0 + 2048, device="cuda")[:, None] // p
         cols = (torch.arange(N * copies, device="cuda")[None, :] % N) // p
-        want = torch.where(rows == cols, same, diff).to(torch.float64)
+        # (float64 scalars as tensors: torch.where with Python floats would build float32)
+        want = torch.where(rows == cols, torch.tensor(same, dtype=torch.float64, device="cuda"),
+                           torch.tensor(diff, dtype=torch.float64, device="cuda"))
         d = Y[r0:r0 + 2048].to(torch.float64) - want
         err2 += float((d * d).sum())
         ref2 += float((want * want).sum())

@@ -168,3 +168,53 @@ def test_batched_split_matches_single_process():
     Xb = W.gen_c3(batch=9, seed=4)
     Y, _ = O.cpa_shrink_batched(Xb, O.Kernel(**W.CONFIGS["c3"]["kernel"]), 8, T=20)
     assert np.array_equal(res[0], Y)
+
+
+def test_panel_partition_host_logic():
+    """Tile ranges of the multi-GPU s x s recurrence: contiguous, covering all T(T+1)/2 lower
+    tiles, balanced to one tile."""
+    D = _load_dist()
+    for s in (1, 64, 65, 1024, 16384):
+        T = (s + 63) // 64
+        ntri = T * (T + 1) // 2
+        for P_ in (1, 2, 3, 8):
+            r = D.panel_ranges(s, P_)
+            assert r[0][0] == 0 and r[-1][1] == ntri and all(a[1] == b[0] for a, b in zip(r, r[1:]))
+            sizes = [b - a for a, b in r]
+            assert max(sizes) - min(sizes) <= 1
+
+
+class _RecordingHandle:
+    """Stands in for the library Handle: records what dist.apply_sharded passes to cpa_svt_apply."""
+
+    def __init__(self, world, has_comm=True):
+        self.world, self.has_comm, self.calls = world, has_comm, []
+
+    def apply(self, X, kernel, K, **kw):
+        self.calls.append(kw)
+        return X
+
+
+def _sharded_args(rank, world):
+    D = _load_dist()
+    out = []
+    for (m, n) in ((64, 301), (301, 64)):
+        h = _RecordingHandle(world)
+        X = np.zeros((m, n))
+        D.apply_sharded(h, D.local_block(X, world, rank), m, n, {"kind": "soft"}, 5, T=3)
+        out.append((h.calls[0]["shard"], h.calls[0]["long_global"], D.local_block(X, world, rank).shape))
+    return out
+
+
+def test_apply_sharded_arguments_gloo():
+    """dist.apply_sharded passes the library the shard mode and the GLOBAL long extent on every
+    rank, each rank's block being its contiguous share of the long dimension."""
+    res = _run(_sharded_args)
+    for r in (0, 1):
+        (s1, l1, sh1), (s2, l2, sh2) = res[r]
+        assert (s1, l1) == ("cols", 301) and (s2, l2) == ("rows", 301)
+    assert res[0][0][2][1] + res[1][0][2][1] == 301 and res[0][1][2][0] + res[1][1][2][0] == 301
+    D = _load_dist()
+    h = _RecordingHandle(1, has_comm=False)
+    D.apply_sharded(h, np.zeros((4, 9)), 4, 9, {"kind": "soft"}, 5)
+    assert h.calls[0]["shard"] == "none"

@@ -21,19 +21,9 @@ import paper_1705_07112_b200 as P  # noqa: E402
 import workloads as W  # noqa: E402
 
 
-def h_soft(lam, tau):
-    r = torch.sqrt(torch.clamp(lam, min=0))
-    return torch.where(r > tau, (r - tau) / torch.where(r > 0, r, torch.ones_like(r)), torch.zeros_like(r))
-
-
 def exact_evd(X, tau):
-    m, n = X.shape
-    left = m <= n
-    G = X @ X.T if left else X.T @ X
-    lam, V = torch.linalg.eigh(G)
-    hv = h_soft(lam, tau)
-    Hm = (V * hv) @ V.T
-    return Hm @ X if left else X @ Hm
+    from paper_1705_07112_b200 import exact as E
+    return E.exact_shrink(X, {"kind": "soft"}, tau=tau)
 
 
 def timed(fn, reps):
