@@ -187,6 +187,12 @@ struct cpa_svt_handle {
   size_t hx_bytes = 0;
   std::string err;
   int64_t launches = 0;
+  // CPA_SVT_GUARD=1 (read at init; tests / debugging, compute-sanitizer being unavailable on
+  // the pool): every workspace allocation carries a guard band filled with kGuardByte from the
+  // end of what the current call uses, checked after every public call (E_CUDA on a change).
+  bool guard = false;
+  struct GuardBand { void** p; size_t from, to; };
+  std::vector<GuardBand> guards;
   bool use_flow = true;            // persistent dataflow recurrence (CPA_SVT_FLOW=0: one launch per step)
   int form = 0;                    // CPA_SVT_OPT_FORM
   // profiling (cpa_svt_profile): event pairs per phase, resolved at read time
@@ -263,7 +269,34 @@ void phase_hook(void* ctx, int ph, int begin) {
     }                                                                                \
   } while (0)
 
+constexpr size_t kGuardBytes = 1 << 16;
+constexpr unsigned char kGuardByte = 0xA5;
+
 static cpa_svt_status grow(cpa_svt_handle* h, void** p, size_t* have, size_t need) {
+  if (h->guard) {
+    // allocation = capacity + guard band; the band of this call starts at `need`
+    need = (need + 255) / 256 * 256;
+    if (need > *have) {
+      if (*p) {
+        cudaStreamSynchronize(h->stream);
+        cudaFree(*p);
+        *p = nullptr;
+        *have = 0;
+      }
+      if (cudaMalloc(p, need + kGuardBytes) != cudaSuccess) {
+        cudaGetLastError();
+        h->err = "workspace cudaMalloc (guarded)";
+        return CPA_SVT_E_NOMEM;
+      }
+      *have = need;
+    }
+    if (cudaMemsetAsync((char*)*p + need, kGuardByte, *have + kGuardBytes - need, h->stream) != cudaSuccess)
+      return CPA_SVT_E_CUDA;
+    for (auto& g : h->guards)
+      if (g.p == p) { g.from = need; g.to = *have + kGuardBytes; return CPA_SVT_OK; }
+    h->guards.push_back({p, need, *have + kGuardBytes});
+    return CPA_SVT_OK;
+  }
   if (need <= *have) return CPA_SVT_OK;
   if (*p) {
     cudaStreamSynchronize(h->stream);
@@ -350,6 +383,7 @@ cpa_svt_status cpa_svt_init(cpa_svt_handle** out, int device, void* cuda_stream,
   h->rank = rank;
   h->world = world;
   if (const char* f = getenv("CPA_SVT_FLOW")) h->use_flow = f[0] != '0';
+  h->guard = env_on("CPA_SVT_GUARD");
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (e == cudaSuccess) e = cudaMalloc(&h->P, sizeof(SeriesParams));
@@ -524,6 +558,25 @@ static cpa_svt_status read_verdict(cpa_svt_handle* h) {
     return CPA_SVT_E_DIVERGED;
   }
   return CPA_SVT_OK;
+}
+
+// CPA_SVT_GUARD: every guard band still holds kGuardByte (synchronises).
+static cpa_svt_status guard_check(cpa_svt_handle* h, cpa_svt_status st) {
+  if (!h->guard) return st;
+  CU(cudaStreamSynchronize(h->stream));
+  std::vector<unsigned char> buf;
+  for (auto& g : h->guards) {
+    if (!*g.p) continue;
+    buf.resize(g.to - g.from);
+    CU(cudaMemcpy(buf.data(), (char*)*g.p + g.from, buf.size(), cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < buf.size(); ++i)
+      if (buf[i] != kGuardByte) {
+        h->err = "workspace guard band overwritten at byte " + std::to_string(g.from + i) + " of a buffer whose call used " +
+                 std::to_string(g.from) + " bytes";
+        return CPA_SVT_E_CUDA;
+      }
+  }
+  return st;
 }
 
 // SPEC.md:215 divergence check of the output against the input (check.cu); the verdict is read
@@ -1151,11 +1204,12 @@ cpa_svt_status cpa_svt_apply(cpa_svt_handle* h, cpa_svt_dtype dtype, cpa_svt_mat
   cpa_svt_kernel kz{};
   if (!k) k = &kz;
   if (dtype == CPA_SVT_F64 && math == CPA_SVT_MATH_NATIVE)
-    return apply_f64(h, m, n, shard, long_global, (const double*)X, ldx, (double*)Y, ldy, k, K, c, lam, info);
+    return guard_check(h, apply_f64(h, m, n, shard, long_global, (const double*)X, ldx, (double*)Y, ldy, k, K, c,
+                                    lam, info));
   if (h->transform) return CPA_SVT_E_UNSUPPORTED;  // the transform variant is fp64-only
   if (dtype == CPA_SVT_F32 && (math == CPA_SVT_MATH_TF32 || math == CPA_SVT_MATH_3XTF32))
-    return apply_tf32(h, math == CPA_SVT_MATH_TF32 ? 1 : 3, m, n, shard, long_global, (const float*)X, ldx, (float*)Y,
-                      ldy, k, K, c, lam, info);
+    return guard_check(h, apply_tf32(h, math == CPA_SVT_MATH_TF32 ? 1 : 3, m, n, shard, long_global, (const float*)X,
+                                     ldx, (float*)Y, ldy, k, K, c, lam, info));
   return CPA_SVT_E_UNSUPPORTED;
 }
 
@@ -1219,14 +1273,14 @@ cpa_svt_status cpa_svt_apply_host(cpa_svt_handle* h, cpa_svt_dtype dtype, cpa_sv
     if (!delivered) CU(cudaMemcpyAsync(Y_host, dY, bytes, cudaMemcpyDeviceToHost, h->stream));
     CU(cudaStreamSynchronize(h->stream));
     CU(cudaStreamSynchronize(h->copy_stream));
-    return read_verdict(h);
+    return guard_check(h, read_verdict(h));
   }
   CU(cudaMemcpyAsync(dX, X_host, bytes, cudaMemcpyHostToDevice, h->stream));
   st = cpa_svt_apply(h, dtype, math, m, n, CPA_SVT_SHARD_NONE, 0, dX, n, dY, n, k, K, nullptr, lam, info);
   if (st != CPA_SVT_OK && st != CPA_SVT_E_DIVERGED) return st;
   CU(cudaMemcpyAsync(Y_host, dY, bytes, cudaMemcpyDeviceToHost, h->stream));
   CU(cudaStreamSynchronize(h->stream));
-  return read_verdict(h);
+  return guard_check(h, read_verdict(h));
 }
 
 // NEXT-3 (synthetic experiment PAPER.md:1095-1100): ADMM recovery of L from
@@ -1334,7 +1388,7 @@ cpa_svt_status cpa_svt_admm_recover(cpa_svt_handle* h, int64_t m, int64_t n, con
   opt->last_rel = rel;
   opt->ms_shrink = ms_shrink;
   opt->ms_total = mt;
-  return CPA_SVT_OK;
+  return guard_check(h, CPA_SVT_OK);
 }
 
 cpa_svt_status cpa_svt_apply_batched(cpa_svt_handle* h, int64_t batch, int m, int n, const float* X, float* Y,
@@ -1363,7 +1417,7 @@ cpa_svt_status cpa_svt_apply_batched(cpa_svt_handle* h, int64_t batch, int m, in
                            h->num_sms, h->stream, &launches, (double*)h->ws));
   }
   h->launches += launches;
-  return CPA_SVT_OK;
+  return guard_check(h, CPA_SVT_OK);
 }
 
 cpa_svt_status cpa_svt_apply_csr(cpa_svt_handle* h, int64_t m, int64_t n, int64_t nnz, const int64_t* row_ptr,
@@ -1400,7 +1454,7 @@ cpa_svt_status cpa_svt_apply_csr(cpa_svt_handle* h, int64_t m, int64_t n, int64_
     info->ms_total = info->ms_recurrence = tm.ms(0, 1);
     info->kernel_launches = launches;
   }
-  return st;
+  return guard_check(h, st);
 }
 
 }  // extern "C"

@@ -31,6 +31,7 @@
 // four halve the epilogue between two MMAs, which is exposed (tensor pipe idle) whenever
 // the other CTA on the SM is in its own epilogue.
 #include <cstdlib>
+#include <cstdio>
 
 #include <algorithm>
 
@@ -575,9 +576,24 @@ cudaError_t launch_batched_tc(int64_t batch, int m, int n, const float* X, float
   auto kern = nt == 128 ? btc::k_batched_tc<128> : btc::k_batched_tc<256>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, btc::SMEM);
   if (e != cudaSuccess) return e;
+  // all of the unified L1 / shared storage as shared memory: without this preference the occupancy
+  // query (and the launch) size residency for the default carveout -- one CTA per SM measured
+  // (c3 7.6 -> 18.9 ms)
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+  if (e != cudaSuccess) return e;
   int per_sm = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nt, btc::SMEM);
   if (e != cudaSuccess) return e;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int occ_api = per_sm;
+  per_sm = resident_ctas((const void*)kern, nt, btc::SMEM, dev);
+  if (env_on("CPA_SVT_DEBUG_OCC")) {
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, (const void*)kern);
+    fprintf(stderr, "k_batched_tc<%d>: occupancy API %d, resident %d CTAs/SM, regs %d, static smem %zu, dyn %d, max dyn %d, maxthreads %d\n",
+            nt, occ_api, per_sm, fa.numRegs, fa.sharedSizeBytes, btc::SMEM, fa.maxDynamicSharedSizeBytes, fa.maxThreadsPerBlock);
+  }
   // 3 x (49 KB smem, 256 thr x <= 80 regs, 128 TMEM columns) or 4 x (128 thr x <= 128 regs) fit one SM
   // (never more than `want`: each CTA holds its 128 TMEM columns for the whole persistent loop, so a
   // fifth CTA on an SM would block in tcgen05.alloc forever; fewer if registers / shared memory

@@ -6,6 +6,7 @@
 #include <stdint.h>
 #include <math.h>
 #include <stdlib.h>
+#include <stdio.h>
 
 #include "cpa_svt.h"
 
@@ -54,6 +55,51 @@ __host__ __device__ inline double resolve_tau(const cpa_svt_kernel& k, double si
 // Chebyshev-Gauss node l (1-based) of order K: theta_l = pi (l - 1/2) / K.
 __host__ __device__ inline double cheb_theta(int l, int K) {
   return 3.141592653589793238462643383279502884 * ((double)l - 0.5) / (double)K;
+}
+
+// ---- checked builds (build.py --variant checked CPA_SVT_CHECKED=1): device-side bounds checks
+// on the gathers / scatters whose indices come from data (CSR / CSC, tile decodes, all-gather
+// slots); a failed check prints the site and traps.  compute-sanitizer is not available on the
+// GPU pool, so this build plus the workspace guard bands (CPA_SVT_GUARD) stand in for memcheck.
+#ifdef CPA_SVT_CHECKED
+#define CPA_DCHECK(c)                                                                       \
+  do {                                                                                      \
+    if (!(c)) {                                                                             \
+      printf("CPA_DCHECK failed: %s (%s:%d) block %d thread %d\n", #c, __FILE__, __LINE__,  \
+             (int)blockIdx.x, (int)threadIdx.x);                                            \
+      __trap();                                                                             \
+    }                                                                                       \
+  } while (0)
+#else
+#define CPA_DCHECK(c) \
+  do {                \
+  } while (0)
+#endif
+
+// Resident CTAs per SM of a kernel from its attributes and the device limits (registers in
+// per-warp units of 8, shared memory with the 1 KB the system reserves per CTA, warps, CTA slots).
+// cudaOccupancyMaxActiveBlocksPerMultiprocessor reports 1 for the tcgen05 batched kernel and the
+// warp-specialized recurrence on this driver while 4 / 2 CTAs are measured resident (and run): the
+// persistent launches size their grids with this instead.
+inline int resident_ctas(const void* func, int threads, size_t dyn_smem, int device) {
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, func) != cudaSuccess) return 1;
+  int regs_sm = 65536, smem_sm = 233472, warps_sm = 64, blocks_sm = 32, reserved = 1024;
+  cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, device);
+  cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
+  cudaDeviceGetAttribute(&blocks_sm, cudaDevAttrMaxBlocksPerMultiprocessor, device);
+  cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, device);
+  int tpm = 2048;
+  cudaDeviceGetAttribute(&tpm, cudaDevAttrMaxThreadsPerMultiProcessor, device);
+  warps_sm = tpm / 32;
+  const int warps = (threads + 31) / 32;
+  const int regs_warp = ((fa.numRegs + 7) / 8) * 8 * 32;
+  int n = blocks_sm;
+  if (regs_warp > 0) n = n < regs_sm / (regs_warp * warps) ? n : regs_sm / (regs_warp * warps);
+  n = n < warps_sm / warps ? n : warps_sm / warps;
+  const size_t per = fa.sharedSizeBytes + dyn_smem + (size_t)reserved;
+  if (per > 0) n = n < (int)(smem_sm / per) ? n : (int)(smem_sm / per);
+  return n > 0 ? n : 1;
 }
 
 // ---- small PTX helpers --------------------------------------------------------

@@ -494,15 +494,25 @@ __device__ __forceinline__ void tri_decode_colmajor(int idx, int T, int& row, in
 // After the mainloop of unit (step k, tile (ti, tj), k-split q): split-K publish (q < S-1)
 // or reduce (q = S-1, all partials summed in the fixed order q = 0..S-1), then the fused
 // epilogue on the tile's r >= c elements and the release of its crosses.
-template <bool tma>
-__device__ __forceinline__ void sym_finish(const SymArgs& a, int k, int tile, int q, int ti, int tj,
-                                           double (&acc)[4][4][2]) {
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// WS: run by the 128 epilogue threads (warps 4-7) of k_cheb_sym_ws, thread u = threadIdx.x - 128
+// playing the role of MMA thread u (same fragment positions), synchronised on named barrier 2.
+template <bool tma, bool WS, class Acc>
+__device__ __forceinline__ void sym_finish_impl(const SymArgs& a, int k, int tile, int q, int ti, int tj, Acc&& acc) {
   const int T = a.T;
   const int S = a.split;
   int* cross = a.sync + 1;
   int* split_cnt = a.sync + 1 + a.K * T;
   const int64_t s = a.s;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int u = WS ? (int)threadIdx.x - NTHREADS : (int)threadIdx.x;
+  auto group_sync = [] {
+    if (WS) named_bar(2, NTHREADS);
+    else __syncthreads();
+  };
+  const int warp = u >> 5, lane = u & 31;
   const int g = lane >> 2, t = lane & 3;
   const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
   auto buf = [&](int i) { return i == 0 ? a.W[0] : (i == 1 ? a.W[1] : a.W[2]); };
@@ -513,6 +523,7 @@ __device__ __forceinline__ void sym_finish(const SymArgs& a, int k, int tile, in
   const int kc = a.panel ? 2 : k;         // split counters: per launch in panel mode (zeroed before it)
   if (S > 1) {
     double* slot = a.partial + (int64_t)(tile - (a.panel ? a.tile0 : 0)) * (S - 1) * (BM * BN);
+    CPA_DCHECK(tile - (a.panel ? a.tile0 : 0) >= 0 && tile < a.T * (a.T + 1) / 2);
     if (q < S - 1) {
       double* mine = slot + (int64_t)q * (BM * BN);
 #pragma unroll
@@ -520,29 +531,51 @@ __device__ __forceinline__ void sym_finish(const SymArgs& a, int k, int tile, in
 #pragma unroll
         for (int j = 0; j < 4; ++j)
 #pragma unroll
-          for (int e = 0; e < 2; ++e) __stcg(mine + ((i * 4 + j) * 2 + e) * NTHREADS + threadIdx.x, acc[i][j][e]);
-      __syncthreads();
-      if (threadIdx.x == 0) red_release_add_i32(split_cnt + tile, 1);
+          for (int e = 0; e < 2; ++e) __stcg(mine + ((i * 4 + j) * 2 + e) * NTHREADS + u, acc(i, j, e));
+      group_sync();
+      if (u == 0) red_release_add_i32(split_cnt + tile, 1);
       return;
     }
-    if (threadIdx.x == 0) wait_geq(split_cnt + tile, (S - 1) * (kc - 1));
-    __syncthreads();
-    double sum[32];
+    if (u == 0) wait_geq(split_cnt + tile, (S - 1) * (kc - 1));
+    group_sync();
+    if (!WS) {
+      double sum[32];
 #pragma unroll
-    for (int rr = 0; rr < 32; ++rr) sum[rr] = __ldcg(slot + rr * NTHREADS + threadIdx.x);
-    for (int p = 1; p < S - 1; ++p) {
-      double v[32];
+      for (int rr = 0; rr < 32; ++rr) sum[rr] = __ldcg(slot + rr * NTHREADS + u);
+      for (int p = 1; p < S - 1; ++p) {
+        double v[32];
 #pragma unroll
-      for (int rr = 0; rr < 32; ++rr) v[rr] = __ldcg(slot + (int64_t)p * (BM * BN) + rr * NTHREADS + threadIdx.x);
+        for (int rr = 0; rr < 32; ++rr) v[rr] = __ldcg(slot + (int64_t)p * (BM * BN) + rr * NTHREADS + u);
 #pragma unroll
-      for (int rr = 0; rr < 32; ++rr) sum[rr] += v[rr];
+        for (int rr = 0; rr < 32; ++rr) sum[rr] += v[rr];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) acc(i, j, e) = sum[(i * 4 + j) * 2 + e] + acc(i, j, e);
+    } else {
+      // the same sums in the same order, eight elements at a time (register budget of the 2-CTA kernel)
+#pragma unroll
+      for (int c8 = 0; c8 < 4; ++c8) {
+        double sum[8];
+#pragma unroll
+        for (int x = 0; x < 8; ++x) sum[x] = __ldcg(slot + (c8 * 8 + x) * NTHREADS + u);
+        for (int p = 1; p < S - 1; ++p) {
+          double v[8];
+#pragma unroll
+          for (int x = 0; x < 8; ++x) v[x] = __ldcg(slot + (int64_t)p * (BM * BN) + (c8 * 8 + x) * NTHREADS + u);
+#pragma unroll
+          for (int x = 0; x < 8; ++x) sum[x] += v[x];
+        }
+#pragma unroll
+        for (int x = 0; x < 8; ++x) {
+          const int rr = c8 * 8 + x;
+          acc(rr >> 3, (rr >> 1) & 3, rr & 1) = sum[x] + acc(rr >> 3, (rr >> 1) & 3, rr & 1);
+        }
+      }
     }
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) acc[i][j][e] = sum[(i * 4 + j) * 2 + e] + acc[i][j][e];
   }
   // fused epilogue on the elements r >= c of the tile
   const double s4 = 2.0 * a.P->scale2, ck = a.P->c[k];
@@ -569,9 +602,10 @@ __device__ __forceinline__ void sym_finish(const SymArgs& a, int k, int tile, in
         const int64_t c = n0 + wn + j * 8 + 2 * t + e;
         if (!(rr < s && c <= rr)) continue;
         const int qq = j * 2 + e;
-        const double wv = s4 * acc[i][j][e] - 2.0 * vp[qq] - vpp[qq];  // W_k = 2 B_hat W_{k-1} - W_{k-2}
+        const double wv = s4 * acc(i, j, e) - 2.0 * vp[qq] - vpp[qq];  // W_k = 2 B_hat W_{k-1} - W_{k-2}
         const double y = vy[qq] + ck * wv;                               // H += c_k W_k
         if (a.panel) {   // packed slot of the all-gather: W_k, or H at the last step
+          CPA_DCHECK(tile >= a.tile0 && tile < a.tile0 + a.ntile);
           a.gout[(int64_t)(tile - a.tile0) * (BM * BN) + (rr - m0) * BN + (c - n0)] = last ? y : wv;
           if (!last) a.H[rr * s + c] = y;
           continue;
@@ -585,15 +619,22 @@ __device__ __forceinline__ void sym_finish(const SymArgs& a, int k, int tile, in
       }
   }
   if (a.panel) {   // (the launch boundary orders the stores; no crosses to release)
-    __syncthreads();
+    group_sync();
     return;
   }
   if (tma) fence_proxy_async_global();   // W_k / H stores -> later TMA (async-proxy) reads
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  group_sync();
+  if (u == 0) {
     red_release_add_i32(cross + k * T + ti, 1);
     if (ti != tj) red_release_add_i32(cross + k * T + tj, 1);
   }
+}
+
+// k_cheb_sym / k_cheb_sym_tma: the accumulators in registers
+template <bool tma>
+__device__ __forceinline__ void sym_finish(const SymArgs& a, int k, int tile, int q, int ti, int tj,
+                                           double (&acc)[4][4][2]) {
+  sym_finish_impl<tma, false>(a, k, tile, q, ti, tj, [&](int i, int j, int e) -> double& { return acc[i][j][e]; });
 }
 
 __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB) k_cheb_sym(SymArgs a) {
@@ -618,6 +659,7 @@ __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB) k_cheb_sym(SymArgs a)
     const int tile = r / S + (a.panel ? a.tile0 : 0);
     int ti, tj;
     tri_decode_colmajor(tile, T, ti, tj);
+    CPA_DCHECK(ti >= 0 && ti < T && tj >= 0 && tj <= ti);
     auto buf = [&](int i) { return i == 0 ? a.W[0] : (i == 1 ? a.W[1] : a.W[2]); };
     const double* src = buf((k - 1) % 3);   // W_{k-1}
     const int64_t m0 = (int64_t)ti * BM, n0 = (int64_t)tj * BN;
@@ -708,6 +750,7 @@ __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB)
     const int tile = r / S + (a.panel ? a.tile0 : 0);
     int ti, tj;
     tri_decode_colmajor(tile, T, ti, tj);
+    CPA_DCHECK(ti >= 0 && ti < T && tj >= 0 && tj <= ti);
     const CUtensorMap* wmap = &mp.w[(k - 1) % 3];   // W_{k-1}
     const int m0 = ti * BM, n0 = tj * BN;
     const int kb = (int)((int64_t)nk * q / S), ke = (int)((int64_t)nk * (q + 1) / S);
@@ -788,6 +831,195 @@ __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB)
   }
 }
 
+// Warp-specialized variant of k_cheb_sym_tma (CPA_SVT_SYM_WS): the same units,
+// dependencies, ring and fragment loads, but the four MMA warps (warp 0 lane 0: tickets + TMA) hand
+// each unit's accumulators to four EPILOGUE warps through a double-buffered 32 KB shared-memory
+// staging area (fragment layout, the layout of the split-K slots) and go straight on to the next
+// unit; the epilogue warps run the split-K publish / fixed-order reduction and the fused update
+// (sym_finish<.., WS>) concurrently.  So the DMMA pipe does not idle through the reducer's L2 round
+// trips and the epilogue.  mbarriers: sfull[b] (4 MMA-warp arrivals: unit in staging b),
+// sempty[b] (4 epilogue-warp arrivals: staging b read); meta[b] carries the unit; k < 0 ends.
+struct WsMeta {
+  int k, tile, q, ti, tj;
+};
+
+template <int SBK, int SSTAGES>
+__global__ void __launch_bounds__(2 * NTHREADS, 2)
+    k_cheb_sym_ws(const __grid_constant__ SymMaps mp, SymArgs a) {
+  constexpr int SBOX_BYTES = 16 * SBK * 8;
+  constexpr int SSTAGE_BYTES = 8 * SBOX_BYTES;
+  // all shared state in the dynamic allocation (no static shared memory: two CTAs fill the SM's
+  // 228 KB exactly): mbarriers / ticket / unit records in the first 128 bytes, then the 1024-byte
+  // aligned ring (128-byte swizzle) and the two staging buffers
+  extern __shared__ __align__(16) unsigned char tsm_raw[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(tsm_raw);
+  uint64_t* empty = full + SSTAGES;
+  uint64_t* sfull = empty + SSTAGES;
+  uint64_t* sempty = sfull + 2;
+  int& s_ticket = *reinterpret_cast<int*>(sempty + 2);
+  WsMeta* meta = reinterpret_cast<WsMeta*>(sempty + 4);
+  const uint32_t raw = smem_u32(tsm_raw);
+  unsigned char* base = tsm_raw + (((raw + 128u + 1023u) & ~1023u) - raw);
+  double* stage = reinterpret_cast<double*>(base + SSTAGES * SSTAGE_BYTES);   // 2 x 64 x 64 doubles
+  {
+    uint32_t dyn;
+    asm volatile("mov.u32 %0, %%dynamic_smem_size;\n" : "=r"(dyn));
+    if ((uint32_t)(base - tsm_raw) + SSTAGES * SSTAGE_BYTES + 2 * BM * BN * 8 > dyn) __trap();   // layout check
+  }
+  const int T = a.T;
+  const int ntri = T * (T + 1) / 2;
+  const int S = a.split;
+  const int per_step = (a.panel ? a.ntile : ntri) * S;
+  const int total = a.panel ? per_step : (a.K - 2) * per_step;
+  int* cross = a.sync + 1;
+  const int nk = (int)((a.s + SBK - 1) / SBK);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < SSTAGES; ++st) {
+      mbar_init(full + st, 1);
+      mbar_init(empty + st, 4);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(sfull + b, 4);
+      mbar_init(sempty + b, 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (warp >= 4) {
+    // ---------------- epilogue warps ----------------
+    const int u = threadIdx.x - NTHREADS;
+    for (int n = 0;; ++n) {
+      const int b = n & 1;
+      mbar_wait(sfull + b, (n >> 1) & 1);
+      const WsMeta mt = meta[b];
+      if (mt.k < 0) break;
+      // the accumulators stay in the staging buffer (read where used: the register budget of the
+      // 2-CTA kernel); the buffer is released after the unit
+      double* stg = stage + b * (BM * BN);
+      sym_finish_impl<true, true>(a, mt.k, mt.tile, mt.q, mt.ti, mt.tj, [&](int i, int j, int e) -> double& {
+        return stg[((i * 4 + j) * 2 + e) * NTHREADS + u];
+      });
+      __syncwarp();
+      if (lane == 0) mbar_arrive(sempty + b);   // staging b may be refilled
+    }
+    return;
+  }
+  // ---------------- MMA warps (thread 0: tickets and TMA producer) ----------------
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  uint32_t coff[2][2];
+#pragma unroll
+  for (int par = 0; par < 2; ++par)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) coff[par][h] = ((((h * 8 + g) >> 1) ^ (2 * t + par)) << 4) | ((g & 1) * 8);
+  const uint32_t roff = 256 * t;
+  const uint32_t boxa = (wm >> 4) * SBOX_BYTES, boxb = (4 + (wn >> 4)) * SBOX_BYTES;
+  uint32_t it = 0;    // slabs consumed by this CTA so far
+  int nunit = 0;      // units handed to the epilogue so far
+  for (;;) {
+    if (threadIdx.x == 0) s_ticket = atomicAdd(a.sync, 1);
+    named_bar(1, NTHREADS);
+    const int tk = s_ticket;
+    named_bar(1, NTHREADS);   // (s_ticket is rewritten by the next claim)
+    const int b = nunit & 1;
+    if (tk >= total) {
+      mbar_wait(sempty + b, ((nunit >> 1) & 1) ^ 1);
+      if (threadIdx.x == 0) meta[b].k = -1;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(sfull + b);
+      break;
+    }
+    const int k = a.panel ? a.kstep : 2 + tk / per_step;
+    const int r = tk % per_step;
+    const int q = r % S;
+    const int tile = r / S + (a.panel ? a.tile0 : 0);
+    int ti, tj;
+    tri_decode_colmajor(tile, T, ti, tj);
+    CPA_DCHECK(ti >= 0 && ti < T && tj >= 0 && tj <= ti);
+    const CUtensorMap* wmap = &mp.w[(k - 1) % 3];   // W_{k-1}
+    const int m0 = ti * BM, n0 = tj * BN;
+    const int kb = (int)((int64_t)nk * q / S), ke = (int)((int64_t)nk * (q + 1) / S);
+    const int nku = ke - kb;
+    if (threadIdx.x == 0) {
+      const int P = nku < SSTAGES - 1 ? nku : SSTAGES - 1;
+      for (int p = 0; p < P; ++p) {
+        const uint32_t sl = it + p, st = sl % SSTAGES;
+        mbar_wait(empty + st, ((sl / SSTAGES) & 1) ^ 1);
+        mbar_expect_tx(full + st, SSTAGE_BYTES);
+        for (int bb = 0; bb < 4; ++bb)
+          tma_load_2d(base + st * SSTAGE_BYTES + bb * SBOX_BYTES, &mp.g, m0 + 16 * bb, (kb + p) * SBK, full + st);
+      }
+      if (!a.panel) {
+        if (k >= 3) wait_geq(cross + (k - 1) * T + tj, T);
+        if (k >= 4) wait_geq(cross + (k - 2) * T + ti, T);
+      }
+      fence_proxy_async_global();
+      for (int p = 0; p < P; ++p) {
+        const uint32_t st = (it + p) % SSTAGES;
+        for (int bb = 0; bb < 4; ++bb)
+          tma_load_2d(base + st * SSTAGE_BYTES + (4 + bb) * SBOX_BYTES, wmap, n0 + 16 * bb, (kb + p) * SBK,
+                      full + st);
+      }
+    }
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int kt = 0; kt < nku; ++kt) {
+      if (threadIdx.x == 0 && kt + SSTAGES - 1 < nku) {
+        const int kn = kt + SSTAGES - 1;
+        const uint32_t sl = it + kn, st = sl % SSTAGES;
+        mbar_wait(empty + st, ((sl / SSTAGES) & 1) ^ 1);
+        mbar_expect_tx(full + st, SSTAGE_BYTES);
+        unsigned char* d = base + st * SSTAGE_BYTES;
+        for (int bb = 0; bb < 4; ++bb) tma_load_2d(d + bb * SBOX_BYTES, &mp.g, m0 + 16 * bb, (kb + kn) * SBK, full + st);
+        for (int bb = 0; bb < 4; ++bb)
+          tma_load_2d(d + (4 + bb) * SBOX_BYTES, wmap, n0 + 16 * bb, (kb + kn) * SBK, full + st);
+      }
+      __syncwarp();
+      const uint32_t sl = it + kt, st = sl % SSTAGES;
+      mbar_wait(full + st, (sl / SSTAGES) & 1);
+      const unsigned char* sa = base + st * SSTAGE_BYTES + boxa;
+      const unsigned char* sb = base + st * SSTAGE_BYTES + boxb;
+#pragma unroll
+      for (int kk = 0; kk < SBK / 4; ++kk) {
+        const int par = kk & 1;
+        const uint32_t ro = 1024 * (kk >> 1) + 128 * par + roff;
+        double fa[4], fb[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          fa[i] = *reinterpret_cast<const double*>(sa + (i >> 1) * SBOX_BYTES + ro + coff[par][i & 1]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          fb[j] = *reinterpret_cast<const double*>(sb + (j >> 1) * SBOX_BYTES + ro + coff[par][j & 1]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], fa[i], fb[j]);
+      }
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + st);
+    }
+    it += nku;
+    // hand the accumulators to the epilogue warps
+    mbar_wait(sempty + b, ((nunit >> 1) & 1) ^ 1);
+    double* stg = stage + b * (BM * BN);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) stg[((i * 4 + j) * 2 + e) * NTHREADS + threadIdx.x] = acc[i][j][e];
+    if (threadIdx.x == 0) meta[b] = WsMeta{k, tile, q, ti, tj};
+    __syncwarp();
+    if (lane == 0) mbar_arrive(sfull + b);
+    ++nunit;
+  }
+}
+
 // Cluster variant of k_cheb_sym for small s (c2): the CS k-splits of a tile run as one
 // thread-block cluster and reduce through distributed shared memory instead of L2 partial
 // buffers and a single reducer.  Each CTA stores its partial accumulators in its own shared
@@ -826,6 +1058,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(NTHREADS, CPA_FLOW_
     const int tile = tk % ntri;
     int ti, tj;
     tri_decode_colmajor(tile, T, ti, tj);
+    CPA_DCHECK(ti >= 0 && ti < T && tj >= 0 && tj <= ti);
     auto buf = [&](int i) { return i == 0 ? a.W[0] : (i == 1 ? a.W[1] : a.W[2]); };
     const double* src = buf((k - 1) % 3);   // W_{k-1}
     const double* wpp = buf((k - 2) % 3);   // W_{k-2} (k = 2: identity, implicit)
@@ -1493,6 +1726,29 @@ static cudaError_t sym_launch(SymArgs& a, int64_t total, int slots, int num_sms,
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
     }
+    if (ok && env_on("CPA_SVT_SYM_WS")) {
+      // warp-specialized kernel: 3 x 16-deep (48 KB) or 2 x 32-deep (64 KB) ring + 64 KB staging, 2 CTAs per SM
+      const size_t wsmem = (sbk == 32 ? (size_t)2 * 8 * (16 * 32 * 8) : (size_t)3 * 8 * (16 * 16 * 8)) +
+                           (size_t)2 * BM * BN * 8 + 1024;   // (+ header and alignment: see k_cheb_sym_ws)
+      auto kf = sbk == 32 ? k_cheb_sym_ws<32, 2> : k_cheb_sym_ws<16, 3>;
+      e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem);
+      if (e != cudaSuccess) return e;
+      e = cudaFuncSetAttribute(kf, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+      if (e != cudaSuccess) return e;
+      int dev = 0;
+      cudaGetDevice(&dev);
+      int per_sm = resident_ctas((const void*)kf, 2 * NTHREADS, wsmem, dev);
+      if (env_on("CPA_SVT_DEBUG_OCC")) {
+        cudaFuncAttributes fa;
+        cudaFuncGetAttributes(&fa, (const void*)kf);
+        fprintf(stderr, "k_cheb_sym_ws: occupancy %d CTAs/SM, regs %d, static smem %zu, dyn %zu\n", per_sm, fa.numRegs,
+                fa.sharedSizeBytes, wsmem);
+      }
+      int64_t tgrid = (int64_t)num_sms * per_sm;
+      if (tgrid > total) tgrid = total;
+      void* targs[] = {&mp, &a};
+      return cudaLaunchCooperativeKernel((void*)kf, dim3((unsigned)tgrid), dim3(2 * NTHREADS), targs, wsmem, st);
+    }
     if (ok) {
       // both instances use a 64 KB ring: 4 x 16-deep or 2 x 32-deep stages
       const size_t tsmem = (size_t)4 * 8 * (16 * 16 * 8) + 1024;
@@ -1566,6 +1822,7 @@ __global__ void __launch_bounds__(256) k_sym_unpack(const double* __restrict__ g
   while (p + 1 < P && (ntri * (p + 1)) / P <= t) ++p;
   while (p > 0 && (ntri * p) / P > t) --p;
   const int64_t lt = t - (ntri * p) / P;
+  CPA_DCHECK(p >= 0 && p < P && lt >= 0 && lt < slot && (ntri * p) / P <= t && t < (ntri * (p + 1)) / P);
   const double* src = g + ((int64_t)p * slot + lt) * (BM * BN);
   int ti, tj;
   tri_decode_colmajor((int)t, T, ti, tj);

@@ -40,11 +40,13 @@ __global__ void k_col_count(const int32_t* col, int64_t nnz, int* cnt) {
     atomicAdd(cnt + col[e], 1);
 }
 __global__ void k_col_fill(const int64_t* row_ptr, const int32_t* col, const double* val, int64_t m,
-                           const int64_t* cptr, int* cursor, int32_t* crow, double* cval) {
+                           const int64_t* cptr, int* cursor, int32_t* crow, double* cval, int64_t n_cols) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
     for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
       const int c = col[e];
+      CPA_DCHECK(c >= 0 && c < n_cols);
       const int64_t p = cptr[c] + atomicAdd(cursor + c, 1);
+      CPA_DCHECK(p < cptr[c + 1]);
       crow[p] = (int32_t)i;
       cval[p] = val[e];
     }
@@ -139,26 +141,53 @@ __global__ void k_densify(const int64_t* row_ptr, const int32_t* col, const doub
   }
 }
 
-// Z[b][j][:] = sum_{l in row j of X} x_jl W[b][l][:]    (one warp per (block b, j))
+// Row split points of the CSR for the column passes of k_spmm_wxt: rs[j * (NP + 1) + h] = first
+// entry of row j with column >= n h / NP (columns are sorted within a row).
+__global__ void k_row_split(const int64_t* row_ptr, const int32_t* col, int64_t m, int64_t n, int NP, int64_t* rs) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e0 = row_ptr[j], e1 = row_ptr[j + 1];
+    rs[j * (NP + 1)] = e0;
+    for (int h = 1; h < NP; ++h) {
+      const int64_t cb = n * h / NP;
+      int64_t lo = e0, hi = e1;   // first e in [e0, e1) with col[e] >= cb
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (col[mid] < cb) lo = mid + 1; else hi = mid;
+      }
+      rs[j * (NP + 1) + h] = lo;
+    }
+    rs[j * (NP + 1) + NP] = e1;
+  }
+}
+
+// Z[b][j][:] (+)= sum_{l in row j of X, l in column pass h} x_jl W[b][l][:]   (one warp per (b, j)).
+// The NP column passes run as NP launches in order (pass 0 writes, the others add: a fixed order),
+// so the L2 footprint of a block is its W slice (32 x n / NP doubles) plus the matching CSR slice
+// instead of the whole 51 MB block row (DRAM re-reads of W measured 3.5x with one pass).
 __global__ void __launch_bounds__(SP_WARPS * 32) k_spmm_wxt(const int64_t* row_ptr, const int32_t* col,
                                                             const double* val, int64_t m, int64_t n, int64_t nblk,
-                                                            const double* __restrict__ W, double* __restrict__ Z) {
+                                                            const double* __restrict__ W, double* __restrict__ Z,
+                                                            const int64_t* __restrict__ rs, int NP, int h) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t item = blockIdx.x * (int64_t)SP_WARPS + warp;  // block-major: item = b * m + j
   if (item >= nblk * m) return;
   const int64_t b = item / m, j = item % m;
   const double* Wb = W + b * n * RB + lane;
-  const int64_t e0 = row_ptr[j], e1 = row_ptr[j + 1];
+  const int64_t e0 = NP > 1 ? rs[j * (NP + 1) + h] : row_ptr[j];
+  const int64_t e1 = NP > 1 ? rs[j * (NP + 1) + h + 1] : row_ptr[j + 1];
   double s0 = 0.0, s1 = 0.0;
   int64_t e = e0;
   for (; e + 1 < e1; e += 2) {
     const int32_t c0 = __ldg(col + e), c1 = __ldg(col + e + 1);
     const double x0 = __ldg(val + e), x1 = __ldg(val + e + 1);
+    CPA_DCHECK(c0 >= 0 && c0 < n && c1 >= 0 && c1 < n);
     s0 = fma(x0, Wb[(int64_t)c0 * RB], s0);
     s1 = fma(x1, Wb[(int64_t)c1 * RB], s1);
   }
   if (e < e1) s0 = fma(__ldg(val + e), Wb[(int64_t)__ldg(col + e) * RB], s0);
-  Z[(b * m + j) * RB + lane] = s0 + s1;
+  double* zp = Z + (b * m + j) * RB + lane;
+  if (h == 0) *zp = s0 + s1;
+  else *zp += s0 + s1;
 }
 
 // W_k[b][l][:] = s * sum_{j in col l} x_jl Z[b][j][:] - ... (fused epilogue), one warp per (b, l)
@@ -178,6 +207,7 @@ __global__ void __launch_bounds__(SP_WARPS * 32) k_spmm_zx(const int64_t* cptr, 
   int64_t e = e0;
   for (; e + 1 < e1; e += 2) {
     const int32_t r0 = __ldg(crow + e), r1 = __ldg(crow + e + 1);
+    CPA_DCHECK(r0 >= 0 && r0 < m && r1 >= 0 && r1 < m);
     s0 = fma(__ldg(cval + e), Zb[(int64_t)r0 * RB], s0);
     s1 = fma(__ldg(cval + e + 1), Zb[(int64_t)r1 * RB], s1);
   }
@@ -245,6 +275,10 @@ cudaError_t sparse_apply(int64_t m, int64_t n, int64_t nnz, const int64_t* row_p
   const size_t o_Wb = off;   off += al(blkW * sizeof(double));
   const size_t o_Y = off;    off += al(blkW * sizeof(double));
   const size_t o_Z = off;    off += al(blkZ * sizeof(double));
+  // column passes of Z = W X^T: W slices of <= ~26 MB per 32-row block (CPA_SVT_SP_PASSES overrides)
+  int NP = (int)std::max<int64_t>(1, (n * RB * 8 + (26 << 20) - 1) / (26 << 20));
+  if (const char* v = getenv("CPA_SVT_SP_PASSES")) NP = std::max(1, atoi(v));
+  const size_t o_rs = off;   off += al((size_t)m * (NP + 1) * sizeof(int64_t));
   *ws_needed = off;
   if (!ws || ws_bytes < off) return cudaSuccess;  // size query
   char* base = (char*)ws;
@@ -261,6 +295,7 @@ cudaError_t sparse_apply(int64_t m, int64_t n, int64_t nnz, const int64_t* row_p
   double* Wb = (double*)(base + o_Wb);
   double* Yb = (double*)(base + o_Y);
   double* Z = (double*)(base + o_Z);
+  int64_t* rs = (int64_t*)(base + o_rs);
   int L = 0;
   cudaError_t e;
   const int g = 4 * num_sms;
@@ -275,7 +310,7 @@ cudaError_t sparse_apply(int64_t m, int64_t n, int64_t nnz, const int64_t* row_p
   SPCK(cub::DeviceScan::ExclusiveSum(base + o_scan, scan_bytes, cptr, cnt64, (int)(n + 1), st)); ++L;
   SPCK(cudaMemcpyAsync(cptr, cnt64, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
   SPCK(cudaMemsetAsync(cnt, 0, (n + 1) * sizeof(int), st));
-  k_col_fill<<<g, 256, 0, st>>>(row_ptr, col, val, m, cptr, cnt, crow, cval); ++L;
+  k_col_fill<<<g, 256, 0, st>>>(row_ptr, col, val, m, cptr, cnt, crow, cval, n); ++L;
   k_col_sort<<<g, 256, 0, st>>>(cptr, n, crow, cval); ++L;
   if (hook) hook(hook_ctx, CPA_SVT_PH_GRAM, 0);
   // ---- Lambda_max (m-side power iteration) and coefficients
@@ -307,9 +342,16 @@ cudaError_t sparse_apply(int64_t m, int64_t n, int64_t nnz, const int64_t* row_p
     const unsigned gw = (unsigned)((itemsW + SP_WARPS - 1) / SP_WARPS);
     const double* prev = W0;   // W_{k-1}
     const double* prev2 = nullptr;
+    if (NP > 1) {
+      k_row_split<<<g, 256, 0, st>>>(row_ptr, col, m, n, NP, rs);
+      ++L;
+    }
     for (int k = 1; k < K; ++k) {
       if (hook) hook(hook_ctx, CPA_SVT_PH_SPARSE_Z, 1);
-      k_spmm_wxt<<<gz, SP_WARPS * 32, 0, st>>>(row_ptr, col, val, m, n, nblk, prev, Z); ++L;
+      for (int hp = 0; hp < NP; ++hp) {
+        k_spmm_wxt<<<gz, SP_WARPS * 32, 0, st>>>(row_ptr, col, val, m, n, nblk, prev, Z, rs, NP, hp);
+        ++L;
+      }
       if (hook) hook(hook_ctx, CPA_SVT_PH_SPARSE_Z, 0);
       if (hook) hook(hook_ctx, CPA_SVT_PH_SPARSE_W, 1);
       double* out;

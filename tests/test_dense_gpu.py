@@ -339,3 +339,31 @@ def test_max_order(env, shape):
     Yo, io = O.cpa_shrink(X, O.Kernel(**kern), 512, T=60, return_info=True)
     assert abs(info["lambda_hat"] - io["lambda_hat"]) <= 1e-12 * io["lambda_hat"]
     assert O.rel_fro(Y, Yo) <= TOL64
+
+
+@pytest.mark.parametrize("s,L,K,split", [(1024, 1024, 30, 0), (1024, 1100, 12, 1), (1024, 1024, 9, 3), (256, 300, 5, 2),
+                                         (130, 300, 7, 0), (64, 200, 3, 0), (4096, 4200, 5, 0), (1538, 1600, 6, 5)])
+def test_warp_specialized_recurrence_bitwise(env, s, L, K, split):
+    """k_cheb_sym_ws (MMA warps hand the accumulators to epilogue warps through shared memory)
+    performs the same sums in the same order as k_cheb_sym_tma: bitwise-equal outputs, and the
+    oracle bar."""
+    import os
+    torch, P, _ = env
+    X = W.gen_c2(m=s, n=L, seed=s + K)
+    kern = {"kind": "soft", "tau": 0.05, "tau_relative": True}
+    Xd = torch.from_numpy(X).cuda()
+    out = {}
+    if split:
+        os.environ["CPA_SVT_FLOW_SPLIT"] = str(split)
+    try:
+        for ws in ("0", "1"):
+            os.environ["CPA_SVT_SYM_WS"] = ws
+            h2 = P.Handle(0)
+            out[ws] = h2.apply(Xd, kern, K, T=100).cpu().numpy()
+            h2.close()
+    finally:
+        os.environ.pop("CPA_SVT_SYM_WS", None)
+        os.environ.pop("CPA_SVT_FLOW_SPLIT", None)
+    assert np.array_equal(out["0"], out["1"])
+    if s <= 1100:
+        assert O.rel_fro(out["1"], O.cpa_shrink(X, O.Kernel(**kern), K, T=100)) <= TOL64
