@@ -150,7 +150,7 @@ def cpu_baseline(cfg, budget_s=10.0):
 def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
-        return 0
+        return None
     X = cfg["oracle_X"]()
     F = cfg["oracle_F"]
     for _ in range(args.warmup):
@@ -167,8 +167,7 @@ def run_reference(args, cfg):
             "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": blas_threads(), "kind": "oracle",
                              "sample": cfg["oracle_sample"]},
             "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
-    return 0
+    return line
 
 
 METRIC = "CPA shrinkage GFLOP/s & % of FP64/HBM roofline; ms per SVT at 1/2/4/8 GPUs"
@@ -394,12 +393,33 @@ def run_ours(args, cfg):
         line["nccl"] = {"comm_nranks": nr, "comm_rank": rk, "comm_nranks_ok": nr == world and rk == rank}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, args.cpu_budget)
-    if rank == 0:
-        print(json.dumps(line), flush=True)
     h.close()
     if world > 1:
         dist.destroy_process_group()
-    return 0
+    return line if rank == 0 else None
+
+
+class _StdoutToStderr:
+    """Route fd 1 to stderr while the benchmark runs (NCCL and CUDA libraries print to the C-level
+    stdout, e.g. "NCCL version ..."), so the only thing on stdout is the JSON line."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+        return self
+
+    def __exit__(self, *exc):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
+        return False
+
+
+def emit(line: dict):
+    """The one JSON line on the real stdout."""
+    sys.stdout.flush()
+    os.write(1, (json.dumps(line) + "\n").encode())
 
 
 def main():
@@ -417,9 +437,14 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     name = args.config or ("c2" if world == 1 and args.gpus <= 1 else "c5")
     cfg = make_cfg(name, world, args.math)
-    if args.impl == "reference":
-        return run_reference(args, cfg)
-    return run_ours(args, cfg)
+    with _StdoutToStderr():
+        if args.impl == "reference":
+            line = run_reference(args, cfg)
+        else:
+            line = run_ours(args, cfg)
+    if line is not None:
+        emit(line)
+    return 0
 
 
 if __name__ == "__main__":

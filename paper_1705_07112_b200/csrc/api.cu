@@ -87,6 +87,13 @@ cudaError_t launch_diag_scale(const double* G, int64_t s, double* scale, cudaStr
 cudaError_t launch_power_dense(const double* G, const double* G4, int pw, int64_t s, int T, double* scratch,
                                unsigned int* bar, SeriesParams* P, const cpa_svt_kernel& k, int K, double safety,
                                const double* c_given, int num_sms, cudaStream_t st);
+int64_t power_rows_slot(int64_t s, int P);
+size_t power_rows_scratch_doubles(int64_t s, int P, int num_sms);
+cudaError_t launch_power_rows(const double* G, int64_t s, int t, int v, int P, double* scratch, int num_sms,
+                              cudaStream_t st);
+double* power_rows_buffer(double* scratch, int64_t s, int t, int P);
+cudaError_t launch_power_rows_final(double* scratch, int64_t s, int T, int P, int num_sms, double** lam_hat,
+                                    cudaStream_t st);
 cudaError_t launch_power_dense_f32(const float* G, int64_t s, int64_t ld, int T, double* scratch, unsigned int* bar,
                                    SeriesParams* P, const cpa_svt_kernel& k, int K, double safety,
                                    const double* c_given, int num_sms, cudaStream_t st);
@@ -104,6 +111,15 @@ cudaError_t tf32_prep(const float* X, int64_t m, int64_t n, int64_t ldx, bool tr
 cudaError_t tf32_finish(const float* Yi, int64_t ldi, int64_t m, int64_t n, bool transpose, float* Y, int64_t ldy,
                         int num_sms, cudaStream_t st);
 cudaError_t tf32_eye(float* I, int64_t s, int64_t ld, int num_sms, cudaStream_t st);
+cudaError_t tf32_panel_list(int64_t s, int terms, const int2** list, int* count, int* bn);
+cudaError_t tc_gemm_panel(int terms, int s, const float* Ah, const float* Al, int64_t lda, const float* Bh,
+                          const float* Bl, int64_t ldb, bool last, int64_t ld_out, const float* wp, const float* wpp,
+                          int64_t ld_w, float* y, int64_t ld_y, const SeriesParams* P, int k, int64_t tile0,
+                          int64_t ntile, float* gout, int num_sms, cudaStream_t st);
+cudaError_t tf32_sym_unpack(const float* gbuf, int64_t s, int terms, int P, int64_t slot_tiles, int64_t ld, float* Wf,
+                            float* Wh, float* Wl, float* H, cudaStream_t st);
+cudaError_t launch_power_rows_f32(const float* G, int64_t s, int64_t ld, int t, int v, int P, double* scratch,
+                                  int num_sms, cudaStream_t st);
 // batched_f32.cu
 cudaError_t launch_batched_f32(int64_t batch, int m, int n, const float* X, float* Y, const cpa_svt_kernel& k,
                                int K, int T, double safety, double lam_override, float* lambda_out,
@@ -784,6 +800,8 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
                       ((sharded && (h->world > 1 || env_on("CPA_SVT_PANELS"))) || (panel_sim > 1 && h->world == 1));
   const int panel_P = panels ? (panel_sim > 1 && h->world == 1 ? panel_sim : h->world) : 1;
   const size_t nGb = panels ? (size_t)panel_P * (size_t)dense_sym_panel_slot(s, panel_P) * 4096 : 0;
+  // the panel form also shards the power iteration by rows of G (one all-gather of u per product)
+  const size_t nPR = panels ? (size_t)((power_rows_scratch_doubles(s, panel_P, h->num_sms) + 31) / 32 * 32) : 0;
   if (h->hp_X && (sharded || dct || !poly)) {   // (the host pipeline covers the plain s x s form only)
     CU(cudaMemcpyAsync((double*)X, h->hp_X, (size_t)m * n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
     h->hp_X = nullptr;
@@ -802,7 +820,7 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
                                      final_split && poly ? dense_store_partial_doubles(m, n) : (size_t)0}));
   const size_t nSync = std::max({dense_flow_sync_ints(RM, RN, K), (size_t)((s / 64 + 2) * (s / 64 + 2)),
                                  dense_sym_sync_ints(s, K, h->num_sms), (size_t)1332});
-  const size_t need = (nG + 2 * nW + nX + nPow + nPart + nGb) * sizeof(double) + nSync * sizeof(int) + 256;
+  const size_t need = (nG + 2 * nW + nX + nPow + nPart + nGb + nPR) * sizeof(double) + nSync * sizeof(int) + 256;
   cpa_svt_status st = grow(h, &h->ws, &h->ws_bytes, need);
   if (st != CPA_SVT_OK) return st;
   double* G = (double*)h->ws;
@@ -813,7 +831,8 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
   double* pw = Wb + nW + nX;
   double* part = pw + nPow;
   double* gbuf = part + nPart;    // panel mode: P all-gather slots of packed 64 x 64 tiles
-  int* flow_sync = (int*)(gbuf + nGb);
+  double* prs = gbuf + nGb;       // panel mode: row-sharded power iteration scratch
+  int* flow_sync = (int*)(prs + nPR);
 
   const double* c_dev = nullptr;
   if (c) {
@@ -892,6 +911,28 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
   if (lam->lambda_max > 0.0) {
     Phase p(h, CPA_SVT_PH_POWER);
     CU(launch_series(h->P, *k, K, lam->safety, lam->lambda_max, nullptr, c_dev, h->stream));
+  } else if (panels) {
+    // row-sharded power iteration: rank p computes rows [s p / P, s (p+1) / P) of every product and
+    // the products' slots are all-gathered (in place); virtual ranks one after another in the
+    // simulation.  Same products as the replicated iteration (reading R6), another summation order.
+    Phase p(h, CPA_SVT_PH_POWER);
+    const int64_t pslot = power_rows_slot(s, panel_P);
+    CU(cudaMemsetAsync(prs + 2 * panel_P * pslot + h->num_sms, 0, 2 * sizeof(double), h->stream));
+    for (int t = 1; t <= lam->power_iters; ++t) {
+      const int v0 = panel_sim > 1 ? 0 : h->rank, v1 = panel_sim > 1 ? panel_P : h->rank + 1;
+      for (int v = v0; v < v1; ++v) {
+        CU(launch_power_rows(G, s, t, v, panel_P, prs, h->num_sms, h->stream));
+        ++launches;
+      }
+      if (panel_sim <= 1) {
+        double* gb = power_rows_buffer(prs, s, t, panel_P);
+        NC(g_nccl.AllGather(gb + (size_t)h->rank * pslot, gb, (size_t)pslot, ncclDouble, h->comm, h->stream));
+      }
+    }
+    double* lam_dev = nullptr;
+    CU(launch_power_rows_final(prs, s, lam->power_iters, panel_P, h->num_sms, &lam_dev, h->stream));
+    CU(launch_series(h->P, *k, K, lam->safety, 0.0, lam_dev, c_dev, h->stream));
+    launches += 2;
   } else {
     Phase p(h, CPA_SVT_PH_POWER);
     // Repeated squaring: v_{T-1} ~ G^{T-1} v_0 is reached with (T-1)/p products by
@@ -1063,11 +1104,23 @@ static cpa_svt_status apply_tf32(cpa_svt_handle* h, int terms, int64_t m, int64_
   const int64_t sp = (s + 3) / 4 * 4, Lp = (L + 3) / 4 * 4;
   // s x s form on full tiles (2(K-2) s^3 + 2 s^2 L) when it beats apply-to-X ((K-1) 2 s^2 L)
   const bool poly = K > 2 && h->form != 1;  // symmetric s x s form: fewer flops for any K > 2
+  // multi-GPU s x s form by tile panels (as apply_f64): CPA_SVT_PANELS / CPA_SVT_PANEL_SIM for tests
+  int panel_sim = 0;
+  if (const char* v = getenv("CPA_SVT_PANEL_SIM")) panel_sim = atoi(v);
+  const bool panels = poly && ((sharded && (h->world > 1 || env_on("CPA_SVT_PANELS"))) || (panel_sim > 1 && h->world == 1));
+  const int panel_P = panels ? (panel_sim > 1 && h->world == 1 ? panel_sim : h->world) : 1;
+  const int2* plist = nullptr;
+  int pcount = 0, pbn = 0;
+  if (panels && tf32_panel_list(s, terms, &plist, &pcount, &pbn) != cudaSuccess) return CPA_SVT_E_NOMEM;
+  const int64_t pslot_tiles = panels ? (pcount + panel_P - 1) / panel_P : 0;
   auto al = [](size_t b) { return (b + 255) / 256 * 256; };
   const size_t nA = al((size_t)s * Lp * 4), nG = al((size_t)s * sp * 4);
   const size_t nPow = al(power_dense_scratch_doubles(s) * 8);
+  const size_t nGb = panels ? al((size_t)panel_P * pslot_tiles * 128 * pbn * 4) : 0;
+  const size_t nPR = panels ? al(power_rows_scratch_doubles(s, panel_P, h->num_sms) * 8) : 0;
   // X set (full, hi, lo) | Y_int | G (full, hi, lo) | apply: A set (3 x s*Lp)  poly: I set, B set, H (3 x s*sp each)
-  const size_t need = 4 * nA + 3 * nG + (poly ? 9 * nG : 3 * nA) + nPow + 256;
+  // | power scratch | panel mode: all-gather slots, row-sharded power scratch
+  const size_t need = 4 * nA + 3 * nG + (poly ? 9 * nG : 3 * nA) + nPow + nGb + nPR + 256;
   cpa_svt_status st = grow(h, &h->ws, &h->ws_bytes, need);
   if (st != CPA_SVT_OK) return st;
   char* b = (char*)h->ws;
@@ -1092,6 +1145,8 @@ static cpa_svt_status apply_tf32(cpa_svt_handle* h, int terms, int64_t m, int64_
     }
     pw = (double*)(rest + 9 * nG);
   }
+  float* gbufF = (float*)((char*)pw + nPow);
+  double* prs = (double*)((char*)gbufF + nGb);
   const double* c_dev = nullptr;
   if (c) {
     CU(cudaMemcpyAsync(h->d_c, c, K * sizeof(double), cudaMemcpyHostToDevice, h->stream));
@@ -1121,6 +1176,24 @@ static cpa_svt_status apply_tf32(cpa_svt_handle* h, int terms, int64_t m, int64_
   if (lam->lambda_max > 0.0) {
     Phase p(h, CPA_SVT_PH_POWER);
     CU(launch_series(h->P, *k, K, lam->safety, lam->lambda_max, nullptr, c_dev, h->stream));
+  } else if (panels) {   // row-sharded power iteration (as apply_f64)
+    Phase p(h, CPA_SVT_PH_POWER);
+    const int64_t pslot = power_rows_slot(s, panel_P);
+    CU(cudaMemsetAsync(prs + 2 * panel_P * pslot + h->num_sms, 0, 2 * sizeof(double), h->stream));
+    for (int t = 1; t <= lam->power_iters; ++t) {
+      const int v0 = panel_sim > 1 ? 0 : h->rank, v1 = panel_sim > 1 ? panel_P : h->rank + 1;
+      for (int v = v0; v < v1; ++v) {
+        CU(launch_power_rows_f32(Gf, s, sp, t, v, panel_P, prs, h->num_sms, h->stream));
+        ++launches;
+      }
+      if (panel_sim <= 1) {
+        double* gb = power_rows_buffer(prs, s, t, panel_P);
+        NC(g_nccl.AllGather(gb + (size_t)h->rank * pslot, gb, (size_t)pslot, ncclDouble, h->comm, h->stream));
+      }
+    }
+    double* lam_dev = nullptr;
+    CU(launch_power_rows_final(prs, s, lam->power_iters, panel_P, h->num_sms, &lam_dev, h->stream));
+    CU(launch_series(h->P, *k, K, lam->safety, 0.0, lam_dev, c_dev, h->stream));
   } else {
     Phase p(h, CPA_SVT_PH_POWER);
     CU(launch_power_dense_f32(Gf, s, sp, lam->power_iters, pw, h->bar, h->P, *k, K, lam->safety, c_dev, h->num_sms,
@@ -1147,7 +1220,29 @@ static cpa_svt_status apply_tf32(cpa_svt_handle* h, int terms, int64_t m, int64_
     }
     launches += 2;
   }
-  for (int kk = poly ? 2 : 1; kk < K; ++kk) {
+  for (int kk = poly ? 2 : 1; kk < K && panels; ++kk) {
+    // multi-GPU: this rank's 1/P of the step's lower tiles, packed; in-place all-gather; unpack the
+    // full W_k (fp32 lower + TF32 hi / lo copies of both triangles), or H after the last step
+    float** src = sets[(kk - 1) & 1];
+    float** out = sets[kk & 1];
+    const bool last = kk == K - 1;
+    const size_t slotF = (size_t)pslot_tiles * 128 * pbn;
+    const int v0 = panel_sim > 1 ? 0 : h->rank, v1 = panel_sim > 1 ? panel_P : h->rank + 1;
+    for (int v = v0; v < v1; ++v) {
+      const int64_t t0 = (int64_t)pcount * v / panel_P, t1 = (int64_t)pcount * (v + 1) / panel_P;
+      Phase ps(h, CPA_SVT_PH_STEP);
+      CU(tc_gemm_panel(terms, (int)s, Gh, Gl, sp, src[1], src[2], ldr, last, ldr, src[0], out[0], ldr, Yr, ldr, h->P,
+                       kk, t0, t1 - t0, gbufF + (size_t)v * slotF, h->num_sms, h->stream));
+      ++launches;
+    }
+    Phase px(h, CPA_SVT_PH_EXCHANGE);
+    if (panel_sim <= 1)
+      NC(g_nccl.AllGather(gbufF + (size_t)h->rank * slotF, gbufF, slotF, ncclFloat, h->comm, h->stream));
+    CU(tf32_sym_unpack(gbufF, s, terms, panel_P, pslot_tiles, ldr, out[0], out[1], out[2], last ? Yr : nullptr,
+                       h->stream));
+    ++launches;
+  }
+  for (int kk = poly ? 2 : 1; kk < K && !panels; ++kk) {
     float** src = sets[(kk - 1) & 1];      // W_{k-1}: k=1 -> W_0
     float** out = sets[kk & 1];            // W_k overwrites W_{k-2} (k >= 2)
     const bool last = kk == K - 1;

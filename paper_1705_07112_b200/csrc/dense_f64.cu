@@ -500,7 +500,7 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
 
 // WS: run by the 128 epilogue threads (warps 4-7) of k_cheb_sym_ws, thread u = threadIdx.x - 128
 // playing the role of MMA thread u (same fragment positions), synchronised on named barrier 2.
-template <bool tma, bool WS, class Acc>
+template <bool tma, bool WS, bool PANEL, class Acc>
 __device__ __forceinline__ void sym_finish_impl(const SymArgs& a, int k, int tile, int q, int ti, int tj, Acc&& acc) {
   const int T = a.T;
   const int S = a.split;
@@ -520,10 +520,10 @@ __device__ __forceinline__ void sym_finish_impl(const SymArgs& a, int k, int til
   const double* wpp = buf((k - 2) % 3);   // W_{k-2} (k = 2: identity, implicit)
   double* out = buf(k % 3);               // W_k over W_{k-3}
   const int64_t m0 = (int64_t)ti * BM, n0 = (int64_t)tj * BN;
-  const int kc = a.panel ? 2 : k;         // split counters: per launch in panel mode (zeroed before it)
+  const int kc = PANEL ? 2 : k;         // split counters: per launch in panel mode (zeroed before it)
   if (S > 1) {
-    double* slot = a.partial + (int64_t)(tile - (a.panel ? a.tile0 : 0)) * (S - 1) * (BM * BN);
-    CPA_DCHECK(tile - (a.panel ? a.tile0 : 0) >= 0 && tile < a.T * (a.T + 1) / 2);
+    double* slot = a.partial + (int64_t)(tile - (PANEL ? a.tile0 : 0)) * (S - 1) * (BM * BN);
+    CPA_DCHECK(tile - (PANEL ? a.tile0 : 0) >= 0 && tile < a.T * (a.T + 1) / 2);
     if (q < S - 1) {
       double* mine = slot + (int64_t)q * (BM * BN);
 #pragma unroll
@@ -604,7 +604,7 @@ __device__ __forceinline__ void sym_finish_impl(const SymArgs& a, int k, int til
         const int qq = j * 2 + e;
         const double wv = s4 * acc(i, j, e) - 2.0 * vp[qq] - vpp[qq];  // W_k = 2 B_hat W_{k-1} - W_{k-2}
         const double y = vy[qq] + ck * wv;                               // H += c_k W_k
-        if (a.panel) {   // packed slot of the all-gather: W_k, or H at the last step
+        if (PANEL) {   // packed slot of the all-gather: W_k, or H at the last step
           CPA_DCHECK(tile >= a.tile0 && tile < a.tile0 + a.ntile);
           a.gout[(int64_t)(tile - a.tile0) * (BM * BN) + (rr - m0) * BN + (c - n0)] = last ? y : wv;
           if (!last) a.H[rr * s + c] = y;
@@ -618,7 +618,7 @@ __device__ __forceinline__ void sym_finish_impl(const SymArgs& a, int k, int til
         if (last) a.H[c * s + rr] = y;
       }
   }
-  if (a.panel) {   // (the launch boundary orders the stores; no crosses to release)
+  if (PANEL) {   // (the launch boundary orders the stores; no crosses to release)
     group_sync();
     return;
   }
@@ -631,20 +631,22 @@ __device__ __forceinline__ void sym_finish_impl(const SymArgs& a, int k, int til
 }
 
 // k_cheb_sym / k_cheb_sym_tma: the accumulators in registers
-template <bool tma>
+template <bool tma, bool PANEL>
 __device__ __forceinline__ void sym_finish(const SymArgs& a, int k, int tile, int q, int ti, int tj,
                                            double (&acc)[4][4][2]) {
-  sym_finish_impl<tma, false>(a, k, tile, q, ti, tj, [&](int i, int j, int e) -> double& { return acc[i][j][e]; });
+  sym_finish_impl<tma, false, PANEL>(a, k, tile, q, ti, tj,
+                                     [&](int i, int j, int e) -> double& { return acc[i][j][e]; });
 }
 
+template <bool PANEL>
 __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB) k_cheb_sym(SymArgs a) {
   extern __shared__ __align__(16) double smem[];
   __shared__ int s_ticket;
   const int T = a.T;
   const int ntri = T * (T + 1) / 2;
   const int S = a.split;
-  const int per_step = (a.panel ? a.ntile : ntri) * S;
-  const int total = a.panel ? per_step : (a.K - 2) * per_step;
+  const int per_step = (PANEL ? a.ntile : ntri) * S;
+  const int total = PANEL ? per_step : (a.K - 2) * per_step;
   int* cross = a.sync + 1;
   const int64_t s = a.s;
   const int nk = (int)((s + BKS - 1) / BKS);
@@ -653,10 +655,10 @@ __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB) k_cheb_sym(SymArgs a)
     __syncthreads();
     const int tk = s_ticket;
     if (tk >= total) break;
-    const int k = a.panel ? a.kstep : 2 + tk / per_step;
+    const int k = PANEL ? a.kstep : 2 + tk / per_step;
     const int r = tk % per_step;
     const int q = r % S;
-    const int tile = r / S + (a.panel ? a.tile0 : 0);
+    const int tile = r / S + (PANEL ? a.tile0 : 0);
     int ti, tj;
     tri_decode_colmajor(tile, T, ti, tj);
     CPA_DCHECK(ti >= 0 && ti < T && tj >= 0 && tj <= ti);
@@ -667,14 +669,14 @@ __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB) k_cheb_sym(SymArgs a)
     double acc[4][4][2];
     mainloop_dep(a.G, src, s, m0, n0, a.vec, smem, acc, kb, ke, [&] {
 #ifndef CPA_SYM_NOWAIT  // (timing experiment only: wrong results without the waits)
-      if (threadIdx.x == 0 && !a.panel) {
+      if (threadIdx.x == 0 && !PANEL) {
         if (k >= 3) wait_geq(cross + (k - 1) * T + tj, T);
         if (k >= 4) wait_geq(cross + (k - 2) * T + ti, T);
       }
 #endif
       __syncthreads();
     });
-    sym_finish<false>(a, k, tile, q, ti, tj, acc);
+    sym_finish<false, PANEL>(a, k, tile, q, ti, tj, acc);
   }
 }
 
@@ -701,7 +703,7 @@ struct SymMaps {
 // SBK-deep slabs in an SSTAGES ring: <16, 4> (64 KB) for short units (c2: ~11 slabs each),
 // <32, 2> (64 KB, half the mbarrier round trips) for long ones (s >= 4096: c5 shape 608 ->
 // 586 ms; at c2 it costs 1.27 -> 1.39 ms).
-template <int SBK, int SSTAGES>
+template <int SBK, int SSTAGES, bool PANEL>
 __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB)
     k_cheb_sym_tma(const __grid_constant__ SymMaps mp, SymArgs a) {
   constexpr int SBOX_BYTES = 16 * SBK * 8;
@@ -715,8 +717,8 @@ __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB)
   const int T = a.T;
   const int ntri = T * (T + 1) / 2;
   const int S = a.split;
-  const int per_step = (a.panel ? a.ntile : ntri) * S;
-  const int total = a.panel ? per_step : (a.K - 2) * per_step;
+  const int per_step = (PANEL ? a.ntile : ntri) * S;
+  const int total = PANEL ? per_step : (a.K - 2) * per_step;
   int* cross = a.sync + 1;
   const int nk = (int)((a.s + SBK - 1) / SBK);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -744,10 +746,10 @@ __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB)
     __syncthreads();
     const int tk = s_ticket;
     if (tk >= total) break;
-    const int k = a.panel ? a.kstep : 2 + tk / per_step;
+    const int k = PANEL ? a.kstep : 2 + tk / per_step;
     const int r = tk % per_step;
     const int q = r % S;
-    const int tile = r / S + (a.panel ? a.tile0 : 0);
+    const int tile = r / S + (PANEL ? a.tile0 : 0);
     int ti, tj;
     tri_decode_colmajor(tile, T, ti, tj);
     CPA_DCHECK(ti >= 0 && ti < T && tj >= 0 && tj <= ti);
@@ -765,7 +767,7 @@ __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB)
         for (int b = 0; b < 4; ++b)
           tma_load_2d(base + st * SSTAGE_BYTES + b * SBOX_BYTES, &mp.g, m0 + 16 * b, (kb + p) * SBK, full + st);
       }
-      if (!a.panel) {
+      if (!PANEL) {
         if (k >= 3) wait_geq(cross + (k - 1) * T + tj, T);
         if (k >= 4) wait_geq(cross + (k - 2) * T + ti, T);
       }
@@ -827,7 +829,7 @@ __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB)
       if (lane == 0) mbar_arrive(empty + st);
     }
     it += nku;
-    sym_finish<true>(a, k, tile, q, ti, tj, acc);
+    sym_finish<true, PANEL>(a, k, tile, q, ti, tj, acc);
   }
 }
 
@@ -869,8 +871,8 @@ __global__ void __launch_bounds__(2 * NTHREADS, 2)
   const int T = a.T;
   const int ntri = T * (T + 1) / 2;
   const int S = a.split;
-  const int per_step = (a.panel ? a.ntile : ntri) * S;
-  const int total = a.panel ? per_step : (a.K - 2) * per_step;
+  const int per_step = (false ? a.ntile : ntri) * S;
+  const int total = false ? per_step : (a.K - 2) * per_step;
   int* cross = a.sync + 1;
   const int nk = (int)((a.s + SBK - 1) / SBK);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -897,7 +899,7 @@ __global__ void __launch_bounds__(2 * NTHREADS, 2)
       // the accumulators stay in the staging buffer (read where used: the register budget of the
       // 2-CTA kernel); the buffer is released after the unit
       double* stg = stage + b * (BM * BN);
-      sym_finish_impl<true, true>(a, mt.k, mt.tile, mt.q, mt.ti, mt.tj, [&](int i, int j, int e) -> double& {
+      sym_finish_impl<true, true, false>(a, mt.k, mt.tile, mt.q, mt.ti, mt.tj, [&](int i, int j, int e) -> double& {
         return stg[((i * 4 + j) * 2 + e) * NTHREADS + u];
       });
       __syncwarp();
@@ -930,10 +932,10 @@ __global__ void __launch_bounds__(2 * NTHREADS, 2)
       if (lane == 0) mbar_arrive(sfull + b);
       break;
     }
-    const int k = a.panel ? a.kstep : 2 + tk / per_step;
+    const int k = false ? a.kstep : 2 + tk / per_step;
     const int r = tk % per_step;
     const int q = r % S;
-    const int tile = r / S + (a.panel ? a.tile0 : 0);
+    const int tile = r / S + (false ? a.tile0 : 0);
     int ti, tj;
     tri_decode_colmajor(tile, T, ti, tj);
     CPA_DCHECK(ti >= 0 && ti < T && tj >= 0 && tj <= ti);
@@ -950,7 +952,7 @@ __global__ void __launch_bounds__(2 * NTHREADS, 2)
         for (int bb = 0; bb < 4; ++bb)
           tma_load_2d(base + st * SSTAGE_BYTES + bb * SBOX_BYTES, &mp.g, m0 + 16 * bb, (kb + p) * SBK, full + st);
       }
-      if (!a.panel) {
+      if (!false) {
         if (k >= 3) wait_geq(cross + (k - 1) * T + tj, T);
         if (k >= 4) wait_geq(cross + (k - 2) * T + ti, T);
       }
@@ -1623,8 +1625,9 @@ static size_t sym_smem() { return (size_t)STAGES * (OpLayout<false, BM>::SIZE + 
 
 static int sym_slots(int num_sms) {
   int per_sm = 0;
-  cudaFuncSetAttribute(k_cheb_sym, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sym_smem());
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cheb_sym, NTHREADS, sym_smem()) != cudaSuccess ||
+  cudaFuncSetAttribute(k_cheb_sym<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sym_smem());
+  cudaFuncSetAttribute(k_cheb_sym<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sym_smem());
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cheb_sym<false>, NTHREADS, sym_smem()) != cudaSuccess ||
       per_sm < 1)
     per_sm = 1;
   return num_sms * per_sm;
@@ -1726,7 +1729,7 @@ static cudaError_t sym_launch(SymArgs& a, int64_t total, int slots, int num_sms,
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
     }
-    if (ok && env_on("CPA_SVT_SYM_WS")) {
+    if (ok && env_on("CPA_SVT_SYM_WS") && !a.panel) {
       // warp-specialized kernel: 3 x 16-deep (48 KB) or 2 x 32-deep (64 KB) ring + 64 KB staging, 2 CTAs per SM
       const size_t wsmem = (sbk == 32 ? (size_t)2 * 8 * (16 * 32 * 8) : (size_t)3 * 8 * (16 * 16 * 8)) +
                            (size_t)2 * BM * BN * 8 + 1024;   // (+ header and alignment: see k_cheb_sym_ws)
@@ -1752,7 +1755,8 @@ static cudaError_t sym_launch(SymArgs& a, int64_t total, int slots, int num_sms,
     if (ok) {
       // both instances use a 64 KB ring: 4 x 16-deep or 2 x 32-deep stages
       const size_t tsmem = (size_t)4 * 8 * (16 * 16 * 8) + 1024;
-      auto kf = sbk == 32 ? k_cheb_sym_tma<32, 2> : k_cheb_sym_tma<16, 4>;
+      auto kf = a.panel ? (sbk == 32 ? k_cheb_sym_tma<32, 2, true> : k_cheb_sym_tma<16, 4, true>)
+                        : (sbk == 32 ? k_cheb_sym_tma<32, 2, false> : k_cheb_sym_tma<16, 4, false>);
       e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
       if (e != cudaSuccess) return e;
       int per_sm = 0;
@@ -1765,7 +1769,8 @@ static cudaError_t sym_launch(SymArgs& a, int64_t total, int slots, int num_sms,
     }
   }
   void* args[] = {&a};
-  return cudaLaunchCooperativeKernel((void*)k_cheb_sym, dim3((unsigned)grid), dim3(NTHREADS), args, smem, st);
+  return cudaLaunchCooperativeKernel(a.panel ? (void*)k_cheb_sym<true> : (void*)k_cheb_sym<false>, dim3((unsigned)grid),
+                                     dim3(NTHREADS), args, smem, st);
 }
 
 // ---- panel mode (multi-GPU): one step on a contiguous range of lower tiles ------------

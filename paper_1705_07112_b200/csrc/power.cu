@@ -448,3 +448,149 @@ cudaError_t launch_power_dense_f32(const float* G, int64_t s, int64_t ld, int T,
 }
 
 }  // namespace cpa
+
+namespace cpa {
+// ---------------------------------------------------------------------------------------------
+// Row-sharded power iteration (multi-GPU s x s path, Alg. 1 line 3; reading R6).
+// Rank p owns rows [s p / P, s (p+1) / P) of G.  Product t computes its rows of
+// u_t = G u_{t-1} / ||u_{t-1}|| (u_0 := sqrt(s) v_0, i.e. v_0 = 1/sqrt(s) (1, ..., 1)), writes them and
+// the sum of their squares (last entry) into its slot of an all-gather buffer; after the
+// all-gather every rank holds all of u_t and ||u_t||^2 = the slots' sums added in rank order.
+// lambda_hat = ||u_T|| (= ||G v_{T-1}||).  Two gather buffers alternate (a product reads the
+// previous one).  Deterministic for a fixed P: every sum runs in a fixed order.
+constexpr int kPRThreads = 1024;
+
+__device__ __forceinline__ double pr_norm2(const double* g, int P, int64_t slot) {
+  double n2 = 0.0;
+  for (int p = 0; p < P; ++p) n2 += __ldcg(g + (int64_t)p * slot + slot - 1);
+  return n2;
+}
+
+template <typename E>
+__global__ void __launch_bounds__(kPRThreads, 1) k_power_rows(const E* __restrict__ G, int64_t s, int64_t ld, int P,
+                                                              int64_t slot, const double* __restrict__ gin,
+                                                              int64_t r0, int64_t r1, double* __restrict__ gout,
+                                                              double* __restrict__ bpart, unsigned int* counter) {
+  extern __shared__ double u_s[];   // u_{t-1} (s doubles)
+  __shared__ double red[kPRThreads / 32];
+  __shared__ double s_inv;
+  __shared__ bool last;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    if (gin) {
+      const double n = sqrt(pr_norm2(gin, P, slot));
+      s_inv = n > kDegenerateLambda ? 1.0 / n : 0.0;   // a zero Gram stays zero: lambda_hat = 0 (R17)
+    } else {
+      s_inv = 1.0;
+    }
+  }
+  if (gin) {
+    for (int64_t i = threadIdx.x; i < s; i += blockDim.x) {
+      int p = (int)(i * P / s);
+      while (p + 1 < P && s * (p + 1) / P <= i) ++p;
+      while (p > 0 && s * p / P > i) --p;
+      u_s[i] = __ldcg(gin + (int64_t)p * slot + (i - s * p / P));
+    }
+  } else {
+    const double v0 = 1.0 / sqrt((double)s);
+    for (int64_t i = threadIdx.x; i < s; i += blockDim.x) u_s[i] = v0;
+  }
+  __syncthreads();
+  const double inv = s_inv;
+  double sq = 0.0;   // lane 0: squares of this warp's rows, in row order
+  for (int64_t row = r0 + (int64_t)blockIdx.x * (kPRThreads / 32) + warp; row < r1;
+       row += (int64_t)gridDim.x * (kPRThreads / 32)) {
+    const E* g = G + row * ld;
+    double a0 = 0.0, a1 = 0.0;
+    int64_t c = 2 * lane;
+    if (sizeof(E) == 8 && ((uintptr_t)g & 15) == 0) {
+      for (; c + 1 < s; c += 64) {
+        const double2 v = __ldcs(reinterpret_cast<const double2*>(g + c));
+        a0 = fma(v.x, u_s[c], a0);
+        a1 = fma(v.y, u_s[c + 1], a1);
+      }
+      if (c < s) a0 = fma((double)__ldcs(g + c), u_s[c], a0);
+    } else {
+      for (c = lane; c < s; c += 32) a0 = fma((double)__ldcs(g + c), u_s[c], a0);
+    }
+    double d = a0 + a1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+    const double val = d * inv;
+    if (lane == 0) {
+      gout[row - r0] = val;
+      sq = fma(val, val, sq);
+    }
+  }
+  if (lane == 0) red[warp] = sq;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = 0.0;
+    for (int w = 0; w < kPRThreads / 32; ++w) b += red[w];
+    bpart[blockIdx.x] = b;
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    double tot = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) tot += __ldcg(bpart + b);
+    gout[slot - 1] = tot;   // this slot's sum of squares
+    *counter = 0u;
+  }
+}
+
+__global__ void k_power_rows_final(const double* g, int P, int64_t slot, double* lam_hat) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) *lam_hat = sqrt(pr_norm2(g, P, slot));
+}
+
+int64_t power_rows_slot(int64_t s, int P) { return (s + P - 1) / P + 1; }
+size_t power_rows_scratch_doubles(int64_t s, int P, int num_sms) {
+  return (size_t)(2 * P * power_rows_slot(s, P) + num_sms + 8);
+}
+
+// Product t (1-based) of the row-sharded power iteration for virtual rank v of P: reads the
+// gathered buffer of product t-1 (none at t = 1), writes rank v's slot of the buffer of product t.
+// scratch: [2 * P * slot gather buffers | num_sms block partials | counter | lambda_hat].
+template <typename E>
+static cudaError_t launch_power_rows_t(const E* G, int64_t s, int64_t ld, int t, int v, int P, double* scratch,
+                                       int num_sms, cudaStream_t st) {
+  const int64_t slot = power_rows_slot(s, P);
+  double* gb[2] = {scratch, scratch + P * slot};
+  double* bpart = scratch + 2 * P * slot;
+  unsigned int* counter = reinterpret_cast<unsigned int*>(bpart + num_sms);
+  const double* gin = t == 1 ? nullptr : gb[(t - 1) & 1];
+  double* gout = gb[t & 1] + (int64_t)v * slot;
+  const int64_t r0 = s * v / P, r1 = s * (v + 1) / P;
+  const size_t smem = (size_t)s * sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(k_power_rows<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int grid = num_sms;
+  const int64_t wneed = (r1 - r0 + 31) / 32;
+  if (grid > wneed) grid = (int)(wneed > 0 ? wneed : 1);
+  k_power_rows<E><<<grid, kPRThreads, smem, st>>>(G, s, ld, P, slot, gin, r0, r1, gout, bpart, counter);
+  return cudaGetLastError();
+}
+cudaError_t launch_power_rows(const double* G, int64_t s, int t, int v, int P, double* scratch, int num_sms,
+                              cudaStream_t st) {
+  return launch_power_rows_t<double>(G, s, s, t, v, P, scratch, num_sms, st);
+}
+// fp32 Gram (the TF32 path), row stride ld; the products still accumulate in fp64
+cudaError_t launch_power_rows_f32(const float* G, int64_t s, int64_t ld, int t, int v, int P, double* scratch,
+                                  int num_sms, cudaStream_t st) {
+  return launch_power_rows_t<float>(G, s, ld, t, v, P, scratch, num_sms, st);
+}
+// The buffer product t writes (for the all-gather) and the final lambda_hat slot.
+double* power_rows_buffer(double* scratch, int64_t s, int t, int P) {
+  return scratch + (int64_t)(t & 1) * P * power_rows_slot(s, P);
+}
+cudaError_t launch_power_rows_final(double* scratch, int64_t s, int T, int P, int num_sms, double** lam_hat,
+                                    cudaStream_t st) {
+  const int64_t slot = power_rows_slot(s, P);
+  double* lam = scratch + 2 * P * slot + num_sms + 2;
+  k_power_rows_final<<<1, 32, 0, st>>>(scratch + (int64_t)(T & 1) * P * slot, P, slot, lam);
+  *lam_hat = lam;
+  return cudaGetLastError();
+}
+}  // namespace cpa

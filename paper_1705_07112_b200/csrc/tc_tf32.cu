@@ -81,6 +81,11 @@ struct TcArgs {
   int chunk_kb;                  // k-blocks per TMEM accumulation chunk
   const int2* tile_list;
   int ntiles_list;
+  // panel mode (multi-GPU symmetric steps): tile_list / ntiles_list are this rank's sub-range of the
+  // lower-triangle list; W_k (or, when out_f is null -- the last step -- the updated H) of the tile at
+  // local index t is written packed to gout + t * BM * BN (row-major BM x BN, elements r >= c) instead
+  // of the out_* matrices; H accumulates in place on the own tiles
+  float* gout;
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -371,6 +376,7 @@ __global__ void __launch_bounds__(NTHR, 1)
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
       int tm, tn;
       coords(t, tm, tn);
+      const int t_local = t;
       mbar_wait(sfull + sb, sphase);
       tc_fence_after();
       const uint32_t sum_col = (uint32_t)((NACC + sb) * BN);
@@ -410,7 +416,13 @@ __global__ void __launch_bounds__(NTHR, 1)
               const float wpp = a.wpp[(int64_t)r * a.ld_w + c];
               w = 2.f * s2 * accv - 2.f * wp - wpp;                // W_k = 2 B_hat W_{k-1} - W_{k-2}
               float* yp = a.y + (int64_t)r * a.ld_y + c;
-              *yp = fmaf(ck, w, *yp);                              // Y += c_k W_k
+              const float yv = fmaf(ck, w, *yp);                   // Y += c_k W_k
+              *yp = yv;
+              if (a.gout) {   // panel mode: the all-gather slot (W_k, or H at the last step)
+                a.gout[(int64_t)t_local * (BM * BN) + (int64_t)(r - tm * BM) * BN + (c - tn * BN)] =
+                    a.out_f ? w : yv;
+                continue;
+              }
             }
             const int64_t o = (int64_t)r * a.ld_out + c;
             if (a.out_f) a.out_f[o] = w;
@@ -423,7 +435,7 @@ __global__ void __launch_bounds__(NTHR, 1)
           }
         }
         __syncwarp();
-        if (a.sym) {
+        if (a.sym && !a.gout) {
           // mirror (r, c) -> (c, r) for r > c from the natural layout (lane = row): for a
           // fixed column j the warp writes one coalesced 128-byte segment of row c
           const int r = row0 + lane;
@@ -521,7 +533,8 @@ static cudaError_t tc_gemm_bn(int mode, int terms, int M, int N, int Kd, const f
                               int64_t lda, const float* Bh, const float* Bl, int64_t ldb, bool b_mn, float* out_f,
                               float* out_h, float* out_l, int out_split, int64_t ld_out, const float* wp,
                               const float* wpp, int64_t ld_w, float* y, int64_t ld_y, const SeriesParams* P, int k,
-                              int num_sms, cudaStream_t st, int sym) {
+                              int num_sms, cudaStream_t st, int sym, int64_t p_tile0 = -1, int64_t p_ntile = 0,
+                              float* gout = nullptr) {
   using namespace tc;
   CUtensorMap ah, al, bh, bl;
   cudaError_t e = make_map(&ah, Ah, M, Kd, lda, BM);
@@ -546,6 +559,13 @@ static cudaError_t tc_gemm_bn(int mode, int terms, int M, int N, int Kd, const f
     a.mirror_f = mode == GRAM;
     a.tile_list = sym_tile_list(a.tiles_m, a.tiles_n, BM, BN, &a.ntiles_list);
     if (!a.tile_list) return cudaErrorMemoryAllocation;
+    if (p_tile0 >= 0) {   // panel mode: this rank's sub-range of the list, packed output
+      if (mode != STEP || !gout || p_tile0 + p_ntile > a.ntiles_list) return cudaErrorInvalidValue;
+      a.tile_list += p_tile0;
+      a.ntiles_list = (int)p_ntile;
+      a.gout = gout;
+      if (p_ntile == 0) return cudaSuccess;
+    }
   }
   // 256-wide tiles have one accumulator: the whole K for single-pass TF32, 16 k-blocks (K = 512)
   // for 3xTF32 (the MMA waits for each drain -- a short bubble against 3x the MMA work)
@@ -584,6 +604,79 @@ cudaError_t tc_gemm(int mode, int terms, int M, int N, int Kd, const float* Ah, 
                                ld_out, wp, wpp, ld_w, y, ld_y, P, k, num_sms, st, sym);
   return tc::tc_gemm_bn<128>(mode, terms, M, N, Kd, Ah, Al, lda, Bh, Bl, ldb, b_mn, out_f, out_h, out_l, out_split,
                              ld_out, wp, wpp, ld_w, y, ld_y, P, k, num_sms, st, sym);
+}
+
+// ------------------------------------------------------------------ multi-GPU panels (symmetric steps)
+// The step's tile geometry: 128 x 256 tiles for single-pass TF32 steps, 128 x 128 for 3xTF32 (the
+// choice tc_gemm makes for mode STEP), and its lower-triangle tile list.
+static int tf32_step_bn(int terms) { return terms == 1 ? 256 : 128; }
+
+cudaError_t tf32_panel_list(int64_t s, int terms, const int2** list, int* count, int* bn) {
+  const int BN = tf32_step_bn(terms);
+  const int tm = (int)((s + tc::BM - 1) / tc::BM), tn = (int)((s + BN - 1) / BN);
+  *list = tc::sym_tile_list(tm, tn, tc::BM, BN, count);
+  *bn = BN;
+  return *list ? cudaSuccess : cudaErrorMemoryAllocation;
+}
+
+// Step k of the symmetric TF32 recurrence on tiles [tile0, tile0 + ntile) of the list: W_k (or H
+// at the last step, out_f == nullptr) packed into gout.  Arguments as tc_gemm mode STEP.
+cudaError_t tc_gemm_panel(int terms, int s, const float* Ah, const float* Al, int64_t lda, const float* Bh,
+                          const float* Bl, int64_t ldb, bool last, int64_t ld_out, const float* wp, const float* wpp,
+                          int64_t ld_w, float* y, int64_t ld_y, const SeriesParams* P, int k, int64_t tile0,
+                          int64_t ntile, float* gout, int num_sms, cudaStream_t st) {
+  float* dummy = last ? nullptr : gout;   // non-null out_f marks "W_k" (the epilogue writes gout only)
+  if (terms == 1)
+    return tc::tc_gemm_bn<256>(2, 1, s, s, s, Ah, Al, lda, Bh, Bl, ldb, true, dummy, nullptr, nullptr, 1, ld_out, wp,
+                               wpp, ld_w, y, ld_y, P, k, num_sms, st, 1, tile0, ntile, gout);
+  return tc::tc_gemm_bn<128>(2, 3, s, s, s, Ah, Al, lda, Bh, Bl, ldb, true, dummy, nullptr, nullptr, 3, ld_out, wp,
+                             wpp, ld_w, y, ld_y, P, k, num_sms, st, 1, tile0, ntile, gout);
+}
+
+// Gathered slots -> W_k: fp32 lower triangle into Wf, TF32 hi / lo copies of both triangles into
+// Wh / Wl (the next step's B operand); at the last step (H != nullptr) the lower triangle into H.
+// One CTA per tile of the list; owner p of list entry t: [ntiles p / P, ntiles (p+1) / P).
+__global__ void __launch_bounds__(256) k_tf32_sym_unpack(const float* __restrict__ g, const int2* __restrict__ list,
+                                                         int64_t ntiles, int P, int64_t slot_tiles, int BN, int64_t s,
+                                                         int64_t ld, float* Wf, float* Wh, float* Wl, float* H) {
+  const int64_t t = blockIdx.x;
+  int p = (int)(t * P / ntiles);
+  while (p + 1 < P && ntiles * (p + 1) / P <= t) ++p;
+  while (p > 0 && ntiles * p / P > t) --p;
+  const int64_t lt = t - ntiles * p / P;
+  const float* src = g + ((int64_t)p * slot_tiles + lt) * (tc::BM * BN);
+  const int2 tt = list[t];
+  const int64_t r0 = (int64_t)tt.x * tc::BM, c0 = (int64_t)tt.y * BN;
+  for (int64_t e = threadIdx.x; e < (int64_t)tc::BM * BN; e += blockDim.x) {
+    const int64_t r = r0 + e / BN, c = c0 + e % BN;
+    if (r >= s || c >= s || c > r) continue;
+    const float v = __ldcs(src + e);
+    if (H) {
+      H[r * ld + c] = v;
+      continue;
+    }
+    Wf[r * ld + c] = v;
+    const float hi = tc::rna_tf32(v);
+    Wh[r * ld + c] = hi;
+    Wh[c * ld + r] = hi;
+    if (Wl) {
+      const float lo = tc::rna_tf32(v - hi);
+      Wl[r * ld + c] = lo;
+      Wl[c * ld + r] = lo;
+    }
+  }
+}
+
+cudaError_t tf32_sym_unpack(const float* gbuf, int64_t s, int terms, int P, int64_t slot_tiles, int64_t ld, float* Wf,
+                            float* Wh, float* Wl, float* H, cudaStream_t st) {
+  const int2* list;
+  int count, bn;
+  cudaError_t e = tf32_panel_list(s, terms, &list, &count, &bn);
+  if (e != cudaSuccess) return e;
+  if (count == 0) return cudaSuccess;
+  k_tf32_sym_unpack<<<count, 256, 0, st>>>(gbuf, list, count, P, slot_tiles, bn, s, ld, Wf, Wh, terms == 3 ? Wl : nullptr,
+                                          H);
+  return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ prep / finish

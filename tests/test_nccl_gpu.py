@@ -126,7 +126,8 @@ def test_panel_sharded_recurrence(env, s_, L_, K, mode):
     Psi_k (and H_hat after the last step).  simP: P virtual ranks' panels on this GPU one after
     the other (the slot layout a P-rank all-gather produces); nccl1: the real in-place
     ncclAllGather of a one-rank communicator.  Against the oracle and the persistent one-launch
-    recurrence (another k-split, so agreement to rounding)."""
+    recurrence (another k-split, so agreement to rounding).  The power iteration is row-sharded in
+    this mode as well (rank p computes rows [s p / P, s (p+1) / P) of every product)."""
     import os
     torch, P, D, hc, hp = env
     X = W.gen_c2(m=s_, n=L_, seed=s_ + K)
@@ -148,5 +149,41 @@ def test_panel_sharded_recurrence(env, s_, L_, K, mode):
     assert prof["step"][1] == nsteps * per and prof["exchange"][1] == nsteps
     Yp, Yn = Yp.cpu().numpy(), Yn.cpu().numpy()
     assert O.rel_fro(Yp, Yn) <= 1e-12
-    assert O.rel_fro(Yp, O.cpa_shrink(X, O.Kernel(**kern), K, T=80)) <= TOL64
+    Yo, io = O.cpa_shrink(X, O.Kernel(**kern), K, T=80, return_info=True)
+    # the power iteration runs row-sharded too (one all-gather of u per product)
+    assert abs(info["lambda_hat"] - io["lambda_hat"]) <= 1e-12 * io["lambda_hat"]
+    assert prof["power"][1] >= 1
+    assert O.rel_fro(Yp, Yo) <= TOL64
 
+
+
+@pytest.mark.parametrize("shape,K", [((300, 1200), 15), ((1100, 260), 9), ((520, 600), 3)])
+@pytest.mark.parametrize("math", ["3xtf32", "tf32"])
+@pytest.mark.parametrize("mode", ["sim3", "nccl1"])
+def test_panel_sharded_tf32(env, shape, K, math, mode):
+    """The tcgen05 s x s recurrence by tile panels (each rank 1/P of the lower-triangle tile list
+    of every step, packed slots all-gathered, unpacked into the fp32 lower triangle and the TF32
+    hi / lo operand copies) and the row-sharded power iteration on the fp32 Gram."""
+    import os
+    torch, P, D, hc, hp = env
+    m, n = shape
+    X = W.gen_c2(m=m, n=n, seed=21).astype(np.float32)
+    kern = {"kind": "soft", "tau": 0.1, "tau_relative": True}
+    Xd = torch.from_numpy(X).cuda()
+    env_var = ("CPA_SVT_PANEL_SIM", mode[3:]) if mode.startswith("sim") else ("CPA_SVT_PANELS", "1")
+    os.environ[env_var[0]] = env_var[1]
+    try:
+        hc.profile(True)
+        Yp, info = D.apply_sharded(hc, Xd, m, n, kern, K, T=200, math=math, info=True)
+        prof = hc.profile_read()
+        hc.profile(False)
+    finally:
+        del os.environ[env_var[0]]
+    Yn = hp.apply(Xd, kern, K, T=200, math=math)
+    per = int(mode[3:]) if mode.startswith("sim") else 1
+    assert prof["step"][1] == (K - 2) * per and prof["exchange"][1] == K - 2
+    Yp, Yn = Yp.cpu().numpy().astype(np.float64), Yn.cpu().numpy().astype(np.float64)
+    assert O.rel_fro(Yp, Yn) <= 1e-5
+    Yo, io = O.cpa_shrink(X.astype(np.float64), O.Kernel(**kern), K, T=200, return_info=True)
+    assert abs(info["lambda_hat"] - io["lambda_hat"]) <= 1e-5 * io["lambda_hat"]
+    assert O.rel_fro(Yp, Yo) <= (TOL32 if math == "3xtf32" else 3e-4)
