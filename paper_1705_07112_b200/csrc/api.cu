@@ -672,10 +672,11 @@ static cpa_svt_status run_recurrence_f64(cpa_svt_handle* h, bool left, int64_t M
 // Alg. 1 with symmetric tiles costs (K-2) s^3 + 2 s^2 L_local against
 // (K-1) 2 s^2 L_local for apply-to-X: fewer flops whenever K > 2 (s <= L).
 // Form 3 (the s x s form on full tiles) is kept for cross-checks.
-static int dense_form(const cpa_svt_handle* h, int64_t s, int64_t L_local, int K) {
+// With the multi-GPU panel split (P ranks) each rank does 1/P of the s x s recurrence.
+static int dense_form(const cpa_svt_handle* h, int64_t s, int64_t L_local, int K, int panel_P = 1) {
   if (K <= 2 || h->form == 1) return 1;
   if (h->form == 2 || h->form == 3) return h->form;
-  return (double)(K - 2) * s + 2.0 * L_local < 2.0 * (K - 1) * L_local ? 2 : 1;
+  return (double)(K - 2) * s / panel_P + 2.0 * L_local < 2.0 * (K - 1) * L_local ? 2 : 1;
 }
 static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt_shard shard,
                                 int64_t long_global, const double* X, int64_t ldx, double* Y, int64_t ldy,
@@ -786,8 +787,6 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
     }
     return st;
   }
-  const int form = dct ? 2 : dense_form(h, s, L, K);
-  const bool poly = form != 1;
   // Multi-GPU s x s recurrence (form 2, sharded): each rank computes a contiguous 1/P of the
   // lower tiles of every step and the steps' tiles are all-gathered (ncclAllGather, in place)
   // and unpacked into the full Psi_k on every rank -- instead of every rank evaluating the whole
@@ -796,9 +795,14 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
   // partition / pack / unpack; the slots are already in place, so no collective).
   int panel_sim = 0;
   if (const char* v = getenv("CPA_SVT_PANEL_SIM")) panel_sim = atoi(v);
-  const bool panels = form == 2 && K > 2 && !sparse_eps &&
-                      ((sharded && (h->world > 1 || env_on("CPA_SVT_PANELS"))) || (panel_sim > 1 && h->world == 1));
-  const int panel_P = panels ? (panel_sim > 1 && h->world == 1 ? panel_sim : h->world) : 1;
+  const bool panel_cand = K > 2 && !sparse_eps &&
+                          ((sharded && (h->world > 1 || env_on("CPA_SVT_PANELS"))) || (panel_sim > 1 && h->world == 1));
+  const int panel_cand_P = panel_cand ? (panel_sim > 1 && h->world == 1 ? panel_sim : h->world) : 1;
+  // (the form choice sees the per-rank share of the s x s recurrence)
+  const int form = dct ? 2 : dense_form(h, s, L, K, panel_cand_P);
+  const bool poly = form != 1;
+  const bool panels = panel_cand && form == 2;
+  const int panel_P = panels ? panel_cand_P : 1;
   const size_t nGb = panels ? (size_t)panel_P * (size_t)dense_sym_panel_slot(s, panel_P) * 4096 : 0;
   // the panel form also shards the power iteration by rows of G (one all-gather of u per product)
   const size_t nPR = panels ? (size_t)((power_rows_scratch_doubles(s, panel_P, h->num_sms) + 31) / 32 * 32) : 0;

@@ -485,11 +485,10 @@ __global__ void __launch_bounds__(kPRThreads, 1) k_power_rows(const E* __restric
     }
   }
   if (gin) {
-    for (int64_t i = threadIdx.x; i < s; i += blockDim.x) {
-      int p = (int)(i * P / s);
-      while (p + 1 < P && s * (p + 1) / P <= i) ++p;
-      while (p > 0 && s * p / P > i) --p;
-      u_s[i] = __ldcg(gin + (int64_t)p * slot + (i - s * p / P));
+    for (int p = 0; p < P; ++p) {   // slot p holds rows [s p / P, s (p+1) / P): one coalesced copy each
+      const int64_t b = s * p / P, e = s * (p + 1) / P;
+      const double* src = gin + (int64_t)p * slot - b;
+      for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) u_s[i] = __ldcg(src + i);
     }
   } else {
     const double v0 = 1.0 / sqrt((double)s);
@@ -498,7 +497,9 @@ __global__ void __launch_bounds__(kPRThreads, 1) k_power_rows(const E* __restric
   __syncthreads();
   const double inv = s_inv;
   double sq = 0.0;   // lane 0: squares of this warp's rows, in row order
-  for (int64_t row = r0 + (int64_t)blockIdx.x * (kPRThreads / 32) + warp; row < r1;
+  // rows interleaved over the CTAs first (row = r0 + warp * grid + block), so a short panel still
+  // spreads over every SM
+  for (int64_t row = r0 + (int64_t)warp * gridDim.x + blockIdx.x; row < r1;
        row += (int64_t)gridDim.x * (kPRThreads / 32)) {
     const E* g = G + row * ld;
     double a0 = 0.0, a1 = 0.0;
@@ -567,8 +568,7 @@ static cudaError_t launch_power_rows_t(const E* G, int64_t s, int64_t ld, int t,
   cudaError_t e = cudaFuncSetAttribute(k_power_rows<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int grid = num_sms;
-  const int64_t wneed = (r1 - r0 + 31) / 32;
-  if (grid > wneed) grid = (int)(wneed > 0 ? wneed : 1);
+  if (grid > r1 - r0) grid = (int)(r1 - r0 > 0 ? r1 - r0 : 1);
   k_power_rows<E><<<grid, kPRThreads, smem, st>>>(G, s, ld, P, slot, gin, r0, r1, gout, bpart, counter);
   return cudaGetLastError();
 }

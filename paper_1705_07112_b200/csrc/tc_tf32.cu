@@ -639,6 +639,7 @@ cudaError_t tc_gemm_panel(int terms, int s, const float* Ah, const float* Al, in
 __global__ void __launch_bounds__(256) k_tf32_sym_unpack(const float* __restrict__ g, const int2* __restrict__ list,
                                                          int64_t ntiles, int P, int64_t slot_tiles, int BN, int64_t s,
                                                          int64_t ld, float* Wf, float* Wh, float* Wl, float* H) {
+  __shared__ float tb[8][32][33];   // one 32 x 32 transpose buffer per warp
   const int64_t t = blockIdx.x;
   int p = (int)(t * P / ntiles);
   while (p + 1 < P && ntiles * (p + 1) / P <= t) ++p;
@@ -647,23 +648,38 @@ __global__ void __launch_bounds__(256) k_tf32_sym_unpack(const float* __restrict
   const float* src = g + ((int64_t)p * slot_tiles + lt) * (tc::BM * BN);
   const int2 tt = list[t];
   const int64_t r0 = (int64_t)tt.x * tc::BM, c0 = (int64_t)tt.y * BN;
-  for (int64_t e = threadIdx.x; e < (int64_t)tc::BM * BN; e += blockDim.x) {
-    const int64_t r = r0 + e / BN, c = c0 + e % BN;
-    if (r >= s || c >= s || c > r) continue;
-    const float v = __ldcs(src + e);
-    if (H) {
-      H[r * ld + c] = v;
-      continue;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nsub = (tc::BM / 32) * (BN / 32);
+  // 32 x 32 sub-blocks: direct (r, c) stores along c, mirrored (c, r) stores along r via the buffer
+  for (int sbk = warp; sbk < nsub; sbk += 8) {
+    const int sr = (sbk / (BN / 32)) * 32, sc = (sbk % (BN / 32)) * 32;
+    if (r0 + sr + 31 < c0 + sc) continue;   // entirely above the diagonal: nothing computed there
+    for (int i = 0; i < 32; ++i) {
+      const int64_t r = r0 + sr + i, c = c0 + sc + lane;
+      const float v = __ldcs(src + (int64_t)(sr + i) * BN + sc + lane);
+      tb[warp][i][lane] = v;
+      if (r >= s || c >= s || c > r) continue;
+      if (H) {
+        H[r * ld + c] = v;
+        continue;
+      }
+      Wf[r * ld + c] = v;
+      const float hi = tc::rna_tf32(v);
+      Wh[r * ld + c] = hi;
+      if (Wl) Wl[r * ld + c] = tc::rna_tf32(v - hi);
     }
-    Wf[r * ld + c] = v;
-    const float hi = tc::rna_tf32(v);
-    Wh[r * ld + c] = hi;
-    Wh[c * ld + r] = hi;
-    if (Wl) {
-      const float lo = tc::rna_tf32(v - hi);
-      Wl[r * ld + c] = lo;
-      Wl[c * ld + r] = lo;
+    __syncwarp();
+    if (!H) {
+      for (int j = 0; j < 32; ++j) {   // mirror: row c0 + sc + j of W, columns r0 + sr + lane
+        const int64_t c = c0 + sc + j, r = r0 + sr + lane;
+        if (r >= s || c >= s || c >= r) continue;
+        const float v = tb[warp][lane][j];
+        const float hi = tc::rna_tf32(v);
+        Wh[c * ld + r] = hi;
+        if (Wl) Wl[c * ld + r] = tc::rna_tf32(v - hi);
+      }
     }
+    __syncwarp();
   }
 }
 
