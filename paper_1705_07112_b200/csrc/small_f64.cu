@@ -34,6 +34,7 @@ struct SmallArgs {
   double lam_override;   // > 0: Lambda given, no power iteration
   const double* c_given; // device, nullable
   int nsq;               // squarings before the power iteration
+  int check;             // SPEC.md:215 divergence check folded in (check.cu's rule): ||Y|| vs 1e3 sum|c_k| ||X||
 };
 
 constexpr int SM_THREADS = 128;   // 4 warps: one 32 x 32 quarter of a 64 x 64 DMMA tile each
@@ -235,11 +236,13 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_f64(SmallArgs a) {
   }
   STAMP();
   // ---- line 12: P = H A (s x L; A(k, n) k-major = row-major A), right Y = P^T, left Y = P
+  double xsq = 0.0, ysq = 0.0;   // divergence check: this thread's sums of squares of X and Y
   for (int e = tid; e < 64 * lda; e += SM_THREADS) {
     const int r = e / lda, c = e % lda;
     double v = 0.0;
     if (r < s && c < L) v = left ? a.X[(int64_t)r * a.ldx + c] : a.X[(int64_t)c * a.ldx + r];
     Op[e] = v;
+    xsq = fma(v, v, xsq);
   }
   __syncthreads();
   for (int n0 = 0; n0 < L; n0 += 16 * h) {
@@ -256,8 +259,31 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_f64(SmallArgs a) {
           if (r < s && c < L) {
             if (left) a.Y[(int64_t)r * a.ldy + c] = acc[i][j][e];
             else      a.Y[(int64_t)c * a.ldy + r] = acc[i][j][e];
+            ysq = fma(acc[i][j][e], acc[i][j][e], ysq);
           }
         }
+  }
+  if (a.check) {   // fixed-order block sums (warp butterflies, then warps in order): deterministic
+    __shared__ double s_chk[2][SM_THREADS / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      xsq += __shfl_xor_sync(0xffffffffu, xsq, o);
+      ysq += __shfl_xor_sync(0xffffffffu, ysq, o);
+    }
+    if ((tid & 31) == 0) {
+      s_chk[0][tid >> 5] = xsq;
+      s_chk[1][tid >> 5] = ysq;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double sx = 0.0, sy = 0.0, cs = 0.0;
+      for (int w = 0; w < SM_THREADS / 32; ++w) {
+        sx += s_chk[0][w];
+        sy += s_chk[1][w];
+      }
+      for (int k = 0; k < a.P->K; ++k) cs += fabs(a.P->c[k]);
+      a.P->diverged = (a.P->degenerate || sqrt(sy) <= 1e3 * cs * sqrt(sx)) ? 0 : 1;
+    }
   }
 #ifdef CPA_SMALL_TRACE
   __syncthreads();
@@ -282,8 +308,9 @@ bool small_f64_fits(int64_t m, int64_t n) {
 
 cudaError_t launch_small_f64(const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t m, int64_t n,
                              SeriesParams* P, const cpa_svt_kernel& k, int K, int T, double safety,
-                             double lam_override, const double* c_given, int nsq, cudaStream_t st) {
+                             double lam_override, const double* c_given, int nsq, cudaStream_t st, int check) {
   SmallArgs a{};
+  a.check = check;
   a.X = X; a.ldx = ldx; a.Y = Y; a.ldy = ldy; a.m = (int)m; a.n = (int)n;
   a.P = P; a.kern = k; a.K = K; a.T = T; a.safety = safety; a.lam_override = lam_override;
   a.c_given = c_given; a.nsq = nsq;
