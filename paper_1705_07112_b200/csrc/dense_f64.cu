@@ -500,13 +500,15 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
 
 // WS: run by the 128 epilogue threads (warps 4-7) of k_cheb_sym_ws, thread u = threadIdx.x - 128
 // playing the role of MMA thread u (same fragment positions), synchronised on named barrier 2.
-template <bool tma, bool WS, bool PANEL, class Acc>
+template <bool tma, bool WS, bool PANEL, int NW, class Acc>
 __device__ __forceinline__ void sym_finish_impl(const SymArgs& a, int k, int tile, int q, int ti, int tj, Acc&& acc) {
   const int T = a.T;
   const int S = a.split;
   int* cross = a.sync + 1;
   int* split_cnt = a.sync + 1 + a.K * T;
   const int64_t s = a.s;
+  // NW = 4: warps own 32 x 32 sub-tiles (WJ = 4 column fragments); NW = 8: 32 x 16 (WJ = 2)
+  constexpr int NT = 32 * NW, WJ = NW == 4 ? 4 : 2, NV = 4 * WJ * 2;
   const int u = WS ? (int)threadIdx.x - NTHREADS : (int)threadIdx.x;
   auto group_sync = [] {
     if (WS) named_bar(2, NTHREADS);
@@ -514,7 +516,8 @@ __device__ __forceinline__ void sym_finish_impl(const SymArgs& a, int k, int til
   };
   const int warp = u >> 5, lane = u & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int wm = NW == 4 ? (warp >> 1) * 32 : (warp >> 2) * 32;
+  const int wn = NW == 4 ? (warp & 1) * 32 : (warp & 3) * 16;
   auto buf = [&](int i) { return i == 0 ? a.W[0] : (i == 1 ? a.W[1] : a.W[2]); };
   const double* src = buf((k - 1) % 3);   // W_{k-1}
   const double* wpp = buf((k - 2) % 3);   // W_{k-2} (k = 2: identity, implicit)
@@ -529,9 +532,9 @@ __device__ __forceinline__ void sym_finish_impl(const SymArgs& a, int k, int til
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < WJ; ++j)
 #pragma unroll
-          for (int e = 0; e < 2; ++e) __stcg(mine + ((i * 4 + j) * 2 + e) * NTHREADS + u, acc(i, j, e));
+          for (int e = 0; e < 2; ++e) __stcg(mine + ((i * WJ + j) * 2 + e) * NT + u, acc(i, j, e));
       group_sync();
       if (u == 0) red_release_add_i32(split_cnt + tile, 1);
       return;
@@ -539,20 +542,20 @@ __device__ __forceinline__ void sym_finish_impl(const SymArgs& a, int k, int til
     if (u == 0) wait_geq(split_cnt + tile, (S - 1) * (kc - 1));
     group_sync();
     if (!WS) {
-      double sum[32];
+      double sum[NV];
 #pragma unroll
-      for (int rr = 0; rr < 32; ++rr) sum[rr] = __ldcg(slot + rr * NTHREADS + u);
+      for (int rr = 0; rr < NV; ++rr) sum[rr] = __ldcg(slot + rr * NT + u);
       for (int p = 1; p < S - 1; ++p) {
-        double v[32];
+        double v[NV];
 #pragma unroll
-        for (int rr = 0; rr < 32; ++rr) v[rr] = __ldcg(slot + (int64_t)p * (BM * BN) + rr * NTHREADS + u);
+        for (int rr = 0; rr < NV; ++rr) v[rr] = __ldcg(slot + (int64_t)p * (BM * BN) + rr * NT + u);
 #pragma unroll
-        for (int rr = 0; rr < 32; ++rr) sum[rr] += v[rr];
+        for (int rr = 0; rr < NV; ++rr) sum[rr] += v[rr];
       }
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < WJ; ++j)
 #pragma unroll
           for (int e = 0; e < 2; ++e) acc(i, j, e) = sum[(i * 4 + j) * 2 + e] + acc(i, j, e);
     } else {
@@ -561,18 +564,18 @@ __device__ __forceinline__ void sym_finish_impl(const SymArgs& a, int k, int til
       for (int c8 = 0; c8 < 4; ++c8) {
         double sum[8];
 #pragma unroll
-        for (int x = 0; x < 8; ++x) sum[x] = __ldcg(slot + (c8 * 8 + x) * NTHREADS + u);
+        for (int x = 0; x < 8; ++x) sum[x] = __ldcg(slot + (c8 * 8 + x) * NT + u);
         for (int p = 1; p < S - 1; ++p) {
           double v[8];
 #pragma unroll
-          for (int x = 0; x < 8; ++x) v[x] = __ldcg(slot + (int64_t)p * (BM * BN) + (c8 * 8 + x) * NTHREADS + u);
+          for (int x = 0; x < 8; ++x) v[x] = __ldcg(slot + (int64_t)p * (BM * BN) + (c8 * 8 + x) * NT + u);
 #pragma unroll
           for (int x = 0; x < 8; ++x) sum[x] += v[x];
         }
 #pragma unroll
         for (int x = 0; x < 8; ++x) {
           const int rr = c8 * 8 + x;
-          acc(rr >> 3, (rr >> 1) & 3, rr & 1) = sum[x] + acc(rr >> 3, (rr >> 1) & 3, rr & 1);
+          acc(rr >> 3, (rr >> 1) & 3, rr & 1) = sum[x] + acc(rr >> 3, (rr >> 1) & 3, rr & 1);   // (NW = 4 only)
         }
       }
     }
@@ -583,9 +586,9 @@ __device__ __forceinline__ void sym_finish_impl(const SymArgs& a, int k, int til
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int64_t rr = m0 + wm + i * 8 + g;
-    double vp[8], vpp[8], vy[8];
+    double vp[2 * WJ], vpp[2 * WJ], vy[2 * WJ];
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < WJ; ++j)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int64_t c = n0 + wn + j * 8 + 2 * t + e;
@@ -596,7 +599,7 @@ __device__ __forceinline__ void sym_finish_impl(const SymArgs& a, int k, int til
         vy[j * 2 + e] = ok ? __ldcg(a.H + o) : 0.0;
       }
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < WJ; ++j)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int64_t c = n0 + wn + j * 8 + 2 * t + e;
@@ -631,11 +634,11 @@ __device__ __forceinline__ void sym_finish_impl(const SymArgs& a, int k, int til
 }
 
 // k_cheb_sym / k_cheb_sym_tma: the accumulators in registers
-template <bool tma, bool PANEL>
+template <bool tma, bool PANEL, int NW = 4>
 __device__ __forceinline__ void sym_finish(const SymArgs& a, int k, int tile, int q, int ti, int tj,
-                                           double (&acc)[4][4][2]) {
-  sym_finish_impl<tma, false, PANEL>(a, k, tile, q, ti, tj,
-                                     [&](int i, int j, int e) -> double& { return acc[i][j][e]; });
+                                           double (&acc)[4][NW == 4 ? 4 : 2][2]) {
+  sym_finish_impl<tma, false, PANEL, NW>(a, k, tile, q, ti, tj,
+                                         [&](int i, int j, int e) -> double& { return acc[i][j][e]; });
 }
 
 template <bool PANEL>
@@ -703,8 +706,11 @@ struct SymMaps {
 // SBK-deep slabs in an SSTAGES ring: <16, 4> (64 KB) for short units (c2: ~11 slabs each),
 // <32, 2> (64 KB, half the mbarrier round trips) for long ones (s >= 4096: c5 shape 608 ->
 // 586 ms; at c2 it costs 1.27 -> 1.39 ms).
-template <int SBK, int SSTAGES, bool PANEL>
-__global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB)
+// NW = 8 (CPA_SVT_SYM_NW=8): eight warps of 32 x 16 sub-tiles per 64 x 64 tile -- half the
+// accumulator registers per thread, so three 256-thread CTAs (24 warps, six per SMSP) fit an SM
+// where the 4-warp kernel keeps twelve; the same per-element DMMA order (bitwise-equal results).
+template <int SBK, int SSTAGES, bool PANEL, int NW = 4>
+__global__ void __launch_bounds__(32 * NW, CPA_FLOW_MINB)
     k_cheb_sym_tma(const __grid_constant__ SymMaps mp, SymArgs a) {
   constexpr int SBOX_BYTES = 16 * SBK * 8;
   constexpr int SSTAGE_BYTES = 8 * SBOX_BYTES;
@@ -723,11 +729,13 @@ __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB)
   const int nk = (int)((a.s + SBK - 1) / SBK);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  constexpr int WJ = NW == 4 ? 4 : 2;
+  const int wm = NW == 4 ? (warp >> 1) * 32 : (warp >> 2) * 32;
+  const int wn = NW == 4 ? (warp & 1) * 32 : (warp & 3) * 16;
   if (threadIdx.x == 0) {
     for (int st = 0; st < SSTAGES; ++st) {
       mbar_init(full + st, 1);
-      mbar_init(empty + st, 4);
+      mbar_init(empty + st, NW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -784,11 +792,11 @@ __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB)
     // unit too short to refill (nku < SSTAGES) takes a CTA barrier instead.
     if (nku < SSTAGES) __syncthreads();
     else __syncwarp();
-    double acc[4][4][2];
+    double acc[4][WJ][2];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      for (int j = 0; j < WJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     for (int kt = 0; kt < nku; ++kt) {
       if (threadIdx.x == 0 && kt + SSTAGES - 1 < nku) {   // refill the stage of slab kt-1
         const int kn = kt + SSTAGES - 1;
@@ -809,17 +817,17 @@ __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB)
       for (int kk = 0; kk < SBK / 4; ++kk) {
         const int par = kk & 1;
         const uint32_t ro = 1024 * (kk >> 1) + 128 * par + roff;
-        double fa[4], fb[4];
+        double fa[4], fb[WJ];
 #pragma unroll
         for (int i = 0; i < 4; ++i)
           fa[i] = *reinterpret_cast<const double*>(sa + (i >> 1) * SBOX_BYTES + ro + coff[par][i & 1]);
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < WJ; ++j)
           fb[j] = *reinterpret_cast<const double*>(sb + (j >> 1) * SBOX_BYTES + ro + coff[par][j & 1]);
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], fa[i], fb[j]);
+          for (int j = 0; j < WJ; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], fa[i], fb[j]);
       }
       // the stage is rewritten by the async proxy (TMA) once all four warps have arrived:
       // order this warp's generic-proxy fragment loads before that (without the fence ptxas
@@ -829,7 +837,7 @@ __global__ void __launch_bounds__(NTHREADS, CPA_FLOW_MINB)
       if (lane == 0) mbar_arrive(empty + st);
     }
     it += nku;
-    sym_finish<true, PANEL>(a, k, tile, q, ti, tj, acc);
+    sym_finish<true, PANEL, NW>(a, k, tile, q, ti, tj, acc);
   }
 }
 
@@ -899,7 +907,7 @@ __global__ void __launch_bounds__(2 * NTHREADS, 2)
       // the accumulators stay in the staging buffer (read where used: the register budget of the
       // 2-CTA kernel); the buffer is released after the unit
       double* stg = stage + b * (BM * BN);
-      sym_finish_impl<true, true, false>(a, mt.k, mt.tile, mt.q, mt.ti, mt.tj, [&](int i, int j, int e) -> double& {
+      sym_finish_impl<true, true, false, 4>(a, mt.k, mt.tile, mt.q, mt.ti, mt.tj, [&](int i, int j, int e) -> double& {
         return stg[((i * 4 + j) * 2 + e) * NTHREADS + u];
       });
       __syncwarp();
@@ -1755,17 +1763,23 @@ static cudaError_t sym_launch(SymArgs& a, int64_t total, int slots, int num_sms,
     if (ok) {
       // both instances use a 64 KB ring: 4 x 16-deep or 2 x 32-deep stages
       const size_t tsmem = (size_t)4 * 8 * (16 * 16 * 8) + 1024;
-      auto kf = a.panel ? (sbk == 32 ? k_cheb_sym_tma<32, 2, true> : k_cheb_sym_tma<16, 4, true>)
-                        : (sbk == 32 ? k_cheb_sym_tma<32, 2, false> : k_cheb_sym_tma<16, 4, false>);
+      const int nw = (getenv("CPA_SVT_SYM_NW") && atoi(getenv("CPA_SVT_SYM_NW")) == 8) ? 8 : 4;
+      auto kf = nw == 8 ? (a.panel ? (sbk == 32 ? k_cheb_sym_tma<32, 2, true, 8> : k_cheb_sym_tma<16, 4, true, 8>)
+                                   : (sbk == 32 ? k_cheb_sym_tma<32, 2, false, 8> : k_cheb_sym_tma<16, 4, false, 8>))
+                        : (a.panel ? (sbk == 32 ? k_cheb_sym_tma<32, 2, true> : k_cheb_sym_tma<16, 4, true>)
+                                   : (sbk == 32 ? k_cheb_sym_tma<32, 2, false> : k_cheb_sym_tma<16, 4, false>));
       e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
       if (e != cudaSuccess) return e;
-      int per_sm = 0;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kf, NTHREADS, tsmem) != cudaSuccess || per_sm < 1)
-        return cudaErrorLaunchOutOfResources;
+      e = cudaFuncSetAttribute(kf, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+      if (e != cudaSuccess) return e;
+      int dev = 0;
+      cudaGetDevice(&dev);
+      const int per_sm = resident_ctas((const void*)kf, 32 * nw, tsmem, dev);
+      if (env_on("CPA_SVT_DEBUG_OCC")) fprintf(stderr, "k_cheb_sym_tma<%d,NW=%d>: %d CTAs/SM\n", sbk, nw, per_sm);
       int64_t tgrid = (int64_t)num_sms * per_sm;
       if (tgrid > total) tgrid = total;
       void* targs[] = {&mp, &a};
-      return cudaLaunchCooperativeKernel((void*)kf, dim3((unsigned)tgrid), dim3(NTHREADS), targs, tsmem, st);
+      return cudaLaunchCooperativeKernel((void*)kf, dim3((unsigned)tgrid), dim3(32 * nw), targs, tsmem, st);
     }
   }
   void* args[] = {&a};

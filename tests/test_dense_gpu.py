@@ -367,3 +367,31 @@ def test_warp_specialized_recurrence_bitwise(env, s, L, K, split):
     assert np.array_equal(out["0"], out["1"])
     if s <= 1100:
         assert O.rel_fro(out["1"], O.cpa_shrink(X, O.Kernel(**kern), K, T=100)) <= TOL64
+
+
+@pytest.mark.parametrize("s,L,K,split", [(1024, 1024, 30, 0), (1024, 1100, 12, 1), (1024, 1024, 9, 3), (256, 300, 5, 2),
+                                         (130, 300, 7, 0), (64, 200, 3, 0), (4096, 4200, 5, 0), (1538, 1600, 6, 5)])
+def test_eight_warp_recurrence_bitwise(env, s, L, K, split):
+    """k_cheb_sym_tma with eight 32 x 16 warp tiles per CTA (CPA_SVT_SYM_NW=8) against the four
+    32 x 32 warp tiles: every output element sees the same DMMA k-order and the same split-K sums,
+    so the outputs are bitwise equal; and the oracle bar."""
+    import os
+    torch, P, _ = env
+    X = W.gen_c2(m=s, n=L, seed=s + K + 1)
+    kern = {"kind": "soft", "tau": 0.05, "tau_relative": True}
+    Xd = torch.from_numpy(X).cuda()
+    out = {}
+    if split:
+        os.environ["CPA_SVT_FLOW_SPLIT"] = str(split)
+    try:
+        for nw in ("4", "8"):
+            os.environ["CPA_SVT_SYM_NW"] = nw
+            h2 = P.Handle(0)
+            out[nw] = h2.apply(Xd, kern, K, T=100).cpu().numpy()
+            h2.close()
+    finally:
+        os.environ.pop("CPA_SVT_SYM_NW", None)
+        os.environ.pop("CPA_SVT_FLOW_SPLIT", None)
+    assert np.array_equal(out["4"], out["8"])
+    if s <= 1100:
+        assert O.rel_fro(out["8"], O.cpa_shrink(X, O.Kernel(**kern), K, T=100)) <= TOL64
