@@ -557,7 +557,7 @@ __device__ __forceinline__ void sym_finish_impl(const SymArgs& a, int k, int til
 #pragma unroll
         for (int j = 0; j < WJ; ++j)
 #pragma unroll
-          for (int e = 0; e < 2; ++e) acc(i, j, e) = sum[(i * 4 + j) * 2 + e] + acc(i, j, e);
+          for (int e = 0; e < 2; ++e) acc(i, j, e) = sum[(i * WJ + j) * 2 + e] + acc(i, j, e);
     } else {
       // the same sums in the same order, eight elements at a time (register budget of the 2-CTA kernel)
 #pragma unroll
