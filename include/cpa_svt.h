@@ -185,7 +185,8 @@ cpa_svt_status cpa_svt_apply_host(cpa_svt_handle* h, cpa_svt_dtype dtype, cpa_sv
                                   cpa_svt_info* info);
 
 /* Sparse X (m x n, CSR, fp64): Y = X H_hat(X^T X), the n x n Gram never
- * formed.  Each step runs Z = W_{k-1} X^T (m x m block rows) then
+ * formed.  c: optional host array of K raw coefficients replacing line 4 (as in
+ * cpa_svt_apply; NULL = computed on the device from k and Lambda_max).  Each step runs Z = W_{k-1} X^T (m x m block rows) then
  * W_k = (4/L) Z X - 2 W_{k-1} - W_{k-2} fused with Y += c_k W_k.  X is
  * replicated on every rank (row_ptr int64[m+1], col int32[nnz] sorted per
  * row, val fp64[nnz], all device); this rank computes rows
@@ -194,7 +195,7 @@ cpa_svt_status cpa_svt_apply_host(cpa_svt_handle* h, cpa_svt_dtype dtype, cpa_sv
 cpa_svt_status cpa_svt_apply_csr(cpa_svt_handle* h, int64_t m, int64_t n, int64_t nnz,
                                  const int64_t* row_ptr, const int32_t* col, const double* val,
                                  int64_t row_begin, int64_t row_end, double* Y, int64_t ldy,
-                                 const cpa_svt_kernel* k, int K, cpa_svt_lambda* lam,
+                                 const cpa_svt_kernel* k, int K, const double* c, cpa_svt_lambda* lam,
                                  cpa_svt_info* info);
 
 /* Batched fp32 shrinkage of `batch` independent m x n matrices stored

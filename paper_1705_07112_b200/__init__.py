@@ -71,7 +71,8 @@ lib.cpa_svt_apply.argtypes = [_p, ctypes.c_int, ctypes.c_int, _i64, _i64, ctypes
 lib.cpa_svt_apply_host.argtypes = [_p, ctypes.c_int, ctypes.c_int, _i64, _i64, _p, _p, ctypes.POINTER(Kernel),
                                    ctypes.c_int, ctypes.POINTER(Lambda), ctypes.POINTER(Info)]
 lib.cpa_svt_apply_csr.argtypes = [_p, _i64, _i64, _i64, _p, _p, _p, _i64, _i64, _p, _i64, ctypes.POINTER(Kernel),
-                                  ctypes.c_int, ctypes.POINTER(Lambda), ctypes.POINTER(Info)]
+                                  ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(Lambda),
+                                  ctypes.POINTER(Info)]
 lib.cpa_svt_apply_batched.argtypes = [_p, _i64, ctypes.c_int, ctypes.c_int, _p, _p, ctypes.POINTER(Kernel),
                                       ctypes.c_int, ctypes.POINTER(Lambda), _p]
 lib.cpa_svt_status_string.restype = ctypes.c_char_p
@@ -307,7 +308,7 @@ class Handle:
 
     def apply_csr(self, row_ptr, col, val, m: int, n: int, kernel, K: int, T: int = 300, safety: float = 1.01,
                   lambda_max: float = 0.0, row_begin: int = 0, row_end: int | None = None, Y=None,
-                  info: bool = False, want_lambda: bool = False):
+                  info: bool = False, want_lambda: bool = False, coeffs=None):
         """cpa_svt_apply_csr: CSR X (int64 row_ptr, int32 col, float64 val, all CUDA); returns dense rows."""
         torch = self._torch
         row_end = m if row_end is None else row_end
@@ -322,10 +323,12 @@ class Handle:
             "Y must be a float64 CUDA tensor with >= row_end - row_begin rows of n columns"
         lam = self._lambda(T, safety, lambda_max, want_lambda)
         inf = Info() if info else None
+        cbuf = (ctypes.c_double * len(coeffs))(*coeffs) if coeffs is not None else None
+        K = len(coeffs) if coeffs is not None else K
         st = lib.cpa_svt_apply_csr(self._h, m, n, val.numel(), row_ptr.data_ptr(), col.data_ptr(), val.data_ptr(),
                                    row_begin, row_end, Y.data_ptr(), Y.stride(0),
-                                   ctypes.byref(kernel_from_dict(kernel)), K, ctypes.byref(lam),
-                                   ctypes.byref(inf) if inf is not None else None)
+                                   ctypes.byref(kernel_from_dict(kernel if kernel is not None else {"kind": "hard"})),
+                                   K, cbuf, ctypes.byref(lam), ctypes.byref(inf) if inf is not None else None)
         self._check(st, "cpa_svt_apply_csr")
         if info or want_lambda:
             return Y, (inf.as_dict() if inf is not None else {"lambda_hat": lam.lambda_hat,

@@ -138,7 +138,7 @@ cudaError_t sparse_apply(int64_t m, int64_t n, int64_t nnz, const int64_t* row_p
                          const double* val, int64_t row_begin, int64_t row_end, double* Y, int64_t ldy,
                          const cpa_svt_kernel& k, int K, int T, double safety, double lam_override,
                          SeriesParams* P, void* ws, size_t ws_bytes, size_t* ws_needed, int num_sms,
-                         cudaStream_t st, int* launches, SparsePhaseHook hook, void* hook_ctx);
+                         cudaStream_t st, int* launches, SparsePhaseHook hook, void* hook_ctx, const double* c_given);
 }  // namespace cpa
 
 using namespace cpa;
@@ -1520,27 +1520,39 @@ cpa_svt_status cpa_svt_apply_batched(cpa_svt_handle* h, int64_t batch, int m, in
 
 cpa_svt_status cpa_svt_apply_csr(cpa_svt_handle* h, int64_t m, int64_t n, int64_t nnz, const int64_t* row_ptr,
                                  const int32_t* col, const double* val, int64_t row_begin, int64_t row_end,
-                                 double* Y, int64_t ldy, const cpa_svt_kernel* k, int K, cpa_svt_lambda* lam,
-                                 cpa_svt_info* info) {
+                                 double* Y, int64_t ldy, const cpa_svt_kernel* k, int K, const double* c,
+                                 cpa_svt_lambda* lam, cpa_svt_info* info) {
   if (!h || !row_ptr || !Y || m < 1 || n < 1 || nnz < 0 || (nnz > 0 && (!col || !val))) return CPA_SVT_E_ARG;
   if (row_begin < 0 || row_end > m || row_begin > row_end || ldy < n || K < 2 || K > CPA_SVT_KMAX)
     return CPA_SVT_E_ARG;
   if (m > 2147483647 || n > 2147483647) return CPA_SVT_E_ARG;
-  cpa_svt_status st = check_kernel(k);
-  if (st != CPA_SVT_OK) return st;
+  cpa_svt_status st = CPA_SVT_OK;
+  cpa_svt_kernel kz{};
+  if (c) {   // raw coefficients replace line 4 (the kernel is not used)
+    if (!k) k = &kz;
+  } else {
+    st = check_kernel(k);
+    if (st != CPA_SVT_OK) return st;
+  }
   st = check_lambda(lam);
   if (st != CPA_SVT_OK) return st;
   if (cudaSetDevice(h->device) != cudaSuccess) return CPA_SVT_E_CUDA;
+  const double* c_dev = nullptr;
+  if (c) {
+    CU(cudaMemcpyAsync(h->d_c, c, K * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+    c_dev = h->d_c;
+  }
   size_t need = 0;
   CU(sparse_apply(m, n, nnz, row_ptr, col, val, row_begin, row_end, Y, ldy, *k, K, lam->power_iters, lam->safety,
-                  lam->lambda_max, h->P, nullptr, 0, &need, h->num_sms, h->stream, nullptr, nullptr, nullptr));
+                  lam->lambda_max, h->P, nullptr, 0, &need, h->num_sms, h->stream, nullptr, nullptr, nullptr, c_dev));
   st = grow(h, &h->ws, &h->ws_bytes, need);
   if (st != CPA_SVT_OK) return st;
   PhaseTimer tm;
   tm.start(info != nullptr, h->stream);
   int launches = 0;
   CU(sparse_apply(m, n, nnz, row_ptr, col, val, row_begin, row_end, Y, ldy, *k, K, lam->power_iters, lam->safety,
-                  lam->lambda_max, h->P, h->ws, h->ws_bytes, &need, h->num_sms, h->stream, &launches, phase_hook, h));
+                  lam->lambda_max, h->P, h->ws, h->ws_bytes, &need, h->num_sms, h->stream, &launches, phase_hook, h,
+                  c_dev));
   tm.mark();
   if (h->div_mode && nnz > 0) {   // ||X||_F from the stored values; this rank's rows of Y
     CU(divergence_check_f64(val, 1, nnz, nnz, Y, row_end - row_begin, n, ldy, h->dchk, h->P, h->stream));

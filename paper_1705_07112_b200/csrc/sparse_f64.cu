@@ -253,7 +253,7 @@ cudaError_t sparse_apply(int64_t m, int64_t n, int64_t nnz, const int64_t* row_p
                          const double* val, int64_t row_begin, int64_t row_end, double* Y, int64_t ldy,
                          const cpa_svt_kernel& kern, int K, int T, double safety, double lam_override,
                          SeriesParams* P, void* ws, size_t ws_bytes, size_t* ws_needed, int num_sms,
-                         cudaStream_t st, int* launches, SparsePhaseHook hook, void* hook_ctx) {
+                         cudaStream_t st, int* launches, SparsePhaseHook hook, void* hook_ctx, const double* c_given) {
   const int64_t rows = row_end - row_begin;
   const int64_t nblk = (rows + RB - 1) / RB;
   // workspace layout
@@ -316,7 +316,7 @@ cudaError_t sparse_apply(int64_t m, int64_t n, int64_t nnz, const int64_t* row_p
   // ---- Lambda_max (m-side power iteration) and coefficients
   if (hook) hook(hook_ctx, CPA_SVT_PH_POWER, 1);
   if (lam_override > 0.0) {
-    SPCK(launch_series(P, kern, K, safety, lam_override, nullptr, nullptr, st)); ++L;
+    SPCK(launch_series(P, kern, K, safety, lam_override, nullptr, c_given, st)); ++L;
   } else {
     k_fill<<<g, 256, 0, st>>>(v, m, 1.0 / sqrt((double)m)); ++L;
     const int spg = (int)std::min<int64_t>((m + SP_WARPS - 1) / SP_WARPS, npart);
@@ -326,7 +326,7 @@ cudaError_t sparse_apply(int64_t m, int64_t n, int64_t nnz, const int64_t* row_p
       k_spmv<<<spg, SP_WARPS * 32, 0, st>>>(row_ptr, col, val, m, tv, v, part); ++L;
       k_norm<<<1, 256, 0, st>>>(part, spg, nrm, nrm + 1); ++L;
     }
-    SPCK(launch_series(P, kern, K, safety, 0.0, nrm, nullptr, st)); ++L;
+    SPCK(launch_series(P, kern, K, safety, 0.0, nrm, c_given, st)); ++L;
   }
   if (hook) hook(hook_ctx, CPA_SVT_PH_POWER, 0);
   // ---- recurrence on this rank's rows

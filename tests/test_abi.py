@@ -54,8 +54,11 @@ def test_argument_validation_without_device(P):
     assert L.cpa_svt_apply(None, 0, 0, 4, 4, 0, 0, None, 4, None, 4, ctypes.byref(k), 5, None,
                            ctypes.byref(lam), None) == 1
     assert L.cpa_svt_apply_batched(None, 1, 8, 8, None, None, ctypes.byref(k), 5, ctypes.byref(lam), None) == 1
-    assert L.cpa_svt_apply_csr(None, 4, 4, 0, None, None, None, 0, 4, None, 4, ctypes.byref(k), 5,
+    assert L.cpa_svt_apply_csr(None, 4, 4, 0, None, None, None, 0, 4, None, 4, ctypes.byref(k), 5, None,
                                ctypes.byref(lam), None) == 1
+    nr, rk = ctypes.c_int(), ctypes.c_int()
+    assert L.cpa_svt_comm_info(None, ctypes.byref(nr), ctypes.byref(rk)) == 1
+    assert L.cpa_svt_set_option(None, 3, 1) == 1
     h = ctypes.c_void_p()
     assert L.cpa_svt_init(ctypes.byref(h), 0, None, None, 1, 1) == 1     # rank >= world
     assert L.cpa_svt_init(ctypes.byref(h), 0, None, None, 0, 2) == 1     # world > 1 needs an id

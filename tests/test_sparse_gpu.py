@@ -106,3 +106,28 @@ def test_config4_full_size_sampled(env):
     Yo, io = O.cpa_shrink_sparse_rows(Xs, rows, O.Kernel(**cfg["kernel"]), cfg["K"], T=cfg["T"])
     assert abs(info["lambda_hat"] - io["lambda_hat"]) <= 1e-12 * io["lambda_hat"]
     assert O.rel_fro(Ys, Yo) <= TOL64
+
+
+def test_raw_coefficients_sparse():
+    """P8 on the sparse path: raw coefficients (2, 0, ...) give Y = X's rows, (Lambda, Lambda/2, 0, ...)
+    give the rows of X X^T X (one SpMM pair), e_k gives X Psi_k(B_hat) (oracle)."""
+    import scipy.sparse as sp
+    import torch
+    import paper_1705_07112_b200 as P
+    m, n = 60, 500
+    rp, col, val = W.gen_c4(m=m, n=n, nnz=1500, seed=5)
+    Xs = sp.csr_matrix((val, col, rp), shape=(m, n))
+    Xd = Xs.toarray()
+    lam = 2.0 * float(np.linalg.norm(Xd, 2)) ** 2
+    d = [torch.from_numpy(a).cuda() for a in (rp, col, val)]
+    h = P.Handle(0)
+    Y = h.apply_csr(*d, m, n, None, 4, lambda_max=lam, coeffs=[2.0, 0.0, 0.0, 0.0]).cpu().numpy()
+    assert O.rel_fro(Y, Xd) <= 1e-14
+    Y = h.apply_csr(*d, m, n, None, 4, lambda_max=lam, coeffs=[lam, lam / 2, 0.0, 0.0]).cpu().numpy()
+    assert O.rel_fro(Y, Xd @ Xd.T @ Xd) <= 1e-13
+    for kk in (2, 3, 5):
+        c = [0.0] * 6
+        c[kk] = 1.0
+        Y = h.apply_csr(*d, m, n, None, 6, lambda_max=lam, coeffs=c).cpu().numpy()
+        assert O.rel_fro(Y, O.cpa_shrink(Xd, None, 6, lam=lam, coeffs=c)) <= 1e-12
+    h.close()
