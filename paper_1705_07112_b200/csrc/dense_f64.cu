@@ -709,6 +709,24 @@ struct SymMaps {
 // NW = 8 (CPA_SVT_SYM_NW=8): eight warps of 32 x 16 sub-tiles per 64 x 64 tile -- half the
 // accumulator registers per thread, so three 256-thread CTAs (24 warps, six per SMSP) fit an SM
 // where the 4-warp kernel keeps twelve; the same per-element DMMA order (bitwise-equal results).
+#ifdef CPA_SYM_TRACE
+// Trace build (build.py --variant trace CPA_SYM_TRACE=1): per unit (ticket) the globaltimer at the
+// claim, after the claim broadcast, after the dependency wait, at the mainloop end and at the
+// epilogue end, and the SM / CTA; read with cpa_svt_debug_sym_trace (tools/sym_trace.py).
+constexpr int kTraceUnits = 1 << 16;
+__device__ uint64_t g_trace[kTraceUnits * 6];
+__device__ __forceinline__ uint64_t trace_now() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ uint64_t smid_now() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+#endif
+
 template <int SBK, int SSTAGES, bool PANEL, int NW = 4>
 __global__ void __launch_bounds__(32 * NW, CPA_FLOW_MINB)
     k_cheb_sym_tma(const __grid_constant__ SymMaps mp, SymArgs a) {
@@ -750,9 +768,20 @@ __global__ void __launch_bounds__(32 * NW, CPA_FLOW_MINB)
   const uint32_t boxa = (wm >> 4) * SBOX_BYTES, boxb = (4 + (wn >> 4)) * SBOX_BYTES;
   uint32_t it = 0;  // slabs consumed by this CTA so far (stage = it % SSTAGES, phase = it / SSTAGES)
   for (;;) {
+#ifdef CPA_SYM_TRACE
+    uint64_t t_claim0 = 0;
+    if (threadIdx.x == 0) t_claim0 = trace_now();
+#endif
     if (threadIdx.x == 0) s_ticket = atomicAdd(a.sync, 1);
     __syncthreads();
     const int tk = s_ticket;
+#ifdef CPA_SYM_TRACE
+    if (threadIdx.x == 0 && tk < total && tk < kTraceUnits) {
+      g_trace[tk * 6 + 0] = t_claim0;
+      g_trace[tk * 6 + 1] = trace_now();
+      g_trace[tk * 6 + 5] = smid_now() | ((uint64_t)blockIdx.x << 16);
+    }
+#endif
     if (tk >= total) break;
     const int k = PANEL ? a.kstep : 2 + tk / per_step;
     const int r = tk % per_step;
@@ -779,6 +808,9 @@ __global__ void __launch_bounds__(32 * NW, CPA_FLOW_MINB)
         if (k >= 3) wait_geq(cross + (k - 1) * T + tj, T);
         if (k >= 4) wait_geq(cross + (k - 2) * T + ti, T);
       }
+#ifdef CPA_SYM_TRACE
+      if (tk < kTraceUnits) g_trace[tk * 6 + 2] = trace_now();
+#endif
       fence_proxy_async_global();   // generic-proxy W_{k-1} stores of other CTAs -> TMA reads
       for (int p = 0; p < P; ++p) {
         const uint32_t st = (it + p) % SSTAGES;
@@ -837,7 +869,13 @@ __global__ void __launch_bounds__(32 * NW, CPA_FLOW_MINB)
       if (lane == 0) mbar_arrive(empty + st);
     }
     it += nku;
+#ifdef CPA_SYM_TRACE
+    if (threadIdx.x == 0 && tk < kTraceUnits) g_trace[tk * 6 + 3] = trace_now();
+#endif
     sym_finish<true, PANEL, NW>(a, k, tile, q, ti, tj, acc);
+#ifdef CPA_SYM_TRACE
+    if (threadIdx.x == 0 && tk < kTraceUnits) g_trace[tk * 6 + 4] = trace_now();
+#endif
   }
 }
 
@@ -1944,3 +1982,10 @@ cudaError_t dense_haar_combine(const double* YL, const double* AH, const SeriesP
 }
 
 }  // namespace cpa
+
+#ifdef CPA_SYM_TRACE
+extern "C" int cpa_svt_debug_sym_trace(void* host_out, int64_t units) {
+  if (units > cpa::kTraceUnits) units = cpa::kTraceUnits;
+  return (int)cudaMemcpyFromSymbol(host_out, cpa::g_trace, (size_t)units * 6 * sizeof(uint64_t));
+}
+#endif
