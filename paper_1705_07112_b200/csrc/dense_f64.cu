@@ -630,6 +630,7 @@ __device__ __forceinline__ void sym_finish_impl(const SymArgs& a, int k, int til
   if (u == 0) {
     red_release_add_i32(cross + k * T + ti, 1);
     if (ti != tj) red_release_add_i32(cross + k * T + tj, 1);
+    red_release_add_i32(cross + a.K * T + T * (T + 1) / 2 + k * (T * (T + 1) / 2) + tile, 1);   // tile done
   }
 }
 
@@ -794,28 +795,53 @@ __global__ void __launch_bounds__(32 * NW, CPA_FLOW_MINB)
     const int m0 = ti * BM, n0 = tj * BN;
     const int kb = (int)((int64_t)nk * q / S), ke = (int)((int64_t)nk * (q + 1) / S);
     const int nku = ke - kb;
-    if (threadIdx.x == 0) {
-      // prologue: the static G slabs before the dependency wait, the W_{k-1} slabs after it
+    if (warp == 0) {
+      // prologue: lane 0 issues the static G slabs; meanwhile the lanes poll the unit's dependency
+      // flags in parallel (one flag per lane: each satisfied wait costs one L2 round trip, not one
+      // per flag); after the warp barrier lane 0 issues the W_{k-1} slabs
       const int P = nku < SSTAGES - 1 ? nku : SSTAGES - 1;
-      for (int p = 0; p < P; ++p) {
-        const uint32_t sl = it + p, st = sl % SSTAGES;
-        mbar_wait(empty + st, ((sl / SSTAGES) & 1) ^ 1);
-        mbar_expect_tx(full + st, SSTAGE_BYTES);
-        for (int b = 0; b < 4; ++b)
-          tma_load_2d(base + st * SSTAGE_BYTES + b * SBOX_BYTES, &mp.g, m0 + 16 * b, (kb + p) * SBK, full + st);
+      if (lane == 0) {
+        for (int p = 0; p < P; ++p) {
+          const uint32_t sl = it + p, st = sl % SSTAGES;
+          mbar_wait(empty + st, ((sl / SSTAGES) & 1) ^ 1);
+          mbar_expect_tx(full + st, SSTAGE_BYTES);
+          for (int b = 0; b < 4; ++b)
+            tma_load_2d(base + st * SSTAGE_BYTES + b * SBOX_BYTES, &mp.g, m0 + 16 * b, (kb + p) * SBK, full + st);
+        }
       }
       if (!PANEL) {
-        if (k >= 3) wait_geq(cross + (k - 1) * T + tj, T);
-        if (k >= 4) wait_geq(cross + (k - 2) * T + ti, T);
+        // Fine-grained dependencies: this split reads rows [kb SBK, ke SBK) of column panel tj of
+        // W_{k-1}, i.e. only the step-(k-1) tiles (l, tj) / (tj, l) of the tile rows l it covers (not
+        // the whole cross tj), plus the unit's own tile of step k-1 (the epilogue's W_{k-1} and H).
+        // The in-place write of W_k over W_{k-3} at (ti, tj) and (tj, ti) still waits for crosses ti
+        // and tj of step k-2 (every reader of those W_{k-3} panels).
+        const int* tdone = cross + a.K * T + ntri;
+        const int l0 = (kb * SBK) / BM, l1e = (ke * SBK - 1) / BM, l1 = l1e < T - 1 ? l1e : T - 1;
+        const int* flag = nullptr;
+        int target = 0;
+        if (lane == 0 && k >= 4) { flag = cross + (k - 2) * T + ti; target = T; }
+        if (lane == 1 && k >= 4) { flag = cross + (k - 2) * T + tj; target = T; }
+        if (lane == 2 && k >= 3) { flag = tdone + (k - 1) * ntri + tile; target = 1; }
+        if (lane >= 3 && k >= 3 && l0 + lane - 3 <= l1) {
+          const int l = l0 + lane - 3;
+          flag = tdone + (k - 1) * ntri +
+                 (l >= tj ? tj * (2 * T - tj + 1) / 2 + (l - tj) : l * (2 * T - l + 1) / 2 + (tj - l));
+          target = 1;
+        }
+        if (flag) wait_geq(flag, target);
+        __syncwarp();
       }
 #ifdef CPA_SYM_TRACE
-      if (tk < kTraceUnits) g_trace[tk * 6 + 2] = trace_now();
+      if (lane == 0 && tk < kTraceUnits) g_trace[tk * 6 + 2] = trace_now();
 #endif
-      fence_proxy_async_global();   // generic-proxy W_{k-1} stores of other CTAs -> TMA reads
-      for (int p = 0; p < P; ++p) {
-        const uint32_t st = (it + p) % SSTAGES;
-        for (int b = 0; b < 4; ++b)
-          tma_load_2d(base + st * SSTAGE_BYTES + (4 + b) * SBOX_BYTES, wmap, n0 + 16 * b, (kb + p) * SBK, full + st);
+      if (lane == 0) {
+        fence_proxy_async_global();   // generic-proxy W_{k-1} stores of other CTAs -> TMA reads
+        for (int p = 0; p < P; ++p) {
+          const uint32_t st = (it + p) % SSTAGES;
+          for (int b = 0; b < 4; ++b)
+            tma_load_2d(base + st * SSTAGE_BYTES + (4 + b) * SBOX_BYTES, wmap, n0 + 16 * b, (kb + p) * SBK,
+                        full + st);
+        }
       }
     }
     // The epilogue's generic loads of W_{k-1}, W_{k-2} and H must be ordered after thread 0's
@@ -1694,7 +1720,8 @@ static int sym_split(int64_t s, int slots, int64_t ntiles = -1) {
 size_t dense_sym_sync_ints(int64_t s, int K, int num_sms) {
   (void)num_sms;
   const int64_t T = (s + BM - 1) / BM;
-  return (size_t)(1 + (int64_t)K * T + T * (T + 1) / 2);
+  // [0] ticket | K * T cross counters | ntri split counters | K * ntri tile-done flags
+  return (size_t)(1 + (int64_t)K * T + T * (T + 1) / 2 + (int64_t)K * (T * (T + 1) / 2));
 }
 
 size_t dense_sym_partial_doubles(int64_t s, int num_sms) {
