@@ -387,7 +387,30 @@ struct SymArgs {
   // 64 x 64 -- the slot the all-gather exchanges.  H accumulates in place on the own tiles.
   int panel, kstep, tile0, ntile;
   double* gout;
+  // two-chain mode (chain = 1, see chain_buf): the products of step k = 2 .. K-1 are
+  //   k = 2:   Psi_2 = 2 B_hat Psi_1 - Psi_0                       (A = G, as the one-chain step)
+  //   k >= 3:  Psi_k = 2 Psi_2 Psi_{k-2} - Psi_{|k-4|}             (A = Psi_2 = T_2(B_hat))
+  // i.e. T_k = 2 T_2 T_{k-2} - T_{k-4}: the even and the odd Psi_k form two independent chains of
+  // the same K-2 products, so consecutive steps no longer depend on each other.  Buffers C[8]:
+  // [0] Psi_1 (from k_sym_init), [1] Psi_2, [2..4] odd rotation, [5..7] even rotation; the odd
+  // terms accumulate in H2 (H = H_even + H_odd, summed by the last product's epilogue).
+  int chain;
+  double* C[8];
+  double* H2;
 };
+
+// Buffer of Psi_k in two-chain mode (k >= 1): Psi_k overwrites Psi_{k-6} of its own chain.
+__host__ __device__ __forceinline__ int chain_buf(int k) {
+  return k == 1 ? 0 : k == 2 ? 1 : (k & 1) ? 2 + ((k - 3) >> 1) % 3 : 5 + ((k - 4) >> 1) % 3;
+}
+// sync layout of the symmetric kernels: [0] ticket | K * T cross counters | ntri (two chains:
+// 2 ntri, per tile and chain parity) split-K counters | K * ntri tile-done flags | product-2 count
+__host__ __device__ __forceinline__ int sym_split_off(int K, int T) { return 1 + K * T; }
+// (one chain: ntri split counters, the round-1 layout)
+__host__ __device__ __forceinline__ int sym_tdone_off(int K, int T, bool chain) {
+  return 1 + K * T + (chain ? T * (T + 1) : T * (T + 1) / 2);
+}
+__host__ __device__ __forceinline__ int sym_p2_off(int K, int T) { return 1 + K * T + T * (T + 1) + K * (T * (T + 1) / 2); }
 
 __global__ void k_sym_init(const double* __restrict__ G, int64_t s, double* __restrict__ W1, double* __restrict__ H,
                            const SeriesParams* __restrict__ P) {
@@ -500,13 +523,14 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
 
 // WS: run by the 128 epilogue threads (warps 4-7) of k_cheb_sym_ws, thread u = threadIdx.x - 128
 // playing the role of MMA thread u (same fragment positions), synchronised on named barrier 2.
-template <bool tma, bool WS, bool PANEL, int NW, class Acc>
+template <bool tma, bool WS, bool PANEL, int NW, bool CHAIN, class Acc>
 __device__ __forceinline__ void sym_finish_impl(const SymArgs& a, int k, int tile, int q, int ti, int tj, Acc&& acc) {
   const int T = a.T;
   const int S = a.split;
   int* cross = a.sync + 1;
-  int* split_cnt = a.sync + 1 + a.K * T;
+  int* split_cnt = a.sync + sym_split_off(a.K, T);
   const int64_t s = a.s;
+  const bool chain = CHAIN && a.chain;   // (CHAIN: compiled in; a.chain: this launch)
   // NW = 4: warps own 32 x 32 sub-tiles (WJ = 4 column fragments); NW = 8: 32 x 16 (WJ = 2)
   constexpr int NT = 32 * NW, WJ = NW == 4 ? 4 : 2, NV = 4 * WJ * 2;
   const int u = WS ? (int)threadIdx.x - NTHREADS : (int)threadIdx.x;
@@ -519,13 +543,21 @@ __device__ __forceinline__ void sym_finish_impl(const SymArgs& a, int k, int til
   const int wm = NW == 4 ? (warp >> 1) * 32 : (warp >> 2) * 32;
   const int wn = NW == 4 ? (warp & 1) * 32 : (warp & 3) * 16;
   auto buf = [&](int i) { return i == 0 ? a.W[0] : (i == 1 ? a.W[1] : a.W[2]); };
-  const double* src = buf((k - 1) % 3);   // W_{k-1}
-  const double* wpp = buf((k - 2) % 3);   // W_{k-2} (k = 2: identity, implicit)
-  double* out = buf(k % 3);               // W_k over W_{k-3}
+  // one chain: W_k = s4 (G W_{k-1}) - 2 W_{k-1} - W_{k-2}, over W_{k-3}
+  // two chains (k >= 3): Psi_k = 2 (Psi_2 Psi_{k-2}) - Psi_{|k-4|}, over Psi_{k-6}; k = 2 as one chain
+  const double* src = chain ? a.C[chain_buf(k == 2 ? 1 : k - 2)] : buf((k - 1) % 3);
+  const double* wpp = chain ? (k == 2 ? nullptr : k == 4 ? nullptr : a.C[chain_buf(k == 3 ? 1 : k - 4)])
+                            : buf((k - 2) % 3);   // (nullptr / k = 2: the identity, implicit)
+  double* out = chain ? a.C[chain_buf(k)] : buf(k % 3);
+  double* hmine = chain && (k & 1) ? a.H2 : a.H;
+  const double* hother = chain ? ((k & 1) ? a.H : a.H2) : nullptr;
   const int64_t m0 = (int64_t)ti * BM, n0 = (int64_t)tj * BN;
-  const int kc = PANEL ? 2 : k;         // split counters: per launch in panel mode (zeroed before it)
+  // split counters: per launch in panel mode (zeroed before it); per tile and chain parity with
+  // two chains (the products k and k + 1 of one tile may be in flight together)
+  const int kc = PANEL ? 2 : chain ? (k >> 1) + 1 : k;
+  const int sidx = chain ? 2 * tile + (k & 1) : tile;
   if (S > 1) {
-    double* slot = a.partial + (int64_t)(tile - (PANEL ? a.tile0 : 0)) * (S - 1) * (BM * BN);
+    double* slot = a.partial + (int64_t)(sidx - (PANEL ? a.tile0 : 0)) * (S - 1) * (BM * BN);
     CPA_DCHECK(tile - (PANEL ? a.tile0 : 0) >= 0 && tile < a.T * (a.T + 1) / 2);
     if (q < S - 1) {
       double* mine = slot + (int64_t)q * (BM * BN);
@@ -536,10 +568,10 @@ __device__ __forceinline__ void sym_finish_impl(const SymArgs& a, int k, int til
 #pragma unroll
           for (int e = 0; e < 2; ++e) __stcg(mine + ((i * WJ + j) * 2 + e) * NT + u, acc(i, j, e));
       group_sync();
-      if (u == 0) red_release_add_i32(split_cnt + tile, 1);
+      if (u == 0) red_release_add_i32(split_cnt + sidx, 1);
       return;
     }
-    if (u == 0) wait_geq(split_cnt + tile, (S - 1) * (kc - 1));
+    if (u == 0) wait_geq(split_cnt + sidx, (S - 1) * (kc - 1));
     group_sync();
     if (!WS) {
       double sum[NV];
@@ -583,6 +615,50 @@ __device__ __forceinline__ void sym_finish_impl(const SymArgs& a, int k, int til
   // fused epilogue on the elements r >= c of the tile
   const double s4 = 2.0 * a.P->scale2, ck = a.P->c[k];
   const bool last = k == a.K - 1;
+  if (CHAIN && chain && k >= 3) {
+    // Psi_k = 2 (Psi_2 Psi_{k-2}) - Psi_{|k-4|} (k = 4: Psi_0 = I); H_par(k) += c_k Psi_k, the odd
+    // sum starting at k = 3 from zero; the last product adds the other chain's sum (its tile of
+    // step K-2 is complete: a dependency of this unit) and writes H mirrored.  Psi_k is stored
+    // only while a later product reads it (k <= K-3).
+    const bool store_w = k <= a.K - 3;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t rr = m0 + wm + i * 8 + g;
+      double vpp[2 * WJ], vy[2 * WJ], vo[2 * WJ];
+#pragma unroll
+      for (int j = 0; j < WJ; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t c = n0 + wn + j * 8 + 2 * t + e;
+          const bool ok = rr < s && c <= rr;
+          const int64_t o = rr * s + c;
+          vpp[j * 2 + e] = k == 4 ? (rr == c ? 1.0 : 0.0) : (ok ? __ldcg(wpp + o) : 0.0);
+          vy[j * 2 + e] = (k == 3 || !ok) ? 0.0 : __ldcg(hmine + o);
+          vo[j * 2 + e] = (last && ok) ? __ldcg(hother + o) : 0.0;
+        }
+#pragma unroll
+      for (int j = 0; j < WJ; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t c = n0 + wn + j * 8 + 2 * t + e;
+          if (!(rr < s && c <= rr)) continue;
+          const int qq = j * 2 + e;
+          const double wv = 2.0 * acc(i, j, e) - vpp[qq];
+          const double y = vy[qq] + ck * wv;
+          if (store_w) {
+            out[rr * s + c] = wv;
+            out[c * s + rr] = wv;
+          }
+          if (last) {
+            const double yh = y + vo[qq];
+            a.H[rr * s + c] = yh;
+            a.H[c * s + rr] = yh;
+          } else {
+            hmine[rr * s + c] = y;
+          }
+        }
+    }
+  } else {
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int64_t rr = m0 + wm + i * 8 + g;
@@ -621,6 +697,7 @@ __device__ __forceinline__ void sym_finish_impl(const SymArgs& a, int k, int til
         if (last) a.H[c * s + rr] = y;
       }
   }
+  }
   if (PANEL) {   // (the launch boundary orders the stores; no crosses to release)
     group_sync();
     return;
@@ -630,15 +707,16 @@ __device__ __forceinline__ void sym_finish_impl(const SymArgs& a, int k, int til
   if (u == 0) {
     red_release_add_i32(cross + k * T + ti, 1);
     if (ti != tj) red_release_add_i32(cross + k * T + tj, 1);
-    red_release_add_i32(cross + a.K * T + T * (T + 1) / 2 + k * (T * (T + 1) / 2) + tile, 1);   // tile done
+    red_release_add_i32(a.sync + sym_tdone_off(a.K, T, chain) + k * (T * (T + 1) / 2) + tile, 1);   // tile done
+    if (CHAIN && chain && k == 2) red_release_add_i32(a.sync + sym_p2_off(a.K, T), 1);   // Psi_2 progress
   }
 }
 
 // k_cheb_sym / k_cheb_sym_tma: the accumulators in registers
-template <bool tma, bool PANEL, int NW = 4>
+template <bool tma, bool PANEL, int NW = 4, bool CHAIN = false>
 __device__ __forceinline__ void sym_finish(const SymArgs& a, int k, int tile, int q, int ti, int tj,
                                            double (&acc)[4][NW == 4 ? 4 : 2][2]) {
-  sym_finish_impl<tma, false, PANEL, NW>(a, k, tile, q, ti, tj,
+  sym_finish_impl<tma, false, PANEL, NW, CHAIN>(a, k, tile, q, ti, tj,
                                          [&](int i, int j, int e) -> double& { return acc[i][j][e]; });
 }
 
@@ -704,6 +782,13 @@ struct SymMaps {
   CUtensorMap g;
   CUtensorMap w[3];
 };
+struct SymMapsChain {   // two-chain mode: plus the maps of SymArgs::C
+  CUtensorMap g;
+  CUtensorMap w[3];
+  CUtensorMap c[8];
+};
+template <bool CHAIN>
+using SymMapsT = typename std::conditional<CHAIN, SymMapsChain, SymMaps>::type;
 // SBK-deep slabs in an SSTAGES ring: <16, 4> (64 KB) for short units (c2: ~11 slabs each),
 // <32, 2> (64 KB, half the mbarrier round trips) for long ones (s >= 4096: c5 shape 608 ->
 // 586 ms; at c2 it costs 1.27 -> 1.39 ms).
@@ -728,9 +813,9 @@ __device__ __forceinline__ uint64_t smid_now() {
 }
 #endif
 
-template <int SBK, int SSTAGES, bool PANEL, int NW = 4>
+template <int SBK, int SSTAGES, bool PANEL, int NW = 4, bool CHAIN = false>
 __global__ void __launch_bounds__(32 * NW, CPA_FLOW_MINB)
-    k_cheb_sym_tma(const __grid_constant__ SymMaps mp, SymArgs a) {
+    k_cheb_sym_tma(const __grid_constant__ SymMapsT<CHAIN> mp, SymArgs a) {
   constexpr int SBOX_BYTES = 16 * SBK * 8;
   constexpr int SSTAGE_BYTES = 8 * SBOX_BYTES;
   extern __shared__ unsigned char tsm_raw[];
@@ -791,51 +876,108 @@ __global__ void __launch_bounds__(32 * NW, CPA_FLOW_MINB)
     int ti, tj;
     tri_decode_colmajor(tile, T, ti, tj);
     CPA_DCHECK(ti >= 0 && ti < T && tj >= 0 && tj <= ti);
-    const CUtensorMap* wmap = &mp.w[(k - 1) % 3];   // W_{k-1}
+    // B operand: W_{k-1} (one chain) / Psi_{k-2} (two chains, k >= 3; Psi_1 at k = 2); A operand:
+    // the static G, or Psi_2 for the two-chain products k >= 3
+    const CUtensorMap* wmap;
+    const CUtensorMap* amap;
+    if constexpr (CHAIN) {
+      wmap = &mp.c[chain_buf(k == 2 ? 1 : k - 2)];
+      amap = k >= 3 ? &mp.c[1] : &mp.g;
+    } else {
+      wmap = &mp.w[(k - 1) % 3];
+      amap = &mp.g;
+    }
     const int m0 = ti * BM, n0 = tj * BN;
     const int kb = (int)((int64_t)nk * q / S), ke = (int)((int64_t)nk * (q + 1) / S);
     const int nku = ke - kb;
     if (warp == 0) {
-      // prologue: lane 0 issues the static G slabs; meanwhile the lanes poll the unit's dependency
-      // flags in parallel (one flag per lane: each satisfied wait costs one L2 round trip, not one
-      // per flag); after the warp barrier lane 0 issues the W_{k-1} slabs
+      // prologue: lane 0 issues the A slabs when they are static (G; Psi_2 once complete) while the
+      // lanes poll the unit's dependency flags in parallel (each satisfied wait costs one L2 round
+      // trip, not one per flag); after the warp barrier lane 0 issues the B slabs (and late A slabs)
       const int P = nku < SSTAGES - 1 ? nku : SSTAGES - 1;
-      if (lane == 0) {
+      bool a_early = true;
+      if (CHAIN && k >= 3) {
+        const int v = lane == 0 ? ld_acquire(a.sync + sym_p2_off(a.K, T)) : 0;
+        a_early = __shfl_sync(0xffffffffu, v, 0) >= ntri;
+      }
+      auto issue_a = [&] {
         for (int p = 0; p < P; ++p) {
           const uint32_t sl = it + p, st = sl % SSTAGES;
           mbar_wait(empty + st, ((sl / SSTAGES) & 1) ^ 1);
           mbar_expect_tx(full + st, SSTAGE_BYTES);
           for (int b = 0; b < 4; ++b)
-            tma_load_2d(base + st * SSTAGE_BYTES + b * SBOX_BYTES, &mp.g, m0 + 16 * b, (kb + p) * SBK, full + st);
+            tma_load_2d(base + st * SSTAGE_BYTES + b * SBOX_BYTES, amap, m0 + 16 * b, (kb + p) * SBK, full + st);
         }
-      }
+      };
+      if (lane == 0 && a_early) issue_a();
       if (!PANEL) {
         // Fine-grained dependencies: this split reads rows [kb SBK, ke SBK) of column panel tj of
-        // W_{k-1}, i.e. only the step-(k-1) tiles (l, tj) / (tj, l) of the tile rows l it covers (not
-        // the whole cross tj), plus the unit's own tile of step k-1 (the epilogue's W_{k-1} and H).
-        // The in-place write of W_k over W_{k-3} at (ti, tj) and (tj, ti) still waits for crosses ti
-        // and tj of step k-2 (every reader of those W_{k-3} panels).
-        const int* tdone = cross + a.K * T + ntri;
+        // its B operand, i.e. only the tiles (l, tj) / (tj, l) of the tile rows l it covers (not the
+        // whole cross tj), plus the unit's own tile of the previous step of its chain (the
+        // epilogue's W / H reads).  The in-place write over W_{k-3} (two chains: Psi_{k-6}) at
+        // (ti, tj) and (tj, ti) still waits for crosses ti and tj of step k-2 (k-4): every reader
+        // of those panels.  Two chains add: the A rows of Psi_2 (tiles (ti, l) of step 2) for k = 3,
+        // 4 -- implied for k >= 5 by the own tile of step k-2 -- and, for the last product, the own
+        // tile of step K-2 (the other chain's H).  Flags are polled lane-strided, any count.
+        const int* tdone = a.sync + sym_tdone_off(a.K, T, CHAIN);
         const int l0 = (kb * SBK) / BM, l1e = (ke * SBK - 1) / BM, l1 = l1e < T - 1 ? l1e : T - 1;
-        const int* flag = nullptr;
-        int target = 0;
-        if (lane == 0 && k >= 4) { flag = cross + (k - 2) * T + ti; target = T; }
-        if (lane == 1 && k >= 4) { flag = cross + (k - 2) * T + tj; target = T; }
-        if (lane == 2 && k >= 3) { flag = tdone + (k - 1) * ntri + tile; target = 1; }
-        if (lane >= 3 && k >= 3 && l0 + lane - 3 <= l1) {
-          const int l = l0 + lane - 3;
-          flag = tdone + (k - 1) * ntri +
-                 (l >= tj ? tj * (2 * T - tj + 1) / 2 + (l - tj) : l * (2 * T - l + 1) / 2 + (tj - l));
-          target = 1;
+        const int nl = l1 - l0 + 1;
+        auto tri_idx = [&](int r, int c) { return c * (2 * T - c + 1) / 2 + (r - c); };   // r >= c
+        const int kprev = CHAIN ? k - 2 : k - 1;    // the step whose tiles are B (and own tile)
+        const int khaz = CHAIN ? (k >= 9 ? k - 4 : 0) : (k >= 4 ? k - 2 : 0);
+        const bool need_b = CHAIN ? k >= 4 : k >= 3;
+        const bool need_a = CHAIN && k >= 3 && k <= 4 && !a_early;
+        const bool need_h = CHAIN && k == a.K - 1;
+        // flag list: [0, 1] crosses ti, tj of khaz | [2] own tile of kprev | [3] own tile of K-2
+        // (two chains, last product) | B tiles l0..l1 | A tiles l0..l1
+        if (!CHAIN) {
+          // one chain (the round-1/2 lane layout, kept instruction for instruction: this kernel's
+          // claim-to-start path is measurably sensitive to code changes): lanes 0, 1 crosses ti, tj
+          // of step k-2, lane 2 the own tile of step k-1, lanes 3.. the B tiles (29 per pass)
+          const int* flag = nullptr;
+          int target = 0;
+          if (lane == 0 && k >= 4) { flag = cross + (k - 2) * T + ti; target = T; }
+          if (lane == 1 && k >= 4) { flag = cross + (k - 2) * T + tj; target = T; }
+          if (lane == 2 && k >= 3) { flag = tdone + (k - 1) * ntri + tile; target = 1; }
+          if (lane >= 3 && k >= 3 && l0 + lane - 3 <= l1) {
+            const int l = l0 + lane - 3;
+            flag = tdone + (k - 1) * ntri + (l >= tj ? tri_idx(l, tj) : tri_idx(tj, l));
+            target = 1;
+            if (l1 - l0 > 28) {   // (more B tile rows than lanes: the whole cross tj instead)
+              flag = cross + (k - 1) * T + tj;
+              target = T;
+            }
+          }
+          if (flag) wait_geq(flag, target);
+        } else {
+          const int nflags = 4 + nl + (need_a ? nl : 0);
+          for (int f = lane; f < nflags; f += 32) {
+            const int* flag = nullptr;
+            int target = 1;
+            if (f < 2) {
+              if (khaz) { flag = cross + khaz * T + (f == 0 ? ti : tj); target = T; }
+            } else if (f == 2) {
+              if (need_b) flag = tdone + kprev * ntri + tile;
+            } else if (f == 3) {
+              if (need_h) flag = tdone + (a.K - 2) * ntri + tile;
+            } else if (f < 4 + nl) {
+              const int l = l0 + f - 4;
+              if (need_b) flag = tdone + kprev * ntri + (l >= tj ? tri_idx(l, tj) : tri_idx(tj, l));
+            } else {
+              const int l = l0 + f - 4 - nl;
+              flag = tdone + 2 * ntri + (l >= ti ? tri_idx(l, ti) : tri_idx(ti, l));
+            }
+            if (flag) wait_geq(flag, target);
+          }
         }
-        if (flag) wait_geq(flag, target);
         __syncwarp();
       }
 #ifdef CPA_SYM_TRACE
       if (lane == 0 && tk < kTraceUnits) g_trace[tk * 6 + 2] = trace_now();
 #endif
       if (lane == 0) {
-        fence_proxy_async_global();   // generic-proxy W_{k-1} stores of other CTAs -> TMA reads
+        fence_proxy_async_global();   // generic-proxy W stores of other CTAs -> TMA reads
+        if (!a_early) issue_a();
         for (int p = 0; p < P; ++p) {
           const uint32_t st = (it + p) % SSTAGES;
           for (int b = 0; b < 4; ++b)
@@ -862,7 +1004,7 @@ __global__ void __launch_bounds__(32 * NW, CPA_FLOW_MINB)
         mbar_wait(empty + st, ((sl / SSTAGES) & 1) ^ 1);
         mbar_expect_tx(full + st, SSTAGE_BYTES);
         unsigned char* d = base + st * SSTAGE_BYTES;
-        for (int b = 0; b < 4; ++b) tma_load_2d(d + b * SBOX_BYTES, &mp.g, m0 + 16 * b, (kb + kn) * SBK, full + st);
+        for (int b = 0; b < 4; ++b) tma_load_2d(d + b * SBOX_BYTES, amap, m0 + 16 * b, (kb + kn) * SBK, full + st);
         for (int b = 0; b < 4; ++b)
           tma_load_2d(d + (4 + b) * SBOX_BYTES, wmap, n0 + 16 * b, (kb + kn) * SBK, full + st);
       }
@@ -898,7 +1040,7 @@ __global__ void __launch_bounds__(32 * NW, CPA_FLOW_MINB)
 #ifdef CPA_SYM_TRACE
     if (threadIdx.x == 0 && tk < kTraceUnits) g_trace[tk * 6 + 3] = trace_now();
 #endif
-    sym_finish<true, PANEL, NW>(a, k, tile, q, ti, tj, acc);
+    sym_finish<true, PANEL, NW, CHAIN>(a, k, tile, q, ti, tj, acc);
 #ifdef CPA_SYM_TRACE
     if (threadIdx.x == 0 && tk < kTraceUnits) g_trace[tk * 6 + 4] = trace_now();
 #endif
@@ -971,7 +1113,7 @@ __global__ void __launch_bounds__(2 * NTHREADS, 2)
       // the accumulators stay in the staging buffer (read where used: the register budget of the
       // 2-CTA kernel); the buffer is released after the unit
       double* stg = stage + b * (BM * BN);
-      sym_finish_impl<true, true, false, 4>(a, mt.k, mt.tile, mt.q, mt.ti, mt.tj, [&](int i, int j, int e) -> double& {
+      sym_finish_impl<true, true, false, 4, false>(a, mt.k, mt.tile, mt.q, mt.ti, mt.tj, [&](int i, int j, int e) -> double& {
         return stg[((i * 4 + j) * 2 + e) * NTHREADS + u];
       });
       __syncwarp();
@@ -1720,14 +1862,33 @@ static int sym_split(int64_t s, int slots, int64_t ntiles = -1) {
 size_t dense_sym_sync_ints(int64_t s, int K, int num_sms) {
   (void)num_sms;
   const int64_t T = (s + BM - 1) / BM;
-  // [0] ticket | K * T cross counters | ntri split counters | K * ntri tile-done flags
-  return (size_t)(1 + (int64_t)K * T + T * (T + 1) / 2 + (int64_t)K * (T * (T + 1) / 2));
+  // [0] ticket | K * T cross counters | 2 * ntri split counters | K * ntri tile-done flags | Psi_2 count
+  return (size_t)(1 + (int64_t)K * T + T * (T + 1) + (int64_t)K * (T * (T + 1) / 2) + 1);
 }
 
-size_t dense_sym_partial_doubles(int64_t s, int num_sms) {
+// Two-chain mode (SymArgs::chain) for the one-launch recurrence: on by default while the lower
+// tiles of one step leave the resident slots short of work (the latency-bound regime, c2);
+// CPA_SVT_SYM_CHAIN=0/1 forces it.  Needs K >= 6 (two chains of at least two products).
+bool dense_sym_use_chain(int64_t s, int K, int num_sms) {
+  if (K < 6 || s % 2 != 0 || s > INT32_MAX / 2 || env_on("CPA_SVT_SYM_NOTMA")) return false;
+  if (const char* v = getenv("CPA_SVT_SYM_CHAIN"); v && *v) return atoi(v) != 0;
   const int64_t T = (s + BM - 1) / BM;
-  const int S = sym_split(s, sym_slots(num_sms));
-  return S > 1 ? (size_t)(T * (T + 1) / 2 * (S - 1) * BM * BN) : 0;
+  return T * (T + 1) / 2 < 4 * (int64_t)sym_slots(num_sms);
+}
+
+static int sym_split_mode(int64_t s, int slots, bool chain) {
+  const int64_t T = (s + BM - 1) / BM;
+  int S = sym_split(s, slots, chain ? T * (T + 1) : -1);
+  if (chain) {
+    if (const char* v = getenv("CPA_SVT_CHAIN_SPLIT")) S = (atoi(v) > 0 && atoi(v) <= 16) ? atoi(v) : S;
+  }
+  return S;
+}
+
+size_t dense_sym_partial_doubles(int64_t s, int num_sms, bool chain) {
+  const int64_t T = (s + BM - 1) / BM;
+  const int S = sym_split_mode(s, sym_slots(num_sms), chain);
+  return S > 1 ? (size_t)(T * (T + 1) / 2 * (chain ? 2 : 1) * (S - 1) * BM * BN) : 0;
 }
 
 // W_1 = B_hat (into W1 when K > 2) and H = c_0/2 I + c_1 W_1.
@@ -1741,16 +1902,23 @@ cudaError_t dense_sym_init(int64_t s, const double* G, double* W1, double* H, co
 static cudaError_t sym_launch(SymArgs& a, int64_t total, int slots, int num_sms, cudaStream_t st);
 
 // H_hat += sum_{k=2}^{K-1} c_k Psi_k(B_hat) on the s x s Gram: one persistent launch
-// for all K-2 steps.  W0, W1, W2: s x s buffers, W1 = W_1 from dense_sym_init.
+// for all K-2 steps.  W0, W1, W2: s x s buffers, W1 = W_1 from dense_sym_init.  Two-chain mode
+// (chain != nullptr: eight s x s buffers, chain[0] = W1 = Psi_1, plus H2 for the odd terms).
 cudaError_t dense_cheb_sym(int64_t s, const double* G, double* W0, double* W1, double* W2, double* H,
-                           const SeriesParams* P, int K, int* sync, double* partial, int num_sms, cudaStream_t st) {
+                           const SeriesParams* P, int K, int* sync, double* partial, int num_sms, cudaStream_t st,
+                           double* const* chain, double* H2) {
   if (s == 0 || K <= 2) return cudaSuccess;
   SymArgs a{};
   a.s = s; a.G = G; a.W[0] = W0; a.W[1] = W1; a.W[2] = W2; a.H = H; a.P = P; a.K = K;
   a.T = (int)((s + BM - 1) / BM);
+  a.chain = chain != nullptr && H2 != nullptr;
+  if (a.chain) {
+    for (int i = 0; i < 8; ++i) a.C[i] = chain[i];
+    a.H2 = H2;
+  }
   const size_t smem = sym_smem();
   const int slots = sym_slots(num_sms);
-  a.split = sym_split(s, slots);
+  a.split = sym_split_mode(s, slots, a.chain);
   a.sync = sync;
   a.partial = partial;
   a.vec = aligned16(G, s) && aligned16(W0, s) && aligned16(W1, s) && aligned16(W2, s);
@@ -1758,7 +1926,7 @@ cudaError_t dense_cheb_sym(int64_t s, const double* G, double* W0, double* W1, d
   if (e != cudaSuccess) return e;
   int cs = 0;
   if (const char* v = getenv("CPA_SVT_SYM_CLUSTER")) cs = atoi(v);
-  if (a.split > 1 && (cs == 2 || cs == 4 || cs == 8)) {
+  if (a.split > 1 && (cs == 2 || cs == 4 || cs == 8) && !a.chain) {
     // small s: CS-CTA clusters, k-splits reduced through distributed shared memory
     auto go = [&](auto kern, int CS) -> cudaError_t {
       cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1788,12 +1956,18 @@ static cudaError_t sym_launch(SymArgs& a, int64_t total, int slots, int num_sms,
   if (!env_on("CPA_SVT_SYM_NOTMA") && s % 2 == 0 && s <= INT32_MAX / 2) {
     // one fp64 tensor map per operand (16 x 16 boxes, 128-byte swizzle)
     EncodeTiledFn fn = encode_fn();
+    SymMapsChain mpc;
     SymMaps mp;
     bool ok = fn != nullptr;
     const int sbk = s >= 4096 ? 32 : 16;   // slab depth of the k_cheb_sym_tma instance (see there)
-    const double* ops[4] = {a.G, a.W[0], a.W[1], a.W[2]};
-    CUtensorMap* maps[4] = {&mp.g, &mp.w[0], &mp.w[1], &mp.w[2]};
-    for (int i = 0; i < 4 && ok; ++i) {
+    const double* ops[12] = {a.G, a.W[0], a.W[1], a.W[2]};
+    CUtensorMap* maps[12] = {&mpc.g, &mpc.w[0], &mpc.w[1], &mpc.w[2]};
+    const int nmaps = a.chain ? 12 : 4;
+    for (int i = 0; i < 8 && a.chain; ++i) {
+      ops[4 + i] = a.C[i];
+      maps[4 + i] = &mpc.c[i];
+    }
+    for (int i = 0; i < nmaps && ok; ++i) {
       cuuint64_t dims[2] = {(cuuint64_t)s, (cuuint64_t)s};
       cuuint64_t strides[1] = {(cuuint64_t)(s * sizeof(double))};
       cuuint32_t box[2] = {16u, (cuuint32_t)sbk};
@@ -1802,7 +1976,9 @@ static cudaError_t sym_launch(SymArgs& a, int64_t total, int slots, int num_sms,
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
     }
-    if (ok && env_on("CPA_SVT_SYM_WS") && !a.panel) {
+    mp.g = mpc.g;
+    for (int i = 0; i < 3; ++i) mp.w[i] = mpc.w[i];
+    if (ok && env_on("CPA_SVT_SYM_WS") && !a.panel && !a.chain) {
       // warp-specialized kernel: 3 x 16-deep (48 KB) or 2 x 32-deep (64 KB) ring + 64 KB staging, 2 CTAs per SM
       const size_t wsmem = (sbk == 32 ? (size_t)2 * 8 * (16 * 32 * 8) : (size_t)3 * 8 * (16 * 16 * 8)) +
                            (size_t)2 * BM * BN * 8 + 1024;   // (+ header and alignment: see k_cheb_sym_ws)
@@ -1829,10 +2005,13 @@ static cudaError_t sym_launch(SymArgs& a, int64_t total, int slots, int num_sms,
       // both instances use a 64 KB ring: 4 x 16-deep or 2 x 32-deep stages
       const size_t tsmem = (size_t)4 * 8 * (16 * 16 * 8) + 1024;
       const int nw = (getenv("CPA_SVT_SYM_NW") && atoi(getenv("CPA_SVT_SYM_NW")) == 8) ? 8 : 4;
-      auto kf = nw == 8 ? (a.panel ? (sbk == 32 ? k_cheb_sym_tma<32, 2, true, 8> : k_cheb_sym_tma<16, 4, true, 8>)
-                                   : (sbk == 32 ? k_cheb_sym_tma<32, 2, false, 8> : k_cheb_sym_tma<16, 4, false, 8>))
-                        : (a.panel ? (sbk == 32 ? k_cheb_sym_tma<32, 2, true> : k_cheb_sym_tma<16, 4, true>)
-                                   : (sbk == 32 ? k_cheb_sym_tma<32, 2, false> : k_cheb_sym_tma<16, 4, false>));
+      const void* kf =
+          a.chain ? (sbk == 32 ? (const void*)k_cheb_sym_tma<32, 2, false, 4, true>
+                               : (const void*)k_cheb_sym_tma<16, 4, false, 4, true>)
+                  : (const void*)(nw == 8 ? (a.panel ? (sbk == 32 ? k_cheb_sym_tma<32, 2, true, 8> : k_cheb_sym_tma<16, 4, true, 8>)
+                                     : (sbk == 32 ? k_cheb_sym_tma<32, 2, false, 8> : k_cheb_sym_tma<16, 4, false, 8>))
+                          : (a.panel ? (sbk == 32 ? k_cheb_sym_tma<32, 2, true> : k_cheb_sym_tma<16, 4, true>)
+                                     : (sbk == 32 ? k_cheb_sym_tma<32, 2, false> : k_cheb_sym_tma<16, 4, false>)));
       e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
       if (e != cudaSuccess) return e;
       e = cudaFuncSetAttribute(kf, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
@@ -1843,10 +2022,11 @@ static cudaError_t sym_launch(SymArgs& a, int64_t total, int slots, int num_sms,
       if (env_on("CPA_SVT_DEBUG_OCC")) fprintf(stderr, "k_cheb_sym_tma<%d,NW=%d>: %d CTAs/SM\n", sbk, nw, per_sm);
       int64_t tgrid = (int64_t)num_sms * per_sm;
       if (tgrid > total) tgrid = total;
-      void* targs[] = {&mp, &a};
+      void* targs[] = {a.chain ? (void*)&mpc : (void*)&mp, &a};
       return cudaLaunchCooperativeKernel((void*)kf, dim3((unsigned)tgrid), dim3(32 * nw), targs, tsmem, st);
     }
   }
+  if (a.chain) return cudaErrorInvalidValue;   // (two chains: TMA kernel only; dense_sym_use_chain)
   void* args[] = {&a};
   return cudaLaunchCooperativeKernel(a.panel ? (void*)k_cheb_sym<true> : (void*)k_cheb_sym<false>, dim3((unsigned)grid),
                                      dim3(NTHREADS), args, smem, st);

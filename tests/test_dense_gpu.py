@@ -355,6 +355,7 @@ def test_warp_specialized_recurrence_bitwise(env, s, L, K, split):
     out = {}
     if split:
         os.environ["CPA_SVT_FLOW_SPLIT"] = str(split)
+    os.environ["CPA_SVT_SYM_CHAIN"] = "0"   # (the one-chain kernel is the bitwise reference)
     try:
         for ws in ("0", "1"):
             os.environ["CPA_SVT_SYM_WS"] = ws
@@ -364,6 +365,7 @@ def test_warp_specialized_recurrence_bitwise(env, s, L, K, split):
     finally:
         os.environ.pop("CPA_SVT_SYM_WS", None)
         os.environ.pop("CPA_SVT_FLOW_SPLIT", None)
+        os.environ.pop("CPA_SVT_SYM_CHAIN", None)
     assert np.array_equal(out["0"], out["1"])
     if s <= 1100:
         assert O.rel_fro(out["1"], O.cpa_shrink(X, O.Kernel(**kern), K, T=100)) <= TOL64
@@ -383,6 +385,7 @@ def test_eight_warp_recurrence_bitwise(env, s, L, K, split):
     out = {}
     if split:
         os.environ["CPA_SVT_FLOW_SPLIT"] = str(split)
+    os.environ["CPA_SVT_SYM_CHAIN"] = "0"   # (the one-chain kernel is the bitwise reference)
     try:
         for nw in ("4", "8"):
             os.environ["CPA_SVT_SYM_NW"] = nw
@@ -392,6 +395,44 @@ def test_eight_warp_recurrence_bitwise(env, s, L, K, split):
     finally:
         os.environ.pop("CPA_SVT_SYM_NW", None)
         os.environ.pop("CPA_SVT_FLOW_SPLIT", None)
+        os.environ.pop("CPA_SVT_SYM_CHAIN", None)
     assert np.array_equal(out["4"], out["8"])
     if s <= 1100:
         assert O.rel_fro(out["8"], O.cpa_shrink(X, O.Kernel(**kern), K, T=100)) <= TOL64
+
+
+@pytest.mark.parametrize("s,L,K,split", [(1024, 1024, 30, 0), (1024, 1100, 31, 0), (1024, 1024, 6, 2), (1024, 1030, 7, 3),
+                                         (256, 300, 8, 1), (256, 260, 9, 2), (130, 300, 10, 0), (130, 140, 11, 5),
+                                         (64, 200, 12, 1), (1538, 1600, 13, 4), (2048, 2100, 20, 0), (512, 520, 40, 6)])
+def test_two_chain_recurrence(env, s, L, K, split):
+    """Two-chain symmetric recurrence (Psi_k = 2 Psi_2 Psi_{k-2} - Psi_{|k-4|}: the even and the odd
+    Chebyshev terms as two independent chains, reading R26) against the oracle's one-chain Alg. 1
+     at the fp64 bar, against the one-chain kernel at rounding level, run-to-run
+    deterministic, and H_hat exactly symmetric; K - 1 even and odd (which chain's product sums H),
+    every k-split count."""
+    import os
+    torch, P, _ = env
+    X = W.gen_c2(m=s, n=L, seed=s + K + 7)
+    kern = {"kind": "soft", "tau": 0.05, "tau_relative": True}
+    Xd = torch.from_numpy(X).cuda()
+    out = {}
+    if split:
+        os.environ["CPA_SVT_CHAIN_SPLIT"] = str(split)
+    try:
+        for ch in ("1", "0"):
+            os.environ["CPA_SVT_SYM_CHAIN"] = ch
+            h2 = P.Handle(0)
+            h2.set_form("poly")
+            out[ch] = h2.apply(Xd, kern, K, T=100).cpu().numpy()
+            if ch == "1":
+                out["again"] = h2.apply(Xd, kern, K, T=100).cpu().numpy()
+                out["eye"] = h2.apply(torch.eye(s, dtype=torch.float64, device="cuda"), kern, K, T=60).cpu().numpy()
+            h2.close()
+    finally:
+        os.environ.pop("CPA_SVT_SYM_CHAIN", None)
+        os.environ.pop("CPA_SVT_CHAIN_SPLIT", None)
+    assert np.array_equal(out["1"], out["again"])
+    assert np.array_equal(out["eye"], out["eye"].T)
+    assert O.rel_fro(out["1"], out["0"]) <= 1e-12
+    if s <= 1100:
+        assert O.rel_fro(out["1"], O.cpa_shrink(X, O.Kernel(**kern), K, T=100)) <= TOL64

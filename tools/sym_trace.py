@@ -26,7 +26,8 @@ for _ in range(3):
 torch.cuda.synchronize()
 h.apply(X, kern, 30, T=300)
 torch.cuda.synchronize()
-T, S, K = 16, 6, 30
+T, K = 16, 30
+S = int(os.environ.get("TRACE_S", "6"))   # the k-splits of the launch (two chains at c2: 3)
 units = (K - 2) * T * (T + 1) // 2 * S
 buf = np.zeros(units * 6, dtype=np.uint64)
 assert P.lib.cpa_svt_debug_sym_trace(buf.ctypes.data, units) == 0
