@@ -69,13 +69,13 @@ cudaError_t dense_cheb_sym_panel(int64_t s, const double* G, double* W0, double*
                                  const SeriesParams* P, int K, int kstep, int64_t tile0, int64_t ntile,
                                  double* gout, int* sync, double* partial, int num_sms, cudaStream_t st);
 cudaError_t dense_sym_unpack(const double* gbuf, int64_t s, int P, double* out, cudaStream_t st);
-size_t dense_sym_partial_doubles(int64_t s, int num_sms, bool chain);
-bool dense_sym_use_chain(int64_t s, int K, int num_sms);
+size_t dense_sym_partial_doubles(int64_t s, int num_sms, int m);
+int dense_sym_use_chain(int64_t s, int K, int num_sms);
 cudaError_t dense_sym_init(int64_t s, const double* G, double* Wa, double* H, const SeriesParams* P, int K,
                            int num_sms, cudaStream_t st);
 cudaError_t dense_cheb_sym(int64_t s, const double* G, double* W0, double* W1, double* W2, double* H,
                            const SeriesParams* P, int K, int* sync, double* partial, int num_sms, cudaStream_t st,
-                           double* const* chain = nullptr, double* H2 = nullptr);
+                           int m = 0, double* const* chain = nullptr, double* const* HX = nullptr);
 cudaError_t dense_cheb_flow(bool left, int64_t m, int64_t n, const double* G, const double* X, int64_t ldx,
                             double* Wa, double* Wb, double* Y, int64_t ldy, const SeriesParams* P, int K, int* sync,
                             double* partial, int num_sms, cudaStream_t st);
@@ -818,10 +818,10 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
   auto r32 = [](size_t v) { return (v + 31) / 32 * 32; };
   const size_t nG = r32((size_t)s * s), nW = r32((size_t)RM * RN), nPow = r32(power_dense_scratch_doubles(s));
   const size_t nX = poly ? 2 * nG : 0;
-  // two-chain recurrence (form 2, one launch): six more s x s buffers (Psi_2, the two chains'
-  // rotations beside Wa / Wb / Is, and the odd-term sum H2)
-  const bool chain = form == 2 && !panels && !sparse_eps && dense_sym_use_chain(s, K, h->num_sms);
-  const size_t nCh = chain ? 6 * nG : 0;
+  // m-chain recurrence (form 2, one launch): 4m - 3 + m - 1 more s x s buffers (Psi_2 .. Psi_m, the
+  // chains' rotations beside Wa / Wb / Is, the accumulators HX of all chains but the first)
+  const int chain = form == 2 && !panels && !sparse_eps ? dense_sym_use_chain(s, K, h->num_sms) : 0;
+  const size_t nCh = chain ? (size_t)(5 * chain - 4) * nG : 0;
   const bool final_split = !env_on("CPA_SVT_FINAL_NOSPLIT");  // line-12 product split-K (default on)
   const size_t nPart = r32(std::max({dense_flow_partial_doubles(RM, RN, h->num_sms), dense_gram_partial_doubles(s),
                                      form == 2 ? dense_sym_partial_doubles(s, h->num_sms, chain) : (size_t)0,
@@ -1017,10 +1017,17 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
           }
         } else {
           Phase p(h, CPA_SVT_PH_STEP);
-          if (chain) {   // Psi_1 (Wa, from the init) | Psi_2 | odd rotation | even rotation; H2
-            double* cb[8] = {Wa, chb, Wb, Is, chb + nG, chb + 2 * nG, chb + 3 * nG, chb + 4 * nG};
-            CU(dense_cheb_sym(s, G, Is, Wa, Wb, H, h->P, K, flow_sync, part, h->num_sms, h->stream, cb,
-                              chb + 5 * nG));
+          if (chain) {   // Psi_1 (Wa, from the init) | Psi_2 .. Psi_m | rotations (Wb, Is, then chb); HX
+            double* cb[12];
+            cb[0] = Wa;
+            double* nxt = chb;
+            for (int i = 1; i < 4 * chain; ++i) {
+              if (i == chain) cb[i] = Wb;
+              else if (i == chain + 1) cb[i] = Is;
+              else { cb[i] = nxt; nxt += nG; }
+            }
+            double* hx[2] = {nxt, nxt + nG};
+            CU(dense_cheb_sym(s, G, Is, Wa, Wb, H, h->P, K, flow_sync, part, h->num_sms, h->stream, chain, cb, hx));
           } else {
             CU(dense_cheb_sym(s, G, Is, Wa, Wb, H, h->P, K, flow_sync, part, h->num_sms, h->stream));  // Is: 3rd W buffer
           }

@@ -387,30 +387,35 @@ struct SymArgs {
   // 64 x 64 -- the slot the all-gather exchanges.  H accumulates in place on the own tiles.
   int panel, kstep, tile0, ntile;
   double* gout;
-  // two-chain mode (chain = 1, see chain_buf): the products of step k = 2 .. K-1 are
-  //   k = 2:   Psi_2 = 2 B_hat Psi_1 - Psi_0                       (A = G, as the one-chain step)
-  //   k >= 3:  Psi_k = 2 Psi_2 Psi_{k-2} - Psi_{|k-4|}             (A = Psi_2 = T_2(B_hat))
-  // i.e. T_k = 2 T_2 T_{k-2} - T_{k-4}: the even and the odd Psi_k form two independent chains of
-  // the same K-2 products, so consecutive steps no longer depend on each other.  Buffers C[8]:
-  // [0] Psi_1 (from k_sym_init), [1] Psi_2, [2..4] odd rotation, [5..7] even rotation; the odd
-  // terms accumulate in H2 (H = H_even + H_odd, summed by the last product's epilogue).
+  // m-chain mode (chain = m = 2 or 3, see chain_buf): the products of step k = 2 .. K-1 are
+  //   k = 2 .. m:  Psi_k = 2 B_hat Psi_{k-1} - Psi_{k-2}                 (A = G: the one-chain step)
+  //   k > m:       Psi_k = 2 Psi_m Psi_{k-m} - Psi_{|k-2m|}              (A = Psi_m = T_m(B_hat))
+  // i.e. T_k = 2 T_m T_{k-m} - T_{|k-2m|}: the Psi_k of each residue k mod m form an independent
+  // chain of the same K-2 products, so consecutive steps no longer depend on each other.  Buffers
+  // C[4m]: [j-1] Psi_j for j = 1..m (Psi_1 from k_sym_init), then three rotation buffers per chain;
+  // the terms of residue (k-2) mod m = j accumulate in H (j = 0, with the init's c_0/2 I + c_1 Psi_1)
+  // or HX[j-1] (from zero), summed by the last product's epilogue.
   int chain;
-  double* C[8];
-  double* H2;
+  double* C[12];
+  double* HX[2];
+  int red_bias;         // chains: the reducing split's k-range is (100 + red_bias)% of the others'
 };
 
-// Buffer of Psi_k in two-chain mode (k >= 1): Psi_k overwrites Psi_{k-6} of its own chain.
-__host__ __device__ __forceinline__ int chain_buf(int k) {
-  return k == 1 ? 0 : k == 2 ? 1 : (k & 1) ? 2 + ((k - 3) >> 1) % 3 : 5 + ((k - 4) >> 1) % 3;
+// Buffer of Psi_k in m-chain mode (k >= 1): Psi_k overwrites Psi_{k-3m} of its own chain.
+__host__ __device__ __forceinline__ int chain_buf(int k, int m) {
+  if (k <= m) return k - 1;
+  const int r = (k - m - 1) % m, idx = (k - m - 1) / m;
+  return m + 3 * r + idx % 3;
 }
-// sync layout of the symmetric kernels: [0] ticket | K * T cross counters | ntri (two chains:
-// 2 ntri, per tile and chain parity) split-K counters | K * ntri tile-done flags | product-2 count
+// sync layout of the symmetric kernels: [0] ticket | K * T cross counters | ntri split-K counters
+// (m chains: m ntri, per tile and chain) | K * ntri tile-done flags | product-m tile count
 __host__ __device__ __forceinline__ int sym_split_off(int K, int T) { return 1 + K * T; }
-// (one chain: ntri split counters, the round-1 layout)
-__host__ __device__ __forceinline__ int sym_tdone_off(int K, int T, bool chain) {
-  return 1 + K * T + (chain ? T * (T + 1) : T * (T + 1) / 2);
+__host__ __device__ __forceinline__ int sym_tdone_off(int K, int T, int m) {
+  return 1 + K * T + (m > 1 ? m : 1) * (T * (T + 1) / 2);
 }
-__host__ __device__ __forceinline__ int sym_p2_off(int K, int T) { return 1 + K * T + T * (T + 1) + K * (T * (T + 1) / 2); }
+__host__ __device__ __forceinline__ int sym_pm_off(int K, int T, int m) {
+  return sym_tdone_off(K, T, m) + K * (T * (T + 1) / 2);
+}
 
 __global__ void k_sym_init(const double* __restrict__ G, int64_t s, double* __restrict__ W1, double* __restrict__ H,
                            const SeriesParams* __restrict__ P) {
@@ -523,14 +528,15 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
 
 // WS: run by the 128 epilogue threads (warps 4-7) of k_cheb_sym_ws, thread u = threadIdx.x - 128
 // playing the role of MMA thread u (same fragment positions), synchronised on named barrier 2.
-template <bool tma, bool WS, bool PANEL, int NW, bool CHAIN, class Acc>
+template <bool tma, bool WS, bool PANEL, int NW, int CH, class Acc>
 __device__ __forceinline__ void sym_finish_impl(const SymArgs& a, int k, int tile, int q, int ti, int tj, Acc&& acc) {
   const int T = a.T;
   const int S = a.split;
   int* cross = a.sync + 1;
   int* split_cnt = a.sync + sym_split_off(a.K, T);
   const int64_t s = a.s;
-  const bool chain = CHAIN && a.chain;   // (CHAIN: compiled in; a.chain: this launch)
+  constexpr bool CHAIN = CH > 1;          // m-chain instance (CH = m; one chain: CH = 0)
+  constexpr bool chain = CHAIN;
   // NW = 4: warps own 32 x 32 sub-tiles (WJ = 4 column fragments); NW = 8: 32 x 16 (WJ = 2)
   constexpr int NT = 32 * NW, WJ = NW == 4 ? 4 : 2, NV = 4 * WJ * 2;
   const int u = WS ? (int)threadIdx.x - NTHREADS : (int)threadIdx.x;
@@ -544,18 +550,24 @@ __device__ __forceinline__ void sym_finish_impl(const SymArgs& a, int k, int til
   const int wn = NW == 4 ? (warp & 1) * 32 : (warp & 3) * 16;
   auto buf = [&](int i) { return i == 0 ? a.W[0] : (i == 1 ? a.W[1] : a.W[2]); };
   // one chain: W_k = s4 (G W_{k-1}) - 2 W_{k-1} - W_{k-2}, over W_{k-3}
-  // two chains (k >= 3): Psi_k = 2 (Psi_2 Psi_{k-2}) - Psi_{|k-4|}, over Psi_{k-6}; k = 2 as one chain
-  const double* src = chain ? a.C[chain_buf(k == 2 ? 1 : k - 2)] : buf((k - 1) % 3);
-  const double* wpp = chain ? (k == 2 ? nullptr : k == 4 ? nullptr : a.C[chain_buf(k == 3 ? 1 : k - 4)])
-                            : buf((k - 2) % 3);   // (nullptr / k = 2: the identity, implicit)
-  double* out = chain ? a.C[chain_buf(k)] : buf(k % 3);
-  double* hmine = chain && (k & 1) ? a.H2 : a.H;
-  const double* hother = chain ? ((k & 1) ? a.H : a.H2) : nullptr;
+  // m chains, k > m: Psi_k = 2 (Psi_m Psi_{k-m}) - Psi_{|k-2m|}, over Psi_{k-3m}; k <= m as one chain
+  constexpr int mc = CHAIN ? CH : 1;
+  const bool cstep = chain && k > mc;   // a chain product (A = Psi_m)
+  const double* src = chain ? a.C[chain_buf(cstep ? k - mc : k - 1, mc)] : buf((k - 1) % 3);
+  const double* wpp;                    // (nullptr: the identity Psi_0, implicit)
+  if (!chain) wpp = buf((k - 2) % 3);
+  else if (!cstep) wpp = k == 2 ? nullptr : a.C[chain_buf(k - 2, mc)];
+  else wpp = k == 2 * mc ? nullptr : a.C[chain_buf(k > 2 * mc ? k - 2 * mc : 2 * mc - k, mc)];
+  double* out = chain ? a.C[chain_buf(k, mc)] : buf(k % 3);
+  const int hj = chain ? (k - 2) % mc : 0;            // accumulator of this product's chain
+  double* hmine = hj == 0 ? a.H : a.HX[hj - 1];
+  const bool hzero = chain && hj > 0 && k == 2 + hj;  // first term of an HX accumulator
   const int64_t m0 = (int64_t)ti * BM, n0 = (int64_t)tj * BN;
-  // split counters: per launch in panel mode (zeroed before it); per tile and chain parity with
-  // two chains (the products k and k + 1 of one tile may be in flight together)
-  const int kc = PANEL ? 2 : chain ? (k >> 1) + 1 : k;
-  const int sidx = chain ? 2 * tile + (k & 1) : tile;
+  // split counters: per launch in panel mode (zeroed before it); per tile and chain with m chains
+  // (consecutive products of one tile may be in flight together); kc - 1 = the product's ordinal
+  // among those of its tile and chain
+  const int kc = PANEL ? 2 : chain ? (k - 2 - hj) / mc + 2 : k;
+  const int sidx = chain ? mc * tile + hj : tile;
   if (S > 1) {
     double* slot = a.partial + (int64_t)(sidx - (PANEL ? a.tile0 : 0)) * (S - 1) * (BM * BN);
     CPA_DCHECK(tile - (PANEL ? a.tile0 : 0) >= 0 && tile < a.T * (a.T + 1) / 2);
@@ -615,16 +627,17 @@ __device__ __forceinline__ void sym_finish_impl(const SymArgs& a, int k, int til
   // fused epilogue on the elements r >= c of the tile
   const double s4 = 2.0 * a.P->scale2, ck = a.P->c[k];
   const bool last = k == a.K - 1;
-  if (CHAIN && chain && k >= 3) {
-    // Psi_k = 2 (Psi_2 Psi_{k-2}) - Psi_{|k-4|} (k = 4: Psi_0 = I); H_par(k) += c_k Psi_k, the odd
-    // sum starting at k = 3 from zero; the last product adds the other chain's sum (its tile of
-    // step K-2 is complete: a dependency of this unit) and writes H mirrored.  Psi_k is stored
-    // only while a later product reads it (k <= K-3).
-    const bool store_w = k <= a.K - 3;
+  if (CHAIN && chain) {
+    // chain product (k > m): Psi_k = 2 (Psi_m Psi_{k-m}) - Psi_{|k-2m|} (Psi_0 = I); a G step
+    // (k <= m): the one-chain update.  H_j += c_k Psi_k for the product's chain j (HX from zero at
+    // its first term); the last product adds the other chains' sums (their last tiles are complete:
+    // dependencies of this unit) and writes H mirrored.  Psi_k is stored only while a later
+    // product reads it (k + m <= K - 1).
+    const bool store_w = k + mc <= a.K - 1;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int64_t rr = m0 + wm + i * 8 + g;
-      double vpp[2 * WJ], vy[2 * WJ], vo[2 * WJ];
+      double vp[2 * WJ], vpp[2 * WJ], vy[2 * WJ];
 #pragma unroll
       for (int j = 0; j < WJ; ++j)
 #pragma unroll
@@ -632,9 +645,13 @@ __device__ __forceinline__ void sym_finish_impl(const SymArgs& a, int k, int til
           const int64_t c = n0 + wn + j * 8 + 2 * t + e;
           const bool ok = rr < s && c <= rr;
           const int64_t o = rr * s + c;
-          vpp[j * 2 + e] = k == 4 ? (rr == c ? 1.0 : 0.0) : (ok ? __ldcg(wpp + o) : 0.0);
-          vy[j * 2 + e] = (k == 3 || !ok) ? 0.0 : __ldcg(hmine + o);
-          vo[j * 2 + e] = (last && ok) ? __ldcg(hother + o) : 0.0;
+          vp[j * 2 + e] = (!cstep && ok) ? __ldcg(src + o) : 0.0;
+          vpp[j * 2 + e] = wpp == nullptr ? (rr == c ? 1.0 : 0.0) : (ok ? __ldcg(wpp + o) : 0.0);
+          double y0 = (hzero || !ok) ? 0.0 : __ldcg(hmine + o);
+          if (last && ok)
+            for (int jj = 0; jj < mc; ++jj)
+              if (jj != hj) y0 += __ldcg((jj == 0 ? a.H : a.HX[jj - 1]) + o);
+          vy[j * 2 + e] = y0;
         }
 #pragma unroll
       for (int j = 0; j < WJ; ++j)
@@ -643,16 +660,15 @@ __device__ __forceinline__ void sym_finish_impl(const SymArgs& a, int k, int til
           const int64_t c = n0 + wn + j * 8 + 2 * t + e;
           if (!(rr < s && c <= rr)) continue;
           const int qq = j * 2 + e;
-          const double wv = 2.0 * acc(i, j, e) - vpp[qq];
+          const double wv = cstep ? 2.0 * acc(i, j, e) - vpp[qq] : s4 * acc(i, j, e) - 2.0 * vp[qq] - vpp[qq];
           const double y = vy[qq] + ck * wv;
           if (store_w) {
             out[rr * s + c] = wv;
             out[c * s + rr] = wv;
           }
           if (last) {
-            const double yh = y + vo[qq];
-            a.H[rr * s + c] = yh;
-            a.H[c * s + rr] = yh;
+            a.H[rr * s + c] = y;
+            a.H[c * s + rr] = y;
           } else {
             hmine[rr * s + c] = y;
           }
@@ -707,16 +723,16 @@ __device__ __forceinline__ void sym_finish_impl(const SymArgs& a, int k, int til
   if (u == 0) {
     red_release_add_i32(cross + k * T + ti, 1);
     if (ti != tj) red_release_add_i32(cross + k * T + tj, 1);
-    red_release_add_i32(a.sync + sym_tdone_off(a.K, T, chain) + k * (T * (T + 1) / 2) + tile, 1);   // tile done
-    if (CHAIN && chain && k == 2) red_release_add_i32(a.sync + sym_p2_off(a.K, T), 1);   // Psi_2 progress
+    red_release_add_i32(a.sync + sym_tdone_off(a.K, T, mc) + k * (T * (T + 1) / 2) + tile, 1);   // tile done
+    if (CHAIN && chain && k == mc) red_release_add_i32(a.sync + sym_pm_off(a.K, T, mc), 1);   // Psi_m progress
   }
 }
 
 // k_cheb_sym / k_cheb_sym_tma: the accumulators in registers
-template <bool tma, bool PANEL, int NW = 4, bool CHAIN = false>
+template <bool tma, bool PANEL, int NW = 4, int CH = 0>
 __device__ __forceinline__ void sym_finish(const SymArgs& a, int k, int tile, int q, int ti, int tj,
                                            double (&acc)[4][NW == 4 ? 4 : 2][2]) {
-  sym_finish_impl<tma, false, PANEL, NW, CHAIN>(a, k, tile, q, ti, tj,
+  sym_finish_impl<tma, false, PANEL, NW, CH>(a, k, tile, q, ti, tj,
                                          [&](int i, int j, int e) -> double& { return acc[i][j][e]; });
 }
 
@@ -782,13 +798,13 @@ struct SymMaps {
   CUtensorMap g;
   CUtensorMap w[3];
 };
-struct SymMapsChain {   // two-chain mode: plus the maps of SymArgs::C
+struct SymMapsChain {   // m-chain mode: plus the maps of SymArgs::C
   CUtensorMap g;
   CUtensorMap w[3];
-  CUtensorMap c[8];
+  CUtensorMap c[12];
 };
-template <bool CHAIN>
-using SymMapsT = typename std::conditional<CHAIN, SymMapsChain, SymMaps>::type;
+template <int CH>
+using SymMapsT = typename std::conditional<(CH > 1), SymMapsChain, SymMaps>::type;
 // SBK-deep slabs in an SSTAGES ring: <16, 4> (64 KB) for short units (c2: ~11 slabs each),
 // <32, 2> (64 KB, half the mbarrier round trips) for long ones (s >= 4096: c5 shape 608 ->
 // 586 ms; at c2 it costs 1.27 -> 1.39 ms).
@@ -813,9 +829,10 @@ __device__ __forceinline__ uint64_t smid_now() {
 }
 #endif
 
-template <int SBK, int SSTAGES, bool PANEL, int NW = 4, bool CHAIN = false>
+template <int SBK, int SSTAGES, bool PANEL, int NW = 4, int CH = 0>
 __global__ void __launch_bounds__(32 * NW, CPA_FLOW_MINB)
-    k_cheb_sym_tma(const __grid_constant__ SymMapsT<CHAIN> mp, SymArgs a) {
+    k_cheb_sym_tma(const __grid_constant__ SymMapsT<CH> mp, SymArgs a) {
+  constexpr bool CHAIN = CH > 1;
   constexpr int SBOX_BYTES = 16 * SBK * 8;
   constexpr int SSTAGE_BYTES = 8 * SBOX_BYTES;
   extern __shared__ unsigned char tsm_raw[];
@@ -876,28 +893,35 @@ __global__ void __launch_bounds__(32 * NW, CPA_FLOW_MINB)
     int ti, tj;
     tri_decode_colmajor(tile, T, ti, tj);
     CPA_DCHECK(ti >= 0 && ti < T && tj >= 0 && tj <= ti);
-    // B operand: W_{k-1} (one chain) / Psi_{k-2} (two chains, k >= 3; Psi_1 at k = 2); A operand:
-    // the static G, or Psi_2 for the two-chain products k >= 3
+    // B operand: W_{k-1} (one chain; a G step of the m-chain mode: Psi_{k-1}) / Psi_{k-m} (a chain
+    // product, k > m); A operand: the static G, or Psi_m for the chain products
+    constexpr int mc = CHAIN ? CH : 1;
+    const bool cstep = CHAIN && k > mc;
     const CUtensorMap* wmap;
     const CUtensorMap* amap;
     if constexpr (CHAIN) {
-      wmap = &mp.c[chain_buf(k == 2 ? 1 : k - 2)];
-      amap = k >= 3 ? &mp.c[1] : &mp.g;
+      wmap = &mp.c[chain_buf(cstep ? k - mc : k - 1, mc)];
+      amap = cstep ? &mp.c[mc - 1] : &mp.g;
     } else {
       wmap = &mp.w[(k - 1) % 3];
       amap = &mp.g;
     }
     const int m0 = ti * BM, n0 = tj * BN;
-    const int kb = (int)((int64_t)nk * q / S), ke = (int)((int64_t)nk * (q + 1) / S);
+    int kb = (int)((int64_t)nk * q / S), ke = (int)((int64_t)nk * (q + 1) / S);
+    if (CHAIN) {   // the reducer (q = S - 1) starts last and sums the others: a longer k-range
+      const int64_t wt = 100 * S + a.red_bias;
+      kb = (int)((int64_t)nk * q * 100 / wt);
+      ke = q == S - 1 ? nk : (int)((int64_t)nk * (q + 1) * 100 / wt);
+    }
     const int nku = ke - kb;
     if (warp == 0) {
-      // prologue: lane 0 issues the A slabs when they are static (G; Psi_2 once complete) while the
+      // prologue: lane 0 issues the A slabs when they are static (G; Psi_m once complete) while the
       // lanes poll the unit's dependency flags in parallel (each satisfied wait costs one L2 round
       // trip, not one per flag); after the warp barrier lane 0 issues the B slabs (and late A slabs)
       const int P = nku < SSTAGES - 1 ? nku : SSTAGES - 1;
       bool a_early = true;
-      if (CHAIN && k >= 3) {
-        const int v = lane == 0 ? ld_acquire(a.sync + sym_p2_off(a.K, T)) : 0;
+      if (cstep) {
+        const int v = lane == 0 ? ld_acquire(a.sync + sym_pm_off(a.K, T, mc)) : 0;
         a_early = __shfl_sync(0xffffffffu, v, 0) >= ntri;
       }
       auto issue_a = [&] {
@@ -914,22 +938,25 @@ __global__ void __launch_bounds__(32 * NW, CPA_FLOW_MINB)
         // Fine-grained dependencies: this split reads rows [kb SBK, ke SBK) of column panel tj of
         // its B operand, i.e. only the tiles (l, tj) / (tj, l) of the tile rows l it covers (not the
         // whole cross tj), plus the unit's own tile of the previous step of its chain (the
-        // epilogue's W / H reads).  The in-place write over W_{k-3} (two chains: Psi_{k-6}) at
-        // (ti, tj) and (tj, ti) still waits for crosses ti and tj of step k-2 (k-4): every reader
-        // of those panels.  Two chains add: the A rows of Psi_2 (tiles (ti, l) of step 2) for k = 3,
-        // 4 -- implied for k >= 5 by the own tile of step k-2 -- and, for the last product, the own
-        // tile of step K-2 (the other chain's H).  Flags are polled lane-strided, any count.
-        const int* tdone = a.sync + sym_tdone_off(a.K, T, CHAIN);
+        // epilogue's W / H reads).  The in-place write over W_{k-3} (m chains: Psi_{k-3m}) at
+        // (ti, tj) and (tj, ti) still waits for crosses ti and tj of step k-2 (k-2m): every reader
+        // of those panels.  m chains add, for the chain products k <= 2m: the own tile of step m
+        // (it implies the G steps' own tiles: the epilogue's Psi_{2m-k}) and, unless Psi_m is
+        // complete, the A rows of Psi_m (tiles (ti, l) of step m) -- both implied for k > 2m by the
+        // own tile of step k-m; for the last product, the own tiles of steps K-2 .. K-m (the other
+        // chains' H).  Flags are polled lane-strided, any count.
+        const int* tdone = a.sync + sym_tdone_off(a.K, T, mc);
         const int l0 = (kb * SBK) / BM, l1e = (ke * SBK - 1) / BM, l1 = l1e < T - 1 ? l1e : T - 1;
         const int nl = l1 - l0 + 1;
         auto tri_idx = [&](int r, int c) { return c * (2 * T - c + 1) / 2 + (r - c); };   // r >= c
-        const int kprev = CHAIN ? k - 2 : k - 1;    // the step whose tiles are B (and own tile)
-        const int khaz = CHAIN ? (k >= 9 ? k - 4 : 0) : (k >= 4 ? k - 2 : 0);
-        const bool need_b = CHAIN ? k >= 4 : k >= 3;
-        const bool need_a = CHAIN && k >= 3 && k <= 4 && !a_early;
+        const int kprev = cstep ? k - mc : k - 1;   // the step whose tiles are B (and own tile)
+        const int khaz = cstep ? (k >= 4 * mc + 1 ? k - 2 * mc : 0) : 0;
+        const bool need_b = kprev >= 2;
+        const bool need_m = cstep && k <= 2 * mc;
+        const bool need_a = need_m && !a_early;
         const bool need_h = CHAIN && k == a.K - 1;
-        // flag list: [0, 1] crosses ti, tj of khaz | [2] own tile of kprev | [3] own tile of K-2
-        // (two chains, last product) | B tiles l0..l1 | A tiles l0..l1
+        // flag list: [0, 1] crosses ti, tj of khaz | [2] own tile of kprev | [3] own tile of step m |
+        // [4, 5] own tiles of steps K-2, K-3 (last product) | B tiles l0..l1 | A tiles l0..l1
         if (!CHAIN) {
           // one chain (the round-1/2 lane layout, kept instruction for instruction: this kernel's
           // claim-to-start path is measurably sensitive to code changes): lanes 0, 1 crosses ti, tj
@@ -950,7 +977,7 @@ __global__ void __launch_bounds__(32 * NW, CPA_FLOW_MINB)
           }
           if (flag) wait_geq(flag, target);
         } else {
-          const int nflags = 4 + nl + (need_a ? nl : 0);
+          const int nflags = 6 + nl + (need_a ? nl : 0);
           for (int f = lane; f < nflags; f += 32) {
             const int* flag = nullptr;
             int target = 1;
@@ -959,13 +986,15 @@ __global__ void __launch_bounds__(32 * NW, CPA_FLOW_MINB)
             } else if (f == 2) {
               if (need_b) flag = tdone + kprev * ntri + tile;
             } else if (f == 3) {
-              if (need_h) flag = tdone + (a.K - 2) * ntri + tile;
-            } else if (f < 4 + nl) {
-              const int l = l0 + f - 4;
+              if (need_m) flag = tdone + mc * ntri + tile;
+            } else if (f < 6) {
+              if (need_h && f - 3 < mc) flag = tdone + (a.K - 1 - (f - 3)) * ntri + tile;
+            } else if (f < 6 + nl) {
+              const int l = l0 + f - 6;
               if (need_b) flag = tdone + kprev * ntri + (l >= tj ? tri_idx(l, tj) : tri_idx(tj, l));
             } else {
-              const int l = l0 + f - 4 - nl;
-              flag = tdone + 2 * ntri + (l >= ti ? tri_idx(l, ti) : tri_idx(ti, l));
+              const int l = l0 + f - 6 - nl;
+              flag = tdone + mc * ntri + (l >= ti ? tri_idx(l, ti) : tri_idx(ti, l));
             }
             if (flag) wait_geq(flag, target);
           }
@@ -1040,7 +1069,7 @@ __global__ void __launch_bounds__(32 * NW, CPA_FLOW_MINB)
 #ifdef CPA_SYM_TRACE
     if (threadIdx.x == 0 && tk < kTraceUnits) g_trace[tk * 6 + 3] = trace_now();
 #endif
-    sym_finish<true, PANEL, NW, CHAIN>(a, k, tile, q, ti, tj, acc);
+    sym_finish<true, PANEL, NW, CH>(a, k, tile, q, ti, tj, acc);
 #ifdef CPA_SYM_TRACE
     if (threadIdx.x == 0 && tk < kTraceUnits) g_trace[tk * 6 + 4] = trace_now();
 #endif
@@ -1113,7 +1142,7 @@ __global__ void __launch_bounds__(2 * NTHREADS, 2)
       // the accumulators stay in the staging buffer (read where used: the register budget of the
       // 2-CTA kernel); the buffer is released after the unit
       double* stg = stage + b * (BM * BN);
-      sym_finish_impl<true, true, false, 4, false>(a, mt.k, mt.tile, mt.q, mt.ti, mt.tj, [&](int i, int j, int e) -> double& {
+      sym_finish_impl<true, true, false, 4, 0>(a, mt.k, mt.tile, mt.q, mt.ti, mt.tj, [&](int i, int j, int e) -> double& {
         return stg[((i * 4 + j) * 2 + e) * NTHREADS + u];
       });
       __syncwarp();
@@ -1862,33 +1891,35 @@ static int sym_split(int64_t s, int slots, int64_t ntiles = -1) {
 size_t dense_sym_sync_ints(int64_t s, int K, int num_sms) {
   (void)num_sms;
   const int64_t T = (s + BM - 1) / BM;
-  // [0] ticket | K * T cross counters | 2 * ntri split counters | K * ntri tile-done flags | Psi_2 count
-  return (size_t)(1 + (int64_t)K * T + T * (T + 1) + (int64_t)K * (T * (T + 1) / 2) + 1);
+  // [0] ticket | K * T cross counters | up to 3 ntri split counters (m chains) | K * ntri tile-done
+  // flags | Psi_m count
+  return (size_t)(1 + (int64_t)K * T + 3 * (T * (T + 1) / 2) + (int64_t)K * (T * (T + 1) / 2) + 1);
 }
 
-// Two-chain mode (SymArgs::chain) for the one-launch recurrence: on by default while the lower
-// tiles of one step leave the resident slots short of work (the latency-bound regime, c2);
-// CPA_SVT_SYM_CHAIN=0/1 forces it.  Needs K >= 6 (two chains of at least two products).
-bool dense_sym_use_chain(int64_t s, int K, int num_sms) {
-  if (K < 6 || s % 2 != 0 || s > INT32_MAX / 2 || env_on("CPA_SVT_SYM_NOTMA")) return false;
-  if (const char* v = getenv("CPA_SVT_SYM_CHAIN"); v && *v) return atoi(v) != 0;
+// m-chain mode (SymArgs::chain = m) for the one-launch recurrence: on by default (m = 2) while
+// the lower tiles of one step leave the resident slots short of work (the latency-bound regime,
+// c2); CPA_SVT_SYM_CHAIN=0|1 (off) / 2 / 3 forces it.  Needs K >= 2m + 2.  Returns m, 0 = off.
+int dense_sym_use_chain(int64_t s, int K, int num_sms) {
+  if (s % 2 != 0 || s > INT32_MAX / 2 || env_on("CPA_SVT_SYM_NOTMA")) return 0;
   const int64_t T = (s + BM - 1) / BM;
-  return T * (T + 1) / 2 < 4 * (int64_t)sym_slots(num_sms);
+  int m = T * (T + 1) / 2 < 4 * (int64_t)sym_slots(num_sms) ? 2 : 0;
+  if (const char* v = getenv("CPA_SVT_SYM_CHAIN"); v && *v) m = atoi(v) >= 2 && atoi(v) <= 3 ? atoi(v) : 0;
+  return K >= 2 * m + 2 ? m : 0;
 }
 
-static int sym_split_mode(int64_t s, int slots, bool chain) {
+static int sym_split_mode(int64_t s, int slots, int m) {
   const int64_t T = (s + BM - 1) / BM;
-  int S = sym_split(s, slots, chain ? T * (T + 1) : -1);
-  if (chain) {
+  int S = sym_split(s, slots, m > 1 ? m * (T * (T + 1) / 2) : -1);
+  if (m > 1) {
     if (const char* v = getenv("CPA_SVT_CHAIN_SPLIT")) S = (atoi(v) > 0 && atoi(v) <= 16) ? atoi(v) : S;
   }
   return S;
 }
 
-size_t dense_sym_partial_doubles(int64_t s, int num_sms, bool chain) {
+size_t dense_sym_partial_doubles(int64_t s, int num_sms, int m) {
   const int64_t T = (s + BM - 1) / BM;
-  const int S = sym_split_mode(s, sym_slots(num_sms), chain);
-  return S > 1 ? (size_t)(T * (T + 1) / 2 * (chain ? 2 : 1) * (S - 1) * BM * BN) : 0;
+  const int S = sym_split_mode(s, sym_slots(num_sms), m);
+  return S > 1 ? (size_t)(T * (T + 1) / 2 * (m > 1 ? m : 1) * (S - 1) * BM * BN) : 0;
 }
 
 // W_1 = B_hat (into W1 when K > 2) and H = c_0/2 I + c_1 W_1.
@@ -1902,19 +1933,21 @@ cudaError_t dense_sym_init(int64_t s, const double* G, double* W1, double* H, co
 static cudaError_t sym_launch(SymArgs& a, int64_t total, int slots, int num_sms, cudaStream_t st);
 
 // H_hat += sum_{k=2}^{K-1} c_k Psi_k(B_hat) on the s x s Gram: one persistent launch
-// for all K-2 steps.  W0, W1, W2: s x s buffers, W1 = W_1 from dense_sym_init.  Two-chain mode
-// (chain != nullptr: eight s x s buffers, chain[0] = W1 = Psi_1, plus H2 for the odd terms).
+// for all K-2 steps.  W0, W1, W2: s x s buffers, W1 = W_1 from dense_sym_init.  m-chain mode
+// (m > 1: 4m s x s buffers in chain, chain[0] = W1 = Psi_1, plus m - 1 accumulators HX).
 cudaError_t dense_cheb_sym(int64_t s, const double* G, double* W0, double* W1, double* W2, double* H,
                            const SeriesParams* P, int K, int* sync, double* partial, int num_sms, cudaStream_t st,
-                           double* const* chain, double* H2) {
+                           int m, double* const* chain, double* const* HX) {
   if (s == 0 || K <= 2) return cudaSuccess;
   SymArgs a{};
   a.s = s; a.G = G; a.W[0] = W0; a.W[1] = W1; a.W[2] = W2; a.H = H; a.P = P; a.K = K;
   a.T = (int)((s + BM - 1) / BM);
-  a.chain = chain != nullptr && H2 != nullptr;
+  a.chain = (m == 2 || m == 3) && chain != nullptr && HX != nullptr ? m : 0;
   if (a.chain) {
-    for (int i = 0; i < 8; ++i) a.C[i] = chain[i];
-    a.H2 = H2;
+    for (int i = 0; i < 4 * m; ++i) a.C[i] = chain[i];
+    for (int i = 0; i < m - 1; ++i) a.HX[i] = HX[i];
+    a.red_bias = 20;   // (c2 sweep: 0 / 10 / 20 / 35 / 50 -> 1.167 / 1.163 / 1.160 / 1.166 / 1.176 ms)
+    if (const char* v = getenv("CPA_SVT_RED_BIAS")) a.red_bias = atoi(v);
   }
   const size_t smem = sym_smem();
   const int slots = sym_slots(num_sms);
@@ -1960,10 +1993,10 @@ static cudaError_t sym_launch(SymArgs& a, int64_t total, int slots, int num_sms,
     SymMaps mp;
     bool ok = fn != nullptr;
     const int sbk = s >= 4096 ? 32 : 16;   // slab depth of the k_cheb_sym_tma instance (see there)
-    const double* ops[12] = {a.G, a.W[0], a.W[1], a.W[2]};
-    CUtensorMap* maps[12] = {&mpc.g, &mpc.w[0], &mpc.w[1], &mpc.w[2]};
-    const int nmaps = a.chain ? 12 : 4;
-    for (int i = 0; i < 8 && a.chain; ++i) {
+    const double* ops[16] = {a.G, a.W[0], a.W[1], a.W[2]};
+    CUtensorMap* maps[16] = {&mpc.g, &mpc.w[0], &mpc.w[1], &mpc.w[2]};
+    const int nmaps = 4 + 4 * a.chain;
+    for (int i = 0; i < 4 * a.chain; ++i) {
       ops[4 + i] = a.C[i];
       maps[4 + i] = &mpc.c[i];
     }
@@ -2006,8 +2039,10 @@ static cudaError_t sym_launch(SymArgs& a, int64_t total, int slots, int num_sms,
       const size_t tsmem = (size_t)4 * 8 * (16 * 16 * 8) + 1024;
       const int nw = (getenv("CPA_SVT_SYM_NW") && atoi(getenv("CPA_SVT_SYM_NW")) == 8) ? 8 : 4;
       const void* kf =
-          a.chain ? (sbk == 32 ? (const void*)k_cheb_sym_tma<32, 2, false, 4, true>
-                               : (const void*)k_cheb_sym_tma<16, 4, false, 4, true>)
+          a.chain == 3 ? (sbk == 32 ? (const void*)k_cheb_sym_tma<32, 2, false, 4, 3>
+                                    : (const void*)k_cheb_sym_tma<16, 4, false, 4, 3>)
+          : a.chain == 2 ? (sbk == 32 ? (const void*)k_cheb_sym_tma<32, 2, false, 4, 2>
+                                      : (const void*)k_cheb_sym_tma<16, 4, false, 4, 2>)
                   : (const void*)(nw == 8 ? (a.panel ? (sbk == 32 ? k_cheb_sym_tma<32, 2, true, 8> : k_cheb_sym_tma<16, 4, true, 8>)
                                      : (sbk == 32 ? k_cheb_sym_tma<32, 2, false, 8> : k_cheb_sym_tma<16, 4, false, 8>))
                           : (a.panel ? (sbk == 32 ? k_cheb_sym_tma<32, 2, true> : k_cheb_sym_tma<16, 4, true>)

@@ -401,15 +401,17 @@ def test_eight_warp_recurrence_bitwise(env, s, L, K, split):
         assert O.rel_fro(out["8"], O.cpa_shrink(X, O.Kernel(**kern), K, T=100)) <= TOL64
 
 
+@pytest.mark.parametrize("m", [2, 3])
 @pytest.mark.parametrize("s,L,K,split", [(1024, 1024, 30, 0), (1024, 1100, 31, 0), (1024, 1024, 6, 2), (1024, 1030, 7, 3),
                                          (256, 300, 8, 1), (256, 260, 9, 2), (130, 300, 10, 0), (130, 140, 11, 5),
-                                         (64, 200, 12, 1), (1538, 1600, 13, 4), (2048, 2100, 20, 0), (512, 520, 40, 6)])
-def test_two_chain_recurrence(env, s, L, K, split):
-    """Two-chain symmetric recurrence (Psi_k = 2 Psi_2 Psi_{k-2} - Psi_{|k-4|}: the even and the odd
-    Chebyshev terms as two independent chains, reading R26) against the oracle's one-chain Alg. 1
+                                         (64, 200, 12, 1), (1538, 1600, 13, 4), (2048, 2100, 20, 0), (512, 520, 40, 6),
+                                         (200, 210, 14, 2), (320, 330, 15, 3), (1024, 1024, 29, 2)])
+def test_two_chain_recurrence(env, m, s, L, K, split):
+    """m-chain symmetric recurrence (Psi_k = 2 Psi_m Psi_{k-m} - Psi_{|k-2m|}: the Chebyshev terms of
+    each residue k mod m as an independent chain, reading R28) against the oracle's one-chain Alg. 1
      at the fp64 bar, against the one-chain kernel at rounding level, run-to-run
-    deterministic, and H_hat exactly symmetric; K - 1 even and odd (which chain's product sums H),
-    every k-split count."""
+    deterministic, and H_hat exactly symmetric; every residue of K - 1 (which chain's product sums
+    H), every k-split count, and K below 2m + 2 (the library falls back to one chain)."""
     import os
     torch, P, _ = env
     X = W.gen_c2(m=s, n=L, seed=s + K + 7)
@@ -419,20 +421,21 @@ def test_two_chain_recurrence(env, s, L, K, split):
     if split:
         os.environ["CPA_SVT_CHAIN_SPLIT"] = str(split)
     try:
-        for ch in ("1", "0"):
+        for ch in (str(m), "0"):
             os.environ["CPA_SVT_SYM_CHAIN"] = ch
             h2 = P.Handle(0)
             h2.set_form("poly")
             out[ch] = h2.apply(Xd, kern, K, T=100).cpu().numpy()
-            if ch == "1":
+            if ch != "0":
                 out["again"] = h2.apply(Xd, kern, K, T=100).cpu().numpy()
                 out["eye"] = h2.apply(torch.eye(s, dtype=torch.float64, device="cuda"), kern, K, T=60).cpu().numpy()
             h2.close()
     finally:
         os.environ.pop("CPA_SVT_SYM_CHAIN", None)
         os.environ.pop("CPA_SVT_CHAIN_SPLIT", None)
-    assert np.array_equal(out["1"], out["again"])
+    Ym = out[str(m)]
+    assert np.array_equal(Ym, out["again"])
     assert np.array_equal(out["eye"], out["eye"].T)
-    assert O.rel_fro(out["1"], out["0"]) <= 1e-12
+    assert O.rel_fro(Ym, out["0"]) <= 1e-12
     if s <= 1100:
-        assert O.rel_fro(out["1"], O.cpa_shrink(X, O.Kernel(**kern), K, T=100)) <= TOL64
+        assert O.rel_fro(Ym, O.cpa_shrink(X, O.Kernel(**kern), K, T=100)) <= TOL64
