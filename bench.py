@@ -345,7 +345,9 @@ def run_ours(args, cfg):
     elif form == 2:
         kname = ("k_cheb_sym_tma (symmetric s x s recurrence, TMA-fed DMMA)" if cfg["math"] == "native"
                  else "k_tc_gemm (symmetric s x s recurrence step, tcgen05 " + cfg["math"] + ")")
-        rec_flops = (K - 2) * s_ * s_ * (s_ + 1) * (3 if cfg["math"] == "3xtf32" else 1)
+        # (K - 3 products when Psi_2 came from the power iteration's squaring, reading R29)
+        nprod = info0.get("rec_products") or (K - 2)
+        rec_flops = nprod * s_ * s_ * (s_ + 1) * (3 if cfg["math"] == "3xtf32" else 1)
     else:
         kname = "k_cheb_flow (fused apply-to-X recurrence, DMMA)"
         rec_flops = (K - 1) * 2 * s_ * s_ * (n_g // world if cfg["sharded"] else L_)

@@ -72,10 +72,11 @@ cudaError_t dense_sym_unpack(const double* gbuf, int64_t s, int P, double* out, 
 size_t dense_sym_partial_doubles(int64_t s, int num_sms, int m);
 int dense_sym_use_chain(int64_t s, int K, int num_sms);
 cudaError_t dense_sym_init(int64_t s, const double* G, double* Wa, double* H, const SeriesParams* P, int K,
-                           int num_sms, cudaStream_t st);
+                           int num_sms, cudaStream_t st, double* G2 = nullptr, const double* c2 = nullptr);
 cudaError_t dense_cheb_sym(int64_t s, const double* G, double* W0, double* W1, double* W2, double* H,
                            const SeriesParams* P, int K, int* sync, double* partial, int num_sms, cudaStream_t st,
-                           int m = 0, double* const* chain = nullptr, double* const* HX = nullptr);
+                           int m = 0, double* const* chain = nullptr, double* const* HX = nullptr,
+                           bool psi2_given = false);
 cudaError_t dense_cheb_flow(bool left, int64_t m, int64_t n, const double* G, const double* X, int64_t ldx,
                             double* Wa, double* Wb, double* Y, int64_t ldy, const SeriesParams* P, int K, int* sync,
                             double* partial, int num_sms, cudaStream_t st);
@@ -554,6 +555,7 @@ static cpa_svt_status fill_info(cpa_svt_handle* h, cpa_svt_info* info, cpa_svt_l
     info->tau_used = hp.tau;
     info->side = side;
     info->degenerate = hp.degenerate;
+    info->rec_products = 0;   // (set by the dense fp64 s x s path after this call)
   }
   if (lam && lam->want_lambda) {
     lam->lambda_hat = hp.lambda_hat;
@@ -841,8 +843,9 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
   double* part = pw + nPow;
   double* gbuf = part + nPart;    // panel mode: P all-gather slots of packed 64 x 64 tiles
   double* prs = gbuf + nGb;       // panel mode: row-sharded power iteration scratch
-  double* chb = prs + nPR;         // two-chain mode: 6 s x s buffers
+  double* chb = prs + nPR;         // m-chain mode: 5m - 4 s x s buffers
   int* flow_sync = (int*)(chb + nCh);
+  const double* psi2_sq = nullptr;  // m-chain mode: c^2 (device) when chb holds c^2 G^2
 
   const double* c_dev = nullptr;
   if (c) {
@@ -956,9 +959,13 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
     if (nsq > 0 && nW >= nG) {
       double* sc = pw + power_scale_offset(s);  // scale slot inside the power scratch
       CU(launch_diag_scale(G, s, sc, h->stream));
-      CU(dense_gram_f64(G, s, s, s, true, Wa, h->stream, sc, part, flow_sync));       // c^2 G^2
+      // m-chain mode: c^2 G^2 lands in the Psi_2 buffer, where the init turns it into Psi_2 =
+      // 2 B_hat^2 - I (the recurrence then starts at k = 3); the later squarings use Wa / Wb
+      double* first = (chain && K > 2 && !env_on("CPA_SVT_NO_PSI2_SQ")) ? chb : Wa;
+      CU(dense_gram_f64(G, s, s, s, true, first, h->stream, sc, part, flow_sync));    // c^2 G^2
       launches += 2;
-      G4 = Wa;
+      if (first == chb) psi2_sq = sc;
+      G4 = first;
       gpow = 2;
       for (int j = 1; j < nsq && 2 * gpow <= lam->power_iters - 1; ++j) {              // c^2p G^2p
         double* nxt = G4 == Wa ? Wb : Wa;
@@ -987,7 +994,7 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
     if (form == 2) {  // symmetric tiles (lower triangle computed, mirrored)
       {
         Phase p(h, CPA_SVT_PH_INIT);
-        CU(dense_sym_init(s, G, Wa, H, h->P, K, h->num_sms, h->stream));
+        CU(dense_sym_init(s, G, Wa, H, h->P, K, h->num_sms, h->stream, psi2_sq ? chb : nullptr, psi2_sq));
         ++launches;
       }
       if (K > 2) {
@@ -1027,7 +1034,8 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
               else { cb[i] = nxt; nxt += nG; }
             }
             double* hx[2] = {nxt, nxt + nG};
-            CU(dense_cheb_sym(s, G, Is, Wa, Wb, H, h->P, K, flow_sync, part, h->num_sms, h->stream, chain, cb, hx));
+            CU(dense_cheb_sym(s, G, Is, Wa, Wb, H, h->P, K, flow_sync, part, h->num_sms, h->stream, chain, cb, hx,
+                              psi2_sq != nullptr));
           } else {
             CU(dense_cheb_sym(s, G, Is, Wa, Wb, H, h->P, K, flow_sync, part, h->num_sms, h->stream));  // Is: 3rd W buffer
           }
@@ -1099,6 +1107,7 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
     info->ms_total = tm.ms(0, 4);
     info->kernel_launches = launches;
     info->form = form;
+    info->rec_products = poly && K > 2 ? K - (psi2_sq ? 3 : 2) : 0;
   }
   return st;
 }

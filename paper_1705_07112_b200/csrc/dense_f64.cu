@@ -399,6 +399,7 @@ struct SymArgs {
   double* C[12];
   double* HX[2];
   int red_bias;         // chains: the reducing split's k-range is (100 + red_bias)% of the others'
+  int k0;               // first step of the launch: 2, or 3 when Psi_2 is given (k_sym_init from G^2)
 };
 
 // Buffer of Psi_k in m-chain mode (k >= 1): Psi_k overwrites Psi_{k-3m} of its own chain.
@@ -415,6 +416,36 @@ __host__ __device__ __forceinline__ int sym_tdone_off(int K, int T, int m) {
 }
 __host__ __device__ __forceinline__ int sym_pm_off(int K, int T, int m) {
   return sym_tdone_off(K, T, m) + K * (T * (T + 1) / 2);
+}
+
+// Psi_2 from the power iteration's squaring (m-chain mode): G2 holds c^2 G^2 (c^2 = *c2, an exact
+// power of 2, k_diag_scale); Psi_2 = 2 B_hat^2 - I = 2 a^2 G^2 - 4 a G + I with a = 2/L (Alg. 1
+// line 9 at k = 2 with the product G G the squaring already formed), written over G2; and
+// H = c_0/2 I + c_1 Psi_1 + c_2 Psi_2.
+__global__ void k_sym_init2(const double* __restrict__ G, int64_t s, double* __restrict__ W1, double* G2,
+                            const double* __restrict__ c2, double* __restrict__ H, const SeriesParams* __restrict__ P) {
+  const double a = P->scale2, h0 = 0.5 * P->c[0], c1 = P->c[1], cc2 = P->c[2];
+  const double a2 = 2.0 * a * a / *c2, a4 = 4.0 * a;
+  const int64_t n = s * s;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const double id = (e / s == e % s) ? 1.0 : 0.0;
+    const double g = G[e];
+    const double w = a * g - id;                      // Psi_1 = B_hat = (2/L) G - I
+    const double p2 = a2 * G2[e] - a4 * g + id;       // Psi_2 = 2 B_hat^2 - I
+    W1[e] = w;
+    G2[e] = p2;
+    H[e] = h0 * id + c1 * w + cc2 * p2;
+  }
+}
+// the state of the sync array after step 2 (tile-done flags, the chain-0 split counters, the
+// Psi_2 count) when Psi_2 comes from k_sym_init2
+__global__ void k_sym_mark_step2(int* sync, int K, int T, int m, int S) {
+  const int ntri = T * (T + 1) / 2;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ntri; t += gridDim.x * blockDim.x) {
+    sync[sym_tdone_off(K, T, m) + 2 * ntri + t] = 1;
+    sync[sym_split_off(K, T) + m * t] = S - 1;
+    if (t == 0 && m == 2) sync[sym_pm_off(K, T, m)] = ntri;
+  }
 }
 
 __global__ void k_sym_init(const double* __restrict__ G, int64_t s, double* __restrict__ W1, double* __restrict__ H,
@@ -845,7 +876,7 @@ __global__ void __launch_bounds__(32 * NW, CPA_FLOW_MINB)
   const int ntri = T * (T + 1) / 2;
   const int S = a.split;
   const int per_step = (PANEL ? a.ntile : ntri) * S;
-  const int total = PANEL ? per_step : (a.K - 2) * per_step;
+  const int total = PANEL ? per_step : (a.K - (CH > 1 ? a.k0 : 2)) * per_step;
   int* cross = a.sync + 1;
   const int nk = (int)((a.s + SBK - 1) / SBK);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -886,7 +917,7 @@ __global__ void __launch_bounds__(32 * NW, CPA_FLOW_MINB)
     }
 #endif
     if (tk >= total) break;
-    const int k = PANEL ? a.kstep : 2 + tk / per_step;
+    const int k = PANEL ? a.kstep : (CH > 1 ? a.k0 : 2) + tk / per_step;
     const int r = tk % per_step;
     const int q = r % S;
     const int tile = r / S + (PANEL ? a.tile0 : 0);
@@ -1922,11 +1953,13 @@ size_t dense_sym_partial_doubles(int64_t s, int num_sms, int m) {
   return S > 1 ? (size_t)(T * (T + 1) / 2 * (m > 1 ? m : 1) * (S - 1) * BM * BN) : 0;
 }
 
-// W_1 = B_hat (into W1 when K > 2) and H = c_0/2 I + c_1 W_1.
+// W_1 = B_hat (into W1 when K > 2) and H = c_0/2 I + c_1 W_1; with G2 (c^2 G^2 from the power
+// iteration's first squaring, c^2 = *c2; K > 2): also Psi_2 over G2 and c_2 Psi_2 in H.
 cudaError_t dense_sym_init(int64_t s, const double* G, double* W1, double* H, const SeriesParams* P, int K,
-                           int num_sms, cudaStream_t st) {
+                           int num_sms, cudaStream_t st, double* G2, const double* c2) {
   if (s == 0) return cudaSuccess;
-  k_sym_init<<<num_sms * 4, 256, 0, st>>>(G, s, K > 2 ? W1 : nullptr, H, P);
+  if (G2 && K > 2) k_sym_init2<<<num_sms * 4, 256, 0, st>>>(G, s, W1, G2, c2, H, P);
+  else k_sym_init<<<num_sms * 4, 256, 0, st>>>(G, s, K > 2 ? W1 : nullptr, H, P);
   return cudaGetLastError();
 }
 
@@ -1937,7 +1970,7 @@ static cudaError_t sym_launch(SymArgs& a, int64_t total, int slots, int num_sms,
 // (m > 1: 4m s x s buffers in chain, chain[0] = W1 = Psi_1, plus m - 1 accumulators HX).
 cudaError_t dense_cheb_sym(int64_t s, const double* G, double* W0, double* W1, double* W2, double* H,
                            const SeriesParams* P, int K, int* sync, double* partial, int num_sms, cudaStream_t st,
-                           int m, double* const* chain, double* const* HX) {
+                           int m, double* const* chain, double* const* HX, bool psi2_given) {
   if (s == 0 || K <= 2) return cudaSuccess;
   SymArgs a{};
   a.s = s; a.G = G; a.W[0] = W0; a.W[1] = W1; a.W[2] = W2; a.H = H; a.P = P; a.K = K;
@@ -1957,6 +1990,12 @@ cudaError_t dense_cheb_sym(int64_t s, const double* G, double* W0, double* W1, d
   a.vec = aligned16(G, s) && aligned16(W0, s) && aligned16(W1, s) && aligned16(W2, s);
   cudaError_t e = cudaMemsetAsync(sync, 0, dense_sym_sync_ints(s, K, num_sms) * sizeof(int), st);
   if (e != cudaSuccess) return e;
+  a.k0 = 2;
+  if (a.chain && psi2_given) {   // Psi_2 formed by the init from the squaring's G^2: start at k = 3
+    a.k0 = 3;
+    k_sym_mark_step2<<<(a.T * (a.T + 1) / 2 + 255) / 256, 256, 0, st>>>(sync, K, a.T, a.chain, a.split);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
   int cs = 0;
   if (const char* v = getenv("CPA_SVT_SYM_CLUSTER")) cs = atoi(v);
   if (a.split > 1 && (cs == 2 || cs == 4 || cs == 8) && !a.chain) {
@@ -1975,7 +2014,7 @@ cudaError_t dense_cheb_sym(int64_t s, const double* G, double* W0, double* W1, d
     if (cs == 4) return go(k_cheb_sym_cl<4>, 4);
     return go(k_cheb_sym_cl<8>, 8);
   }
-  const int64_t total = (int64_t)(K - 2) * a.T * (a.T + 1) / 2 * a.split;
+  const int64_t total = (int64_t)(K - a.k0) * a.T * (a.T + 1) / 2 * a.split;
   return sym_launch(a, total, slots, num_sms, st);
 }
 

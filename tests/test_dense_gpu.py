@@ -429,13 +429,18 @@ def test_two_chain_recurrence(env, m, s, L, K, split):
             if ch != "0":
                 out["again"] = h2.apply(Xd, kern, K, T=100).cpu().numpy()
                 out["eye"] = h2.apply(torch.eye(s, dtype=torch.float64, device="cuda"), kern, K, T=60).cpu().numpy()
+                os.environ["CPA_SVT_NO_PSI2_SQ"] = "1"   # Psi_2 by the recurrence's own k = 2 product
+                out["nosq"] = h2.apply(Xd, kern, K, T=100).cpu().numpy()
+                os.environ.pop("CPA_SVT_NO_PSI2_SQ", None)
             h2.close()
     finally:
         os.environ.pop("CPA_SVT_SYM_CHAIN", None)
         os.environ.pop("CPA_SVT_CHAIN_SPLIT", None)
+        os.environ.pop("CPA_SVT_NO_PSI2_SQ", None)
     Ym = out[str(m)]
     assert np.array_equal(Ym, out["again"])
     assert np.array_equal(out["eye"], out["eye"].T)
     assert O.rel_fro(Ym, out["0"]) <= 1e-12
+    assert O.rel_fro(out["nosq"], out["0"]) <= 1e-12
     if s <= 1100:
         assert O.rel_fro(Ym, O.cpa_shrink(X, O.Kernel(**kern), K, T=100)) <= TOL64
