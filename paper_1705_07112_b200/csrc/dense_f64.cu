@@ -439,11 +439,11 @@ __global__ void k_sym_init2(const double* __restrict__ G, int64_t s, double* __r
 }
 // the state of the sync array after step 2 (tile-done flags, the chain-0 split counters, the
 // Psi_2 count) when Psi_2 comes from k_sym_init2
-__global__ void k_sym_mark_step2(int* sync, int K, int T, int m, int S) {
+__global__ void k_sym_mark_step2(int* sync, int K, int T, int m, int split_arrivals) {
   const int ntri = T * (T + 1) / 2;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ntri; t += gridDim.x * blockDim.x) {
     sync[sym_tdone_off(K, T, m) + 2 * ntri + t] = 1;
-    sync[sym_split_off(K, T) + m * t] = S - 1;
+    sync[sym_split_off(K, T) + m * t] = split_arrivals;
     if (t == 0 && m == 2) sync[sym_pm_off(K, T, m)] = ntri;
   }
 }
@@ -965,7 +965,11 @@ __global__ void __launch_bounds__(32 * NW, CPA_FLOW_MINB)
         }
       };
       if (lane == 0 && a_early) issue_a();
+#ifdef CPA_EXP_NODEP
+      if (false) {
+#else
       if (!PANEL) {
+#endif
         // Fine-grained dependencies: this split reads rows [kb SBK, ke SBK) of column panel tj of
         // its B operand, i.e. only the tiles (l, tj) / (tj, l) of the tile rows l it covers (not the
         // whole cross tj), plus the unit's own tile of the previous step of its chain (the
@@ -1099,6 +1103,18 @@ __global__ void __launch_bounds__(32 * NW, CPA_FLOW_MINB)
     it += nku;
 #ifdef CPA_SYM_TRACE
     if (threadIdx.x == 0 && tk < kTraceUnits) g_trace[tk * 6 + 3] = trace_now();
+#endif
+#ifdef CPA_EXP_NOEPI
+    if (CH > 1) {   // (timing experiment: no reduction / epilogue; one store keeps the mainloop live)
+      double sacc = 0.0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < WJ; ++j) sacc += acc[i][j][0] + acc[i][j][1];
+      if (sacc == 1.2345e-300) a.H[threadIdx.x] = sacc;
+      __syncthreads();
+      continue;
+    }
 #endif
     sym_finish<true, PANEL, NW, CH>(a, k, tile, q, ti, tj, acc);
 #ifdef CPA_SYM_TRACE
@@ -1292,6 +1308,392 @@ __global__ void __launch_bounds__(2 * NTHREADS, 2)
     if (threadIdx.x == 0) meta[b] = WsMeta{k, tile, q, ti, tj};
     __syncwarp();
     if (lane == 0) mbar_arrive(sfull + b);
+    ++nunit;
+  }
+}
+
+// Ping-pong m-chain recurrence (k_cheb_sym_pp, opt-in CPA_SVT_SYM_PP=1, measured slower): ONE
+// persistent 384-thread CTA per SM with two MMA warp groups and one epilogue warp group.  Each MMA
+// group (warps 0-3 / 4-7) claims its own units, polls their dependencies, runs its own 4-stage TMA
+// ring and DMMA mainloop, and hands the accumulators to the epilogue group (warps 8-11) through its
+// own 32 KB staging buffer; so while one MMA group claims / waits / refills its ring, the other
+// keeps the DMMA pipe fed (two MMA warps per SMSP sustain 36.8 of the 37.2 TF/s: tools/peaks/
+// dmma_smem_loop), and no MMA warp runs an epilogue.  Split-K by LAST ARRIVAL: every split
+// publishes its partial, the last one to count itself in (acq_rel atomic, ordinal per tile and
+// chain) sums the S partials in the fixed order q = 0 .. S-1 -- the order of k_cheb_sym_tma's
+// reducer, so the results are bitwise equal to it -- and runs the fused chain epilogue; nothing
+// on the epilogue group ever waits for another CTA.
+constexpr int PP_HDR = 256;   // mbarriers, tickets, unit records
+struct PpMeta {
+  int k, tile, q, ti, tj;
+};
+
+template <int CH>
+__device__ __forceinline__ void pp_finish(const SymArgs& a, int k, int tile, int q, int ti, int tj, const double* stg,
+                                          int u, int* s_last) {
+  constexpr int mc = CH, NT = NTHREADS, NV = 32;
+  const int T = a.T;
+  const int S = a.split;
+  const int ntri = T * (T + 1) / 2;
+  int* cross = a.sync + 1;
+  const int64_t s = a.s;
+  const int warp = u >> 5, lane = u & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const bool cstep = k > mc;
+  const int hj = (k - 2) % mc;
+  const int sidx = mc * tile + hj;
+  const int ord = (k - 2 - hj) / mc + 1;          // products of this tile and chain so far
+  double v[NV];
+#pragma unroll
+  for (int rr = 0; rr < NV; ++rr) v[rr] = stg[rr * NT + u];
+  if (S > 1) {
+    double* slots = a.partial + (int64_t)sidx * S * (BM * BN);
+    CPA_DCHECK(tile >= 0 && tile < ntri && q >= 0 && q < S);
+#pragma unroll
+    for (int rr = 0; rr < NV; ++rr) __stcg(slots + (int64_t)q * (BM * BN) + rr * NT + u, v[rr]);
+    named_bar(3, NTHREADS);
+    if (u == 0) {
+      int old;
+      asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;\n"
+                   : "=r"(old)
+                   : "l"(a.sync + sym_split_off(a.K, T) + sidx)
+                   : "memory");
+      *s_last = old + 1 == S * ord;
+    }
+    named_bar(3, NTHREADS);
+    if (!*s_last) return;
+    // the last arrival: the S partials in the fixed order q = 0 .. S-1 (its own from registers),
+    // eight values at a time (register budget)
+#pragma unroll
+    for (int c8 = 0; c8 < NV / 8; ++c8) {
+      double sum[8];
+#pragma unroll
+      for (int x = 0; x < 8; ++x) sum[x] = q == 0 ? v[c8 * 8 + x] : __ldcg(slots + (c8 * 8 + x) * NT + u);
+      for (int p = 1; p < S; ++p) {
+        double w[8];
+#pragma unroll
+        for (int x = 0; x < 8; ++x)
+          w[x] = p == q ? v[c8 * 8 + x] : __ldcg(slots + (int64_t)p * (BM * BN) + (c8 * 8 + x) * NT + u);
+#pragma unroll
+        for (int x = 0; x < 8; ++x) sum[x] += w[x];
+      }
+#pragma unroll
+      for (int x = 0; x < 8; ++x) v[c8 * 8 + x] = sum[x];
+    }
+  }
+  // the fused chain epilogue (as sym_finish_impl's m-chain branch)
+  const double* src = a.C[chain_buf(cstep ? k - mc : k - 1, mc)];
+  const double* wpp = !cstep ? (k == 2 ? nullptr : a.C[chain_buf(k - 2, mc)])
+                             : (k == 2 * mc ? nullptr : a.C[chain_buf(k > 2 * mc ? k - 2 * mc : 2 * mc - k, mc)]);
+  double* out = a.C[chain_buf(k, mc)];
+  double* hmine = hj == 0 ? a.H : a.HX[hj - 1];
+  const bool hzero = hj > 0 && k == 2 + hj;
+  const int64_t m0 = (int64_t)ti * BM, n0 = (int64_t)tj * BN;
+  const double s4 = 2.0 * a.P->scale2, ck = a.P->c[k];
+  const bool last = k == a.K - 1;
+  const bool store_w = k + mc <= a.K - 1;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t rr = m0 + wm + i * 8 + g;
+    double vp[8], vpp[8], vy[8];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t c = n0 + wn + j * 8 + 2 * t + e;
+        const bool ok = rr < s && c <= rr;
+        const int64_t o = rr * s + c;
+        vp[j * 2 + e] = (!cstep && ok) ? __ldcg(src + o) : 0.0;
+        vpp[j * 2 + e] = wpp == nullptr ? (rr == c ? 1.0 : 0.0) : (ok ? __ldcg(wpp + o) : 0.0);
+        double y0 = (hzero || !ok) ? 0.0 : __ldcg(hmine + o);
+        if (last && ok)
+          for (int jj = 0; jj < mc; ++jj)
+            if (jj != hj) y0 += __ldcg((jj == 0 ? a.H : a.HX[jj - 1]) + o);
+        vy[j * 2 + e] = y0;
+      }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t c = n0 + wn + j * 8 + 2 * t + e;
+        if (!(rr < s && c <= rr)) continue;
+        const int qq = j * 2 + e;
+        const double acc = v[(i * 4 + j) * 2 + e];
+        const double wv = cstep ? 2.0 * acc - vpp[qq] : s4 * acc - 2.0 * vp[qq] - vpp[qq];
+        const double y = vy[qq] + ck * wv;
+        if (store_w) {
+          out[rr * s + c] = wv;
+          out[c * s + rr] = wv;
+        }
+        if (last) {
+          a.H[rr * s + c] = y;
+          a.H[c * s + rr] = y;
+        } else {
+          hmine[rr * s + c] = y;
+        }
+      }
+  }
+  fence_proxy_async_global();   // Psi_k / H stores -> later TMA (async-proxy) reads
+  named_bar(3, NTHREADS);
+  if (u == 0) {
+    red_release_add_i32(cross + k * T + ti, 1);
+    if (ti != tj) red_release_add_i32(cross + k * T + tj, 1);
+    red_release_add_i32(a.sync + sym_tdone_off(a.K, T, mc) + k * ntri + tile, 1);   // tile done
+    if (k == mc) red_release_add_i32(a.sync + sym_pm_off(a.K, T, mc), 1);          // Psi_m progress
+  }
+}
+
+template <int SBK, int SSTAGES, int CH>
+__global__ void __launch_bounds__(3 * NTHREADS, 1) k_cheb_sym_pp(const __grid_constant__ SymMapsChain mp, SymArgs a) {
+  constexpr int SBOX_BYTES = 16 * SBK * 8;
+  constexpr int SSTAGE_BYTES = 8 * SBOX_BYTES;
+  constexpr int RING_BYTES = SSTAGES * SSTAGE_BYTES;
+  constexpr int mc = CH;
+  extern __shared__ __align__(16) unsigned char tsm_raw[];
+  uint64_t* fullb = reinterpret_cast<uint64_t*>(tsm_raw);   // [2][SSTAGES]
+  uint64_t* emptyb = fullb + 2 * SSTAGES;                    // [2][SSTAGES]
+  uint64_t* sfull = emptyb + 2 * SSTAGES;                    // [2]
+  uint64_t* sempty = sfull + 2;                              // [2]
+  int* s_ticket = reinterpret_cast<int*>(sempty + 2);        // [2][2]
+  int* s_ctl = s_ticket + 4;                                 // [0] selected group, [1] last arrival
+  PpMeta* meta = reinterpret_cast<PpMeta*>(s_ctl + 2);       // [2]
+  static_assert(8 * (4 * SSTAGES + 4) + 4 * 6 + 2 * sizeof(PpMeta) <= PP_HDR, "header");
+  const uint32_t raw = smem_u32(tsm_raw);
+  unsigned char* base = tsm_raw + (((raw + PP_HDR + 1023u) & ~1023u) - raw);
+  double* stage = reinterpret_cast<double*>(base + 2 * RING_BYTES);   // [2][64 x 64]
+  {
+    uint32_t dyn;
+    asm volatile("mov.u32 %0, %%dynamic_smem_size;\n" : "=r"(dyn));
+    if ((uint32_t)(base - tsm_raw) + 2 * RING_BYTES + 2 * BM * BN * 8 > dyn) __trap();   // layout check
+  }
+  const int T = a.T;
+  const int ntri = T * (T + 1) / 2;
+  const int S = a.split;
+  const int per_step = ntri * S;
+  const int total = (a.K - a.k0) * per_step;
+  int* cross = a.sync + 1;
+  const int nk = (int)((a.s + SBK - 1) / SBK);
+  const int wg = threadIdx.x / NTHREADS;
+  const int tid = threadIdx.x % NTHREADS;
+  const int warp = tid >> 5, lane = tid & 31;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < 2 * SSTAGES; ++st) {
+      mbar_init(fullb + st, 1);
+      mbar_init(emptyb + st, 4);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(sfull + b, 4);
+      mbar_init(sempty + b, 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (wg == 2) {
+    // ---------------- epilogue warp group: serves the two MMA groups in arrival order ----------------
+    uint32_t n0 = 0, n1 = 0;
+    bool done0 = false, done1 = false;
+    for (;;) {
+      if (tid == 0) {
+        int sel = -1;
+        while (sel < 0) {
+          uint32_t ok = 0;
+          if (!done0) {
+            asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+                         : "=r"(ok) : "r"(smem_u32(sfull)), "r"(n0 & 1) : "memory");
+            if (ok) sel = 0;
+          }
+          if (sel < 0 && !done1) {
+            asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+                         : "=r"(ok) : "r"(smem_u32(sfull + 1)), "r"(n1 & 1) : "memory");
+            if (ok) sel = 1;
+          }
+        }
+        s_ctl[0] = sel;
+      }
+      named_bar(3, NTHREADS);
+      const int gsel = s_ctl[0];
+      named_bar(3, NTHREADS);   // (s_ctl[0] is rewritten by the next selection)
+      const uint32_t n = gsel ? n1 : n0;
+      mbar_wait(sfull + gsel, n & 1);   // (complete: orders this thread's staging reads after it)
+      const PpMeta mt = meta[gsel];
+      if (mt.k >= 0) {
+        pp_finish<CH>(a, mt.k, mt.tile, mt.q, mt.ti, mt.tj, stage + gsel * (BM * BN), tid, s_ctl + 1);
+        __syncwarp();
+      }
+      if (lane == 0) mbar_arrive(sempty + gsel);   // staging gsel may be refilled
+      if (gsel) { ++n1; done1 = mt.k < 0; } else { ++n0; done0 = mt.k < 0; }
+      if (done0 && done1) break;
+    }
+    return;
+  }
+  // ---------------- MMA warp groups (thread 0 of each: tickets and TMA producer) ----------------
+  unsigned char* ring = base + wg * RING_BYTES;
+  uint64_t* full = fullb + wg * SSTAGES;
+  uint64_t* empty = emptyb + wg * SSTAGES;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  uint32_t coff[2][2];
+#pragma unroll
+  for (int par = 0; par < 2; ++par)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) coff[par][h] = ((((h * 8 + g) >> 1) ^ (2 * t + par)) << 4) | ((g & 1) * 8);
+  const uint32_t roff = 256 * t;
+  const uint32_t boxa = (wm >> 4) * SBOX_BYTES, boxb = (4 + (wn >> 4)) * SBOX_BYTES;
+  const int bar_id = 1 + wg;
+  uint32_t it = 0;   // slabs consumed by this group so far
+  uint32_t nunit = 0;
+  for (;;) {
+    int* my_ticket = s_ticket + 2 * wg + (nunit & 1);
+    if (tid == 0) *my_ticket = atomicAdd(a.sync, 1);
+    named_bar(bar_id, NTHREADS);
+    const int tk = *my_ticket;
+    if (tk >= total) {
+      mbar_wait(sempty + wg, (nunit & 1) ^ 1);
+      if (tid == 0) meta[wg].k = -1;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(sfull + wg);
+      break;
+    }
+    const int k = a.k0 + tk / per_step;
+    const int r = tk % per_step;
+    const int q = r % S;
+    const int tile = r / S;
+    int ti, tj;
+    tri_decode_colmajor(tile, T, ti, tj);
+    CPA_DCHECK(ti >= 0 && ti < T && tj >= 0 && tj <= ti);
+    const bool cstep = k > mc;
+    const CUtensorMap* wmap = &mp.c[chain_buf(cstep ? k - mc : k - 1, mc)];
+    const CUtensorMap* amap = cstep ? &mp.c[mc - 1] : &mp.g;
+    const int m0 = ti * BM, n0 = tj * BN;
+    int kb, ke;
+    {   // the last split takes a (100 + red_bias)% k-range (as k_cheb_sym_tma's m-chain instance)
+      const int64_t wt = 100 * S + a.red_bias;
+      kb = (int)((int64_t)nk * q * 100 / wt);
+      ke = q == S - 1 ? nk : (int)((int64_t)nk * (q + 1) * 100 / wt);
+    }
+    const int nku = ke - kb;
+    if (warp == 0) {
+      const int P = nku < SSTAGES - 1 ? nku : SSTAGES - 1;
+      bool a_early = true;
+      if (cstep) {
+        const int v = lane == 0 ? ld_acquire(a.sync + sym_pm_off(a.K, T, mc)) : 0;
+        a_early = __shfl_sync(0xffffffffu, v, 0) >= ntri;
+      }
+      auto issue_a = [&] {
+        for (int p = 0; p < P; ++p) {
+          const uint32_t sl = it + p, st = sl % SSTAGES;
+          mbar_wait(empty + st, ((sl / SSTAGES) & 1) ^ 1);
+          mbar_expect_tx(full + st, SSTAGE_BYTES);
+          for (int b = 0; b < 4; ++b)
+            tma_load_2d(ring + st * SSTAGE_BYTES + b * SBOX_BYTES, amap, m0 + 16 * b, (kb + p) * SBK, full + st);
+        }
+      };
+      if (lane == 0 && a_early) issue_a();
+      {   // dependencies: the rules of k_cheb_sym_tma's m-chain instance (see there)
+        const int* tdone = a.sync + sym_tdone_off(a.K, T, mc);
+        const int l0 = (kb * SBK) / BM, l1e = (ke * SBK - 1) / BM, l1 = l1e < T - 1 ? l1e : T - 1;
+        const int nl = l1 - l0 + 1;
+        auto tri_idx = [&](int rr, int cc) { return cc * (2 * T - cc + 1) / 2 + (rr - cc); };   // rr >= cc
+        const int kprev = cstep ? k - mc : k - 1;
+        const int khaz = cstep ? (k >= 4 * mc + 1 ? k - 2 * mc : 0) : 0;
+        const bool need_b = kprev >= 2;
+        const bool need_m = cstep && k <= 2 * mc;
+        const bool need_a = need_m && !a_early;
+        const bool need_h = k == a.K - 1;
+        const int nflags = 6 + nl + (need_a ? nl : 0);
+        for (int f = lane; f < nflags; f += 32) {
+          const int* flag = nullptr;
+          int target = 1;
+          if (f < 2) {
+            if (khaz) { flag = cross + khaz * T + (f == 0 ? ti : tj); target = T; }
+          } else if (f == 2) {
+            if (need_b) flag = tdone + kprev * ntri + tile;
+          } else if (f == 3) {
+            if (need_m) flag = tdone + mc * ntri + tile;
+          } else if (f < 6) {
+            if (need_h && f - 3 < mc) flag = tdone + (a.K - 1 - (f - 3)) * ntri + tile;
+          } else if (f < 6 + nl) {
+            const int l = l0 + f - 6;
+            if (need_b) flag = tdone + kprev * ntri + (l >= tj ? tri_idx(l, tj) : tri_idx(tj, l));
+          } else {
+            const int l = l0 + f - 6 - nl;
+            flag = tdone + mc * ntri + (l >= ti ? tri_idx(l, ti) : tri_idx(ti, l));
+          }
+          if (flag) wait_geq(flag, target);
+        }
+        __syncwarp();
+      }
+      if (lane == 0) {
+        fence_proxy_async_global();   // generic-proxy stores of other CTAs -> TMA reads
+        if (!a_early) issue_a();
+        for (int p = 0; p < P; ++p) {
+          const uint32_t st = (it + p) % SSTAGES;
+          for (int b = 0; b < 4; ++b)
+            tma_load_2d(ring + st * SSTAGE_BYTES + (4 + b) * SBOX_BYTES, wmap, n0 + 16 * b, (kb + p) * SBK,
+                        full + st);
+        }
+      }
+    }
+    // (the epilogue group's generic loads are ordered after warp 0's acquire through the full
+    // barriers of refilled slabs and the staging handover; a unit too short to refill takes a
+    // group barrier, as in k_cheb_sym_tma)
+    if (nku < SSTAGES) named_bar(bar_id, NTHREADS);
+    else __syncwarp();
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int kt = 0; kt < nku; ++kt) {
+      if (tid == 0 && kt + SSTAGES - 1 < nku) {   // refill the stage of slab kt-1
+        const int kn = kt + SSTAGES - 1;
+        const uint32_t sl = it + kn, st = sl % SSTAGES;
+        mbar_wait(empty + st, ((sl / SSTAGES) & 1) ^ 1);
+        mbar_expect_tx(full + st, SSTAGE_BYTES);
+        unsigned char* d = ring + st * SSTAGE_BYTES;
+        for (int b = 0; b < 4; ++b) tma_load_2d(d + b * SBOX_BYTES, amap, m0 + 16 * b, (kb + kn) * SBK, full + st);
+        for (int b = 0; b < 4; ++b)
+          tma_load_2d(d + (4 + b) * SBOX_BYTES, wmap, n0 + 16 * b, (kb + kn) * SBK, full + st);
+      }
+      __syncwarp();
+      const uint32_t sl = it + kt, st = sl % SSTAGES;
+      mbar_wait(full + st, (sl / SSTAGES) & 1);
+      const unsigned char* sa = ring + st * SSTAGE_BYTES + boxa;
+      const unsigned char* sb = ring + st * SSTAGE_BYTES + boxb;
+#pragma unroll
+      for (int kk = 0; kk < SBK / 4; ++kk) {
+        const int par = kk & 1;
+        const uint32_t ro = 1024 * (kk >> 1) + 128 * par + roff;
+        double fa[4], fb[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          fa[i] = *reinterpret_cast<const double*>(sa + (i >> 1) * SBOX_BYTES + ro + coff[par][i & 1]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          fb[j] = *reinterpret_cast<const double*>(sb + (j >> 1) * SBOX_BYTES + ro + coff[par][j & 1]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], fa[i], fb[j]);
+      }
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + st);
+    }
+    it += nku;
+    // hand the accumulators to the epilogue group (layout [reg][thread], the split-K slot layout)
+    mbar_wait(sempty + wg, (nunit & 1) ^ 1);
+    double* stg = stage + wg * (BM * BN);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) stg[((i * 4 + j) * 2 + e) * NTHREADS + tid] = acc[i][j][e];
+    if (tid == 0) meta[wg] = PpMeta{k, tile, q, ti, tj};
+    __syncwarp();
+    if (lane == 0) mbar_arrive(sfull + wg);
     ++nunit;
   }
 }
@@ -1947,10 +2349,23 @@ static int sym_split_mode(int64_t s, int slots, int m) {
   return S;
 }
 
+// Ping-pong kernel for the m-chain mode (k_cheb_sym_pp: one CTA per SM, two MMA groups, last-
+// arrival split-K), opt-in with CPA_SVT_SYM_PP=1: measured slower than the 3-CTA k_cheb_sym_tma
+// instance at c2.
+static bool sym_use_pp(int m) { return m > 1 && getenv("CPA_SVT_SYM_PP") && atoi(getenv("CPA_SVT_SYM_PP")) == 1; }
+
+static int sym_split_pp(int64_t s, int num_sms, int m) {
+  const int64_t T = (s + BM - 1) / BM;
+  int S = sym_split(s, 2 * num_sms, m * (T * (T + 1) / 2));
+  if (const char* v = getenv("CPA_SVT_CHAIN_SPLIT")) S = (atoi(v) > 0 && atoi(v) <= 16) ? atoi(v) : S;
+  return S;
+}
+
 size_t dense_sym_partial_doubles(int64_t s, int num_sms, int m) {
   const int64_t T = (s + BM - 1) / BM;
-  const int S = sym_split_mode(s, sym_slots(num_sms), m);
-  return S > 1 ? (size_t)(T * (T + 1) / 2 * (m > 1 ? m : 1) * (S - 1) * BM * BN) : 0;
+  const int S = sym_use_pp(m) ? sym_split_pp(s, num_sms, m) : sym_split_mode(s, sym_slots(num_sms), m);
+  // (m chains: S slots per tile and chain -- the ping-pong kernel publishes every split)
+  return S > 1 ? (size_t)(T * (T + 1) / 2 * (m > 1 ? m * S : S - 1) * BM * BN) : 0;
 }
 
 // W_1 = B_hat (into W1 when K > 2) and H = c_0/2 I + c_1 W_1; with G2 (c^2 G^2 from the power
@@ -1984,7 +2399,8 @@ cudaError_t dense_cheb_sym(int64_t s, const double* G, double* W0, double* W1, d
   }
   const size_t smem = sym_smem();
   const int slots = sym_slots(num_sms);
-  a.split = sym_split_mode(s, slots, a.chain);
+  const bool pp = sym_use_pp(a.chain);
+  a.split = pp ? sym_split_pp(s, num_sms, a.chain) : sym_split_mode(s, slots, a.chain);
   a.sync = sync;
   a.partial = partial;
   a.vec = aligned16(G, s) && aligned16(W0, s) && aligned16(W1, s) && aligned16(W2, s);
@@ -1993,7 +2409,8 @@ cudaError_t dense_cheb_sym(int64_t s, const double* G, double* W0, double* W1, d
   a.k0 = 2;
   if (a.chain && psi2_given) {   // Psi_2 formed by the init from the squaring's G^2: start at k = 3
     a.k0 = 3;
-    k_sym_mark_step2<<<(a.T * (a.T + 1) / 2 + 255) / 256, 256, 0, st>>>(sync, K, a.T, a.chain, a.split);
+    k_sym_mark_step2<<<(a.T * (a.T + 1) / 2 + 255) / 256, 256, 0, st>>>(sync, K, a.T, a.chain,
+                                                                          pp ? a.split : a.split - 1);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   int cs = 0;
@@ -2097,6 +2514,23 @@ static cudaError_t sym_launch(SymArgs& a, int64_t total, int slots, int num_sms,
       int64_t tgrid = (int64_t)num_sms * per_sm;
       if (tgrid > total) tgrid = total;
       void* targs[] = {a.chain ? (void*)&mpc : (void*)&mp, &a};
+      if (a.chain && sym_use_pp(a.chain)) {
+        // ping-pong: one 384-thread CTA per SM, two 64 KB rings + two 32 KB staging buffers
+        // (16-deep slabs: 5 stages per ring by default -- two 80 KB rings and the staging fill the
+        // 227 KB; CPA_SVT_PP_STAGES=4 for 64 KB rings; 32-deep slabs: 2 stages)
+        const int pst = sbk == 32 ? 2 : (getenv("CPA_SVT_PP_STAGES") && atoi(getenv("CPA_SVT_PP_STAGES")) == 4 ? 4 : 5);
+        const size_t psmem = PP_HDR + 1024 + 2 * (size_t)pst * 8 * (16 * sbk * 8) + 2 * BM * BN * 8;
+        const void* pk =
+            a.chain == 3 ? (sbk == 32 ? (const void*)k_cheb_sym_pp<32, 2, 3>
+                                      : pst == 4 ? (const void*)k_cheb_sym_pp<16, 4, 3> : (const void*)k_cheb_sym_pp<16, 5, 3>)
+                         : (sbk == 32 ? (const void*)k_cheb_sym_pp<32, 2, 2>
+                                      : pst == 4 ? (const void*)k_cheb_sym_pp<16, 4, 2> : (const void*)k_cheb_sym_pp<16, 5, 2>);
+        e = cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
+        if (e != cudaSuccess) return e;
+        int64_t pgrid = num_sms;
+        if (env_on("CPA_SVT_DEBUG_OCC")) fprintf(stderr, "k_cheb_sym_pp<%d>: %d CTAs, smem %zu\n", sbk, (int)pgrid, psmem);
+        return cudaLaunchCooperativeKernel((void*)pk, dim3((unsigned)pgrid), dim3(3 * NTHREADS), targs, psmem, st);
+      }
       return cudaLaunchCooperativeKernel((void*)kf, dim3((unsigned)tgrid), dim3(32 * nw), targs, tsmem, st);
     }
   }

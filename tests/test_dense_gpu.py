@@ -444,3 +444,32 @@ def test_two_chain_recurrence(env, m, s, L, K, split):
     assert O.rel_fro(out["nosq"], out["0"]) <= 1e-12
     if s <= 1100:
         assert O.rel_fro(Ym, O.cpa_shrink(X, O.Kernel(**kern), K, T=100)) <= TOL64
+
+
+@pytest.mark.parametrize("m,s,L,K,split", [(2, 1024, 1024, 30, 3), (2, 1024, 1100, 31, 2), (3, 1024, 1024, 30, 2),
+                                           (2, 256, 300, 9, 1), (3, 320, 330, 15, 3), (2, 130, 140, 11, 5)])
+def test_pingpong_recurrence_bitwise(env, m, s, L, K, split):
+    """k_cheb_sym_pp (one CTA per SM: two MMA warp groups and an epilogue group, split-K by last
+    arrival; opt-in CPA_SVT_SYM_PP=1) sums each tile's partials in the order of k_cheb_sym_tma's
+    reducer: bitwise-equal outputs, and the oracle bar."""
+    import os
+    torch, P, _ = env
+    X = W.gen_c2(m=s, n=L, seed=s + K + 3)
+    kern = {"kind": "soft", "tau": 0.05, "tau_relative": True}
+    Xd = torch.from_numpy(X).cuda()
+    out = {}
+    os.environ["CPA_SVT_SYM_CHAIN"] = str(m)
+    os.environ["CPA_SVT_CHAIN_SPLIT"] = str(split)
+    try:
+        for pp in ("0", "1"):
+            os.environ["CPA_SVT_SYM_PP"] = pp
+            h2 = P.Handle(0)
+            h2.set_form("poly")
+            out[pp] = h2.apply(Xd, kern, K, T=100).cpu().numpy()
+            h2.close()
+    finally:
+        for v in ("CPA_SVT_SYM_PP", "CPA_SVT_SYM_CHAIN", "CPA_SVT_CHAIN_SPLIT"):
+            os.environ.pop(v, None)
+    assert np.array_equal(out["0"], out["1"])
+    if s <= 1100:
+        assert O.rel_fro(out["1"], O.cpa_shrink(X, O.Kernel(**kern), K, T=100)) <= TOL64

@@ -21,7 +21,7 @@ for s in sizes:
     X = torch.from_numpy(W.gen_c2(m=s, n=s)).cuda()
     Y = torch.empty_like(X)
     ref = None
-    grid = [("0", "")] + [(m, str(q)) for m in ("2", "3") for q in (0, 2, 3, 4)]
+    grid = [("0", "")] + [(m, str(q)) for m in ("2", "3") for q in (0, 1, 2, 3, 4, 6)]
     for chain, split in ([("0", "")] if os.environ.get("SWEEP_ONECHAIN") else grid):
         os.environ["CPA_SVT_SYM_CHAIN"] = chain
         if split and split != "0":

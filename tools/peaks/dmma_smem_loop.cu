@@ -42,16 +42,19 @@ int main() {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0); cudaEventCreate(&e1);
   const int iters = 4000;
-  for (int sync = 0; sync < 2; ++sync)
-    for (int rep = 0; rep < 2; ++rep) {
-      cudaEventRecord(e0);
-      if (sync) k<true><<<148 * 3, 128>>>(out, iters); else k<false><<<148 * 3, 128>>>(out, iters);
-      cudaEventRecord(e1);
-      cudaEventSynchronize(e1);
-      float ms;
-      cudaEventElapsedTime(&ms, e0, e1);
-      const double fl = 2.0 * 64 * 64 * 16 * (double)iters * 148 * 3;
-      if (rep) printf("smem-fed DMMA loop, %s: %.2f TFLOP/s\n", sync ? "__syncthreads per slab" : "no barrier", fl / ms / 1e9);
-    }
+  // resident CTAs per SM: 1, 2, 3 (the grid is 148 x cps; 3 fit by registers)
+  for (int cps = 1; cps <= 3; ++cps)
+    for (int sync = 0; sync < 2; ++sync)
+      for (int rep = 0; rep < 2; ++rep) {
+        cudaEventRecord(e0);
+        if (sync) k<true><<<148 * cps, 128>>>(out, iters); else k<false><<<148 * cps, 128>>>(out, iters);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        const double fl = 2.0 * 64 * 64 * 16 * (double)iters * 148 * cps;
+        if (rep) printf("smem-fed DMMA loop, %d CTA(s)/SM, %s: %.2f TFLOP/s\n", cps,
+                        sync ? "__syncthreads per slab" : "no barrier", fl / ms / 1e9);
+      }
   return 0;
 }
