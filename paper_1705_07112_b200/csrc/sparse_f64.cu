@@ -164,6 +164,40 @@ __global__ void k_row_split(const int64_t* row_ptr, const int32_t* col, int64_t 
 // The NP column passes run as NP launches in order (pass 0 writes, the others add: a fixed order),
 // so the L2 footprint of a block is its W slice (32 x n / NP doubles) plus the matching CSR slice
 // instead of the whole 51 MB block row (DRAM re-reads of W measured 3.5x with one pass).
+// sum_{e in [e0, e1)} x[e] V[idx[e]][lane] with U gathers in flight (U accumulators, the tail in
+// accumulator 0, summed in a fixed tree: a fixed order)
+template <int U>
+__device__ __forceinline__ double gather_sum(const int32_t* __restrict__ idx, const double* __restrict__ x, int64_t e0,
+                                             int64_t e1, const double* __restrict__ Vb, int64_t nidx) {
+  (void)nidx;
+  double acc[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) acc[u] = 0.0;
+  int64_t e = e0;
+  for (; e + U <= e1; e += U) {
+    int32_t c[U];
+    double xv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      c[u] = __ldg(idx + e + u);
+      xv[u] = __ldg(x + e + u);
+      CPA_DCHECK(c[u] >= 0 && c[u] < nidx);
+    }
+    double g[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) g[u] = Vb[(int64_t)c[u] * RB];
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc[u] = fma(xv[u], g[u], acc[u]);
+  }
+  for (; e < e1; ++e) acc[0] = fma(__ldg(x + e), Vb[(int64_t)__ldg(idx + e) * RB], acc[0]);
+#pragma unroll
+  for (int w = 1; w < U; w *= 2)
+#pragma unroll
+    for (int u = 0; u + w < U; u += 2 * w) acc[u] += acc[u + w];
+  return acc[0];
+}
+
+template <int U>
 __global__ void __launch_bounds__(SP_WARPS * 32) k_spmm_wxt(const int64_t* row_ptr, const int32_t* col,
                                                             const double* val, int64_t m, int64_t n, int64_t nblk,
                                                             const double* __restrict__ W, double* __restrict__ Z,
@@ -175,23 +209,17 @@ __global__ void __launch_bounds__(SP_WARPS * 32) k_spmm_wxt(const int64_t* row_p
   const double* Wb = W + b * n * RB + lane;
   const int64_t e0 = NP > 1 ? rs[j * (NP + 1) + h] : row_ptr[j];
   const int64_t e1 = NP > 1 ? rs[j * (NP + 1) + h + 1] : row_ptr[j + 1];
-  double s0 = 0.0, s1 = 0.0;
-  int64_t e = e0;
-  for (; e + 1 < e1; e += 2) {
-    const int32_t c0 = __ldg(col + e), c1 = __ldg(col + e + 1);
-    const double x0 = __ldg(val + e), x1 = __ldg(val + e + 1);
-    CPA_DCHECK(c0 >= 0 && c0 < n && c1 >= 0 && c1 < n);
-    s0 = fma(x0, Wb[(int64_t)c0 * RB], s0);
-    s1 = fma(x1, Wb[(int64_t)c1 * RB], s1);
-  }
-  if (e < e1) s0 = fma(__ldg(val + e), Wb[(int64_t)__ldg(col + e) * RB], s0);
+  const double sum = gather_sum<U>(col, val, e0, e1, Wb, n);
   double* zp = Z + (b * m + j) * RB + lane;
-  if (h == 0) *zp = s0 + s1;
-  else *zp += s0 + s1;
+  if (h == 0) *zp = sum;
+  else *zp += sum;
 }
 
 // W_k[b][l][:] = s * sum_{j in col l} x_jl Z[b][j][:] - ... (fused epilogue), one warp per (b, l)
-template <bool INIT>
+// W_k[b][l][:] = 2 s (sum_{j in col l} x_jl Z[b][j][:]) - 2 W_{k-1} - W_{k-2}, Y += c_k W_k (fused
+// epilogue), one warp per (b, l).  (Evict-first / streaming hints on the epilogue's streamed
+// operands, loaded ahead of the gathers, measured slower: 74.5 -> 77.5 ms per c4 step.)
+template <int U, bool INIT>
 __global__ void __launch_bounds__(SP_WARPS * 32) k_spmm_zx(const int64_t* cptr, const int32_t* crow,
                                                            const double* cval, int64_t m, int64_t n, int64_t nblk,
                                                            const double* __restrict__ Z, const double* Wp,
@@ -201,18 +229,7 @@ __global__ void __launch_bounds__(SP_WARPS * 32) k_spmm_zx(const int64_t* cptr, 
   const int64_t item = blockIdx.x * (int64_t)SP_WARPS + warp;  // item = b * n + l
   if (item >= nblk * n) return;
   const int64_t b = item / n, l = item % n;
-  const double* Zb = Z + b * m * RB + lane;
-  const int64_t e0 = cptr[l], e1 = cptr[l + 1];
-  double s0 = 0.0, s1 = 0.0;
-  int64_t e = e0;
-  for (; e + 1 < e1; e += 2) {
-    const int32_t r0 = __ldg(crow + e), r1 = __ldg(crow + e + 1);
-    CPA_DCHECK(r0 >= 0 && r0 < m && r1 >= 0 && r1 < m);
-    s0 = fma(__ldg(cval + e), Zb[(int64_t)r0 * RB], s0);
-    s1 = fma(__ldg(cval + e + 1), Zb[(int64_t)r1 * RB], s1);
-  }
-  if (e < e1) s0 = fma(__ldg(cval + e), Zb[(int64_t)__ldg(crow + e) * RB], s0);
-  const double acc = s0 + s1;
+  const double acc = gather_sum<U>(crow, cval, cptr[l], cptr[l + 1], Z + b * m * RB + lane, m);
   const int64_t o = item * RB + lane;
   const double s2 = P->scale2;
   if (INIT) {
@@ -338,6 +355,11 @@ cudaError_t sparse_apply(int64_t m, int64_t n, int64_t nnz, const int64_t* row_p
     double* W0 = Wa;
     double* W1 = Wb;
     const int64_t itemsZ = nblk * m, itemsW = nblk * n;
+    // gathers in flight per warp in the SpMM pair (CPA_SVT_SP_UNROLL = 2 | 4 | 8; c4 per step, Z / W
+    // kernels: 55.0 / 77.6, 55.6 / 91.6, 78.2 / 109.7 ms -- more loads in flight only add L2
+    // contention; the index loads of a pair ahead of the two gathers: Z 65 -> 55 ms)
+    int U = 2;
+    if (const char* v = getenv("CPA_SVT_SP_UNROLL")) U = atoi(v) == 8 ? 8 : atoi(v) == 4 ? 4 : 2;
     const unsigned gz = (unsigned)((itemsZ + SP_WARPS - 1) / SP_WARPS);
     const unsigned gw = (unsigned)((itemsW + SP_WARPS - 1) / SP_WARPS);
     const double* prev = W0;   // W_{k-1}
@@ -349,7 +371,8 @@ cudaError_t sparse_apply(int64_t m, int64_t n, int64_t nnz, const int64_t* row_p
     for (int k = 1; k < K; ++k) {
       if (hook) hook(hook_ctx, CPA_SVT_PH_SPARSE_Z, 1);
       for (int hp = 0; hp < NP; ++hp) {
-        k_spmm_wxt<<<gz, SP_WARPS * 32, 0, st>>>(row_ptr, col, val, m, n, nblk, prev, Z, rs, NP, hp);
+        auto kz = U == 8 ? k_spmm_wxt<8> : U == 4 ? k_spmm_wxt<4> : k_spmm_wxt<2>;
+        kz<<<gz, SP_WARPS * 32, 0, st>>>(row_ptr, col, val, m, n, nblk, prev, Z, rs, NP, hp);
         ++L;
       }
       if (hook) hook(hook_ctx, CPA_SVT_PH_SPARSE_Z, 0);
@@ -358,10 +381,11 @@ cudaError_t sparse_apply(int64_t m, int64_t n, int64_t nnz, const int64_t* row_p
       if (k == 1) out = W1;                  // W_1 -> Wb
       else out = (k & 1) ? Wb : Wa;          // W_k overwrites W_{k-2} in place
       if (k == K - 1) out = nullptr;
-      if (k == 1)
-        k_spmm_zx<true><<<gw, SP_WARPS * 32, 0, st>>>(cptr, crow, cval, m, n, nblk, Z, prev, nullptr, out, Yb, P, k);
-      else
-        k_spmm_zx<false><<<gw, SP_WARPS * 32, 0, st>>>(cptr, crow, cval, m, n, nblk, Z, prev, prev2, out, Yb, P, k);
+      {
+        auto kw = k == 1 ? (U == 8 ? k_spmm_zx<8, true> : U == 4 ? k_spmm_zx<4, true> : k_spmm_zx<2, true>)
+                         : (U == 8 ? k_spmm_zx<8, false> : U == 4 ? k_spmm_zx<4, false> : k_spmm_zx<2, false>);
+        kw<<<gw, SP_WARPS * 32, 0, st>>>(cptr, crow, cval, m, n, nblk, Z, prev, k == 1 ? nullptr : prev2, out, Yb, P, k);
+      }
       ++L;
       if (hook) hook(hook_ctx, CPA_SVT_PH_SPARSE_W, 0);
       prev2 = prev;
