@@ -16,7 +16,10 @@
  *   - the Alg. 1 s x s form (default for K > 2): the three-term recurrence on the
  *     s x s Gram, Psi_0 = Id, Psi_1 = B_hat, Psi_k = 2 B_hat Psi_{k-1} - Psi_{k-2}
  *     (PAPER.md:364-370), H_hat = c_0/2 Id + sum_k c_k Psi_k formed on the device,
- *     then ONE product Y = H_hat X (or X H_hat), Alg. 1 line 12;
+ *     then ONE product Y = H_hat X (or X H_hat), Alg. 1 line 12.  For small s the
+ *     same products run as two independent Chebyshev chains (even / odd k:
+ *     Psi_k = 2 Psi_2 Psi_{k-2} - Psi_{|k-4|}, reading R28), with Psi_2
+ *     formed from the power iteration's G^2 when that squaring ran (R29);
  *   - the apply-to-X form (line 12 distributed over the sum):
  *     W_0 = X,  W_1 = (2/L) G X - X,  W_k = (4/L) G W_{k-1} - 2 W_{k-1} - W_{k-2},
  *     Y = c_0/2 W_0 + c_1 W_1 + sum_{k>=2} c_k W_k.
