@@ -348,6 +348,8 @@ def run_ours(args, cfg):
         # (K - 3 products when Psi_2 came from the power iteration's squaring, reading R29)
         nprod = info0.get("rec_products") or (K - 2)
         rec_flops = nprod * s_ * s_ * (s_ + 1) * (3 if cfg["math"] == "3xtf32" else 1)
+        if info0.get("line12_in_recurrence"):   # line 12 (2 s^2 L) ran inside the same launch
+            rec_flops += 2 * s_ * s_ * L_
     else:
         kname = "k_cheb_flow (fused apply-to-X recurrence, DMMA)"
         rec_flops = (K - 1) * 2 * s_ * s_ * (n_g // world if cfg["sharded"] else L_)

@@ -129,6 +129,8 @@ typedef struct {
   int32_t rec_products;  /* s x s products the recurrence (Alg. 1 lines 8-11) launched for the dense
                             fp64 s x s forms: K - 2, or K - 3 when Psi_2 = 2 B_hat^2 - I was formed
                             from the power iteration's squaring (reading R29); 0 elsewhere */
+  int32_t line12_in_recurrence;  /* 1: Alg. 1 line 12 (Y = H_hat X) ran inside the recurrence launch
+                                    (m-chain mode, left side), its time in ms_recurrence */
 } cpa_svt_info;
 
 /* Multi-GPU sharding of the long dimension for cpa_svt_apply (handles with a communicator). */

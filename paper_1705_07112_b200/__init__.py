@@ -52,7 +52,8 @@ class Info(ctypes.Structure):
                 ("side", ctypes.c_int32), ("degenerate", ctypes.c_int32),
                 ("ms_gram", ctypes.c_float), ("ms_allreduce", ctypes.c_float), ("ms_power", ctypes.c_float),
                 ("ms_recurrence", ctypes.c_float), ("ms_total", ctypes.c_float),
-                ("kernel_launches", ctypes.c_int32), ("form", ctypes.c_int32), ("rec_products", ctypes.c_int32)]
+                ("kernel_launches", ctypes.c_int32), ("form", ctypes.c_int32), ("rec_products", ctypes.c_int32),
+                ("line12_in_recurrence", ctypes.c_int32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

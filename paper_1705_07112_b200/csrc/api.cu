@@ -60,7 +60,8 @@ cudaError_t dense_haar_split(const double* X, int64_t m, int64_t n, int64_t ldx,
 cudaError_t dense_haar_combine(const double* YL, const double* AH, const SeriesParams* P, int64_t m, int64_t n,
                                bool left, double* Y, int64_t ldy, int num_sms, cudaStream_t st);
 cudaError_t dense_eye(double* I, int64_t s, cudaStream_t st);
-size_t dense_sym_sync_ints(int64_t s, int K, int num_sms);
+size_t dense_sym_sync_ints(int64_t s, int K, int num_sms, int64_t L = 0);
+size_t dense_sym_l12_partial_doubles(int64_t s, int64_t L, int num_sms);
 int64_t dense_sym_ntri(int64_t s);
 int64_t dense_sym_panel_tile0(int64_t s, int p, int P);
 int64_t dense_sym_panel_slot(int64_t s, int P);
@@ -76,7 +77,8 @@ cudaError_t dense_sym_init(int64_t s, const double* G, double* Wa, double* H, co
 cudaError_t dense_cheb_sym(int64_t s, const double* G, double* W0, double* W1, double* W2, double* H,
                            const SeriesParams* P, int K, int* sync, double* partial, int num_sms, cudaStream_t st,
                            int m = 0, double* const* chain = nullptr, double* const* HX = nullptr,
-                           bool psi2_given = false);
+                           bool psi2_given = false, const double* X = nullptr, int64_t ldx = 0, double* Y = nullptr,
+                           int64_t ldy = 0, int64_t L = 0, double* l12_partial = nullptr);
 cudaError_t dense_cheb_flow(bool left, int64_t m, int64_t n, const double* G, const double* X, int64_t ldx,
                             double* Wa, double* Wb, double* Y, int64_t ldy, const SeriesParams* P, int K, int* sync,
                             double* partial, int num_sms, cudaStream_t st);
@@ -556,6 +558,7 @@ static cpa_svt_status fill_info(cpa_svt_handle* h, cpa_svt_info* info, cpa_svt_l
     info->side = side;
     info->degenerate = hp.degenerate;
     info->rec_products = 0;   // (set by the dense fp64 s x s path after this call)
+    info->line12_in_recurrence = 0;
   }
   if (lam && lam->want_lambda) {
     lam->lambda_hat = hp.lambda_hat;
@@ -824,14 +827,19 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
   // chains' rotations beside Wa / Wb / Is, the accumulators HX of all chains but the first)
   const int chain = form == 2 && !panels && !sparse_eps ? dense_sym_use_chain(s, K, h->num_sms) : 0;
   const size_t nCh = chain ? (size_t)(5 * chain - 4) * nG : 0;
+  // line 12 folded into the m-chain launch (left side, device-resident Y, no transform; TMA needs
+  // 16-byte rows of X): its units follow the last product's, row panel by row panel of H_hat
+  const bool fold12 = chain && left && !h->hp_Y && !dct && h->transform == 0 && ldx % 2 == 0 &&
+                      ((uintptr_t)X & 15) == 0 && !env_on("CPA_SVT_NO_L12_FOLD");
+  const size_t nP12 = fold12 ? r32(dense_sym_l12_partial_doubles(s, n, h->num_sms)) : 0;
   const bool final_split = !env_on("CPA_SVT_FINAL_NOSPLIT");  // line-12 product split-K (default on)
   const size_t nPart = r32(std::max({dense_flow_partial_doubles(RM, RN, h->num_sms), dense_gram_partial_doubles(s),
                                      form == 2 ? dense_sym_partial_doubles(s, h->num_sms, chain) : (size_t)0,
                                      panels ? dense_sym_panel_partial_doubles(s, panel_P, h->num_sms) : (size_t)0,
                                      final_split && poly ? dense_store_partial_doubles(m, n) : (size_t)0}));
   const size_t nSync = std::max({dense_flow_sync_ints(RM, RN, K), (size_t)((s / 64 + 2) * (s / 64 + 2)),
-                                 dense_sym_sync_ints(s, K, h->num_sms), (size_t)1332});
-  const size_t need = (nG + 2 * nW + nX + nPow + nPart + nGb + nPR + nCh) * sizeof(double) + nSync * sizeof(int) + 256;
+                                 dense_sym_sync_ints(s, K, h->num_sms, fold12 ? n : 0), (size_t)1332});
+  const size_t need = (nG + 2 * nW + nX + nPow + nPart + nGb + nPR + nCh + nP12) * sizeof(double) + nSync * sizeof(int) + 256;
   cpa_svt_status st = grow(h, &h->ws, &h->ws_bytes, need);
   if (st != CPA_SVT_OK) return st;
   double* G = (double*)h->ws;
@@ -844,7 +852,8 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
   double* gbuf = part + nPart;    // panel mode: P all-gather slots of packed 64 x 64 tiles
   double* prs = gbuf + nGb;       // panel mode: row-sharded power iteration scratch
   double* chb = prs + nPR;         // m-chain mode: 5m - 4 s x s buffers
-  int* flow_sync = (int*)(chb + nCh);
+  double* p12 = chb + nCh;         // line 12 in the m-chain launch: its split-K partials
+  int* flow_sync = (int*)(p12 + nP12);
   const double* psi2_sq = nullptr;  // m-chain mode: c^2 (device) when chb holds c^2 G^2
 
   const double* c_dev = nullptr;
@@ -1035,7 +1044,7 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
             }
             double* hx[2] = {nxt, nxt + nG};
             CU(dense_cheb_sym(s, G, Is, Wa, Wb, H, h->P, K, flow_sync, part, h->num_sms, h->stream, chain, cb, hx,
-                              psi2_sq != nullptr));
+                              psi2_sq != nullptr, fold12 ? X : nullptr, ldx, Y, ldy, n, p12));
           } else {
             CU(dense_cheb_sym(s, G, Is, Wa, Wb, H, h->P, K, flow_sync, part, h->num_sms, h->stream));  // Is: 3rd W buffer
           }
@@ -1088,6 +1097,8 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
       }
       --launches;
       h->hp_Y = nullptr;   // delivered
+    } else if (fold12) {
+      --launches;   // (line 12 ran inside the recurrence launch)
     } else {
       if (left) CU(dense_gemm_store(s, n, s, Hm, s, X, ldx, Y, ldy, h->stream, fp, fs));
       else      CU(dense_gemm_store(m, s, s, X, ldx, Hm, s, Y, ldy, h->stream, fp, fs));
@@ -1108,6 +1119,7 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
     info->kernel_launches = launches;
     info->form = form;
     info->rec_products = poly && K > 2 ? K - (psi2_sq ? 3 : 2) : 0;
+    info->line12_in_recurrence = fold12 ? 1 : 0;
   }
   return st;
 }

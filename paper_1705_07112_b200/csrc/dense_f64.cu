@@ -400,6 +400,16 @@ struct SymArgs {
   double* HX[2];
   int red_bias;         // chains: the reducing split's k-range is (100 + red_bias)% of the others'
   int k0;               // first step of the launch: 2, or 3 when Psi_2 is given (k_sym_init from G^2)
+  // m chains, left side: Alg. 1 line 12 (Y = H_hat X, X: s x L) appended to the launch as units
+  // (row panel r, column tile c, k-split q) after the last product's; a unit waits for cross r of
+  // step K-1 (H_hat's row panel r final)
+  int l12;              // 0: line 12 runs as its own launch
+  double* Y;
+  int64_t ldy, L;
+  int l12_tn, l12_split;   // column tiles of Y, k-splits per line-12 tile
+  double* l12_partial;     // tiles * (l12_split - 1) * 64 * 64
+  const double* X;         // (host side: the map of line 12's B operand)
+  int64_t ldx;
 };
 
 // Buffer of Psi_k in m-chain mode (k >= 1): Psi_k overwrites Psi_{k-3m} of its own chain.
@@ -417,6 +427,8 @@ __host__ __device__ __forceinline__ int sym_tdone_off(int K, int T, int m) {
 __host__ __device__ __forceinline__ int sym_pm_off(int K, int T, int m) {
   return sym_tdone_off(K, T, m) + K * (T * (T + 1) / 2);
 }
+// (line 12 in the launch: its split-K counters, one per Y tile, after the Psi_m count)
+__host__ __device__ __forceinline__ int sym_l12_off(int K, int T, int m) { return sym_pm_off(K, T, m) + 1; }
 
 // Psi_2 from the power iteration's squaring (m-chain mode): G2 holds c^2 G^2 (c^2 = *c2, an exact
 // power of 2, k_diag_scale); Psi_2 = 2 B_hat^2 - I = 2 a^2 G^2 - 4 a G + I with a = 2/L (Alg. 1
@@ -829,10 +841,11 @@ struct SymMaps {
   CUtensorMap g;
   CUtensorMap w[3];
 };
-struct SymMapsChain {   // m-chain mode: plus the maps of SymArgs::C
+struct SymMapsChain {   // m-chain mode: plus the maps of SymArgs::C (and line 12's H_hat, X)
   CUtensorMap g;
   CUtensorMap w[3];
   CUtensorMap c[12];
+  CUtensorMap h, x;
 };
 template <int CH>
 using SymMapsT = typename std::conditional<(CH > 1), SymMapsChain, SymMaps>::type;
@@ -860,6 +873,65 @@ __device__ __forceinline__ uint64_t smid_now() {
 }
 #endif
 
+// Line 12 unit's epilogue (m-chain launch): split-K publish / fixed-order reduce (the reducer q =
+// S-1 waits for the others), then Y = the tile's sum (row r0.., column c0.. of the caller's Y).
+__device__ __forceinline__ void l12_finish(const SymArgs& a, int t12, int q, int64_t r0, int64_t c0,
+                                           double (&acc)[4][4][2]) {
+  constexpr int NT = NTHREADS, NV = 32;
+  const int u = threadIdx.x;
+  const int warp = u >> 5, lane = u & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int S = a.l12_split;
+  if (S > 1) {
+    double* slot = a.l12_partial + (int64_t)t12 * (S - 1) * (BM * BN);
+    int* cnt = a.sync + sym_l12_off(a.K, a.T, a.chain) + t12;
+    if (q < S - 1) {
+      double* mine = slot + (int64_t)q * (BM * BN);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) __stcg(mine + ((i * 4 + j) * 2 + e) * NT + u, acc[i][j][e]);
+      __syncthreads();
+      if (u == 0) red_release_add_i32(cnt, 1);
+      return;
+    }
+    if (u == 0) wait_geq(cnt, S - 1);
+    __syncthreads();
+#pragma unroll
+    for (int c8 = 0; c8 < NV / 8; ++c8) {
+      double sum[8];
+#pragma unroll
+      for (int x = 0; x < 8; ++x) sum[x] = __ldcg(slot + (c8 * 8 + x) * NT + u);
+      for (int p = 1; p < S - 1; ++p) {
+        double v[8];
+#pragma unroll
+        for (int x = 0; x < 8; ++x) v[x] = __ldcg(slot + (int64_t)p * (BM * BN) + (c8 * 8 + x) * NT + u);
+#pragma unroll
+        for (int x = 0; x < 8; ++x) sum[x] += v[x];
+      }
+#pragma unroll
+      for (int x = 0; x < 8; ++x) {
+        const int rr = c8 * 8 + x;
+        acc[rr >> 3][(rr >> 1) & 3][rr & 1] = sum[x] + acc[rr >> 3][(rr >> 1) & 3][rr & 1];
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t rr = r0 + wm + i * 8 + g;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t c = c0 + wn + j * 8 + 2 * t + e;
+        if (rr < a.s && c < a.L) a.Y[rr * a.ldy + c] = acc[i][j][e];
+      }
+  }
+}
+
 template <int SBK, int SSTAGES, bool PANEL, int NW = 4, int CH = 0>
 __global__ void __launch_bounds__(32 * NW, CPA_FLOW_MINB)
     k_cheb_sym_tma(const __grid_constant__ SymMapsT<CH> mp, SymArgs a) {
@@ -876,7 +948,9 @@ __global__ void __launch_bounds__(32 * NW, CPA_FLOW_MINB)
   const int ntri = T * (T + 1) / 2;
   const int S = a.split;
   const int per_step = (PANEL ? a.ntile : ntri) * S;
-  const int total = PANEL ? per_step : (a.K - (CH > 1 ? a.k0 : 2)) * per_step;
+  const int rec_total = PANEL ? per_step : (a.K - (CH > 1 ? a.k0 : 2)) * per_step;
+  // (m chains: line 12's units after the recurrence's)
+  const int total = rec_total + ((CH > 1 && a.l12) ? T * a.l12_tn * a.l12_split : 0);
   int* cross = a.sync + 1;
   const int nk = (int)((a.s + SBK - 1) / SBK);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -917,22 +991,32 @@ __global__ void __launch_bounds__(32 * NW, CPA_FLOW_MINB)
     }
 #endif
     if (tk >= total) break;
-    const int k = PANEL ? a.kstep : (CH > 1 ? a.k0 : 2) + tk / per_step;
-    const int r = tk % per_step;
-    const int q = r % S;
-    const int tile = r / S + (PANEL ? a.tile0 : 0);
-    int ti, tj;
-    tri_decode_colmajor(tile, T, ti, tj);
-    CPA_DCHECK(ti >= 0 && ti < T && tj >= 0 && tj <= ti);
+    const bool is12 = CHAIN && tk >= rec_total;   // a line-12 unit (Y tile (ti, tj), k-split q)
+    int k, q, tile, ti, tj;
+    if (is12) {
+      const int u12 = tk - rec_total;
+      q = u12 % a.l12_split;
+      tile = u12 / a.l12_split;
+      ti = tile / a.l12_tn;
+      tj = tile % a.l12_tn;
+      k = a.K;
+    } else {
+      k = PANEL ? a.kstep : (CH > 1 ? a.k0 : 2) + tk / per_step;
+      const int r = tk % per_step;
+      q = r % S;
+      tile = r / S + (PANEL ? a.tile0 : 0);
+      tri_decode_colmajor(tile, T, ti, tj);
+      CPA_DCHECK(ti >= 0 && ti < T && tj >= 0 && tj <= ti);
+    }
     // B operand: W_{k-1} (one chain; a G step of the m-chain mode: Psi_{k-1}) / Psi_{k-m} (a chain
-    // product, k > m); A operand: the static G, or Psi_m for the chain products
+    // product, k > m) / X (line 12); A operand: the static G, Psi_m for the chain products, or H_hat
     constexpr int mc = CHAIN ? CH : 1;
-    const bool cstep = CHAIN && k > mc;
+    const bool cstep = CHAIN && k > mc && !is12;
     const CUtensorMap* wmap;
     const CUtensorMap* amap;
     if constexpr (CHAIN) {
-      wmap = &mp.c[chain_buf(cstep ? k - mc : k - 1, mc)];
-      amap = cstep ? &mp.c[mc - 1] : &mp.g;
+      wmap = is12 ? &mp.x : &mp.c[chain_buf(cstep ? k - mc : k - 1, mc)];
+      amap = is12 ? &mp.h : cstep ? &mp.c[mc - 1] : &mp.g;
     } else {
       wmap = &mp.w[(k - 1) % 3];
       amap = &mp.g;
@@ -940,9 +1024,10 @@ __global__ void __launch_bounds__(32 * NW, CPA_FLOW_MINB)
     const int m0 = ti * BM, n0 = tj * BN;
     int kb = (int)((int64_t)nk * q / S), ke = (int)((int64_t)nk * (q + 1) / S);
     if (CHAIN) {   // the reducer (q = S - 1) starts last and sums the others: a longer k-range
-      const int64_t wt = 100 * S + a.red_bias;
+      const int SS = is12 ? a.l12_split : S;
+      const int64_t wt = 100 * SS + (is12 ? 0 : a.red_bias);
       kb = (int)((int64_t)nk * q * 100 / wt);
-      ke = q == S - 1 ? nk : (int)((int64_t)nk * (q + 1) * 100 / wt);
+      ke = q == SS - 1 ? nk : (int)((int64_t)nk * (q + 1) * 100 / wt);
     }
     const int nku = ke - kb;
     if (warp == 0) {
@@ -950,7 +1035,7 @@ __global__ void __launch_bounds__(32 * NW, CPA_FLOW_MINB)
       // lanes poll the unit's dependency flags in parallel (each satisfied wait costs one L2 round
       // trip, not one per flag); after the warp barrier lane 0 issues the B slabs (and late A slabs)
       const int P = nku < SSTAGES - 1 ? nku : SSTAGES - 1;
-      bool a_early = true;
+      bool a_early = !is12;   // (line 12: H_hat's rows are final only after the dependency)
       if (cstep) {
         const int v = lane == 0 ? ld_acquire(a.sync + sym_pm_off(a.K, T, mc)) : 0;
         a_early = __shfl_sync(0xffffffffu, v, 0) >= ntri;
@@ -992,7 +1077,9 @@ __global__ void __launch_bounds__(32 * NW, CPA_FLOW_MINB)
         const bool need_h = CHAIN && k == a.K - 1;
         // flag list: [0, 1] crosses ti, tj of khaz | [2] own tile of kprev | [3] own tile of step m |
         // [4, 5] own tiles of steps K-2, K-3 (last product) | B tiles l0..l1 | A tiles l0..l1
-        if (!CHAIN) {
+        if (is12) {
+          if (lane == 0) wait_geq(cross + (a.K - 1) * T + ti, T);   // H_hat's row panel ti is final
+        } else if (!CHAIN) {
           // one chain (the round-1/2 lane layout, kept instruction for instruction: this kernel's
           // claim-to-start path is measurably sensitive to code changes): lanes 0, 1 crosses ti, tj
           // of step k-2, lane 2 the own tile of step k-1, lanes 3.. the B tiles (29 per pass)
@@ -1116,6 +1203,12 @@ __global__ void __launch_bounds__(32 * NW, CPA_FLOW_MINB)
       continue;
     }
 #endif
+    if constexpr (CH > 1 && NW == 4) {
+      if (is12) {
+        l12_finish(a, tile, q, (int64_t)m0, (int64_t)n0, acc);
+        continue;
+      }
+    }
     sym_finish<true, PANEL, NW, CH>(a, k, tile, q, ti, tj, acc);
 #ifdef CPA_SYM_TRACE
     if (threadIdx.x == 0 && tk < kTraceUnits) g_trace[tk * 6 + 4] = trace_now();
@@ -2321,9 +2414,11 @@ static int sym_split(int64_t s, int slots, int64_t ntiles = -1) {
   return S;
 }
 
-size_t dense_sym_sync_ints(int64_t s, int K, int num_sms) {
+size_t dense_sym_sync_ints(int64_t s, int K, int num_sms, int64_t L) {
   (void)num_sms;
   const int64_t T = (s + BM - 1) / BM;
+  if (L > 0)   // (+ line 12 in the m-chain launch: one split-K counter per Y tile)
+    return dense_sym_sync_ints(s, K, num_sms, 0) + (size_t)(T * ((L + BN - 1) / BN));
   // [0] ticket | K * T cross counters | up to 3 ntri split counters (m chains) | K * ntri tile-done
   // flags | Psi_m count
   return (size_t)(1 + (int64_t)K * T + 3 * (T * (T + 1) / 2) + (int64_t)K * (T * (T + 1) / 2) + 1);
@@ -2383,9 +2478,22 @@ static cudaError_t sym_launch(SymArgs& a, int64_t total, int slots, int num_sms,
 // H_hat += sum_{k=2}^{K-1} c_k Psi_k(B_hat) on the s x s Gram: one persistent launch
 // for all K-2 steps.  W0, W1, W2: s x s buffers, W1 = W_1 from dense_sym_init.  m-chain mode
 // (m > 1: 4m s x s buffers in chain, chain[0] = W1 = Psi_1, plus m - 1 accumulators HX).
+static int sym_l12_split(int64_t s, int64_t L, int num_sms) {
+  const int64_t T = (s + BM - 1) / BM, tn = (L + BN - 1) / BN;
+  int S = sym_split(s, sym_slots(num_sms), T * tn);
+  if (const char* v = getenv("CPA_SVT_L12_SPLIT")) S = (atoi(v) > 0 && atoi(v) <= 16) ? atoi(v) : S;
+  return S;
+}
+size_t dense_sym_l12_partial_doubles(int64_t s, int64_t L, int num_sms) {
+  const int64_t T = (s + BM - 1) / BM, tn = (L + BN - 1) / BN;
+  const int S = sym_l12_split(s, L, num_sms);
+  return S > 1 ? (size_t)(T * tn * (S - 1) * BM * BN) : 0;
+}
+
 cudaError_t dense_cheb_sym(int64_t s, const double* G, double* W0, double* W1, double* W2, double* H,
                            const SeriesParams* P, int K, int* sync, double* partial, int num_sms, cudaStream_t st,
-                           int m, double* const* chain, double* const* HX, bool psi2_given) {
+                           int m, double* const* chain, double* const* HX, bool psi2_given, const double* X,
+                           int64_t ldx, double* Y, int64_t ldy, int64_t L, double* l12_partial) {
   if (s == 0 || K <= 2) return cudaSuccess;
   SymArgs a{};
   a.s = s; a.G = G; a.W[0] = W0; a.W[1] = W1; a.W[2] = W2; a.H = H; a.P = P; a.K = K;
@@ -2404,7 +2512,19 @@ cudaError_t dense_cheb_sym(int64_t s, const double* G, double* W0, double* W1, d
   a.sync = sync;
   a.partial = partial;
   a.vec = aligned16(G, s) && aligned16(W0, s) && aligned16(W1, s) && aligned16(W2, s);
-  cudaError_t e = cudaMemsetAsync(sync, 0, dense_sym_sync_ints(s, K, num_sms) * sizeof(int), st);
+  // line 12 (Y = H_hat X, left side) folded into the m-chain launch (X rows 16-byte aligned for TMA)
+  if (a.chain && X && Y && L > 0 && ldx % 2 == 0 && ((uintptr_t)X & 15) == 0 && !sym_use_pp(a.chain)) {
+    a.l12 = 1;
+    a.Y = Y;
+    a.ldy = ldy;
+    a.L = L;
+    a.l12_tn = (int)((L + BN - 1) / BN);
+    a.l12_split = sym_l12_split(s, L, num_sms);
+    a.l12_partial = l12_partial;
+    a.X = X;
+    a.ldx = ldx;
+  }
+  cudaError_t e = cudaMemsetAsync(sync, 0, dense_sym_sync_ints(s, K, num_sms, a.l12 ? L : 0) * sizeof(int), st);
   if (e != cudaSuccess) return e;
   a.k0 = 2;
   if (a.chain && psi2_given) {   // Psi_2 formed by the init from the squaring's G^2: start at k = 3
@@ -2431,7 +2551,8 @@ cudaError_t dense_cheb_sym(int64_t s, const double* G, double* W0, double* W1, d
     if (cs == 4) return go(k_cheb_sym_cl<4>, 4);
     return go(k_cheb_sym_cl<8>, 8);
   }
-  const int64_t total = (int64_t)(K - a.k0) * a.T * (a.T + 1) / 2 * a.split;
+  const int64_t total = (int64_t)(K - a.k0) * a.T * (a.T + 1) / 2 * a.split +
+                        (a.l12 ? (int64_t)a.T * a.l12_tn * a.l12_split : 0);
   return sym_launch(a, total, slots, num_sms, st);
 }
 
@@ -2455,6 +2576,18 @@ static cudaError_t sym_launch(SymArgs& a, int64_t total, int slots, int num_sms,
     for (int i = 0; i < 4 * a.chain; ++i) {
       ops[4 + i] = a.C[i];
       maps[4 + i] = &mpc.c[i];
+    }
+    if (a.l12 && ok) {   // line 12 in the m-chain launch: H_hat (symmetric, as G) and X (s x L, ld)
+      cuuint64_t hd[2] = {(cuuint64_t)s, (cuuint64_t)s}, hs[1] = {(cuuint64_t)(s * sizeof(double))};
+      cuuint64_t xd[2] = {(cuuint64_t)a.L, (cuuint64_t)s}, xs[1] = {(cuuint64_t)(a.ldx * sizeof(double))};
+      cuuint32_t box[2] = {16u, (cuuint32_t)sbk}, estr[2] = {1u, 1u};
+      ok = fn(&mpc.h, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)a.H, hd, hs, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+               CUDA_SUCCESS &&
+           fn(&mpc.x, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)a.X, xd, xs, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+               CUDA_SUCCESS;
+      if (!ok) return cudaErrorInvalidValue;
     }
     for (int i = 0; i < nmaps && ok; ++i) {
       cuuint64_t dims[2] = {(cuuint64_t)s, (cuuint64_t)s};
@@ -2578,7 +2711,7 @@ cudaError_t dense_cheb_sym_panel(int64_t s, const double* G, double* W0, double*
   a.tile0 = (int)tile0;
   a.ntile = (int)ntile;
   a.gout = gout;
-  cudaError_t e = cudaMemsetAsync(sync, 0, dense_sym_sync_ints(s, K, num_sms) * sizeof(int), st);
+  cudaError_t e = cudaMemsetAsync(sync, 0, dense_sym_sync_ints(s, K, num_sms, 0) * sizeof(int), st);
   if (e != cudaSuccess) return e;
   return sym_launch(a, ntile * a.split, slots, num_sms, st);
 }

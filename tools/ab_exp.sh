@@ -1,4 +1,4 @@
-# sparse c4 SpMM pair (tools/sparse_step.py)
-echo "nohint"; CPA_SVT_SP_NOHINT=1 python tools/sparse_step.py 5 1
-echo "hint"; python tools/sparse_step.py 5 1
-echo "hint U4"; CPA_SVT_SP_UNROLL=4 python tools/sparse_step.py 5 1
+for r in 1 2; do
+  echo "line 12 folded"; python tools/ab_c2.py . 30
+  echo "separate line 12"; CPA_SVT_NO_L12_FOLD=1 python tools/ab_c2.py . 30
+done
