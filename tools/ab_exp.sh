@@ -1,4 +1,6 @@
 for r in 1 2; do
-  echo "line 12 folded"; python tools/ab_c2.py . 30
-  echo "separate line 12"; CPA_SVT_NO_L12_FOLD=1 python tools/ab_c2.py . 30
+  echo "default"; python tools/ab_c2.py . 30
+  echo "last arrival"; CPA_SVT_CHAIN_LAST=1 python tools/ab_c2.py . 30
+  echo "last arrival S=2"; CPA_SVT_CHAIN_LAST=1 CPA_SVT_CHAIN_SPLIT=2 python tools/ab_c2.py . 30
+  echo "last arrival S=4"; CPA_SVT_CHAIN_LAST=1 CPA_SVT_CHAIN_SPLIT=4 python tools/ab_c2.py . 30
 done
