@@ -1,6 +1,4 @@
 for r in 1 2; do
-  echo "default"; python tools/ab_c2.py . 30
-  echo "last arrival"; CPA_SVT_CHAIN_LAST=1 python tools/ab_c2.py . 30
-  echo "last arrival S=2"; CPA_SVT_CHAIN_LAST=1 CPA_SVT_CHAIN_SPLIT=2 python tools/ab_c2.py . 30
-  echo "last arrival S=4"; CPA_SVT_CHAIN_LAST=1 CPA_SVT_CHAIN_SPLIT=4 python tools/ab_c2.py . 30
-done
+for sp in 0 2 3 4; do
+  if [ $sp = 0 ]; then echo "gram split default"; python tools/ab_c2.py . 30; else echo "gram split $sp"; CPA_SVT_GRAM_SPLIT=$sp python tools/ab_c2.py . 30; fi
+done; done
