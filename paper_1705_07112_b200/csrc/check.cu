@@ -8,6 +8,8 @@
 // anywhere in Y fails the comparison too.  The sums of squares are block partials added
 // in a fixed order (deterministic), and the verdict lands in SeriesParams::diverged,
 // which the host reads when the call synchronises (fill_info in api.cu).
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace cpa {
@@ -31,7 +33,37 @@ __global__ void __launch_bounds__(kCheckThreads) k_divcheck(const T* __restrict_
   double acc = 0.0;
   const int64_t n = rows * cols;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  if (ld == cols) {
+  constexpr int VW = 16 / sizeof(T);   // elements per 16-byte load
+  if (ld == cols && (reinterpret_cast<uintptr_t>(A) & 15) == 0) {
+    // 16-byte loads, four in flight per thread (c2: 10.7 -> ~3 us per check)
+    using V = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
+    const V* A4 = reinterpret_cast<const V*>(A);
+    const int64_t nv = n / VW;
+    double a4[4] = {0.0, 0.0, 0.0, 0.0};
+    int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    for (; e + 3 * stride < nv; e += 4 * stride) {
+      V v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldcs(A4 + e + u * stride);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const T* x = reinterpret_cast<const T*>(&v[u]);
+#pragma unroll
+        for (int i = 0; i < VW; ++i) a4[u] += (double)x[i] * (double)x[i];
+      }
+    }
+    for (; e < nv; e += stride) {
+      const V v = __ldcs(A4 + e);
+      const T* x = reinterpret_cast<const T*>(&v);
+#pragma unroll
+      for (int i = 0; i < VW; ++i) a4[0] += (double)x[i] * (double)x[i];
+    }
+    for (int64_t t = nv * VW + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += stride) {
+      const double v = (double)A[t];
+      a4[0] += v * v;
+    }
+    acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+  } else if (ld == cols) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += stride) {
       const double v = (double)A[e];
       acc += v * v;
