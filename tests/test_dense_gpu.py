@@ -473,3 +473,37 @@ def test_pingpong_recurrence_bitwise(env, m, s, L, K, split):
     assert np.array_equal(out["0"], out["1"])
     if s <= 1100:
         assert O.rel_fro(out["1"], O.cpa_shrink(X, O.Kernel(**kern), K, T=100)) <= TOL64
+
+
+@pytest.mark.parametrize("case", ["left", "left_odd_ld", "right"])
+def test_chain_line12_fold_variants(env, case):
+    """Line 12 inside the m-chain launch (left side, 16-byte X rows) against the separate line-12
+    product (CPA_SVT_NO_L12_FOLD) and the oracle; an odd leading dimension of X and the right side
+    fall back to the separate product (info.line12_in_recurrence = 0) and meet the same bar."""
+    import os
+    torch, P, _ = env
+    if case == "right":
+        X = W.gen_c2(m=1100, n=1024, seed=5)
+        Xd = torch.from_numpy(X).cuda()
+    else:
+        X = W.gen_c2(m=1024, n=1100, seed=6)
+        if case == "left_odd_ld":
+            buf = torch.zeros((1024, 1101), dtype=torch.float64, device="cuda")
+            buf[:, :1100] = torch.from_numpy(X).cuda()
+            Xd = buf[:, :1100]
+        else:
+            Xd = torch.from_numpy(X).cuda()
+    kern = {"kind": "soft", "tau": 0.05, "tau_relative": True}
+    h2 = P.Handle(0)
+    Y, info = h2.apply(Xd, kern, 30, T=300, info=True)
+    os.environ["CPA_SVT_NO_L12_FOLD"] = "1"
+    try:
+        Ysep = h2.apply(Xd, kern, 30, T=300)
+    finally:
+        os.environ.pop("CPA_SVT_NO_L12_FOLD", None)
+    h2.close()
+    Y, Ysep = Y.cpu().numpy(), Ysep.cpu().numpy()
+    assert info["line12_in_recurrence"] == (1 if case == "left" else 0)
+    assert info["rec_products"] == 27   # Psi_2 from the power iteration's squaring (R29)
+    assert O.rel_fro(Y, Ysep) <= 1e-12
+    assert O.rel_fro(Y, O.cpa_shrink(X, O.Kernel(**kern), 30, T=300)) <= TOL64
