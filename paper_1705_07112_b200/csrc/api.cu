@@ -188,6 +188,7 @@ struct cpa_svt_handle {
   cudaStream_t stream = nullptr;
   int rank = 0, world = 1;
   ncclComm_t comm = nullptr;
+  int* dvote = nullptr;            // sharded calls: the ranks' pre-collective status vote (device int)
   int num_sms = 148;
   SeriesParams* P = nullptr;       // device
   unsigned int* bar = nullptr;     // device, 2 uints (grid barrier)
@@ -432,6 +433,10 @@ cpa_svt_status cpa_svt_init(cpa_svt_handle** out, int device, void* cuda_stream,
       cpa_svt_free(h);
       return CPA_SVT_E_NCCL;
     }
+    if (cudaMalloc(&h->dvote, sizeof(int)) != cudaSuccess) {
+      cpa_svt_free(h);
+      return CPA_SVT_E_NOMEM;
+    }
   }
   *out = h;
   return CPA_SVT_OK;
@@ -443,6 +448,7 @@ cpa_svt_status cpa_svt_free(cpa_svt_handle* h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   else cudaDeviceSynchronize();
   if (h->comm) g_nccl.CommDestroy(h->comm);
+  cudaFree(h->dvote);
   cudaFree(h->P);
   cudaFree(h->bar);
   cudaFree(h->d_c);
@@ -604,6 +610,23 @@ static cpa_svt_status guard_check(cpa_svt_handle* h, cpa_svt_status st) {
 
 // SPEC.md:215 divergence check of the output against the input (check.cu); the verdict is read
 // by fill_info / read_verdict.  Off with CPA_SVT_OPT_DIVERGENCE = 0.
+// Sharded calls: every rank reaches this point before its first collective, whatever its local
+// status (a workspace that failed to grow on one rank only); the worst status over the ranks is
+// returned on all of them, so either every rank enqueues the collectives or none does (ADVICE r1:
+// a rank returning early would leave its peers waiting inside NCCL).  One int all-reduce + a sync.
+static cpa_svt_status rank_vote(cpa_svt_handle* h, cpa_svt_status local) {
+  if (!h->comm || !h->dvote) return local;
+  int v = (int)local;
+  if (cudaMemcpyAsync(h->dvote, &v, sizeof(int), cudaMemcpyHostToDevice, h->stream) != cudaSuccess)
+    return CPA_SVT_E_CUDA;
+  if (g_nccl.AllReduce(h->dvote, h->dvote, 1, ncclInt32, ncclMax, h->comm, h->stream) != ncclSuccess)
+    return CPA_SVT_E_NCCL;
+  if (cudaMemcpyAsync(&v, h->dvote, sizeof(int), cudaMemcpyDeviceToHost, h->stream) != cudaSuccess ||
+      cudaStreamSynchronize(h->stream) != cudaSuccess)
+    return CPA_SVT_E_CUDA;
+  return (cpa_svt_status)v;
+}
+
 static cpa_svt_status check_f64(cpa_svt_handle* h, const double* X, int64_t xr, int64_t xc, int64_t ldx,
                                 const double* Y, int64_t yr, int64_t yc, int64_t ldy, int* launches) {
   if (!h->div_mode) return CPA_SVT_OK;
@@ -841,6 +864,7 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
                                  dense_sym_sync_ints(s, K, h->num_sms, fold12 ? n : 0), (size_t)1332});
   const size_t need = (nG + 2 * nW + nX + nPow + nPart + nGb + nPR + nCh + nP12) * sizeof(double) + nSync * sizeof(int) + 256;
   cpa_svt_status st = grow(h, &h->ws, &h->ws_bytes, need);
+  if (sharded) st = rank_vote(h, st);
   if (st != CPA_SVT_OK) return st;
   double* G = (double*)h->ws;
   double* Wa = G + nG;
@@ -1166,6 +1190,7 @@ static cpa_svt_status apply_tf32(cpa_svt_handle* h, int terms, int64_t m, int64_
   // | power scratch | panel mode: all-gather slots, row-sharded power scratch
   const size_t need = 4 * nA + 3 * nG + (poly ? 9 * nG : 3 * nA) + nPow + nGb + nPR + 256;
   cpa_svt_status st = grow(h, &h->ws, &h->ws_bytes, need);
+  if (sharded) st = rank_vote(h, st);
   if (st != CPA_SVT_OK) return st;
   char* b = (char*)h->ws;
   float* Xs[3] = {(float*)b, (float*)(b + nA), (float*)(b + 2 * nA)};
