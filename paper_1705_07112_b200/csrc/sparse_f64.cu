@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(SP_WARPS * 32) k_spmm_zx(const int64_t* cptr, 
                                                            const double* cval, int64_t m, int64_t n, int64_t nblk,
                                                            const double* __restrict__ Z, const double* Wp,
                                                            const double* Wpp, double* Wout, double* Yb,
-                                                           const SeriesParams* P, int k) {
+                                                           const SeriesParams* P, int k, int yterms) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t item = blockIdx.x * (int64_t)SP_WARPS + warp;  // item = b * n + l
   if (item >= nblk * n) return;
@@ -238,9 +238,17 @@ __global__ void __launch_bounds__(SP_WARPS * 32) k_spmm_zx(const int64_t* cptr, 
     if (Wout) Wout[o] = w;
     Yb[o] = 0.5 * P->c[0] * x + P->c[1] * w;       // Y = c0/2 W_0 + c1 W_1
   } else {
-    const double w = 2.0 * s2 * acc - 2.0 * Wp[o] - Wpp[o];  // W_k = 2 B_hat W_{k-1} - W_{k-2}
+    const double wp = Wp[o], wpp = Wpp[o];
+    const double w = 2.0 * s2 * acc - 2.0 * wp - wpp;   // W_k = 2 B_hat W_{k-1} - W_{k-2}
     if (Wout) Wout[o] = w;
-    Yb[o] += P->c[k] * w;                          // Y += c_k W_k
+    // Y += c_j W_j for the yterms latest j (1 to 3: W_{k-2}, W_{k-1} are in registers already), so Y
+    // is read and written once every third step (sparse_apply)
+    if (yterms > 0) {
+      double t = P->c[k] * w;
+      if (yterms >= 2) t = P->c[k - 1] * wp + t;
+      if (yterms >= 3) t = P->c[k - 2] * wpp + t;
+      Yb[o] += t;
+    }
   }
 }
 
@@ -360,6 +368,7 @@ cudaError_t sparse_apply(int64_t m, int64_t n, int64_t nnz, const int64_t* row_p
     // contention; the index loads of a pair ahead of the two gathers: Z 65 -> 55 ms)
     int U = 2;
     if (const char* v = getenv("CPA_SVT_SP_UNROLL")) U = atoi(v) == 8 ? 8 : atoi(v) == 4 ? 4 : 2;
+    const bool yevery = env_on("CPA_SVT_SP_YEVERY");
     const unsigned gz = (unsigned)((itemsZ + SP_WARPS - 1) / SP_WARPS);
     const unsigned gw = (unsigned)((itemsW + SP_WARPS - 1) / SP_WARPS);
     const double* prev = W0;   // W_{k-1}
@@ -384,7 +393,15 @@ cudaError_t sparse_apply(int64_t m, int64_t n, int64_t nnz, const int64_t* row_p
       {
         auto kw = k == 1 ? (U == 8 ? k_spmm_zx<8, true> : U == 4 ? k_spmm_zx<4, true> : k_spmm_zx<2, true>)
                          : (U == 8 ? k_spmm_zx<8, false> : U == 4 ? k_spmm_zx<4, false> : k_spmm_zx<2, false>);
-        kw<<<gw, SP_WARPS * 32, 0, st>>>(cptr, crow, cval, m, n, nblk, Z, prev, k == 1 ? nullptr : prev2, out, Yb, P, k);
+        // Y += c_j W_j in groups of three steps (k = 4, 7, 10, ...: the terms since the last group),
+        // the last step flushing the rest (CPA_SVT_SP_YEVERY=1: every step, Alg. 1's order)
+        int yt = 1;
+        if (!yevery && k >= 2) {
+          const int last = k - ((k - 1) % 3 == 0 ? 3 : (k - 1) % 3);   // the latest group step < k (1 = init)
+          yt = ((k - 1) % 3 == 0 || k == K - 1) ? k - last : 0;
+        }
+        kw<<<gw, SP_WARPS * 32, 0, st>>>(cptr, crow, cval, m, n, nblk, Z, prev, k == 1 ? nullptr : prev2, out, Yb, P, k,
+                                         yt);
       }
       ++L;
       if (hook) hook(hook_ctx, CPA_SVT_PH_SPARSE_W, 0);

@@ -131,3 +131,25 @@ def test_raw_coefficients_sparse():
         Y = h.apply_csr(*d, m, n, None, 6, lambda_max=lam, coeffs=c).cpu().numpy()
         assert O.rel_fro(Y, O.cpa_shrink(Xd, None, 6, lam=lam, coeffs=c)) <= 1e-12
     h.close()
+
+
+@pytest.mark.parametrize("K", [3, 4, 5, 6, 7, 8, 11, 13])
+def test_sparse_grouped_y_updates(env, K):
+    """Y += c_j W_j grouped over three steps (Y read and written every third step, the last step
+    flushing the rest; reading R30) against the per-step updates (CPA_SVT_SP_YEVERY=1, Alg. 1's
+    order) at rounding level and the oracle at the fp64 bar, for every residue of K."""
+    import os
+    torch, P, h = env
+    m, n = 60, 500
+    row_ptr, col, val = W.gen_c4(seed=K, m=m, n=n, nnz=1500)
+    kern = {"kind": "soft", "tau": 0.3, "tau_relative": True}
+    args = _dev(torch, row_ptr, col, val)
+    Y = h.apply_csr(*args, m, n, kern, K, T=60).cpu().numpy()
+    os.environ["CPA_SVT_SP_YEVERY"] = "1"
+    try:
+        Ye = h.apply_csr(*args, m, n, kern, K, T=60).cpu().numpy()
+    finally:
+        os.environ.pop("CPA_SVT_SP_YEVERY", None)
+    Yo = O.cpa_shrink(_dense(row_ptr, col, val, m, n), O.Kernel(**kern), K, T=60)
+    assert O.rel_fro(Y, Ye) <= 1e-13
+    assert O.rel_fro(Y, Yo) <= TOL64
