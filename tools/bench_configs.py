@@ -68,15 +68,19 @@ def dense(name, h, reps, m=None, n=None, K=None, dtype="f64", math="native"):
     Y = torch.empty_like(X)
     T = cfg["T"]
     ms, ph = timed(lambda: h.apply(X, cfg["kernel"], K, T=T, Y=Y, math=math), reps, h)
-    form = h.apply(X, cfg["kernel"], K, T=T, Y=Y, math=math, info=True)[1]["form"]
+    info = h.apply(X, cfg["kernel"], K, T=T, Y=Y, math=math, info=True)[1]
+    form = info["form"]
     s, L = min(m, n), max(m, n)
     # recurrence flops of the form that ran: 1 apply-to-X (K-1) 2 s^2 L; 2 symmetric s x s (K-2) s^2 (s+1)
     # (+ final 2 s^2 L); 3 s x s on full tiles (K-2) 2 s^3 (+ final)
     # 4: the whole SVT in one thread block (s <= 64, L <= 128): full s x s products, the step
     #    phase is the whole kernel
-    rec = {1: (K - 1) * 2 * s * s * L, 2: (K - 2) * s * s * (s + 1), 3: (K - 2) * 2 * s ** 3,
+    nprod = info.get("rec_products") or (K - 2)   # (K - 3 when Psi_2 came from the squaring, R29)
+    rec = {1: (K - 1) * 2 * s * s * L, 2: nprod * s * s * (s + 1), 3: (K - 2) * 2 * s ** 3,
            4: (K - 2) * 2 * s ** 3}[form]
-    F_exec = s * (s + 1) * L + rec + (0 if form == 1 else 2 * s * s * L)
+    if info.get("line12_in_recurrence"):   # line 12 ran inside the step launch (m-chain mode)
+        rec += 2 * s * s * L
+    F_exec = s * (s + 1) * L + rec + (0 if form == 1 or info.get("line12_in_recurrence") else 2 * s * s * L)
     F_eff = s * (s + 1) * L + (K - 1) * 2 * s * s * L   # bench.py's fixed per-workload count
     step_ms = ph.get("step", (0, 0))[0] + (ph.get("init", (0, 0))[0] if form == 1 else 0)
     r = {"config": name, "shape": [m, n], "K": K, "T": T, "dtype": dtype, "math": math,
