@@ -329,10 +329,11 @@ def test_small_kernel_against_grid_path_and_oracle(env, shape):
     assert O.rel_fro(Y1, Yo) <= TOL64
 
 
-@pytest.mark.parametrize("shape", [(40, 56), (150, 90)])
+@pytest.mark.parametrize("shape", [(40, 56), (150, 90), (90, 150)])
 def test_max_order(env, shape):
-    """K = CPA_SVT_KMAX (512) on the single-block path (40 x 56) and the grid path (150 x 90):
-    the coefficients of the 512-point rule and 510 recurrence steps against the oracle."""
+    """K = CPA_SVT_KMAX (512) on the single-block path (40 x 56) and the grid path (150 x 90; 90 x 150:
+    the two-chain launch with line 12 inside): the coefficients of the 512-point rule and 510
+    recurrence steps against the oracle."""
     X = W.random_dense(*shape, seed=21)
     kern = {"kind": "soft", "tau": 0.25, "tau_relative": True}
     Y, info = _run(env, X, kern, 512, T=60)
