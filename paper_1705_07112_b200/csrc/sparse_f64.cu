@@ -6,10 +6,10 @@
 //   W_k     = (4/L) Z X - 2 W_{k-1} - W_{k-2},  Y += c_k W_k   (fused epilogue)
 //   init:   W_1 = (2/L) (X X^T)|rows X - X,  Y = c_0/2 X + c_1 W_1
 //
-// Layout: this rank's rows [row_begin, row_end) are cut into blocks of 32
+// Layout: this rank's rows [row_begin, row_end) are cut into blocks of RB = 64
 // rows; every dense operand (W, Y, Z) is stored block-interleaved --
-// element (i, c) of block b at ((b * C + c) * 32 + i%32) -- so one warp owns a
-// block row and each gathered column c is one coalesced 256-byte load, and
+// element (i, c) of block b at ((b * C + c) * RB + i%RB) -- so one warp owns a
+// block row and each gathered column c is one coalesced 512-byte load, and
 // rows of a block never interact (the recurrence is row-independent).  Kernels
 // launch block-major, so the gathered W (or Z) block stays L2-resident.
 // Sums run in a fixed order (CSR row order / sorted CSC column order): the
@@ -25,8 +25,43 @@
 
 namespace cpa {
 
-constexpr int RB = 32;          // rows per interleaved block (= warp width)
+// Rows per interleaved block RB = 32 VW: lane l owns rows VW l .. VW l + VW - 1 of its block, so a
+// gathered column is one coalesced 32 VW x 8-byte warp load.  VW = 2 (512-byte gathers) moves
+// 19-20 TB/s of random L2 gathers where 256-byte ones (VW = 1) move 12.6 (tools/probes/
+// l2_gather512.cu); CPA_SP_VW=1 builds the 32-row layout.
+#ifndef CPA_SP_VW
+#define CPA_SP_VW 2
+#endif
+constexpr int VW = CPA_SP_VW;
+constexpr int RB = 32 * VW;     // rows per interleaved block
 constexpr int SP_WARPS = 8;     // warps per CTA in the SpMM kernels
+
+// VW consecutive doubles of a lane (one 8- or 16-byte access)
+struct Vw {
+  double v[VW];
+};
+__device__ __forceinline__ Vw ldv(const double* p) {
+  Vw r;
+  if constexpr (VW >= 2) {
+#pragma unroll
+    for (int h = 0; h < VW / 2; ++h) {
+      const double2 q = reinterpret_cast<const double2*>(p)[h];
+      r.v[2 * h] = q.x;
+      r.v[2 * h + 1] = q.y;
+    }
+  } else {
+    r.v[0] = *p;
+  }
+  return r;
+}
+__device__ __forceinline__ void stv(double* p, const Vw& a) {
+  if constexpr (VW >= 2) {
+#pragma unroll
+    for (int h = 0; h < VW / 2; ++h) reinterpret_cast<double2*>(p)[h] = make_double2(a.v[2 * h], a.v[2 * h + 1]);
+  } else {
+    *p = a.v[0];
+  }
+}
 
 __device__ __forceinline__ double warp_sum_sp(double v) {
 #pragma unroll
@@ -167,12 +202,14 @@ __global__ void k_row_split(const int64_t* row_ptr, const int32_t* col, int64_t 
 // sum_{e in [e0, e1)} x[e] V[idx[e]][lane] with U gathers in flight (U accumulators, the tail in
 // accumulator 0, summed in a fixed tree: a fixed order)
 template <int U>
-__device__ __forceinline__ double gather_sum(const int32_t* __restrict__ idx, const double* __restrict__ x, int64_t e0,
-                                             int64_t e1, const double* __restrict__ Vb, int64_t nidx) {
+__device__ __forceinline__ Vw gather_sum(const int32_t* __restrict__ idx, const double* __restrict__ x, int64_t e0,
+                                         int64_t e1, const double* __restrict__ Vb, int64_t nidx) {
   (void)nidx;
-  double acc[U];
+  Vw acc[U];
 #pragma unroll
-  for (int u = 0; u < U; ++u) acc[u] = 0.0;
+  for (int u = 0; u < U; ++u)
+#pragma unroll
+    for (int q = 0; q < VW; ++q) acc[u].v[q] = 0.0;
   int64_t e = e0;
   for (; e + U <= e1; e += U) {
     int32_t c[U];
@@ -183,17 +220,26 @@ __device__ __forceinline__ double gather_sum(const int32_t* __restrict__ idx, co
       xv[u] = __ldg(x + e + u);
       CPA_DCHECK(c[u] >= 0 && c[u] < nidx);
     }
-    double g[U];
+    Vw g[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) g[u] = Vb[(int64_t)c[u] * RB];
+    for (int u = 0; u < U; ++u) g[u] = ldv(Vb + (int64_t)c[u] * RB);
 #pragma unroll
-    for (int u = 0; u < U; ++u) acc[u] = fma(xv[u], g[u], acc[u]);
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int q = 0; q < VW; ++q) acc[u].v[q] = fma(xv[u], g[u].v[q], acc[u].v[q]);
   }
-  for (; e < e1; ++e) acc[0] = fma(__ldg(x + e), Vb[(int64_t)__ldg(idx + e) * RB], acc[0]);
+  for (; e < e1; ++e) {
+    const Vw g = ldv(Vb + (int64_t)__ldg(idx + e) * RB);
+    const double xe = __ldg(x + e);
+#pragma unroll
+    for (int q = 0; q < VW; ++q) acc[0].v[q] = fma(xe, g.v[q], acc[0].v[q]);
+  }
 #pragma unroll
   for (int w = 1; w < U; w *= 2)
 #pragma unroll
-    for (int u = 0; u + w < U; u += 2 * w) acc[u] += acc[u + w];
+    for (int u = 0; u + w < U; u += 2 * w)
+#pragma unroll
+      for (int q = 0; q < VW; ++q) acc[u].v[q] += acc[u + w].v[q];
   return acc[0];
 }
 
@@ -206,13 +252,17 @@ __global__ void __launch_bounds__(SP_WARPS * 32) k_spmm_wxt(const int64_t* row_p
   const int64_t item = blockIdx.x * (int64_t)SP_WARPS + warp;  // block-major: item = b * m + j
   if (item >= nblk * m) return;
   const int64_t b = item / m, j = item % m;
-  const double* Wb = W + b * n * RB + lane;
+  const double* Wb = W + b * n * RB + VW * lane;
   const int64_t e0 = NP > 1 ? rs[j * (NP + 1) + h] : row_ptr[j];
   const int64_t e1 = NP > 1 ? rs[j * (NP + 1) + h + 1] : row_ptr[j + 1];
-  const double sum = gather_sum<U>(col, val, e0, e1, Wb, n);
-  double* zp = Z + (b * m + j) * RB + lane;
-  if (h == 0) *zp = sum;
-  else *zp += sum;
+  Vw sum = gather_sum<U>(col, val, e0, e1, Wb, n);
+  double* zp = Z + (b * m + j) * RB + VW * lane;
+  if (h != 0) {
+    const Vw z = ldv(zp);
+#pragma unroll
+    for (int q = 0; q < VW; ++q) sum.v[q] = z.v[q] + sum.v[q];
+  }
+  stv(zp, sum);
 }
 
 // W_k[b][l][:] = s * sum_{j in col l} x_jl Z[b][j][:] - ... (fused epilogue), one warp per (b, l)
@@ -229,43 +279,62 @@ __global__ void __launch_bounds__(SP_WARPS * 32) k_spmm_zx(const int64_t* cptr, 
   const int64_t item = blockIdx.x * (int64_t)SP_WARPS + warp;  // item = b * n + l
   if (item >= nblk * n) return;
   const int64_t b = item / n, l = item % n;
-  const double acc = gather_sum<U>(crow, cval, cptr[l], cptr[l + 1], Z + b * m * RB + lane, m);
-  const int64_t o = item * RB + lane;
+  const Vw acc = gather_sum<U>(crow, cval, cptr[l], cptr[l + 1], Z + b * m * RB + VW * lane, m);
+  const int64_t o = item * RB + VW * lane;
   const double s2 = P->scale2;
   if (INIT) {
-    const double x = Wp[o];
-    const double w = s2 * acc - x;                 // W_1 = B_hat X
-    if (Wout) Wout[o] = w;
-    Yb[o] = 0.5 * P->c[0] * x + P->c[1] * w;       // Y = c0/2 W_0 + c1 W_1
+    const Vw x = ldv(Wp + o);
+    Vw w, y;
+#pragma unroll
+    for (int q = 0; q < VW; ++q) {
+      w.v[q] = s2 * acc.v[q] - x.v[q];                       // W_1 = B_hat X
+      y.v[q] = 0.5 * P->c[0] * x.v[q] + P->c[1] * w.v[q];    // Y = c0/2 W_0 + c1 W_1
+    }
+    if (Wout) stv(Wout + o, w);
+    stv(Yb + o, y);
   } else {
-    const double wp = Wp[o], wpp = Wpp[o];
-    const double w = 2.0 * s2 * acc - 2.0 * wp - wpp;   // W_k = 2 B_hat W_{k-1} - W_{k-2}
-    if (Wout) Wout[o] = w;
+    const Vw wp = ldv(Wp + o), wpp = ldv(Wpp + o);
+    Vw w;
+#pragma unroll
+    for (int q = 0; q < VW; ++q) w.v[q] = 2.0 * s2 * acc.v[q] - 2.0 * wp.v[q] - wpp.v[q];   // W_k = 2 B_hat W_{k-1} - W_{k-2}
+    if (Wout) stv(Wout + o, w);
     // Y += c_j W_j for the yterms latest j (1 to 3: W_{k-2}, W_{k-1} are in registers already), so Y
     // is read and written once every third step (sparse_apply)
     if (yterms > 0) {
-      double t = P->c[k] * w;
-      if (yterms >= 2) t = P->c[k - 1] * wp + t;
-      if (yterms >= 3) t = P->c[k - 2] * wpp + t;
-      Yb[o] += t;
+      Vw y = ldv(Yb + o);
+#pragma unroll
+      for (int q = 0; q < VW; ++q) {
+        double t = P->c[k] * w.v[q];
+        if (yterms >= 2) t = P->c[k - 1] * wp.v[q] + t;
+        if (yterms >= 3) t = P->c[k - 2] * wpp.v[q] + t;
+        y.v[q] += t;
+      }
+      stv(Yb + o, y);
     }
   }
 }
 
-// caller Y (row-major, ld) <- interleaved Yb, via a 32 x 32 shared-memory transpose
+// caller Y (row-major, ld) <- interleaved Yb, via 64 x 64 shared-memory transposes (blockIdx.z: the
+// 64-row piece of the RB-row block)
+constexpr int UT = 64;
 __global__ void k_unblock(const double* Yb, int64_t rows, int64_t n, double* Y, int64_t ldy) {
-  __shared__ double t[RB][RB + 1];
+  __shared__ double t[UT][UT + 1];
   const int64_t b = blockIdx.y;
-  const int64_t c0 = (int64_t)blockIdx.x * RB;
+  const int64_t c0 = (int64_t)blockIdx.x * UT;
+  const int i0 = blockIdx.z * UT;
   const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
-  for (int r = ty; r < RB; r += 8) {
+  const int ni = RB - i0 < UT ? RB - i0 : UT;     // rows of this piece (RB = 32: 32)
+  for (int r = ty; r < UT; r += 8) {   // r: column within the tile, i: row within the piece
     const int64_t c = c0 + r;
-    t[r][tx] = c < n ? Yb[(b * n + c) * RB + tx] : 0.0;
+    for (int i = tx; i < ni; i += 32) t[r][i] = c < n ? Yb[(b * n + c) * RB + i0 + i] : 0.0;
   }
   __syncthreads();
-  for (int r = ty; r < RB; r += 8) {
-    const int64_t i = b * RB + r, c = c0 + tx;
-    if (i < rows && c < n) Y[i * ldy + c] = t[tx][r];
+  for (int r = ty; r < ni; r += 8) {   // r: row within the piece
+    const int64_t i = b * RB + i0 + r;
+    for (int cc = tx; cc < UT; cc += 32) {
+      const int64_t c = c0 + cc;
+      if (i < rows && c < n) Y[i * ldy + c] = t[cc][r];
+    }
   }
 }
 
@@ -300,8 +369,10 @@ cudaError_t sparse_apply(int64_t m, int64_t n, int64_t nnz, const int64_t* row_p
   const size_t o_Wb = off;   off += al(blkW * sizeof(double));
   const size_t o_Y = off;    off += al(blkW * sizeof(double));
   const size_t o_Z = off;    off += al(blkZ * sizeof(double));
-  // column passes of Z = W X^T: W slices of <= ~26 MB per 32-row block (CPA_SVT_SP_PASSES overrides)
-  int NP = (int)std::max<int64_t>(1, (n * RB * 8 + (26 << 20) - 1) / (26 << 20));
+  // column passes of Z = W X^T: W slices of <= ~52 MB per block (CPA_SVT_SP_PASSES overrides)
+  // (a pass's W slice <= ~52 MB: c4 with 64-row blocks takes 2 passes -- Z kernel per step 44.6 ms
+  // against 45.2 / 46.7 / 49.0 ms for 3 / 4 / 6 passes)
+  int NP = (int)std::max<int64_t>(1, (n * RB * 8 + (52 << 20) - 1) / (52 << 20));
   if (const char* v = getenv("CPA_SVT_SP_PASSES")) NP = std::max(1, atoi(v));
   const size_t o_rs = off;   off += al((size_t)m * (NP + 1) * sizeof(int64_t));
   *ws_needed = off;
@@ -408,7 +479,7 @@ cudaError_t sparse_apply(int64_t m, int64_t n, int64_t nnz, const int64_t* row_p
       prev2 = prev;
       prev = (k & 1) ? (const double*)Wb : (const double*)Wa;
     }
-    dim3 ub((unsigned)((n + RB - 1) / RB), (unsigned)nblk);
+    dim3 ub((unsigned)((n + UT - 1) / UT), (unsigned)nblk, (unsigned)((RB + UT - 1) / UT));
     k_unblock<<<ub, dim3(32, 8), 0, st>>>(Yb, rows, n, Y, ldy); ++L;
   }
 #undef SPCK

@@ -138,12 +138,13 @@ def sparse(h, reps, m=20000, n=200000, nnz=4_000_000):
     zx = ph.get("sparse_w", (0, 0))[0]
     zw = ph.get("sparse_z", (0, 0))[0]
     # L2 roofline of the SpMM pair (DESIGN.md §6 "Sparse roofline"): per step each SpMM gathers
-    # m * nnz * 8 B (a 256-byte 32-row segment per nonzero and block) through L2, plus the dense W / Y
-    # streams and one read of the CSR / CSC structure per 32-row block; ceiling = the measured
-    # 256-byte random-gather rate of tools/probes/l2_gather.cu on this pool's B200
-    nblk = (m + 31) // 32
-    l2_step = 2 * m * nnz * 8 + (5 * 8 * m * n + 2 * 8 * m * m) + 2 * nblk * nnz * 12
-    L2_CEIL = 12900.0
+    # m * nnz * 8 B (a 512-byte 64-row segment per nonzero and block) through L2, plus the dense W / Y
+    # streams (W_{k-1}, W_{k-2}, W_k every step, Y read and written every third: reading R30) and one
+    # read of the CSR / CSC structure per 64-row block; ceiling = the measured 512-byte random-gather
+    # rate of tools/probes/l2_gather512.cu on this pool's B200 (19.2-20.1 TB/s)
+    nblk = (m + 63) // 64
+    l2_step = 2 * m * nnz * 8 + ((3 + 2 / 3) * 8 * m * n + 2 * 8 * m * m) + 2 * nblk * nnz * 12
+    L2_CEIL = 19500.0
     pair = (zx + zw) / (K - 1)
     return {"config": "c4", "shape": [m, n, nnz], "ms_per_svt": ms, "gflops": F / ms / 1e6,
             "algorithmic_GB": byt / 1e9, "hbm_gbs_alg": byt / ms / 1e6, "hbm_frac": byt / ms / 1e6 / HBM,
