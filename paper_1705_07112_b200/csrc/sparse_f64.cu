@@ -437,8 +437,10 @@ cudaError_t sparse_apply(int64_t m, int64_t n, int64_t nnz, const int64_t* row_p
     // gathers in flight per warp in the SpMM pair (CPA_SVT_SP_UNROLL = 2 | 4 | 8; c4 per step, Z / W
     // kernels: 55.0 / 77.6, 55.6 / 91.6, 78.2 / 109.7 ms -- more loads in flight only add L2
     // contention; the index loads of a pair ahead of the two gathers: Z 65 -> 55 ms)
-    int U = 2;
-    if (const char* v = getenv("CPA_SVT_SP_UNROLL")) U = atoi(v) == 8 ? 8 : atoi(v) == 4 ? 4 : 2;
+    // (64-row blocks: the Z kernel best at 2, the W kernel at 1 -- c4 per step 44.4 / 52.4 ms against
+    // 45.7 / 56.4 the other way round)
+    int U = 2, UW = 1;
+    if (const char* v = getenv("CPA_SVT_SP_UNROLL")) UW = U = atoi(v) == 8 ? 8 : atoi(v) == 4 ? 4 : atoi(v) == 1 ? 1 : 2;
     const bool yevery = env_on("CPA_SVT_SP_YEVERY");
     const unsigned gz = (unsigned)((itemsZ + SP_WARPS - 1) / SP_WARPS);
     const unsigned gw = (unsigned)((itemsW + SP_WARPS - 1) / SP_WARPS);
@@ -451,7 +453,7 @@ cudaError_t sparse_apply(int64_t m, int64_t n, int64_t nnz, const int64_t* row_p
     for (int k = 1; k < K; ++k) {
       if (hook) hook(hook_ctx, CPA_SVT_PH_SPARSE_Z, 1);
       for (int hp = 0; hp < NP; ++hp) {
-        auto kz = U == 8 ? k_spmm_wxt<8> : U == 4 ? k_spmm_wxt<4> : k_spmm_wxt<2>;
+        auto kz = U == 8 ? k_spmm_wxt<8> : U == 4 ? k_spmm_wxt<4> : U == 1 ? k_spmm_wxt<1> : k_spmm_wxt<2>;
         kz<<<gz, SP_WARPS * 32, 0, st>>>(row_ptr, col, val, m, n, nblk, prev, Z, rs, NP, hp);
         ++L;
       }
@@ -462,8 +464,8 @@ cudaError_t sparse_apply(int64_t m, int64_t n, int64_t nnz, const int64_t* row_p
       else out = (k & 1) ? Wb : Wa;          // W_k overwrites W_{k-2} in place
       if (k == K - 1) out = nullptr;
       {
-        auto kw = k == 1 ? (U == 8 ? k_spmm_zx<8, true> : U == 4 ? k_spmm_zx<4, true> : k_spmm_zx<2, true>)
-                         : (U == 8 ? k_spmm_zx<8, false> : U == 4 ? k_spmm_zx<4, false> : k_spmm_zx<2, false>);
+        auto kw = k == 1 ? (UW == 8 ? k_spmm_zx<8, true> : UW == 4 ? k_spmm_zx<4, true> : UW == 1 ? k_spmm_zx<1, true> : k_spmm_zx<2, true>)
+                         : (UW == 8 ? k_spmm_zx<8, false> : UW == 4 ? k_spmm_zx<4, false> : UW == 1 ? k_spmm_zx<1, false> : k_spmm_zx<2, false>);
         // Y += c_j W_j in groups of three steps (k = 4, 7, 10, ...: the terms since the last group),
         // the last step flushing the rest (CPA_SVT_SP_YEVERY=1: every step, Alg. 1's order)
         int yt = 1;
