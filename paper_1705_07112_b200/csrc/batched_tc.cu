@@ -174,6 +174,7 @@ struct Args {
   double safety, lam_override;
   float* lambda_out;
   const double* costab;   // cos(k theta_l), K x K
+  int psi2_sq;            // Psi_2 from the power iteration's first squaring (R29; CPA_SVT_NO_PSI2_SQ: off)
 };
 
 // smem: one B operand (hi, lo; 32 KB, 1 KB aligned): rows of A (line 1), of c^p G^p (squarings),
@@ -355,6 +356,9 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : 4) k_batched_tc(Args a) {
     //      c^4 G^4 (c = 2^-ilogb(max G_ii), exact) then T - 4q by G; two extra tcgen05 products
     //      instead of 3q power steps.
     double lam_hat;
+    // (reading R29: the first squaring's c^2 G^2, kept in the H buffer until the init forms Psi_2)
+    bool have_g2 = false;
+    float cs2v = 1.f;
     if (a.lam_override > 0.0) {
       lam_hat = a.lam_override / a.safety;
     } else {
@@ -386,6 +390,13 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : 4) k_batched_tc(Args a) {
           phase ^= 1;
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
           ld_frag2(tD + lane_off, tD1 + lane_off, g4);
+          if (sq == 0 && a.psi2_sq && K > 3) {        // c^2 G^2 into this thread's H slots (free until the init)
+#pragma unroll
+            for (int c = 0; c < FR / 4; ++c)
+              sH4[c * NT + tid] = make_float4(g4[4 * c], g4[4 * c + 1], g4[4 * c + 2], g4[4 * c + 3]);
+            have_g2 = true;
+            cs2v = cs * cs;
+          }
           asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
           __syncthreads();                             // everyone has read D and the operands
         }
@@ -464,7 +475,41 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : 4) k_batched_tc(Args a) {
     // with -2 Psi_{k-1} - Psi_{k-2}, so D0 + D1 = Psi_{k-1} (s4 G)^T - 2 Psi_{k-1} - Psi_{k-2}
     // = Psi_k (lines 8-9) and only Psi_{k-1} stays in registers.
     float wp[FR];
-    {
+    int k_first = 2;
+    if (have_g2) {
+      // Psi_1 = s2 G - I and Psi_2 = 2 s2^2 G^2 - 2 s2 G ... = 2 B_hat^2 - I from the squaring's c^2 G^2
+      // (reading R29): H = c0/2 I + c1 Psi_1 + c2 Psi_2, the steps start at k = 3 with A = Psi_2
+      // and D0 = -2 Psi_2 - Psi_1
+      const float h0 = 0.5f * sC[0], c1 = sC[1], c2 = sC[2];
+      const float a2 = 2.f * s2 * s2 / cs2v, a4 = 2.f * s2;
+      float hh[FR];
+#pragma unroll
+      for (int c = 0; c < FR / 4; ++c) {
+        const float4 q4 = sH4[c * NT + tid];
+        const float gq[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+          const int e = 4 * c + x;
+          const float id = (rowof(e) == colof(e)) ? 1.f : 0.f;
+          const float w = s2 * g[e] - id;                         // Psi_1
+          const float p2 = a2 * gq[x] - 2.f * a4 * g[e] + id;     // Psi_2 = 2 s2^2 G^2 - 4 s2 G + I
+          hh[e] = h0 * id + c1 * w + c2 * p2;
+          wp[e] = p2;
+          g[e] *= s4;
+        }
+      }
+      k_first = 3;
+#pragma unroll
+      for (int c = 0; c < FR / 4; ++c) sH4[c * NT + tid] = make_float4(hh[4 * c], hh[4 * c + 1], hh[4 * c + 2], hh[4 * c + 3]);
+      put_frag(sB, row0, col0, g);                      // B operand of the steps: rows of s4 G
+      st_frag_hl(tAh + lane_off, tAl + lane_off, wp); // A operand (TMEM): rows of Psi_2
+#pragma unroll
+      for (int e = 0; e < FR; ++e) {                     // D0 = -2 Psi_2 - Psi_1 (Psi_1 recomputed from s4 G)
+        const float id = (rowof(e) == colof(e)) ? 1.f : 0.f;
+        hh[e] = -2.f * wp[e] - (0.5f * g[e] - id);
+      }
+      st_frag(tD + lane_off, hh);
+    } else {
       const float h0 = 0.5f * sC[0], c1 = sC[1];
       float hh[FR];
 #pragma unroll
@@ -485,7 +530,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : 4) k_batched_tc(Args a) {
     }
     sync_for_mma();
     // ---- lines 8-11: Psi_k = D0 + D1, H += c_k Psi_k; next A = Psi_k, next D0 = -2 Psi_k - Psi_{k-1}
-    for (int k = 2; k < K; ++k) {
+    for (int k = k_first; k < K; ++k) {
       if (tid == 0) btc::mma64_ts<true>(tD, tD1, tAh, tAl, sB, &bar);
       mbar_wait(&bar, phase);
       phase ^= 1;
@@ -570,7 +615,7 @@ cudaError_t launch_batched_tc(int64_t batch, int m, int n, const float* X, float
   if (K > 128) return cudaErrorNotSupported;
   k_costab<<<(K * K + 255) / 256, 256, 0, st>>>(costab, K);
   if (launches) ++*launches;
-  btc::Args a{batch, m, n, X, Y, k, K, T, safety, lam_override, lambda_out, costab};
+  btc::Args a{batch, m, n, X, Y, k, K, T, safety, lam_override, lambda_out, costab, env_on("CPA_SVT_NO_PSI2_SQ") ? 0 : 1};
   const char* ntv = getenv("CPA_SVT_BTC_NT");
   const int nt = (ntv && atoi(ntv) == 256) ? 256 : 128;   // 128: measured c3 8.05 ms against 8.62 ms
   auto kern = nt == 128 ? btc::k_batched_tc<128> : btc::k_batched_tc<256>;

@@ -128,3 +128,24 @@ def test_batched_argument_checks(env):
         h.apply_batched(X, kern, 5, lambda_out=torch.zeros(3, dtype=torch.float32, device="cuda"))
     with pytest.raises(AssertionError):
         h.apply_batched(X, kern, 5, lambda_out=torch.zeros(4, dtype=torch.float64, device="cuda"))
+
+
+@pytest.mark.parametrize("K,T", [(20, 30), (4, 30), (5, 8), (12, 7)])
+def test_batched_psi2_from_squaring(env, K, T):
+    """Psi_2 formed from the power iteration's first squaring (reading R29: c^2 G^2 kept in the H
+    buffer, the steps start at k = 3) against the k = 2 product (CPA_SVT_NO_PSI2_SQ=1) at fp32
+    rounding level and the oracle at the 1e-4 bar; T < 8 (no squaring) and K = 4 included."""
+    import os
+    torch, P, h = env
+    Xb = W.gen_c3(batch=257, seed=K + T)
+    cfg = W.CONFIGS["c3"]
+    Y, lam = _run(env, Xb, cfg["kernel"], K, T=T)
+    os.environ["CPA_SVT_NO_PSI2_SQ"] = "1"
+    try:
+        Y0, lam0 = _run(env, Xb, cfg["kernel"], K, T=T)
+    finally:
+        os.environ.pop("CPA_SVT_NO_PSI2_SQ", None)
+    Yo, _ = O.cpa_shrink_batched(Xb.astype(np.float64), O.Kernel(**cfg["kernel"]), K, T=T)
+    assert np.array_equal(lam, lam0)
+    assert O.rel_fro(Y.astype(np.float64), Y0.astype(np.float64)) <= 1e-5
+    assert O.rel_fro(Y.astype(np.float64), Yo) <= 1e-4

@@ -115,7 +115,9 @@ def batched(h, reps, batch=65536):
     # tcgen05 engine (default): Gram, 2 squarings, K-2 steps, line 12 = K + 1 products of 64^3,
     # each 3 TF32 MMAs (3xTF32); TF32 dense peak = MEASURED_PEAKS bf16 / 2, halved at M = 64
     # (one MMA of M64 N64 K8 per 64 cycles per SM)
-    products = (2 if T >= 8 else 0) + 1 + (K - 2) + 1
+    # (K - 3 steps when Psi_2 comes from the first squaring: reading R29, T >= 8, K > 3)
+    psi2 = T >= 8 and K > 3 and not os.environ.get("CPA_SVT_NO_PSI2_SQ")
+    products = (2 if T >= 8 else 0) + 1 + (K - 3 if psi2 else K - 2) + 1
     tensor_flops = batch * products * 3 * 2 * s * s * L
     tf32_peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"] / 2
     return {"config": "c3", "batch": batch, "engine": "tcgen05 3xTF32 (M=N=64, A in TMEM)", "ms_per_svt_batch": ms,
