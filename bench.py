@@ -341,7 +341,10 @@ def run_ours(args, cfg):
     avg = step_ms / max(step_n, 1)
     if form == 4:   # (c1-sized problems: the whole SVT in one thread block)
         kname = "k_small_f64 (all of Alg. 1 in one thread block, shared memory, DMMA)"
-        rec_flops = dense_executed_flops(m_g, n_g, K, 3)
+        s1, L1 = min(m_g, n_g), max(m_g, n_g)
+        # (K - 3 products with the two chains and Psi_2 from the squaring, readings R28/R29)
+        nprod = info0.get("rec_products") or (K - 2)
+        rec_flops = s1 * (s1 + 1) * L1 + nprod * 2 * s1 ** 3 + 2 * s1 * s1 * L1
     elif form == 2:
         kname = ("k_cheb_sym_tma (symmetric s x s recurrence, TMA-fed DMMA)" if cfg["math"] == "native"
                  else "k_tc_gemm (symmetric s x s recurrence step, tcgen05 " + cfg["math"] + ")")

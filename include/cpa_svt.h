@@ -127,8 +127,8 @@ typedef struct {
   int32_t form;          /* dense form that ran: 1 = apply-to-X, 2 = s x s symmetric, 3 = s x s full tiles,
                             4 = s x s in one thread block (fp64, s <= 64 and L <= 128, FORM auto) */
   int32_t rec_products;  /* s x s products the recurrence (Alg. 1 lines 8-11) launched for the dense
-                            fp64 s x s forms: K - 2, or K - 3 when Psi_2 = 2 B_hat^2 - I was formed
-                            from the power iteration's squaring (reading R29); 0 elsewhere */
+                            fp64 s x s forms (2 and 4): K - 2, or K - 3 when Psi_2 = 2 B_hat^2 - I was
+                            formed from the power iteration's squaring (reading R29); 0 elsewhere */
   int32_t line12_in_recurrence;  /* 1: Alg. 1 line 12 (Y = H_hat X) ran inside the recurrence launch
                                     (m-chain mode, left side), its time in ms_recurrence */
 } cpa_svt_info;

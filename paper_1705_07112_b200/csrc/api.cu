@@ -28,6 +28,7 @@ size_t dense_flow_sync_ints(int64_t m, int64_t n, int K);
 size_t dense_flow_partial_doubles(int64_t m, int64_t n, int num_sms);
 void dense_gram_chunk_range(int64_t kd, int q, int S, int64_t* k0, int64_t* k1);
 bool small_f64_fits(int64_t m, int64_t n);
+int small_f64_products(int64_t m, int64_t n, int K, int nsq, double lam_override);
 cudaError_t launch_small_f64(const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t m, int64_t n,
                              SeriesParams* P, const cpa_svt_kernel& k, int K, int T, double safety,
                              double lam_override, const double* c_given, int nsq, cudaStream_t st, int check);
@@ -813,6 +814,8 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
       info->ms_total = tm.ms(0, 1);
       info->kernel_launches = nl;
       info->form = 4;
+      info->rec_products = small_f64_products(m, n, K, lam->lambda_max > 0.0 ? 0 : power_squarings(s, lam->power_iters),
+                                              lam->lambda_max);
     }
     return st;
   }

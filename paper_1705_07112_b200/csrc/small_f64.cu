@@ -35,6 +35,7 @@ struct SmallArgs {
   const double* c_given; // device, nullable
   int nsq;               // squarings before the power iteration
   int check;             // SPEC.md:215 divergence check folded in (check.cu's rule): ||Y|| vs 1e3 sum|c_k| ||X||
+  int chain;             // two Chebyshev chains (R28) with Psi_2 from the first squaring (R29): one more buffer
 };
 
 constexpr int SM_THREADS = 128;   // 4 warps: one 32 x 32 quarter of a 64 x 64 DMMA tile each
@@ -157,6 +158,10 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_f64(SmallArgs a) {
       }
       __syncthreads();
       sq_product<h>(G, G, Gp, s, s_scal[0]);          // c^2 G^2
+      if (a.chain) {                                  // (kept for Psi_2: Wb is free until the recurrence)
+        for (int e = tid; e < 64 * LDP; e += SM_THREADS) Wb[e] = Gp[e];
+        __syncthreads();
+      }
       p = 2;
       for (int j = 1; j < a.nsq && 2 * p <= a.T - 1; ++j) {
         sq_product<h>(Gp, Gp, Wa, s, 1.0);            // c^{2p} G^{2p}
@@ -198,8 +203,91 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_f64(SmallArgs a) {
   __syncthreads();
   STAMP();
   const double s2 = a.P->scale2, s4 = 2.0 * s2;
-  // ---- lines 5-7: W_1 (Wa), H (Gp), zero outside s x s
   double* H = Gp;
+  const int ks = (s + 3) & ~3;
+  if (a.chain && a.K >= 4 && a.lam_override <= 0.0 && a.nsq > 0) {
+    // ---- two chains (R28): Psi_1 (Wa), Psi_2 = 2 s2^2 G^2 - 4 s2 G + I from the squaring's c^2 G^2
+    //      (R29, over G), H = c0/2 I + c1 Psi_1 + c2 Psi_2; then the products in pairs
+    //      Psi_k = 2 Psi_2 Psi_{k-2} - Psi_{|k-4|} (k odd, k + 1 even) sharing the A fragments of
+    //      Psi_2: twice the independent DMMAs per barrier.  Odd chain in Wa / Wb, even in E1 / E2
+    //      (E2 = the operand buffer, free until line 12); Psi_k over Psi_{k-4}, own elements.
+    const double c2inv = 1.0 / s_scal[0];
+    double* P2 = G;
+    const int opn = max(max(kL * LDP, 64 * (((L + 63) & ~63) + 4)), 64 * LDP);   // small_f64_smem's op
+    double* E1 = Op + opn + 64;       // the extra buffer (small_f64_smem with chains)
+    double* E2 = Op;
+    for (int e = tid; e < 64 * LDP; e += SM_THREADS) {
+      const int r = e / LDP, c = e % LDP;
+      const bool in = r < s && c < s;
+      const double id = (r == c && r < s) ? 1.0 : 0.0;
+      const double gg = G[e];
+      const double w1 = in ? s2 * gg - id : 0.0;
+      const double p2 = in ? 2.0 * s2 * s2 * (Wb[e] * c2inv) - 2.0 * s4 * gg + id : 0.0;
+      Wa[e] = w1;
+      P2[e] = p2;
+      H[e] = 0.5 * a.P->c[0] * id + a.P->c[1] * w1 + a.P->c[2] * p2;
+      E1[e] = 0.0;
+      E2[e] = 0.0;
+    }
+    __syncthreads();
+    auto ebuf = [&](int k) { return k == 2 ? P2 : (((k - 4) >> 1) & 1) ? E2 : E1; };   // even k >= 2
+    auto obuf = [&](int k) { return (((k - 1) >> 1) & 1) ? Wb : Wa; };                // odd k >= 1
+    for (int k = 3; k < a.K; k += 2) {
+      const bool two = k + 1 < a.K;   // the pair (k odd, k + 1 even); the last may be single
+      const double* Bo = obuf(k - 2);
+      const double* Be = ebuf(k - 1);   // (k + 1) - 2
+      double acc_o[4][4][2], acc_e[4][4][2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc_o[i][j][0] = acc_o[i][j][1] = acc_e[i][j][0] = acc_e[i][j][1] = 0.0;
+#pragma unroll 2
+      for (int kk = 0; kk < ks; kk += 4) {
+        double fa[4], fo[4], fe[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) fa[i] = i < h ? P2[(kk + t) * LDP + wm + i * 8 + g] : 0.0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          fo[j] = j < h ? Bo[(kk + t) * LDP + wn + j * 8 + g] : 0.0;
+          fe[j] = (j < h && two) ? Be[(kk + t) * LDP + wn + j * 8 + g] : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (i < h && j < h) {
+              dmma_8x8x4(acc_o[i][j][0], acc_o[i][j][1], fa[i], fo[j]);
+              if (two) dmma_8x8x4(acc_e[i][j][0], acc_e[i][j][1], fa[i], fe[j]);
+            }
+      }
+      const double cko = a.P->c[k], cke = two ? a.P->c[k + 1] : 0.0;
+      double* Oo = obuf(k);                       // Psi_k over Psi_{k-4} (k = 3: a fresh buffer)
+      const double* Qo = obuf(k == 3 ? 1 : k - 4);
+      double* Oe = ebuf(k + 1);
+      const double* Qe = (k + 1) == 4 ? nullptr : ebuf(k - 3);   // Psi_{k+1-4} (Psi_0 = I at k + 1 = 4)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (i < h && j < h)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int r = wm + i * 8 + g, c = wn + j * 8 + 2 * t + e, o = r * LDP + c;
+              const double wo = 2.0 * acc_o[i][j][e] - Qo[o];
+              double hv = H[o] + cko * wo;
+              Oo[o] = wo;                                                // (read only by this thread)
+              if (two) {
+                const double q = Qe ? Qe[o] : ((r == c && r < s) ? 1.0 : 0.0);
+                const double we = 2.0 * acc_e[i][j][e] - q;
+                Oe[o] = we;
+                hv += cke * we;
+              }
+              H[o] = hv;
+            }
+      __syncthreads();
+    }
+  } else {
+  // ---- lines 5-7: W_1 (Wa), H (Gp), zero outside s x s
   for (int e = tid; e < 64 * LDP; e += SM_THREADS) {
     const int r = e / LDP, c = e % LDP;
     const double id = (r == c && r < s) ? 1.0 : 0.0;
@@ -211,7 +299,6 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_f64(SmallArgs a) {
   // ---- lines 8-11: W_k = s4 G W_{k-1} - 2 W_{k-1} - W_{k-2} over W_{k-2}, H += c_k W_k
   double* Wp = Wa;   // W_{k-1}
   double* Wq = Wb;   // W_{k-2} (k = 2: the identity, implicit)
-  const int ks = (s + 3) & ~3;
   for (int k = 2; k < a.K; ++k) {
     double acc[4][4][2];
     dmma_tile<h>(G, LDP, Wp, LDP, ks, 0, acc);
@@ -233,6 +320,7 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_f64(SmallArgs a) {
     double* tmp = Wp;
     Wp = Wq;
     Wq = tmp;
+  }
   }
   STAMP();
   // ---- line 12: P = H A (s x L; A(k, n) k-major = row-major A), right Y = P^T, left Y = P
@@ -294,16 +382,29 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_f64(SmallArgs a) {
 #undef STAMP
 }
 
-size_t small_f64_smem(int64_t m, int64_t n) {
+size_t small_f64_smem(int64_t m, int64_t n, bool chain) {
   const int64_t s = m < n ? m : n, L = m < n ? n : m;
   const int64_t kL = (L + 3) / 4 * 4, ncol = (L + 63) / 64 * 64;
-  const int64_t op = std::max(kL * LDP, 64 * (ncol + 4));   // At for line 1 / A for line 12
+  const int64_t op = std::max(std::max(kL * LDP, 64 * (ncol + 4)), chain ? (int64_t)64 * LDP : (int64_t)0);   // At for line 1 / A for line 12 (/ E2)
   (void)s;
-  return (size_t)(4 * 64 * LDP + op + 64) * sizeof(double);   // (+64: line-12 fragment reads past the last row)
+  // (+64: line-12 fragment reads past the last row; chains: one more s x s buffer after Op)
+  return (size_t)((4 + (chain ? 1 : 0)) * 64 * LDP + op + 64) * sizeof(double);
 }
 bool small_f64_fits(int64_t m, int64_t n) {
   const int64_t s = m < n ? m : n, L = m < n ? n : m;
-  return s >= 1 && s <= 64 && L <= 128 && small_f64_smem(m, n) <= 220 * 1024;
+  return s >= 1 && s <= 64 && L <= 128 && small_f64_smem(m, n, false) <= 220 * 1024;
+}
+
+// two chains when the extra buffer fits (CPA_SVT_SMALL_CHAIN=0: the one-chain recurrence)
+static bool small_f64_chain_buf(int64_t m, int64_t n) {
+  const char* e = getenv("CPA_SVT_SMALL_CHAIN");
+  return small_f64_smem(m, n, true) <= 220 * 1024 && !(e && atoi(e) == 0);
+}
+
+// recurrence products the kernel performs: K - 3 with the chains (Psi_2 from the squaring), else K - 2
+int small_f64_products(int64_t m, int64_t n, int K, int nsq, double lam_override) {
+  const bool ch = small_f64_chain_buf(m, n) && K >= 4 && !(lam_override > 0.0) && nsq > 0;
+  return K < 2 ? 0 : ch ? K - 3 : K - 2;
 }
 
 cudaError_t launch_small_f64(const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t m, int64_t n,
@@ -314,7 +415,8 @@ cudaError_t launch_small_f64(const double* X, int64_t ldx, double* Y, int64_t ld
   a.X = X; a.ldx = ldx; a.Y = Y; a.ldy = ldy; a.m = (int)m; a.n = (int)n;
   a.P = P; a.kern = k; a.K = K; a.T = T; a.safety = safety; a.lam_override = lam_override;
   a.c_given = c_given; a.nsq = nsq;
-  const size_t smem = small_f64_smem(m, n);
+  a.chain = small_f64_chain_buf(m, n);
+  const size_t smem = small_f64_smem(m, n, a.chain != 0);
   const int64_t s = m < n ? m : n;
   const int h = (int)(((s + 7) / 8 + 1) / 2);
   auto kf = h == 1 ? k_small_f64<1> : h == 2 ? k_small_f64<2> : h == 3 ? k_small_f64<3> : k_small_f64<4>;

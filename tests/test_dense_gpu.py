@@ -329,6 +329,29 @@ def test_small_kernel_against_grid_path_and_oracle(env, shape):
     assert O.rel_fro(Y1, Yo) <= TOL64
 
 
+@pytest.mark.parametrize("shape,K", [((48, 64), 4), ((48, 64), 5), ((64, 128), 12), ((33, 7), 13), ((5, 9), 30)])
+def test_small_kernel_two_chains(env, shape, K):
+    """The single-block kernel's two-chain recurrence (R28) with Psi_2 from the first squaring (R29)
+    against its one-chain recurrence (CPA_SVT_SMALL_CHAIN=0) and the oracle; K even and odd (the last
+    pair single), K = 4 (one pair); 64 x 128 has no room for the extra buffer (one chain both ways)."""
+    import os
+    X = W.random_dense(*shape, seed=K)
+    kern = {"kind": "soft", "tau": 0.2, "tau_relative": True}
+    Y1, i1 = _run(env, X, kern, K, T=30)
+    os.environ["CPA_SVT_SMALL_CHAIN"] = "0"
+    try:
+        Y2, i2 = _run(env, X, kern, K, T=30)
+    finally:
+        del os.environ["CPA_SVT_SMALL_CHAIN"]
+    assert i1["form"] == 4 and i2["form"] == 4
+    # (the extra buffer fits beside the line-12 operand for L <= 64: 64 x 128 keeps one chain)
+    assert i1["rec_products"] == (K - 3 if max(shape) <= 64 else K - 2) and i2["rec_products"] == K - 2
+    assert i1["lambda_hat"] == i2["lambda_hat"]
+    assert O.rel_fro(Y1, Y2) <= 1e-12
+    Yo = O.cpa_shrink(X, O.Kernel(**kern), K, T=30)
+    assert O.rel_fro(Y1, Yo) <= TOL64
+
+
 @pytest.mark.parametrize("shape", [(40, 56), (150, 90), (90, 150)])
 def test_max_order(env, shape):
     """K = CPA_SVT_KMAX (512) on the single-block path (40 x 56) and the grid path (150 x 90; 90 x 150:

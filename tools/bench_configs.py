@@ -77,7 +77,7 @@ def dense(name, h, reps, m=None, n=None, K=None, dtype="f64", math="native"):
     #    phase is the whole kernel
     nprod = info.get("rec_products") or (K - 2)   # (K - 3 when Psi_2 came from the squaring, R29)
     rec = {1: (K - 1) * 2 * s * s * L, 2: nprod * s * s * (s + 1), 3: (K - 2) * 2 * s ** 3,
-           4: (K - 2) * 2 * s ** 3}[form]
+           4: nprod * 2 * s ** 3}[form]
     if info.get("line12_in_recurrence"):   # line 12 ran inside the step launch (m-chain mode)
         rec += 2 * s * s * L
     F_exec = s * (s + 1) * L + rec + (0 if form == 1 or info.get("line12_in_recurrence") else 2 * s * s * L)
