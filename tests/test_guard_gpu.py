@@ -122,3 +122,17 @@ def test_dataflow_repeatability_stress(env, split):
             assert torch.equal(h.apply(X, kern, 12, T=120), ref)
     finally:
         del os.environ["CPA_SVT_FLOW_SPLIT"]
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_bench_config_repeatability_stress(env, name):
+    """The configurations bench.py / smoke() time, exactly as they run there (c2: the two-chain launch
+    with line 12 inside it; c1: the single-block two-chain kernel): 40 runs bitwise equal."""
+    torch, P, h = env
+    cfg = W.CONFIGS[name]
+    X = torch.from_numpy(W.gen_c1() if name == "c1" else W.gen_c2()).cuda()
+    Y = torch.empty_like(X)
+    ref = h.apply(X, cfg["kernel"], cfg["K"], T=cfg["T"]).clone()
+    for _ in range(40):
+        h.apply(X, cfg["kernel"], cfg["K"], T=cfg["T"], Y=Y)
+        assert torch.equal(Y, ref)
