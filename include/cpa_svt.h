@@ -40,6 +40,13 @@
  *     synchronises the stream before returning.  cpa_svt_apply_host is always
  *     synchronous.
  *   - Y must not alias X.  Y may be any caller buffer of the same shape.
+ *   - Empty inputs are valid (dims < 0 are E_ARG): an X with m or n zero (a batch
+ *     of zero matrices, a CSR row range with no rows) has an empty Y; the call
+ *     validates its other arguments and returns CPA_SVT_OK without device work
+ *     (X and Y may then be NULL).  In a sharded call a rank's block of the long
+ *     dimension may be empty (long extent below the world size): that rank takes
+ *     part in every collective with a zero partial Gram and writes nothing; the
+ *     short dimension is global and must be >= 1.
  *   - The handle owns its workspace (Gram, two recurrence buffers, power
  *     iteration scratch, series parameters), grows it lazily and frees it in
  *     cpa_svt_free.  A handle is not thread-safe; use one per host thread.

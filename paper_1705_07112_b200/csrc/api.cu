@@ -830,8 +830,11 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
   const bool panel_cand = K > 2 && !sparse_eps &&
                           ((sharded && (h->world > 1 || env_on("CPA_SVT_PANELS"))) || (panel_sim > 1 && h->world == 1));
   const int panel_cand_P = panel_cand ? (panel_sim > 1 && h->world == 1 ? panel_sim : h->world) : 1;
-  // (the form choice sees the per-rank share of the s x s recurrence)
-  const int form = dct ? 2 : dense_form(h, s, L, K, panel_cand_P);
+  // (the form choice sees the per-rank share of the s x s recurrence; sharded: from the global
+  // long extent, so that every rank -- an empty block included -- takes the same form and so
+  // enqueues the same collectives)
+  const int64_t L_form = sharded ? std::max<int64_t>(1, (long_global + h->world - 1) / h->world) : L;
+  const int form = dct ? 2 : dense_form(h, s, L_form, K, panel_cand_P);
   const bool poly = form != 1;
   const bool panels = panel_cand && form == 2;
   const int panel_P = panels ? panel_cand_P : 1;
@@ -855,7 +858,7 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
   const size_t nCh = chain ? (size_t)(5 * chain - 4) * nG : 0;
   // line 12 folded into the m-chain launch (left side, device-resident Y, no transform; TMA needs
   // 16-byte rows of X): its units follow the last product's, row panel by row panel of H_hat
-  const bool fold12 = chain && left && !h->hp_Y && !dct && h->transform == 0 && ldx % 2 == 0 &&
+  const bool fold12 = chain && left && L > 0 && !h->hp_Y && !dct && h->transform == 0 && ldx % 2 == 0 &&
                       ((uintptr_t)X & 15) == 0 && !env_on("CPA_SVT_NO_L12_FOLD");
   const size_t nP12 = fold12 ? r32(dense_sym_l12_partial_doubles(s, n, h->num_sms)) : 0;
   const bool final_split = !env_on("CPA_SVT_FINAL_NOSPLIT");  // line-12 product split-K (default on)
@@ -914,6 +917,9 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
         CU(dense_gram_f64_chunk(X, m, n, ldx, left, G, h->stream, part, flow_sync, q, S));
         ++launches;
       }
+      --launches;
+    } else if (L == 0) {   // an empty block of a sharded X: a zero partial Gram
+      CU(cudaMemsetAsync(G, 0, (size_t)s * s * sizeof(double), h->stream));
       --launches;
     } else {
       CU(dense_gram_f64(X, m, n, ldx, left, G, h->stream, nullptr, part, flow_sync));
@@ -1021,9 +1027,12 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
   }
   tm.mark();
   if (!poly) {
-    // Alg. 1 lines 5-11 in the apply-to-X form: W_k = Psi_k(B_hat) X, Y = sum c_k W_k
-    st = run_recurrence_f64(h, left, m, n, G, X, ldx, Wa, Wb, Y, ldy, K, part, flow_sync, &launches);
-    if (st != CPA_SVT_OK) return st;
+    // Alg. 1 lines 5-11 in the apply-to-X form: W_k = Psi_k(B_hat) X, Y = sum c_k W_k (no
+    // collectives: an empty block has nothing to do)
+    if (L > 0) {
+      st = run_recurrence_f64(h, left, m, n, G, X, ldx, Wa, Wb, Y, ldy, K, part, flow_sync, &launches);
+      if (st != CPA_SVT_OK) return st;
+    }
   } else {
     // Alg. 1 literally: lines 5-11 on the s x s Gram with Psi_0 = Id (H_hat = sum c_k Psi_k),
     // then line 12: Y = H_hat X (left) or X H_hat (right) -- one product
@@ -1124,8 +1133,8 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
       }
       --launches;
       h->hp_Y = nullptr;   // delivered
-    } else if (fold12) {
-      --launches;   // (line 12 ran inside the recurrence launch)
+    } else if (fold12 || L == 0) {
+      --launches;   // (line 12 ran inside the recurrence launch / an empty block: no output)
     } else {
       if (left) CU(dense_gemm_store(s, n, s, Hm, s, X, ldx, Y, ldy, h->stream, fp, fs));
       else      CU(dense_gemm_store(m, s, s, X, ldx, Hm, s, Y, ldy, h->stream, fp, fs));
@@ -1133,8 +1142,10 @@ static cpa_svt_status apply_f64(cpa_svt_handle* h, int64_t m, int64_t n, cpa_svt
     ++launches;
   }
   tm.mark();
-  st = check_f64(h, X, m, n, ldx, Y, m, n, ldy, &launches);
-  if (st != CPA_SVT_OK) return st;
+  if (L > 0) {
+    st = check_f64(h, X, m, n, ldx, Y, m, n, ldy, &launches);
+    if (st != CPA_SVT_OK) return st;
+  }
   h->launches += launches;
   st = fill_info(h, info, lam, left ? 0 : 1);
   if (info) {
@@ -1227,7 +1238,11 @@ static cpa_svt_status apply_tf32(cpa_svt_handle* h, int terms, int64_t m, int64_
   PhaseTimer tm;
   tm.start(info != nullptr, h->stream);
   int launches = 0;
-  {
+  if (L == 0) {   // an empty block of a sharded X: a zero partial Gram (the split copies are
+                  // rebuilt from the reduced Gram below)
+    Phase p(h, CPA_SVT_PH_GRAM);
+    CU(cudaMemsetAsync(Gf, 0, (size_t)s * sp * sizeof(float), h->stream));
+  } else {
     Phase p(h, CPA_SVT_PH_GRAM);
     CU(tf32_prep(X, m, n, ldx, !left, Xs[0], Xs[1], Xs[2], Lp, h->num_sms, h->stream));
     // Gram always 3xTF32: G(i,j) = sum_l A(i,l) A(j,l), both operands K-major
@@ -1314,7 +1329,7 @@ static cpa_svt_status apply_tf32(cpa_svt_handle* h, int terms, int64_t m, int64_
                        h->stream));
     ++launches;
   }
-  for (int kk = poly ? 2 : 1; kk < K && !panels; ++kk) {
+  for (int kk = poly ? 2 : 1; kk < K && !panels && RN > 0; ++kk) {
     float** src = sets[(kk - 1) & 1];      // W_{k-1}: k=1 -> W_0
     float** out = sets[kk & 1];            // W_k overwrites W_{k-2} (k >= 2)
     const bool last = kk == K - 1;
@@ -1324,7 +1339,7 @@ static cpa_svt_status apply_tf32(cpa_svt_handle* h, int terms, int64_t m, int64_
                kk == 1 ? nullptr : out[0], ldr, Yr, ldr, h->P, kk, h->num_sms, h->stream, poly ? 1 : 0));
     ++launches;
   }
-  if (poly) {
+  if (poly && L > 0) {
     // Alg. 1 line 12: Y = H_hat A, one tcgen05 product (H_hat split into hi/lo operands)
     Phase p(h, CPA_SVT_PH_FINAL);
     CU(tf32_sym_prep(Hs[0], s, sp, Hs[1], Hs[2], h->num_sms, h->stream));  // H lower -> full hi / lo
@@ -1332,10 +1347,12 @@ static cpa_svt_status apply_tf32(cpa_svt_handle* h, int terms, int64_t m, int64_
                Lp, nullptr, nullptr, 0, nullptr, 0, nullptr, 0, h->num_sms, h->stream));
     launches += 2;
   }
-  CU(tf32_finish(Yi, Lp, m, n, !left, Y, ldy, h->num_sms, h->stream));
-  ++launches;
+  if (L > 0) {
+    CU(tf32_finish(Yi, Lp, m, n, !left, Y, ldy, h->num_sms, h->stream));
+    ++launches;
+  }
   tm.mark();
-  if (h->div_mode) {
+  if (h->div_mode && L > 0) {
     Phase p(h, CPA_SVT_PH_FINAL, 0);
     CU(divergence_check_f32(X, m, n, ldx, Y, m, n, ldy, h->dchk, h->P, h->stream));
     launches += 1;
@@ -1358,15 +1375,40 @@ cpa_svt_status cpa_svt_apply(cpa_svt_handle* h, cpa_svt_dtype dtype, cpa_svt_mat
                              cpa_svt_shard shard, int64_t long_global, const void* X, int64_t ldx, void* Y,
                              int64_t ldy, const cpa_svt_kernel* k, int K, const double* c, cpa_svt_lambda* lam,
                              cpa_svt_info* info) {
-  if (!h || !X || !Y || X == Y) return CPA_SVT_E_ARG;
-  if (m < 1 || n < 1 || ldx < n || ldy < n || K < 2 || K > CPA_SVT_KMAX) return CPA_SVT_E_ARG;
+  if (!h) return CPA_SVT_E_ARG;
+  if (m < 0 || n < 0 || ldx < n || ldy < n || K < 2 || K > CPA_SVT_KMAX) return CPA_SVT_E_ARG;
   if (shard < CPA_SVT_SHARD_NONE || shard > CPA_SVT_SHARD_ROWS) return CPA_SVT_E_ARG;
+  // Empty inputs.  Without a shard mode (or a communicator) an empty X has an empty Y: nothing
+  // to do, no device work.  In a sharded call the rank's block of the long dimension may be
+  // empty (a long extent below the world size: dist.shard_range): that rank still takes part in
+  // every collective with a zero partial Gram and its share of the s x s steps, and writes no
+  // output; the short dimension is global and must be >= 1.
+  const bool sharded_call = shard != CPA_SVT_SHARD_NONE && h->comm != nullptr;
+  const bool empty_block = sharded_call && (shard == CPA_SVT_SHARD_COLS ? (n == 0 && m >= 1) : (m == 0 && n >= 1));
+  if (!empty_block && (m >= 1 && n >= 1) && (!X || !Y || X == Y)) return CPA_SVT_E_ARG;
   if (!c) {
     cpa_svt_status st = check_kernel(k);
     if (st != CPA_SVT_OK) return st;
   }
   cpa_svt_status st = check_lambda(lam);
   if (st != CPA_SVT_OK) return st;
+  const bool supported = (dtype == CPA_SVT_F64 && math == CPA_SVT_MATH_NATIVE) ||
+                         (dtype == CPA_SVT_F32 && (math == CPA_SVT_MATH_TF32 || math == CPA_SVT_MATH_3XTF32) &&
+                          !h->transform);
+  if (!supported) return CPA_SVT_E_UNSUPPORTED;
+  if ((m == 0 || n == 0) && !empty_block) {
+    if (sharded_call) return CPA_SVT_E_ARG;   // (an empty short dimension: the global X is empty)
+    if (info) {
+      *info = cpa_svt_info{};
+      info->side = m <= n ? 0 : 1;
+      info->degenerate = 1;
+    }
+    if (lam && lam->want_lambda) {
+      lam->lambda_hat = lam->lambda_max > 0.0 ? lam->lambda_max / lam->safety : 0.0;
+      if (!(lam->lambda_max > 0.0)) lam->lambda_max = 0.0;
+    }
+    return CPA_SVT_OK;
+  }
   if (cudaSetDevice(h->device) != cudaSuccess) return CPA_SVT_E_CUDA;
   cpa_svt_kernel kz{};
   if (!k) k = &kz;
@@ -1405,7 +1447,11 @@ cpa_svt_status cpa_svt_debug_gemm_tf32(cpa_svt_handle* h, int M, int N, int Kd, 
 cpa_svt_status cpa_svt_apply_host(cpa_svt_handle* h, cpa_svt_dtype dtype, cpa_svt_math math, int64_t m, int64_t n,
                                   const void* X_host, void* Y_host, const cpa_svt_kernel* k, int K,
                                   cpa_svt_lambda* lam, cpa_svt_info* info) {
-  if (!h || !X_host || !Y_host || m < 1 || n < 1) return CPA_SVT_E_ARG;
+  if (!h || m < 0 || n < 0) return CPA_SVT_E_ARG;
+  if (m == 0 || n == 0)   // an empty X: cpa_svt_apply validates the rest and returns (no device work)
+    return cpa_svt_apply(h, dtype, math, m, n, CPA_SVT_SHARD_NONE, 0, nullptr, n, nullptr, n, k, K, nullptr, lam,
+                         info);
+  if (!X_host || !Y_host) return CPA_SVT_E_ARG;
   const size_t es = dtype == CPA_SVT_F64 ? 8 : 4;
   const size_t bytes = (size_t)m * n * es;
   if (cudaSetDevice(h->device) != cudaSuccess) return CPA_SVT_E_CUDA;
@@ -1561,15 +1607,16 @@ cpa_svt_status cpa_svt_admm_recover(cpa_svt_handle* h, int64_t m, int64_t n, con
 cpa_svt_status cpa_svt_apply_batched(cpa_svt_handle* h, int64_t batch, int m, int n, const float* X, float* Y,
                                      const cpa_svt_kernel* k, int K, const cpa_svt_lambda* lam,
                                      float* lambda_out) {
-  if (!h || !X || !Y || (const void*)X == (void*)Y || batch < 0 || m < 1 || n < 1 || m > 64 || n > 64)
-    return CPA_SVT_E_ARG;
+  if (!h || batch < 0 || m < 0 || n < 0 || m > 64 || n > 64) return CPA_SVT_E_ARG;
+  const bool empty = batch == 0 || m == 0 || n == 0;   // nothing to shrink: no device work
+  if (!empty && (!X || !Y || (const void*)X == (void*)Y)) return CPA_SVT_E_ARG;
   if (K < 2 || K > CPA_SVT_KMAX) return CPA_SVT_E_ARG;
   cpa_svt_status st = check_kernel(k);
   if (st != CPA_SVT_OK) return st;
   st = check_lambda(lam);
   if (st != CPA_SVT_OK) return st;
   if (K > 128) return CPA_SVT_E_UNSUPPORTED;
-  if (batch == 0) return CPA_SVT_OK;
+  if (empty) return CPA_SVT_OK;
   if (cudaSetDevice(h->device) != cudaSuccess) return CPA_SVT_E_CUDA;
   st = grow(h, &h->ws, &h->ws_bytes, 128 * 128 * sizeof(double));  // cos table
   if (st != CPA_SVT_OK) return st;
@@ -1591,9 +1638,12 @@ cpa_svt_status cpa_svt_apply_csr(cpa_svt_handle* h, int64_t m, int64_t n, int64_
                                  const int32_t* col, const double* val, int64_t row_begin, int64_t row_end,
                                  double* Y, int64_t ldy, const cpa_svt_kernel* k, int K, const double* c,
                                  cpa_svt_lambda* lam, cpa_svt_info* info) {
-  if (!h || !row_ptr || !Y || m < 1 || n < 1 || nnz < 0 || (nnz > 0 && (!col || !val))) return CPA_SVT_E_ARG;
+  if (!h || m < 0 || n < 0 || nnz < 0 || (nnz > 0 && (!col || !val))) return CPA_SVT_E_ARG;
   if (row_begin < 0 || row_end > m || row_begin > row_end || ldy < n || K < 2 || K > CPA_SVT_KMAX)
     return CPA_SVT_E_ARG;
+  // an empty X (m or n zero): an empty Y, no device work (after the argument checks below)
+  const bool empty = m == 0 || n == 0;
+  if (!empty && (!row_ptr || (!Y && row_end > row_begin))) return CPA_SVT_E_ARG;
   if (m > 2147483647 || n > 2147483647) return CPA_SVT_E_ARG;
   cpa_svt_status st = CPA_SVT_OK;
   cpa_svt_kernel kz{};
@@ -1605,6 +1655,14 @@ cpa_svt_status cpa_svt_apply_csr(cpa_svt_handle* h, int64_t m, int64_t n, int64_
   }
   st = check_lambda(lam);
   if (st != CPA_SVT_OK) return st;
+  if (empty) {
+    if (info) {
+      *info = cpa_svt_info{};
+      info->side = 1;
+      info->degenerate = 1;
+    }
+    return CPA_SVT_OK;
+  }
   if (cudaSetDevice(h->device) != cudaSuccess) return CPA_SVT_E_CUDA;
   const double* c_dev = nullptr;
   if (c) {
