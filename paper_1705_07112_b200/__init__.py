@@ -29,6 +29,14 @@ STATUS = {0: "ok", 1: "E_ARG", 2: "E_DOMAIN", 3: "E_DIVERGED", 4: "E_CUDA", 5: "
           7: "E_UNSUPPORTED"}
 
 
+def _require(cond, msg: str):
+    """Argument check of the binding (raises ValueError; not an assert, so it survives python -O):
+    the library writes through the pointers it is given, so shapes, dtypes and devices of every
+    output buffer are checked before the call."""
+    if not cond:
+        raise ValueError(msg)
+
+
 class Kernel(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("tau_relative", ctypes.c_int32), ("tau", ctypes.c_double),
                 ("w_c", ctypes.c_double), ("w_shift", ctypes.c_double), ("w_eps", ctypes.c_double)]
@@ -155,6 +163,10 @@ class Handle:
         self.rank, self.world = rank, world
         self.has_comm = nccl_id is not None   # the library created an NCCL communicator (any world size)
 
+    def _on_device(self, t):
+        _require(t.device.index == self.device,
+                 f"tensor on {t.device}, handle on cuda:{self.device} (the library's kernels run on the handle's device)")
+
     def _check(self, st, what):
         if st:
             raise CpaSvtError(st, f"{what}: {lib.cpa_svt_last_error(self._h).decode()}")
@@ -234,12 +246,15 @@ class Handle:
         """cpa_svt_apply on a 2-D CUDA tensor (float64: DMMA path; float32: tcgen05 3xTF32 by
         default, math='tf32' for the single-pass reduced-accuracy mode)."""
         torch = self._torch
-        assert X.is_cuda and X.dim() == 2 and X.stride(1) == 1 and X.dtype in (torch.float64, torch.float32)
+        _require(X.is_cuda and X.dim() == 2 and X.stride(1) == 1 and X.dtype in (torch.float64, torch.float32),
+                 "X must be a 2-D float64 / float32 CUDA tensor with unit column stride")
+        self._on_device(X)
         if math is None:
             math = "native" if X.dtype == torch.float64 else "3xtf32"
         if Y is None:
             Y = torch.empty(X.shape, dtype=X.dtype, device=X.device)
-        assert Y.shape == X.shape and Y.dtype == X.dtype and Y.stride(1) == 1 and Y.device == X.device
+        _require(Y.shape == X.shape and Y.dtype == X.dtype and Y.stride(1) == 1 and Y.device == X.device,
+                 "Y must be a CUDA tensor shaped like X, of X's dtype, with unit column stride")
         dt = F64 if X.dtype == torch.float64 else F32
         lam = self._lambda(T, safety, lambda_max, want_lambda)
         inf = Info() if info else None
@@ -259,7 +274,10 @@ class Handle:
                    math: str = "native", info: bool = False):
         """cpa_svt_apply_host: X, Y are contiguous CPU tensors (pinned for full bandwidth)."""
         torch = self._torch
-        assert not X.is_cuda and X.is_contiguous() and Y.is_contiguous() and X.shape == Y.shape
+        # the library copies m*n elements of X's dtype into Y: Y must be that large and of that dtype
+        _require(not X.is_cuda and not Y.is_cuda and X.dim() == 2 and X.is_contiguous() and Y.is_contiguous()
+                 and X.shape == Y.shape and X.dtype == Y.dtype and X.dtype in (torch.float64, torch.float32),
+                 "X and Y must be contiguous 2-D host tensors of one shape and dtype (float64 / float32)")
         dt = F64 if X.dtype == torch.float64 else F32
         lam = self._lambda(T, safety, lambda_max, False)
         inf = Info() if info else None
@@ -273,16 +291,18 @@ class Handle:
                       Y=None, lambda_out=None):
         """cpa_svt_apply_batched on a [batch, m, n] float32 CUDA tensor."""
         torch = self._torch
-        assert X.is_cuda and X.dim() == 3 and X.dtype == torch.float32 and X.is_contiguous()
+        _require(X.is_cuda and X.dim() == 3 and X.dtype == torch.float32 and X.is_contiguous(),
+                 "X must be a contiguous [batch, m, n] float32 CUDA tensor")
+        self._on_device(X)
         if Y is None:
             Y = torch.empty_like(X)
         # the kernel writes batch*m*n floats at Y and one float per matrix at lambda_out
-        assert (Y.is_cuda and Y.device == X.device and Y.dtype == torch.float32 and Y.is_contiguous()
-                and Y.shape == X.shape), "Y must be a contiguous float32 CUDA tensor shaped like X"
+        _require(Y.is_cuda and Y.device == X.device and Y.dtype == torch.float32 and Y.is_contiguous()
+                 and Y.shape == X.shape, "Y must be a contiguous float32 CUDA tensor shaped like X")
         if lambda_out is not None:
-            assert (lambda_out.is_cuda and lambda_out.device == X.device and lambda_out.dtype == torch.float32
-                    and lambda_out.is_contiguous() and lambda_out.numel() >= X.shape[0]), \
-                "lambda_out must be a contiguous float32 CUDA tensor with >= batch elements"
+            _require(lambda_out.is_cuda and lambda_out.device == X.device and lambda_out.dtype == torch.float32
+                     and lambda_out.is_contiguous() and lambda_out.numel() >= X.shape[0],
+                     "lambda_out must be a contiguous float32 CUDA tensor with >= batch elements")
         lam = self._lambda(T, safety, lambda_max, False)
         st = lib.cpa_svt_apply_batched(self._h, X.shape[0], X.shape[1], X.shape[2], X.data_ptr(), Y.data_ptr(),
                                        ctypes.byref(kernel_from_dict(kernel)), K, ctypes.byref(lam),
@@ -296,10 +316,15 @@ class Handle:
         m x n) under a uint8 CUDA mask (nonzero = observed); returns (L, info).  adaptive_eps: the
         recommended epsilon(E_t) schedule of PAPER.md:968-975 (needs set_transform('dct'|'dct8'))."""
         torch = self._torch
-        assert D.is_cuda and D.dtype == torch.float64 and D.is_contiguous() and D.dim() == 2
-        assert mask.is_cuda and mask.dtype == torch.uint8 and mask.shape == D.shape and mask.is_contiguous()
+        _require(D.is_cuda and D.dtype == torch.float64 and D.is_contiguous() and D.dim() == 2,
+                 "D must be a contiguous 2-D float64 CUDA tensor")
+        self._on_device(D)
+        _require(mask.is_cuda and mask.dtype == torch.uint8 and mask.shape == D.shape and mask.is_contiguous()
+                 and mask.device == D.device, "mask must be a contiguous uint8 CUDA tensor shaped like D")
         if L is None:
             L = torch.empty_like(D)
+        _require(L.is_cuda and L.dtype == torch.float64 and L.is_contiguous() and L.shape == D.shape
+                 and L.device == D.device, "L must be a contiguous float64 CUDA tensor shaped like D")
         lam = self._lambda(T, safety, 0.0, False)
         opt = Admm(float(rho), float(eta), float(tol), int(max_iter), 0, 0.0, 0.0, 0.0, int(bool(adaptive_eps)), 0)
         st = lib.cpa_svt_admm_recover(self._h, D.shape[0], D.shape[1], D.data_ptr(), mask.data_ptr(), K,
@@ -313,15 +338,19 @@ class Handle:
         """cpa_svt_apply_csr: CSR X (int64 row_ptr, int32 col, float64 val, all CUDA); returns dense rows."""
         torch = self._torch
         row_end = m if row_end is None else row_end
-        assert row_ptr.is_cuda and row_ptr.dtype == torch.int64 and row_ptr.is_contiguous() and row_ptr.numel() == m + 1
-        assert col.is_cuda and col.dtype == torch.int32 and col.is_contiguous()
-        assert val.is_cuda and val.dtype == torch.float64 and val.is_contiguous() and col.numel() == val.numel()
-        assert 0 <= row_begin <= row_end <= m
+        _require(row_ptr.is_cuda and row_ptr.dtype == torch.int64 and row_ptr.is_contiguous()
+                 and row_ptr.numel() == m + 1, "row_ptr must be a contiguous int64 CUDA tensor of m + 1 entries")
+        self._on_device(row_ptr)
+        _require(col.is_cuda and col.dtype == torch.int32 and col.is_contiguous() and col.device == row_ptr.device,
+                 "col must be a contiguous int32 CUDA tensor")
+        _require(val.is_cuda and val.dtype == torch.float64 and val.is_contiguous() and col.numel() == val.numel()
+                 and val.device == row_ptr.device, "val must be a contiguous float64 CUDA tensor, one per col entry")
+        _require(0 <= row_begin <= row_end <= m, "need 0 <= row_begin <= row_end <= m")
         if Y is None:
             Y = torch.empty((row_end - row_begin, n), dtype=torch.float64, device=val.device)
-        assert (Y.is_cuda and Y.device == val.device and Y.dtype == torch.float64 and Y.dim() == 2
-                and Y.stride(1) == 1 and Y.shape[0] >= row_end - row_begin and Y.shape[1] == n), \
-            "Y must be a float64 CUDA tensor with >= row_end - row_begin rows of n columns"
+        _require(Y.is_cuda and Y.device == val.device and Y.dtype == torch.float64 and Y.dim() == 2
+                 and Y.stride(1) == 1 and Y.shape[0] >= row_end - row_begin and Y.shape[1] == n,
+                 "Y must be a float64 CUDA tensor with >= row_end - row_begin rows of n columns")
         lam = self._lambda(T, safety, lambda_max, want_lambda)
         inf = Info() if info else None
         cbuf = (ctypes.c_double * len(coeffs))(*coeffs) if coeffs is not None else None

@@ -120,13 +120,13 @@ def test_batched_argument_checks(env):
     torch, P, h = env
     X = torch.zeros((4, 8, 8), dtype=torch.float32, device="cuda")
     kern = {"kind": "soft", "tau": 0.5}
-    with pytest.raises(AssertionError):
+    with pytest.raises(ValueError):
         h.apply_batched(X, kern, 5, Y=torch.zeros((3, 8, 8), dtype=torch.float32, device="cuda"))
-    with pytest.raises(AssertionError):
+    with pytest.raises(ValueError):
         h.apply_batched(X, kern, 5, Y=torch.zeros((4, 8, 8), dtype=torch.float64, device="cuda"))
-    with pytest.raises(AssertionError):
+    with pytest.raises(ValueError):
         h.apply_batched(X, kern, 5, lambda_out=torch.zeros(3, dtype=torch.float32, device="cuda"))
-    with pytest.raises(AssertionError):
+    with pytest.raises(ValueError):
         h.apply_batched(X, kern, 5, lambda_out=torch.zeros(4, dtype=torch.float64, device="cuda"))
 
 

@@ -531,3 +531,20 @@ def test_chain_line12_fold_variants(env, case):
     assert info["rec_products"] == 27   # Psi_2 from the power iteration's squaring (R29)
     assert O.rel_fro(Y, Ysep) <= 1e-12
     assert O.rel_fro(Y, O.cpa_shrink(X, O.Kernel(**kern), 30, T=300)) <= TOL64
+
+
+def test_binding_rejects_mismatched_buffers(env):
+    """The binding checks every buffer the library writes through (ValueError, not assert): an
+    apply_host Y of another dtype would take m*n*8 bytes into a 4-byte-per-element host buffer."""
+    torch, P, h = env
+    kern = {"kind": "soft", "tau": 0.5}
+    X = torch.zeros((8, 8), dtype=torch.float64)
+    with pytest.raises(ValueError):
+        h.apply_host(X, torch.zeros((8, 8), dtype=torch.float32), kern, 5)
+    with pytest.raises(ValueError):
+        h.apply_host(X, torch.zeros((8, 4), dtype=torch.float64), kern, 5)
+    Xd = X.cuda()
+    with pytest.raises(ValueError):
+        h.apply(Xd, kern, 5, Y=torch.zeros((8, 8), dtype=torch.float32, device="cuda"))
+    with pytest.raises(ValueError):
+        h.apply(Xd.cpu(), kern, 5)
