@@ -264,6 +264,28 @@ def test_p15_power_iteration():
     assert O.power_iteration(lambda v: 0 * v, 5, 10)[0] == 0.0
 
 
+def test_p15b_power_iteration_finite_T_closed_form():
+    """Every iterate, not only the converged value: for Phi = diag(a) and v_0 = 1_s / sqrt(s)
+    (reading R6), v_{t-1} is proportional to Phi^{t-1} 1, so
+    lambda_t = ||Phi v_{t-1}|| = sqrt(sum a_i^{2t} / sum a_i^{2t-2}) exactly (sum a_i^0 = s).
+    Pins the start vector and the product count T (a v_0 or an off-by-one in T changes
+    lambda_T); the reference values are exact rationals (fractions), not the oracle's arithmetic.
+    Hand values for SPEC.md:61's diag(1, 2, 3): lambda_1 = sqrt(14/3), lambda_2 = sqrt(7)."""
+    from fractions import Fraction
+    lam1, _ = O.power_iteration(lambda v: np.diag([1.0, 2.0, 3.0]) @ v, 3, 1)
+    assert abs(lam1 - math.sqrt(14.0 / 3.0)) <= 1e-15 * lam1
+    lam2, hist2 = O.power_iteration(lambda v: np.diag([1.0, 2.0, 3.0]) @ v, 3, 2)
+    assert abs(lam2 - math.sqrt(7.0)) <= 1e-15 * lam2 and len(hist2) == 2
+    for a, T in (([1, 2, 3], 7), ([5, 1, 4, 4, 2], 12), ([3, 3, 1], 30), ([7, 6, 1, 2, 2, 5, 6], 40)):
+        G = np.diag(np.array(a, dtype=np.float64))
+        lam, hist = O.power_iteration(lambda v: G @ v, len(a), T)
+        assert len(hist) == T
+        for t, got in enumerate(hist, start=1):
+            want = math.sqrt(Fraction(sum(x ** (2 * t) for x in a), sum(x ** (2 * t - 2) for x in a)))
+            assert abs(got - want) <= 4e-15 * want, (a, t, got, want)
+        assert lam == hist[-1]
+
+
 # --- P17: the paper's block-diagonal D, closed form ------------------------------------------------------
 
 @pytest.mark.parametrize("N,nb,copies", [(1000, 10, 1), (200, 4, 1), (120, 6, 4)])
@@ -304,6 +326,15 @@ def test_vector_forms_match_alg1():
     Xt = Xw.T.copy()
     Yr, _ = O.cpa_shrink_rows(Xt, [3, 4], k, 14, T=100)
     assert O.rel_fro(Yr, Y.T[[3, 4], :]) < 1e-12
+    # unconverged power iterations (T = 3, 7): the vector forms run the same T products from the
+    # same 1/sqrt(s) on the same (Gram) side as Alg. 1, so lambda_hat and the columns still agree
+    for T in (3, 7):
+        Yt, it = O.cpa_shrink(Xw, k, 14, T=T, return_info=True)
+        Yc, ic = O.cpa_shrink_columns(Xw, [0, 7, 29], k, 14, T=T)
+        Yr, ir = O.cpa_shrink_rows(Xt, [3, 4], k, 14, T=T)
+        for inf in (ic, ir):
+            assert abs(inf["lambda_hat"] - it["lambda_hat"]) <= 1e-13 * it["lambda_hat"], (T, inf, it)
+        assert O.rel_fro(Yc, Yt[:, [0, 7, 29]]) < 1e-12 and O.rel_fro(Yr, Yt.T[[3, 4], :]) < 1e-12
     # sparse: lambda from the m-side (XX^T) power iteration; use a given lambda to compare forms
     row_ptr, col, val = W.gen_c4(m=40, n=400, nnz=800)
     Xs = sp.csr_matrix((val, col, row_ptr), shape=(40, 400))
