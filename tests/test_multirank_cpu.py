@@ -218,3 +218,29 @@ def test_apply_sharded_arguments_gloo():
     h = _RecordingHandle(1, has_comm=False)
     D.apply_sharded(h, np.zeros((4, 9)), 4, 9, {"kind": "soft"}, 5)
     assert h.calls[0]["shard"] == "none"
+
+
+def _empty_block_args(rank, world):
+    D = _load_dist()
+    out = []
+    for (m, n) in ((3, 3), (5, 4)):     # long extent 3 / 5 < 2 ranks x 2: ... and a tall one
+        X = np.zeros((m, n))
+        h = _RecordingHandle(world)
+        blk = D.local_block(X, 4 * world, rank)   # 4 * world "ranks" of which this is one: empty blocks
+        D.apply_sharded(h, blk, m, n, {"kind": "soft"}, 5, T=3)
+        out.append((h.calls[0]["shard"], h.calls[0]["long_global"], blk.shape))
+    return out
+
+
+def test_empty_blocks_make_the_same_call_gloo():
+    """A long extent below the number of ranks leaves some ranks an empty block; those ranks make
+    the SAME library call (shard mode, global long extent) as their peers, only with a zero-width
+    block -- the library then joins every collective with a zero partial Gram (empty
+    inputs) instead of returning early."""
+    res = _run(_empty_block_args)
+    for r in (0, 1):
+        (s1, l1, sh1), (s2, l2, sh2) = res[r]
+        assert (s1, l1) == ("cols", 3) and (s2, l2) == ("rows", 5)
+    D = _load_dist()
+    shapes = [D.local_block(np.zeros((3, 3)), 8, r).shape for r in range(8)]
+    assert sum(sh[1] for sh in shapes) == 3 and shapes[-1] == (3, 0)
