@@ -39,6 +39,20 @@ MUTS = [
  ("batched safety", "Y[b], info = cpa_shrink(Xb[b], kernel, K, T=T, safety=safety, return_info=True)", "Y[b], info = cpa_shrink(Xb[b], kernel, K, T=T, safety=safety * 1.001, return_info=True)"),
  ("alg1 T+1", "        lambda: power_iteration(lambda v: Phi_ @ v, n, T)[0], lam_override, safety)", "        lambda: power_iteration(lambda v: Phi_ @ v, n, T + 1)[0], lam_override, safety)"),
  ("sparse T+1", "return power_iteration(lambda v: Xs @ (Xs.T @ v), m, T)", "return power_iteration(lambda v: Xs @ (Xs.T @ v), m, T + 1)"),
+ ("haar high sign", "        T[nl + i, 2 * i + 1] = -r", "        T[nl + i, 2 * i + 1] = r"),
+ ("haar odd tail", "        T[nl - 1, n - 1] = 1.0", "        T[nl - 1, n - 1] = r"),
+ ("dct a0", "    C[0, :] = math.sqrt(1.0 / n)", "    C[0, :] = math.sqrt(2.0 / n)"),
+ ("dct phase", "    C = np.cos(np.pi * (2 * j + 1) * k / (2 * n)) * math.sqrt(2.0 / n)", "    C = np.cos(np.pi * (2 * j) * k / (2 * n)) * math.sqrt(2.0 / n)"),
+ ("block dct size", "def dct2_block_matrix(n: int, b: int = 8) -> np.ndarray:", "def dct2_block_matrix(n: int, b: int = 4) -> np.ndarray:"),
+ ("haar highpass kept", "        Phi_[nl:, :] = 0.0\n        Phi_[:, nl:] = 0.0", "        Phi_[nl:, :] = 0.0"),
+ ("threshold >", "    return np.where(A >= thr, Phi, 0.0), thr", "    return np.where(A > thr, Phi, 0.0), thr"),
+ ("topk index", "        thr = float(flat[min(max(k, 1), flat.size) - 1])", "        thr = float(flat[min(max(k, 1), flat.size - 1)])"),
+ ("transform line12", "    Y = B @ Tm.T @ H @ Tm\n", "    Y = B @ Tm @ H @ Tm.T\n"),
+ ("eps schedule El", "    frac = 0.5e-4 if E > 0.3e-1 else (1.5e-4 if E > 6e-4 else 0.5e-3)", "    frac = 0.5e-4 if E > 0.3e-2 else (1.5e-4 if E > 6e-4 else 0.5e-3)"),
+ ("synthetic D", "        D[b * p:(b + 1) * p, b * p:(b + 1) * p] -= 0.5", "        D[b * p:(b + 1) * p, b * p:(b + 1) * p] -= 0.25"),
+ ("admm l update", "        l = ((z1 - u1) + psit(z2 - u2) + w * (z3 - u3) + (z4 - u4)) / (3.0 + w)", "        l = ((z1 - u1) + psit(z2 - u2) + w * (z3 - u3) + (z4 - u4)) / (4.0 + w)"),
+ ("admm z2 threshold", "        z2 = np.sign(v2) * np.maximum(np.abs(v2) - eta / rho, 0.0)", "        z2 = np.sign(v2) * np.maximum(np.abs(v2) - eta * rho, 0.0)"),
+ ("admm z4 clip", "        z4 = np.clip(l + u4, 0.0, 1.0)", "        z4 = np.clip(l + u4, 0.0, 2.0)"),
 ]
 
 
