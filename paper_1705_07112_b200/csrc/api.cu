@@ -1378,6 +1378,8 @@ cpa_svt_status cpa_svt_apply(cpa_svt_handle* h, cpa_svt_dtype dtype, cpa_svt_mat
   if (!h) return CPA_SVT_E_ARG;
   if (m < 0 || n < 0 || ldx < n || ldy < n || K < 2 || K > CPA_SVT_KMAX) return CPA_SVT_E_ARG;
   if (shard < CPA_SVT_SHARD_NONE || shard > CPA_SVT_SHARD_ROWS) return CPA_SVT_E_ARG;
+  if ((dtype != CPA_SVT_F64 && dtype != CPA_SVT_F32) || math < CPA_SVT_MATH_NATIVE || math > CPA_SVT_MATH_3XTF32)
+    return CPA_SVT_E_ARG;   // (bad enum; valid but unbuilt combinations are E_UNSUPPORTED below)
   // Empty inputs.  Without a shard mode (or a communicator) an empty X has an empty Y: nothing
   // to do, no device work.  In a sharded call the rank's block of the long dimension may be
   // empty (a long extent below the world size: dist.shard_range): that rank still takes part in
@@ -1607,7 +1609,7 @@ cpa_svt_status cpa_svt_admm_recover(cpa_svt_handle* h, int64_t m, int64_t n, con
 cpa_svt_status cpa_svt_apply_batched(cpa_svt_handle* h, int64_t batch, int m, int n, const float* X, float* Y,
                                      const cpa_svt_kernel* k, int K, const cpa_svt_lambda* lam,
                                      float* lambda_out) {
-  if (!h || batch < 0 || m < 0 || n < 0 || m > 64 || n > 64) return CPA_SVT_E_ARG;
+  if (!h || batch < 0 || m < 0 || n < 0) return CPA_SVT_E_ARG;
   const bool empty = batch == 0 || m == 0 || n == 0;   // nothing to shrink: no device work
   if (!empty && (!X || !Y || (const void*)X == (void*)Y)) return CPA_SVT_E_ARG;
   if (K < 2 || K > CPA_SVT_KMAX) return CPA_SVT_E_ARG;
@@ -1615,7 +1617,7 @@ cpa_svt_status cpa_svt_apply_batched(cpa_svt_handle* h, int64_t batch, int m, in
   if (st != CPA_SVT_OK) return st;
   st = check_lambda(lam);
   if (st != CPA_SVT_OK) return st;
-  if (K > 128) return CPA_SVT_E_UNSUPPORTED;
+  if (K > 128 || m > 64 || n > 64) return CPA_SVT_E_UNSUPPORTED;   // (the header's contract)
   if (empty) return CPA_SVT_OK;
   if (cudaSetDevice(h->device) != cudaSuccess) return CPA_SVT_E_CUDA;
   st = grow(h, &h->ws, &h->ws_bytes, 128 * 128 * sizeof(double));  // cos table

@@ -149,3 +149,16 @@ def test_batched_psi2_from_squaring(env, K, T):
     assert np.array_equal(lam, lam0)
     assert O.rel_fro(Y.astype(np.float64), Y0.astype(np.float64)) <= 1e-5
     assert O.rel_fro(Y.astype(np.float64), Yo) <= 1e-4
+
+
+def test_batched_size_limits(env):
+    """The header's contract: m, n <= 64 and K <= 128, else CPA_SVT_E_UNSUPPORTED (a valid request
+    this build does not implement); negative sizes are argument errors."""
+    torch, P, h = env
+    kern = {"kind": "soft", "tau": 0.5}
+    for shape, K in (((2, 65, 8), 5), ((2, 8, 65), 5), ((2, 8, 8), 129)):
+        X = torch.zeros(shape, dtype=torch.float32, device="cuda")
+        with pytest.raises(P.CpaSvtError) as e:
+            h.apply_batched(X, kern, K)
+        assert e.value.status == 7, (shape, K)
+

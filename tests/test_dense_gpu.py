@@ -548,3 +548,20 @@ def test_binding_rejects_mismatched_buffers(env):
         h.apply(Xd, kern, 5, Y=torch.zeros((8, 8), dtype=torch.float32, device="cuda"))
     with pytest.raises(ValueError):
         h.apply(Xd.cpu(), kern, 5)
+
+
+def test_enum_arguments(env):
+    """Bad enums are E_ARG; a valid but unbuilt combination (fp32 data, MATH_NATIVE) is
+    E_UNSUPPORTED -- also for an empty X (header: cpa_svt_status)."""
+    import ctypes
+    torch, P, h = env
+    k = P.kernel_from_dict({"kind": "soft", "tau": 0.5})
+    lam = P.Lambda(10, 0, 1.01, 0.0, 0.0)
+    X = torch.zeros((8, 8), dtype=torch.float64, device="cuda")
+    Y = torch.zeros_like(X)
+    call = lambda dt, math, m=8: P.lib.cpa_svt_apply(h._h, dt, math, m, 8, 0, 0, X.data_ptr(), 8, Y.data_ptr(), 8,
+                                                     ctypes.byref(k), 5, None, ctypes.byref(lam), None)
+    assert call(2, 0) == 1 and call(0, 3) == 1 and call(-1, 0) == 1
+    assert call(1, 0) == 7 and call(1, 0, m=0) == 7
+    assert call(0, 0) == 0
+
