@@ -29,7 +29,7 @@ __all__ = [
     "sparse_power_iteration", "cpa_shrink_sparse_rows", "jacobi_svd",
     "exact_shrink", "svd_characterization", "rel_fro", "haar1_matrix", "cpa_shrink_transform",
     "dct2_matrix", "dct2_block_matrix", "synthetic_D", "admm_recover", "threshold_components",
-    "epsilon_schedule_k",
+    "epsilon_schedule_k", "admm_l_step", "admm_z2_step", "admm_z4_step",
     "DEFAULT_SAFETY", "DEGENERATE_LAMBDA",
 ]
 
@@ -406,6 +406,25 @@ def epsilon_schedule_k(E: float, n: int) -> int:
     return max(1, int(frac * n * n))
 
 
+def admm_l_step(zu1, zu2, zu3, zu4, w, psit):
+    """l-update of the ADMM (eq. admm_algorithm_inp): the least-squares
+    solution l = (K^T K)^-1 K^T (z - u) of K l = z - u for K l = [l; Psi l; Omega l; l] (Psi the
+    orthonormal 2-D DCT, so Psi^T Psi = I; Omega = diag(mask), mask in {0, 1}): K^T K = (3 + mask) I
+    elementwise.  zu_i = z_i - u_i."""
+    return (zu1 + psit(zu2) + w * zu3 + zu4) / (3.0 + w)
+
+
+def admm_z2_step(v, eta: float, rho: float):
+    """z2-update: prox of (eta / rho) ||.||_1 at v, the elementwise soft threshold at eta / rho
+    (PAPER.md:1193-1214)."""
+    return np.sign(v) * np.maximum(np.abs(v) - eta / rho, 0.0)
+
+
+def admm_z4_step(v):
+    """z4-update: Euclidean projection onto the box [0, 1] (Pi_D)."""
+    return np.clip(v, 0.0, 1.0)
+
+
 def admm_recover(D_obs, mask, kernel: Kernel, K: int, T: int, rho: float, eta: float,
                  max_iter: int = 300, tol: float = 1e-4, shrink=None, return_history: bool = False,
                  transform: str | None = None, adaptive_eps: bool = False):
@@ -447,12 +466,11 @@ def admm_recover(D_obs, mask, kernel: Kernel, K: int, T: int, rho: float, eta: f
     hist = []
     for it in range(max_iter):
         l_prev = l
-        l = ((z1 - u1) + psit(z2 - u2) + w * (z3 - u3) + (z4 - u4)) / (3.0 + w)
+        l = admm_l_step(z1 - u1, z2 - u2, z3 - u3, z4 - u4, w, psit)
         pl = psi(l)
         z1 = shrink(l + u1)
-        v2 = pl + u2
-        z2 = np.sign(v2) * np.maximum(np.abs(v2) - eta / rho, 0.0)
-        z4 = np.clip(l + u4, 0.0, 1.0)
+        z2 = admm_z2_step(pl + u2, eta, rho)
+        z4 = admm_z4_step(l + u4)
         u1 = u1 + l - z1
         u2 = u2 + pl - z2
         u3 = u3 + w * l - z3

@@ -671,3 +671,36 @@ def test_relative_tau_is_tau_times_sigma_max():
     # scale invariance of a relative threshold: shrink(a X) = a shrink(X)
     k = O.Kernel("soft", tau=0.37, tau_relative=True)
     assert O.rel_fro(O.cpa_shrink(3.0 * X, k, 16, T=400), 3.0 * O.cpa_shrink(X, k, 16, T=400)) < 1e-12
+
+
+# ---- NEXT-3 ADMM steps against their definitions (eq. admm_algorithm_inp)
+
+def test_admm_steps_match_their_definitions():
+    """Each ADMM sub-step against what defines it, computed another way:
+    z2 = prox of (eta/rho)|.| -- argmin_z eta |z| + rho/2 (z - v)^2 by bounded scalar minimisation;
+    z4 = Euclidean projection onto [0, 1] -- argmin over [0, 1] the same way;
+    l  = least-squares solution of K l = z - u with K = [I; Psi; diag(mask); I] assembled as an
+         explicit matrix (Psi = C_m (.) C_n^T on the row-major vec: kron(C_m, C_n)) -- numpy lstsq."""
+    from scipy.optimize import minimize_scalar
+    rng = np.random.default_rng(11)
+    eta, rho = 0.7, 2.5                                  # eta / rho = 0.28, eta * rho = 1.75
+    v = rng.uniform(-2.0, 2.0, 40)
+    z2 = O.admm_z2_step(v, eta, rho)
+    for vi, zi in zip(v, z2):
+        r = minimize_scalar(lambda z: eta * abs(z) + 0.5 * rho * (z - vi) ** 2, bounds=(-3, 3), method="bounded",
+                            options={"xatol": 1e-12})
+        assert abs(zi - r.x) < 1e-7, (vi, zi, r.x)
+    v4 = rng.uniform(-1.0, 2.0, 40)
+    z4 = O.admm_z4_step(v4)
+    for vi, zi in zip(v4, z4):
+        r = minimize_scalar(lambda z: (z - vi) ** 2, bounds=(0.0, 1.0), method="bounded", options={"xatol": 1e-12})
+        assert abs(zi - r.x) < 1e-6, (vi, zi, r.x)
+    m, n = 3, 4
+    Cm, Cn = O.dct2_matrix(m), O.dct2_matrix(n)
+    w = (rng.random((m, n)) < 0.6).astype(float)
+    zu = [rng.standard_normal((m, n)) for _ in range(4)]
+    Kmat = np.vstack([np.eye(m * n), np.kron(Cm, Cn), np.diag(w.ravel()), np.eye(m * n)])
+    rhs = np.concatenate([z.ravel() for z in zu])
+    l_ls = np.linalg.lstsq(Kmat, rhs, rcond=None)[0].reshape(m, n)
+    l = O.admm_l_step(zu[0], zu[1], zu[2], zu[3], w, lambda S: Cm.T @ S @ Cn)
+    assert np.allclose(l, l_ls, atol=1e-12), np.abs(l - l_ls).max()

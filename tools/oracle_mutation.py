@@ -50,9 +50,10 @@ MUTS = [
  ("transform line12", "    Y = B @ Tm.T @ H @ Tm\n", "    Y = B @ Tm @ H @ Tm.T\n"),
  ("eps schedule El", "    frac = 0.5e-4 if E > 0.3e-1 else (1.5e-4 if E > 6e-4 else 0.5e-3)", "    frac = 0.5e-4 if E > 0.3e-2 else (1.5e-4 if E > 6e-4 else 0.5e-3)"),
  ("synthetic D", "        D[b * p:(b + 1) * p, b * p:(b + 1) * p] -= 0.5", "        D[b * p:(b + 1) * p, b * p:(b + 1) * p] -= 0.25"),
- ("admm l update", "        l = ((z1 - u1) + psit(z2 - u2) + w * (z3 - u3) + (z4 - u4)) / (3.0 + w)", "        l = ((z1 - u1) + psit(z2 - u2) + w * (z3 - u3) + (z4 - u4)) / (4.0 + w)"),
- ("admm z2 threshold", "        z2 = np.sign(v2) * np.maximum(np.abs(v2) - eta / rho, 0.0)", "        z2 = np.sign(v2) * np.maximum(np.abs(v2) - eta * rho, 0.0)"),
- ("admm z4 clip", "        z4 = np.clip(l + u4, 0.0, 1.0)", "        z4 = np.clip(l + u4, 0.0, 2.0)"),
+ ("admm l update", "    return (zu1 + psit(zu2) + w * zu3 + zu4) / (3.0 + w)", "    return (zu1 + psit(zu2) + w * zu3 + zu4) / (4.0 + w)"),
+ ("admm l no inverse DCT", "    return (zu1 + psit(zu2) + w * zu3 + zu4) / (3.0 + w)", "    return (zu1 + zu2 + w * zu3 + zu4) / (3.0 + w)"),
+ ("admm z2 threshold", "    return np.sign(v) * np.maximum(np.abs(v) - eta / rho, 0.0)", "    return np.sign(v) * np.maximum(np.abs(v) - eta * rho, 0.0)"),
+ ("admm z4 clip", "    return np.clip(v, 0.0, 1.0)", "    return np.clip(v, 0.0, 2.0)"),
 ]
 
 
