@@ -1504,10 +1504,18 @@ cpa_svt_status cpa_svt_apply_host(cpa_svt_handle* h, cpa_svt_dtype dtype, cpa_sv
 // handle.  One host sync per iteration (the stopping test).
 cpa_svt_status cpa_svt_admm_recover(cpa_svt_handle* h, int64_t m, int64_t n, const double* D, const uint8_t* mask,
                                     int K, const cpa_svt_lambda* lam, cpa_svt_admm* opt, double* L) {
-  if (!h || !D || !mask || !L || !opt || !lam || m < 1 || n < 1 || K < 2 || K > CPA_SVT_KMAX) return CPA_SVT_E_ARG;
+  if (!h || !opt || !lam || m < 0 || n < 0 || K < 2 || K > CPA_SVT_KMAX) return CPA_SVT_E_ARG;
+  const bool empty = m == 0 || n == 0;   // an empty D: nothing to recover, no device work
+  if (!empty && (!D || !mask || !L)) return CPA_SVT_E_ARG;
   if (!(opt->rho > 0.0) || !(opt->eta >= 0.0) || !(opt->tol >= 0.0) || opt->max_iter < 1) return CPA_SVT_E_DOMAIN;
   cpa_svt_status st = check_lambda(lam);
   if (st != CPA_SVT_OK) return st;
+  if (empty) {
+    opt->iters = 0;
+    opt->last_rel = 0.0;
+    opt->ms_shrink = opt->ms_total = 0.0;
+    return CPA_SVT_OK;
+  }
   if (cudaSetDevice(h->device) != cudaSuccess) return CPA_SVT_E_CUDA;
   const int64_t N = m * n;
   auto r32 = [](size_t v) { return (v + 31) / 32 * 32; };

@@ -117,3 +117,13 @@ def test_sharded_empty_short_dimension_is_an_error(env):
     with pytest.raises(P.CpaSvtError) as e:
         hc.apply(X, KERN, 9, T=20, shard="cols", long_global=5)
     assert e.value.status == 1
+
+
+def test_admm_empty(env):
+    torch, P, D, h, hc = env
+    for shape in [(0, 6), (6, 0)]:
+        Dm = torch.empty(shape, dtype=torch.float64, device="cuda")
+        mask = torch.empty(shape, dtype=torch.uint8, device="cuda")
+        L, st = h.admm_recover(Dm, mask, K=8, rho=1.0, eta=0.01)
+        assert L.shape == shape and st["iters"] == 0
+
