@@ -704,3 +704,10 @@ def test_admm_steps_match_their_definitions():
     l_ls = np.linalg.lstsq(Kmat, rhs, rcond=None)[0].reshape(m, n)
     l = O.admm_l_step(zu[0], zu[1], zu[2], zu[3], w, lambda S: Cm.T @ S @ Cn)
     assert np.allclose(l, l_ls, atol=1e-12), np.abs(l - l_ls).max()
+
+
+def test_rel_fro_is_relative_to_the_reference():
+    """The parity metric (reading R16): ||A - B||_F / ||B||_F, B the oracle's output -- hand values."""
+    assert abs(O.rel_fro(np.array([[3.0, 4.0]]), np.array([[0.0, 5.0]])) - math.sqrt(10.0) / 5.0) < 1e-15
+    assert O.rel_fro(np.array([2.0]), np.array([1.0])) == 1.0
+    assert O.rel_fro(np.array([1.0]), np.array([0.0])) == 1.0     # zero reference: the absolute norm
