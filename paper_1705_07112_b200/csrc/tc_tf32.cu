@@ -24,6 +24,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <map>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -504,9 +505,15 @@ static cudaError_t launch_t(const CUtensorMap& ah, const CUtensorMap& al, const 
 
 // Lower-triangle tile list (tm >= tn) of a T x T tile grid in the grouped-M raster
 // order of tile_coords; built once per T and kept on the device.
+// (one list per device: handles on several devices, or in several host threads, share the cache
+// under a mutex)
 static const int2* sym_tile_list(int tiles_m, int tiles_n, int bm, int bn, int* count) {
-  static std::map<long long, std::pair<int2*, int>> cache;
-  const long long key = ((long long)tiles_m << 40) | ((long long)tiles_n << 16) | (bn << 1) | (bm == 128);
+  static std::map<std::pair<int, long long>, std::pair<int2*, int>> cache;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  const auto key = std::make_pair(dev, ((long long)tiles_m << 40) | ((long long)tiles_n << 16) | (bn << 1) | (bm == 128));
   auto it = cache.find(key);
   if (it != cache.end()) {
     *count = it->second.second;
