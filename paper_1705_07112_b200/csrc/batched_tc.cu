@@ -46,6 +46,9 @@ namespace btc {
 // FR = 4096 / NT fragment elements per thread.  More matrices in flight per SM beat a shorter
 // epilogue per matrix: c3 8.05 ms (128) against 8.62 ms (256).
 constexpr int OPB = 64 * 64 * 4;        // bytes of one 64 x 64 fp32 operand (two 8 KB k-blocks)
+#ifndef BTC_LATE_H
+#define BTC_LATE_H 1   // H += c_k Psi_k under the next step's MMA (0: in the epilogue, the round-2 order)
+#endif
 
 __device__ __forceinline__ uint32_t sw(int r, int k) {  // byte offset of (r, k) in a K-major SW128 operand
   return (uint32_t)((k >> 5) * 8192 + r * 128 + ((((k & 31) >> 2) ^ (r & 7)) << 4) + (k & 3) * 4);
@@ -530,23 +533,35 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : 4) k_batched_tc(Args a) {
     }
     sync_for_mma();
     // ---- lines 8-11: Psi_k = D0 + D1, H += c_k Psi_k; next A = Psi_k, next D0 = -2 Psi_k - Psi_{k-1}
+    // H += c_k Psi_k (this thread's fragment slots of H in shared memory)
+    auto h_update = [&](float ck, const float (&v)[FR]) {
+#pragma unroll
+      for (int c = 0; c < FR / 4; ++c) {
+        float4 h4 = sH4[c * NT + tid];
+        h4.x = fmaf(ck, v[4 * c], h4.x);
+        h4.y = fmaf(ck, v[4 * c + 1], h4.y);
+        h4.z = fmaf(ck, v[4 * c + 2], h4.z);
+        h4.w = fmaf(ck, v[4 * c + 3], h4.w);
+        sH4[c * NT + tid] = h4;
+      }
+    };
     for (int k = k_first; k < K; ++k) {
       if (tid == 0) btc::mma64_ts<true>(tD, tD1, tAh, tAl, sB, &bar);
+#if BTC_LATE_H
+      // H += c_{k-1} Psi_{k-1} (wp) while the tensor core computes Psi_k: the update is not an
+      // input of the MMA, so it leaves the epilogue's critical path (same sums, same order)
+      if (k > k_first) h_update(sC[k - 1], wp);
+#endif
       mbar_wait(&bar, phase);
       phase ^= 1;
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       float d[FR];
       ld_frag2(tD + lane_off, tD1 + lane_off, d);
-      const float ck = sC[k];
-#pragma unroll
-      for (int c = 0; c < FR / 4; ++c) {
-        float4 h4 = sH4[c * NT + tid];
-        h4.x = fmaf(ck, d[4 * c], h4.x);                       // H += c_k Psi_k
-        h4.y = fmaf(ck, d[4 * c + 1], h4.y);
-        h4.z = fmaf(ck, d[4 * c + 2], h4.z);
-        h4.w = fmaf(ck, d[4 * c + 3], h4.w);
-        sH4[c * NT + tid] = h4;
-      }
+#if BTC_LATE_H
+      if (k + 1 == K) h_update(sC[k], d);
+#else
+      h_update(sC[k], d);
+#endif
       if (k + 1 < K) {
         st_frag_hl(tAh + lane_off, tAl + lane_off, d);
 #pragma unroll
